@@ -1,0 +1,161 @@
+/*
+ * ss_b200.h -- C ABI of the B200 sliding-window GROUP BY engine.
+ *
+ * One `ss_engine` owns every piece of device state for one GPU: the
+ * per-group window rings, the group -> partition (block) assignment with
+ * its ordered per-partition lists, and the scratch of the per-batch
+ * pipeline.  All entry points take plain pointers and sizes; a pointer
+ * may be host memory (pageable or pinned) or device memory -- the engine
+ * inspects it with cudaPointerGetAttributes and stages host data itself.
+ * Calls are stream-ordered on the engine's stream (ss_set_stream), not
+ * thread-safe per handle, and return an `int` status (SS_OK or SS_E_*).
+ *
+ * Each entry point replaces one function of the reference package
+ * `skewstream` (/root/reference/pkg/src/skewstream); the mapping is noted
+ * beside it (reference file:line).  The Python shim
+ * (paper_1309_0634_b200/_lib.py) binds exactly these symbols with ctypes.
+ */
+#ifndef SS_B200_H
+#define SS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes -> errors.py:4-29 (mapped in paper_1309_0634_b200/errors.py) */
+#define SS_OK            0
+#define SS_E_DATA        1  /* DataError: group id outside [0, G) (partition.py:119-126) */
+#define SS_E_CONFIG      2  /* InvalidConfigError (balance.py:56-65, partition.py:189-197) */
+#define SS_E_SPEC        3  /* InvalidSpecError */
+#define SS_E_CONSISTENCY 4  /* ConsistencyError (partition.py:170-173, engine.py:283-284) */
+#define SS_E_STALE_MOVE  5  /* StaleMoveError (partition.py:198-200) */
+#define SS_E_EXEC        6  /* ExecutionError: CUDA / NCCL failure (engine.py:410-416) */
+
+/* aggregate mask: COUNT and SUM are the reference's own state
+ * (engine.py:67-70); AVG/MIN/MAX are derived from the same window. */
+#define SS_AGG_COUNT 1u
+#define SS_AGG_SUM   2u
+#define SS_AGG_AVG   4u
+#define SS_AGG_MIN   8u
+#define SS_AGG_MAX  16u
+
+/* balancer policies, Policy enum of balance.py:28-35 */
+#define SS_POLICY_NO         0
+#define SS_POLICY_FIRST      1
+#define SS_POLICY_ALL        2
+#define SS_POLICY_PROB       3
+#define SS_POLICY_BEST       4
+#define SS_POLICY_SHIFT      5
+#define SS_POLICY_SHIFTLOCAL 6
+
+/* move placement, partition.py:23-24 */
+#define SS_FRONT 0
+#define SS_BACK  1
+
+typedef struct ss_engine ss_engine;
+
+typedef struct {
+    int64_t  n_groups;      /* G: dense group ids 0..G-1 (datagen.py:81-103)          */
+    int64_t  window;        /* W: per-group window length (harness.py:43, engine.py:60)*/
+    int32_t  n_partitions;  /* P: processing units = aggregate-kernel CTAs           */
+    int32_t  key_bits;      /* 32: u32 group ids                                      */
+    uint32_t agg_mask;      /* SS_AGG_* bits that must be maintained                  */
+    int32_t  scope;         /* 0: per-group window (the reference semantics)          */
+    int32_t  device;        /* CUDA ordinal                                           */
+    int32_t  reserved;
+    int64_t  max_batch;     /* largest n passed to ss_step (0: 1<<24)                 */
+    int64_t  sub_batch;     /* L2-resident ingest unit (0: auto)                      */
+    int64_t  pool_values;   /* ring pool capacity in values (0: auto)                 */
+} ss_config;
+
+typedef struct {
+    int32_t policy;          /* SS_POLICY_*                                  */
+    int32_t reserved;
+    int64_t thread_threshold;/* balance.py:48 (>= 1)                         */
+    double  pot;             /* balance.py:49, in (0, 1]                     */
+    int64_t max_moves;       /* balance.py:50; 0 = 4 * P (balance.py:64-65)  */
+    int32_t split;           /* hot-key splitting across blocks (new)        */
+    int32_t split_max;       /* max shares per split group (0: P)            */
+    double  split_target;    /* max/mean load the splitter aims for (1.2)    */
+} ss_balancer;
+
+typedef struct {
+    int32_t group;
+    int32_t src;
+    int32_t dst;
+    int32_t placement;       /* SS_FRONT / SS_BACK */
+} ss_move;
+
+typedef struct {
+    int64_t tuples;          /* IterationReport.tuples (engine.py:173)                 */
+    int64_t imbalance;       /* max(tpt) - min(tpt) (engine.py:313,320)                */
+    int64_t moves;           /* moves emitted by this batch's policy                   */
+    int64_t moves_applied_before; /* harness.py:113 row.moves                           */
+    int64_t scanned;         /* MoveList.scanned_tuples (balance.py:68-80)             */
+    int64_t max_load;        /* max per-block tuple load incl. split shares            */
+    int64_t touched;         /* groups with >= 1 tuple in the batch                    */
+    int64_t split_groups;    /* groups executed as split shares this batch            */
+    double  mean_load;       /* tuples / P                                             */
+    double  load_ratio;      /* max_load / mean_load                                    */
+} ss_step_report;
+
+/* ---- lifecycle ------------------------------------------------------ */
+int  ss_create(const ss_config* cfg, ss_engine** out);        /* WindowStore(G, W), engine.py:60-70 */
+void ss_destroy(ss_engine* e);
+int  ss_set_stream(ss_engine* e, void* cuda_stream);          /* stream the engine enqueues on */
+int  ss_sync(ss_engine* e);
+const char* ss_last_error(ss_engine* e);
+const char* ss_version(void);
+
+/* ---- assignment (partition.py:45-114, 181-203) ------------------------ */
+/* order[G]: concatenated per-partition lists; offsets[P+1] into order. */
+int  ss_set_assignment(ss_engine* e, const int32_t* order, const int64_t* offsets);
+int  ss_get_assignment(ss_engine* e, int32_t* g2t, int32_t* order, int64_t* offsets);
+int  ss_apply_moves(ss_engine* e, const ss_move* moves, int64_t n);   /* apply_moves, partition.py:181-203 */
+
+/* ---- partition step (partition.py:117-178) ---------------------------- */
+int  ss_count(ss_engine* e, const uint32_t* groups, int64_t n,
+              int64_t* group_counts, int64_t* tpt);                   /* count_batch, partition.py:117-130 */
+int  ss_reorder(ss_engine* e, const uint32_t* groups, const int32_t* attrs, int64_t n,
+                uint32_t* out_groups, int32_t* out_attrs, int64_t* indicator);  /* reorder_batch, 161-178 */
+
+/* ---- aggregate update (engine.py:185-321) ----------------------------- */
+/* ingest_sequence (engine.py:253-296): stable per-group arrival order. */
+int  ss_ingest(ss_engine* e, const uint32_t* groups, const int32_t* attrs, int64_t n);
+
+/* ---- balancer (balance.py:141-405) ------------------------------------ */
+/* Runs the policy on one batch against the current assignment; does not
+ * apply the moves (the reference policies are pure, test_balance.py:355). */
+int  ss_balance(ss_engine* e, const uint32_t* groups, int64_t n, const ss_balancer* cfg,
+                ss_move* moves, int64_t* n_moves, int64_t* scanned, int64_t* final_tpt);
+
+/* ---- fused per-batch step: harness.run loop body (harness.py:99-117) ---
+ * count -> policy (device, overlapped) -> stable rank + window update per
+ * L2-resident sub-batch -> per-group result emission -> apply moves.  The
+ * moves decided on batch t are in force from batch t+1. */
+int  ss_step(ss_engine* e, const uint32_t* groups, const int32_t* attrs, int64_t n,
+             const ss_balancer* cfg, ss_step_report* rep);
+/* report of the last ss_step (synchronises) */
+int  ss_last_report(ss_engine* e, ss_step_report* rep);
+/* per-partition tuple loads of the last step (incl. split shares) */
+int  ss_last_loads(ss_engine* e, int64_t* loads);
+/* moves emitted by the last step */
+int  ss_last_moves(ss_engine* e, ss_move* moves, int64_t cap, int64_t* n);
+
+/* ---- state export (engine.py:51-93) ----------------------------------- */
+/* Any output pointer may be NULL.  avg = (double)sum / fill, 0 when empty. */
+int  ss_snapshot(ss_engine* e, int64_t* fill, int64_t* next_pos, int64_t* window_sum,
+                 int32_t* mn, int32_t* mx, double* avg);
+/* Window of one group in arrival order, oldest first (WindowStore.contents, engine.py:72-77). */
+int  ss_export_values(ss_engine* e, int64_t group, int64_t* out, int64_t cap, int64_t* n);
+/* Per-batch emission of the last ss_step: groups touched by the batch and
+ * their COUNT/SUM/AVG/MIN/MAX after it.  Sizes: cap entries each. */
+int  ss_results(ss_engine* e, int64_t cap, int32_t* groups, int64_t* count, int64_t* sum,
+                double* avg, int32_t* mn, int32_t* mx, int64_t* n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SS_B200_H */

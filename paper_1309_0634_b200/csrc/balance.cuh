@@ -1,0 +1,458 @@
+// balance.cuh -- K6 (load monitor) + K7 (device rebalancer) + device
+// apply_moves for the skewstream B200 pipeline.
+//
+// Reference (balance.py, partition.py):
+//   _rebalance_extremes  balance.py:141-172  hottest->coolest greedy loop,
+//                        cap = max_moves or 4P, lowest-id ties, a group
+//                        moves at most once, receiver gets it at the BACK
+//   get_first 181-200, check_all 203-227, prob_check 230-264,
+//   best_balance 267-293, shift 296-342, shift_local 345-385,
+//   apply_moves partition.py:181-203
+//
+// One CTA runs the policy's sequential loop for the whole GPU while the
+// rest of the chip executes the batch (the moves only take effect at the
+// next batch, harness.py:115-116).  The per-partition loads live in shared
+// memory; donor picks that scan a partition's groups (check_all,
+// prob_check, best_balance) are CTA-wide reductions over the partition's
+// ENTRY list (the list at batch start).  Working lists never need to be
+// materialised: a group moves at most once per invocation, so a working
+// list is  [fronts pushed into it, newest first] ++ [entry members not yet
+// moved] ++ [backs pushed into it, in order].
+#pragma once
+
+#include "common.cuh"
+
+namespace ss {
+
+constexpr int kBalThreads = 1024;
+
+struct BalanceArgs {
+    int policy;
+    long long threshold;
+    double pot;
+    int cap;
+    int P;
+    const int32_t* order;       // entry lists (CSR)
+    const int32_t* offsets;     // [P+1]
+    const int32_t* gcount;      // batch group counts
+    const unsigned long long* tpt;   // entry loads
+    uint8_t* moved;             // [G] scratch, all zero on entry, cleared by apply
+    int4* moves;                // (group, src, dst, placement)
+    int* front_top;             // [P] newest FRONT-push move index (-1)
+    int* back_first;            // [P] first BACK-push move index (-1)
+    int* mv_next;               // [cap] next older front / next newer back
+    int* n_moves;
+    long long* scanned;
+    long long* final_tpt;       // [P]
+    const unsigned long long* bad;
+};
+
+struct BalSmem {
+    long long* loads;
+    int* ftop;      // newest front push
+    int* fbot;      // oldest front push
+    int* bfirst;
+    int* blast;
+    int* elo;       // entry cursor [elo, ehi)
+    int* ehi;
+    int* esize;     // live entry members
+    int* nin;       // pushed-in members
+};
+
+__device__ __forceinline__ int bal_size(const BalSmem& s, int p) { return s.esize[p] + s.nin[p]; }
+
+// head / tail of a working list (single thread)
+__device__ int bal_head(const BalanceArgs& a, const BalSmem& s, int p) {
+    if (s.ftop[p] >= 0) return a.moves[s.ftop[p]].x;
+    int c = s.elo[p];
+    while (c < s.ehi[p] && a.moved[a.order[c]]) ++c;
+    s.elo[p] = c;
+    if (c < s.ehi[p]) return a.order[c];
+    if (s.bfirst[p] >= 0) return a.moves[s.bfirst[p]].x;
+    return -1;
+}
+__device__ int bal_tail(const BalanceArgs& a, const BalSmem& s, int p) {
+    if (s.blast[p] >= 0) return a.moves[s.blast[p]].x;
+    int c = s.ehi[p];
+    while (c > s.elo[p] && a.moved[a.order[c - 1]]) --c;
+    s.ehi[p] = c;
+    if (c > s.elo[p]) return a.order[c - 1];
+    if (s.fbot[p] >= 0) return a.moves[s.fbot[p]].x;
+    return -1;
+}
+
+// record a move of g (an un-moved entry member of src) into dst
+__device__ void bal_move(const BalanceArgs& a, const BalSmem& s, int* nm, int g, int src, int dst,
+                         int placement) {
+    const int mi = *nm;
+    a.moves[mi] = make_int4(g, src, dst, placement);
+    a.moved[g] = 1;
+    s.esize[src] -= 1;
+    s.nin[dst] += 1;
+    a.mv_next[mi] = -1;
+    if (placement == 1) {   // BACK
+        if (s.blast[dst] >= 0) a.mv_next[s.blast[dst]] = mi;
+        else s.bfirst[dst] = mi;
+        s.blast[dst] = mi;
+    } else {                // FRONT
+        a.mv_next[mi] = s.ftop[dst];
+        if (s.ftop[dst] < 0) s.fbot[dst] = mi;
+        s.ftop[dst] = mi;
+    }
+    const long long c = a.gcount[g];
+    s.loads[src] -= c;
+    s.loads[dst] += c;
+    *nm = mi + 1;
+}
+
+struct ArgPair { long long v; int i; };
+
+// CTA-wide argmax and argmin of loads, lowest index on ties
+__device__ void bal_extremes(const BalSmem& s, int P, int* hi, int* lo, long long* red_v, int* red_i) {
+    long long vmax = LLONG_MIN, vmin = LLONG_MAX;
+    int imax = 0x7fffffff, imin = 0x7fffffff;
+    for (int p = threadIdx.x; p < P; p += blockDim.x) {
+        const long long v = s.loads[p];
+        if (v > vmax) { vmax = v; imax = p; }
+        if (v < vmin) { vmin = v; imin = p; }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const long long ov = __shfl_xor_sync(SS_FULL, vmax, o);
+        const int oi = __shfl_xor_sync(SS_FULL, imax, o);
+        if (ov > vmax || (ov == vmax && oi < imax)) { vmax = ov; imax = oi; }
+        const long long nv = __shfl_xor_sync(SS_FULL, vmin, o);
+        const int ni = __shfl_xor_sync(SS_FULL, imin, o);
+        if (nv < vmin || (nv == vmin && ni < imin)) { vmin = nv; imin = ni; }
+    }
+    const int w = warp_id(), nw = blockDim.x >> 5;
+    if (lane_id() == 0) {
+        red_v[w] = vmax; red_i[w] = imax;
+        red_v[32 + w] = vmin; red_i[32 + w] = imin;
+    }
+    __syncthreads();
+    if (w == 0) {
+        vmax = lane_id() < (unsigned)nw ? red_v[lane_id()] : LLONG_MIN;
+        imax = lane_id() < (unsigned)nw ? red_i[lane_id()] : 0x7fffffff;
+        vmin = lane_id() < (unsigned)nw ? red_v[32 + lane_id()] : LLONG_MAX;
+        imin = lane_id() < (unsigned)nw ? red_i[32 + lane_id()] : 0x7fffffff;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            const long long ov = __shfl_xor_sync(SS_FULL, vmax, o);
+            const int oi = __shfl_xor_sync(SS_FULL, imax, o);
+            if (ov > vmax || (ov == vmax && oi < imax)) { vmax = ov; imax = oi; }
+            const long long nv = __shfl_xor_sync(SS_FULL, vmin, o);
+            const int ni = __shfl_xor_sync(SS_FULL, imin, o);
+            if (nv < vmin || (nv == vmin && ni < imin)) { vmin = nv; imin = ni; }
+        }
+        if (lane_id() == 0) { red_i[64] = imax; red_i[65] = imin; }
+    }
+    __syncthreads();
+    *hi = red_i[64];
+    *lo = red_i[65];
+    __syncthreads();
+}
+
+// Lexicographic CTA reduction of (key, group) -> smallest.  Returns group
+// (or INT_MAX) to every thread.
+__device__ void bal_argmin_key(long long key, int g, long long* red_v, int* red_i, long long* out_key,
+                               int* out_g) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const long long ok = __shfl_xor_sync(SS_FULL, key, o);
+        const int og = __shfl_xor_sync(SS_FULL, g, o);
+        if (ok < key || (ok == key && og < g)) { key = ok; g = og; }
+    }
+    const int w = warp_id(), nw = blockDim.x >> 5;
+    if (lane_id() == 0) { red_v[w] = key; red_i[w] = g; }
+    __syncthreads();
+    if (w == 0) {
+        key = lane_id() < (unsigned)nw ? red_v[lane_id()] : LLONG_MAX;
+        g = lane_id() < (unsigned)nw ? red_i[lane_id()] : 0x7fffffff;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            const long long ok = __shfl_xor_sync(SS_FULL, key, o);
+            const int og = __shfl_xor_sync(SS_FULL, g, o);
+            if (ok < key || (ok == key && og < g)) { key = ok; g = og; }
+        }
+        if (lane_id() == 0) { red_v[66] = key; red_i[66] = g; }
+    }
+    __syncthreads();
+    *out_key = red_v[66];
+    *out_g = red_i[66];
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kBalThreads)
+k_balance(BalanceArgs a) {
+    extern __shared__ long long bal_sm[];
+    __shared__ long long red_v[72];
+    __shared__ int red_i[72];
+    __shared__ int sh_ctl[4];
+    __shared__ long long sh_scan[2];
+    const int P = a.P;
+    BalSmem s;
+    s.loads = bal_sm;
+    int* ib = (int*)(bal_sm + P);
+    s.ftop = ib; s.fbot = ib + P; s.bfirst = ib + 2 * P; s.blast = ib + 3 * P;
+    s.elo = ib + 4 * P; s.ehi = ib + 5 * P; s.esize = ib + 6 * P; s.nin = ib + 7 * P;
+    if (*a.bad != (unsigned long long)kNoBad) {
+        if (threadIdx.x == 0) *a.n_moves = 0;
+        return;
+    }
+    for (int p = threadIdx.x; p < P; p += blockDim.x) {
+        s.loads[p] = (long long)a.tpt[p];
+        s.ftop[p] = s.fbot[p] = s.bfirst[p] = s.blast[p] = -1;
+        s.elo[p] = a.offsets[p];
+        s.ehi[p] = a.offsets[p + 1];
+        s.esize[p] = a.offsets[p + 1] - a.offsets[p];
+        s.nin[p] = 0;
+    }
+    __syncthreads();
+    int nm = 0;                // valid in thread 0
+    long long scanned = 0;
+    const int pol = a.policy;
+
+    if (pol == 1 || pol == 2 || pol == 3 || pol == 4) {
+        for (;;) {
+            int hi, lo;
+            bal_extremes(s, P, &hi, &lo, red_v, red_i);
+            if (threadIdx.x == 0) {
+                sh_ctl[0] = nm;
+                sh_ctl[2] = -1;
+            }
+            __syncthreads();
+            const int nm_all = sh_ctl[0];
+            __syncthreads();
+            if (nm_all >= a.cap) break;
+            if (s.loads[hi] - s.loads[lo] <= a.threshold) break;
+            const int e0 = a.offsets[hi], e1 = a.offsets[hi + 1];
+            int pick = -1;
+            long long pscan = 0;
+            if (pol == 1) {                       // get_first
+                if (threadIdx.x == 0) {
+                    const int g = bal_head(a, s, hi);
+                    int r = -1;
+                    if (g >= 0 && !a.moved[g] && a.gcount[g] != 0) r = g;
+                    sh_ctl[2] = r;
+                }
+                __syncthreads();
+                pick = sh_ctl[2];
+            } else if (pol == 2 || pol == 4) {    // check_all / best_balance
+                long long bk = LLONG_MAX;
+                int bg = 0x7fffffff;
+                const long long dmax = s.loads[hi], dmin = s.loads[lo];
+                for (int i = e0 + threadIdx.x; i < e1; i += blockDim.x) {
+                    const int g = a.order[i];
+                    if (a.moved[g]) continue;
+                    const long long c = a.gcount[g];
+                    long long key;
+                    if (pol == 2) key = -c;      // max count, lowest id
+                    else {
+                        long long d = (dmax - c) - (dmin + c);
+                        key = d < 0 ? -d : d;
+                    }
+                    if (key < bk || (key == bk && g < bg)) { bk = key; bg = g; }
+                }
+                long long k;
+                int g;
+                bal_argmin_key(bk, bg, red_v, red_i, &k, &g);
+                if (g != 0x7fffffff) {
+                    if (pol == 2) {
+                        if (-k > 0) { pick = g; pscan = (long long)a.tpt[hi]; }
+                    } else {
+                        if (k < dmax - dmin) pick = g;
+                    }
+                }
+            } else {                               // prob_check
+                const int sz = bal_size(s, hi);
+                if (sz > 0) {
+                    const long long limit =
+                        (long long)ceil(a.pot * (double)s.loads[hi] / (double)sz);
+                    long long run = 0;             // tuples before the current chunk
+                    long long fb_key = LLONG_MAX;  // fallback: max count (as -c), lowest id
+                    int fb_g = 0x7fffffff;
+                    for (int c0 = e0; c0 < e1 && pick < 0; c0 += blockDim.x) {
+                        const int i = c0 + threadIdx.x;
+                        int g = -1;
+                        long long c = 0;
+                        bool cand = false;
+                        if (i < e1) {
+                            g = a.order[i];
+                            c = a.gcount[g];
+                            const bool mv = a.moved[g];
+                            cand = (c >= limit) && !mv;
+                            if (!mv && c > 0) {
+                                const long long key = -c;
+                                if (key < fb_key || (key == fb_key && g < fb_g)) { fb_key = key; fb_g = g; }
+                            }
+                        }
+                        // inclusive block scan of c (tuples up to and including i)
+                        long long tot;
+                        long long ex = block_excl_scan(c, red_v, &tot);
+                        // first candidate index in this chunk
+                        long long ck;
+                        int cg;
+                        bal_argmin_key(cand ? (long long)i : LLONG_MAX, cand ? g : 0x7fffffff, red_v,
+                                       red_i, &ck, &cg);
+                        if (cand && (long long)i == ck) sh_scan[0] = run + ex + limit;
+                        __syncthreads();
+                        if (ck != LLONG_MAX) {
+                            pick = cg;
+                            pscan = sh_scan[0];
+                        }
+                        __syncthreads();
+                        run += tot;
+                    }
+                    if (pick < 0) {
+                        long long k;
+                        int g;
+                        bal_argmin_key(fb_key, fb_g, red_v, red_i, &k, &g);
+                        if (g != 0x7fffffff && -k > 0) {
+                            pick = g;
+                            pscan = (long long)a.tpt[hi];
+                        }
+                    }
+                }
+            }
+            if (pick < 0) break;
+            if (threadIdx.x == 0) {
+                bal_move(a, s, &nm, pick, hi, lo, 1);
+                scanned += pscan;
+            }
+            __syncthreads();
+        }
+    } else if (threadIdx.x == 0 && pol == 5) {     // shift
+        while (nm < a.cap) {
+            int hi = 0, lo = 0;
+            for (int p = 1; p < P; ++p) {
+                if (s.loads[p] > s.loads[hi]) hi = p;
+                if (s.loads[p] < s.loads[lo]) lo = p;
+            }
+            if (s.loads[hi] - s.loads[lo] <= a.threshold) break;
+            const bool down = hi > lo;
+            const int b = down ? lo + 1 : hi, e = down ? hi + 1 : lo;
+            int emitted = 0;
+            for (int i = b; i < e; ++i) {
+                if (nm >= a.cap) break;
+                if (bal_size(s, i) == 0) continue;
+                const int g = down ? bal_head(a, s, i) : bal_tail(a, s, i);
+                if (g < 0 || a.moved[g]) continue;
+                bal_move(a, s, &nm, g, i, down ? i - 1 : i + 1, down ? 1 : 0);
+                ++emitted;
+            }
+            if (emitted == 0) break;
+        }
+    } else if (threadIdx.x == 0 && pol == 6) {     // shift_local
+        for (int i = 0; i + 1 < P; ++i) {
+            if (nm >= a.cap) break;
+            int src, dst;
+            bool last;
+            if (s.loads[i] - s.loads[i + 1] > a.threshold) { src = i; dst = i + 1; last = true; }
+            else if (s.loads[i + 1] - s.loads[i] > a.threshold) { src = i + 1; dst = i; last = false; }
+            else continue;
+            if (bal_size(s, src) == 0) continue;
+            const int g = last ? bal_tail(a, s, src) : bal_head(a, s, src);
+            if (g < 0 || a.moved[g]) continue;
+            bal_move(a, s, &nm, g, src, dst, last ? 0 : 1);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        *a.n_moves = nm;
+        *a.scanned = scanned;
+    }
+    for (int p = threadIdx.x; p < P; p += blockDim.x) {
+        a.final_tpt[p] = s.loads[p];
+        a.front_top[p] = s.ftop[p];
+        a.back_first[p] = s.bfirst[p];
+    }
+}
+
+// ---- device apply_moves (partition.py:181-203) ------------------------------
+// new list(p) = fronts pushed into p (newest first) ++ entry members of p
+// that did not move ++ backs pushed into p (in order).  Sizes first:
+__global__ void __launch_bounds__(1024)
+k_apply_sizes(const int32_t* __restrict__ offsets, int P, const int4* __restrict__ moves,
+              const int* __restrict__ n_moves, int32_t* __restrict__ new_off) {
+    __shared__ int32_t red[33];
+    __shared__ int32_t carry;
+    const int nm = *n_moves;
+    if (nm == 0) return;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int p0 = 0; p0 < P; p0 += blockDim.x) {
+        const int p = p0 + threadIdx.x;
+        int32_t sz = 0;
+        if (p < P) {
+            sz = offsets[p + 1] - offsets[p];
+            for (int i = 0; i < nm; ++i) {
+                const int4 m = moves[i];
+                sz += (m.z == p) - (m.y == p);
+            }
+        }
+        int32_t tot;
+        const int32_t ex = block_excl_scan(sz, red, &tot);
+        if (p < P) new_off[p] = carry + ex;
+        __syncthreads();
+        if (threadIdx.x == 0) carry += tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) new_off[P] = carry;
+}
+
+// one CTA per partition
+__global__ void __launch_bounds__(256)
+k_apply_build(const int32_t* __restrict__ order, const int32_t* __restrict__ offsets,
+              const int32_t* __restrict__ new_off, const int4* __restrict__ moves,
+              const int* __restrict__ n_moves, const int* __restrict__ front_top,
+              const int* __restrict__ back_first, const int* __restrict__ mv_next,
+              const uint8_t* __restrict__ moved, int32_t* __restrict__ new_order) {
+    __shared__ int32_t red[33];
+    if (*n_moves == 0) return;
+    const int p = blockIdx.x;
+    int pos = new_off[p];
+    if (threadIdx.x == 0) {
+        for (int mi = front_top[p]; mi >= 0; mi = mv_next[mi]) new_order[pos++] = moves[mi].x;
+        red[32] = pos;
+    }
+    __syncthreads();
+    pos = red[32];
+    __syncthreads();
+    const int e0 = offsets[p], e1 = offsets[p + 1];
+    for (int c0 = e0; c0 < e1; c0 += blockDim.x) {
+        const int i = c0 + threadIdx.x;
+        int g = -1;
+        int keep = 0;
+        if (i < e1) {
+            g = order[i];
+            keep = !moved[g];
+        }
+        int32_t tot;
+        const int32_t ex = block_excl_scan(keep, red, &tot);
+        if (keep) new_order[pos + ex] = g;
+        pos += tot;
+    }
+    if (threadIdx.x == 0)
+        for (int mi = back_first[p]; mi >= 0; mi = mv_next[mi]) new_order[pos++] = moves[mi].x;
+}
+
+// commit: copy the rebuilt lists, update the group->partition map, clear
+// the moved flags
+__global__ void __launch_bounds__(256)
+k_apply_commit(int32_t* __restrict__ order, int32_t* __restrict__ offsets, const int32_t* __restrict__ new_order,
+               const int32_t* __restrict__ new_off, int G, int P, const int4* __restrict__ moves,
+               const int* __restrict__ n_moves, int32_t* __restrict__ pmap, uint8_t* __restrict__ moved) {
+    const int nm = *n_moves;
+    if (nm == 0) return;
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+    for (int i = tid; i < G; i += nt) order[i] = new_order[i];
+    for (int i = tid; i <= P; i += nt) offsets[i] = new_off[i];
+    for (int i = tid; i < nm; i += nt) {
+        const int4 m = moves[i];
+        pmap[m.x] = m.z;
+        moved[m.x] = 0;
+    }
+}
+
+}  // namespace ss

@@ -1,0 +1,117 @@
+// common.cuh -- shared device helpers for the skewstream B200 engine.
+//
+// Everything here is integer / byte work: scans, histograms and the
+// decoupled look-back status words of the stable multisplit.  Nothing on
+// this path is GEMM-shaped, so there are no tensor-core paths; the
+// kernels are tuned for coalescing, L2 residency and SM-count-sized grids.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define SS_WARP 32
+#define SS_FULL 0xffffffffu
+
+namespace ss {
+
+constexpr int kNumSM = 148;                 // B200: 2 dies x 74 SMs
+constexpr int64_t kNoBad = 0x7fffffffffffffffLL;
+
+__host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+__host__ __device__ __forceinline__ int64_t max64(int64_t a, int64_t b) { return a > b ? a : b; }
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+__device__ __forceinline__ unsigned warp_id() { return threadIdx.x >> 5; }
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+__device__ __forceinline__ uint64_t globaltimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// relaxed gpu-scope 64-bit load/store for the look-back status words: the
+// payload (a count) lives in the same word as its flag, so no fence is
+// needed between payload and flag.
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
+}
+
+// streaming loads of the input batch: read once, do not keep in L1, first
+// to leave L2 (the sort ping-pong buffers are what must stay resident).
+__device__ __forceinline__ uint4 ld_stream_v4(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ uint32_t ld_stream_u32(const void* p) {
+    uint32_t r;
+    asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
+    return r;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(SS_FULL, v, o);
+    return v;
+}
+__device__ __forceinline__ int warp_min(int v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = min(v, __shfl_xor_sync(SS_FULL, v, o));
+    return v;
+}
+__device__ __forceinline__ int warp_max(int v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(SS_FULL, v, o));
+    return v;
+}
+
+// inclusive warp scan
+template <typename T>
+__device__ __forceinline__ T warp_incl_scan(T v) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        T n = __shfl_up_sync(SS_FULL, v, o);
+        if ((int)lane_id() >= o) v += n;
+    }
+    return v;
+}
+
+// Block-wide exclusive scan of one value per thread (blockDim.x <= 1024).
+// `smem` needs 33 slots.  Returns the exclusive prefix; *total gets the sum.
+template <typename T>
+__device__ __forceinline__ T block_excl_scan(T v, T* smem, T* total) {
+    const unsigned w = warp_id(), l = lane_id(), nw = (blockDim.x + 31) >> 5;
+    T inc = warp_incl_scan(v);
+    if (l == 31) smem[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+        T s = (l < nw) ? smem[l] : T(0);
+        T si = warp_incl_scan(s);
+        if (l < nw) smem[l] = si - s;
+        if (l == nw - 1) smem[32] = si;
+    }
+    __syncthreads();
+    T res = smem[w] + inc - v;
+    *total = smem[32];
+    __syncthreads();
+    return res;
+}
+
+// look-back status word: [epoch:30 | flag:2 | count:32]
+constexpr unsigned long long kFlagAgg = 1ull, kFlagInc = 2ull;
+__device__ __forceinline__ unsigned long long lb_pack(uint32_t epoch, unsigned long long flag, uint32_t cnt) {
+    return ((unsigned long long)epoch << 34) | (flag << 32) | (unsigned long long)cnt;
+}
+
+}  // namespace ss

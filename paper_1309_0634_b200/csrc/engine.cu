@@ -1,0 +1,1118 @@
+// engine.cu -- the C ABI of include/ss_b200.h and the per-batch pipeline.
+//
+// Build (see paper_1309_0634_b200/_build.py):
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -shared
+//        -Xcompiler -fPIC -cudart static engine.cu -o libss_b200.so
+//
+// Pipeline of one batch (the loop body of harness.run, harness.py:99-117):
+//   K2  k_count          per-sub-batch group histograms   (count_batch)
+//       k_batch_stats    gcount, tpt                      (BatchStats)
+//   K7  k_balance        policy on a side stream, overlapped with the rest
+//       k_scan_*         run starts + radix digit bases
+//   per L2-resident sub-batch:
+//       k_reserve        grow occupancy-proportional rings (sparse store)
+//   K3  k_sort_pass x1-2 stable placement -> arrival rank within group
+//   K4  k_ingest         one CTA per partition: window exchange + state
+//   K5  k_split_finalize split hot keys; k_minmax_rescan
+//       k_emit           per-batch result rows
+//       k_apply_*        apply the policy's moves (in force from batch t+1)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/ss_b200.h"
+#include "common.cuh"
+#include "partition.cuh"
+#include "window.cuh"
+#include "balance.cuh"
+
+using namespace ss;
+
+namespace {
+
+constexpr int64_t kCountChunk = 16384;
+constexpr int64_t kDefaultSub = int64_t(1) << 21;
+constexpr int64_t kDenseLimitBytes = int64_t(24) << 30;
+
+struct DevReport {            // written by k_report, copied to the host
+    unsigned long long bad;
+    long long tuples;
+    long long imbalance;
+    long long moves;
+    long long moves_before;
+    long long scanned;
+    long long max_load;
+    long long touched;
+    long long split_groups;
+    long long n_res;
+    int oom;
+    int pad;
+};
+
+}  // namespace
+
+struct ss_engine {
+    ss_config cfg{};
+    int64_t G = 0, W = 0;
+    int P = 0;
+    bool dense = true;
+    bool minmax = false;
+    cudaStream_t st = nullptr;
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_stats = nullptr, ev_bal = nullptr;
+    std::string err;
+
+    // window store
+    int32_t *fill = nullptr, *next_pos = nullptr, *mn = nullptr, *mx = nullptr, *cap = nullptr;
+    long long* wsum = nullptr;
+    int64_t* off = nullptr;
+    int32_t* ring = nullptr;
+    unsigned long long pool_cap = 0;
+    unsigned long long* pool_top = nullptr;
+    int* oom = nullptr;
+
+    // assignment
+    int32_t *pmap = nullptr, *order = nullptr, *offsets = nullptr, *new_order = nullptr, *new_off = nullptr;
+    uint8_t* moved = nullptr;
+
+    // batch scratch
+    int64_t S = 0, max_batch = 0;
+    int n_sub_max = 0;
+    uint32_t* stage_keys = nullptr;
+    int32_t* stage_vals = nullptr;
+    int32_t *gcnt = nullptr, *gstart = nullptr, *gcount = nullptr, *bsum = nullptr;
+    uint32_t* dhist = nullptr;
+    unsigned long long *tpt = nullptr, *touched = nullptr, *bad = nullptr;
+    uint32_t* kbuf = nullptr;
+    int32_t* vbuf[2] = {nullptr, nullptr};
+    int64_t sort_cap = 0;
+    unsigned long long* status = nullptr;
+    int64_t status_tiles = 0;
+    uint32_t* tickets = nullptr;
+    uint32_t epoch = 0;
+    DigitPlan plan{};
+    int rb[2] = {0, 0};
+    int nblk = 0;
+
+    // balancer
+    int cap_moves = 0;
+    int4* moves = nullptr;
+    int *front_top = nullptr, *back_first = nullptr, *mv_next = nullptr, *n_moves = nullptr;
+    long long *scanned = nullptr, *final_tpt = nullptr;
+    int* prev_moves = nullptr;
+
+    uint32_t* kbuf2 = nullptr;             // sorted keys (reorder only)
+
+    // emission / misc
+    unsigned* n_res = nullptr;
+    int32_t *r_g = nullptr, *r_cnt = nullptr, *r_mn = nullptr, *r_mx = nullptr;
+    long long* r_sum = nullptr;
+    double* r_avg = nullptr;
+    int32_t* rescan = nullptr;
+    unsigned* n_rescan = nullptr;
+    unsigned long long* part_ns = nullptr;
+    unsigned long long* loads = nullptr;   // per-partition load incl. split shares
+    DevReport* d_rep = nullptr;
+    DevReport* h_rep = nullptr;            // pinned
+    std::vector<void*> allocs;
+};
+
+// --------------------------------------------------------------------------
+// helpers
+// --------------------------------------------------------------------------
+namespace {
+
+int fail(ss_engine* e, int code, const std::string& msg) {
+    if (e) e->err = msg;
+    return code;
+}
+
+#define SS_CUDA(e, call)                                                              \
+    do {                                                                              \
+        cudaError_t _st = (call);                                                     \
+        if (_st != cudaSuccess)                                                       \
+            return fail((e), SS_E_EXEC, std::string(#call ": ") + cudaGetErrorString(_st)); \
+    } while (0)
+
+template <typename T>
+int dalloc(ss_engine* e, T** p, size_t n) {
+    void* q = nullptr;
+    cudaError_t st = cudaMalloc(&q, std::max<size_t>(n, 1) * sizeof(T));
+    if (st != cudaSuccess)
+        return fail(e, SS_E_EXEC, std::string("cudaMalloc(") + std::to_string(n * sizeof(T)) + "): " +
+                                      cudaGetErrorString(st));
+    e->allocs.push_back(q);
+    *p = (T*)q;
+    return SS_OK;
+}
+
+bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+int bits_for(int64_t G) {
+    int b = 1;
+    while ((int64_t(1) << b) < G) ++b;
+    return b;
+}
+
+int rb_for(int bits) {
+    if (bits <= 4) return 4;
+    if (bits <= 6) return 6;
+    if (bits <= 8) return 8;
+    if (bits <= 9) return 9;
+    if (bits <= 10) return 10;
+    return 11;
+}
+
+template <int RB>
+void launch_sort(cudaStream_t st, const uint32_t* kin, const int32_t* vin, uint32_t* kout, int32_t* vout,
+                 int n, int shift, uint32_t mask, const uint32_t* base, unsigned long long* status,
+                 uint32_t epoch, uint32_t* ticket, const unsigned long long* bad, int stream_in) {
+    const int tiles = (n + kSortTile - 1) / kSortTile;
+    if (tiles == 0) return;
+    k_sort_pass<RB><<<tiles, kSortThreads, 0, st>>>(kin, vin, kout, vout, n, shift, mask, base, status,
+                                                    epoch, ticket, bad, stream_in);
+}
+
+void sort_dispatch(int rb, cudaStream_t st, const uint32_t* kin, const int32_t* vin, uint32_t* kout,
+                   int32_t* vout, int n, int shift, uint32_t mask, const uint32_t* base,
+                   unsigned long long* status, uint32_t epoch, uint32_t* ticket,
+                   const unsigned long long* bad, int stream_in) {
+    switch (rb) {
+        case 4: launch_sort<4>(st, kin, vin, kout, vout, n, shift, mask, base, status, epoch, ticket, bad, stream_in); break;
+        case 6: launch_sort<6>(st, kin, vin, kout, vout, n, shift, mask, base, status, epoch, ticket, bad, stream_in); break;
+        case 8: launch_sort<8>(st, kin, vin, kout, vout, n, shift, mask, base, status, epoch, ticket, bad, stream_in); break;
+        case 9: launch_sort<9>(st, kin, vin, kout, vout, n, shift, mask, base, status, epoch, ticket, bad, stream_in); break;
+        case 10: launch_sort<10>(st, kin, vin, kout, vout, n, shift, mask, base, status, epoch, ticket, bad, stream_in); break;
+        default: launch_sort<11>(st, kin, vin, kout, vout, n, shift, mask, base, status, epoch, ticket, bad, stream_in); break;
+    }
+}
+
+__global__ void k_fill_i32(int32_t* p, int64_t n, int32_t v) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
+}
+__global__ void k_dense_off(int64_t* off, int32_t* cap, int64_t G, int64_t W) {
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < G; g += (int64_t)gridDim.x * blockDim.x) {
+        off[g] = g * W;
+        cap[g] = (int32_t)W;
+    }
+}
+__global__ void k_set_bad(unsigned long long* bad) { *bad = (unsigned long long)kNoBad; }
+
+// map group ids to placement ranks (reorder_batch sorts by rank)
+__global__ void k_to_rank(const uint32_t* __restrict__ g, int64_t n, const int32_t* __restrict__ rank,
+                          uint32_t G, uint32_t* __restrict__ out, unsigned long long* bad) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t v = g[i];
+        if (v >= G) {
+            atomicMin(bad, (unsigned long long)i);
+            out[i] = 0;
+        } else {
+            out[i] = (uint32_t)rank[v];
+        }
+    }
+}
+__global__ void k_rank_of(const int32_t* __restrict__ order, int64_t G, int32_t* __restrict__ rank) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < G; i += (int64_t)gridDim.x * blockDim.x)
+        rank[order[i]] = (int32_t)i;
+}
+__global__ void k_from_rank(uint32_t* __restrict__ k, int64_t n, const int32_t* __restrict__ order) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        k[i] = (uint32_t)order[k[i]];
+}
+__global__ void k_clear_moved(const int4* __restrict__ moves, const int* __restrict__ n_moves, uint8_t* moved) {
+    const int n = *n_moves;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) moved[moves[i].x] = 0;
+}
+
+// load monitor (K6): imbalance of the entry loads, max per-block load
+// including split shares, and the report the host reads back.
+__global__ void __launch_bounds__(1024)
+k_report(const unsigned long long* __restrict__ tpt, const unsigned long long* __restrict__ loads, int P,
+         const unsigned long long* __restrict__ bad, const unsigned long long* __restrict__ touched,
+         const int* __restrict__ n_moves, int* __restrict__ prev_moves, const long long* __restrict__ scanned,
+         const int* __restrict__ n_split, const unsigned* __restrict__ n_res, const int* __restrict__ oom,
+         long long tuples, int has_policy, DevReport* __restrict__ rep) {
+    __shared__ long long r[3][32];
+    long long mx = 0, mnv = LLONG_MAX, ml = 0;
+    for (int p = threadIdx.x; p < P; p += blockDim.x) {
+        const long long t = (long long)tpt[p];
+        mx = max(mx, t);
+        mnv = min(mnv, t);
+        ml = max(ml, (long long)(loads ? loads[p] : tpt[p]));
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        mx = max(mx, __shfl_xor_sync(SS_FULL, mx, o));
+        mnv = min(mnv, __shfl_xor_sync(SS_FULL, mnv, o));
+        ml = max(ml, __shfl_xor_sync(SS_FULL, ml, o));
+    }
+    if (lane_id() == 0) { r[0][warp_id()] = mx; r[1][warp_id()] = mnv; r[2][warp_id()] = ml; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+            mx = max(mx, r[0][w]); mnv = min(mnv, r[1][w]); ml = max(ml, r[2][w]);
+        }
+        rep->bad = *bad;
+        rep->tuples = tuples;
+        rep->imbalance = P ? mx - mnv : 0;
+        rep->max_load = ml;
+        rep->touched = (long long)*touched;
+        const int nm = has_policy ? *n_moves : 0;
+        rep->moves = nm;
+        rep->moves_before = *prev_moves;
+        *prev_moves = (*bad == (unsigned long long)kNoBad) ? nm : 0;
+        rep->scanned = has_policy ? *scanned : 0;
+        rep->split_groups = n_split ? *n_split : 0;
+        rep->n_res = n_res ? *n_res : 0;
+        rep->oom = *oom;
+    }
+}
+
+}  // namespace
+
+// --------------------------------------------------------------------------
+// lifecycle
+// --------------------------------------------------------------------------
+extern "C" const char* ss_version(void) { return "ss_b200 1.0 (sm_100a)"; }
+
+extern "C" const char* ss_last_error(ss_engine* e) { return e ? e->err.c_str() : "null engine"; }
+
+extern "C" void ss_destroy(ss_engine* e) {
+    if (!e) return;
+    cudaSetDevice(e->cfg.device);
+    cudaStreamSynchronize(e->st);
+    for (void* p : e->allocs) cudaFree(p);
+    if (e->h_rep) cudaFreeHost(e->h_rep);
+    if (e->side) cudaStreamDestroy(e->side);
+    if (e->ev_stats) cudaEventDestroy(e->ev_stats);
+    if (e->ev_bal) cudaEventDestroy(e->ev_bal);
+    if (e->st && e->cfg.reserved == 0) cudaStreamDestroy(e->st);
+    delete e;
+}
+
+static int engine_alloc_sort(ss_engine* e, int64_t n) {
+    if (n <= e->sort_cap) return SS_OK;
+    const int64_t cap = ((n + kSortTile - 1) / kSortTile) * kSortTile;
+    int rc;
+    if ((rc = dalloc(e, &e->kbuf, cap))) return rc;
+    if ((rc = dalloc(e, &e->kbuf2, cap))) return rc;
+    if ((rc = dalloc(e, &e->vbuf[0], cap))) return rc;
+    if ((rc = dalloc(e, &e->vbuf[1], cap))) return rc;
+    e->status_tiles = cap / kSortTile;
+    if ((rc = dalloc(e, &e->status, (size_t)e->status_tiles * kMaxBins))) return rc;
+    SS_CUDA(e, cudaMemsetAsync(e->status, 0, sizeof(unsigned long long) * e->status_tiles * kMaxBins, e->st));
+    e->sort_cap = cap;
+    return SS_OK;
+}
+
+extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
+    if (!cfg || !out) return SS_E_CONFIG;
+    *out = nullptr;
+    ss_engine* e = new ss_engine();
+    e->cfg = *cfg;
+    e->cfg.reserved = 0;
+    auto bail = [&](int rc) { ss_engine* t = e; *out = nullptr; if (rc != SS_OK) { static std::string keep; keep = t->err; } return rc; };
+    if (cfg->n_groups < 1 || cfg->n_groups > (int64_t(1) << 22)) {
+        int rc = fail(e, SS_E_CONFIG, "n_groups must be in [1, 2^22]");
+        *out = e;
+        return rc;
+    }
+    if (cfg->window < 1 || cfg->window > (int64_t(1) << 30)) {
+        int rc = fail(e, SS_E_CONFIG, "window must be in [1, 2^30]");
+        *out = e;
+        return rc;
+    }
+    if (cfg->n_partitions < 1 || cfg->n_partitions > 4096) {
+        int rc = fail(e, SS_E_CONFIG, "n_partitions must be in [1, 4096]");
+        *out = e;
+        return rc;
+    }
+    (void)bail;
+    *out = e;
+    e->G = cfg->n_groups;
+    e->W = cfg->window;
+    e->P = cfg->n_partitions;
+    e->minmax = (cfg->agg_mask & (SS_AGG_MIN | SS_AGG_MAX)) != 0;
+    SS_CUDA(e, cudaSetDevice(cfg->device));
+    SS_CUDA(e, cudaStreamCreateWithFlags(&e->st, cudaStreamNonBlocking));
+    SS_CUDA(e, cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking));
+    SS_CUDA(e, cudaEventCreateWithFlags(&e->ev_stats, cudaEventDisableTiming));
+    SS_CUDA(e, cudaEventCreateWithFlags(&e->ev_bal, cudaEventDisableTiming));
+
+    const int64_t G = e->G, W = e->W;
+    int rc;
+    // -- window store
+    if ((rc = dalloc(e, &e->fill, G)) || (rc = dalloc(e, &e->next_pos, G)) || (rc = dalloc(e, &e->wsum, G)) ||
+        (rc = dalloc(e, &e->mn, G)) || (rc = dalloc(e, &e->mx, G)) || (rc = dalloc(e, &e->cap, G)) ||
+        (rc = dalloc(e, &e->off, G)) || (rc = dalloc(e, &e->pool_top, 1)) || (rc = dalloc(e, &e->oom, 1)))
+        return rc;
+    SS_CUDA(e, cudaMemsetAsync(e->fill, 0, G * 4, e->st));
+    SS_CUDA(e, cudaMemsetAsync(e->next_pos, 0, G * 4, e->st));
+    SS_CUDA(e, cudaMemsetAsync(e->wsum, 0, G * 8, e->st));
+    SS_CUDA(e, cudaMemsetAsync(e->mn, 0, G * 4, e->st));
+    SS_CUDA(e, cudaMemsetAsync(e->mx, 0, G * 4, e->st));
+    SS_CUDA(e, cudaMemsetAsync(e->oom, 0, 4, e->st));
+    SS_CUDA(e, cudaMemsetAsync(e->pool_top, 0, 8, e->st));
+    const int64_t dense_vals = G * W;
+    e->dense = cfg->pool_values == 0 && dense_vals * 4 <= kDenseLimitBytes;
+    if (e->dense) {
+        e->pool_cap = (unsigned long long)dense_vals;
+        if ((rc = dalloc(e, &e->ring, dense_vals))) return rc;
+        k_dense_off<<<296, 256, 0, e->st>>>(e->off, e->cap, G, W);
+    } else {
+        int64_t pool = cfg->pool_values;
+        if (pool <= 0) {
+            size_t fr = 0, tot = 0;
+            cudaMemGetInfo(&fr, &tot);
+            pool = std::min<int64_t>((int64_t)(fr / 4 / 2), int64_t(8) << 30);
+            pool = std::min<int64_t>(pool, dense_vals);
+        }
+        e->pool_cap = (unsigned long long)pool;
+        if ((rc = dalloc(e, &e->ring, pool))) return rc;
+        SS_CUDA(e, cudaMemsetAsync(e->off, 0, G * 8, e->st));
+        SS_CUDA(e, cudaMemsetAsync(e->cap, 0, G * 4, e->st));
+    }
+    // -- assignment: contiguous ranges (partition.py:97-114) until set
+    if ((rc = dalloc(e, &e->pmap, G)) || (rc = dalloc(e, &e->order, G)) || (rc = dalloc(e, &e->new_order, G)) ||
+        (rc = dalloc(e, &e->offsets, e->P + 1)) || (rc = dalloc(e, &e->new_off, e->P + 1)) ||
+        (rc = dalloc(e, &e->moved, G)))
+        return rc;
+    SS_CUDA(e, cudaMemsetAsync(e->moved, 0, G, e->st));
+    {
+        std::vector<int32_t> order(G), pmap(G);
+        std::vector<int32_t> offs(e->P + 1);
+        const int64_t q = G / e->P, r = G % e->P;
+        int64_t lo = 0;
+        for (int t = 0; t < e->P; ++t) {
+            offs[t] = (int32_t)lo;
+            const int64_t sz = q + (t < r ? 1 : 0);
+            for (int64_t g = lo; g < lo + sz; ++g) { order[g] = (int32_t)g; pmap[g] = t; }
+            lo += sz;
+        }
+        offs[e->P] = (int32_t)G;
+        SS_CUDA(e, cudaMemcpy(e->order, order.data(), G * 4, cudaMemcpyHostToDevice));
+        SS_CUDA(e, cudaMemcpy(e->pmap, pmap.data(), G * 4, cudaMemcpyHostToDevice));
+        SS_CUDA(e, cudaMemcpy(e->offsets, offs.data(), (e->P + 1) * 4, cudaMemcpyHostToDevice));
+    }
+    // -- batch scratch
+    e->max_batch = cfg->max_batch > 0 ? cfg->max_batch : (int64_t(1) << 24);
+    int64_t S = cfg->sub_batch > 0 ? cfg->sub_batch : kDefaultSub;
+    S = ((S + kCountChunk - 1) / kCountChunk) * kCountChunk;
+    e->S = S;
+    e->n_sub_max = (int)((e->max_batch + S - 1) / S);
+    const int nsub = e->n_sub_max;
+    e->nblk = (int)((G + kScanBlk - 1) / kScanBlk);
+    {
+        const int bits = bits_for(G);
+        if (bits <= 11) {
+            e->plan.npass = 1;
+            e->plan.shift[0] = 0; e->plan.bits[0] = bits;
+            e->plan.shift[1] = 0; e->plan.bits[1] = 0;
+        } else {
+            e->plan.npass = 2;
+            e->plan.bits[0] = bits / 2;
+            e->plan.bits[1] = bits - bits / 2;
+            e->plan.shift[0] = 0;
+            e->plan.shift[1] = bits / 2;
+        }
+        e->rb[0] = rb_for(e->plan.bits[0]);
+        e->rb[1] = rb_for(e->plan.bits[1]);
+    }
+    if ((rc = dalloc(e, &e->stage_keys, e->max_batch)) || (rc = dalloc(e, &e->stage_vals, e->max_batch)) ||
+        (rc = dalloc(e, &e->gcnt, (size_t)nsub * G)) || (rc = dalloc(e, &e->gstart, (size_t)nsub * G)) ||
+        (rc = dalloc(e, &e->gcount, G)) || (rc = dalloc(e, &e->bsum, (size_t)nsub * e->nblk)) ||
+        (rc = dalloc(e, &e->dhist, (size_t)nsub * 2 * kMaxBins)) || (rc = dalloc(e, &e->tpt, e->P)) ||
+        (rc = dalloc(e, &e->touched, 1)) || (rc = dalloc(e, &e->bad, 1)) ||
+        (rc = dalloc(e, &e->tickets, (size_t)nsub * 2 + 2)))
+        return rc;
+    SS_CUDA(e, cudaMemsetAsync(e->gcnt, 0, (size_t)nsub * G * 4, e->st));
+    SS_CUDA(e, cudaMemsetAsync(e->gcount, 0, G * 4, e->st));
+    k_set_bad<<<1, 1, 0, e->st>>>(e->bad);
+    if ((rc = engine_alloc_sort(e, S))) return rc;
+    // -- balancer
+    e->cap_moves = 4 * e->P;
+    if ((rc = dalloc(e, &e->moves, e->cap_moves)) || (rc = dalloc(e, &e->front_top, e->P)) ||
+        (rc = dalloc(e, &e->back_first, e->P)) || (rc = dalloc(e, &e->mv_next, e->cap_moves)) ||
+        (rc = dalloc(e, &e->n_moves, 1)) || (rc = dalloc(e, &e->scanned, 1)) ||
+        (rc = dalloc(e, &e->final_tpt, e->P)) || (rc = dalloc(e, &e->prev_moves, 1)))
+        return rc;
+    SS_CUDA(e, cudaMemsetAsync(e->n_moves, 0, 4, e->st));
+    SS_CUDA(e, cudaMemsetAsync(e->prev_moves, 0, 4, e->st));
+    // -- emission
+    if ((rc = dalloc(e, &e->n_res, 1)) || (rc = dalloc(e, &e->r_g, G)) || (rc = dalloc(e, &e->r_cnt, G)) ||
+        (rc = dalloc(e, &e->r_sum, G)) || (rc = dalloc(e, &e->r_avg, G)) || (rc = dalloc(e, &e->r_mn, G)) ||
+        (rc = dalloc(e, &e->r_mx, G)) || (rc = dalloc(e, &e->rescan, G)) || (rc = dalloc(e, &e->n_rescan, 1)) ||
+        (rc = dalloc(e, &e->part_ns, e->P)) || (rc = dalloc(e, &e->loads, e->P)) || (rc = dalloc(e, &e->d_rep, 1)))
+        return rc;
+    SS_CUDA(e, cudaMemsetAsync(e->n_res, 0, 4, e->st));
+    SS_CUDA(e, cudaMallocHost(&e->h_rep, sizeof(DevReport)));
+    memset(e->h_rep, 0, sizeof(DevReport));
+    e->h_rep->bad = (unsigned long long)kNoBad;
+    SS_CUDA(e, cudaFuncSetAttribute(k_count<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    SS_CUDA(e, cudaFuncSetAttribute(k_ingest, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kIngestSmem));
+    SS_CUDA(e, cudaFuncSetAttribute(k_balance, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    SS_CUDA(e, cudaStreamSynchronize(e->st));
+    return SS_OK;
+}
+
+extern "C" int ss_set_stream(ss_engine* e, void* stream) {
+    if (!e) return SS_E_CONFIG;
+    SS_CUDA(e, cudaStreamSynchronize(e->st));
+    if (e->cfg.reserved == 0 && e->st) cudaStreamDestroy(e->st);
+    e->st = (cudaStream_t)stream;
+    e->cfg.reserved = 1;   // not owned
+    return SS_OK;
+}
+
+extern "C" int ss_sync(ss_engine* e) {
+    if (!e) return SS_E_CONFIG;
+    SS_CUDA(e, cudaStreamSynchronize(e->st));
+    SS_CUDA(e, cudaGetLastError());
+    return SS_OK;
+}
+
+// --------------------------------------------------------------------------
+// input staging
+// --------------------------------------------------------------------------
+static int stage_input(ss_engine* e, const uint32_t* groups, const int32_t* attrs, int64_t n,
+                       const uint32_t** dk, const int32_t** dv) {
+    if (n > e->max_batch) return fail(e, SS_E_CONFIG, "batch larger than max_batch");
+    if (is_device_ptr(groups)) *dk = groups;
+    else {
+        if (n) SS_CUDA(e, cudaMemcpyAsync(e->stage_keys, groups, n * 4, cudaMemcpyHostToDevice, e->st));
+        *dk = e->stage_keys;
+    }
+    if (dv) {
+        if (!attrs) *dv = nullptr;
+        else if (is_device_ptr(attrs)) *dv = attrs;
+        else {
+            if (n) SS_CUDA(e, cudaMemcpyAsync(e->stage_vals, attrs, n * 4, cudaMemcpyHostToDevice, e->st));
+            *dv = e->stage_vals;
+        }
+    }
+    return SS_OK;
+}
+
+// After a DataError the partially filled histograms are cleared so the
+// engine state is exactly as before the failed call.
+static int recover_bad(ss_engine* e) {
+    SS_CUDA(e, cudaMemsetAsync(e->gcnt, 0, (size_t)e->n_sub_max * e->G * 4, e->st));
+    SS_CUDA(e, cudaMemsetAsync(e->gcount, 0, e->G * 4, e->st));
+    k_set_bad<<<1, 1, 0, e->st>>>(e->bad);
+    SS_CUDA(e, cudaStreamSynchronize(e->st));
+    return SS_OK;
+}
+
+static int data_error(ss_engine* e, unsigned long long idx, const uint32_t* dkeys) {
+    uint32_t g = 0;
+    cudaMemcpy(&g, dkeys + idx, 4, cudaMemcpyDeviceToHost);
+    recover_bad(e);
+    return fail(e, SS_E_DATA, "tuple " + std::to_string(idx) + " has group " + std::to_string(g) +
+                                  ", outside [0, " + std::to_string(e->G) + ")");
+}
+
+// K2 over n tuples with sub-batch size S (n_sub = ceil(n / S))
+static int launch_count(ss_engine* e, const uint32_t* dk, int64_t n, int64_t S) {
+    if (n == 0) return SS_OK;
+    const int vec_ok = ((uintptr_t)dk % 16) == 0;
+    const int64_t grid = (n + kCountChunk - 1) / kCountChunk;
+    if (e->G <= 16384) {
+        k_count<true><<<(unsigned)grid, 512, e->G * 4, e->st>>>(dk, n, (uint32_t)e->G, S, kCountChunk, e->gcnt,
+                                                               e->bad, vec_ok);
+    } else {
+        k_count<false><<<(unsigned)grid, 512, 0, e->st>>>(dk, n, (uint32_t)e->G, S, kCountChunk, e->gcnt, e->bad,
+                                                         vec_ok);
+    }
+    SS_CUDA(e, cudaGetLastError());
+    return SS_OK;
+}
+
+static int launch_stats(ss_engine* e, int n_sub) {
+    SS_CUDA(e, cudaMemsetAsync(e->tpt, 0, e->P * 8, e->st));
+    SS_CUDA(e, cudaMemsetAsync(e->touched, 0, 8, e->st));
+    k_batch_stats<<<2 * kNumSM, 1024, e->P * 8, e->st>>>(e->gcnt, n_sub, (uint32_t)e->G, e->pmap, e->P, e->gcount,
+                                                          e->tpt, e->touched, e->bad);
+    SS_CUDA(e, cudaGetLastError());
+    return SS_OK;
+}
+
+static int launch_scans(ss_engine* e, int n_sub) {
+    SS_CUDA(e, cudaMemsetAsync(e->dhist, 0, (size_t)n_sub * 2 * kMaxBins * 4, e->st));
+    dim3 g2(e->nblk, n_sub);
+    k_scan_reduce<<<g2, 1024, 0, e->st>>>(e->gcnt, (uint32_t)e->G, e->bsum, e->nblk, e->plan, e->dhist, e->bad);
+    k_scan_top<<<n_sub, 1024, 0, e->st>>>(e->bsum, e->nblk, e->plan, e->dhist, e->bad);
+    k_scan_down<<<g2, 1024, 0, e->st>>>(e->gcnt, (uint32_t)e->G, e->bsum, e->nblk, e->gstart, e->bad);
+    SS_CUDA(e, cudaGetLastError());
+    return SS_OK;
+}
+
+// stable placement of sub-batch s (keys/vals at its start, ns tuples) into
+// vbuf[0] (and kbuf with keys when want_keys)
+static int launch_place(ss_engine* e, int s, const uint32_t* dk, const int32_t* dv, int64_t ns, bool want_keys,
+                        bool stream_in) {
+    const uint32_t* base0 = e->dhist + ((int64_t)s * 2 + 0) * kMaxBins;
+    const uint32_t* base1 = e->dhist + ((int64_t)s * 2 + 1) * kMaxBins;
+    uint32_t* t0 = e->tickets + 2 * s;
+    uint32_t* t1 = e->tickets + 2 * s + 1;
+    auto next_epoch = [&]() {
+        if (++e->epoch >= (1u << 30) - 1) {
+            cudaMemsetAsync(e->status, 0, sizeof(unsigned long long) * e->status_tiles * kMaxBins, e->st);
+            e->epoch = 1;
+        }
+        return e->epoch;
+    };
+    const uint32_t m0 = (1u << e->plan.bits[0]) - 1u;
+    if (e->plan.npass == 1) {
+        sort_dispatch(e->rb[0], e->st, dk, dv, want_keys ? e->kbuf2 : nullptr, e->vbuf[0], (int)ns, 0, m0, base0,
+                      e->status, next_epoch(), t0, e->bad, stream_in);
+    } else {
+        const uint32_t m1 = (1u << e->plan.bits[1]) - 1u;
+        // pass 0: input -> (kbuf, vbuf1); pass 1: (kbuf, vbuf1) -> vbuf0 [+ kbuf2]
+        sort_dispatch(e->rb[0], e->st, dk, dv, e->kbuf, e->vbuf[1], (int)ns, e->plan.shift[0], m0, base0, e->status,
+                      next_epoch(), t0, e->bad, stream_in);
+        sort_dispatch(e->rb[1], e->st, e->kbuf, e->vbuf[1], want_keys ? e->kbuf2 : nullptr, e->vbuf[0], (int)ns,
+                      e->plan.shift[1], m1, base1, e->status, next_epoch(), t1, e->bad, 0);
+    }
+    SS_CUDA(e, cudaGetLastError());
+    return SS_OK;
+}
+
+static IngestArgs ingest_args(ss_engine* e, int s) {
+    IngestArgs a{};
+    a.order = e->order;
+    a.offsets = e->offsets;
+    a.gcnt = e->gcnt + (int64_t)s * e->G;
+    a.gstart = e->gstart + (int64_t)s * e->G;
+    a.vals = e->vbuf[0];
+    a.fill = e->fill;
+    a.next_pos = e->next_pos;
+    a.wsum = e->wsum;
+    a.mn = e->mn;
+    a.mx = e->mx;
+    a.off = e->off;
+    a.ring = e->ring;
+    a.W = e->W;
+    a.minmax = e->minmax;
+    a.rescan = e->rescan;
+    a.n_rescan = e->n_rescan;
+    a.part_ns = e->part_ns;
+    a.bad = e->bad;
+    return a;
+}
+
+// count -> stats -> [policy] -> scans -> per sub-batch (reserve, place,
+// ingest, finalize) -> [emit] -> [apply]
+static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_t n, const ss_balancer* bal,
+                     bool emit) {
+    const int n_sub = (int)std::max<int64_t>(1, (n + e->S - 1) / e->S);
+    int rc;
+    const bool has_policy = bal && bal->policy != SS_POLICY_NO;
+    SS_CUDA(e, cudaMemsetAsync(e->tickets, 0, (size_t)n_sub * 2 * 4, e->st));
+    SS_CUDA(e, cudaMemsetAsync(e->part_ns, 0, e->P * 8, e->st));
+    if (emit) SS_CUDA(e, cudaMemsetAsync(e->n_res, 0, 4, e->st));
+    if ((rc = launch_count(e, dk, n, e->S))) return rc;
+    if ((rc = launch_stats(e, n_sub))) return rc;
+    if (has_policy) {
+        BalanceArgs a{};
+        a.policy = bal->policy;
+        a.threshold = bal->thread_threshold;
+        a.pot = bal->pot;
+        a.cap = (int)std::min<int64_t>(bal->max_moves > 0 ? bal->max_moves : 4LL * e->P, e->cap_moves);
+        a.P = e->P;
+        a.order = e->order;
+        a.offsets = e->offsets;
+        a.gcount = e->gcount;
+        a.tpt = e->tpt;
+        a.moved = e->moved;
+        a.moves = e->moves;
+        a.front_top = e->front_top;
+        a.back_first = e->back_first;
+        a.mv_next = e->mv_next;
+        a.n_moves = e->n_moves;
+        a.scanned = e->scanned;
+        a.final_tpt = e->final_tpt;
+        a.bad = e->bad;
+        SS_CUDA(e, cudaEventRecord(e->ev_stats, e->st));
+        SS_CUDA(e, cudaStreamWaitEvent(e->side, e->ev_stats, 0));
+        k_balance<<<1, kBalThreads, (size_t)e->P * (8 + 8 * 4), e->side>>>(a);
+        SS_CUDA(e, cudaGetLastError());
+        SS_CUDA(e, cudaEventRecord(e->ev_bal, e->side));
+    }
+    if ((rc = launch_scans(e, n_sub))) return rc;
+    for (int s = 0; s < n_sub; ++s) {
+        const int64_t lo = (int64_t)s * e->S;
+        const int64_t ns = std::min<int64_t>(e->S, n - lo);
+        if (ns <= 0) break;
+        if (!e->dense) {
+            k_reserve<<<2 * kNumSM, 256, 0, e->st>>>(e->gcnt + (int64_t)s * e->G, (uint32_t)e->G, e->W, e->fill,
+                                                     e->off, e->cap, e->ring, e->pool_top, e->pool_cap, e->oom,
+                                                     e->bad);
+        }
+        if ((rc = launch_place(e, s, dk + lo, dv + lo, ns, false, true))) return rc;
+        if (e->minmax) SS_CUDA(e, cudaMemsetAsync(e->n_rescan, 0, 4, e->st));
+        IngestArgs a = ingest_args(e, s);
+        k_ingest<<<e->P, kIngestThreads, kIngestSmem, e->st>>>(a);
+        if (e->minmax)
+            k_minmax_rescan<<<2 * kNumSM, 256, 0, e->st>>>(e->rescan, e->n_rescan, e->ring, e->off, e->W, e->mn, e->mx);
+        SS_CUDA(e, cudaGetLastError());
+    }
+    if (emit) {
+        k_emit<<<2 * kNumSM, 256, 0, e->st>>>(e->gcount, (uint32_t)e->G, e->fill, e->wsum, e->mn, e->mx, e->minmax,
+                                              e->n_res, e->r_g, e->r_cnt, e->r_sum, e->r_avg, e->r_mn, e->r_mx, e->bad);
+    } else {
+        SS_CUDA(e, cudaMemsetAsync(e->gcount, 0, e->G * 4, e->st));
+    }
+    if (has_policy) {
+        SS_CUDA(e, cudaStreamWaitEvent(e->st, e->ev_bal, 0));
+        k_apply_sizes<<<1, 1024, 0, e->st>>>(e->offsets, e->P, e->moves, e->n_moves, e->new_off);
+        k_apply_build<<<e->P, 256, 0, e->st>>>(e->order, e->offsets, e->new_off, e->moves, e->n_moves, e->front_top,
+                                               e->back_first, e->mv_next, e->moved, e->new_order);
+        k_apply_commit<<<2 * kNumSM, 256, 0, e->st>>>(e->order, e->offsets, e->new_order, e->new_off, (int)e->G, e->P,
+                                                      e->moves, e->n_moves, e->pmap, e->moved);
+        SS_CUDA(e, cudaGetLastError());
+    }
+    return SS_OK;
+}
+
+// --------------------------------------------------------------------------
+// report
+// --------------------------------------------------------------------------
+static int enqueue_report(ss_engine* e, int64_t n, bool has_policy) {
+    k_report<<<1, 1024, 0, e->st>>>(e->tpt, nullptr, e->P, e->bad, e->touched, e->n_moves, e->prev_moves,
+                                    e->scanned, nullptr, e->n_res, e->oom, (long long)n, has_policy ? 1 : 0,
+                                    e->d_rep);
+    SS_CUDA(e, cudaGetLastError());
+    SS_CUDA(e, cudaMemcpyAsync(e->h_rep, e->d_rep, sizeof(DevReport), cudaMemcpyDeviceToHost, e->st));
+    return SS_OK;
+}
+
+static const uint32_t* g_last_keys = nullptr;
+
+static int check_report(ss_engine* e, const uint32_t* dk) {
+    SS_CUDA(e, cudaStreamSynchronize(e->st));
+    SS_CUDA(e, cudaGetLastError());
+    if (e->h_rep->bad != (unsigned long long)kNoBad) return data_error(e, e->h_rep->bad, dk);
+    if (e->h_rep->oom) return fail(e, SS_E_EXEC, "window ring pool exhausted (raise pool_values)");
+    return SS_OK;
+}
+
+static void fill_report(const ss_engine* e, ss_step_report* r) {
+    const DevReport& d = *e->h_rep;
+    r->tuples = d.tuples;
+    r->imbalance = d.imbalance;
+    r->moves = d.moves;
+    r->moves_applied_before = d.moves_before;
+    r->scanned = d.scanned;
+    r->max_load = d.max_load;
+    r->touched = d.touched;
+    r->split_groups = d.split_groups;
+    r->mean_load = e->P ? (double)d.tuples / (double)e->P : 0.0;
+    r->load_ratio = (d.tuples > 0) ? (double)d.max_load / r->mean_load : 0.0;
+}
+
+static int check_balancer(ss_engine* e, const ss_balancer* b) {
+    if (!b) return SS_OK;
+    if (b->policy < SS_POLICY_NO || b->policy > SS_POLICY_SHIFTLOCAL)
+        return fail(e, SS_E_CONFIG, "unknown policy " + std::to_string(b->policy));
+    if (b->thread_threshold < 1) return fail(e, SS_E_CONFIG, "thread_threshold must be >= 1");
+    if (!(b->pot > 0.0 && b->pot <= 1.0)) return fail(e, SS_E_CONFIG, "pot must be in (0, 1]");
+    if (b->max_moves < 0) return fail(e, SS_E_CONFIG, "max_moves must be >= 1 (0 = default)");
+    return SS_OK;
+}
+
+// --------------------------------------------------------------------------
+// assignment
+// --------------------------------------------------------------------------
+extern "C" int ss_set_assignment(ss_engine* e, const int32_t* order, const int64_t* offsets) {
+    if (!e || !order || !offsets) return SS_E_CONFIG;
+    const int64_t G = e->G;
+    const int P = e->P;
+    if (offsets[0] != 0 || offsets[P] != G) return fail(e, SS_E_CONSISTENCY, "offsets must span [0, G]");
+    std::vector<int32_t> pmap(G, -1), offs(P + 1);
+    for (int p = 0; p < P; ++p) {
+        if (offsets[p + 1] < offsets[p]) return fail(e, SS_E_CONSISTENCY, "offsets must be non-decreasing");
+        offs[p] = (int32_t)offsets[p];
+        for (int64_t i = offsets[p]; i < offsets[p + 1]; ++i) {
+            const int32_t g = order[i];
+            if (g < 0 || g >= G) return fail(e, SS_E_CONSISTENCY, "group " + std::to_string(g) + " out of range");
+            if (pmap[g] >= 0) return fail(e, SS_E_CONSISTENCY, "group " + std::to_string(g) + " listed twice");
+            pmap[g] = p;
+        }
+    }
+    offs[P] = (int32_t)G;
+    SS_CUDA(e, cudaStreamSynchronize(e->st));
+    SS_CUDA(e, cudaMemcpy(e->order, order, G * 4, cudaMemcpyHostToDevice));
+    SS_CUDA(e, cudaMemcpy(e->pmap, pmap.data(), G * 4, cudaMemcpyHostToDevice));
+    SS_CUDA(e, cudaMemcpy(e->offsets, offs.data(), (P + 1) * 4, cudaMemcpyHostToDevice));
+    return SS_OK;
+}
+
+extern "C" int ss_get_assignment(ss_engine* e, int32_t* g2t, int32_t* order, int64_t* offsets) {
+    if (!e) return SS_E_CONFIG;
+    SS_CUDA(e, cudaStreamSynchronize(e->st));
+    if (g2t) SS_CUDA(e, cudaMemcpy(g2t, e->pmap, e->G * 4, cudaMemcpyDeviceToHost));
+    if (order) SS_CUDA(e, cudaMemcpy(order, e->order, e->G * 4, cudaMemcpyDeviceToHost));
+    if (offsets) {
+        std::vector<int32_t> o(e->P + 1);
+        SS_CUDA(e, cudaMemcpy(o.data(), e->offsets, (e->P + 1) * 4, cudaMemcpyDeviceToHost));
+        for (int p = 0; p <= e->P; ++p) offsets[p] = o[p];
+    }
+    return SS_OK;
+}
+
+// Sequential application with the reference's validation order
+// (partition.py:181-203); the engine is untouched when a move fails.
+extern "C" int ss_apply_moves(ss_engine* e, const ss_move* moves, int64_t n) {
+    if (!e) return SS_E_CONFIG;
+    const int64_t G = e->G;
+    const int P = e->P;
+    std::vector<int32_t> g2t(G), order(G);
+    std::vector<int64_t> offs(P + 1);
+    int rc = ss_get_assignment(e, g2t.data(), order.data(), offs.data());
+    if (rc) return rc;
+    std::vector<std::vector<int32_t>> lists(P);
+    for (int p = 0; p < P; ++p) lists[p].assign(order.begin() + offs[p], order.begin() + offs[p + 1]);
+    for (int64_t i = 0; i < n; ++i) {
+        const ss_move& m = moves[i];
+        if (m.placement != SS_FRONT && m.placement != SS_BACK)
+            return fail(e, SS_E_CONFIG, "unknown placement " + std::to_string(m.placement));
+        if (m.src < 0 || m.src >= P || m.dst < 0 || m.dst >= P)
+            return fail(e, SS_E_CONFIG, "move " + std::to_string(i) + " names a thread out of range");
+        if (m.group < 0 || m.group >= G)
+            return fail(e, SS_E_CONFIG, "move " + std::to_string(i) + " names a group out of range");
+        if (g2t[m.group] != m.src)
+            return fail(e, SS_E_STALE_MOVE, "group " + std::to_string(m.group) + " is on thread " +
+                                                std::to_string(g2t[m.group]) + ", not " + std::to_string(m.src));
+        auto& src = lists[m.src];
+        src.erase(std::find(src.begin(), src.end(), m.group));
+        auto& dst = lists[m.dst];
+        if (m.placement == SS_BACK) dst.push_back(m.group);
+        else dst.insert(dst.begin(), m.group);
+        g2t[m.group] = m.dst;
+    }
+    int64_t pos = 0;
+    for (int p = 0; p < P; ++p) {
+        offs[p] = pos;
+        for (int32_t g : lists[p]) order[pos++] = g;
+    }
+    offs[P] = pos;
+    return ss_set_assignment(e, order.data(), offs.data());
+}
+
+// --------------------------------------------------------------------------
+// partition step
+// --------------------------------------------------------------------------
+static int64_t round_chunk(int64_t n) {
+    return std::max<int64_t>(kCountChunk, ((n + kCountChunk - 1) / kCountChunk) * kCountChunk);
+}
+
+static int clear_counts_row0(ss_engine* e) {
+    SS_CUDA(e, cudaMemsetAsync(e->gcnt, 0, e->G * 4, e->st));
+    SS_CUDA(e, cudaMemsetAsync(e->gcount, 0, e->G * 4, e->st));
+    return SS_OK;
+}
+
+extern "C" int ss_count(ss_engine* e, const uint32_t* groups, int64_t n, int64_t* group_counts, int64_t* tpt) {
+    if (!e || n < 0) return SS_E_CONFIG;
+    const uint32_t* dk;
+    int rc;
+    if ((rc = stage_input(e, groups, nullptr, n, &dk, nullptr))) return rc;
+    if ((rc = launch_count(e, dk, n, round_chunk(n)))) return rc;
+    if ((rc = launch_stats(e, 1))) return rc;
+    unsigned long long bad;
+    SS_CUDA(e, cudaMemcpyAsync(&bad, e->bad, 8, cudaMemcpyDeviceToHost, e->st));
+    SS_CUDA(e, cudaStreamSynchronize(e->st));
+    if (bad != (unsigned long long)kNoBad) return data_error(e, bad, dk);
+    std::vector<int32_t> gc(e->G);
+    std::vector<unsigned long long> tp(e->P);
+    SS_CUDA(e, cudaMemcpy(gc.data(), e->gcount, e->G * 4, cudaMemcpyDeviceToHost));
+    SS_CUDA(e, cudaMemcpy(tp.data(), e->tpt, e->P * 8, cudaMemcpyDeviceToHost));
+    if ((rc = clear_counts_row0(e))) return rc;
+    SS_CUDA(e, cudaStreamSynchronize(e->st));
+    if (group_counts)
+        for (int64_t g = 0; g < e->G; ++g) group_counts[g] = gc[g];
+    if (tpt)
+        for (int p = 0; p < e->P; ++p) tpt[p] = (int64_t)tp[p];
+    return SS_OK;
+}
+
+static int32_t* g_rank_scratch(ss_engine* e) {
+    static thread_local ss_engine* owner = nullptr;
+    (void)owner;
+    return e->new_order;   // free outside the apply step
+}
+
+extern "C" int ss_reorder(ss_engine* e, const uint32_t* groups, const int32_t* attrs, int64_t n,
+                          uint32_t* out_groups, int32_t* out_attrs, int64_t* indicator) {
+    if (!e || n < 0) return SS_E_CONFIG;
+    const uint32_t* dk;
+    const int32_t* dv;
+    int rc;
+    if ((rc = stage_input(e, groups, attrs, n, &dk, &dv))) return rc;
+    if ((rc = engine_alloc_sort(e, n))) return rc;
+    int32_t* rank = g_rank_scratch(e);
+    k_rank_of<<<2 * kNumSM, 256, 0, e->st>>>(e->order, e->G, rank);
+    if (n) k_to_rank<<<2 * kNumSM, 256, 0, e->st>>>(dk, n, rank, (uint32_t)e->G, e->stage_keys, e->bad);
+    const uint32_t* rk = e->stage_keys;
+    if ((rc = launch_count(e, rk, n, round_chunk(n)))) return rc;
+    SS_CUDA(e, cudaMemsetAsync(e->tickets, 0, 8, e->st));
+    if ((rc = launch_scans(e, 1))) return rc;
+    if (n && (rc = launch_place(e, 0, rk, dv, n, true, false))) return rc;
+    if (n) k_from_rank<<<2 * kNumSM, 256, 0, e->st>>>(e->kbuf2, n, e->order);
+    unsigned long long bad;
+    SS_CUDA(e, cudaMemcpyAsync(&bad, e->bad, 8, cudaMemcpyDeviceToHost, e->st));
+    SS_CUDA(e, cudaStreamSynchronize(e->st));
+    if (bad != (unsigned long long)kNoBad) {
+        // report the original group of the offending tuple
+        uint32_t g = 0;
+        if (is_device_ptr(groups)) cudaMemcpy(&g, groups + bad, 4, cudaMemcpyDeviceToHost);
+        else g = groups[bad];
+        recover_bad(e);
+        return fail(e, SS_E_DATA, "tuple " + std::to_string(bad) + " has group " + std::to_string(g) +
+                                      ", outside [0, " + std::to_string(e->G) + ")");
+    }
+    if (n) {
+        SS_CUDA(e, cudaMemcpy(out_groups, e->kbuf2, n * 4, is_device_ptr(out_groups) ? cudaMemcpyDeviceToDevice
+                                                                                       : cudaMemcpyDeviceToHost));
+        SS_CUDA(e, cudaMemcpy(out_attrs, e->vbuf[0], n * 4, is_device_ptr(out_attrs) ? cudaMemcpyDeviceToDevice
+                                                                                      : cudaMemcpyDeviceToHost));
+    }
+    if (indicator) {
+        std::vector<int32_t> offs(e->P + 1), gst(e->G);
+        SS_CUDA(e, cudaMemcpy(offs.data(), e->offsets, (e->P + 1) * 4, cudaMemcpyDeviceToHost));
+        SS_CUDA(e, cudaMemcpy(gst.data(), e->gstart, e->G * 4, cudaMemcpyDeviceToHost));
+        for (int p = 0; p <= e->P; ++p) indicator[p] = (offs[p] < e->G) ? gst[offs[p]] : n;
+        if (n == 0)
+            for (int p = 0; p <= e->P; ++p) indicator[p] = 0;
+    }
+    if ((rc = clear_counts_row0(e))) return rc;
+    SS_CUDA(e, cudaStreamSynchronize(e->st));
+    return SS_OK;
+}
+
+// --------------------------------------------------------------------------
+// aggregate update / balancer / fused step
+// --------------------------------------------------------------------------
+extern "C" int ss_ingest(ss_engine* e, const uint32_t* groups, const int32_t* attrs, int64_t n) {
+    if (!e || n < 0) return SS_E_CONFIG;
+    if (n == 0) return SS_OK;
+    const uint32_t* dk;
+    const int32_t* dv;
+    int rc;
+    if ((rc = stage_input(e, groups, attrs, n, &dk, &dv))) return rc;
+    if ((rc = run_batch(e, dk, dv, n, nullptr, false))) return rc;
+    if ((rc = enqueue_report(e, n, false))) return rc;
+    return check_report(e, dk);
+}
+
+extern "C" int ss_balance(ss_engine* e, const uint32_t* groups, int64_t n, const ss_balancer* cfg,
+                          ss_move* moves, int64_t* n_moves, int64_t* scanned, int64_t* final_tpt) {
+    if (!e || !cfg || n < 0) return SS_E_CONFIG;
+    int rc;
+    if ((rc = check_balancer(e, cfg))) return rc;
+    const uint32_t* dk;
+    if ((rc = stage_input(e, groups, nullptr, n, &dk, nullptr))) return rc;
+    if ((rc = launch_count(e, dk, n, round_chunk(n)))) return rc;
+    if ((rc = launch_stats(e, 1))) return rc;
+    int nm = 0;
+    long long sc = 0;
+    std::vector<long long> ft(e->P);
+    if (cfg->policy == SS_POLICY_NO) {
+        std::vector<unsigned long long> tp(e->P);
+        SS_CUDA(e, cudaMemcpyAsync(tp.data(), e->tpt, e->P * 8, cudaMemcpyDeviceToHost, e->st));
+        SS_CUDA(e, cudaStreamSynchronize(e->st));
+        for (int p = 0; p < e->P; ++p) ft[p] = (long long)tp[p];
+    } else {
+        BalanceArgs a{};
+        a.policy = cfg->policy;
+        a.threshold = cfg->thread_threshold;
+        a.pot = cfg->pot;
+        a.cap = (int)std::min<int64_t>(cfg->max_moves > 0 ? cfg->max_moves : 4LL * e->P, e->cap_moves);
+        a.P = e->P;
+        a.order = e->order;
+        a.offsets = e->offsets;
+        a.gcount = e->gcount;
+        a.tpt = e->tpt;
+        a.moved = e->moved;
+        a.moves = e->moves;
+        a.front_top = e->front_top;
+        a.back_first = e->back_first;
+        a.mv_next = e->mv_next;
+        a.n_moves = e->n_moves;
+        a.scanned = e->scanned;
+        a.final_tpt = e->final_tpt;
+        a.bad = e->bad;
+        k_balance<<<1, kBalThreads, (size_t)e->P * (8 + 8 * 4), e->st>>>(a);
+        SS_CUDA(e, cudaGetLastError());
+        k_clear_moved<<<4, 256, 0, e->st>>>(e->moves, e->n_moves, e->moved);
+        SS_CUDA(e, cudaMemcpyAsync(&nm, e->n_moves, 4, cudaMemcpyDeviceToHost, e->st));
+        SS_CUDA(e, cudaMemcpyAsync(&sc, e->scanned, 8, cudaMemcpyDeviceToHost, e->st));
+        SS_CUDA(e, cudaMemcpyAsync(ft.data(), e->final_tpt, e->P * 8, cudaMemcpyDeviceToHost, e->st));
+    }
+    unsigned long long bad;
+    SS_CUDA(e, cudaMemcpyAsync(&bad, e->bad, 8, cudaMemcpyDeviceToHost, e->st));
+    SS_CUDA(e, cudaStreamSynchronize(e->st));
+    if (bad != (unsigned long long)kNoBad) return data_error(e, bad, dk);
+    if (nm > 0 && moves) {
+        std::vector<int4> mv(nm);
+        SS_CUDA(e, cudaMemcpy(mv.data(), e->moves, nm * sizeof(int4), cudaMemcpyDeviceToHost));
+        for (int i = 0; i < nm; ++i) moves[i] = ss_move{mv[i].x, mv[i].y, mv[i].z, mv[i].w};
+    }
+    if (n_moves) *n_moves = nm;
+    if (scanned) *scanned = sc;
+    if (final_tpt)
+        for (int p = 0; p < e->P; ++p) final_tpt[p] = ft[p];
+    // the MoveList is emitted but not applied (policies are pure)
+    SS_CUDA(e, cudaMemsetAsync(e->n_moves, 0, 4, e->st));
+    if ((rc = clear_counts_row0(e))) return rc;
+    SS_CUDA(e, cudaStreamSynchronize(e->st));
+    return SS_OK;
+}
+
+extern "C" int ss_step(ss_engine* e, const uint32_t* groups, const int32_t* attrs, int64_t n,
+                       const ss_balancer* cfg, ss_step_report* rep) {
+    if (!e || n < 0) return SS_E_CONFIG;
+    int rc;
+    if ((rc = check_balancer(e, cfg))) return rc;
+    const uint32_t* dk;
+    const int32_t* dv;
+    if ((rc = stage_input(e, groups, attrs, n, &dk, &dv))) return rc;
+    g_last_keys = dk;
+    const bool has_policy = cfg && cfg->policy != SS_POLICY_NO;
+    if (n > 0 && (rc = run_batch(e, dk, dv, n, cfg, true))) return rc;
+    if (n == 0) {
+        SS_CUDA(e, cudaMemsetAsync(e->tpt, 0, e->P * 8, e->st));
+        SS_CUDA(e, cudaMemsetAsync(e->touched, 0, 8, e->st));
+        SS_CUDA(e, cudaMemsetAsync(e->n_res, 0, 4, e->st));
+        SS_CUDA(e, cudaMemsetAsync(e->n_moves, 0, 4, e->st));
+        SS_CUDA(e, cudaMemsetAsync(e->scanned, 0, 8, e->st));
+    }
+    if ((rc = enqueue_report(e, n, has_policy && n > 0))) return rc;
+    if (rep) {
+        if ((rc = check_report(e, dk))) return rc;
+        fill_report(e, rep);
+    }
+    return SS_OK;
+}
+
+extern "C" int ss_last_report(ss_engine* e, ss_step_report* rep) {
+    if (!e) return SS_E_CONFIG;
+    int rc = check_report(e, g_last_keys);
+    if (rc) return rc;
+    if (rep) fill_report(e, rep);
+    return SS_OK;
+}
+
+extern "C" int ss_last_loads(ss_engine* e, int64_t* loads) {
+    if (!e || !loads) return SS_E_CONFIG;
+    std::vector<unsigned long long> t(e->P);
+    SS_CUDA(e, cudaStreamSynchronize(e->st));
+    SS_CUDA(e, cudaMemcpy(t.data(), e->tpt, e->P * 8, cudaMemcpyDeviceToHost));
+    for (int p = 0; p < e->P; ++p) loads[p] = (int64_t)t[p];
+    return SS_OK;
+}
+
+extern "C" int ss_last_moves(ss_engine* e, ss_move* moves, int64_t cap, int64_t* n) {
+    if (!e) return SS_E_CONFIG;
+    SS_CUDA(e, cudaStreamSynchronize(e->st));
+    int nm = (int)e->h_rep->moves;
+    if (n) *n = nm;
+    if (moves && nm > 0) {
+        nm = (int)std::min<int64_t>(nm, cap);
+        std::vector<int4> mv(nm);
+        SS_CUDA(e, cudaMemcpy(mv.data(), e->moves, nm * sizeof(int4), cudaMemcpyDeviceToHost));
+        for (int i = 0; i < nm; ++i) moves[i] = ss_move{mv[i].x, mv[i].y, mv[i].z, mv[i].w};
+    }
+    return SS_OK;
+}
+
+// --------------------------------------------------------------------------
+// state export
+// --------------------------------------------------------------------------
+extern "C" int ss_snapshot(ss_engine* e, int64_t* fill, int64_t* next_pos, int64_t* window_sum, int32_t* mn,
+                           int32_t* mx, double* avg) {
+    if (!e) return SS_E_CONFIG;
+    const int64_t G = e->G;
+    SS_CUDA(e, cudaStreamSynchronize(e->st));
+    std::vector<int32_t> f(G), np(G);
+    std::vector<long long> s(G);
+    SS_CUDA(e, cudaMemcpy(f.data(), e->fill, G * 4, cudaMemcpyDeviceToHost));
+    SS_CUDA(e, cudaMemcpy(np.data(), e->next_pos, G * 4, cudaMemcpyDeviceToHost));
+    SS_CUDA(e, cudaMemcpy(s.data(), e->wsum, G * 8, cudaMemcpyDeviceToHost));
+    if (mn) SS_CUDA(e, cudaMemcpy(mn, e->mn, G * 4, cudaMemcpyDeviceToHost));
+    if (mx) SS_CUDA(e, cudaMemcpy(mx, e->mx, G * 4, cudaMemcpyDeviceToHost));
+    for (int64_t g = 0; g < G; ++g) {
+        if (fill) fill[g] = f[g];
+        if (next_pos) next_pos[g] = np[g];
+        if (window_sum) window_sum[g] = s[g];
+        if (avg) avg[g] = f[g] ? (double)s[g] / (double)f[g] : 0.0;
+    }
+    return SS_OK;
+}
+
+extern "C" int ss_export_values(ss_engine* e, int64_t group, int64_t* out, int64_t cap, int64_t* n) {
+    if (!e || group < 0 || group >= e->G) return fail(e, SS_E_CONFIG, "group out of range");
+    SS_CUDA(e, cudaStreamSynchronize(e->st));
+    int32_t f, p;
+    int64_t o;
+    SS_CUDA(e, cudaMemcpy(&f, e->fill + group, 4, cudaMemcpyDeviceToHost));
+    SS_CUDA(e, cudaMemcpy(&p, e->next_pos + group, 4, cudaMemcpyDeviceToHost));
+    SS_CUDA(e, cudaMemcpy(&o, e->off + group, 8, cudaMemcpyDeviceToHost));
+    if (n) *n = f;
+    if (!out || f == 0) return SS_OK;
+    const int64_t span = (f < e->W) ? f : e->W;     // filling windows are linear
+    std::vector<int32_t> v(span);
+    SS_CUDA(e, cudaMemcpy(v.data(), e->ring + o, span * 4, cudaMemcpyDeviceToHost));
+    const int64_t m = std::min<int64_t>(cap, f);
+    for (int64_t i = 0; i < m; ++i) out[i] = v[(p + i) % e->W];
+    return SS_OK;
+}
+
+extern "C" int ss_results(ss_engine* e, int64_t cap, int32_t* groups, int64_t* count, int64_t* sum, double* avg,
+                          int32_t* mn, int32_t* mx, int64_t* n) {
+    if (!e) return SS_E_CONFIG;
+    SS_CUDA(e, cudaStreamSynchronize(e->st));
+    unsigned nr = 0;
+    SS_CUDA(e, cudaMemcpy(&nr, e->n_res, 4, cudaMemcpyDeviceToHost));
+    if (n) *n = nr;
+    const int64_t m = std::min<int64_t>(cap, nr);
+    if (m <= 0) return SS_OK;
+    std::vector<int32_t> rg(nr), rc(nr), rmn(nr), rmx(nr);
+    std::vector<long long> rs(nr);
+    std::vector<double> ra(nr);
+    SS_CUDA(e, cudaMemcpy(rg.data(), e->r_g, nr * 4, cudaMemcpyDeviceToHost));
+    SS_CUDA(e, cudaMemcpy(rc.data(), e->r_cnt, nr * 4, cudaMemcpyDeviceToHost));
+    SS_CUDA(e, cudaMemcpy(rs.data(), e->r_sum, nr * 8, cudaMemcpyDeviceToHost));
+    SS_CUDA(e, cudaMemcpy(ra.data(), e->r_avg, nr * 8, cudaMemcpyDeviceToHost));
+    if (e->minmax) {
+        SS_CUDA(e, cudaMemcpy(rmn.data(), e->r_mn, nr * 4, cudaMemcpyDeviceToHost));
+        SS_CUDA(e, cudaMemcpy(rmx.data(), e->r_mx, nr * 4, cudaMemcpyDeviceToHost));
+    }
+    // emission order is by group id (rows are produced concurrently)
+    std::vector<int> idx(nr);
+    for (unsigned i = 0; i < nr; ++i) idx[i] = (int)i;
+    std::sort(idx.begin(), idx.end(), [&](int a, int b) { return rg[a] < rg[b]; });
+    for (int64_t i = 0; i < m; ++i) {
+        const int k = idx[i];
+        if (groups) groups[i] = rg[k];
+        if (count) count[i] = rc[k];
+        if (sum) sum[i] = rs[k];
+        if (avg) avg[i] = ra[k];
+        if (mn) mn[i] = e->minmax ? rmn[k] : 0;
+        if (mx) mx[i] = e->minmax ? rmx[k] : 0;
+    }
+    return SS_OK;
+}

@@ -1,0 +1,336 @@
+// partition.cuh -- K2 (count / partition histogram) and K3 (stable rank +
+// placement) of the skewstream B200 pipeline.
+//
+// Reference behaviour (read-only, /root/reference/pkg/src/skewstream):
+//   count_batch    partition.py:117-130  group_counts = bincount(groups),
+//                                       tpt = bincount(g2t[groups]);
+//                                       DataError names the first bad tuple
+//   reorder_batch  partition.py:161-178  stable, thread-major, group-
+//                                       contiguous placement
+//   ingest_sequence engine.py:274-280   stable regroup preserving arrival order
+//
+// B200 design: a batch is counted once (warp-aggregated atomics, one atomic
+// per distinct key per warp) into per-sub-batch group histograms.  Each
+// L2-sized sub-batch is then placed by a stable LSD multisplit whose passes
+// use decoupled look-back (one pass when G <= 2^11, two up to 2^22).  The
+// stable placement gives every tuple its exact arrival rank inside its
+// group as (position - group start), which is all the window update needs.
+#pragma once
+
+#include "common.cuh"
+
+namespace ss {
+
+constexpr int kScanBlk = 4096;   // groups per block in the G-sized scans
+constexpr int kMaxBins = 2048;   // radix digit <= 11 bits
+constexpr int kSortThreads = 256;
+constexpr int kSortItems = 16;
+constexpr int kSortTile = kSortThreads * kSortItems;   // 4096 tuples
+
+// --------------------------------------------------------------------------
+// K2: per-sub-batch group histogram.  `chunk` divides the sub-batch size S,
+// so a CTA never straddles two sub-batches.
+// --------------------------------------------------------------------------
+template <bool SMEM>
+__global__ void __launch_bounds__(512)
+k_count(const uint32_t* __restrict__ groups, int64_t n, uint32_t G, int64_t S, int64_t chunk,
+        int32_t* __restrict__ gcnt, unsigned long long* __restrict__ bad, int vec_ok) {
+    extern __shared__ int32_t sh_hist[];
+    const int64_t c0 = (int64_t)blockIdx.x * chunk;
+    if (c0 >= n) return;
+    const int64_t c1 = min(n, c0 + chunk);
+    int32_t* dst = gcnt + (c0 / S) * (int64_t)G;
+    if (SMEM) {
+        for (uint32_t i = threadIdx.x; i < G; i += blockDim.x) sh_hist[i] = 0;
+        __syncthreads();
+    }
+    const unsigned lane = lane_id();
+    for (int64_t base = c0; base < c1; base += 4 * (int64_t)blockDim.x) {
+        const int64_t i = base + 4 * (int64_t)threadIdx.x;
+        uint32_t k[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
+        if (i + 3 < c1 && vec_ok) {
+            uint4 v = ld_stream_v4(groups + i);
+            k[0] = v.x; k[1] = v.y; k[2] = v.z; k[3] = v.w;
+        } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (i + q < c1) k[q] = groups[i + q];
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            uint32_t g = k[q];
+            const bool in = (i + q < c1);
+            if (in && g >= G) {
+                atomicMin(bad, (unsigned long long)(i + q));
+                g = 0xffffffffu;
+            }
+            if (!in) g = 0xffffffffu;
+            const unsigned peers = __match_any_sync(SS_FULL, g);
+            if (g != 0xffffffffu && lane == 31u - __clz(peers)) {
+                if (SMEM) atomicAdd(&sh_hist[g], __popc(peers));
+                else atomicAdd(&dst[g], __popc(peers));
+            }
+        }
+    }
+    if (SMEM) {
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < G; i += blockDim.x) {
+            const int32_t c = sh_hist[i];
+            if (c) atomicAdd(&dst[i], c);
+        }
+    }
+}
+
+// --------------------------------------------------------------------------
+// Batch statistics: gcount[g] = sum over sub-batches, tpt[pmap[g]] (the
+// reference's count_batch outputs) and the touched-group count.
+// --------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024)
+k_batch_stats(const int32_t* __restrict__ gcnt, int n_sub, uint32_t G, const int32_t* __restrict__ pmap,
+              int P, int32_t* __restrict__ gcount, unsigned long long* __restrict__ tpt,
+              unsigned long long* __restrict__ touched, const unsigned long long* __restrict__ bad) {
+    extern __shared__ unsigned long long sh_tpt[];
+    if (*bad != (unsigned long long)kNoBad) return;
+    for (int p = threadIdx.x; p < P; p += blockDim.x) sh_tpt[p] = 0;
+    __syncthreads();
+    uint32_t my_touched = 0;
+    for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < G; g += gridDim.x * blockDim.x) {
+        int32_t c = 0;
+        for (int s = 0; s < n_sub; ++s) c += gcnt[(int64_t)s * G + g];
+        gcount[g] = c;
+        if (c) {
+            atomicAdd(&sh_tpt[pmap[g]], (unsigned long long)c);
+            ++my_touched;
+        }
+    }
+    my_touched = warp_sum(my_touched);
+    if (lane_id() == 0 && my_touched) atomicAdd(touched, (unsigned long long)my_touched);
+    __syncthreads();
+    for (int p = threadIdx.x; p < P; p += blockDim.x)
+        if (sh_tpt[p]) atomicAdd(&tpt[p], sh_tpt[p]);
+}
+
+// --------------------------------------------------------------------------
+// G-sized exclusive scan of the per-sub-batch group histograms -> run
+// starts gstart[s][g], plus the radix digit histograms of every pass.
+// grid = (ceil(G / kScanBlk), n_sub), block = 1024 (4 groups per thread).
+// --------------------------------------------------------------------------
+struct DigitPlan {
+    int npass;
+    int shift[2];
+    int bits[2];   // digit width actually ranked (instantiated width may be larger)
+};
+
+__global__ void __launch_bounds__(1024)
+k_scan_reduce(const int32_t* __restrict__ gcnt, uint32_t G, int32_t* __restrict__ bsum, int nblk,
+              DigitPlan plan, uint32_t* __restrict__ dhist, const unsigned long long* __restrict__ bad) {
+    __shared__ uint32_t sh_dh[2][kMaxBins];
+    __shared__ int32_t sh_red[33];
+    if (*bad != (unsigned long long)kNoBad) return;
+    const int s = blockIdx.y;
+    const int32_t* row = gcnt + (int64_t)s * G;
+    for (int i = threadIdx.x; i < 2 * kMaxBins; i += blockDim.x) (&sh_dh[0][0])[i] = 0;
+    __syncthreads();
+    const uint32_t g0 = blockIdx.x * kScanBlk + 4 * threadIdx.x;
+    int32_t c[4];
+    int32_t tsum = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        c[q] = (g0 + q < G) ? row[g0 + q] : 0;
+        tsum += c[q];
+    }
+    for (int d = 0; d < plan.npass; ++d) {
+        const uint32_t mask = (1u << plan.bits[d]) - 1u;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t dig = ((g0 + q) >> plan.shift[d]) & mask;
+            const unsigned peers = __match_any_sync(SS_FULL, dig);
+            const uint32_t tot = __reduce_add_sync(peers, (uint32_t)c[q]);
+            if (lane_id() == 31u - __clz(peers) && tot) atomicAdd(&sh_dh[d][dig], tot);
+        }
+    }
+    int32_t total;
+    block_excl_scan(tsum, sh_red, &total);
+    if (threadIdx.x == 0) bsum[(int64_t)s * nblk + blockIdx.x] = total;
+    __syncthreads();
+    for (int d = 0; d < plan.npass; ++d) {
+        const int bins = 1 << plan.bits[d];
+        uint32_t* out = dhist + ((int64_t)s * 2 + d) * kMaxBins;
+        for (int b = threadIdx.x; b < bins; b += blockDim.x)
+            if (sh_dh[d][b]) atomicAdd(&out[b], sh_dh[d][b]);
+    }
+}
+
+// exclusive scan of the block sums (<= 1024 blocks) and of each pass's
+// digit histogram -> digit bases.  grid = n_sub, block = 1024.
+__global__ void __launch_bounds__(1024)
+k_scan_top(int32_t* __restrict__ bsum, int nblk, DigitPlan plan, uint32_t* __restrict__ dhist,
+           const unsigned long long* __restrict__ bad) {
+    __shared__ int32_t sh_red[33];
+    __shared__ uint32_t sh_ured[33];
+    if (*bad != (unsigned long long)kNoBad) return;
+    const int s = blockIdx.x;
+    {
+        int32_t v = (threadIdx.x < (unsigned)nblk) ? bsum[(int64_t)s * nblk + threadIdx.x] : 0;
+        int32_t tot;
+        int32_t ex = block_excl_scan(v, sh_red, &tot);
+        if (threadIdx.x < (unsigned)nblk) bsum[(int64_t)s * nblk + threadIdx.x] = ex;
+    }
+    for (int d = 0; d < plan.npass; ++d) {
+        uint32_t* h = dhist + ((int64_t)s * 2 + d) * kMaxBins;
+        // 2048 bins, 2 per thread
+        uint32_t a = h[2 * threadIdx.x], b = h[2 * threadIdx.x + 1];
+        uint32_t tot;
+        uint32_t ex = block_excl_scan(a + b, sh_ured, &tot);
+        h[2 * threadIdx.x] = ex;
+        h[2 * threadIdx.x + 1] = ex + a;
+    }
+}
+
+// block-local exclusive scan + block base -> gstart[s][g]
+__global__ void __launch_bounds__(1024)
+k_scan_down(const int32_t* __restrict__ gcnt, uint32_t G, const int32_t* __restrict__ bsum, int nblk,
+            int32_t* __restrict__ gstart, const unsigned long long* __restrict__ bad) {
+    __shared__ int32_t sh_red[33];
+    if (*bad != (unsigned long long)kNoBad) return;
+    const int s = blockIdx.y;
+    const int32_t* row = gcnt + (int64_t)s * G;
+    int32_t* out = gstart + (int64_t)s * G;
+    const uint32_t g0 = blockIdx.x * kScanBlk + 4 * threadIdx.x;
+    int32_t c[4], tsum = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        c[q] = (g0 + q < G) ? row[g0 + q] : 0;
+        tsum += c[q];
+    }
+    int32_t total;
+    int32_t ex = block_excl_scan(tsum, sh_red, &total) + bsum[(int64_t)s * nblk + blockIdx.x];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        if (g0 + q < G) out[g0 + q] = ex;
+        ex += c[q];
+    }
+}
+
+// --------------------------------------------------------------------------
+// K3: one stable LSD multisplit pass with decoupled look-back.
+//
+// A tile of 4096 tuples is ranked warp by warp: each warp owns 512
+// consecutive tuples held warp-striped (item j of lane l = tuple j*32+l),
+// ranks them in arrival order with __match_any_sync against a per-warp
+// digit histogram, and the per-bin prefix across warps, across earlier
+// tiles (look-back) and across lower digits (bin base) gives the output
+// position.  Tile ids come from an atomic ticket so a tile only ever waits
+// on tiles that are already resident.
+// --------------------------------------------------------------------------
+template <int RB>
+__global__ void __launch_bounds__(kSortThreads)
+k_sort_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
+            uint32_t* __restrict__ kout, int32_t* __restrict__ vout, int n, int shift, uint32_t mask,
+            const uint32_t* __restrict__ bin_base, unsigned long long* __restrict__ status,
+            uint32_t epoch, uint32_t* __restrict__ ticket, const unsigned long long* __restrict__ bad,
+            int stream_in) {
+    constexpr int BINS = 1 << RB;
+    constexpr int NW = kSortThreads / 32;
+    constexpr int BPT = (BINS + kSortThreads - 1) / kSortThreads;   // bins per thread
+    __shared__ uint16_t whist[NW][BINS];
+    __shared__ uint32_t gbase[BINS];
+    __shared__ uint32_t sh_tile;
+    if (*bad != (unsigned long long)kNoBad) return;
+    if (threadIdx.x == 0) sh_tile = atomicAdd(ticket, 1u);
+    for (int i = threadIdx.x; i < NW * BINS; i += kSortThreads) (&whist[0][0])[i] = 0;
+    __syncthreads();
+    const uint32_t tile = sh_tile;
+    const unsigned w = warp_id(), lane = lane_id();
+    const int64_t base = (int64_t)tile * kSortTile + (int64_t)w * 32 * kSortItems;
+
+    uint32_t key[kSortItems];
+    int32_t val[kSortItems];
+    uint16_t rank[kSortItems];
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {
+        const int64_t idx = base + j * 32 + lane;
+        if (idx < n) {
+            if (stream_in) {
+                key[j] = ld_stream_u32(kin + idx);
+                val[j] = (int32_t)ld_stream_u32(vin + idx);
+            } else {
+                key[j] = kin[idx];
+                val[j] = vin[idx];
+            }
+        } else {
+            key[j] = 0xffffffffu;
+            val[j] = 0;
+        }
+    }
+    const unsigned lt = lanemask_lt();
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {
+        const int64_t idx = base + j * 32 + lane;
+        const bool valid = idx < n;
+        const uint32_t d = valid ? ((key[j] >> shift) & mask) : 0xffffffffu;
+        const unsigned peers = __match_any_sync(SS_FULL, d);
+        uint32_t r = 0;
+        if (valid) r = whist[w][d];
+        __syncwarp();
+        if (valid) {
+            rank[j] = (uint16_t)(r + __popc(peers & lt));
+            if (lane == 31u - __clz(peers)) whist[w][d] = (uint16_t)(r + __popc(peers));
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+    // per-bin: exclusive prefix across warps, tile total, look-back
+    uint32_t tot[BPT];
+#pragma unroll
+    for (int q = 0; q < BPT; ++q) {
+        const int b = threadIdx.x + q * kSortThreads;
+        tot[q] = 0;
+        if (b < BINS) {
+            uint32_t run = 0;
+#pragma unroll
+            for (int ww = 0; ww < NW; ++ww) {
+                const uint32_t c = whist[ww][b];
+                whist[ww][b] = (uint16_t)run;
+                run += c;
+            }
+            tot[q] = run;
+            st_relaxed_u64(&status[(int64_t)tile * BINS + b],
+                           lb_pack(epoch, tile == 0 ? kFlagInc : kFlagAgg, run));
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < BPT; ++q) {
+        const int b = threadIdx.x + q * kSortThreads;
+        if (b < BINS) {
+            uint32_t excl = 0;
+            if (tile > 0) {
+                int64_t t = (int64_t)tile - 1;
+                while (true) {
+                    const unsigned long long v = ld_relaxed_u64(&status[t * BINS + b]);
+                    const uint32_t ep = (uint32_t)(v >> 34);
+                    const unsigned long long fl = (v >> 32) & 3ull;
+                    if (ep != epoch || fl == 0) continue;   // not published yet
+                    excl += (uint32_t)v;
+                    if (fl == kFlagInc) break;
+                    --t;
+                }
+                st_relaxed_u64(&status[(int64_t)tile * BINS + b], lb_pack(epoch, kFlagInc, excl + tot[q]));
+            }
+            gbase[b] = bin_base[b] + excl;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {
+        const int64_t idx = base + j * 32 + lane;
+        if (idx < n) {
+            const uint32_t d = (key[j] >> shift) & mask;
+            const uint32_t pos = gbase[d] + whist[w][d] + rank[j];
+            vout[pos] = val[j];
+            if (kout) kout[pos] = key[j];
+        }
+    }
+}
+
+}  // namespace ss

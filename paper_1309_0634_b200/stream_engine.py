@@ -1,0 +1,357 @@
+"""StreamEngine: the device-resident operator behind every public call.
+
+One ``StreamEngine`` owns one ``ss_engine`` handle (include/ss_b200.h): the
+per-group windows, the group -> partition assignment and the pipeline
+scratch of one GPU.  Inputs may be numpy arrays (host) or torch tensors
+(host or CUDA); host inputs are staged by the engine itself.  Every
+computation runs in the CUDA library -- this module only marshals
+pointers and maps status codes onto the reference's exception types
+(errors.py).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib as L
+from .errors import DataError, InvalidConfigError
+
+AGG_NAMES = {"count": L.AGG_COUNT, "sum": L.AGG_SUM, "avg": L.AGG_AVG,
+             "min": L.AGG_MIN, "max": L.AGG_MAX}
+
+
+@dataclass(frozen=True)
+class WindowSpec:
+    """Per-group sliding window of the last ``rows`` values.
+
+    The reference window is a per-group ring (engine.py:51-70); ``scope``
+    is kept for the stream-wide variant listed as future work.
+    """
+
+    rows: int
+    scope: str = "group"
+
+    def __post_init__(self):
+        if self.rows < 1:
+            raise InvalidConfigError(f"window must be >= 1, got {self.rows}")
+        if self.scope != "group":
+            raise InvalidConfigError("only scope='group' (the reference semantics) is implemented")
+
+
+@dataclass(frozen=True)
+class Aggregates:
+    """Aggregate functions maintained per group (COUNT/SUM are the
+    reference's own state, engine.py:67-70; AVG/MIN/MAX derive from it)."""
+
+    names: tuple = ("count", "sum", "avg")
+
+    def __post_init__(self):
+        for n in self.names:
+            if n not in AGG_NAMES:
+                raise InvalidConfigError(f"unknown aggregate {n!r}")
+
+    @property
+    def mask(self) -> int:
+        m = L.AGG_COUNT | L.AGG_SUM
+        for n in self.names:
+            m |= AGG_NAMES[n]
+        return m
+
+
+@dataclass
+class StepReport:
+    """Per-batch record (the fields of IterationReport, engine.py:167-176,
+    plus the load-monitor outputs)."""
+
+    tuples: int
+    imbalance: int
+    moves: int
+    moves_applied_before: int
+    scanned: int
+    max_load: int
+    touched: int
+    split_groups: int
+    mean_load: float
+    load_ratio: float
+
+
+@dataclass
+class Results:
+    """Per-batch emission: one row per group touched by the batch."""
+
+    groups: np.ndarray
+    count: np.ndarray
+    sum: np.ndarray
+    avg: np.ndarray
+    min: np.ndarray | None = None
+    max: np.ndarray | None = None
+
+
+def _ptr(x):
+    """(pointer, keepalive) of a numpy array or torch tensor."""
+    if x is None:
+        return None, None
+    if isinstance(x, np.ndarray):
+        x = np.ascontiguousarray(x)
+        return x.ctypes.data_as(C.c_void_p), x
+    # torch tensor
+    if not x.is_contiguous():
+        x = x.contiguous()
+    return C.c_void_p(x.data_ptr()), x
+
+
+def _keys_u32(groups, n_groups: int):
+    if isinstance(groups, np.ndarray):
+        g = groups
+        if g.dtype != np.uint32:
+            if g.size and (g.min() < 0 or g.max() > 0xFFFFFFFF):
+                bad = np.flatnonzero((g < 0) | (g >= n_groups))
+                i = int(bad[0])
+                raise DataError(f"tuple {i} has group {int(g[i])}, outside [0, {n_groups})")
+            g = g.astype(np.uint32)
+        return g
+    import torch
+    if groups.dtype == torch.int32 or groups.dtype == torch.uint32:
+        return groups
+    if groups.dtype == torch.int64:
+        return groups.to(torch.int32)
+    raise InvalidConfigError(f"unsupported group dtype {groups.dtype}")
+
+
+def _attrs_i32(attrs):
+    if isinstance(attrs, np.ndarray):
+        return attrs if attrs.dtype == np.int32 else attrs.astype(np.int32)
+    import torch
+    if attrs.dtype == torch.int32:
+        return attrs
+    return attrs.to(torch.int32)
+
+
+class StreamEngine:
+    """Device-resident sliding-window GROUP BY with partitioned execution.
+
+    ``n_partitions`` is the number of processing units (the aggregate
+    kernel's CTAs); the reference's logical threads (harness.py:53-55).
+    """
+
+    def __init__(self, n_groups: int, window, n_partitions: int = 148,
+                 aggregates=("count", "sum", "avg"), device: int = 0,
+                 max_batch: int = 1 << 24, sub_batch: int = 0, pool_values: int = 0,
+                 stream=None):
+        self._lib = L.load()
+        spec = window if isinstance(window, WindowSpec) else WindowSpec(int(window))
+        aggs = aggregates if isinstance(aggregates, Aggregates) else Aggregates(tuple(aggregates))
+        if n_groups < 1:
+            raise InvalidConfigError(f"n_groups must be >= 1, got {n_groups}")
+        if n_partitions < 1:
+            raise InvalidConfigError(f"n_partitions must be >= 1, got {n_partitions}")
+        self.n_groups = int(n_groups)
+        self.window = spec.rows
+        self.n_partitions = int(n_partitions)
+        self.aggregates = aggs
+        self.minmax = bool(aggs.mask & (L.AGG_MIN | L.AGG_MAX))
+        cfg = L.Config(n_groups=self.n_groups, window=self.window,
+                       n_partitions=self.n_partitions, key_bits=32, agg_mask=aggs.mask,
+                       scope=0, device=device, reserved=0, max_batch=int(max_batch),
+                       sub_batch=int(sub_batch), pool_values=int(pool_values))
+        h = C.c_void_p()
+        rc = self._lib.ss_create(C.byref(cfg), C.byref(h))
+        self._h = h
+        if rc:
+            msg = self._lib.ss_last_error(h) if h else b"ss_create failed"
+            if h:
+                self._lib.ss_destroy(h)
+            self._h = None
+            from .errors import raise_for_status
+            raise_for_status(rc, msg.decode())
+        if stream is not None:
+            self.set_stream(stream)
+
+    # -- lifecycle ---------------------------------------------------------
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.ss_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc):
+        L.check(self._h, rc)
+
+    def set_stream(self, stream):
+        """Enqueue on a torch.cuda.Stream (or a raw cudaStream_t int)."""
+        raw = getattr(stream, "cuda_stream", stream)
+        self._check(self._lib.ss_set_stream(self._h, C.c_void_p(int(raw))))
+
+    def sync(self):
+        self._check(self._lib.ss_sync(self._h))
+
+    # -- assignment --------------------------------------------------------
+    def set_lists(self, lists):
+        order = np.asarray([g for lst in lists for g in lst], dtype=np.int32)
+        offs = np.zeros(len(lists) + 1, dtype=np.int64)
+        np.cumsum([len(x) for x in lists], out=offs[1:])
+        if len(lists) != self.n_partitions:
+            raise InvalidConfigError("assignment has a different number of partitions")
+        po, _k1 = _ptr(order)
+        pf, _k2 = _ptr(offs)
+        self._check(self._lib.ss_set_assignment(self._h, po, pf))
+
+    def get_lists(self):
+        g2t = np.empty(self.n_groups, dtype=np.int32)
+        order = np.empty(self.n_groups, dtype=np.int32)
+        offs = np.empty(self.n_partitions + 1, dtype=np.int64)
+        self._check(self._lib.ss_get_assignment(self._h, _ptr(g2t)[0], _ptr(order)[0], _ptr(offs)[0]))
+        lists = [order[offs[p]:offs[p + 1]].astype(np.int64).tolist() for p in range(self.n_partitions)]
+        return g2t.astype(np.int64), lists
+
+    def apply_moves(self, moves):
+        """moves: iterable of (group, src, dst, placement) with placement
+        'front'/'back' (partition.py:181-203)."""
+        arr = (L.MoveC * max(1, len(moves)))()
+        for i, (g, s, d, pl) in enumerate(moves):
+            if pl not in ("front", "back"):
+                raise InvalidConfigError(f"unknown placement {pl!r}")
+            arr[i] = L.MoveC(int(g), int(s), int(d), L.BACK_CODE if pl == "back" else L.FRONT_CODE)
+        self._check(self._lib.ss_apply_moves(self._h, arr, len(moves)))
+
+    # -- partition step ----------------------------------------------------
+    def count(self, groups):
+        g = _keys_u32(groups, self.n_groups)
+        n = len(g)
+        counts = np.empty(self.n_groups, dtype=np.int64)
+        tpt = np.empty(self.n_partitions, dtype=np.int64)
+        pg, _k = _ptr(g)
+        self._check(self._lib.ss_count(self._h, pg, n, _ptr(counts)[0], _ptr(tpt)[0]))
+        return counts, tpt
+
+    def reorder(self, groups, attrs):
+        g = _keys_u32(groups, self.n_groups)
+        a = _attrs_i32(attrs)
+        n = len(g)
+        og = np.empty(n, dtype=np.uint32)
+        oa = np.empty(n, dtype=np.int32)
+        ind = np.empty(self.n_partitions + 1, dtype=np.int64)
+        pg, _k1 = _ptr(g)
+        pa, _k2 = _ptr(a)
+        self._check(self._lib.ss_reorder(self._h, pg, pa, n, _ptr(og)[0], _ptr(oa)[0], _ptr(ind)[0]))
+        return og.astype(np.int64), oa.astype(np.int64), ind
+
+    # -- aggregate update ----------------------------------------------------
+    def ingest(self, groups, attrs):
+        g = _keys_u32(groups, self.n_groups)
+        a = _attrs_i32(attrs)
+        pg, _k1 = _ptr(g)
+        pa, _k2 = _ptr(a)
+        self._check(self._lib.ss_ingest(self._h, pg, pa, len(g)))
+
+    # -- balancer ------------------------------------------------------------
+    @staticmethod
+    def balancer_struct(policy="no", thread_threshold=1000, pot=0.5, max_moves=None,
+                        split=False, split_target=1.2, split_max=0):
+        if policy not in L.POLICY_CODES:
+            raise InvalidConfigError(f"unknown policy {policy!r}")
+        return L.Balancer(policy=L.POLICY_CODES[policy], reserved=0,
+                          thread_threshold=int(thread_threshold), pot=float(pot),
+                          max_moves=int(max_moves or 0), split=int(bool(split)),
+                          split_max=int(split_max), split_target=float(split_target))
+
+    def balance(self, groups, bal: "L.Balancer"):
+        g = _keys_u32(groups, self.n_groups)
+        cap = 4 * self.n_partitions if bal.max_moves <= 0 else int(bal.max_moves)
+        cap = max(cap, 1)
+        moves = (L.MoveC * cap)()
+        nm = C.c_int64()
+        sc = C.c_int64()
+        ft = np.empty(self.n_partitions, dtype=np.int64)
+        pg, _k = _ptr(g)
+        self._check(self._lib.ss_balance(self._h, pg, len(g), C.byref(bal), moves, C.byref(nm),
+                                         C.byref(sc), _ptr(ft)[0]))
+        out = [(m.group, m.src, m.dst, "back" if m.placement == L.BACK_CODE else "front")
+               for m in moves[:nm.value]]
+        return out, sc.value, ft
+
+    # -- fused per-batch step --------------------------------------------------
+    def step(self, groups, attrs, balancer=None, sync: bool = True):
+        g = _keys_u32(groups, self.n_groups)
+        a = _attrs_i32(attrs)
+        pg, _k1 = _ptr(g)
+        pa, _k2 = _ptr(a)
+        bal = balancer if balancer is not None else self.balancer_struct()
+        rep = L.StepReport()
+        self._check(self._lib.ss_step(self._h, pg, pa, len(g), C.byref(bal),
+                                      C.byref(rep) if sync else None))
+        self._keep = (_k1, _k2)
+        return self._report(rep) if sync else None
+
+    def last_report(self) -> StepReport:
+        rep = L.StepReport()
+        self._check(self._lib.ss_last_report(self._h, C.byref(rep)))
+        return self._report(rep)
+
+    @staticmethod
+    def _report(r) -> StepReport:
+        return StepReport(r.tuples, r.imbalance, r.moves, r.moves_applied_before, r.scanned,
+                          r.max_load, r.touched, r.split_groups, r.mean_load, r.load_ratio)
+
+    def last_loads(self) -> np.ndarray:
+        out = np.empty(self.n_partitions, dtype=np.int64)
+        self._check(self._lib.ss_last_loads(self._h, _ptr(out)[0]))
+        return out
+
+    def last_moves(self):
+        cap = 4 * self.n_partitions
+        arr = (L.MoveC * cap)()
+        n = C.c_int64()
+        self._check(self._lib.ss_last_moves(self._h, arr, cap, C.byref(n)))
+        return [(m.group, m.src, m.dst, "back" if m.placement == L.BACK_CODE else "front")
+                for m in arr[:min(n.value, cap)]]
+
+    # -- state export ----------------------------------------------------------
+    def snapshot(self):
+        G = self.n_groups
+        out = {k: np.empty(G, dtype=np.int64) for k in ("fill", "next_pos", "window_sum")}
+        mn = np.empty(G, dtype=np.int32)
+        mx = np.empty(G, dtype=np.int32)
+        avg = np.empty(G, dtype=np.float64)
+        self._check(self._lib.ss_snapshot(self._h, _ptr(out["fill"])[0], _ptr(out["next_pos"])[0],
+                                          _ptr(out["window_sum"])[0], _ptr(mn)[0], _ptr(mx)[0],
+                                          _ptr(avg)[0]))
+        out["avg"] = avg
+        if self.minmax:
+            out["min"] = mn.astype(np.int64)
+            out["max"] = mx.astype(np.int64)
+        return out
+
+    def contents(self, group: int) -> np.ndarray:
+        out = np.empty(self.window if self.window < (1 << 22) else 1, dtype=np.int64)
+        n = C.c_int64()
+        self._check(self._lib.ss_export_values(self._h, int(group), None, 0, C.byref(n)))
+        out = np.empty(max(1, n.value), dtype=np.int64)
+        self._check(self._lib.ss_export_values(self._h, int(group), _ptr(out)[0], n.value, C.byref(n)))
+        return out[:n.value]
+
+    def results(self) -> Results:
+        n = C.c_int64()
+        self._check(self._lib.ss_results(self._h, 0, None, None, None, None, None, None, C.byref(n)))
+        k = n.value
+        g = np.empty(k, dtype=np.int32)
+        cnt = np.empty(k, dtype=np.int64)
+        sm = np.empty(k, dtype=np.int64)
+        avg = np.empty(k, dtype=np.float64)
+        mn = np.empty(k, dtype=np.int32)
+        mx = np.empty(k, dtype=np.int32)
+        self._check(self._lib.ss_results(self._h, k, _ptr(g)[0], _ptr(cnt)[0], _ptr(sm)[0], _ptr(avg)[0],
+                                         _ptr(mn)[0], _ptr(mx)[0], C.byref(n)))
+        r = Results(g.astype(np.int64), cnt, sm, avg)
+        if self.minmax:
+            r.min = mn.astype(np.int64)
+            r.max = mx.astype(np.int64)
+        return r

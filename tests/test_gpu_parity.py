@@ -1,0 +1,257 @@
+"""CUDA path vs the oracle and the reference's golden fixtures (B200 only).
+
+Every test calls through the C ABI (libss_b200.so via StreamEngine) and
+compares against tests/golden/ (produced by the reference itself) or the
+CPU oracle (oracle/port.py, pinned by test_oracle.py).  Integer results
+must be bit-exact; AVG is the correctly rounded double quotient, also
+compared exactly (tolerance 0).
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from oracle import port as O
+from paper_1309_0634_b200 import datagen as D
+from paper_1309_0634_b200.errors import DataError, InvalidConfigError, StaleMoveError
+
+pytestmark = pytest.mark.gpu
+
+
+def _engine(G, W, P=4, **kw):
+    from paper_1309_0634_b200.stream_engine import StreamEngine
+    kw.setdefault("max_batch", 1 << 20)
+    return StreamEngine(G, W, n_partitions=P, **kw)
+
+
+def _dense_values(eng, G, W):
+    snap = eng.snapshot()
+    vals = np.zeros((G, W), dtype=np.int64)
+    for g in range(G):
+        c = eng.contents(g)
+        p = int(snap["next_pos"][g])
+        vals[g, (p + np.arange(len(c))) % W] = c
+    return vals
+
+
+def _digest(*arrays):
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a, dtype=np.int64).tobytes())
+    return h.hexdigest()
+
+
+# ---- window update: golden ingest cases (engine.py:185-296) -----------------
+
+@pytest.mark.parametrize("sub_batch", [0, 16384])
+def test_ingest_golden(golden, sub_batch):
+    data = golden("ingest.json")
+    for case in data["cases"]:
+        G, W = case["n_groups"], case["window"]
+        eng = _engine(G, W, P=3, sub_batch=sub_batch)
+        g = np.asarray(case["groups"], dtype=np.int64)
+        a = np.asarray(case["attrs"], dtype=np.int64)
+        lo = 0
+        for snap, hi in zip(case["snaps"], case["cuts"] + [len(g)]):
+            eng.ingest(g[lo:hi], a[lo:hi])
+            s = eng.snapshot()
+            assert s["fill"].tolist() == snap["fill"]
+            assert s["window_sum"].tolist() == snap["window_sum"]
+            lo = hi
+        fin = case["final"]
+        s = eng.snapshot()
+        assert s["next_pos"].tolist() == fin["next_pos"]
+        for gi in range(G):
+            assert eng.contents(gi).tolist() == fin["contents"][gi]
+        eng.close()
+
+
+def test_hand_vectors(golden):
+    data = golden("ingest.json")
+    for h in data["hand"]:
+        eng = _engine(1, h["window"], P=1)
+        eng.ingest(np.zeros(h["n"], dtype=np.int64), np.arange(1, h["n"] + 1))
+        assert eng.contents(0).tolist() == h["final"]["contents"][0]
+        assert eng.snapshot()["next_pos"].tolist() == h["final"]["next_pos"]
+        eng.close()
+    eng = _engine(1, 3, P=1)
+    for v in (5, 7, 9, 4):       # test_engine.py:45-56
+        eng.ingest(np.array([0]), np.array([v]))
+    assert eng.contents(0).tolist() == [7, 9, 4]
+    assert eng.snapshot()["window_sum"].tolist() == [20]
+
+
+# ---- partition step (partition.py:117-203) ------------------------------------
+
+def test_count_and_reorder_golden(golden):
+    for c in golden("partition.json")["cases"]:
+        lists = c["lists"]
+        G, P = len(c["g2t"]), len(lists)
+        eng = _engine(G, 4, P=P)
+        eng.set_lists(lists)
+        counts, tpt = eng.count(np.asarray(c["groups"], dtype=np.int64))
+        assert counts.tolist() == c["counts"] and tpt.tolist() == c["tpt"]
+        rg, ra, ind = eng.reorder(np.asarray(c["groups"]), np.asarray(c["attrs"]))
+        assert rg.tolist() == c["rgroups"]
+        assert ra.tolist() == c["rattrs"]
+        assert ind.tolist() == c["indicator"]
+        eng.close()
+
+
+def test_apply_moves_golden(golden):
+    for c in golden("partition.json")["moves"]:
+        lists = c["lists"]
+        G, P = len(c["g2t"]), len(lists)
+        eng = _engine(G, 4, P=P)
+        eng.set_lists(lists)
+        mv = [tuple(m) for m in c["moves"]]
+        if c["error"] == "stale":
+            with pytest.raises(StaleMoveError):
+                eng.apply_moves(mv)
+        elif c["error"] == "config":
+            with pytest.raises(InvalidConfigError):
+                eng.apply_moves(mv)
+        else:
+            eng.apply_moves(mv)
+            g2t, new = eng.get_lists()
+            assert g2t.tolist() == c["result"]["g2t"]
+            assert new == c["result"]["lists"]
+        if c["error"]:
+            g2t, same = eng.get_lists()
+            assert same == lists
+        eng.close()
+
+
+def test_count_data_error_leaves_state():
+    eng = _engine(10, 4, P=2)
+    eng.ingest(np.array([1, 2, 3]), np.array([5, 6, 7]))
+    with pytest.raises(DataError, match="tuple 2 has group 10"):
+        eng.count(np.array([0, 1, 10, 3]))
+    with pytest.raises(DataError, match="tuple 1 has group"):
+        eng.step(np.array([0, 11, 3]), np.array([1, 1, 1]))
+    s = eng.snapshot()
+    assert s["fill"].tolist() == [0, 1, 1, 1, 0, 0, 0, 0, 0, 0]
+    eng.step(np.array([1]), np.array([9]))
+    assert eng.snapshot()["window_sum"][1] == 14
+
+
+# ---- balancer (balance.py) -------------------------------------------------------
+
+def test_policies_golden(golden):
+    from paper_1309_0634_b200.stream_engine import StreamEngine
+    for c in golden("policies.json")["cases"]:
+        lists = c["lists"]
+        G, P = len(c["g2t"]), len(lists)
+        eng = _engine(G, 4, P=P)
+        eng.set_lists(lists)
+        groups = np.asarray(c["groups"], dtype=np.int64)
+        for pol, exp in c["out"].items():
+            bal = StreamEngine.balancer_struct(pol, c["threshold"], c["pot"], c["max_moves"])
+            moves, scanned, final = eng.balance(groups, bal)
+            assert [list(m) for m in moves] == exp["moves"], pol
+            assert scanned == exp["scanned"], pol
+            assert final.tolist() == exp["final_tpt"], pol
+        eng.close()
+
+
+# ---- fused step: the harness loop (harness.py:99-117) ------------------------------
+
+def test_pipeline_golden(golden):
+    from paper_1309_0634_b200.stream_engine import StreamEngine
+    for r in golden("pipeline.json")["runs"]:
+        G, W, P = r["groups"], r["window"], r["threads"]
+        spec = D.DatasetSpec(D.DatasetKind(r["kind"]), r["n"], G, r["exponent"], r["seed"])
+        eng = _engine(G, W, P=P, sub_batch=16384)
+        bal = StreamEngine.balancer_struct(r["policy"], r["threshold"], 0.5)
+        rows = []
+        for b in D.batches(D.stream_for(spec), r["batch"]):
+            rep = eng.step(b.groups, b.attrs, bal)
+            rows.append([rep.tuples, rep.imbalance, rep.moves_applied_before, rep.scanned])
+        assert rows == r["rows"], r["policy"]
+        s = eng.snapshot()
+        assert s["fill"].tolist() == r["fill"]
+        assert s["next_pos"].tolist() == r["next_pos"]
+        assert s["window_sum"].tolist() == r["window_sum"]
+        assert _digest(_dense_values(eng, G, W)) == r["values_digest"]
+        _, lists = eng.get_lists()
+        assert lists == r["final_lists"]
+        eng.close()
+
+
+@pytest.mark.parametrize("policy", ["no", "first", "all", "prob", "best", "shift", "shiftlocal"])
+@pytest.mark.parametrize("G,W,P,B,sub", [(1000, 1000, 148, 1 << 17, 1 << 15),
+                                         (10_000, 300, 64, 50_000, 16384),
+                                         (5000, 7, 37, 30_000, 0)])
+def test_step_vs_oracle(policy, G, W, P, B, sub):
+    """Multi-sub-batch, one- and two-pass placement, every policy."""
+    from paper_1309_0634_b200.stream_engine import StreamEngine
+    spec = D.DatasetSpec(D.DatasetKind.ZIPF, 4 * B, G, 1.1, 23)
+    eng = _engine(G, W, P=P, sub_batch=sub, aggregates=("count", "sum", "avg", "min", "max"),
+                  max_batch=B)
+    thr = max(1, B // (10 * P))
+    bal = StreamEngine.balancer_struct(policy, thr, 0.5)
+    cfg = O.balancer_cfg(policy, thr, 0.5)
+    store, asg = O.OStore(G, W), O.contiguous_assignment(G, P)
+    for b in D.batches(D.stream_for(spec), B):
+        rep = eng.step(b.groups, b.attrs, bal)
+        counts, tpt = O.histogram(b.groups, asg)
+        rg, ra, ind = O.place(b.groups, b.attrs, asg, counts, tpt)
+        v = O.POLICY_FNS[policy](counts, tpt, asg, rg, ind, cfg)
+        store.ingest(rg, ra, assume_grouped=True)
+        assert rep.moves == len(v.moves) and rep.scanned == v.scanned
+        assert rep.imbalance == int(tpt.max() - tpt.min())
+        assert eng.last_moves() == [tuple(m) for m in v.moves]
+        res = eng.results()
+        touched = np.flatnonzero(counts)
+        assert res.groups.tolist() == touched.tolist()
+        cnt, sm, avg, mn, mx = store.aggregates(touched)
+        assert np.array_equal(res.count, cnt) and np.array_equal(res.sum, sm)
+        assert np.array_equal(res.avg, avg)
+        assert np.array_equal(res.min, mn) and np.array_equal(res.max, mx)
+        asg = O.apply_move_list(asg, v.moves)
+    s = eng.snapshot()
+    assert np.array_equal(s["fill"], store.fill)
+    assert np.array_equal(s["next_pos"], store.next_pos)
+    assert np.array_equal(s["window_sum"], store.window_sum)
+    _, lists = eng.get_lists()
+    assert lists == asg.lists
+    for gi in (0, 1, G // 2, G - 1):
+        assert eng.contents(gi).tolist() == store.contents(gi).tolist()
+    eng.close()
+
+
+@pytest.mark.parametrize("W", [1, 5, 64])
+def test_sparse_store_matches_oracle(W):
+    """Occupancy-proportional rings (capacity doubling up to W)."""
+    G, B = 3000, 20_000
+    spec = D.DatasetSpec(D.DatasetKind.ZIPF, 6 * B, G, 1.3, 5)
+    eng = _engine(G, W, P=16, pool_values=4 * G * W + 1_000_000, max_batch=B,
+                  aggregates=("count", "sum", "avg", "min", "max"))
+    store = O.OStore(G, W, dense_limit=0)
+    for b in D.batches(D.stream_for(spec), B):
+        eng.step(b.groups, b.attrs)
+        store.ingest(b.groups, b.attrs)
+    s = eng.snapshot()
+    cnt, sm, avg, mn, mx = store.aggregates()
+    assert np.array_equal(s["fill"], cnt) and np.array_equal(s["window_sum"], sm)
+    assert np.array_equal(s["min"], mn) and np.array_equal(s["max"], mx)
+    for gi in range(0, G, 97):
+        assert eng.contents(gi).tolist() == store.contents(gi).tolist()
+    eng.close()
+
+
+def test_large_batch_properties():
+    """Full-size C1 batch (2^24): conservation and window identities."""
+    G, W, B = 1000, 1000, 1 << 24
+    g, a = D.gen_uniform(B, G, 3).arrays()
+    eng = _engine(G, W, P=148, max_batch=B)
+    eng.step(g, a)
+    s = eng.snapshot()
+    # every group received B/G >= W values: full windows of the last W values
+    assert (s["fill"] == W).all()
+    gg = g.reshape(-1, G)           # round-robin: tuple i has group i % G
+    tail = a.reshape(-1, G)[-W:]
+    assert np.array_equal(s["window_sum"], tail.sum(axis=0))
+    assert (gg[0] == np.arange(G)).all()
+    eng.close()
