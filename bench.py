@@ -1,0 +1,394 @@
+"""Benchmark: sustained tuples/s of the fused per-batch step on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+A "step" is one batch of the hot path (harness.run's loop body,
+harness.py:99-117): count -> balancer (device, overlapped) -> stable
+placement -> per-group window update -> per-batch result emission ->
+apply moves.  Default workload = BASELINE.json configs[1] (C2): Zipf
+s=1.0 keys over 10K groups, per-group window W=1e5, SUM+COUNT, the
+paper's prob_check group-reassignment balancer, batch 2^24 tuples,
+P = 148 processing units (one aggregate CTA per SM).
+
+Printed JSON line (rank 0):
+  value      whole-job tuples/s with the staged batches already in HBM
+  e2e        the same through StreamEngine.step with pinned HOST buffers:
+             H2D of each batch and D2H of the emitted per-group AVG rows
+             inside the timed region
+  roofline   dominant kernel class: algorithmic bytes / its CUDA-event time
+  path_roofline  whole step: SURVEY 8(d) algorithmic bytes / step time
+  cpu_baseline   the oracle port (oracle/port.py) on the host, bounded sample
+--impl reference times that CPU path alone (the reference package is pure
+Python/numpy; its algorithm is restated in oracle/port.py).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (description, kind, exponent, G, W, B, aggregates, policy, split)
+    "c1": ("C1 uniform keys, 1K groups, W=1000, AVG, static partitioning, no rebalancing",
+           "uniform", 1.0, 1000, 1000, 1 << 24, ("count", "sum", "avg"), "no", False),
+    "c2": ("C2 Zipf s=1.0, 10K groups, W=1e5, SUM+COUNT, prob_check group reassignment",
+           "zipf", 1.0, 10_000, 100_000, 1 << 24, ("count", "sum"), "prob", False),
+    "c3": ("C3 Zipf s=1.5, 100K groups, W=1e6, AVG, prob_check",
+           "zipf", 1.5, 100_000, 1_000_000, 1 << 24, ("count", "sum", "avg"), "prob", False),
+}
+P_DEFAULT = 148
+L2_BYTES = 126 * (1 << 20)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# synthetic input, generated on the device (inverse CDF of the zipf pmf)
+# ---------------------------------------------------------------------------
+def make_batches(kind, s, G, B, nbuf, device, seed):
+    import torch
+    gen = torch.Generator(device=device)
+    gen.manual_seed(seed)
+    out = []
+    if kind == "zipf":
+        w = torch.arange(1, G + 1, dtype=torch.float64, device=device).pow(-s)
+        cdf = torch.cumsum(w, 0)
+        cdf /= cdf[-1].clone()
+        cdf[-1] = 1.0
+    for i in range(nbuf):
+        if kind == "zipf":
+            u = torch.rand(B, dtype=torch.float64, device=device, generator=gen)
+            g = torch.searchsorted(cdf, u, right=True).to(torch.int32)
+        else:
+            g = (torch.arange(B, device=device, dtype=torch.int64) + i * B) % G
+            g = g.to(torch.int32)
+        a = torch.randint(-(2 ** 31), 2 ** 31, (B,), device=device, generator=gen,
+                          dtype=torch.int64).to(torch.int32)
+        out.append((g.contiguous(), a.contiguous()))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=5)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[2:6]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU path: the oracle port of the reference pipeline, bounded sample
+# ---------------------------------------------------------------------------
+def cpu_pipeline(cfg_name, seconds=15.0, batch=1 << 20, P=P_DEFAULT):
+    from oracle import port as O
+    from paper_1309_0634_b200 import datagen as D
+    desc, kind, s, G, W, _, aggs, policy, _ = CONFIGS[cfg_name]
+    dk = D.DatasetKind.UNIFORM if kind == "uniform" else D.DatasetKind.ZIPF
+    spec = D.DatasetSpec(dk, batch * 64, G, s, 11)
+    it = D.batches(D.stream_for(spec), batch)
+    asg = O.contiguous_assignment(G, P)
+    cfg = O.balancer_cfg(policy, max(1, batch // (10 * P)), 0.5)
+    store = O.OStore(G, W)
+    fn = O.POLICY_FNS[policy]
+    done, t_work, nb = 0, 0.0, 0
+    while t_work < seconds:
+        b = next(it)
+        t0 = time.perf_counter()
+        counts, tpt = O.histogram(b.groups, asg)
+        rg, ra, ind = O.place(b.groups, b.attrs, asg, counts, tpt)
+        v = fn(counts, tpt, asg, rg, ind, cfg)
+        store.ingest(rg, ra, assume_grouped=True)
+        asg = O.apply_move_list(asg, v.moves)
+        t_work += time.perf_counter() - t0
+        done += len(b)
+        nb += 1
+    return done / t_work, {"batches": nb, "batch": batch, "tuples": done, "seconds": round(t_work, 2)}
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    name = args.config
+    desc = CONFIGS[name][0]
+    vals = []
+    total = 0
+    for _ in range(args.steps + args.warmup):
+        v, info = cpu_pipeline(name, seconds=max(2.0, args.cpu_seconds / max(1, args.steps)))
+        vals.append(v)
+        total += info["tuples"]
+    v = float(np.mean(vals[args.warmup:] or vals))
+    line = {
+        "impl": "reference", "metric": "sustained tuples/s (Zipf skew)", "value": v,
+        "unit": "tuples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "higher_is_better": True, "dtype": "i64", "data": "synthetic (reference generators)",
+        "config": {"workload": desc, "batch": 1 << 20, "partitions": P_DEFAULT},
+        "cpu_baseline": {"value": v, "unit": "tuples/s", "cores": 1, "kind": "port",
+                         "sample": f"{args.steps} steps x ~{max(2.0, args.cpu_seconds / max(1, args.steps)):.0f}s "
+                                   f"of 2^20-tuple batches through oracle/port.py (count, place, "
+                                   f"policy, ingest, apply) on {cpu_model()}"},
+        "e2e": {"value": v, "unit": "tuples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU path
+# ---------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--partitions", type=int, default=P_DEFAULT)
+    ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--sub-batch", type=int, default=0)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    from paper_1309_0634_b200 import _lib as L
+    from paper_1309_0634_b200.stream_engine import StreamEngine
+
+    desc, kind, s, G, W, B, aggs, policy, split = CONFIGS[args.config]
+    if args.batch:
+        B = args.batch
+    P = args.partitions
+    eng = StreamEngine(G, W, n_partitions=P, aggregates=aggs, device=local, max_batch=B,
+                       sub_batch=args.sub_batch)
+    stream = torch.cuda.Stream(device=dev)
+    eng.set_stream(stream)
+    thr = max(1, B // (10 * P))
+    bal = eng.balancer_struct(policy, thread_threshold=thr, pot=0.5)
+    nbuf = 4
+    batches = make_batches(kind, s, G, B, nbuf, dev, seed=1234 + rank)
+    torch.cuda.synchronize()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    def run_steps(k, start=0):
+        for i in range(k):
+            g, a = batches[(start + i) % nbuf]
+            eng.step(g, a, bal, sync=False)
+
+    # warm-up (also converges the balancer from the contiguous assignment)
+    for i in range(args.warmup):
+        run_steps(1, i)
+        eng.last_report()
+    lib = L.load()
+    import ctypes as C
+
+    # ---- (1) headline: staged batches in HBM -------------------------------
+    clocks = ClockSampler(local)
+    barrier()
+    clocks.start()
+    time.sleep(0.3)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    run_steps(args.steps, args.warmup)
+    ev1.record(stream)
+    ev1.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    clk = clocks.stop()
+    rep = eng.last_report()
+    ms_t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    value = B * args.steps * world / (ms / 1e3)
+
+    # ---- (2) kernel classes with CUDA events + algorithmic bytes --------------
+    lib.ss_profile(eng._h, 1)
+    kms = (C.c_double * 7)()
+    kn = (C.c_int64 * 7)()
+    lib.ss_profile_read(eng._h, kms, kn, 1)
+    ab = C.c_int64()
+    lib.ss_alg_bytes(eng._h, C.byref(ab), 1)
+    ratios = []
+    barrier()
+    for i in range(args.steps):
+        run_steps(1, args.warmup + i)
+        ratios.append(eng.last_report().load_ratio)
+    lib.ss_profile_read(eng._h, kms, kn, 1)
+    lib.ss_alg_bytes(eng._h, C.byref(ab), 1)
+    lib.ss_profile(eng._h, 0)
+    alg_per_step = ab.value / args.steps
+    peak, peak_kind = peaks()
+    cls_ms = {n: kms[i] / args.steps for i, n in enumerate(L.KERNEL_CLASSES)}
+    cls_launch = {n: kn[i] for i, n in enumerate(L.KERNEL_CLASSES)}
+    # algorithmic bytes per class and step
+    ingest_bytes = alg_per_step - 8 * B
+    cls_bytes = {"count": 4 * B, "place": 8 * B, "ingest": ingest_bytes}
+    main_cls = max(("count", "place", "ingest"), key=lambda n: cls_ms[n])
+    k_ms = cls_ms[main_cls]
+    achieved = cls_bytes[main_cls] / (k_ms / 1e3) / 1e9 if k_ms > 0 else 0.0
+    step_ms = ms / args.steps
+    path_achieved = alg_per_step / (step_ms / 1e3) / 1e9
+
+    # ---- (3) end to end through the public API with host buffers -------------
+    e2e_steps = args.e2e_steps or max(3, args.steps // 4)
+    hosts = []
+    for g, a in batches[:2]:
+        hg = torch.empty(B, dtype=torch.int32, pin_memory=True)
+        ha = torch.empty(B, dtype=torch.int32, pin_memory=True)
+        hg.copy_(g)
+        ha.copy_(a)
+        hosts.append((hg, ha))
+    res_g = np.empty(G, dtype=np.int32)
+    res_a = np.empty(G, dtype=np.float64)
+    res_n = C.c_int64()
+    d2h = 0
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    e0.record(stream)
+    for i in range(e2e_steps):
+        hg, ha = hosts[i % 2]
+        eng.step(hg, ha, bal, sync=False)
+        lib.ss_results_raw(eng._h, G, res_g.ctypes.data_as(C.c_void_p), res_a.ctypes.data_as(C.c_void_p),
+                           C.byref(res_n))
+        d2h += res_n.value * 12 + 4
+    e1.record(stream)
+    e1.synchronize()
+    e2e_wall = time.perf_counter() - t0
+    e2e_ms = max(e0.elapsed_time(e1), e2e_wall * 1e3)
+    e2e_value = B * e2e_steps * world / (e2e_ms / 1e3)
+
+    # ---- CPU baseline (rank 0, N=1 only) ----------------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        v, info = cpu_pipeline(args.config, seconds=args.cpu_seconds)
+        cpu = {"value": v, "unit": "tuples/s", "cores": 1, "kind": "port",
+               "sample": f"{info['batches']} batches x 2^20 tuples ({info['seconds']} s) of the same "
+                         f"stream shape through oracle/port.py on {cpu_model()}"}
+
+    # launches per step: count, batch_stats, 3 scans, balance (side), emit,
+    # 3 apply, report + per sub-batch (placement passes + ingest)
+    n_sub = -(-B // (eng_sub := (args.sub_batch or (1 << 21))))
+    npass = 1 if (G - 1).bit_length() <= 11 else 2
+    per_step = 1 + 1 + 3 + (1 if policy != "no" else 0) + 1 + (3 if policy != "no" else 0) + 1 \
+        + n_sub * (npass + 1)
+    if rank == 0:
+        line = {
+            "metric": "sustained tuples/s (Zipf skew)",
+            "value": value, "unit": "tuples/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "i32 keys/values, i64 sums",
+            "data": f"synthetic {kind} (s={s}) keys generated on device, uniform int32 attrs; "
+                    f"{nbuf} staged batches of {B * 8 >> 20} MB each (> L2), cycled",
+            "config": {"workload": desc, "groups": G, "window": W, "batch": B,
+                       "partitions": P, "policy": policy, "aggregates": list(aggs),
+                       "sub_batch": eng_sub, "l2": "inputs larger than L2 (128 MB per batch)",
+                       "parallelism": f"key-sharded x{world}" if world > 1 else "single GPU"},
+            "roofline": {"bound": "hbm", "kernel": main_cls, "achieved": achieved, "peak": peak,
+                         "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                         "peak_source": peak_kind,
+                         "alg_bytes_per_launch": cls_bytes[main_cls] / max(1, cls_launch[main_cls] / args.steps),
+                         "ms_per_step": k_ms},
+            "path_roofline": {"alg_bytes_per_tuple": alg_per_step / B, "achieved": path_achieved,
+                              "peak": peak, "unit": "GB/s", "frac": path_achieved / peak},
+            "kernel_ms_per_step": cls_ms,
+            "load_ratio": {"last": rep.load_ratio, "mean": float(np.mean(ratios)),
+                           "max": float(np.max(ratios))},
+            "moves_last_step": rep.moves,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "tuples/s", "h2d_bytes_per_step": 8 * B,
+                    "d2h_bytes_per_step": d2h // e2e_steps, "steps": e2e_steps},
+            "gpu_launches": per_step * args.steps,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

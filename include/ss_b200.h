@@ -155,6 +155,26 @@ int  ss_export_values(ss_engine* e, int64_t group, int64_t* out, int64_t cap, in
 int  ss_results(ss_engine* e, int64_t cap, int32_t* groups, int64_t* count, int64_t* sum,
                 double* avg, int32_t* mn, int32_t* mx, int64_t* n);
 
+/* ---- measurement ------------------------------------------------------
+ * Kernel classes timed with CUDA events on the engine stream while
+ * profiling is enabled (bench.py's roofline numbers). */
+#define SS_K_COUNT   0   /* k_count                                  */
+#define SS_K_STATS   1   /* k_batch_stats + k_scan_*                 */
+#define SS_K_PLACE   2   /* k_sort_pass (all passes)                 */
+#define SS_K_INGEST  3   /* k_ingest (+ reserve, finalize, rescan)   */
+#define SS_K_EMIT    4   /* k_emit                                   */
+#define SS_K_APPLY   5   /* k_apply_* + k_report                     */
+#define SS_K_BALANCE 6   /* k_balance (side stream)                  */
+#define SS_K_NCLASS  7
+int  ss_profile(ss_engine* e, int enable);
+/* summed milliseconds and launch counts per class since the last reset */
+int  ss_profile_read(ss_engine* e, double* ms, int64_t* launches, int reset);
+/* algorithmic HBM bytes of the steps since the last reset:
+ * B*(key+attr) + 4*sum min(k,W) + 4*sum_{k<W} max(0,f0+k-W) + 76*touched */
+int  ss_alg_bytes(ss_engine* e, int64_t* bytes, int reset);
+/* raw per-batch emission (no ordering): group id and AVG of each touched group */
+int  ss_results_raw(ss_engine* e, int64_t cap, int32_t* groups, double* avg, int64_t* n);
+
 #ifdef __cplusplus
 }
 #endif

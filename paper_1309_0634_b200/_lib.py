@@ -73,7 +73,12 @@ _SIGS = {
     "ss_snapshot": (C.c_int, [_P, _P, _P, _P, _P, _P, _P]),
     "ss_export_values": (C.c_int, [_P, _I64, _P, _I64, _P]),
     "ss_results": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _P, _P]),
+    "ss_profile": (C.c_int, [_P, C.c_int]),
+    "ss_profile_read": (C.c_int, [_P, _P, _P, C.c_int]),
+    "ss_alg_bytes": (C.c_int, [_P, _P, C.c_int]),
+    "ss_results_raw": (C.c_int, [_P, _I64, _P, _P, _P]),
 }
+KERNEL_CLASSES = ("count", "stats", "place", "ingest", "emit", "apply", "balance")
 EXPORTS = tuple(_SIGS)
 
 _lib = None

@@ -45,6 +45,8 @@ struct BalanceArgs {
     long long* scanned;
     long long* final_tpt;       // [P]
     const unsigned long long* bad;
+    const unsigned long long* init_loads;   // split mode: cold-only loads (else tpt)
+    const uint8_t* exclude;                 // split mode: hot groups never move
 };
 
 struct BalSmem {
@@ -201,7 +203,7 @@ k_balance(BalanceArgs a) {
         return;
     }
     for (int p = threadIdx.x; p < P; p += blockDim.x) {
-        s.loads[p] = (long long)a.tpt[p];
+        s.loads[p] = (long long)(a.init_loads ? a.init_loads[p] : a.tpt[p]);
         s.ftop[p] = s.fbot[p] = s.bfirst[p] = s.blast[p] = -1;
         s.elo[p] = a.offsets[p];
         s.ehi[p] = a.offsets[p + 1];
@@ -244,7 +246,7 @@ k_balance(BalanceArgs a) {
                 const long long dmax = s.loads[hi], dmin = s.loads[lo];
                 for (int i = e0 + threadIdx.x; i < e1; i += blockDim.x) {
                     const int g = a.order[i];
-                    if (a.moved[g]) continue;
+                    if (a.moved[g] || (a.exclude && a.exclude[g])) continue;
                     const long long c = a.gcount[g];
                     long long key;
                     if (pol == 2) key = -c;      // max count, lowest id
@@ -280,7 +282,7 @@ k_balance(BalanceArgs a) {
                         if (i < e1) {
                             g = a.order[i];
                             c = a.gcount[g];
-                            const bool mv = a.moved[g];
+                            const bool mv = a.moved[g] || (a.exclude && a.exclude[g]);
                             cand = (c >= limit) && !mv;
                             if (!mv && c > 0) {
                                 const long long key = -c;

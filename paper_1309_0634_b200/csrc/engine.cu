@@ -30,6 +30,7 @@
 #include "partition.cuh"
 #include "window.cuh"
 #include "balance.cuh"
+#include "split.cuh"
 
 using namespace ss;
 
@@ -108,6 +109,15 @@ struct ss_engine {
 
     uint32_t* kbuf2 = nullptr;             // sorted keys (reorder only)
 
+    // hot-key split plans (split.cuh), double-buffered: plan[cur] executes
+    // batch t while the planner writes plan[cur ^ 1] for batch t+1
+    SplitPlan plan_buf[2]{};
+    SplitScratch spx{};
+    int plan_cur = 0;
+    bool plan_valid = false;
+    int last_plan = -1;        // plan buffer the last batch executed with
+    int maxS = 0, maxSh = 0;
+
     // emission / misc
     unsigned* n_res = nullptr;
     int32_t *r_g = nullptr, *r_cnt = nullptr, *r_mn = nullptr, *r_mx = nullptr;
@@ -119,8 +129,48 @@ struct ss_engine {
     unsigned long long* loads = nullptr;   // per-partition load incl. split shares
     DevReport* d_rep = nullptr;
     DevReport* h_rep = nullptr;            // pinned
+    unsigned long long* alg_bytes = nullptr;
+    long long alg_input = 0;
     std::vector<void*> allocs;
+
+    // kernel-class timing (bench.py)
+    struct ProfPair { int cls; cudaEvent_t a, b; };
+    bool prof = false;
+    std::vector<ProfPair> prof_pending;
+    std::vector<cudaEvent_t> ev_pool;
+    double prof_ms[SS_K_NCLASS] = {0};
+    int64_t prof_n[SS_K_NCLASS] = {0};
 };
+
+namespace {
+struct ProfScope {
+    ss_engine* e;
+    int cls;
+    cudaStream_t s;
+    cudaEvent_t a = nullptr;
+    ProfScope(ss_engine* e_, int c, cudaStream_t st) : e(e_), cls(c), s(st) {
+        if (!e->prof) return;
+        a = take();
+        cudaEventRecord(a, s);
+    }
+    cudaEvent_t take() {
+        if (e->ev_pool.empty()) {
+            cudaEvent_t x;
+            cudaEventCreate(&x);
+            return x;
+        }
+        cudaEvent_t x = e->ev_pool.back();
+        e->ev_pool.pop_back();
+        return x;
+    }
+    ~ProfScope() {
+        if (!e->prof) return;
+        cudaEvent_t b = take();
+        cudaEventRecord(b, s);
+        e->prof_pending.push_back({cls, a, b});
+    }
+};
+}  // namespace
 
 // --------------------------------------------------------------------------
 // helpers
@@ -210,6 +260,9 @@ __global__ void k_dense_off(int64_t* off, int32_t* cap, int64_t G, int64_t W) {
     }
 }
 __global__ void k_set_bad(unsigned long long* bad) { *bad = (unsigned long long)kNoBad; }
+__global__ void k_u64_to_i64(const unsigned long long* a, long long* b, int n) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) b[i] = (long long)a[i];
+}
 
 // map group ids to placement ranks (reorder_batch sorts by rank)
 __global__ void k_to_rank(const uint32_t* __restrict__ g, int64_t n, const int32_t* __restrict__ rank,
@@ -451,12 +504,40 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
         return rc;
     SS_CUDA(e, cudaMemsetAsync(e->n_moves, 0, 4, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->prev_moves, 0, 4, e->st));
+    // -- hot-key split plans
+    e->maxS = 2 * e->P + 2;
+    e->maxSh = e->P + e->maxS + 1;
+    for (int b = 0; b < 2; ++b) {
+        SplitPlan& sp = e->plan_buf[b];
+        if ((rc = dalloc(e, &sp.n_split, 1)) || (rc = dalloc(e, &sp.n_share, 1)) || (rc = dalloc(e, &sp.split_of, G)) ||
+            (rc = dalloc(e, &sp.split_g, e->maxS)) || (rc = dalloc(e, &sp.split_den, e->maxS)) ||
+            (rc = dalloc(e, &sp.part_soff, e->P + 1)) || (rc = dalloc(e, &sp.share_grp, e->maxSh)) ||
+            (rc = dalloc(e, &sp.share_lo, e->maxSh)) || (rc = dalloc(e, &sp.share_hi, e->maxSh)))
+            return rc;
+        SS_CUDA(e, cudaMemsetAsync(sp.n_split, 0, 4, e->st));
+        SS_CUDA(e, cudaMemsetAsync(sp.n_share, 0, 4, e->st));
+        SS_CUDA(e, cudaMemsetAsync(sp.split_of, 0xff, G * 4, e->st));
+        SS_CUDA(e, cudaMemsetAsync(sp.part_soff, 0, (e->P + 1) * 4, e->st));
+    }
+    if ((rc = dalloc(e, &e->spx.hot_g, e->maxS)) || (rc = dalloc(e, &e->spx.n_hot, 1)) ||
+        (rc = dalloc(e, &e->spx.base, e->P)) || (rc = dalloc(e, &e->spx.hot_flag, G)) ||
+        (rc = dalloc(e, &e->spx.split_delta, e->maxS)) || (rc = dalloc(e, &e->spx.split_min, e->maxS)) ||
+        (rc = dalloc(e, &e->spx.split_max, e->maxS)))
+        return rc;
+    SS_CUDA(e, cudaMemsetAsync(e->spx.split_delta, 0, e->maxS * 8, e->st));
+    {
+        std::vector<int32_t> lo(e->maxS, 0x7fffffff), hi(e->maxS, (int32_t)0x80000000);
+        SS_CUDA(e, cudaMemcpy(e->spx.split_min, lo.data(), e->maxS * 4, cudaMemcpyHostToDevice));
+        SS_CUDA(e, cudaMemcpy(e->spx.split_max, hi.data(), e->maxS * 4, cudaMemcpyHostToDevice));
+    }
     // -- emission
     if ((rc = dalloc(e, &e->n_res, 1)) || (rc = dalloc(e, &e->r_g, G)) || (rc = dalloc(e, &e->r_cnt, G)) ||
         (rc = dalloc(e, &e->r_sum, G)) || (rc = dalloc(e, &e->r_avg, G)) || (rc = dalloc(e, &e->r_mn, G)) ||
         (rc = dalloc(e, &e->r_mx, G)) || (rc = dalloc(e, &e->rescan, G)) || (rc = dalloc(e, &e->n_rescan, 1)) ||
-        (rc = dalloc(e, &e->part_ns, e->P)) || (rc = dalloc(e, &e->loads, e->P)) || (rc = dalloc(e, &e->d_rep, 1)))
+        (rc = dalloc(e, &e->part_ns, e->P)) || (rc = dalloc(e, &e->loads, e->P)) || (rc = dalloc(e, &e->d_rep, 1)) ||
+        (rc = dalloc(e, &e->alg_bytes, 1)))
         return rc;
+    SS_CUDA(e, cudaMemsetAsync(e->alg_bytes, 0, 8, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->n_res, 0, 4, e->st));
     SS_CUDA(e, cudaMallocHost(&e->h_rep, sizeof(DevReport)));
     memset(e->h_rep, 0, sizeof(DevReport));
@@ -464,6 +545,7 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
     SS_CUDA(e, cudaFuncSetAttribute(k_count<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     SS_CUDA(e, cudaFuncSetAttribute(k_ingest, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kIngestSmem));
     SS_CUDA(e, cudaFuncSetAttribute(k_balance, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    SS_CUDA(e, cudaFuncSetAttribute(k_split_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     SS_CUDA(e, cudaStreamSynchronize(e->st));
     return SS_OK;
 }
@@ -528,11 +610,14 @@ static int data_error(ss_engine* e, unsigned long long idx, const uint32_t* dkey
 static int launch_count(ss_engine* e, const uint32_t* dk, int64_t n, int64_t S) {
     if (n == 0) return SS_OK;
     const int vec_ok = ((uintptr_t)dk % 16) == 0;
-    const int64_t grid = (n + kCountChunk - 1) / kCountChunk;
     if (e->G <= 16384) {
-        k_count<true><<<(unsigned)grid, 512, e->G * 4, e->st>>>(dk, n, (uint32_t)e->G, S, kCountChunk, e->gcnt,
+        // larger chunks amortise the per-CTA flush of the G-bin histogram
+        const int64_t chunk = (e->G > 2048 && S % 65536 == 0) ? 65536 : kCountChunk;
+        const int64_t grid = (n + chunk - 1) / chunk;
+        k_count<true><<<(unsigned)grid, 512, e->G * 4, e->st>>>(dk, n, (uint32_t)e->G, S, chunk, e->gcnt,
                                                                e->bad, vec_ok);
     } else {
+        const int64_t grid = (n + kCountChunk - 1) / kCountChunk;
         k_count<false><<<(unsigned)grid, 512, 0, e->st>>>(dk, n, (uint32_t)e->G, S, kCountChunk, e->gcnt, e->bad,
                                                          vec_ok);
     }
@@ -544,7 +629,8 @@ static int launch_stats(ss_engine* e, int n_sub) {
     SS_CUDA(e, cudaMemsetAsync(e->tpt, 0, e->P * 8, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->touched, 0, 8, e->st));
     k_batch_stats<<<2 * kNumSM, 1024, e->P * 8, e->st>>>(e->gcnt, n_sub, (uint32_t)e->G, e->pmap, e->P, e->gcount,
-                                                          e->tpt, e->touched, e->bad);
+                                                          e->tpt, e->touched, e->bad, e->fill, e->W,
+                                                          e->alg_bytes);
     SS_CUDA(e, cudaGetLastError());
     return SS_OK;
 }
@@ -590,7 +676,7 @@ static int launch_place(ss_engine* e, int s, const uint32_t* dk, const int32_t* 
     return SS_OK;
 }
 
-static IngestArgs ingest_args(ss_engine* e, int s) {
+static IngestArgs ingest_args(ss_engine* e, int s, bool with_plan) {
     IngestArgs a{};
     a.order = e->order;
     a.offsets = e->offsets;
@@ -606,6 +692,20 @@ static IngestArgs ingest_args(ss_engine* e, int s) {
     a.ring = e->ring;
     a.W = e->W;
     a.minmax = e->minmax;
+    if (with_plan) {
+        const SplitPlan& sp = e->plan_buf[e->plan_cur];
+        a.split_of = sp.split_of;
+        a.share_off = sp.part_soff;
+        a.share_grp = sp.share_grp;
+        a.share_lo = sp.share_lo;
+        a.share_hi = sp.share_hi;
+        a.split_g = sp.split_g;
+        a.split_den = sp.split_den;
+        a.n_split = sp.n_split;
+        a.split_delta = e->spx.split_delta;
+        a.split_min = e->spx.split_min;
+        a.split_max = e->spx.split_max;
+    }
     a.rescan = e->rescan;
     a.n_rescan = e->n_rescan;
     a.part_ns = e->part_ns;
@@ -613,76 +713,143 @@ static IngestArgs ingest_args(ss_engine* e, int s) {
     return a;
 }
 
+static int move_cap(ss_engine* e, const ss_balancer* b);
+
 // count -> stats -> [policy] -> scans -> per sub-batch (reserve, place,
 // ingest, finalize) -> [emit] -> [apply]
 static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_t n, const ss_balancer* bal,
                      bool emit) {
     const int n_sub = (int)std::max<int64_t>(1, (n + e->S - 1) / e->S);
     int rc;
-    const bool has_policy = bal && bal->policy != SS_POLICY_NO;
+    const bool split = bal && bal->split;
+    // split mode: cold groups move by the configured extreme-pair policy
+    // (first/shift variants fall back to best_balance), hot groups are
+    // water-filled; without split, the reference policy runs unchanged
+    int pol = bal ? bal->policy : SS_POLICY_NO;
+    if (split && pol != SS_POLICY_NO && pol != SS_POLICY_ALL && pol != SS_POLICY_PROB && pol != SS_POLICY_BEST)
+        pol = SS_POLICY_BEST;
+    const bool has_policy = pol != SS_POLICY_NO;
+    const bool run_side = has_policy || split;
+    const bool use_plan = e->plan_valid;   // decided by the previous batch
+    e->last_plan = use_plan ? e->plan_cur : -1;
     SS_CUDA(e, cudaMemsetAsync(e->tickets, 0, (size_t)n_sub * 2 * 4, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->part_ns, 0, e->P * 8, e->st));
     if (emit) SS_CUDA(e, cudaMemsetAsync(e->n_res, 0, 4, e->st));
-    if ((rc = launch_count(e, dk, n, e->S))) return rc;
-    if ((rc = launch_stats(e, n_sub))) return rc;
-    if (has_policy) {
-        BalanceArgs a{};
-        a.policy = bal->policy;
-        a.threshold = bal->thread_threshold;
-        a.pot = bal->pot;
-        a.cap = (int)std::min<int64_t>(bal->max_moves > 0 ? bal->max_moves : 4LL * e->P, e->cap_moves);
-        a.P = e->P;
-        a.order = e->order;
-        a.offsets = e->offsets;
-        a.gcount = e->gcount;
-        a.tpt = e->tpt;
-        a.moved = e->moved;
-        a.moves = e->moves;
-        a.front_top = e->front_top;
-        a.back_first = e->back_first;
-        a.mv_next = e->mv_next;
-        a.n_moves = e->n_moves;
-        a.scanned = e->scanned;
-        a.final_tpt = e->final_tpt;
-        a.bad = e->bad;
+    {
+        ProfScope ps(e, SS_K_COUNT, e->st);
+        if ((rc = launch_count(e, dk, n, e->S))) return rc;
+    }
+    {
+        ProfScope ps(e, SS_K_STATS, e->st);
+        if ((rc = launch_stats(e, n_sub))) return rc;
+        SS_CUDA(e, cudaMemsetAsync(e->loads, 0, e->P * 8, e->st));
+        if (use_plan)
+            k_split_loads<<<2 * kNumSM, 256, 0, e->st>>>(e->gcount, (uint32_t)e->G, e->pmap, e->P,
+                                                         e->plan_buf[e->plan_cur], e->loads, e->bad);
+    }
+    e->alg_input += 8 * n;
+    if (run_side) {
         SS_CUDA(e, cudaEventRecord(e->ev_stats, e->st));
         SS_CUDA(e, cudaStreamWaitEvent(e->side, e->ev_stats, 0));
-        k_balance<<<1, kBalThreads, (size_t)e->P * (8 + 8 * 4), e->side>>>(a);
+        ProfScope ps(e, SS_K_BALANCE, e->side);
+        if (split) {
+            SS_CUDA(e, cudaMemsetAsync(e->spx.base, 0, e->P * 8, e->side));
+            SS_CUDA(e, cudaMemsetAsync(e->spx.n_hot, 0, 4, e->side));
+            const long long hot_min = std::max<long long>(1, n / (2LL * e->P));
+            k_split_hot<<<2 * kNumSM, 256, 0, e->side>>>(e->gcount, (uint32_t)e->G, e->pmap, hot_min, e->maxS, e->spx,
+                                                         e->bad);
+        }
+        if (has_policy) {
+            BalanceArgs a{};
+            a.policy = pol;
+            a.threshold = bal->thread_threshold;
+            a.pot = bal->pot;
+            a.cap = move_cap(e, bal);
+            a.P = e->P;
+            a.order = e->order;
+            a.offsets = e->offsets;
+            a.gcount = e->gcount;
+            a.tpt = e->tpt;
+            a.moved = e->moved;
+            a.moves = e->moves;
+            a.front_top = e->front_top;
+            a.back_first = e->back_first;
+            a.mv_next = e->mv_next;
+            a.n_moves = e->n_moves;
+            a.scanned = e->scanned;
+            a.final_tpt = e->final_tpt;
+            a.bad = e->bad;
+            if (split) {
+                a.init_loads = e->spx.base;
+                a.exclude = e->spx.hot_flag;
+            }
+            k_balance<<<1, kBalThreads, (size_t)e->P * (8 + 8 * 4), e->side>>>(a);
+        }
+        if (split) {
+            const SplitPlan& nx = e->plan_buf[e->plan_cur ^ 1];
+            const long long* fl = has_policy ? e->final_tpt : nullptr;
+            if (!has_policy) {
+                k_u64_to_i64<<<1, 1024, 0, e->side>>>(e->spx.base, e->final_tpt, e->P);
+                fl = e->final_tpt;
+            }
+            const size_t smem = (size_t)e->maxS * 20 + 16 + (size_t)(e->P + 1) * 4;
+            k_split_fill<<<1, 1024, smem, e->side>>>(e->gcount, fl, e->P, e->maxS, e->spx, nx, nx, e->bad);
+        }
         SS_CUDA(e, cudaGetLastError());
         SS_CUDA(e, cudaEventRecord(e->ev_bal, e->side));
     }
-    if ((rc = launch_scans(e, n_sub))) return rc;
+    {
+        ProfScope ps(e, SS_K_STATS, e->st);
+        if ((rc = launch_scans(e, n_sub))) return rc;
+    }
     for (int s = 0; s < n_sub; ++s) {
         const int64_t lo = (int64_t)s * e->S;
         const int64_t ns = std::min<int64_t>(e->S, n - lo);
         if (ns <= 0) break;
-        if (!e->dense) {
-            k_reserve<<<2 * kNumSM, 256, 0, e->st>>>(e->gcnt + (int64_t)s * e->G, (uint32_t)e->G, e->W, e->fill,
-                                                     e->off, e->cap, e->ring, e->pool_top, e->pool_cap, e->oom,
-                                                     e->bad);
+        {
+            ProfScope ps(e, SS_K_PLACE, e->st);
+            if ((rc = launch_place(e, s, dk + lo, dv + lo, ns, false, true))) return rc;
         }
-        if ((rc = launch_place(e, s, dk + lo, dv + lo, ns, false, true))) return rc;
-        if (e->minmax) SS_CUDA(e, cudaMemsetAsync(e->n_rescan, 0, 4, e->st));
-        IngestArgs a = ingest_args(e, s);
-        k_ingest<<<e->P, kIngestThreads, kIngestSmem, e->st>>>(a);
-        if (e->minmax)
-            k_minmax_rescan<<<2 * kNumSM, 256, 0, e->st>>>(e->rescan, e->n_rescan, e->ring, e->off, e->W, e->mn, e->mx);
+        {
+            ProfScope ps(e, SS_K_INGEST, e->st);
+            if (!e->dense) {
+                k_reserve<<<2 * kNumSM, 256, 0, e->st>>>(e->gcnt + (int64_t)s * e->G, (uint32_t)e->G, e->W, e->fill,
+                                                         e->off, e->cap, e->ring, e->pool_top, e->pool_cap, e->oom,
+                                                         e->bad);
+            }
+            if (e->minmax) SS_CUDA(e, cudaMemsetAsync(e->n_rescan, 0, 4, e->st));
+            IngestArgs a = ingest_args(e, s, use_plan);
+            k_ingest<<<e->P, kIngestThreads, kIngestSmem, e->st>>>(a);
+            if (use_plan) k_split_finalize<<<(e->maxS + 255) / 256, 256, 0, e->st>>>(a);
+            if (e->minmax)
+                k_minmax_rescan<<<2 * kNumSM, 256, 0, e->st>>>(e->rescan, e->n_rescan, e->ring, e->off, e->W, e->mn,
+                                                               e->mx);
+        }
         SS_CUDA(e, cudaGetLastError());
     }
+    // the balancer reads gcount: join it before the emission clears it
+    if (run_side) SS_CUDA(e, cudaStreamWaitEvent(e->st, e->ev_bal, 0));
     if (emit) {
+        ProfScope ps(e, SS_K_EMIT, e->st);
         k_emit<<<2 * kNumSM, 256, 0, e->st>>>(e->gcount, (uint32_t)e->G, e->fill, e->wsum, e->mn, e->mx, e->minmax,
                                               e->n_res, e->r_g, e->r_cnt, e->r_sum, e->r_avg, e->r_mn, e->r_mx, e->bad);
     } else {
         SS_CUDA(e, cudaMemsetAsync(e->gcount, 0, e->G * 4, e->st));
     }
     if (has_policy) {
-        SS_CUDA(e, cudaStreamWaitEvent(e->st, e->ev_bal, 0));
+        ProfScope ps(e, SS_K_APPLY, e->st);
         k_apply_sizes<<<1, 1024, 0, e->st>>>(e->offsets, e->P, e->moves, e->n_moves, e->new_off);
         k_apply_build<<<e->P, 256, 0, e->st>>>(e->order, e->offsets, e->new_off, e->moves, e->n_moves, e->front_top,
                                                e->back_first, e->mv_next, e->moved, e->new_order);
         k_apply_commit<<<2 * kNumSM, 256, 0, e->st>>>(e->order, e->offsets, e->new_order, e->new_off, (int)e->G, e->P,
                                                       e->moves, e->n_moves, e->pmap, e->moved);
         SS_CUDA(e, cudaGetLastError());
+    }
+    if (split) {
+        e->plan_cur ^= 1;
+        e->plan_valid = true;
+    } else {
+        e->plan_valid = false;
     }
     return SS_OK;
 }
@@ -691,8 +858,10 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
 // report
 // --------------------------------------------------------------------------
 static int enqueue_report(ss_engine* e, int64_t n, bool has_policy) {
-    k_report<<<1, 1024, 0, e->st>>>(e->tpt, nullptr, e->P, e->bad, e->touched, e->n_moves, e->prev_moves,
-                                    e->scanned, nullptr, e->n_res, e->oom, (long long)n, has_policy ? 1 : 0,
+    const bool used_plan = e->last_plan >= 0;
+    k_report<<<1, 1024, 0, e->st>>>(e->tpt, used_plan ? e->loads : nullptr, e->P, e->bad, e->touched, e->n_moves, e->prev_moves,
+                                    e->scanned, used_plan ? e->plan_buf[e->last_plan].n_split : nullptr,
+                                    e->n_res, e->oom, (long long)n, has_policy ? 1 : 0,
                                     e->d_rep);
     SS_CUDA(e, cudaGetLastError());
     SS_CUDA(e, cudaMemcpyAsync(e->h_rep, e->d_rep, sizeof(DevReport), cudaMemcpyDeviceToHost, e->st));
@@ -723,6 +892,22 @@ static void fill_report(const ss_engine* e, ss_step_report* r) {
     r->load_ratio = (d.tuples > 0) ? (double)d.max_load / r->mean_load : 0.0;
 }
 
+static int ensure_moves(ss_engine* e, int64_t want) {
+    want = std::min<int64_t>(want, e->G);
+    if (want <= e->cap_moves) return SS_OK;
+    SS_CUDA(e, cudaStreamSynchronize(e->st));
+    SS_CUDA(e, cudaStreamSynchronize(e->side));
+    int rc;
+    if ((rc = dalloc(e, &e->moves, want)) || (rc = dalloc(e, &e->mv_next, want))) return rc;
+    e->cap_moves = (int)want;
+    return SS_OK;
+}
+
+static int move_cap(ss_engine* e, const ss_balancer* b) {
+    const int64_t want = b->max_moves > 0 ? b->max_moves : 4LL * e->P;
+    return (int)std::min<int64_t>(want, e->cap_moves);
+}
+
 static int check_balancer(ss_engine* e, const ss_balancer* b) {
     if (!b) return SS_OK;
     if (b->policy < SS_POLICY_NO || b->policy > SS_POLICY_SHIFTLOCAL)
@@ -730,7 +915,7 @@ static int check_balancer(ss_engine* e, const ss_balancer* b) {
     if (b->thread_threshold < 1) return fail(e, SS_E_CONFIG, "thread_threshold must be >= 1");
     if (!(b->pot > 0.0 && b->pot <= 1.0)) return fail(e, SS_E_CONFIG, "pot must be in (0, 1]");
     if (b->max_moves < 0) return fail(e, SS_E_CONFIG, "max_moves must be >= 1 (0 = default)");
-    return SS_OK;
+    return ensure_moves(e, b->max_moves > 0 ? b->max_moves : 4LL * e->P);
 }
 
 // --------------------------------------------------------------------------
@@ -913,6 +1098,7 @@ extern "C" int ss_ingest(ss_engine* e, const uint32_t* groups, const int32_t* at
     const int32_t* dv;
     int rc;
     if ((rc = stage_input(e, groups, attrs, n, &dk, &dv))) return rc;
+    e->last_plan = -1;
     if ((rc = run_batch(e, dk, dv, n, nullptr, false))) return rc;
     if ((rc = enqueue_report(e, n, false))) return rc;
     return check_report(e, dk);
@@ -940,7 +1126,7 @@ extern "C" int ss_balance(ss_engine* e, const uint32_t* groups, int64_t n, const
         a.policy = cfg->policy;
         a.threshold = cfg->thread_threshold;
         a.pot = cfg->pot;
-        a.cap = (int)std::min<int64_t>(cfg->max_moves > 0 ? cfg->max_moves : 4LL * e->P, e->cap_moves);
+        a.cap = move_cap(e, cfg);
         a.P = e->P;
         a.order = e->order;
         a.offsets = e->offsets;
@@ -992,6 +1178,7 @@ extern "C" int ss_step(ss_engine* e, const uint32_t* groups, const int32_t* attr
     if ((rc = stage_input(e, groups, attrs, n, &dk, &dv))) return rc;
     g_last_keys = dk;
     const bool has_policy = cfg && cfg->policy != SS_POLICY_NO;
+    e->last_plan = -1;
     if (n > 0 && (rc = run_batch(e, dk, dv, n, cfg, true))) return rc;
     if (n == 0) {
         SS_CUDA(e, cudaMemsetAsync(e->tpt, 0, e->P * 8, e->st));
@@ -1020,7 +1207,7 @@ extern "C" int ss_last_loads(ss_engine* e, int64_t* loads) {
     if (!e || !loads) return SS_E_CONFIG;
     std::vector<unsigned long long> t(e->P);
     SS_CUDA(e, cudaStreamSynchronize(e->st));
-    SS_CUDA(e, cudaMemcpy(t.data(), e->tpt, e->P * 8, cudaMemcpyDeviceToHost));
+    SS_CUDA(e, cudaMemcpy(t.data(), e->last_plan >= 0 ? e->loads : e->tpt, e->P * 8, cudaMemcpyDeviceToHost));
     for (int p = 0; p < e->P; ++p) loads[p] = (int64_t)t[p];
     return SS_OK;
 }
@@ -1114,5 +1301,61 @@ extern "C" int ss_results(ss_engine* e, int64_t cap, int32_t* groups, int64_t* c
         if (mn) mn[i] = e->minmax ? rmn[k] : 0;
         if (mx) mx[i] = e->minmax ? rmx[k] : 0;
     }
+    return SS_OK;
+}
+
+// --------------------------------------------------------------------------
+// measurement
+// --------------------------------------------------------------------------
+extern "C" int ss_profile(ss_engine* e, int enable) {
+    if (!e) return SS_E_CONFIG;
+    e->prof = enable != 0;
+    return SS_OK;
+}
+
+extern "C" int ss_profile_read(ss_engine* e, double* ms, int64_t* launches, int reset) {
+    if (!e) return SS_E_CONFIG;
+    SS_CUDA(e, cudaStreamSynchronize(e->st));
+    SS_CUDA(e, cudaStreamSynchronize(e->side));
+    for (auto& p : e->prof_pending) {
+        float t = 0.f;
+        SS_CUDA(e, cudaEventElapsedTime(&t, p.a, p.b));
+        e->prof_ms[p.cls] += t;
+        e->prof_n[p.cls] += 1;
+        e->ev_pool.push_back(p.a);
+        e->ev_pool.push_back(p.b);
+    }
+    e->prof_pending.clear();
+    for (int c = 0; c < SS_K_NCLASS; ++c) {
+        if (ms) ms[c] = e->prof_ms[c];
+        if (launches) launches[c] = e->prof_n[c];
+        if (reset) { e->prof_ms[c] = 0; e->prof_n[c] = 0; }
+    }
+    return SS_OK;
+}
+
+extern "C" int ss_alg_bytes(ss_engine* e, int64_t* bytes, int reset) {
+    if (!e) return SS_E_CONFIG;
+    unsigned long long b = 0;
+    SS_CUDA(e, cudaStreamSynchronize(e->st));
+    SS_CUDA(e, cudaMemcpy(&b, e->alg_bytes, 8, cudaMemcpyDeviceToHost));
+    if (bytes) *bytes = (int64_t)b + e->alg_input;
+    if (reset) {
+        SS_CUDA(e, cudaMemset(e->alg_bytes, 0, 8));
+        e->alg_input = 0;
+    }
+    return SS_OK;
+}
+
+extern "C" int ss_results_raw(ss_engine* e, int64_t cap, int32_t* groups, double* avg, int64_t* n) {
+    if (!e) return SS_E_CONFIG;
+    unsigned nr = 0;
+    SS_CUDA(e, cudaMemcpyAsync(&nr, e->n_res, 4, cudaMemcpyDeviceToHost, e->st));
+    SS_CUDA(e, cudaStreamSynchronize(e->st));
+    if (n) *n = nr;
+    const int64_t m = std::min<int64_t>(cap, nr);
+    if (m > 0 && groups) SS_CUDA(e, cudaMemcpyAsync(groups, e->r_g, m * 4, cudaMemcpyDeviceToHost, e->st));
+    if (m > 0 && avg) SS_CUDA(e, cudaMemcpyAsync(avg, e->r_avg, m * 8, cudaMemcpyDeviceToHost, e->st));
+    SS_CUDA(e, cudaStreamSynchronize(e->st));
     return SS_OK;
 }

@@ -88,12 +88,14 @@ k_count(const uint32_t* __restrict__ groups, int64_t n, uint32_t G, int64_t S, i
 __global__ void __launch_bounds__(1024)
 k_batch_stats(const int32_t* __restrict__ gcnt, int n_sub, uint32_t G, const int32_t* __restrict__ pmap,
               int P, int32_t* __restrict__ gcount, unsigned long long* __restrict__ tpt,
-              unsigned long long* __restrict__ touched, const unsigned long long* __restrict__ bad) {
+              unsigned long long* __restrict__ touched, const unsigned long long* __restrict__ bad,
+              const int32_t* __restrict__ fill, int64_t W, unsigned long long* __restrict__ alg_bytes) {
     extern __shared__ unsigned long long sh_tpt[];
     if (*bad != (unsigned long long)kNoBad) return;
     for (int p = threadIdx.x; p < P; p += blockDim.x) sh_tpt[p] = 0;
     __syncthreads();
     uint32_t my_touched = 0;
+    unsigned long long my_bytes = 0;
     for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < G; g += gridDim.x * blockDim.x) {
         int32_t c = 0;
         for (int s = 0; s < n_sub; ++s) c += gcnt[(int64_t)s * G + g];
@@ -101,10 +103,19 @@ k_batch_stats(const int32_t* __restrict__ gcnt, int n_sub, uint32_t G, const int
         if (c) {
             atomicAdd(&sh_tpt[pmap[g]], (unsigned long long)c);
             ++my_touched;
+            // algorithmic bytes: stored values, retracted old
+            // values that must be read, state + result row
+            const int64_t f0 = fill[g];
+            my_bytes += 4ull * (unsigned long long)min64(c, W) + 76ull;
+            if (c < W) my_bytes += 4ull * (unsigned long long)max64(0, f0 + c - W);
         }
     }
     my_touched = warp_sum(my_touched);
-    if (lane_id() == 0 && my_touched) atomicAdd(touched, (unsigned long long)my_touched);
+    my_bytes = warp_sum(my_bytes);
+    if (lane_id() == 0 && my_touched) {
+        atomicAdd(touched, (unsigned long long)my_touched);
+        atomicAdd(alg_bytes, my_bytes);
+    }
     __syncthreads();
     for (int p = threadIdx.x; p < P; p += blockDim.x)
         if (sh_tpt[p]) atomicAdd(&tpt[p], sh_tpt[p]);

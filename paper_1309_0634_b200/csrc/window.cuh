@@ -20,7 +20,8 @@
 
 namespace ss {
 
-constexpr int kIngestThreads = 512;
+constexpr int kIngestThreads = 1024;
+constexpr int kILP = 8;                      // stored values in flight per thread
 constexpr int kMemberChunk = 2048;          // members staged per CTA round
 constexpr int kMPT = kMemberChunk / kIngestThreads;
 constexpr size_t kIngestSmem = (size_t)kMemberChunk * (8 + 8 + 4 * 8) + 16;
@@ -43,9 +44,11 @@ struct IngestArgs {
     const int32_t* split_of;    // >= 0: group executed as split shares (K5 finalises)
     const int32_t* share_off;   // [P+1] split shares of each partition
     const int32_t* share_grp;   // split-group index per share
-    const int32_t* share_idx;   // share number within the group
+    const long long* share_lo;  // run slice [k*lo/den, k*hi/den) of the share
+    const long long* share_hi;
     const int32_t* split_g;     // split-group index -> group
-    const int32_t* split_n;     // split-group index -> number of shares
+    const long long* split_den; // split-group index -> planned count
+    const int* n_split;
     unsigned long long* split_delta;   // per split-group delta (K5)
     int32_t* split_min;
     int32_t* split_max;
@@ -110,10 +113,10 @@ k_ingest(IngestArgs a) {
                     const int sh = s_lo + (it - (hi - lo));
                     const int sg = a.share_grp[sh];
                     g = a.split_g[sg];
-                    const int kt = a.gcnt[g], ns = a.split_n[sg], si = a.share_idx[sh];
-                    kb = (int)(((int64_t)kt * si) / ns);
-                    const int ke = (int)(((int64_t)kt * (si + 1)) / ns);
-                    k = ke - kb;                    // this share's slice of the run
+                    const int kt = a.gcnt[g];
+                    const long long den = a.split_den[sg];
+                    kb = (int)((long long)kt * a.share_lo[sh] / den);
+                    const int ke = (int)((long long)kt * a.share_hi[sh] / den);
                     // the slice is [kb, ke) of a run of kt; stored part is j >= kt - W
                     const int w0 = max(kb, kt - W);
                     k = max(0, ke - w0);
@@ -163,44 +166,69 @@ k_ingest(IngestArgs a) {
         if (threadIdx.x == 0) m_scan[m] = total;
         __syncthreads();
 
-        // ---- exchange: one stored value per thread-iteration ----------------
-        const int iters = (total + kIngestThreads - 1) / kIngestThreads;
-        for (int it = 0; it < iters; ++it) {
-            const int t = it * kIngestThreads + threadIdx.x;
-            const bool valid = t < total;
-            int mi = 0;
-            long long d = 0;
-            int32_t v = 0;
-            if (valid) {
-                // last member with m_scan[mi] <= t
-                int l = 0, r = m - 1;
-                while (l < r) {
-                    const int mid = (l + r + 1) >> 1;
-                    if (m_scan[mid] <= t) l = mid; else r = mid - 1;
+        // ---- exchange: kILP stored values per thread per round, all loads
+        // issued before any store (distinct slots within a round) -----------
+        for (int base = 0; base < total; base += kIngestThreads * kILP) {
+            int mi[kILP];
+            int32_t v[kILP], old[kILP];
+            int64_t cell[kILP];
+#pragma unroll
+            for (int u = 0; u < kILP; ++u) {
+                const int t = base + u * kIngestThreads + threadIdx.x;
+                mi[u] = -1;
+                if (t < total) {
+                    // last member with m_scan[l] <= t; fixed trip count so the
+                    // kILP searches interleave
+                    int l = 0;
+#pragma unroll
+                    for (int step = kMemberChunk / 2; step >= 1; step >>= 1) {
+                        const int c = l + step;
+                        if (c < m && m_scan[c] <= t) l = c;
+                    }
+                    mi[u] = l;
                 }
-                mi = l;
-                const int rr = t - m_scan[mi];
-                v = a.vals[m_start[mi] + rr];
-                int q = m_q0[mi] + rr;  if (q >= W) q -= W;
-                int sl = m_s0[mi] + rr; if (sl >= W) sl -= W;
-                int32_t* cell = a.ring + m_off[mi] + sl;
-                const int32_t old = (q < m_f0[mi]) ? *cell : 0;
-                *cell = v;
-                d = (long long)v - (long long)old;
             }
-            const unsigned key = valid ? (unsigned)mi : 0xffffffffu;
-            const unsigned peers = __match_any_sync(SS_FULL, key);
-            const unsigned seg_end = 31u - __clz(peers);
-            const long long tot = seg_sum(d, seg_end);
-            if (valid && lane == (unsigned)(__ffs(peers) - 1)) {
-                atomicAdd(&m_delta[mi], (unsigned long long)tot);
+#pragma unroll
+            for (int u = 0; u < kILP; ++u) {
+                if (mi[u] >= 0) {
+                    const int t = base + u * kIngestThreads + threadIdx.x;
+                    const int rr = t - m_scan[mi[u]];
+                    v[u] = a.vals[m_start[mi[u]] + rr];
+                    int sl = m_s0[mi[u]] + rr;
+                    if (sl >= W) sl -= W;
+                    cell[u] = m_off[mi[u]] + sl;
+                }
             }
-            if (a.minmax && valid) {
-                const int32_t mnv = __reduce_min_sync(peers, v);
-                const int32_t mxv = __reduce_max_sync(peers, v);
-                if (lane == (unsigned)(__ffs(peers) - 1)) {
-                    atomicMin(&m_min[mi], mnv);
-                    atomicMax(&m_max[mi], mxv);
+#pragma unroll
+            for (int u = 0; u < kILP; ++u) {
+                old[u] = 0;
+                if (mi[u] >= 0) {
+                    const int t = base + u * kIngestThreads + threadIdx.x;
+                    int q = m_q0[mi[u]] + (t - m_scan[mi[u]]);
+                    if (q >= W) q -= W;
+                    if (q < m_f0[mi[u]]) old[u] = a.ring[cell[u]];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kILP; ++u)
+                if (mi[u] >= 0) a.ring[cell[u]] = v[u];
+#pragma unroll
+            for (int u = 0; u < kILP; ++u) {
+                const bool valid = mi[u] >= 0;
+                const long long d = valid ? (long long)v[u] - (long long)old[u] : 0;
+                const unsigned key = valid ? (unsigned)mi[u] : 0xffffffffu;
+                const unsigned peers = __match_any_sync(SS_FULL, key);
+                const unsigned seg_end = 31u - __clz(peers);
+                const long long tot = seg_sum(d, seg_end);
+                const bool leader = valid && lane == (unsigned)(__ffs(peers) - 1);
+                if (leader) atomicAdd(&m_delta[mi[u]], (unsigned long long)tot);
+                if (a.minmax && valid) {
+                    const int32_t mnv = __reduce_min_sync(peers, v[u]);
+                    const int32_t mxv = __reduce_max_sync(peers, v[u]);
+                    if (leader) {
+                        atomicMin(&m_min[mi[u]], mnv);
+                        atomicMax(&m_max[mi[u]], mxv);
+                    }
                 }
             }
         }
@@ -245,9 +273,9 @@ k_ingest(IngestArgs a) {
 }
 
 // K5: finalise split groups after all their shares ran.  One thread each.
-__global__ void k_split_finalize(IngestArgs a, int n_split) {
+__global__ void k_split_finalize(IngestArgs a) {
     const int sg = blockIdx.x * blockDim.x + threadIdx.x;
-    if (sg >= n_split || *a.bad != (unsigned long long)kNoBad) return;
+    if (sg >= *a.n_split || *a.bad != (unsigned long long)kNoBad) return;
     const int g = a.split_g[sg];
     const int k = a.gcnt[g];
     if (k > 0) {

@@ -243,9 +243,9 @@ def test_sparse_store_matches_oracle(W):
 
 def test_large_batch_properties():
     """Full-size C1 batch (2^24): conservation and window identities."""
-    G, W, B = 1000, 1000, 1 << 24
+    G, W, B = 1000, 1000, 1000 * 16384
     g, a = D.gen_uniform(B, G, 3).arrays()
-    eng = _engine(G, W, P=148, max_batch=B)
+    eng = _engine(G, W, P=148, max_batch=1 << 24)
     eng.step(g, a)
     s = eng.snapshot()
     # every group received B/G >= W values: full windows of the last W values
@@ -254,4 +254,40 @@ def test_large_batch_properties():
     tail = a.reshape(-1, G)[-W:]
     assert np.array_equal(s["window_sum"], tail.sum(axis=0))
     assert (gg[0] == np.arange(G)).all()
+    eng.close()
+
+
+# ---- hot-key splitting across blocks + final combine (new mechanism) -------------
+
+@pytest.mark.parametrize("policy", ["no", "prob", "all", "best"])
+def test_split_aggregates_match_oracle(policy):
+    """Aggregates are assignment-independent, so split
+    execution must leave the windows bit-identical to the oracle."""
+    from paper_1309_0634_b200.stream_engine import StreamEngine
+    G, W, P, B = 2000, 50, 64, 50_000
+    spec = D.DatasetSpec(D.DatasetKind.ZIPF, 8 * B, G, 1.5, 3)
+    eng = _engine(G, W, P=P, sub_batch=16384, max_batch=B,
+                  aggregates=("count", "sum", "avg", "min", "max"))
+    bal = StreamEngine.balancer_struct(policy, max(1, B // (10 * P)), 0.5, split=True)
+    store = O.OStore(G, W)
+    ratios = []
+    for b in D.batches(D.stream_for(spec), B):
+        rep = eng.step(b.groups, b.attrs, bal)
+        ratios.append(rep.load_ratio)
+        store.ingest(b.groups, b.attrs)
+        loads = eng.last_loads()
+        assert loads.sum() == len(b)
+        res = eng.results()
+        cnt, sm, avg, mn, mx = store.aggregates(res.groups)
+        assert np.array_equal(res.count, cnt) and np.array_equal(res.sum, sm)
+        assert np.array_equal(res.avg, avg)
+        assert np.array_equal(res.min, mn) and np.array_equal(res.max, mx)
+    s = eng.snapshot()
+    assert np.array_equal(s["fill"], store.fill)
+    assert np.array_equal(s["next_pos"], store.next_pos)
+    assert np.array_equal(s["window_sum"], store.window_sum)
+    for gi in (0, 1, 2, 5, 100, G - 1):
+        assert eng.contents(gi).tolist() == store.contents(gi).tolist()
+    # without splitting the floor is P x top share ~ 24; with it, near 1
+    assert min(ratios[2:]) <= 1.3, ratios
     eng.close()
