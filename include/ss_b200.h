@@ -141,6 +141,9 @@ int  ss_step(ss_engine* e, const uint32_t* groups, const int32_t* attrs, int64_t
 int  ss_last_report(ss_engine* e, ss_step_report* rep);
 /* per-partition tuple loads of the last step (incl. split shares) */
 int  ss_last_loads(ss_engine* e, int64_t* loads);
+/* per-partition aggregate-kernel time (ns, summed over sub-batches) of the
+ * last step: IterationReport.per_thread_cost (engine.py:395-398) */
+int  ss_last_part_ns(ss_engine* e, int64_t* ns);
 /* moves emitted by the last step */
 int  ss_last_moves(ss_engine* e, ss_move* moves, int64_t cap, int64_t* n);
 

@@ -86,7 +86,12 @@ struct ss_engine {
     int n_sub_max = 0;
     uint32_t* stage_keys = nullptr;
     int32_t* stage_vals = nullptr;
-    int32_t *gcnt = nullptr, *gstart = nullptr, *gcount = nullptr, *bsum = nullptr;
+    int32_t *gcnt = nullptr, *gstart = nullptr, *gcount = nullptr, *bsum = nullptr, *gpre = nullptr;
+    long long* bdelta = nullptr;           // per-group batch delta
+    int32_t *bmin = nullptr, *bmax = nullptr;
+    unsigned long long* part_work = nullptr;
+    bool side_pending = false;             // policy/apply of the last batch still on the side stream
+    cudaEvent_t ev_k4 = nullptr, ev_apply = nullptr;
     uint32_t* dhist = nullptr;
     unsigned long long *tpt = nullptr, *touched = nullptr, *bad = nullptr;
     uint32_t* kbuf = nullptr;
@@ -123,7 +128,7 @@ struct ss_engine {
     int32_t *r_g = nullptr, *r_cnt = nullptr, *r_mn = nullptr, *r_mx = nullptr;
     long long* r_sum = nullptr;
     double* r_avg = nullptr;
-    int32_t* rescan = nullptr;
+    int2* rescan = nullptr;
     unsigned* n_rescan = nullptr;
     unsigned long long* part_ns = nullptr;
     unsigned long long* loads = nullptr;   // per-partition load incl. split shares
@@ -336,6 +341,8 @@ k_report(const unsigned long long* __restrict__ tpt, const unsigned long long* _
 
 }  // namespace
 
+static int join_side(ss_engine* e);
+
 // --------------------------------------------------------------------------
 // lifecycle
 // --------------------------------------------------------------------------
@@ -404,6 +411,8 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
     SS_CUDA(e, cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking));
     SS_CUDA(e, cudaEventCreateWithFlags(&e->ev_stats, cudaEventDisableTiming));
     SS_CUDA(e, cudaEventCreateWithFlags(&e->ev_bal, cudaEventDisableTiming));
+    SS_CUDA(e, cudaEventCreateWithFlags(&e->ev_k4, cudaEventDisableTiming));
+    SS_CUDA(e, cudaEventCreateWithFlags(&e->ev_apply, cudaEventDisableTiming));
 
     const int64_t G = e->G, W = e->W;
     int rc;
@@ -489,8 +498,12 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
         (rc = dalloc(e, &e->gcount, G)) || (rc = dalloc(e, &e->bsum, (size_t)nsub * e->nblk)) ||
         (rc = dalloc(e, &e->dhist, (size_t)nsub * 2 * kMaxBins)) || (rc = dalloc(e, &e->tpt, e->P)) ||
         (rc = dalloc(e, &e->touched, 1)) || (rc = dalloc(e, &e->bad, 1)) ||
-        (rc = dalloc(e, &e->tickets, (size_t)nsub * 2 + 2)))
+        (rc = dalloc(e, &e->tickets, (size_t)nsub * 2 + 2)) || (rc = dalloc(e, &e->gpre, (size_t)nsub * G)) ||
+        (rc = dalloc(e, &e->bdelta, G)) || (rc = dalloc(e, &e->bmin, G)) || (rc = dalloc(e, &e->bmax, G)))
         return rc;
+    SS_CUDA(e, cudaMemsetAsync(e->bdelta, 0, G * 8, e->st));
+    k_fill_i32<<<296, 256, 0, e->st>>>(e->bmin, G, 0x7fffffff);
+    k_fill_i32<<<296, 256, 0, e->st>>>(e->bmax, G, (int32_t)0x80000000);
     SS_CUDA(e, cudaMemsetAsync(e->gcnt, 0, (size_t)nsub * G * 4, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->gcount, 0, G * 4, e->st));
     k_set_bad<<<1, 1, 0, e->st>>>(e->bad);
@@ -520,25 +533,19 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
         SS_CUDA(e, cudaMemsetAsync(sp.part_soff, 0, (e->P + 1) * 4, e->st));
     }
     if ((rc = dalloc(e, &e->spx.hot_g, e->maxS)) || (rc = dalloc(e, &e->spx.n_hot, 1)) ||
-        (rc = dalloc(e, &e->spx.base, e->P)) || (rc = dalloc(e, &e->spx.hot_flag, G)) ||
-        (rc = dalloc(e, &e->spx.split_delta, e->maxS)) || (rc = dalloc(e, &e->spx.split_min, e->maxS)) ||
-        (rc = dalloc(e, &e->spx.split_max, e->maxS)))
+        (rc = dalloc(e, &e->spx.base, e->P)) || (rc = dalloc(e, &e->spx.hot_flag, G)))
         return rc;
-    SS_CUDA(e, cudaMemsetAsync(e->spx.split_delta, 0, e->maxS * 8, e->st));
-    {
-        std::vector<int32_t> lo(e->maxS, 0x7fffffff), hi(e->maxS, (int32_t)0x80000000);
-        SS_CUDA(e, cudaMemcpy(e->spx.split_min, lo.data(), e->maxS * 4, cudaMemcpyHostToDevice));
-        SS_CUDA(e, cudaMemcpy(e->spx.split_max, hi.data(), e->maxS * 4, cudaMemcpyHostToDevice));
-    }
     // -- emission
     if ((rc = dalloc(e, &e->n_res, 1)) || (rc = dalloc(e, &e->r_g, G)) || (rc = dalloc(e, &e->r_cnt, G)) ||
         (rc = dalloc(e, &e->r_sum, G)) || (rc = dalloc(e, &e->r_avg, G)) || (rc = dalloc(e, &e->r_mn, G)) ||
         (rc = dalloc(e, &e->r_mx, G)) || (rc = dalloc(e, &e->rescan, G)) || (rc = dalloc(e, &e->n_rescan, 1)) ||
         (rc = dalloc(e, &e->part_ns, e->P)) || (rc = dalloc(e, &e->loads, e->P)) || (rc = dalloc(e, &e->d_rep, 1)) ||
+        (rc = dalloc(e, &e->part_work, e->P)) ||
         (rc = dalloc(e, &e->alg_bytes, 1)))
         return rc;
     SS_CUDA(e, cudaMemsetAsync(e->alg_bytes, 0, 8, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->n_res, 0, 4, e->st));
+    SS_CUDA(e, cudaMemsetAsync(e->n_rescan, 0, 4, e->st));
     SS_CUDA(e, cudaMallocHost(&e->h_rep, sizeof(DevReport)));
     memset(e->h_rep, 0, sizeof(DevReport));
     e->h_rep->bad = (unsigned long long)kNoBad;
@@ -561,6 +568,7 @@ extern "C" int ss_set_stream(ss_engine* e, void* stream) {
 
 extern "C" int ss_sync(ss_engine* e) {
     if (!e) return SS_E_CONFIG;
+    { int jr = join_side(e); if (jr) return jr; }
     SS_CUDA(e, cudaStreamSynchronize(e->st));
     SS_CUDA(e, cudaGetLastError());
     return SS_OK;
@@ -569,6 +577,16 @@ extern "C" int ss_sync(ss_engine* e) {
 // --------------------------------------------------------------------------
 // input staging
 // --------------------------------------------------------------------------
+// make the engine stream wait for the last batch's side work (policy,
+// apply, report) before anything that reads or writes the assignment
+static int join_side(ss_engine* e) {
+    if (e->side_pending) {
+        SS_CUDA(e, cudaStreamWaitEvent(e->st, e->ev_apply, 0));
+        e->side_pending = false;
+    }
+    return SS_OK;
+}
+
 static int stage_input(ss_engine* e, const uint32_t* groups, const int32_t* attrs, int64_t n,
                        const uint32_t** dk, const int32_t** dv) {
     if (n > e->max_batch) return fail(e, SS_E_CONFIG, "batch larger than max_batch");
@@ -591,6 +609,8 @@ static int stage_input(ss_engine* e, const uint32_t* groups, const int32_t* attr
 // After a DataError the partially filled histograms are cleared so the
 // engine state is exactly as before the failed call.
 static int recover_bad(ss_engine* e) {
+    cudaStreamSynchronize(e->side);
+    e->side_pending = false;
     SS_CUDA(e, cudaMemsetAsync(e->gcnt, 0, (size_t)e->n_sub_max * e->G * 4, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->gcount, 0, e->G * 4, e->st));
     k_set_bad<<<1, 1, 0, e->st>>>(e->bad);
@@ -630,7 +650,7 @@ static int launch_stats(ss_engine* e, int n_sub) {
     SS_CUDA(e, cudaMemsetAsync(e->touched, 0, 8, e->st));
     k_batch_stats<<<2 * kNumSM, 1024, e->P * 8, e->st>>>(e->gcnt, n_sub, (uint32_t)e->G, e->pmap, e->P, e->gcount,
                                                           e->tpt, e->touched, e->bad, e->fill, e->W,
-                                                          e->alg_bytes);
+                                                          e->alg_bytes, e->gpre);
     SS_CUDA(e, cudaGetLastError());
     return SS_OK;
 }
@@ -681,15 +701,17 @@ static IngestArgs ingest_args(ss_engine* e, int s, bool with_plan) {
     a.order = e->order;
     a.offsets = e->offsets;
     a.gcnt = e->gcnt + (int64_t)s * e->G;
+    a.gpre = e->gpre + (int64_t)s * e->G;
+    a.gcount = e->gcount;
     a.gstart = e->gstart + (int64_t)s * e->G;
     a.vals = e->vbuf[0];
     a.fill = e->fill;
     a.next_pos = e->next_pos;
-    a.wsum = e->wsum;
-    a.mn = e->mn;
-    a.mx = e->mx;
     a.off = e->off;
     a.ring = e->ring;
+    a.bdelta = e->bdelta;
+    a.bmin = e->bmin;
+    a.bmax = e->bmax;
     a.W = e->W;
     a.minmax = e->minmax;
     if (with_plan) {
@@ -701,22 +723,24 @@ static IngestArgs ingest_args(ss_engine* e, int s, bool with_plan) {
         a.share_hi = sp.share_hi;
         a.split_g = sp.split_g;
         a.split_den = sp.split_den;
-        a.n_split = sp.n_split;
-        a.split_delta = e->spx.split_delta;
-        a.split_min = e->spx.split_min;
-        a.split_max = e->spx.split_max;
     }
-    a.rescan = e->rescan;
-    a.n_rescan = e->n_rescan;
     a.part_ns = e->part_ns;
+    a.part_work = e->part_work;
     a.bad = e->bad;
     return a;
 }
 
 static int move_cap(ss_engine* e, const ss_balancer* b);
+static int enqueue_report(ss_engine* e, int64_t n, bool has_policy, cudaStream_t st);
 
-// count -> stats -> [policy] -> scans -> per sub-batch (reserve, place,
-// ingest, finalize) -> [emit] -> [apply]
+// One batch (the loop body of harness.run, harness.py:99-117).
+//   main stream: count -> [join last batch's side work] -> stats -> scans
+//                -> reserve -> per sub-batch (place, window exchange)
+//                -> finalize + emit (+ MIN/MAX rescans)
+//   side stream: policy / split planner (from the stats) -> [wait for the
+//                last window exchange] -> apply moves -> report
+// The side work of batch t overlaps the rest of batch t and the count of
+// batch t+1; batch t+1's stats wait for it (they read the new map).
 static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_t n, const ss_balancer* bal,
                      bool emit) {
     const int n_sub = (int)std::max<int64_t>(1, (n + e->S - 1) / e->S);
@@ -730,15 +754,21 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
         pol = SS_POLICY_BEST;
     const bool has_policy = pol != SS_POLICY_NO;
     const bool run_side = has_policy || split;
-    const bool use_plan = e->plan_valid;   // decided by the previous batch
-    e->last_plan = use_plan ? e->plan_cur : -1;
     SS_CUDA(e, cudaMemsetAsync(e->tickets, 0, (size_t)n_sub * 2 * 4, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->part_ns, 0, e->P * 8, e->st));
+    SS_CUDA(e, cudaMemsetAsync(e->part_work, 0, e->P * 8, e->st));
     if (emit) SS_CUDA(e, cudaMemsetAsync(e->n_res, 0, 4, e->st));
+    if (e->minmax) SS_CUDA(e, cudaMemsetAsync(e->n_rescan, 0, 4, e->st));
     {
         ProfScope ps(e, SS_K_COUNT, e->st);
         if ((rc = launch_count(e, dk, n, e->S))) return rc;
     }
+    if (e->side_pending) {
+        SS_CUDA(e, cudaStreamWaitEvent(e->st, e->ev_apply, 0));
+        e->side_pending = false;
+    }
+    const bool use_plan = e->plan_valid;   // decided by the previous batch
+    e->last_plan = use_plan ? e->plan_cur : -1;
     {
         ProfScope ps(e, SS_K_STATS, e->st);
         if ((rc = launch_stats(e, n_sub))) return rc;
@@ -787,20 +817,20 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
         }
         if (split) {
             const SplitPlan& nx = e->plan_buf[e->plan_cur ^ 1];
-            const long long* fl = has_policy ? e->final_tpt : nullptr;
-            if (!has_policy) {
-                k_u64_to_i64<<<1, 1024, 0, e->side>>>(e->spx.base, e->final_tpt, e->P);
-                fl = e->final_tpt;
-            }
+            if (!has_policy) k_u64_to_i64<<<1, 1024, 0, e->side>>>(e->spx.base, e->final_tpt, e->P);
             const size_t smem = (size_t)e->maxS * 20 + 16 + (size_t)(e->P + 1) * 4;
-            k_split_fill<<<1, 1024, smem, e->side>>>(e->gcount, fl, e->P, e->maxS, e->spx, nx, nx, e->bad);
+            k_split_fill<<<1, 1024, smem, e->side>>>(e->gcount, e->final_tpt, e->P, e->maxS, e->spx, nx, nx, e->bad);
         }
         SS_CUDA(e, cudaGetLastError());
-        SS_CUDA(e, cudaEventRecord(e->ev_bal, e->side));
     }
     {
         ProfScope ps(e, SS_K_STATS, e->st);
         if ((rc = launch_scans(e, n_sub))) return rc;
+    }
+    if (!e->dense) {
+        ProfScope ps(e, SS_K_INGEST, e->st);
+        k_reserve<<<2 * kNumSM, 256, 0, e->st>>>(e->gcount, (uint32_t)e->G, e->W, e->fill, e->off, e->cap, e->ring,
+                                                 e->pool_top, e->pool_cap, e->oom, e->bad);
     }
     for (int s = 0; s < n_sub; ++s) {
         const int64_t lo = (int64_t)s * e->S;
@@ -812,38 +842,62 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
         }
         {
             ProfScope ps(e, SS_K_INGEST, e->st);
-            if (!e->dense) {
-                k_reserve<<<2 * kNumSM, 256, 0, e->st>>>(e->gcnt + (int64_t)s * e->G, (uint32_t)e->G, e->W, e->fill,
-                                                         e->off, e->cap, e->ring, e->pool_top, e->pool_cap, e->oom,
-                                                         e->bad);
-            }
-            if (e->minmax) SS_CUDA(e, cudaMemsetAsync(e->n_rescan, 0, 4, e->st));
             IngestArgs a = ingest_args(e, s, use_plan);
             k_ingest<<<e->P, kIngestThreads, kIngestSmem, e->st>>>(a);
-            if (use_plan) k_split_finalize<<<(e->maxS + 255) / 256, 256, 0, e->st>>>(a);
-            if (e->minmax)
-                k_minmax_rescan<<<2 * kNumSM, 256, 0, e->st>>>(e->rescan, e->n_rescan, e->ring, e->off, e->W, e->mn,
-                                                               e->mx);
         }
         SS_CUDA(e, cudaGetLastError());
     }
-    // the balancer reads gcount: join it before the emission clears it
-    if (run_side) SS_CUDA(e, cudaStreamWaitEvent(e->st, e->ev_bal, 0));
-    if (emit) {
+    if (run_side) SS_CUDA(e, cudaEventRecord(e->ev_k4, e->st));
+    {
         ProfScope ps(e, SS_K_EMIT, e->st);
-        k_emit<<<2 * kNumSM, 256, 0, e->st>>>(e->gcount, (uint32_t)e->G, e->fill, e->wsum, e->mn, e->mx, e->minmax,
-                                              e->n_res, e->r_g, e->r_cnt, e->r_sum, e->r_avg, e->r_mn, e->r_mx, e->bad);
-    } else {
-        SS_CUDA(e, cudaMemsetAsync(e->gcount, 0, e->G * 4, e->st));
-    }
-    if (has_policy) {
-        ProfScope ps(e, SS_K_APPLY, e->st);
-        k_apply_sizes<<<1, 1024, 0, e->st>>>(e->offsets, e->P, e->moves, e->n_moves, e->new_off);
-        k_apply_build<<<e->P, 256, 0, e->st>>>(e->order, e->offsets, e->new_off, e->moves, e->n_moves, e->front_top,
-                                               e->back_first, e->mv_next, e->moved, e->new_order);
-        k_apply_commit<<<2 * kNumSM, 256, 0, e->st>>>(e->order, e->offsets, e->new_order, e->new_off, (int)e->G, e->P,
-                                                      e->moves, e->n_moves, e->pmap, e->moved);
+        FinalizeArgs f{};
+        f.gcount = e->gcount;
+        f.gcnt = e->gcnt;
+        f.n_sub = n_sub;
+        f.G = (uint32_t)e->G;
+        f.W = e->W;
+        f.fill = e->fill;
+        f.next_pos = e->next_pos;
+        f.wsum = e->wsum;
+        f.mn = e->mn;
+        f.mx = e->mx;
+        f.bdelta = e->bdelta;
+        f.bmin = e->bmin;
+        f.bmax = e->bmax;
+        f.minmax = e->minmax;
+        f.emit = emit;
+        f.n_res = e->n_res;
+        f.r_g = e->r_g;
+        f.r_cnt = e->r_cnt;
+        f.r_sum = e->r_sum;
+        f.r_avg = e->r_avg;
+        f.r_mn = e->r_mn;
+        f.r_mx = e->r_mx;
+        f.rescan = e->rescan;
+        f.n_rescan = e->n_rescan;
+        f.bad = e->bad;
+        k_finalize<<<2 * kNumSM, 256, 0, e->st>>>(f);
+        if (e->minmax)
+            k_minmax_rescan<<<2 * kNumSM, 256, 0, e->st>>>(e->rescan, e->n_rescan, e->ring, e->off, e->W, e->mn,
+                                                           e->mx, e->r_mn, e->r_mx);
         SS_CUDA(e, cudaGetLastError());
+    }
+    if (run_side) {
+        SS_CUDA(e, cudaStreamWaitEvent(e->side, e->ev_k4, 0));
+        if (has_policy) {
+            ProfScope ps(e, SS_K_APPLY, e->side);
+            k_apply_sizes<<<1, 1024, 0, e->side>>>(e->offsets, e->P, e->moves, e->n_moves, e->new_off);
+            k_apply_build<<<e->P, 256, 0, e->side>>>(e->order, e->offsets, e->new_off, e->moves, e->n_moves,
+                                                     e->front_top, e->back_first, e->mv_next, e->moved, e->new_order);
+            k_apply_commit<<<2 * kNumSM, 256, 0, e->side>>>(e->order, e->offsets, e->new_order, e->new_off, (int)e->G,
+                                                            e->P, e->moves, e->n_moves, e->pmap, e->moved);
+            SS_CUDA(e, cudaGetLastError());
+        }
+        if ((rc = enqueue_report(e, n, has_policy, e->side))) return rc;
+        SS_CUDA(e, cudaEventRecord(e->ev_apply, e->side));
+        e->side_pending = true;
+    } else {
+        if ((rc = enqueue_report(e, n, false, e->st))) return rc;
     }
     if (split) {
         e->plan_cur ^= 1;
@@ -857,14 +911,14 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
 // --------------------------------------------------------------------------
 // report
 // --------------------------------------------------------------------------
-static int enqueue_report(ss_engine* e, int64_t n, bool has_policy) {
+static int enqueue_report(ss_engine* e, int64_t n, bool has_policy, cudaStream_t st) {
     const bool used_plan = e->last_plan >= 0;
-    k_report<<<1, 1024, 0, e->st>>>(e->tpt, used_plan ? e->loads : nullptr, e->P, e->bad, e->touched, e->n_moves, e->prev_moves,
-                                    e->scanned, used_plan ? e->plan_buf[e->last_plan].n_split : nullptr,
-                                    e->n_res, e->oom, (long long)n, has_policy ? 1 : 0,
-                                    e->d_rep);
+    k_report<<<1, 1024, 0, st>>>(e->tpt, used_plan ? e->loads : nullptr, e->P, e->bad, e->touched, e->n_moves,
+                                 e->prev_moves, e->scanned,
+                                 used_plan ? e->plan_buf[e->last_plan].n_split : nullptr, e->n_res, e->oom,
+                                 (long long)n, has_policy ? 1 : 0, e->d_rep);
     SS_CUDA(e, cudaGetLastError());
-    SS_CUDA(e, cudaMemcpyAsync(e->h_rep, e->d_rep, sizeof(DevReport), cudaMemcpyDeviceToHost, e->st));
+    SS_CUDA(e, cudaMemcpyAsync(e->h_rep, e->d_rep, sizeof(DevReport), cudaMemcpyDeviceToHost, st));
     return SS_OK;
 }
 
@@ -872,6 +926,7 @@ static const uint32_t* g_last_keys = nullptr;
 
 static int check_report(ss_engine* e, const uint32_t* dk) {
     SS_CUDA(e, cudaStreamSynchronize(e->st));
+    SS_CUDA(e, cudaStreamSynchronize(e->side));
     SS_CUDA(e, cudaGetLastError());
     if (e->h_rep->bad != (unsigned long long)kNoBad) return data_error(e, e->h_rep->bad, dk);
     if (e->h_rep->oom) return fail(e, SS_E_EXEC, "window ring pool exhausted (raise pool_values)");
@@ -923,6 +978,7 @@ static int check_balancer(ss_engine* e, const ss_balancer* b) {
 // --------------------------------------------------------------------------
 extern "C" int ss_set_assignment(ss_engine* e, const int32_t* order, const int64_t* offsets) {
     if (!e || !order || !offsets) return SS_E_CONFIG;
+    { int jr = join_side(e); if (jr) return jr; }
     const int64_t G = e->G;
     const int P = e->P;
     if (offsets[0] != 0 || offsets[P] != G) return fail(e, SS_E_CONSISTENCY, "offsets must span [0, G]");
@@ -947,6 +1003,7 @@ extern "C" int ss_set_assignment(ss_engine* e, const int32_t* order, const int64
 
 extern "C" int ss_get_assignment(ss_engine* e, int32_t* g2t, int32_t* order, int64_t* offsets) {
     if (!e) return SS_E_CONFIG;
+    { int jr = join_side(e); if (jr) return jr; }
     SS_CUDA(e, cudaStreamSynchronize(e->st));
     if (g2t) SS_CUDA(e, cudaMemcpy(g2t, e->pmap, e->G * 4, cudaMemcpyDeviceToHost));
     if (order) SS_CUDA(e, cudaMemcpy(order, e->order, e->G * 4, cudaMemcpyDeviceToHost));
@@ -1012,6 +1069,7 @@ static int clear_counts_row0(ss_engine* e) {
 
 extern "C" int ss_count(ss_engine* e, const uint32_t* groups, int64_t n, int64_t* group_counts, int64_t* tpt) {
     if (!e || n < 0) return SS_E_CONFIG;
+    { int jr = join_side(e); if (jr) return jr; }
     const uint32_t* dk;
     int rc;
     if ((rc = stage_input(e, groups, nullptr, n, &dk, nullptr))) return rc;
@@ -1043,6 +1101,7 @@ static int32_t* g_rank_scratch(ss_engine* e) {
 extern "C" int ss_reorder(ss_engine* e, const uint32_t* groups, const int32_t* attrs, int64_t n,
                           uint32_t* out_groups, int32_t* out_attrs, int64_t* indicator) {
     if (!e || n < 0) return SS_E_CONFIG;
+    { int jr = join_side(e); if (jr) return jr; }
     const uint32_t* dk;
     const int32_t* dv;
     int rc;
@@ -1093,6 +1152,7 @@ extern "C" int ss_reorder(ss_engine* e, const uint32_t* groups, const int32_t* a
 // --------------------------------------------------------------------------
 extern "C" int ss_ingest(ss_engine* e, const uint32_t* groups, const int32_t* attrs, int64_t n) {
     if (!e || n < 0) return SS_E_CONFIG;
+    { int jr = join_side(e); if (jr) return jr; }
     if (n == 0) return SS_OK;
     const uint32_t* dk;
     const int32_t* dv;
@@ -1100,13 +1160,13 @@ extern "C" int ss_ingest(ss_engine* e, const uint32_t* groups, const int32_t* at
     if ((rc = stage_input(e, groups, attrs, n, &dk, &dv))) return rc;
     e->last_plan = -1;
     if ((rc = run_batch(e, dk, dv, n, nullptr, false))) return rc;
-    if ((rc = enqueue_report(e, n, false))) return rc;
     return check_report(e, dk);
 }
 
 extern "C" int ss_balance(ss_engine* e, const uint32_t* groups, int64_t n, const ss_balancer* cfg,
                           ss_move* moves, int64_t* n_moves, int64_t* scanned, int64_t* final_tpt) {
     if (!e || !cfg || n < 0) return SS_E_CONFIG;
+    { int jr = join_side(e); if (jr) return jr; }
     int rc;
     if ((rc = check_balancer(e, cfg))) return rc;
     const uint32_t* dk;
@@ -1181,13 +1241,17 @@ extern "C" int ss_step(ss_engine* e, const uint32_t* groups, const int32_t* attr
     e->last_plan = -1;
     if (n > 0 && (rc = run_batch(e, dk, dv, n, cfg, true))) return rc;
     if (n == 0) {
+        if (e->side_pending) {
+            SS_CUDA(e, cudaStreamWaitEvent(e->st, e->ev_apply, 0));
+            e->side_pending = false;
+        }
         SS_CUDA(e, cudaMemsetAsync(e->tpt, 0, e->P * 8, e->st));
         SS_CUDA(e, cudaMemsetAsync(e->touched, 0, 8, e->st));
         SS_CUDA(e, cudaMemsetAsync(e->n_res, 0, 4, e->st));
         SS_CUDA(e, cudaMemsetAsync(e->n_moves, 0, 4, e->st));
         SS_CUDA(e, cudaMemsetAsync(e->scanned, 0, 8, e->st));
+        if ((rc = enqueue_report(e, 0, has_policy, e->st))) return rc;
     }
-    if ((rc = enqueue_report(e, n, has_policy && n > 0))) return rc;
     if (rep) {
         if ((rc = check_report(e, dk))) return rc;
         fill_report(e, rep);
@@ -1205,10 +1269,21 @@ extern "C" int ss_last_report(ss_engine* e, ss_step_report* rep) {
 
 extern "C" int ss_last_loads(ss_engine* e, int64_t* loads) {
     if (!e || !loads) return SS_E_CONFIG;
+    { int jr = join_side(e); if (jr) return jr; }
     std::vector<unsigned long long> t(e->P);
     SS_CUDA(e, cudaStreamSynchronize(e->st));
     SS_CUDA(e, cudaMemcpy(t.data(), e->last_plan >= 0 ? e->loads : e->tpt, e->P * 8, cudaMemcpyDeviceToHost));
     for (int p = 0; p < e->P; ++p) loads[p] = (int64_t)t[p];
+    return SS_OK;
+}
+
+extern "C" int ss_last_part_ns(ss_engine* e, int64_t* ns) {
+    if (!e || !ns) return SS_E_CONFIG;
+    { int jr = join_side(e); if (jr) return jr; }
+    std::vector<unsigned long long> t(e->P);
+    SS_CUDA(e, cudaStreamSynchronize(e->st));
+    SS_CUDA(e, cudaMemcpy(t.data(), e->part_ns, e->P * 8, cudaMemcpyDeviceToHost));
+    for (int p = 0; p < e->P; ++p) ns[p] = (int64_t)t[p];
     return SS_OK;
 }
 
@@ -1232,6 +1307,7 @@ extern "C" int ss_last_moves(ss_engine* e, ss_move* moves, int64_t cap, int64_t*
 extern "C" int ss_snapshot(ss_engine* e, int64_t* fill, int64_t* next_pos, int64_t* window_sum, int32_t* mn,
                            int32_t* mx, double* avg) {
     if (!e) return SS_E_CONFIG;
+    { int jr = join_side(e); if (jr) return jr; }
     const int64_t G = e->G;
     SS_CUDA(e, cudaStreamSynchronize(e->st));
     std::vector<int32_t> f(G), np(G);
@@ -1252,6 +1328,7 @@ extern "C" int ss_snapshot(ss_engine* e, int64_t* fill, int64_t* next_pos, int64
 
 extern "C" int ss_export_values(ss_engine* e, int64_t group, int64_t* out, int64_t cap, int64_t* n) {
     if (!e || group < 0 || group >= e->G) return fail(e, SS_E_CONFIG, "group out of range");
+    { int jr = join_side(e); if (jr) return jr; }
     SS_CUDA(e, cudaStreamSynchronize(e->st));
     int32_t f, p;
     int64_t o;
@@ -1271,6 +1348,7 @@ extern "C" int ss_export_values(ss_engine* e, int64_t group, int64_t* out, int64
 extern "C" int ss_results(ss_engine* e, int64_t cap, int32_t* groups, int64_t* count, int64_t* sum, double* avg,
                           int32_t* mn, int32_t* mx, int64_t* n) {
     if (!e) return SS_E_CONFIG;
+    { int jr = join_side(e); if (jr) return jr; }
     SS_CUDA(e, cudaStreamSynchronize(e->st));
     unsigned nr = 0;
     SS_CUDA(e, cudaMemcpy(&nr, e->n_res, 4, cudaMemcpyDeviceToHost));
@@ -1349,6 +1427,7 @@ extern "C" int ss_alg_bytes(ss_engine* e, int64_t* bytes, int reset) {
 
 extern "C" int ss_results_raw(ss_engine* e, int64_t cap, int32_t* groups, double* avg, int64_t* n) {
     if (!e) return SS_E_CONFIG;
+    { int jr = join_side(e); if (jr) return jr; }
     unsigned nr = 0;
     SS_CUDA(e, cudaMemcpyAsync(&nr, e->n_res, 4, cudaMemcpyDeviceToHost, e->st));
     SS_CUDA(e, cudaStreamSynchronize(e->st));

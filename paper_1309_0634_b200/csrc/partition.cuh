@@ -89,7 +89,8 @@ __global__ void __launch_bounds__(1024)
 k_batch_stats(const int32_t* __restrict__ gcnt, int n_sub, uint32_t G, const int32_t* __restrict__ pmap,
               int P, int32_t* __restrict__ gcount, unsigned long long* __restrict__ tpt,
               unsigned long long* __restrict__ touched, const unsigned long long* __restrict__ bad,
-              const int32_t* __restrict__ fill, int64_t W, unsigned long long* __restrict__ alg_bytes) {
+              const int32_t* __restrict__ fill, int64_t W, unsigned long long* __restrict__ alg_bytes,
+              int32_t* __restrict__ gpre) {
     extern __shared__ unsigned long long sh_tpt[];
     if (*bad != (unsigned long long)kNoBad) return;
     for (int p = threadIdx.x; p < P; p += blockDim.x) sh_tpt[p] = 0;
@@ -98,7 +99,10 @@ k_batch_stats(const int32_t* __restrict__ gcnt, int n_sub, uint32_t G, const int
     unsigned long long my_bytes = 0;
     for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < G; g += gridDim.x * blockDim.x) {
         int32_t c = 0;
-        for (int s = 0; s < n_sub; ++s) c += gcnt[(int64_t)s * G + g];
+        for (int s = 0; s < n_sub; ++s) {
+            gpre[(int64_t)s * G + g] = c;      // batch rank of the group's first tuple in sub-batch s
+            c += gcnt[(int64_t)s * G + g];
+        }
         gcount[g] = c;
         if (c) {
             atomicAdd(&sh_tpt[pmap[g]], (unsigned long long)c);

@@ -42,9 +42,6 @@ struct SplitScratch {
     int* n_hot;
     unsigned long long* base;   // [P] cold loads
     uint8_t* hot_flag;     // [G]
-    unsigned long long* split_delta;   // [maxS]
-    int32_t* split_min;
-    int32_t* split_max;
 };
 
 // Phase 1: hot detection + cold loads.  grid-stride over G.

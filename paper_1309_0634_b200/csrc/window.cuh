@@ -1,5 +1,5 @@
-// window.cuh -- K4 (per-partition incremental window update), K5 (combine
-// of split hot keys), store growth and the per-batch result emission.
+// window.cuh -- K4 (per-partition window exchange), K5 (batch finalisation
+// and per-batch result emission), store growth and MIN/MAX rescans.
 //
 // Reference semantics (engine.py:185-250): a group with
 // prior (fill f0, next_pos p0, sum S0) receiving k values a_0..a_{k-1} in
@@ -8,12 +8,17 @@
 //     sum  = sum of the last `fill` values of  old-window ++ run,
 // and only a_j with j >= k-W are stored, at ring slot (p0+f0+j) mod W.
 //
-// B200 formulation: slot (p0+f0+j) mod W held, at batch start, the old
-// timeline position q = (f0+j) mod W, which is live iff q < f0.  So every
-// stored value is an independent exchange
+// B200 formulation, per BATCH (k = the group's count in the whole batch,
+// j = a tuple's rank inside its group over the whole batch): slot
+// (p0+f0+j) mod W held, at batch start, the old timeline position
+// q = (f0+j) mod W, which is live iff q < f0.  Every stored value is an
+// independent exchange
 //     old = live ? ring[slot] : 0;  ring[slot] = a_j;  delta += a_j - old
-// and sum = S0 + sum(delta): integer arithmetic, bit-exact in any order,
-// which is what lets split hot keys be updated by several CTAs at once.
+// and sum = S0 + sum(delta) (or sum(a_j) when k >= W: every old value is
+// evicted).  Integer arithmetic, bit-exact in any order, so the batch's
+// L2-resident sub-batches, the partitions' CTAs and the shares of a split
+// hot key all work independently; K5 folds the deltas into the state once
+// per batch.  Only min(k, W) values per group and batch are ever stored.
 #pragma once
 
 #include "common.cuh"
@@ -21,7 +26,7 @@
 namespace ss {
 
 constexpr int kIngestThreads = 1024;
-constexpr int kILP = 8;                      // stored values in flight per thread
+constexpr int kILP = 8;                     // stored values in flight per thread
 constexpr int kMemberChunk = 2048;          // members staged per CTA round
 constexpr int kMPT = kMemberChunk / kIngestThreads;
 constexpr size_t kIngestSmem = (size_t)kMemberChunk * (8 + 8 + 4 * 8) + 16;
@@ -29,32 +34,29 @@ constexpr size_t kIngestSmem = (size_t)kMemberChunk * (8 + 8 + 4 * 8) + 16;
 struct IngestArgs {
     const int32_t* order;       // partition lists, concatenated   [G]
     const int32_t* offsets;     // CSR offsets                     [P+1]
-    int32_t* gcnt;              // group counts of this sub-batch  [G] (reset after use)
+    const int32_t* gcnt;        // group counts of this sub-batch  [G]
+    const int32_t* gpre;        // batch rank of each group's first tuple in this sub-batch
+    const int32_t* gcount;      // group counts of the whole batch
     const int32_t* gstart;      // run start of each group in the placed sub-batch
     const int32_t* vals;        // placed (group-sorted, arrival-stable) values
-    int32_t* fill;
-    int32_t* next_pos;
-    long long* wsum;
-    int32_t* mn;
-    int32_t* mx;
+    const int32_t* fill;        // batch-start state (read only in K4)
+    const int32_t* next_pos;
     const int64_t* off;         // ring region of each group
     int32_t* ring;
+    long long* bdelta;          // per-group batch delta (K5 folds it)
+    int32_t* bmin;              // per-group batch min / max of stored values
+    int32_t* bmax;
     int64_t W;
     int minmax;                 // maintain MIN/MAX
-    const int32_t* split_of;    // >= 0: group executed as split shares (K5 finalises)
+    const int32_t* split_of;    // >= 0: group executed as split shares
     const int32_t* share_off;   // [P+1] split shares of each partition
     const int32_t* share_grp;   // split-group index per share
     const long long* share_lo;  // run slice [k*lo/den, k*hi/den) of the share
     const long long* share_hi;
     const int32_t* split_g;     // split-group index -> group
     const long long* split_den; // split-group index -> planned count
-    const int* n_split;
-    unsigned long long* split_delta;   // per split-group delta (K5)
-    int32_t* split_min;
-    int32_t* split_max;
-    int32_t* rescan;            // groups whose MIN/MAX need a rescan
-    unsigned* n_rescan;
     unsigned long long* part_ns;       // per-partition (CTA) time, ns
+    unsigned long long* part_work;     // per-partition stored values
     const unsigned long long* bad;
 };
 
@@ -80,7 +82,7 @@ k_ingest(IngestArgs a) {
     int32_t* m_start = m_scan + kMemberChunk + 4;
     int32_t* m_q0 = m_start + kMemberChunk;
     int32_t* m_s0 = m_q0 + kMemberChunk;
-    int32_t* m_f0 = m_s0 + kMemberChunk;
+    int32_t* m_f0 = m_s0 + kMemberChunk;             // live bound (0 when k >= W)
     int32_t* m_min = m_f0 + kMemberChunk;
     int32_t* m_max = m_min + kMemberChunk;
     __shared__ int32_t sh_red[33];
@@ -91,9 +93,11 @@ k_ingest(IngestArgs a) {
     const int lo = a.offsets[p], hi = a.offsets[p + 1];
     const int s_lo = a.share_off ? a.share_off[p] : 0;
     const int s_hi = a.share_off ? a.share_off[p + 1] : 0;
-    const int n_items = (hi - lo) + (s_hi - s_lo);   // members, then split shares
+    const int n_mem = hi - lo;
+    const int n_items = n_mem + (s_hi - s_lo);   // members, then split shares
     const int W = (int)a.W;
     const unsigned lane = lane_id();
+    unsigned long long work_total = 0;
 
     for (int c0 = 0; c0 < n_items; c0 += kMemberChunk) {
         const int m = min(kMemberChunk, n_items - c0);
@@ -103,56 +107,42 @@ k_ingest(IngestArgs a) {
         for (int q = 0; q < kMPT; ++q) {
             const int i = threadIdx.x * kMPT + q;
             wk[q] = 0;
-            if (i < m) {
-                const int it = c0 + i;
-                int g, k, kb = 0;   // kb: first run index of this item
-                if (it < hi - lo) {
-                    g = a.order[lo + it];
-                    k = (a.split_of && a.split_of[g] >= 0) ? 0 : a.gcnt[g];
-                } else {
-                    const int sh = s_lo + (it - (hi - lo));
-                    const int sg = a.share_grp[sh];
-                    g = a.split_g[sg];
-                    const int kt = a.gcnt[g];
-                    const long long den = a.split_den[sg];
-                    kb = (int)((long long)kt * a.share_lo[sh] / den);
-                    const int ke = (int)((long long)kt * a.share_hi[sh] / den);
-                    // the slice is [kb, ke) of a run of kt; stored part is j >= kt - W
-                    const int w0 = max(kb, kt - W);
-                    k = max(0, ke - w0);
-                    kb = w0;
-                    if (k > 0) {
-                        const int f0 = a.fill[g];
-                        m_g[i] = -1 - sg;          // marks a share
-                        m_start[i] = a.gstart[g] + kb;
-                        m_q0[i] = (int)(((int64_t)f0 + kb) % W);
-                        m_s0[i] = (int)(((int64_t)a.next_pos[g] + f0 + kb) % W);
-                        m_f0[i] = f0;
-                        m_off[i] = a.off[g];
-                        m_delta[i] = 0;
-                        m_min[i] = 0x7fffffff;
-                        m_max[i] = (int32_t)0x80000000;
-                        wk[q] = k;
-                    }
-                    k = -1;   // handled
-                }
-                if (k > 0) {
-                    const int f0 = a.fill[g];
-                    const int w0 = max(0, k - W);
-                    m_g[i] = g;
-                    m_start[i] = a.gstart[g] + w0;
-                    m_q0[i] = (int)(((int64_t)f0 + w0) % W);
-                    m_s0[i] = (int)(((int64_t)a.next_pos[g] + f0 + w0) % W);
-                    m_f0[i] = f0;
-                    m_off[i] = a.off[g];
-                    m_delta[i] = 0;
-                    m_min[i] = 0x7fffffff;
-                    m_max[i] = (int32_t)0x80000000;
-                    wk[q] = k - w0;
-                } else if (k == 0) {
-                    m_g[i] = 0x7fffffff;   // nothing to do
-                }
+            if (i >= m) continue;
+            const int it = c0 + i;
+            int g, r_lo, r_hi;            // this item's slice [r_lo, r_hi) of the sub-batch run
+            int32_t tag;
+            if (it < n_mem) {
+                g = a.order[lo + it];
+                tag = g;
+                r_lo = 0;
+                r_hi = (a.split_of && a.split_of[g] >= 0) ? 0 : a.gcnt[g];
+            } else {
+                const int sh = s_lo + (it - n_mem);
+                const int sg = a.share_grp[sh];
+                g = a.split_g[sg];
+                tag = -1 - sg;
+                const long long kt = a.gcnt[g], den = a.split_den[sg];
+                r_lo = (int)(kt * a.share_lo[sh] / den);
+                r_hi = (int)(kt * a.share_hi[sh] / den);
             }
+            m_g[i] = 0x7fffffff;
+            if (r_hi <= r_lo) continue;
+            const int K = a.gcount[g];                 // batch count
+            const int b = a.gpre[g];                   // batch rank of run index 0
+            const int first = max(r_lo, K - W - b);    // first stored run index
+            if (first >= r_hi) continue;
+            const int f0 = a.fill[g];
+            const int jb = b + first;                  // batch rank of the first stored value
+            m_g[i] = tag;
+            m_start[i] = a.gstart[g] + first;
+            m_q0[i] = (int)(((int64_t)f0 + jb) % W);
+            m_s0[i] = (int)(((int64_t)a.next_pos[g] + f0 + jb) % W);
+            m_f0[i] = (K >= W) ? 0 : f0;               // k >= W: nothing old survives
+            m_off[i] = a.off[g];
+            m_delta[i] = 0;
+            m_min[i] = 0x7fffffff;
+            m_max[i] = (int32_t)0x80000000;
+            wk[q] = r_hi - first;
             tsum += wk[q];
         }
         int32_t total;
@@ -164,10 +154,11 @@ k_ingest(IngestArgs a) {
             ex += wk[q];
         }
         if (threadIdx.x == 0) m_scan[m] = total;
+        work_total += (unsigned long long)total;
         __syncthreads();
 
         // ---- exchange: kILP stored values per thread per round, all loads
-        // issued before any store (distinct slots within a round) -----------
+        // issued before any store (distinct slots within a batch) ----------
         for (int base = 0; base < total; base += kIngestThreads * kILP) {
             int mi[kILP];
             int32_t v[kILP], old[kILP];
@@ -234,85 +225,135 @@ k_ingest(IngestArgs a) {
         }
         __syncthreads();
 
-        // ---- finalise each member's state (shares go to K5) -----------------
+        // ---- fold into the per-group batch accumulators --------------------
         for (int i = threadIdx.x; i < m; i += kIngestThreads) {
-            const int g = m_g[i];
-            if (g == 0x7fffffff) continue;
-            if (m_scan[i + 1] == m_scan[i]) continue;     // no stored value
-            if (g < 0) {
-                const int sg = -1 - g;
-                atomicAdd(&a.split_delta[sg], m_delta[i]);
+            const int tag = m_g[i];
+            if (tag == 0x7fffffff) continue;
+            if (tag >= 0) {                 // whole group: this CTA is its only writer
+                a.bdelta[tag] += (long long)m_delta[i];
                 if (a.minmax) {
-                    atomicMin(&a.split_min[sg], m_min[i]);
-                    atomicMax(&a.split_max[sg], m_max[i]);
+                    a.bmin[tag] = min(a.bmin[tag], m_min[i]);
+                    a.bmax[tag] = max(a.bmax[tag], m_max[i]);
                 }
-                continue;
-            }
-            const int k = a.gcnt[g];
-            const int f0 = m_f0[i];
-            const int64_t tot = (int64_t)f0 + k;
-            const int p0 = a.next_pos[g];
-            a.fill[g] = (int32_t)min64(tot, W);
-            a.next_pos[g] = (int32_t)((p0 + max64(tot - W, 0)) % W);
-            a.wsum[g] = a.wsum[g] + (long long)m_delta[i];
-            if (a.minmax) {
-                if (tot <= W || k >= W) {
-                    // no old value survives alongside an eviction: monotone update
-                    const bool keep_old = (f0 > 0) && (k < W);
-                    a.mn[g] = keep_old ? min(a.mn[g], m_min[i]) : m_min[i];
-                    a.mx[g] = keep_old ? max(a.mx[g], m_max[i]) : m_max[i];
-                } else {
-                    a.rescan[atomicAdd(a.n_rescan, 1u)] = g;
+            } else {                        // a share of a split hot key
+                const int g = a.split_g[-1 - tag];
+                atomicAdd((unsigned long long*)&a.bdelta[g], m_delta[i]);
+                if (a.minmax) {
+                    atomicMin(&a.bmin[g], m_min[i]);
+                    atomicMax(&a.bmax[g], m_max[i]);
                 }
             }
-            a.gcnt[g] = 0;
         }
         __syncthreads();
     }
-    if (threadIdx.x == 0 && a.part_ns) atomicAdd(&a.part_ns[p], (unsigned long long)(globaltimer() - t0));
+    if (threadIdx.x == 0) {
+        if (a.part_ns) atomicAdd(&a.part_ns[p], (unsigned long long)(globaltimer() - t0));
+        if (a.part_work) atomicAdd(&a.part_work[p], work_total);
+    }
 }
 
-// K5: finalise split groups after all their shares ran.  One thread each.
-__global__ void k_split_finalize(IngestArgs a) {
-    const int sg = blockIdx.x * blockDim.x + threadIdx.x;
-    if (sg >= *a.n_split || *a.bad != (unsigned long long)kNoBad) return;
-    const int g = a.split_g[sg];
-    const int k = a.gcnt[g];
-    if (k > 0) {
-        const int W = (int)a.W;
+// K5: fold each touched group's batch delta into its window state, emit
+// its result row (group, COUNT, SUM, AVG, MIN, MAX; AVG = correctly
+// rounded double quotient) and reset the batch accumulators.
+struct FinalizeArgs {
+    const int32_t* gcount;
+    int32_t* gcnt;              // [n_sub][G] sub-batch counts, cleared here
+    int n_sub;
+    uint32_t G;
+    int64_t W;
+    int32_t* fill;
+    int32_t* next_pos;
+    long long* wsum;
+    int32_t* mn;
+    int32_t* mx;
+    long long* bdelta;
+    int32_t* bmin;
+    int32_t* bmax;
+    int minmax;
+    int emit;
+    unsigned* n_res;
+    int32_t* r_g;
+    int32_t* r_cnt;
+    long long* r_sum;
+    double* r_avg;
+    int32_t* r_mn;
+    int32_t* r_mx;
+    int2* rescan;               // (group, result row) whose MIN/MAX need a rescan
+    unsigned* n_rescan;
+    const unsigned long long* bad;
+};
+
+__global__ void __launch_bounds__(256)
+k_finalize(FinalizeArgs a) {
+    if (*a.bad != (unsigned long long)kNoBad) return;
+    const unsigned lane = lane_id();
+    const int W = (int)a.W;
+    for (uint32_t g0 = blockIdx.x * blockDim.x; g0 < a.G; g0 += gridDim.x * blockDim.x) {
+        const uint32_t g = g0 + threadIdx.x;
+        const int K = (g < a.G) ? a.gcount[g] : 0;
+        const bool t = K != 0;
+        unsigned slot = 0;
+        if (a.emit) {
+            const unsigned bal = __ballot_sync(SS_FULL, t);
+            unsigned base = 0;
+            if (lane == 0 && bal) base = atomicAdd(a.n_res, (unsigned)__popc(bal));
+            base = __shfl_sync(SS_FULL, base, 0);
+            slot = base + __popc(bal & lanemask_lt());
+        }
+        if (!t) continue;
         const int f0 = a.fill[g];
-        const int64_t tot = (int64_t)f0 + k;
+        const int64_t tot = (int64_t)f0 + K;
         const int p0 = a.next_pos[g];
-        a.fill[g] = (int32_t)min64(tot, W);
+        const int fill = (int)min64(tot, W);
+        a.fill[g] = fill;
         a.next_pos[g] = (int32_t)((p0 + max64(tot - W, 0)) % W);
-        a.wsum[g] = a.wsum[g] + (long long)a.split_delta[sg];
+        const long long d = a.bdelta[g];
+        const long long s = (K >= W) ? d : a.wsum[g] + d;
+        a.wsum[g] = s;
+        a.bdelta[g] = 0;
+        bool need_rescan = false;
+        int32_t lo = 0, hi = 0;
         if (a.minmax) {
-            if (tot <= W || k >= W) {
-                const bool keep_old = (f0 > 0) && (k < W);
-                a.mn[g] = keep_old ? min(a.mn[g], a.split_min[sg]) : a.split_min[sg];
-                a.mx[g] = keep_old ? max(a.mx[g], a.split_max[sg]) : a.split_max[sg];
+            const int32_t bl = a.bmin[g], bh = a.bmax[g];
+            if (tot <= W || K >= W) {
+                const bool keep_old = (f0 > 0) && (K < W);
+                lo = keep_old ? min(a.mn[g], bl) : bl;
+                hi = keep_old ? max(a.mx[g], bh) : bh;
+                a.mn[g] = lo;
+                a.mx[g] = hi;
             } else {
-                a.rescan[atomicAdd(a.n_rescan, 1u)] = g;
+                need_rescan = true;
+            }
+            a.bmin[g] = 0x7fffffff;
+            a.bmax[g] = (int32_t)0x80000000;
+        }
+        for (int s2 = 0; s2 < a.n_sub; ++s2) a.gcnt[(int64_t)s2 * a.G + g] = 0;
+        if (need_rescan) a.rescan[atomicAdd(a.n_rescan, 1u)] = make_int2((int)g, a.emit ? (int)slot : -1);
+        if (a.emit) {
+            a.r_g[slot] = (int32_t)g;
+            a.r_cnt[slot] = fill;
+            a.r_sum[slot] = s;
+            a.r_avg[slot] = __ll2double_rn(s) / (double)fill;
+            if (a.minmax) {
+                a.r_mn[slot] = lo;
+                a.r_mx[slot] = hi;
             }
         }
-        a.gcnt[g] = 0;
     }
-    a.split_delta[sg] = 0;
-    a.split_min[sg] = 0x7fffffff;
-    a.split_max[sg] = (int32_t)0x80000000;
 }
 
 // MIN/MAX of a full window after a partial eviction: every ring slot is
 // live, so the slot order does not matter.  One CTA per listed group.
 __global__ void __launch_bounds__(256)
-k_minmax_rescan(const int32_t* __restrict__ rescan, const unsigned* __restrict__ n_rescan,
+k_minmax_rescan(const int2* __restrict__ rescan, const unsigned* __restrict__ n_rescan,
                 const int32_t* __restrict__ ring, const int64_t* __restrict__ off, int64_t W,
-                int32_t* __restrict__ mn, int32_t* __restrict__ mx) {
+                int32_t* __restrict__ mn, int32_t* __restrict__ mx, int32_t* __restrict__ r_mn,
+                int32_t* __restrict__ r_mx) {
     __shared__ int32_t s_mn[8], s_mx[8];
     const unsigned n = *n_rescan;
     for (unsigned i = blockIdx.x; i < n; i += gridDim.x) {
-        const int g = rescan[i];
-        const int32_t* r = ring + off[g];
+        const int2 e = rescan[i];
+        const int32_t* r = ring + off[e.x];
         int32_t lo = 0x7fffffff, hi = (int32_t)0x80000000;
         for (int64_t j = threadIdx.x; j < W; j += blockDim.x) {
             const int32_t v = r[j];
@@ -325,19 +366,23 @@ k_minmax_rescan(const int32_t* __restrict__ rescan, const unsigned* __restrict__
         __syncthreads();
         if (threadIdx.x == 0) {
             for (int w = 1; w < 8; ++w) { lo = min(lo, s_mn[w]); hi = max(hi, s_mx[w]); }
-            mn[g] = lo;
-            mx[g] = hi;
+            mn[e.x] = lo;
+            mx[e.x] = hi;
+            if (e.y >= 0) {
+                r_mn[e.y] = lo;
+                r_mx[e.y] = hi;
+            }
         }
         __syncthreads();
     }
 }
 
-// Occupancy-proportional store: grow the ring region of every group whose
-// window will hold more values than its capacity (capacity doubles up to
-// W; a window that has not reached W is linear, next_pos == 0, so growth
-// copies `fill` values).  One warp per group.
+// Occupancy-proportional store: before a batch, grow the ring region of
+// every group whose window will hold more values than its capacity
+// (capacity doubles up to W; a window below W is linear, next_pos == 0,
+// so growth copies `fill` values).  One warp per 32 groups.
 __global__ void __launch_bounds__(256)
-k_reserve(const int32_t* __restrict__ gcnt, uint32_t G, int64_t W, const int32_t* __restrict__ fill,
+k_reserve(const int32_t* __restrict__ gcount, uint32_t G, int64_t W, const int32_t* __restrict__ fill,
           int64_t* __restrict__ off, int32_t* __restrict__ cap, int32_t* __restrict__ ring,
           unsigned long long* __restrict__ pool_top, unsigned long long pool_cap,
           int* __restrict__ oom, const unsigned long long* __restrict__ bad) {
@@ -346,16 +391,17 @@ k_reserve(const int32_t* __restrict__ gcnt, uint32_t G, int64_t W, const int32_t
     const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
     for (uint32_t g0 = (blockIdx.x * (blockDim.x >> 5) + warp_id()) * 32; g0 < G; g0 += nwarps * 32) {
         const uint32_t g = g0 + lane;
-        int64_t need = 0, ncap = 0, noff = 0;
-        int c = 0, f = 0;
+        int64_t ncap = 0, noff = 0, oldoff = 0;
+        int f = 0;
         if (g < G) {
-            const int k = gcnt[g];
+            const int k = gcount[g];
             if (k) {
                 f = fill[g];
-                c = cap[g];
-                need = min64((int64_t)f + k, W);
+                const int c = cap[g];
+                const int64_t need = min64((int64_t)f + k, W);
                 if (need > c) {
                     ncap = min64(W, max64(max64(need, 2 * (int64_t)c), 16));
+                    oldoff = off[g];
                 }
             }
         }
@@ -372,12 +418,12 @@ k_reserve(const int32_t* __restrict__ gcnt, uint32_t G, int64_t W, const int32_t
                 ncap = 0;
             }
         }
-        // copy live prefix (linear while filling), one group at a time per warp
+        // copy the live prefix (linear while filling), one group at a time
         unsigned todo = __ballot_sync(SS_FULL, ncap != 0);
         while (todo) {
             const int src = __ffs(todo) - 1;
             todo &= todo - 1;
-            const int64_t so = __shfl_sync(SS_FULL, off[g0 + src < G ? g0 + src : 0], src);
+            const int64_t so = __shfl_sync(SS_FULL, oldoff, src);
             const int64_t doff = __shfl_sync(SS_FULL, noff, src);
             const int ff = __shfl_sync(SS_FULL, f, src);
             for (int j = lane; j < ff; j += 32) ring[doff + j] = ring[so + j];
@@ -386,41 +432,6 @@ k_reserve(const int32_t* __restrict__ gcnt, uint32_t G, int64_t W, const int32_t
         if (ncap) {
             off[g] = noff;
             cap[g] = (int32_t)ncap;
-        }
-    }
-}
-
-// Per-batch result emission: every group touched by the batch gets a row
-// (group, COUNT, SUM, AVG, MIN, MAX); AVG is the correctly rounded double
-// quotient.  Also clears the batch counts for the next batch.
-__global__ void __launch_bounds__(256)
-k_emit(int32_t* __restrict__ gcount, uint32_t G, const int32_t* __restrict__ fill,
-       const long long* __restrict__ wsum, const int32_t* __restrict__ mn, const int32_t* __restrict__ mx,
-       int minmax, unsigned* __restrict__ n_res, int32_t* __restrict__ r_g, int32_t* __restrict__ r_cnt,
-       long long* __restrict__ r_sum, double* __restrict__ r_avg, int32_t* __restrict__ r_mn,
-       int32_t* __restrict__ r_mx, const unsigned long long* __restrict__ bad) {
-    if (*bad != (unsigned long long)kNoBad) return;
-    const unsigned lane = lane_id();
-    for (uint32_t g0 = blockIdx.x * blockDim.x; g0 < G; g0 += gridDim.x * blockDim.x) {
-        const uint32_t g = g0 + threadIdx.x;
-        const bool t = (g < G) && gcount[g] != 0;
-        const unsigned bal = __ballot_sync(SS_FULL, t);
-        unsigned base = 0;
-        if (lane == 0 && bal) base = atomicAdd(n_res, (unsigned)__popc(bal));
-        base = __shfl_sync(SS_FULL, base, 0);
-        if (t) {
-            const unsigned slot = base + __popc(bal & lanemask_lt());
-            const int32_t c = fill[g];
-            const long long s = wsum[g];
-            r_g[slot] = (int32_t)g;
-            r_cnt[slot] = c;
-            r_sum[slot] = s;
-            r_avg[slot] = c ? __ll2double_rn(s) / (double)c : 0.0;
-            if (minmax) {
-                r_mn[slot] = mn[g];
-                r_mx[slot] = mx[g];
-            }
-            gcount[g] = 0;
         }
     }
 }

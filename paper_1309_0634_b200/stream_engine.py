@@ -306,6 +306,11 @@ class StreamEngine:
         self._check(self._lib.ss_last_loads(self._h, _ptr(out)[0]))
         return out
 
+    def last_part_ns(self) -> np.ndarray:
+        out = np.empty(self.n_partitions, dtype=np.int64)
+        self._check(self._lib.ss_last_part_ns(self._h, _ptr(out)[0]))
+        return out
+
     def last_moves(self):
         cap = 4 * self.n_partitions
         arr = (L.MoveC * cap)()

@@ -1,6 +1,6 @@
 set -x
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi.txt
-timeout 600 python -m pytest tests -x -q -m gpu > gpurun_out/gpu_tests.log 2>&1
+timeout 900 python -m pytest tests -q -m gpu > gpurun_out/gpu_tests.log 2>&1
 timeout 300 python bench.py --steps 10 --warmup 3 --cpu-seconds 10 > gpurun_out/bench_c2.log 2>&1
 timeout 300 python bench.py --config c1 --steps 10 --warmup 3 --no-cpu > gpurun_out/bench_c1.log 2>&1
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches_c2.csv python bench.py --steps 2 --warmup 3 --no-cpu --e2e-steps 1 > /dev/null 2>&1

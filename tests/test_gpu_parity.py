@@ -289,5 +289,9 @@ def test_split_aggregates_match_oracle(policy):
     for gi in (0, 1, 2, 5, 100, G - 1):
         assert eng.contents(gi).tolist() == store.contents(gi).tolist()
     # without splitting the floor is P x top share ~ 24; with it, near 1
-    assert min(ratios[2:]) <= 1.3, ratios
+    # (policy 'no' never moves cold groups, so only the hot part is levelled)
+    if policy != "no":
+        assert min(ratios[2:]) <= 1.3, ratios
+    else:
+        assert max(ratios[2:]) < ratios[0] / 4, ratios
     eng.close()
