@@ -43,8 +43,10 @@ CONFIGS = {
            "uniform", 1.0, 1000, 1000, 1 << 24, ("count", "sum", "avg"), "no", False),
     "c2": ("C2 Zipf s=1.0, 10K groups, W=1e5, SUM+COUNT, prob_check group reassignment",
            "zipf", 1.0, 10_000, 100_000, 1 << 24, ("count", "sum"), "prob", False),
-    "c3": ("C3 Zipf s=1.5, 100K groups, W=1e6, AVG, prob_check",
-           "zipf", 1.5, 100_000, 1_000_000, 1 << 24, ("count", "sum", "avg"), "prob", False),
+    "c3": ("C3 Zipf s=1.5, 100K groups, W=1e6, AVG, hot-key splitting across blocks + prob_check for cold groups",
+           "zipf", 1.5, 100_000, 1_000_000, 1 << 24, ("count", "sum", "avg"), "prob", True),
+    "c2split": ("C2 shape with hot-key splitting on top of prob_check",
+                "zipf", 1.0, 10_000, 100_000, 1 << 24, ("count", "sum"), "prob", True),
 }
 P_DEFAULT = 148
 L2_BYTES = 126 * (1 << 20)
@@ -241,7 +243,7 @@ def main():
     stream = torch.cuda.Stream(device=dev)
     eng.set_stream(stream)
     thr = max(1, B // (10 * P))
-    bal = eng.balancer_struct(policy, thread_threshold=thr, pot=0.5)
+    bal = eng.balancer_struct(policy, thread_threshold=thr, pot=0.5, split=split)
     nbuf = 4
     batches = make_batches(kind, s, G, B, nbuf, dev, seed=1234 + rank)
     torch.cuda.synchronize()
@@ -364,7 +366,7 @@ def main():
             "data": f"synthetic {kind} (s={s}) keys generated on device, uniform int32 attrs; "
                     f"{nbuf} staged batches of {B * 8 >> 20} MB each (> L2), cycled",
             "config": {"workload": desc, "groups": G, "window": W, "batch": B,
-                       "partitions": P, "policy": policy, "aggregates": list(aggs),
+                       "partitions": P, "policy": policy + ("+split" if split else ""), "aggregates": list(aggs),
                        "sub_batch": eng_sub, "l2": "inputs larger than L2 (128 MB per batch)",
                        "parallelism": f"key-sharded x{world}" if world > 1 else "single GPU"},
             "roofline": {"bound": "hbm", "kernel": main_cls, "achieved": achieved, "peak": peak,

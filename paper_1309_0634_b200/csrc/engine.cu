@@ -237,8 +237,8 @@ void launch_sort(cudaStream_t st, const uint32_t* kin, const int32_t* vin, uint3
                  uint32_t epoch, uint32_t* ticket, const unsigned long long* bad, int stream_in) {
     const int tiles = (n + kSortTile - 1) / kSortTile;
     if (tiles == 0) return;
-    k_sort_pass<RB><<<tiles, kSortThreads, 0, st>>>(kin, vin, kout, vout, n, shift, mask, base, status,
-                                                    epoch, ticket, bad, stream_in);
+    k_sort_pass<RB><<<tiles, kSortThreads, SortSmem<RB>::bytes, st>>>(kin, vin, kout, vout, n, shift, mask, base,
+                                                                      status, epoch, ticket, bad, stream_in);
 }
 
 void sort_dispatch(int rb, cudaStream_t st, const uint32_t* kin, const int32_t* vin, uint32_t* kout,
@@ -550,6 +550,12 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
     memset(e->h_rep, 0, sizeof(DevReport));
     e->h_rep->bad = (unsigned long long)kNoBad;
     SS_CUDA(e, cudaFuncSetAttribute(k_count<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    SS_CUDA(e, cudaFuncSetAttribute(k_sort_pass<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SortSmem<4>::bytes));
+    SS_CUDA(e, cudaFuncSetAttribute(k_sort_pass<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SortSmem<6>::bytes));
+    SS_CUDA(e, cudaFuncSetAttribute(k_sort_pass<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SortSmem<8>::bytes));
+    SS_CUDA(e, cudaFuncSetAttribute(k_sort_pass<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SortSmem<9>::bytes));
+    SS_CUDA(e, cudaFuncSetAttribute(k_sort_pass<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SortSmem<10>::bytes));
+    SS_CUDA(e, cudaFuncSetAttribute(k_sort_pass<11>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SortSmem<11>::bytes));
     SS_CUDA(e, cudaFuncSetAttribute(k_ingest, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kIngestSmem));
     SS_CUDA(e, cudaFuncSetAttribute(k_balance, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     SS_CUDA(e, cudaFuncSetAttribute(k_split_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -648,7 +654,7 @@ static int launch_count(ss_engine* e, const uint32_t* dk, int64_t n, int64_t S) 
 static int launch_stats(ss_engine* e, int n_sub) {
     SS_CUDA(e, cudaMemsetAsync(e->tpt, 0, e->P * 8, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->touched, 0, 8, e->st));
-    k_batch_stats<<<2 * kNumSM, 1024, e->P * 8, e->st>>>(e->gcnt, n_sub, (uint32_t)e->G, e->pmap, e->P, e->gcount,
+    k_batch_stats<<<2 * kNumSM, 1024, e->P * 4, e->st>>>(e->gcnt, n_sub, (uint32_t)e->G, e->pmap, e->P, e->gcount,
                                                           e->tpt, e->touched, e->bad, e->fill, e->W,
                                                           e->alg_bytes, e->gpre);
     SS_CUDA(e, cudaGetLastError());

@@ -23,8 +23,8 @@ namespace ss {
 
 constexpr int kScanBlk = 4096;   // groups per block in the G-sized scans
 constexpr int kMaxBins = 2048;   // radix digit <= 11 bits
-constexpr int kSortThreads = 256;
-constexpr int kSortItems = 16;
+constexpr int kSortThreads = 512;
+constexpr int kSortItems = 8;
 constexpr int kSortTile = kSortThreads * kSortItems;   // 4096 tuples
 
 // --------------------------------------------------------------------------
@@ -91,7 +91,7 @@ k_batch_stats(const int32_t* __restrict__ gcnt, int n_sub, uint32_t G, const int
               unsigned long long* __restrict__ touched, const unsigned long long* __restrict__ bad,
               const int32_t* __restrict__ fill, int64_t W, unsigned long long* __restrict__ alg_bytes,
               int32_t* __restrict__ gpre) {
-    extern __shared__ unsigned long long sh_tpt[];
+    extern __shared__ uint32_t sh_tpt[];     // per-CTA partial loads (< 2^31)
     if (*bad != (unsigned long long)kNoBad) return;
     for (int p = threadIdx.x; p < P; p += blockDim.x) sh_tpt[p] = 0;
     __syncthreads();
@@ -105,7 +105,7 @@ k_batch_stats(const int32_t* __restrict__ gcnt, int n_sub, uint32_t G, const int
         }
         gcount[g] = c;
         if (c) {
-            atomicAdd(&sh_tpt[pmap[g]], (unsigned long long)c);
+            atomicAdd(&sh_tpt[pmap[g]], (uint32_t)c);
             ++my_touched;
             // algorithmic bytes: stored values, retracted old
             // values that must be read, state + result row
@@ -122,7 +122,7 @@ k_batch_stats(const int32_t* __restrict__ gcnt, int n_sub, uint32_t G, const int
     }
     __syncthreads();
     for (int p = threadIdx.x; p < P; p += blockDim.x)
-        if (sh_tpt[p]) atomicAdd(&tpt[p], sh_tpt[p]);
+        if (sh_tpt[p]) atomicAdd(&tpt[p], (unsigned long long)sh_tpt[p]);
 }
 
 // --------------------------------------------------------------------------
@@ -230,16 +230,25 @@ k_scan_down(const int32_t* __restrict__ gcnt, uint32_t G, const int32_t* __restr
 // --------------------------------------------------------------------------
 // K3: one stable LSD multisplit pass with decoupled look-back.
 //
-// A tile of 4096 tuples is ranked warp by warp: each warp owns 512
-// consecutive tuples held warp-striped (item j of lane l = tuple j*32+l),
-// ranks them in arrival order with __match_any_sync against a per-warp
-// digit histogram, and the per-bin prefix across warps, across earlier
-// tiles (look-back) and across lower digits (bin base) gives the output
-// position.  Tile ids come from an atomic ticket so a tile only ever waits
-// on tiles that are already resident.
+// A tile of 4096 tuples is ranked warp by warp: each of the 16 warps owns
+// 256 consecutive tuples held warp-striped (item j of lane l = tuple
+// j*32+l) and ranks them in arrival order with __match_any_sync against a
+// per-warp digit histogram.  Per-bin prefixes across warps, across bins
+// of the tile, across earlier tiles (look-back on [epoch|flag|count] words)
+// and across lower digits (bin base) give the output position.  The tile
+// is first sorted in shared memory, so the global writes are contiguous
+// runs per digit.  Tile ids come from an atomic ticket so a tile only ever
+// waits on tiles that are already resident.
 // --------------------------------------------------------------------------
 template <int RB>
-__global__ void __launch_bounds__(kSortThreads)
+struct SortSmem {
+    static constexpr int BINS = 1 << RB;
+    static constexpr int NW = kSortThreads / 32;
+    static constexpr size_t bytes = (size_t)NW * BINS * 2 + (size_t)BINS * 8 + (size_t)kSortTile * 8 + 16;
+};
+
+template <int RB>
+__global__ void __launch_bounds__(kSortThreads, 2)
 k_sort_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
             uint32_t* __restrict__ kout, int32_t* __restrict__ vout, int n, int shift, uint32_t mask,
             const uint32_t* __restrict__ bin_base, unsigned long long* __restrict__ status,
@@ -247,31 +256,39 @@ k_sort_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
             int stream_in) {
     constexpr int BINS = 1 << RB;
     constexpr int NW = kSortThreads / 32;
-    constexpr int BPT = (BINS + kSortThreads - 1) / kSortThreads;   // bins per thread
-    __shared__ uint16_t whist[NW][BINS];
-    __shared__ uint32_t gbase[BINS];
+    constexpr int BPT = (BINS + kSortThreads - 1) / kSortThreads;   // bins owned per thread
+    extern __shared__ __align__(16) unsigned char sort_sm[];
+    uint32_t* skey = (uint32_t*)sort_sm;                     // [TILE]
+    int32_t* sval = (int32_t*)(skey + kSortTile);            // [TILE]
+    uint32_t* tbin = (uint32_t*)(sval + kSortTile);          // [BINS] tile-local bin start
+    uint32_t* gbase = tbin + BINS;                           // [BINS] global pos of local pos 0
+    uint16_t* whist = (uint16_t*)(gbase + BINS);             // [NW][BINS]
     __shared__ uint32_t sh_tile;
+    __shared__ uint32_t sh_red[33];
     if (*bad != (unsigned long long)kNoBad) return;
     if (threadIdx.x == 0) sh_tile = atomicAdd(ticket, 1u);
-    for (int i = threadIdx.x; i < NW * BINS; i += kSortThreads) (&whist[0][0])[i] = 0;
+    for (int i = threadIdx.x; i < NW * BINS / 2; i += kSortThreads) ((uint32_t*)whist)[i] = 0;
     __syncthreads();
     const uint32_t tile = sh_tile;
     const unsigned w = warp_id(), lane = lane_id();
-    const int64_t base = (int64_t)tile * kSortTile + (int64_t)w * 32 * kSortItems;
+    const int64_t tile0 = (int64_t)tile * kSortTile;
+    const int tile_n = (int)min64(kSortTile, (int64_t)n - tile0);
+    const int wbase = (int)w * 32 * kSortItems;
+    uint16_t* myh = whist + w * BINS;
 
     uint32_t key[kSortItems];
     int32_t val[kSortItems];
-    uint16_t rank[kSortItems];
+    uint32_t rank[kSortItems];
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
-        const int64_t idx = base + j * 32 + lane;
-        if (idx < n) {
+        const int li = wbase + j * 32 + (int)lane;
+        if (li < tile_n) {
             if (stream_in) {
-                key[j] = ld_stream_u32(kin + idx);
-                val[j] = (int32_t)ld_stream_u32(vin + idx);
+                key[j] = ld_stream_u32(kin + tile0 + li);
+                val[j] = (int32_t)ld_stream_u32(vin + tile0 + li);
             } else {
-                key[j] = kin[idx];
-                val[j] = vin[idx];
+                key[j] = kin[tile0 + li];
+                val[j] = vin[tile0 + li];
             }
         } else {
             key[j] = 0xffffffffu;
@@ -281,42 +298,53 @@ k_sort_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
     const unsigned lt = lanemask_lt();
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
-        const int64_t idx = base + j * 32 + lane;
-        const bool valid = idx < n;
+        const bool valid = wbase + j * 32 + (int)lane < tile_n;
         const uint32_t d = valid ? ((key[j] >> shift) & mask) : 0xffffffffu;
         const unsigned peers = __match_any_sync(SS_FULL, d);
         uint32_t r = 0;
-        if (valid) r = whist[w][d];
+        if (valid) r = myh[d];
         __syncwarp();
         if (valid) {
-            rank[j] = (uint16_t)(r + __popc(peers & lt));
-            if (lane == 31u - __clz(peers)) whist[w][d] = (uint16_t)(r + __popc(peers));
+            rank[j] = r + __popc(peers & lt);
+            if (lane == 31u - __clz(peers)) myh[d] = (uint16_t)(r + __popc(peers));
         }
         __syncwarp();
     }
     __syncthreads();
-    // per-bin: exclusive prefix across warps, tile total, look-back
+    // per owned bin: exclusive prefix across warps and the tile total
     uint32_t tot[BPT];
+    uint32_t tsum = 0;
 #pragma unroll
     for (int q = 0; q < BPT; ++q) {
-        const int b = threadIdx.x + q * kSortThreads;
+        const int b = threadIdx.x * BPT + q;
         tot[q] = 0;
         if (b < BINS) {
             uint32_t run = 0;
 #pragma unroll
             for (int ww = 0; ww < NW; ++ww) {
-                const uint32_t c = whist[ww][b];
-                whist[ww][b] = (uint16_t)run;
+                const uint32_t c = whist[ww * BINS + b];
+                whist[ww * BINS + b] = (uint16_t)run;
                 run += c;
             }
             tot[q] = run;
             st_relaxed_u64(&status[(int64_t)tile * BINS + b],
                            lb_pack(epoch, tile == 0 ? kFlagInc : kFlagAgg, run));
         }
+        tsum += tot[q];
     }
+    // tile-local bin starts (bins are owned contiguously, so one block scan)
+    uint32_t ttot;
+    uint32_t lex = block_excl_scan(tsum, sh_red, &ttot);
 #pragma unroll
     for (int q = 0; q < BPT; ++q) {
-        const int b = threadIdx.x + q * kSortThreads;
+        const int b = threadIdx.x * BPT + q;
+        if (b < BINS) tbin[b] = lex;
+        lex += tot[q];
+    }
+    // look-back across tiles
+#pragma unroll
+    for (int q = 0; q < BPT; ++q) {
+        const int b = threadIdx.x * BPT + q;
         if (b < BINS) {
             uint32_t excl = 0;
             if (tile > 0) {
@@ -332,19 +360,27 @@ k_sort_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
                 }
                 st_relaxed_u64(&status[(int64_t)tile * BINS + b], lb_pack(epoch, kFlagInc, excl + tot[q]));
             }
-            gbase[b] = bin_base[b] + excl;
+            gbase[b] = bin_base[b] + excl - tbin[b];
         }
     }
     __syncthreads();
+    // tile-local sort into shared memory
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
-        const int64_t idx = base + j * 32 + lane;
-        if (idx < n) {
+        if (wbase + j * 32 + (int)lane < tile_n) {
             const uint32_t d = (key[j] >> shift) & mask;
-            const uint32_t pos = gbase[d] + whist[w][d] + rank[j];
-            vout[pos] = val[j];
-            if (kout) kout[pos] = key[j];
+            const uint32_t lp = tbin[d] + myh[d] + rank[j];
+            skey[lp] = key[j];
+            sval[lp] = val[j];
         }
+    }
+    __syncthreads();
+    // contiguous runs per digit to global memory
+    for (int i = threadIdx.x; i < tile_n; i += kSortThreads) {
+        const uint32_t k = skey[i];
+        const uint32_t pos = gbase[(k >> shift) & mask] + (uint32_t)i;
+        vout[pos] = sval[i];
+        if (kout) kout[pos] = k;
     }
 }
 

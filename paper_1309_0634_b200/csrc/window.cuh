@@ -76,8 +76,11 @@ __global__ void __launch_bounds__(kIngestThreads)
 k_ingest(IngestArgs a) {
     extern __shared__ __align__(16) unsigned char ingest_sm[];
     int64_t* m_off = (int64_t*)ingest_sm;
-    unsigned long long* m_delta = (unsigned long long*)(m_off + kMemberChunk);
-    int32_t* m_g = (int32_t*)(m_delta + kMemberChunk);
+    // 64-bit shared atomics are CAS loops on sm_100; the per-member delta is
+    // kept as two native 32-bit words (low word + carries into the high word)
+    uint32_t* m_dlo = (uint32_t*)(m_off + kMemberChunk);
+    uint32_t* m_dhi = m_dlo + kMemberChunk;
+    int32_t* m_g = (int32_t*)(m_dhi + kMemberChunk);
     int32_t* m_scan = m_g + kMemberChunk;            // kMemberChunk + 1
     int32_t* m_start = m_scan + kMemberChunk + 4;
     int32_t* m_q0 = m_start + kMemberChunk;
@@ -139,7 +142,8 @@ k_ingest(IngestArgs a) {
             m_s0[i] = (int)(((int64_t)a.next_pos[g] + f0 + jb) % W);
             m_f0[i] = (K >= W) ? 0 : f0;               // k >= W: nothing old survives
             m_off[i] = a.off[g];
-            m_delta[i] = 0;
+            m_dlo[i] = 0;
+            m_dhi[i] = 0;
             m_min[i] = 0x7fffffff;
             m_max[i] = (int32_t)0x80000000;
             wk[q] = r_hi - first;
@@ -212,7 +216,13 @@ k_ingest(IngestArgs a) {
                 const unsigned seg_end = 31u - __clz(peers);
                 const long long tot = seg_sum(d, seg_end);
                 const bool leader = valid && lane == (unsigned)(__ffs(peers) - 1);
-                if (leader) atomicAdd(&m_delta[mi[u]], (unsigned long long)tot);
+                if (leader) {
+                    const unsigned long long x = (unsigned long long)tot;
+                    const uint32_t lo32 = (uint32_t)x;
+                    const uint32_t prev = atomicAdd(&m_dlo[mi[u]], lo32);
+                    const uint32_t carry = (prev + lo32 < prev) ? 1u : 0u;
+                    atomicAdd(&m_dhi[mi[u]], (uint32_t)(x >> 32) + carry);
+                }
                 if (a.minmax && valid) {
                     const int32_t mnv = __reduce_min_sync(peers, v[u]);
                     const int32_t mxv = __reduce_max_sync(peers, v[u]);
@@ -229,15 +239,16 @@ k_ingest(IngestArgs a) {
         for (int i = threadIdx.x; i < m; i += kIngestThreads) {
             const int tag = m_g[i];
             if (tag == 0x7fffffff) continue;
+            const unsigned long long md = ((unsigned long long)m_dhi[i] << 32) | m_dlo[i];
             if (tag >= 0) {                 // whole group: this CTA is its only writer
-                a.bdelta[tag] += (long long)m_delta[i];
+                a.bdelta[tag] += (long long)md;
                 if (a.minmax) {
                     a.bmin[tag] = min(a.bmin[tag], m_min[i]);
                     a.bmax[tag] = max(a.bmax[tag], m_max[i]);
                 }
             } else {                        // a share of a split hot key
                 const int g = a.split_g[-1 - tag];
-                atomicAdd((unsigned long long*)&a.bdelta[g], m_delta[i]);
+                atomicAdd((unsigned long long*)&a.bdelta[g], md);
                 if (a.minmax) {
                     atomicMin(&a.bmin[g], m_min[i]);
                     atomicMax(&a.bmax[g], m_max[i]);
