@@ -238,11 +238,24 @@ def main():
     if args.batch:
         B = args.batch
     P = args.partitions
-    eng = StreamEngine(G, W, n_partitions=P, aggregates=aggs, device=local, max_batch=B,
-                       sub_batch=args.sub_batch)
     stream = torch.cuda.Stream(device=dev)
-    eng.set_stream(stream)
+    torch.cuda.set_stream(stream)          # NCCL routing and the engine share one stream
     thr = max(1, B // (10 * P))
+    sharded = None
+    if world > 1:
+        # key-sharded: each rank's B tuples are its slice of a global batch of
+        # world*B; tuples travel to their owner GPU by NCCL all-to-all, and the
+        # GPU-level balancer (prob_check on all-reduced counts) moves groups
+        # between GPUs (weak scaling: per-rank input fixed)
+        from paper_1309_0634_b200.sharded import ShardedEngine
+        sharded = ShardedEngine(G, W, n_partitions=P, aggregates=aggs, device=local, max_batch=world * B,
+                                sub_batch=args.sub_batch)
+        eng = sharded.local
+        gbal = eng.balancer_struct("prob", thread_threshold=max(1, B // 10), pot=0.5)
+    else:
+        eng = StreamEngine(G, W, n_partitions=P, aggregates=aggs, device=local, max_batch=B,
+                           sub_batch=args.sub_batch)
+    eng.set_stream(stream)
     bal = eng.balancer_struct(policy, thread_threshold=thr, pot=0.5, split=split)
     nbuf = 4
     batches = make_batches(kind, s, G, B, nbuf, dev, seed=1234 + rank)
@@ -256,7 +269,10 @@ def main():
     def run_steps(k, start=0):
         for i in range(k):
             g, a = batches[(start + i) % nbuf]
-            eng.step(g, a, bal, sync=False)
+            if sharded is not None:
+                sharded.step(g, a, bal, gbal)
+            else:
+                eng.step(g, a, bal, sync=False)
 
     # warm-up (also converges the balancer from the contiguous assignment)
     for i in range(args.warmup):
@@ -333,7 +349,10 @@ def main():
     e0.record(stream)
     for i in range(e2e_steps):
         hg, ha = hosts[i % 2]
-        eng.step(hg, ha, bal, sync=False)
+        if sharded is not None:
+            sharded.step(hg, ha, bal, gbal)
+        else:
+            eng.step(hg, ha, bal, sync=False)
         lib.ss_results_raw(eng._h, G, res_g.ctypes.data_as(C.c_void_p), res_a.ctypes.data_as(C.c_void_p),
                            C.byref(res_n))
         d2h += res_n.value * 12 + 4
@@ -368,7 +387,9 @@ def main():
             "config": {"workload": desc, "groups": G, "window": W, "batch": B,
                        "partitions": P, "policy": policy + ("+split" if split else ""), "aggregates": list(aggs),
                        "sub_batch": eng_sub, "l2": "inputs larger than L2 (128 MB per batch)",
-                       "parallelism": f"key-sharded x{world}" if world > 1 else "single GPU"},
+                       "parallelism": (f"key-sharded x{world}: NCCL all-to-all routing, GPU-level prob_check"
+                                       if world > 1 else "single GPU"),
+                       "global_batch": B * world},
             "roofline": {"bound": "hbm", "kernel": main_cls, "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak, "traffic": None,
                          "peak_source": peak_kind,
@@ -387,7 +408,10 @@ def main():
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)
-    eng.close()
+    if sharded is not None:
+        sharded.close()
+    else:
+        eng.close()
     if world > 1:
         dist.destroy_process_group()
 

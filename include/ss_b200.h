@@ -158,6 +158,25 @@ int  ss_export_values(ss_engine* e, int64_t group, int64_t* out, int64_t cap, in
 int  ss_results(ss_engine* e, int64_t cap, int32_t* groups, int64_t* count, int64_t* sum,
                 double* avg, int32_t* mn, int32_t* mx, int64_t* n);
 
+/* ---- multi-GPU: groups shard by key across GPUs ----------- */
+/* owner_of[G] in [0, n_dest), n_dest <= 16 */
+int  ss_set_owner(ss_engine* e, const int32_t* owner_of, int n_dest);
+/* stable split of a batch by owning GPU (arrival order kept per owner);
+ * counts[n_dest] tuples per destination */
+int  ss_route(ss_engine* e, const uint32_t* groups, const int32_t* attrs, int64_t n,
+              uint32_t* out_groups, int32_t* out_attrs, int64_t* counts);
+/* per-group counts of the last step's batch */
+int  ss_group_counts(ss_engine* e, int32_t* counts);
+/* policy on given per-group counts (BatchStats.group_counts, balance.py:175-385) */
+int  ss_balance_counts(ss_engine* e, const int32_t* counts, const ss_balancer* cfg, ss_move* moves,
+                       int64_t* n_moves, int64_t* scanned, int64_t* final_tpt);
+/* window-state migration: meta[5n] = (fill, next_pos, sum, min, max), values
+ * = ring images (span = fill if fill < W else W) concatenated */
+int  ss_export_state(ss_engine* e, const int32_t* groups, int64_t n, int64_t* meta, int32_t* values,
+                     int64_t cap, int64_t* n_values);
+int  ss_import_state(ss_engine* e, const int32_t* groups, int64_t n, const int64_t* meta,
+                     const int32_t* values);
+
 /* ---- measurement ------------------------------------------------------
  * Kernel classes timed with CUDA events on the engine stream while
  * profiling is enabled (bench.py's roofline numbers). */

@@ -78,6 +78,12 @@ _SIGS = {
     "ss_profile_read": (C.c_int, [_P, _P, _P, C.c_int]),
     "ss_alg_bytes": (C.c_int, [_P, _P, C.c_int]),
     "ss_results_raw": (C.c_int, [_P, _I64, _P, _P, _P]),
+    "ss_set_owner": (C.c_int, [_P, _P, C.c_int]),
+    "ss_route": (C.c_int, [_P, _P, _P, _I64, _P, _P, _P]),
+    "ss_group_counts": (C.c_int, [_P, _P]),
+    "ss_balance_counts": (C.c_int, [_P, _P, C.POINTER(Balancer), _P, _P, _P, _P]),
+    "ss_export_state": (C.c_int, [_P, _P, _I64, _P, _P, _I64, _P]),
+    "ss_import_state": (C.c_int, [_P, _P, _I64, _P, _P]),
 }
 KERNEL_CLASSES = ("count", "stats", "place", "ingest", "emit", "apply", "balance")
 EXPORTS = tuple(_SIGS)

@@ -24,7 +24,7 @@
 
 namespace ss {
 
-constexpr int kBalThreads = 1024;
+constexpr int kBalThreads = 512;        // co-resides with a K4 CTA on its SM
 
 struct BalanceArgs {
     int policy;

@@ -90,6 +90,11 @@ struct ss_engine {
     long long* bdelta = nullptr;           // per-group batch delta
     int32_t *bmin = nullptr, *bmax = nullptr;
     unsigned long long* part_work = nullptr;
+    RingCopy* copies = nullptr;            // ring growth copies (sparse store)
+    unsigned* n_copies = nullptr;
+    int32_t *hot_of = nullptr, *hot_g = nullptr;   // count-kernel hot cache (large G)
+    int* n_hot_dev = nullptr;
+    int n_hot = 0;                                 // host copy (read at the report sync)
     bool side_pending = false;             // policy/apply of the last batch still on the side stream
     cudaEvent_t ev_k4 = nullptr, ev_apply = nullptr;
     uint32_t* dhist = nullptr;
@@ -113,6 +118,12 @@ struct ss_engine {
     int* prev_moves = nullptr;
 
     uint32_t* kbuf2 = nullptr;             // sorted keys (reorder only)
+
+    // multi-GPU routing: group -> owning GPU
+    int32_t* owner = nullptr;
+    int n_dest = 0;
+    unsigned long long* route_cnt = nullptr;   // [16]
+    uint32_t* route_base = nullptr;            // [16]
 
     // hot-key split plans (split.cuh), double-buffered: plan[cur] executes
     // batch t while the planner writes plan[cur ^ 1] for batch t+1
@@ -419,7 +430,8 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
     // -- window store
     if ((rc = dalloc(e, &e->fill, G)) || (rc = dalloc(e, &e->next_pos, G)) || (rc = dalloc(e, &e->wsum, G)) ||
         (rc = dalloc(e, &e->mn, G)) || (rc = dalloc(e, &e->mx, G)) || (rc = dalloc(e, &e->cap, G)) ||
-        (rc = dalloc(e, &e->off, G)) || (rc = dalloc(e, &e->pool_top, 1)) || (rc = dalloc(e, &e->oom, 1)))
+        (rc = dalloc(e, &e->off, G)) || (rc = dalloc(e, &e->pool_top, 1)) || (rc = dalloc(e, &e->oom, 1)) ||
+        (rc = dalloc(e, &e->copies, G)) || (rc = dalloc(e, &e->n_copies, 1)))
         return rc;
     SS_CUDA(e, cudaMemsetAsync(e->fill, 0, G * 4, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->next_pos, 0, G * 4, e->st));
@@ -499,8 +511,11 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
         (rc = dalloc(e, &e->dhist, (size_t)nsub * 2 * kMaxBins)) || (rc = dalloc(e, &e->tpt, e->P)) ||
         (rc = dalloc(e, &e->touched, 1)) || (rc = dalloc(e, &e->bad, 1)) ||
         (rc = dalloc(e, &e->tickets, (size_t)nsub * 2 + 2)) || (rc = dalloc(e, &e->gpre, (size_t)nsub * G)) ||
-        (rc = dalloc(e, &e->bdelta, G)) || (rc = dalloc(e, &e->bmin, G)) || (rc = dalloc(e, &e->bmax, G)))
+        (rc = dalloc(e, &e->bdelta, G)) || (rc = dalloc(e, &e->bmin, G)) || (rc = dalloc(e, &e->bmax, G)) ||
+        (rc = dalloc(e, &e->hot_of, G)) || (rc = dalloc(e, &e->hot_g, kHotCache)) || (rc = dalloc(e, &e->n_hot_dev, 1)))
         return rc;
+    SS_CUDA(e, cudaMemsetAsync(e->hot_of, 0xff, G * 4, e->st));
+    SS_CUDA(e, cudaMemsetAsync(e->n_hot_dev, 0, 4, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->bdelta, 0, G * 8, e->st));
     k_fill_i32<<<296, 256, 0, e->st>>>(e->bmin, G, 0x7fffffff);
     k_fill_i32<<<296, 256, 0, e->st>>>(e->bmax, G, (int32_t)0x80000000);
@@ -556,6 +571,8 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
     SS_CUDA(e, cudaFuncSetAttribute(k_sort_pass<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SortSmem<9>::bytes));
     SS_CUDA(e, cudaFuncSetAttribute(k_sort_pass<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SortSmem<10>::bytes));
     SS_CUDA(e, cudaFuncSetAttribute(k_sort_pass<11>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SortSmem<11>::bytes));
+    SS_CUDA(e, cudaFuncSetAttribute(k_sort_pass<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)SortSmem<4>::bytes));
     SS_CUDA(e, cudaFuncSetAttribute(k_ingest, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kIngestSmem));
     SS_CUDA(e, cudaFuncSetAttribute(k_balance, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     SS_CUDA(e, cudaFuncSetAttribute(k_split_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -633,19 +650,22 @@ static int data_error(ss_engine* e, unsigned long long idx, const uint32_t* dkey
 }
 
 // K2 over n tuples with sub-batch size S (n_sub = ceil(n / S))
-static int launch_count(ss_engine* e, const uint32_t* dk, int64_t n, int64_t S) {
+static int launch_count(ss_engine* e, const uint32_t* dk, int64_t n, int64_t S, bool use_hot = false) {
     if (n == 0) return SS_OK;
     const int vec_ok = ((uintptr_t)dk % 16) == 0;
     if (e->G <= 16384) {
         // larger chunks amortise the per-CTA flush of the G-bin histogram
         const int64_t chunk = (e->G > 2048 && S % 65536 == 0) ? 65536 : kCountChunk;
         const int64_t grid = (n + chunk - 1) / chunk;
-        k_count<true><<<(unsigned)grid, 512, e->G * 4, e->st>>>(dk, n, (uint32_t)e->G, S, chunk, e->gcnt,
-                                                               e->bad, vec_ok);
+        k_count<true><<<(unsigned)grid, 512, e->G * 4, e->st>>>(dk, n, (uint32_t)e->G, S, chunk, e->gcnt, e->bad,
+                                                               vec_ok, nullptr, nullptr, 0);
     } else {
+        // the hot cache holds the previous batch's hot groups; its size is
+        // fixed at kHotCache slots (unused slots count nothing)
         const int64_t grid = (n + kCountChunk - 1) / kCountChunk;
-        k_count<false><<<(unsigned)grid, 512, 0, e->st>>>(dk, n, (uint32_t)e->G, S, kCountChunk, e->gcnt, e->bad,
-                                                         vec_ok);
+        const int nh = use_hot ? kHotCache : 0;
+        k_count<false><<<(unsigned)grid, 512, (size_t)nh * 4, e->st>>>(dk, n, (uint32_t)e->G, S, kCountChunk, e->gcnt,
+                                                                      e->bad, vec_ok, e->hot_of, e->hot_g, nh);
     }
     SS_CUDA(e, cudaGetLastError());
     return SS_OK;
@@ -767,7 +787,7 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
     if (e->minmax) SS_CUDA(e, cudaMemsetAsync(e->n_rescan, 0, 4, e->st));
     {
         ProfScope ps(e, SS_K_COUNT, e->st);
-        if ((rc = launch_count(e, dk, n, e->S))) return rc;
+        if ((rc = launch_count(e, dk, n, e->S, e->G > 16384))) return rc;
     }
     if (e->side_pending) {
         SS_CUDA(e, cudaStreamWaitEvent(e->st, e->ev_apply, 0));
@@ -782,6 +802,13 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
         if (use_plan)
             k_split_loads<<<2 * kNumSM, 256, 0, e->st>>>(e->gcount, (uint32_t)e->G, e->pmap, e->P,
                                                          e->plan_buf[e->plan_cur], e->loads, e->bad);
+        if (e->G > 16384) {
+            // hot cache for the next batch's count: > 1/(4 kHotCache) of the batch
+            SS_CUDA(e, cudaMemsetAsync(e->n_hot_dev, 0, 4, e->st));
+            k_hot_select<<<2 * kNumSM, 256, 0, e->st>>>(e->gcount, (uint32_t)e->G,
+                                                        std::max<long long>(32, n / (4 * kHotCache)), e->hot_of,
+                                                        e->hot_g, e->n_hot_dev, e->bad);
+        }
     }
     e->alg_input += 8 * n;
     if (run_side) {
@@ -835,8 +862,10 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
     }
     if (!e->dense) {
         ProfScope ps(e, SS_K_INGEST, e->st);
-        k_reserve<<<2 * kNumSM, 256, 0, e->st>>>(e->gcount, (uint32_t)e->G, e->W, e->fill, e->off, e->cap, e->ring,
-                                                 e->pool_top, e->pool_cap, e->oom, e->bad);
+        SS_CUDA(e, cudaMemsetAsync(e->n_copies, 0, 4, e->st));
+        k_reserve<<<2 * kNumSM, 256, 0, e->st>>>(e->gcount, (uint32_t)e->G, e->W, e->fill, e->off, e->cap,
+                                                 e->pool_top, e->pool_cap, e->oom, e->copies, e->n_copies, e->bad);
+        k_ring_copy<<<8 * kNumSM, 256, 0, e->st>>>(e->copies, e->n_copies, e->ring);
     }
     for (int s = 0; s < n_sub; ++s) {
         const int64_t lo = (int64_t)s * e->S;
@@ -1442,5 +1471,235 @@ extern "C" int ss_results_raw(ss_engine* e, int64_t cap, int32_t* groups, double
     if (m > 0 && groups) SS_CUDA(e, cudaMemcpyAsync(groups, e->r_g, m * 4, cudaMemcpyDeviceToHost, e->st));
     if (m > 0 && avg) SS_CUDA(e, cudaMemcpyAsync(avg, e->r_avg, m * 8, cudaMemcpyDeviceToHost, e->st));
     SS_CUDA(e, cudaStreamSynchronize(e->st));
+    return SS_OK;
+}
+
+// --------------------------------------------------------------------------
+// multi-GPU: owner map, stable route by owner, direct-count policies,
+// window-state migration
+// --------------------------------------------------------------------------
+extern "C" int ss_set_owner(ss_engine* e, const int32_t* owner_of, int n_dest) {
+    if (!e || !owner_of || n_dest < 1 || n_dest > 16) return fail(e, SS_E_CONFIG, "n_dest must be in [1, 16]");
+    { int jr = join_side(e); if (jr) return jr; }
+    for (int64_t g = 0; g < e->G; ++g)
+        if (owner_of[g] < 0 || owner_of[g] >= n_dest) return fail(e, SS_E_CONFIG, "owner out of range");
+    int rc;
+    if (!e->owner) {
+        if ((rc = dalloc(e, &e->owner, e->G)) || (rc = dalloc(e, &e->route_cnt, 16)) ||
+            (rc = dalloc(e, &e->route_base, 16)))
+            return rc;
+    }
+    SS_CUDA(e, cudaMemcpyAsync(e->owner, owner_of, e->G * 4, cudaMemcpyHostToDevice, e->st));
+    SS_CUDA(e, cudaStreamSynchronize(e->st));
+    e->n_dest = n_dest;
+    return SS_OK;
+}
+
+// Stable split of a batch by owning GPU: out = [tuples of GPU 0 in arrival
+// order] ++ [GPU 1] ++ ...; counts[d] = tuples for GPU d.  One mapped
+// multisplit pass (k_sort_pass<4, true>).
+extern "C" int ss_route(ss_engine* e, const uint32_t* groups, const int32_t* attrs, int64_t n, uint32_t* out_groups,
+                        int32_t* out_attrs, int64_t* counts) {
+    if (!e || n < 0) return SS_E_CONFIG;
+    if (!e->owner) return fail(e, SS_E_CONFIG, "ss_set_owner first");
+    { int jr = join_side(e); if (jr) return jr; }
+    const uint32_t* dk;
+    const int32_t* dv;
+    int rc;
+    if ((rc = stage_input(e, groups, attrs, n, &dk, &dv))) return rc;
+    if ((rc = engine_alloc_sort(e, n))) return rc;
+    SS_CUDA(e, cudaMemsetAsync(e->route_cnt, 0, 16 * 8, e->st));
+    if (n) k_owner_hist<<<2 * kNumSM, 256, 0, e->st>>>(dk, n, (uint32_t)e->G, e->owner, e->route_cnt, e->bad);
+    unsigned long long hc[16];
+    unsigned long long bad;
+    SS_CUDA(e, cudaMemcpyAsync(hc, e->route_cnt, 16 * 8, cudaMemcpyDeviceToHost, e->st));
+    SS_CUDA(e, cudaMemcpyAsync(&bad, e->bad, 8, cudaMemcpyDeviceToHost, e->st));
+    SS_CUDA(e, cudaStreamSynchronize(e->st));
+    if (bad != (unsigned long long)kNoBad) return data_error(e, bad, dk);
+    uint32_t base[16];
+    uint64_t run = 0;
+    for (int d = 0; d < 16; ++d) {
+        base[d] = (uint32_t)run;
+        run += hc[d];
+        if (counts && d < e->n_dest) counts[d] = (int64_t)hc[d];
+    }
+    if (n == 0) return SS_OK;
+    SS_CUDA(e, cudaMemcpyAsync(e->route_base, base, sizeof(base), cudaMemcpyHostToDevice, e->st));
+    SS_CUDA(e, cudaMemsetAsync(e->tickets, 0, 8, e->st));
+    const bool dev_out = is_device_ptr(out_groups) && is_device_ptr(out_attrs);
+    uint32_t* ko = dev_out ? out_groups : e->kbuf2;
+    int32_t* vo = dev_out ? out_attrs : e->vbuf[0];
+    if (++e->epoch >= (1u << 30) - 1) {
+        SS_CUDA(e, cudaMemsetAsync(e->status, 0, sizeof(unsigned long long) * e->status_tiles * kMaxBins, e->st));
+        e->epoch = 1;
+    }
+    const int tiles = (int)((n + kSortTile - 1) / kSortTile);
+    k_sort_pass<4, true><<<tiles, kSortThreads, SortSmem<4>::bytes, e->st>>>(
+        dk, dv, ko, vo, (int)n, 0, 15u, e->route_base, e->status, e->epoch, e->tickets, e->bad, 0, e->owner);
+    SS_CUDA(e, cudaGetLastError());
+    if (!dev_out) {
+        SS_CUDA(e, cudaMemcpyAsync(out_groups, ko, n * 4, cudaMemcpyDeviceToHost, e->st));
+        SS_CUDA(e, cudaMemcpyAsync(out_attrs, vo, n * 4, cudaMemcpyDeviceToHost, e->st));
+    }
+    SS_CUDA(e, cudaStreamSynchronize(e->st));
+    return SS_OK;
+}
+
+// batch group counts of the last step (valid until the next step)
+extern "C" int ss_group_counts(ss_engine* e, int32_t* counts) {
+    if (!e || !counts) return SS_E_CONFIG;
+    SS_CUDA(e, cudaStreamSynchronize(e->st));
+    SS_CUDA(e, cudaStreamSynchronize(e->side));
+    SS_CUDA(e, cudaMemcpy(counts, e->gcount, e->G * 4,
+                          is_device_ptr(counts) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost));
+    return SS_OK;
+}
+
+__global__ void k_tpt_from_counts(const int32_t* __restrict__ counts, int64_t G, const int32_t* __restrict__ pmap,
+                                  unsigned long long* __restrict__ tpt) {
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < G; g += (int64_t)gridDim.x * blockDim.x)
+        if (counts[g]) atomicAdd(&tpt[pmap[g]], (unsigned long long)counts[g]);
+}
+
+// The policy on given per-group counts (BatchStats.group_counts) against
+// the current assignment; nothing is applied.  Used by the GPU-level
+// balancer (partitions = GPUs) and by the reference-signature policies.
+extern "C" int ss_balance_counts(ss_engine* e, const int32_t* counts, const ss_balancer* cfg, ss_move* moves,
+                                 int64_t* n_moves, int64_t* scanned, int64_t* final_tpt) {
+    if (!e || !cfg || !counts) return SS_E_CONFIG;
+    int rc;
+    if ((rc = check_balancer(e, cfg))) return rc;
+    { int jr = join_side(e); if (jr) return jr; }
+    SS_CUDA(e, cudaMemcpyAsync(e->gcount, counts, e->G * 4,
+                               is_device_ptr(counts) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, e->st));
+    SS_CUDA(e, cudaMemsetAsync(e->tpt, 0, e->P * 8, e->st));
+    k_tpt_from_counts<<<2 * kNumSM, 256, 0, e->st>>>(e->gcount, e->G, e->pmap, e->tpt);
+    int nm = 0;
+    long long sc = 0;
+    std::vector<long long> ft(e->P);
+    if (cfg->policy == SS_POLICY_NO) {
+        std::vector<unsigned long long> tp(e->P);
+        SS_CUDA(e, cudaMemcpyAsync(tp.data(), e->tpt, e->P * 8, cudaMemcpyDeviceToHost, e->st));
+        SS_CUDA(e, cudaStreamSynchronize(e->st));
+        for (int p = 0; p < e->P; ++p) ft[p] = (long long)tp[p];
+    } else {
+        BalanceArgs a{};
+        a.policy = cfg->policy;
+        a.threshold = cfg->thread_threshold;
+        a.pot = cfg->pot;
+        a.cap = move_cap(e, cfg);
+        a.P = e->P;
+        a.order = e->order;
+        a.offsets = e->offsets;
+        a.gcount = e->gcount;
+        a.tpt = e->tpt;
+        a.moved = e->moved;
+        a.moves = e->moves;
+        a.front_top = e->front_top;
+        a.back_first = e->back_first;
+        a.mv_next = e->mv_next;
+        a.n_moves = e->n_moves;
+        a.scanned = e->scanned;
+        a.final_tpt = e->final_tpt;
+        a.bad = e->bad;
+        k_balance<<<1, kBalThreads, (size_t)e->P * (8 + 8 * 4), e->st>>>(a);
+        SS_CUDA(e, cudaGetLastError());
+        k_clear_moved<<<4, 256, 0, e->st>>>(e->moves, e->n_moves, e->moved);
+        SS_CUDA(e, cudaMemcpyAsync(&nm, e->n_moves, 4, cudaMemcpyDeviceToHost, e->st));
+        SS_CUDA(e, cudaMemcpyAsync(&sc, e->scanned, 8, cudaMemcpyDeviceToHost, e->st));
+        SS_CUDA(e, cudaMemcpyAsync(ft.data(), e->final_tpt, e->P * 8, cudaMemcpyDeviceToHost, e->st));
+        SS_CUDA(e, cudaStreamSynchronize(e->st));
+    }
+    if (nm > 0 && moves) {
+        std::vector<int4> mv(nm);
+        SS_CUDA(e, cudaMemcpy(mv.data(), e->moves, nm * sizeof(int4), cudaMemcpyDeviceToHost));
+        for (int i = 0; i < nm; ++i) moves[i] = ss_move{mv[i].x, mv[i].y, mv[i].z, mv[i].w};
+    }
+    if (n_moves) *n_moves = nm;
+    if (scanned) *scanned = sc;
+    if (final_tpt)
+        for (int p = 0; p < e->P; ++p) final_tpt[p] = ft[p];
+    SS_CUDA(e, cudaMemsetAsync(e->n_moves, 0, 4, e->st));
+    SS_CUDA(e, cudaMemsetAsync(e->gcount, 0, e->G * 4, e->st));
+    SS_CUDA(e, cudaStreamSynchronize(e->st));
+    return SS_OK;
+}
+
+// Window state of `groups` in ring-slot layout: meta[5*i..] = (fill,
+// next_pos, window_sum, min, max); values = concatenated ring images of
+// span = fill (< W, linear) or W slots.  Import writes the same layout, so
+// a migrated group is bit-identical (next_pos included).
+static int64_t state_span(int32_t fill, int64_t W) { return fill < W ? fill : W; }
+
+extern "C" int ss_export_state(ss_engine* e, const int32_t* groups, int64_t n, int64_t* meta, int32_t* values,
+                               int64_t cap, int64_t* n_values) {
+    if (!e || n < 0) return SS_E_CONFIG;
+    { int jr = join_side(e); if (jr) return jr; }
+    SS_CUDA(e, cudaStreamSynchronize(e->st));
+    int64_t pos = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        const int64_t g = groups[i];
+        if (g < 0 || g >= e->G) return fail(e, SS_E_CONFIG, "group out of range");
+        int32_t f, np, lo, hi;
+        long long s;
+        int64_t o;
+        SS_CUDA(e, cudaMemcpy(&f, e->fill + g, 4, cudaMemcpyDeviceToHost));
+        SS_CUDA(e, cudaMemcpy(&np, e->next_pos + g, 4, cudaMemcpyDeviceToHost));
+        SS_CUDA(e, cudaMemcpy(&s, e->wsum + g, 8, cudaMemcpyDeviceToHost));
+        SS_CUDA(e, cudaMemcpy(&lo, e->mn + g, 4, cudaMemcpyDeviceToHost));
+        SS_CUDA(e, cudaMemcpy(&hi, e->mx + g, 4, cudaMemcpyDeviceToHost));
+        SS_CUDA(e, cudaMemcpy(&o, e->off + g, 8, cudaMemcpyDeviceToHost));
+        if (meta) {
+            meta[5 * i + 0] = f; meta[5 * i + 1] = np; meta[5 * i + 2] = s;
+            meta[5 * i + 3] = lo; meta[5 * i + 4] = hi;
+        }
+        const int64_t span = state_span(f, e->W);
+        if (values && pos + span <= cap && span)
+            SS_CUDA(e, cudaMemcpy(values + pos, e->ring + o, span * 4, cudaMemcpyDeviceToHost));
+        pos += span;
+    }
+    if (n_values) *n_values = pos;
+    return SS_OK;
+}
+
+extern "C" int ss_import_state(ss_engine* e, const int32_t* groups, int64_t n, const int64_t* meta,
+                               const int32_t* values) {
+    if (!e || n < 0 || (n && (!meta || !groups))) return SS_E_CONFIG;
+    { int jr = join_side(e); if (jr) return jr; }
+    SS_CUDA(e, cudaStreamSynchronize(e->st));
+    int64_t pos = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        const int64_t g = groups[i];
+        if (g < 0 || g >= e->G) return fail(e, SS_E_CONFIG, "group out of range");
+        const int32_t f = (int32_t)meta[5 * i + 0], np = (int32_t)meta[5 * i + 1];
+        const long long s = meta[5 * i + 2];
+        const int32_t lo = (int32_t)meta[5 * i + 3], hi = (int32_t)meta[5 * i + 4];
+        const int64_t span = state_span(f, e->W);
+        int64_t o;
+        SS_CUDA(e, cudaMemcpy(&o, e->off + g, 8, cudaMemcpyDeviceToHost));
+        if (!e->dense) {
+            int32_t c;
+            SS_CUDA(e, cudaMemcpy(&c, e->cap + g, 4, cudaMemcpyDeviceToHost));
+            if (c < span) {
+                unsigned long long top;
+                SS_CUDA(e, cudaMemcpy(&top, e->pool_top, 8, cudaMemcpyDeviceToHost));
+                const int64_t ncap = std::min<int64_t>(e->W, std::max<int64_t>(span, 16));
+                if (top + ncap > e->pool_cap) return fail(e, SS_E_EXEC, "window ring pool exhausted");
+                o = (int64_t)top;
+                top += ncap;
+                const int32_t c32 = (int32_t)ncap;
+                SS_CUDA(e, cudaMemcpy(e->pool_top, &top, 8, cudaMemcpyHostToDevice));
+                SS_CUDA(e, cudaMemcpy(e->off + g, &o, 8, cudaMemcpyHostToDevice));
+                SS_CUDA(e, cudaMemcpy(e->cap + g, &c32, 4, cudaMemcpyHostToDevice));
+            }
+        }
+        if (span) SS_CUDA(e, cudaMemcpy(e->ring + o, values + pos, span * 4, cudaMemcpyHostToDevice));
+        SS_CUDA(e, cudaMemcpy(e->fill + g, &f, 4, cudaMemcpyHostToDevice));
+        SS_CUDA(e, cudaMemcpy(e->next_pos + g, &np, 4, cudaMemcpyHostToDevice));
+        SS_CUDA(e, cudaMemcpy(e->wsum + g, &s, 8, cudaMemcpyHostToDevice));
+        SS_CUDA(e, cudaMemcpy(e->mn + g, &lo, 4, cudaMemcpyHostToDevice));
+        SS_CUDA(e, cudaMemcpy(e->mx + g, &hi, 4, cudaMemcpyHostToDevice));
+        pos += span;
+    }
     return SS_OK;
 }

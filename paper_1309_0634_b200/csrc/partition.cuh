@@ -30,20 +30,27 @@ constexpr int kSortTile = kSortThreads * kSortItems;   // 4096 tuples
 // --------------------------------------------------------------------------
 // K2: per-sub-batch group histogram.  `chunk` divides the sub-batch size S,
 // so a CTA never straddles two sub-batches.
+//   SMEM (G <= 16K): the whole histogram lives in shared memory.
+//   else: groups that were hot in the previous batch (hot_of[g] >= 0, at
+//   most kHotCache of them) are counted in shared memory, the cold tail
+//   with warp-aggregated global atomics -- under Zipf skew the hottest
+//   keys would otherwise serialise on one L2 slice.
 // --------------------------------------------------------------------------
+constexpr int kHotCache = 2048;
+
 template <bool SMEM>
 __global__ void __launch_bounds__(512)
 k_count(const uint32_t* __restrict__ groups, int64_t n, uint32_t G, int64_t S, int64_t chunk,
-        int32_t* __restrict__ gcnt, unsigned long long* __restrict__ bad, int vec_ok) {
+        int32_t* __restrict__ gcnt, unsigned long long* __restrict__ bad, int vec_ok,
+        const int32_t* __restrict__ hot_of, const int32_t* __restrict__ hot_g, int n_hot) {
     extern __shared__ int32_t sh_hist[];
     const int64_t c0 = (int64_t)blockIdx.x * chunk;
     if (c0 >= n) return;
     const int64_t c1 = min(n, c0 + chunk);
     int32_t* dst = gcnt + (c0 / S) * (int64_t)G;
-    if (SMEM) {
-        for (uint32_t i = threadIdx.x; i < G; i += blockDim.x) sh_hist[i] = 0;
-        __syncthreads();
-    }
+    const int nbins = SMEM ? (int)G : n_hot;
+    for (int i = threadIdx.x; i < nbins; i += blockDim.x) sh_hist[i] = 0;
+    __syncthreads();
     const unsigned lane = lane_id();
     for (int64_t base = c0; base < c1; base += 4 * (int64_t)blockDim.x) {
         const int64_t i = base + 4 * (int64_t)threadIdx.x;
@@ -65,19 +72,42 @@ k_count(const uint32_t* __restrict__ groups, int64_t n, uint32_t G, int64_t S, i
                 g = 0xffffffffu;
             }
             if (!in) g = 0xffffffffu;
-            const unsigned peers = __match_any_sync(SS_FULL, g);
-            if (g != 0xffffffffu && lane == 31u - __clz(peers)) {
-                if (SMEM) atomicAdd(&sh_hist[g], __popc(peers));
-                else atomicAdd(&dst[g], __popc(peers));
+            if (SMEM) {
+                if (g != 0xffffffffu) atomicAdd(&sh_hist[g], 1);
+            } else {
+                const int h = (g != 0xffffffffu && n_hot) ? hot_of[g] : -1;
+                if (h >= 0) {
+                    atomicAdd(&sh_hist[h], 1);
+                    g = 0xffffffffu;
+                }
+                const unsigned peers = __match_any_sync(SS_FULL, g);
+                if (g != 0xffffffffu && lane == 31u - __clz(peers)) atomicAdd(&dst[g], __popc(peers));
             }
         }
     }
-    if (SMEM) {
-        __syncthreads();
-        for (uint32_t i = threadIdx.x; i < G; i += blockDim.x) {
-            const int32_t c = sh_hist[i];
-            if (c) atomicAdd(&dst[i], c);
+    __syncthreads();
+    for (int i = threadIdx.x; i < nbins; i += blockDim.x) {
+        const int32_t c = sh_hist[i];
+        if (c) atomicAdd(&dst[SMEM ? i : hot_g[i]], c);
+    }
+}
+
+// The hot-group cache of the next batch's count: groups above `thr` in
+// this batch (first kHotCache found).  hot_of is reset for the old list.
+__global__ void __launch_bounds__(256)
+k_hot_select(const int32_t* __restrict__ gcount, uint32_t G, long long thr, int32_t* __restrict__ hot_of,
+             int32_t* __restrict__ hot_g, int* __restrict__ n_hot_dev, const unsigned long long* __restrict__ bad) {
+    if (*bad != (unsigned long long)kNoBad) return;
+    for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < G; g += gridDim.x * blockDim.x) {
+        int h = -1;
+        if (gcount[g] > thr) {
+            const int slot = atomicAdd(n_hot_dev, 1);
+            if (slot < kHotCache) {
+                hot_g[slot] = (int32_t)g;
+                h = slot;
+            }
         }
+        hot_of[g] = h;
     }
 }
 
@@ -247,13 +277,13 @@ struct SortSmem {
     static constexpr size_t bytes = (size_t)NW * BINS * 2 + (size_t)BINS * 8 + (size_t)kSortTile * 8 + 16;
 };
 
-template <int RB>
+template <int RB, bool MAPPED = false>
 __global__ void __launch_bounds__(kSortThreads, 2)
 k_sort_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
             uint32_t* __restrict__ kout, int32_t* __restrict__ vout, int n, int shift, uint32_t mask,
             const uint32_t* __restrict__ bin_base, unsigned long long* __restrict__ status,
             uint32_t epoch, uint32_t* __restrict__ ticket, const unsigned long long* __restrict__ bad,
-            int stream_in) {
+            int stream_in, const int32_t* __restrict__ dmap = nullptr) {
     constexpr int BINS = 1 << RB;
     constexpr int NW = kSortThreads / 32;
     constexpr int BPT = (BINS + kSortThreads - 1) / kSortThreads;   // bins owned per thread
@@ -299,7 +329,7 @@ k_sort_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
         const bool valid = wbase + j * 32 + (int)lane < tile_n;
-        const uint32_t d = valid ? ((key[j] >> shift) & mask) : 0xffffffffu;
+        const uint32_t d = valid ? (MAPPED ? (uint32_t)dmap[key[j]] : ((key[j] >> shift) & mask)) : 0xffffffffu;
         const unsigned peers = __match_any_sync(SS_FULL, d);
         uint32_t r = 0;
         if (valid) r = myh[d];
@@ -368,7 +398,7 @@ k_sort_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
         if (wbase + j * 32 + (int)lane < tile_n) {
-            const uint32_t d = (key[j] >> shift) & mask;
+            const uint32_t d = MAPPED ? (uint32_t)dmap[key[j]] : ((key[j] >> shift) & mask);
             const uint32_t lp = tbin[d] + myh[d] + rank[j];
             skey[lp] = key[j];
             sval[lp] = val[j];
@@ -378,10 +408,26 @@ k_sort_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
     // contiguous runs per digit to global memory
     for (int i = threadIdx.x; i < tile_n; i += kSortThreads) {
         const uint32_t k = skey[i];
-        const uint32_t pos = gbase[(k >> shift) & mask] + (uint32_t)i;
+        const uint32_t pos = gbase[MAPPED ? (uint32_t)dmap[k] : ((k >> shift) & mask)] + (uint32_t)i;
         vout[pos] = sval[i];
         if (kout) kout[pos] = k;
     }
+}
+
+// histogram of destination owners for the multi-GPU route (<= 16 owners)
+__global__ void __launch_bounds__(256)
+k_owner_hist(const uint32_t* __restrict__ keys, int64_t n, uint32_t G, const int32_t* __restrict__ owner,
+             unsigned long long* __restrict__ counts, unsigned long long* __restrict__ bad) {
+    __shared__ uint32_t h[16];
+    if (threadIdx.x < 16) h[threadIdx.x] = 0;
+    __syncthreads();
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t k = keys[i];
+        if (k >= G) { atomicMin(bad, (unsigned long long)i); continue; }
+        atomicAdd(&h[owner[k]], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x < 16 && h[threadIdx.x]) atomicAdd(&counts[threadIdx.x], (unsigned long long)h[threadIdx.x]);
 }
 
 }  // namespace ss

@@ -25,7 +25,7 @@
 
 namespace ss {
 
-constexpr int kIngestThreads = 1024;
+constexpr int kIngestThreads = 512;       // 2 CTAs/SM fit, so the balancer's CTA never blocks a partition
 constexpr int kILP = 8;                     // stored values in flight per thread
 constexpr int kMemberChunk = 2048;          // members staged per CTA round
 constexpr int kMPT = kMemberChunk / kIngestThreads;
@@ -72,7 +72,7 @@ __device__ __forceinline__ long long seg_sum(long long v, unsigned seg_end) {
     return v;
 }
 
-__global__ void __launch_bounds__(kIngestThreads)
+__global__ void __launch_bounds__(kIngestThreads, 2)
 k_ingest(IngestArgs a) {
     extern __shared__ __align__(16) unsigned char ingest_sm[];
     int64_t* m_off = (int64_t*)ingest_sm;
@@ -391,18 +391,25 @@ k_minmax_rescan(const int2* __restrict__ rescan, const unsigned* __restrict__ n_
 // Occupancy-proportional store: before a batch, grow the ring region of
 // every group whose window will hold more values than its capacity
 // (capacity doubles up to W; a window below W is linear, next_pos == 0,
-// so growth copies `fill` values).  One warp per 32 groups.
+// so growth copies `fill` values).  Phase 1 reserves (warp-aggregated
+// atomics on the pool top) and lists the copies; phase 2 copies them with
+// one CTA per grown group.
+struct RingCopy {
+    int64_t src, dst;
+    int32_t len, pad;
+};
+
 __global__ void __launch_bounds__(256)
 k_reserve(const int32_t* __restrict__ gcount, uint32_t G, int64_t W, const int32_t* __restrict__ fill,
-          int64_t* __restrict__ off, int32_t* __restrict__ cap, int32_t* __restrict__ ring,
-          unsigned long long* __restrict__ pool_top, unsigned long long pool_cap,
-          int* __restrict__ oom, const unsigned long long* __restrict__ bad) {
+          int64_t* __restrict__ off, int32_t* __restrict__ cap, unsigned long long* __restrict__ pool_top,
+          unsigned long long pool_cap, int* __restrict__ oom, RingCopy* __restrict__ copies,
+          unsigned* __restrict__ n_copies, const unsigned long long* __restrict__ bad) {
     if (*bad != (unsigned long long)kNoBad) return;
     const unsigned lane = lane_id();
     const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
     for (uint32_t g0 = (blockIdx.x * (blockDim.x >> 5) + warp_id()) * 32; g0 < G; g0 += nwarps * 32) {
         const uint32_t g = g0 + lane;
-        int64_t ncap = 0, noff = 0, oldoff = 0;
+        int64_t ncap = 0, oldoff = 0;
         int f = 0;
         if (g < G) {
             const int k = gcount[g];
@@ -416,34 +423,37 @@ k_reserve(const int32_t* __restrict__ gcount, uint32_t G, int64_t W, const int32
                 }
             }
         }
-        // warp-aggregated reservation
         const int64_t incl = warp_incl_scan(ncap);
         const int64_t wtot = __shfl_sync(SS_FULL, incl, 31);
         unsigned long long base = 0;
         if (lane == 31 && wtot) base = atomicAdd(pool_top, (unsigned long long)wtot);
         base = __shfl_sync(SS_FULL, base, 31);
         if (ncap) {
-            noff = (int64_t)base + incl - ncap;
+            const int64_t noff = (int64_t)base + incl - ncap;
             if ((unsigned long long)(noff + ncap) > pool_cap) {
                 *oom = 1;
-                ncap = 0;
+            } else {
+                if (f) {
+                    RingCopy rc;
+                    rc.src = oldoff;
+                    rc.dst = noff;
+                    rc.len = f;
+                    rc.pad = 0;
+                    copies[atomicAdd(n_copies, 1u)] = rc;
+                }
+                off[g] = noff;
+                cap[g] = (int32_t)ncap;
             }
         }
-        // copy the live prefix (linear while filling), one group at a time
-        unsigned todo = __ballot_sync(SS_FULL, ncap != 0);
-        while (todo) {
-            const int src = __ffs(todo) - 1;
-            todo &= todo - 1;
-            const int64_t so = __shfl_sync(SS_FULL, oldoff, src);
-            const int64_t doff = __shfl_sync(SS_FULL, noff, src);
-            const int ff = __shfl_sync(SS_FULL, f, src);
-            for (int j = lane; j < ff; j += 32) ring[doff + j] = ring[so + j];
-        }
-        __syncwarp();
-        if (ncap) {
-            off[g] = noff;
-            cap[g] = (int32_t)ncap;
-        }
+    }
+}
+
+__global__ void __launch_bounds__(256)
+k_ring_copy(const RingCopy* __restrict__ copies, const unsigned* __restrict__ n_copies, int32_t* __restrict__ ring) {
+    const unsigned n = *n_copies;
+    for (unsigned i = blockIdx.x; i < n; i += gridDim.x) {
+        const RingCopy c = copies[i];
+        for (int j = threadIdx.x; j < c.len; j += blockDim.x) ring[c.dst + j] = ring[c.src + j];
     }
 }
 

@@ -278,6 +278,19 @@ class StreamEngine:
                for m in moves[:nm.value]]
         return out, sc.value, ft
 
+    def balance_counts(self, counts, bal: "L.Balancer"):
+        """The policy on given per-group counts (no recount); nothing applied."""
+        c = np.ascontiguousarray(counts, dtype=np.int32)
+        cap = 4 * self.n_partitions if bal.max_moves <= 0 else int(bal.max_moves)
+        moves = (L.MoveC * max(cap, 1))()
+        nm, sc = C.c_int64(), C.c_int64()
+        ft = np.empty(self.n_partitions, dtype=np.int64)
+        self._check(self._lib.ss_balance_counts(self._h, _ptr(c)[0], C.byref(bal), moves, C.byref(nm),
+                                                C.byref(sc), _ptr(ft)[0]))
+        out = [(m.group, m.src, m.dst, "back" if m.placement == L.BACK_CODE else "front")
+               for m in moves[:nm.value]]
+        return out, sc.value, ft
+
     # -- fused per-batch step --------------------------------------------------
     def step(self, groups, attrs, balancer=None, sync: bool = True):
         g = _keys_u32(groups, self.n_groups)
