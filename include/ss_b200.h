@@ -60,7 +60,7 @@ typedef struct {
     int64_t  n_groups;      /* G: dense group ids 0..G-1 (datagen.py:81-103)          */
     int64_t  window;        /* W: per-group window length (harness.py:43, engine.py:60)*/
     int32_t  n_partitions;  /* P: processing units = aggregate-kernel CTAs           */
-    int32_t  key_bits;      /* 32: u32 group ids                                      */
+    int32_t  key_bits;      /* 32: u32 group ids; 64: int64 keys (ss_step_keys64)     */
     uint32_t agg_mask;      /* SS_AGG_* bits that must be maintained                  */
     int32_t  scope;         /* 0: per-group window (the reference semantics)          */
     int32_t  device;        /* CUDA ordinal                                           */
@@ -157,6 +157,15 @@ int  ss_export_values(ss_engine* e, int64_t group, int64_t* out, int64_t cap, in
  * their COUNT/SUM/AVG/MIN/MAX after it.  Sizes: cap entries each. */
 int  ss_results(ss_engine* e, int64_t cap, int32_t* groups, int64_t* count, int64_t* sum,
                 double* avg, int32_t* mn, int32_t* mx, int64_t* n);
+
+/* ---- int64 group keys (key_bits = 64; BASELINE C4/C5) ------------------
+ * Keys map to dense slots 0..G-1 in order of first appearance in the
+ * stream (a device hash table); every other entry point then sees slots. */
+int  ss_map_keys(ss_engine* e, const int64_t* keys, int64_t n, uint32_t* out_slots);
+int  ss_step_keys64(ss_engine* e, const int64_t* keys, const int32_t* attrs, int64_t n,
+                    const ss_balancer* cfg, ss_step_report* rep);
+/* key of every assigned slot (keys[n_slots]) */
+int  ss_slot_keys(ss_engine* e, int64_t* keys, int64_t* n_slots);
 
 /* ---- multi-GPU: groups shard by key across GPUs ----------- */
 /* owner_of[G] in [0, n_dest), n_dest <= 16 */

@@ -84,6 +84,9 @@ _SIGS = {
     "ss_balance_counts": (C.c_int, [_P, _P, C.POINTER(Balancer), _P, _P, _P, _P]),
     "ss_export_state": (C.c_int, [_P, _P, _I64, _P, _P, _I64, _P]),
     "ss_import_state": (C.c_int, [_P, _P, _I64, _P, _P]),
+    "ss_map_keys": (C.c_int, [_P, _P, _I64, _P]),
+    "ss_step_keys64": (C.c_int, [_P, _P, _P, _I64, C.POINTER(Balancer), C.POINTER(StepReport)]),
+    "ss_slot_keys": (C.c_int, [_P, _P, _P]),
 }
 KERNEL_CLASSES = ("count", "stats", "place", "ingest", "emit", "apply", "balance")
 EXPORTS = tuple(_SIGS)

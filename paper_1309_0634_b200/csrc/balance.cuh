@@ -47,6 +47,7 @@ struct BalanceArgs {
     const unsigned long long* bad;
     const unsigned long long* init_loads;   // split mode: cold-only loads (else tpt)
     const uint8_t* exclude;                 // split mode: hot groups never move
+    long long stop_load;                    // split mode: done once max load <= this (0: off)
 };
 
 struct BalSmem {
@@ -228,6 +229,7 @@ k_balance(BalanceArgs a) {
             __syncthreads();
             if (nm_all >= a.cap) break;
             if (s.loads[hi] - s.loads[lo] <= a.threshold) break;
+            if (a.stop_load > 0 && s.loads[hi] <= a.stop_load) break;
             const int e0 = a.offsets[hi], e1 = a.offsets[hi + 1];
             int pick = -1;
             long long pscan = 0;

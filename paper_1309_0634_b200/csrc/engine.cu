@@ -31,6 +31,7 @@
 #include "window.cuh"
 #include "balance.cuh"
 #include "split.cuh"
+#include "keys.cuh"
 
 using namespace ss;
 
@@ -118,6 +119,12 @@ struct ss_engine {
     int* prev_moves = nullptr;
 
     uint32_t* kbuf2 = nullptr;             // sorted keys (reorder only)
+
+    // int64 keys (key_bits == 64): key -> dense slot table
+    bool keys64 = false;
+    KeyTable kt{};
+    long long* stage_keys64 = nullptr;
+    int32_t* kbsum = nullptr;
 
     // multi-GPU routing: group -> owning GPU
     int32_t* owner = nullptr;
@@ -276,6 +283,9 @@ __global__ void k_dense_off(int64_t* off, int32_t* cap, int64_t G, int64_t W) {
     }
 }
 __global__ void k_set_bad(unsigned long long* bad) { *bad = (unsigned long long)kNoBad; }
+__global__ void k_fill_u64(unsigned long long* p, int64_t n, unsigned long long v) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
+}
 __global__ void k_u64_to_i64(const unsigned long long* a, long long* b, int n) {
     for (int i = threadIdx.x; i < n; i += blockDim.x) b[i] = (long long)a[i];
 }
@@ -523,6 +533,32 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
     SS_CUDA(e, cudaMemsetAsync(e->gcount, 0, G * 4, e->st));
     k_set_bad<<<1, 1, 0, e->st>>>(e->bad);
     if ((rc = engine_alloc_sort(e, S))) return rc;
+    // -- int64 key table
+    e->keys64 = cfg->key_bits == 64;
+    if (e->keys64) {
+        uint64_t cap = 1;
+        while (cap < 2 * (uint64_t)G) cap <<= 1;
+        KeyTable& t = e->kt;
+        if ((rc = dalloc(e, &t.keys, cap + 1)) || (rc = dalloc(e, &t.slot, cap + 1)) ||
+            (rc = dalloc(e, &t.first, cap + 1)) || (rc = dalloc(e, &t.ent, e->max_batch)) ||
+            (rc = dalloc(e, &t.new_ent, G)) || (rc = dalloc(e, &t.n_new, 1)) || (rc = dalloc(e, &t.n_slots, 1)) ||
+            (rc = dalloc(e, &t.mark, e->max_batch)) || (rc = dalloc(e, &t.slot_keys, G)) ||
+            (rc = dalloc(e, &t.min_key_entry, 1)) || (rc = dalloc(e, &t.overflow, 1)) ||
+            (rc = dalloc(e, &e->stage_keys64, e->max_batch)) ||
+            (rc = dalloc(e, &e->kbsum, e->max_batch / kMarkBlk + 2)))
+            return rc;
+        t.cap_mask = cap - 1;
+        t.G = (int)G;
+        SS_CUDA(e, cudaMemsetAsync(t.keys, 0, (cap + 1) * 8, e->st));
+        k_fill_u64<<<296, 256, 0, e->st>>>(t.keys, cap + 1, kEmptyKey);
+        SS_CUDA(e, cudaMemsetAsync(t.slot, 0xff, (cap + 1) * 4, e->st));
+        SS_CUDA(e, cudaMemsetAsync(t.first, 0xff, (cap + 1) * 4, e->st));
+        SS_CUDA(e, cudaMemsetAsync(t.mark, 0xff, e->max_batch * 4, e->st));
+        SS_CUDA(e, cudaMemsetAsync(t.n_new, 0, 4, e->st));
+        SS_CUDA(e, cudaMemsetAsync(t.n_slots, 0, 4, e->st));
+        SS_CUDA(e, cudaMemsetAsync(t.min_key_entry, 0xff, 4, e->st));
+        SS_CUDA(e, cudaMemsetAsync(t.overflow, 0, 4, e->st));
+    }
     // -- balancer
     e->cap_moves = 4 * e->P;
     if ((rc = dalloc(e, &e->moves, e->cap_moves)) || (rc = dalloc(e, &e->front_top, e->P)) ||
@@ -843,8 +879,11 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
             a.final_tpt = e->final_tpt;
             a.bad = e->bad;
             if (split) {
+                // cold groups only need to move off partitions above the mean:
+                // the water level of the hot shares is >= the mean
                 a.init_loads = e->spx.base;
                 a.exclude = e->spx.hot_flag;
+                a.stop_load = std::max<long long>(1, (n + e->P - 1) / e->P);
             }
             k_balance<<<1, kBalThreads, (size_t)e->P * (8 + 8 * 4), e->side>>>(a);
         }
@@ -965,6 +1004,11 @@ static int check_report(ss_engine* e, const uint32_t* dk) {
     SS_CUDA(e, cudaGetLastError());
     if (e->h_rep->bad != (unsigned long long)kNoBad) return data_error(e, e->h_rep->bad, dk);
     if (e->h_rep->oom) return fail(e, SS_E_EXEC, "window ring pool exhausted (raise pool_values)");
+    if (e->keys64) {
+        int ov = 0;
+        SS_CUDA(e, cudaMemcpy(&ov, e->kt.overflow, 4, cudaMemcpyDeviceToHost));
+        if (ov) return fail(e, SS_E_DATA, "more than n_groups distinct keys");
+    }
     return SS_OK;
 }
 
@@ -1701,5 +1745,67 @@ extern "C" int ss_import_state(ss_engine* e, const int32_t* groups, int64_t n, c
         SS_CUDA(e, cudaMemcpy(e->mx + g, &hi, 4, cudaMemcpyHostToDevice));
         pos += span;
     }
+    return SS_OK;
+}
+
+// --------------------------------------------------------------------------
+// int64 keys
+// --------------------------------------------------------------------------
+static int map_keys(ss_engine* e, const int64_t* keys, int64_t n, uint32_t* dout) {
+    const long long* dk;
+    if (is_device_ptr(keys)) dk = (const long long*)keys;
+    else {
+        if (n) SS_CUDA(e, cudaMemcpyAsync(e->stage_keys64, keys, n * 8, cudaMemcpyHostToDevice, e->st));
+        dk = e->stage_keys64;
+    }
+    if (n == 0) return SS_OK;
+    KeyTable& t = e->kt;
+    const int nblk = (int)((n + kMarkBlk - 1) / kMarkBlk);
+    k_key_probe<<<4 * kNumSM, 256, 0, e->st>>>(dk, n, t);
+    k_key_rank_small<<<1, 1024, 0, e->st>>>(t);
+    k_key_mark<<<2 * kNumSM, 256, 0, e->st>>>(t);
+    k_key_mark_count<<<nblk, 1024, 0, e->st>>>(t, n, e->kbsum);
+    k_key_mark_scan<<<1, 1024, 0, e->st>>>(t, e->kbsum, nblk);
+    k_key_mark_assign<<<nblk, 1024, 0, e->st>>>(t, n, e->kbsum);
+    k_key_mark_done<<<1, 1, 0, e->st>>>(t);
+    k_key_map<<<4 * kNumSM, 256, 0, e->st>>>(dk, n, t, dout);
+    SS_CUDA(e, cudaGetLastError());
+    return SS_OK;
+}
+
+// key -> dense slot of a batch (slots assigned in first-appearance order)
+extern "C" int ss_map_keys(ss_engine* e, const int64_t* keys, int64_t n, uint32_t* out_slots) {
+    if (!e || n < 0) return SS_E_CONFIG;
+    if (!e->keys64) return fail(e, SS_E_CONFIG, "engine was created with key_bits = 32");
+    if (n > e->max_batch) return fail(e, SS_E_CONFIG, "batch larger than max_batch");
+    { int jr = join_side(e); if (jr) return jr; }
+    const bool dev = is_device_ptr(out_slots);
+    int rc;
+    if ((rc = map_keys(e, keys, n, dev ? out_slots : e->stage_keys))) return rc;
+    if (!dev && n) SS_CUDA(e, cudaMemcpyAsync(out_slots, e->stage_keys, n * 4, cudaMemcpyDeviceToHost, e->st));
+    SS_CUDA(e, cudaStreamSynchronize(e->st));
+    return SS_OK;
+}
+
+// the fused step on int64 keys: map to slots, then ss_step on the slots
+extern "C" int ss_step_keys64(ss_engine* e, const int64_t* keys, const int32_t* attrs, int64_t n,
+                              const ss_balancer* cfg, ss_step_report* rep) {
+    if (!e || n < 0) return SS_E_CONFIG;
+    if (!e->keys64) return fail(e, SS_E_CONFIG, "engine was created with key_bits = 32");
+    if (n > e->max_batch) return fail(e, SS_E_CONFIG, "batch larger than max_batch");
+    int rc;
+    if ((rc = map_keys(e, keys, n, e->stage_keys))) return rc;
+    return ss_step(e, e->stage_keys, attrs, n, cfg, rep);
+}
+
+extern "C" int ss_slot_keys(ss_engine* e, int64_t* keys, int64_t* n_slots) {
+    if (!e) return SS_E_CONFIG;
+    if (!e->keys64) return fail(e, SS_E_CONFIG, "engine was created with key_bits = 32");
+    { int jr = join_side(e); if (jr) return jr; }
+    SS_CUDA(e, cudaStreamSynchronize(e->st));
+    int ns = 0;
+    SS_CUDA(e, cudaMemcpy(&ns, e->kt.n_slots, 4, cudaMemcpyDeviceToHost));
+    if (n_slots) *n_slots = ns;
+    if (keys && ns) SS_CUDA(e, cudaMemcpy(keys, e->kt.slot_keys, (size_t)ns * 8, cudaMemcpyDeviceToHost));
     return SS_OK;
 }

@@ -142,7 +142,7 @@ class ShardedEngine:
     def route(self, groups, attrs):
         import torch
         n = len(groups)
-        dev = groups.device if hasattr(groups, "device") else None
+        dev = groups.device if isinstance(groups, torch.Tensor) else None
         if dev is not None and dev.type == "cuda":
             og = torch.empty(n, dtype=torch.int32, device=dev)
             oa = torch.empty(n, dtype=torch.int32, device=dev)

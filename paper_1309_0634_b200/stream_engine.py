@@ -140,8 +140,11 @@ class StreamEngine:
     def __init__(self, n_groups: int, window, n_partitions: int = 148,
                  aggregates=("count", "sum", "avg"), device: int = 0,
                  max_batch: int = 1 << 24, sub_batch: int = 0, pool_values: int = 0,
-                 stream=None):
+                 stream=None, key_bits: int = 32):
         self._lib = L.load()
+        if key_bits not in (32, 64):
+            raise InvalidConfigError("key_bits must be 32 or 64")
+        self.key_bits = key_bits
         spec = window if isinstance(window, WindowSpec) else WindowSpec(int(window))
         aggs = aggregates if isinstance(aggregates, Aggregates) else Aggregates(tuple(aggregates))
         if n_groups < 1:
@@ -154,7 +157,7 @@ class StreamEngine:
         self.aggregates = aggs
         self.minmax = bool(aggs.mask & (L.AGG_MIN | L.AGG_MAX))
         cfg = L.Config(n_groups=self.n_groups, window=self.window,
-                       n_partitions=self.n_partitions, key_bits=32, agg_mask=aggs.mask,
+                       n_partitions=self.n_partitions, key_bits=key_bits, agg_mask=aggs.mask,
                        scope=0, device=device, reserved=0, max_batch=int(max_batch),
                        sub_batch=int(sub_batch), pool_values=int(pool_values))
         h = C.c_void_p()
@@ -293,6 +296,8 @@ class StreamEngine:
 
     # -- fused per-batch step --------------------------------------------------
     def step(self, groups, attrs, balancer=None, sync: bool = True):
+        if self.key_bits == 64:
+            return self._step64(groups, attrs, balancer, sync)
         g = _keys_u32(groups, self.n_groups)
         a = _attrs_i32(attrs)
         pg, _k1 = _ptr(g)
@@ -303,6 +308,30 @@ class StreamEngine:
                                       C.byref(rep) if sync else None))
         self._keep = (_k1, _k2)
         return self._report(rep) if sync else None
+
+    def _step64(self, keys, attrs, balancer, sync):
+        if isinstance(keys, np.ndarray):
+            k = np.ascontiguousarray(keys, dtype=np.int64)
+        else:
+            import torch
+            k = keys.to(torch.int64).contiguous()
+        a = _attrs_i32(attrs)
+        pk, _k1 = _ptr(k)
+        pa, _k2 = _ptr(a)
+        bal = balancer if balancer is not None else self.balancer_struct()
+        rep = L.StepReport()
+        self._check(self._lib.ss_step_keys64(self._h, pk, pa, len(k), C.byref(bal),
+                                             C.byref(rep) if sync else None))
+        self._keep = (_k1, _k2)
+        return self._report(rep) if sync else None
+
+    def slot_keys(self) -> np.ndarray:
+        """int64 key of every assigned group slot (slots follow first appearance)."""
+        n = C.c_int64()
+        self._check(self._lib.ss_slot_keys(self._h, None, C.byref(n)))
+        out = np.empty(max(1, n.value), dtype=np.int64)
+        self._check(self._lib.ss_slot_keys(self._h, _ptr(out)[0], C.byref(n)))
+        return out[:n.value]
 
     def last_report(self) -> StepReport:
         rep = L.StepReport()

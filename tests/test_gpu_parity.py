@@ -295,3 +295,56 @@ def test_split_aggregates_match_oracle(policy):
     else:
         assert max(ratios[2:]) < ratios[0] / 4, ratios
     eng.close()
+
+
+# ---- int64 keys (C4 shape): hash table, slots in first-appearance order --------
+
+def _first_appearance_ids(stream_batches, G):
+    seen = np.full(G, -1, dtype=np.int64)
+    nxt = 0
+    for g in stream_batches:
+        u, idx = np.unique(g, return_index=True)
+        for x in u[np.argsort(idx)]:
+            if seen[x] < 0:
+                seen[x] = nxt
+                nxt += 1
+    return seen
+
+
+@pytest.mark.parametrize("policy", ["no", "prob"])
+def test_int64_keys_match_oracle(policy):
+    from paper_1309_0634_b200.stream_engine import StreamEngine
+    G, W, P, B = 5000, 30, 32, 40_000
+    spec = D.DatasetSpec(D.DatasetKind.PERMUTED_ZIPF, 5 * B, G, 1.1, 9)
+    bl = list(D.batches(D.stream_for(spec), B))
+    slot_of = _first_appearance_ids([b.groups for b in bl], G)
+    eng = _engine(G, W, P=P, key_bits=64, max_batch=B, sub_batch=16384,
+                  aggregates=("count", "sum", "avg", "min", "max"))
+    thr = max(1, B // (10 * P))
+    bal = StreamEngine.balancer_struct(policy, thr, 0.5)
+    cfg = O.balancer_cfg(policy, thr, 0.5)
+    n_seen = int((slot_of >= 0).sum())
+    store, asg = O.OStore(G, W), O.contiguous_assignment(G, P)
+    for b in bl:
+        keys = D.mix64(b.groups)
+        rep = eng.step(keys, b.attrs, bal)
+        rg = slot_of[b.groups]
+        counts, tpt = O.histogram(rg, asg)
+        pg, pa, ind = O.place(rg, b.attrs, asg, counts, tpt)
+        v = O.POLICY_FNS[policy](counts, tpt, asg, pg, ind, cfg)
+        store.ingest(pg, pa, assume_grouped=True)
+        asg = O.apply_move_list(asg, v.moves)
+        assert rep.moves == len(v.moves) and rep.scanned == v.scanned
+    sk = eng.slot_keys()
+    assert len(sk) == n_seen
+    inv = np.empty(n_seen, dtype=np.int64)
+    inv[slot_of[slot_of >= 0]] = np.flatnonzero(slot_of >= 0)
+    assert np.array_equal(D.unmix64(sk), inv)
+    s = eng.snapshot()
+    assert np.array_equal(s["fill"], store.fill) and np.array_equal(s["window_sum"], store.window_sum)
+    assert np.array_equal(s["next_pos"], store.next_pos)
+    cnt, sm, avg, mn, mx = store.aggregates()
+    assert np.array_equal(s["min"], mn) and np.array_equal(s["max"], mx)
+    with pytest.raises(DataError):
+        eng.step(D.mix64(np.arange(G, 2 * G + 100)), np.zeros(G + 100, dtype=np.int64), bal)
+    eng.close()

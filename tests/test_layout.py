@@ -12,7 +12,7 @@ PKG = os.path.join(ROOT, "paper_1309_0634_b200")
 
 def _header_symbols():
     src = open(os.path.join(ROOT, "include", "ss_b200.h")).read()
-    return sorted(set(re.findall(r"\b(ss_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(ss_[a-z_0-9]+)\s*\(", src)))
 
 
 def test_library_exports_every_declared_symbol():
