@@ -951,9 +951,12 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
         f.n_rescan = e->n_rescan;
         f.bad = e->bad;
         k_finalize<<<2 * kNumSM, 256, 0, e->st>>>(f);
-        if (e->minmax)
-            k_minmax_rescan<<<2 * kNumSM, 256, 0, e->st>>>(e->rescan, e->n_rescan, e->ring, e->off, e->W, e->mn,
-                                                           e->mx, e->r_mn, e->r_mx);
+        if (e->minmax) {
+            k_rescan_reset<<<4, 256, 0, e->st>>>(e->rescan, e->n_rescan, e->mn, e->mx);
+            k_minmax_rescan<<<8 * kNumSM, 256, 0, e->st>>>(e->rescan, e->n_rescan, e->ring, e->off, e->W, e->mn,
+                                                           e->mx);
+            k_rescan_rows<<<4, 256, 0, e->st>>>(e->rescan, e->n_rescan, e->mn, e->mx, e->r_mn, e->r_mx);
+        }
         SS_CUDA(e, cudaGetLastError());
     }
     if (run_side) {

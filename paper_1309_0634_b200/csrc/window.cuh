@@ -29,7 +29,7 @@ constexpr int kIngestThreads = 512;       // 2 CTAs/SM fit, so the balancer's CT
 constexpr int kILP = 8;                     // stored values in flight per thread
 constexpr int kMemberChunk = 2048;          // members staged per CTA round
 constexpr int kMPT = kMemberChunk / kIngestThreads;
-constexpr size_t kIngestSmem = (size_t)kMemberChunk * (8 + 8 + 4 * 8) + 16;
+constexpr size_t kIngestSmem = (size_t)kMemberChunk * (8 + 8 + 4 * 10) + 64;
 
 struct IngestArgs {
     const int32_t* order;       // partition lists, concatenated   [G]
@@ -72,21 +72,33 @@ __device__ __forceinline__ long long seg_sum(long long v, unsigned seg_end) {
     return v;
 }
 
+// per-member 64-bit delta kept as two native 32-bit shared words (64-bit
+// shared atomics are CAS loops on sm_100): low word + carries into high
+__device__ __forceinline__ void add_delta(uint32_t* lo, uint32_t* hi, long long v) {
+    const unsigned long long x = (unsigned long long)v;
+    const uint32_t lo32 = (uint32_t)x;
+    const uint32_t prev = atomicAdd(lo, lo32);
+    const uint32_t carry = (prev + lo32 < prev) ? 1u : 0u;
+    atomicAdd(hi, (uint32_t)(x >> 32) + carry);
+}
+
+constexpr int kUnit = 32 * kILP;            // values of one warp unit (long members)
+
 __global__ void __launch_bounds__(kIngestThreads, 2)
 k_ingest(IngestArgs a) {
     extern __shared__ __align__(16) unsigned char ingest_sm[];
     int64_t* m_off = (int64_t*)ingest_sm;
-    // 64-bit shared atomics are CAS loops on sm_100; the per-member delta is
-    // kept as two native 32-bit words (low word + carries into the high word)
     uint32_t* m_dlo = (uint32_t*)(m_off + kMemberChunk);
     uint32_t* m_dhi = m_dlo + kMemberChunk;
     int32_t* m_g = (int32_t*)(m_dhi + kMemberChunk);
-    int32_t* m_scan = m_g + kMemberChunk;            // kMemberChunk + 1
-    int32_t* m_start = m_scan + kMemberChunk + 4;
+    int32_t* m_scan = m_g + kMemberChunk;            // short members: value scan  [kMemberChunk + 1]
+    int32_t* m_uscan = m_scan + kMemberChunk + 4;    // long members: unit scan    [kMemberChunk + 1]
+    int32_t* m_start = m_uscan + kMemberChunk + 4;
     int32_t* m_q0 = m_start + kMemberChunk;
     int32_t* m_s0 = m_q0 + kMemberChunk;
     int32_t* m_f0 = m_s0 + kMemberChunk;             // live bound (0 when k >= W)
-    int32_t* m_min = m_f0 + kMemberChunk;
+    int32_t* m_w = m_f0 + kMemberChunk;              // stored values of the member
+    int32_t* m_min = m_w + kMemberChunk;
     int32_t* m_max = m_min + kMemberChunk;
     __shared__ int32_t sh_red[33];
     if (*a.bad != (unsigned long long)kNoBad) return;
@@ -100,16 +112,18 @@ k_ingest(IngestArgs a) {
     const int n_items = n_mem + (s_hi - s_lo);   // members, then split shares
     const int W = (int)a.W;
     const unsigned lane = lane_id();
+    const int nw = kIngestThreads / 32;
     unsigned long long work_total = 0;
 
     for (int c0 = 0; c0 < n_items; c0 += kMemberChunk) {
         const int m = min(kMemberChunk, n_items - c0);
-        int32_t wk[kMPT];
-        int32_t tsum = 0;
+        int32_t wshort[kMPT], wunits[kMPT];
+        int32_t ssum = 0, usum = 0;
 #pragma unroll
         for (int q = 0; q < kMPT; ++q) {
             const int i = threadIdx.x * kMPT + q;
-            wk[q] = 0;
+            wshort[q] = 0;
+            wunits[q] = 0;
             if (i >= m) continue;
             const int it = c0 + i;
             int g, r_lo, r_hi;            // this item's slice [r_lo, r_hi) of the sub-batch run
@@ -129,6 +143,7 @@ k_ingest(IngestArgs a) {
                 r_hi = (int)(kt * a.share_hi[sh] / den);
             }
             m_g[i] = 0x7fffffff;
+            m_w[i] = 0;
             if (r_hi <= r_lo) continue;
             const int K = a.gcount[g];                 // batch count
             const int b = a.gpre[g];                   // batch rank of run index 0
@@ -136,7 +151,9 @@ k_ingest(IngestArgs a) {
             if (first >= r_hi) continue;
             const int f0 = a.fill[g];
             const int jb = b + first;                  // batch rank of the first stored value
+            const int w = r_hi - first;
             m_g[i] = tag;
+            m_w[i] = w;
             m_start[i] = a.gstart[g] + first;
             m_q0[i] = (int)(((int64_t)f0 + jb) % W);
             m_s0[i] = (int)(((int64_t)a.next_pos[g] + f0 + jb) % W);
@@ -146,24 +163,93 @@ k_ingest(IngestArgs a) {
             m_dhi[i] = 0;
             m_min[i] = 0x7fffffff;
             m_max[i] = (int32_t)0x80000000;
-            wk[q] = r_hi - first;
-            tsum += wk[q];
+            if (w >= 32) wunits[q] = (w + kUnit - 1) / kUnit;
+            else wshort[q] = w;
+            ssum += wshort[q];
+            usum += wunits[q];
+            work_total += (unsigned long long)w;
         }
-        int32_t total;
-        int32_t ex = block_excl_scan(tsum, sh_red, &total);
+        int32_t s_total, u_total;
+        int32_t sex = block_excl_scan(ssum, sh_red, &s_total);
+        int32_t uex = block_excl_scan(usum, sh_red, &u_total);
 #pragma unroll
         for (int q = 0; q < kMPT; ++q) {
             const int i = threadIdx.x * kMPT + q;
-            if (i < m) m_scan[i] = ex;
-            ex += wk[q];
+            if (i < m) {
+                m_scan[i] = sex;
+                m_uscan[i] = uex;
+            }
+            sex += wshort[q];
+            uex += wunits[q];
         }
-        if (threadIdx.x == 0) m_scan[m] = total;
-        work_total += (unsigned long long)total;
+        if (threadIdx.x == 0) {
+            m_scan[m] = s_total;
+            m_uscan[m] = u_total;
+        }
         __syncthreads();
 
-        // ---- exchange: kILP stored values per thread per round, all loads
-        // issued before any store (distinct slots within a batch) ----------
-        for (int base = 0; base < total; base += kIngestThreads * kILP) {
+        // ---- long members: one warp per unit of kUnit contiguous values ----
+        for (int u = warp_id(); u < u_total; u += nw) {
+            int mi = 0;                                 // last member with m_uscan[mi] <= u
+#pragma unroll
+            for (int step = kMemberChunk / 2; step >= 1; step >>= 1) {
+                const int c = mi + step;
+                if (c < m && m_uscan[c] <= u) mi = c;
+            }
+            const int r0 = (u - m_uscan[mi]) * kUnit;
+            const int w = m_w[mi];
+            const int start = m_start[mi], q0 = m_q0[mi], s0 = m_s0[mi], f0 = m_f0[mi];
+            const int64_t offg = m_off[mi];
+            int32_t v[kILP], old[kILP];
+            int64_t cell[kILP];
+#pragma unroll
+            for (int k = 0; k < kILP; ++k) {
+                const int r = r0 + k * 32 + (int)lane;
+                if (r < w) {
+                    v[k] = a.vals[start + r];
+                    int sl = s0 + r;
+                    if (sl >= W) sl -= W;
+                    cell[k] = offg + sl;
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < kILP; ++k) {
+                const int r = r0 + k * 32 + (int)lane;
+                old[k] = 0;
+                if (r < w) {
+                    int qq = q0 + r;
+                    if (qq >= W) qq -= W;
+                    if (qq < f0) old[k] = a.ring[cell[k]];
+                }
+            }
+            long long d = 0;
+            int32_t mnv = 0x7fffffff, mxv = (int32_t)0x80000000;
+#pragma unroll
+            for (int k = 0; k < kILP; ++k) {
+                const int r = r0 + k * 32 + (int)lane;
+                if (r < w) {
+                    a.ring[cell[k]] = v[k];
+                    d += (long long)v[k] - (long long)old[k];
+                    mnv = min(mnv, v[k]);
+                    mxv = max(mxv, v[k]);
+                }
+            }
+            d = warp_sum(d);
+            if (a.minmax) {
+                mnv = warp_min(mnv);
+                mxv = warp_max(mxv);
+            }
+            if (lane == 0) {
+                add_delta(&m_dlo[mi], &m_dhi[mi], d);
+                if (a.minmax) {
+                    atomicMin(&m_min[mi], mnv);
+                    atomicMax(&m_max[mi], mxv);
+                }
+            }
+        }
+
+        // ---- short members (< 32 values): kILP packed values per thread ----
+        for (int base = 0; base < s_total; base += kIngestThreads * kILP) {
             int mi[kILP];
             int32_t v[kILP], old[kILP];
             int64_t cell[kILP];
@@ -171,10 +257,8 @@ k_ingest(IngestArgs a) {
             for (int u = 0; u < kILP; ++u) {
                 const int t = base + u * kIngestThreads + threadIdx.x;
                 mi[u] = -1;
-                if (t < total) {
-                    // last member with m_scan[l] <= t; fixed trip count so the
-                    // kILP searches interleave
-                    int l = 0;
+                if (t < s_total) {
+                    int l = 0;                 // last member with m_scan[l] <= t
 #pragma unroll
                     for (int step = kMemberChunk / 2; step >= 1; step >>= 1) {
                         const int c = l + step;
@@ -216,13 +300,7 @@ k_ingest(IngestArgs a) {
                 const unsigned seg_end = 31u - __clz(peers);
                 const long long tot = seg_sum(d, seg_end);
                 const bool leader = valid && lane == (unsigned)(__ffs(peers) - 1);
-                if (leader) {
-                    const unsigned long long x = (unsigned long long)tot;
-                    const uint32_t lo32 = (uint32_t)x;
-                    const uint32_t prev = atomicAdd(&m_dlo[mi[u]], lo32);
-                    const uint32_t carry = (prev + lo32 < prev) ? 1u : 0u;
-                    atomicAdd(&m_dhi[mi[u]], (uint32_t)(x >> 32) + carry);
-                }
+                if (leader) add_delta(&m_dlo[mi[u]], &m_dhi[mi[u]], tot);
                 if (a.minmax && valid) {
                     const int32_t mnv = __reduce_min_sync(peers, v[u]);
                     const int32_t mxv = __reduce_max_sync(peers, v[u]);
@@ -257,10 +335,9 @@ k_ingest(IngestArgs a) {
         }
         __syncthreads();
     }
-    if (threadIdx.x == 0) {
-        if (a.part_ns) atomicAdd(&a.part_ns[p], (unsigned long long)(globaltimer() - t0));
-        if (a.part_work) atomicAdd(&a.part_work[p], work_total);
-    }
+    work_total = warp_sum(work_total);
+    if (lane == 0 && a.part_work && work_total) atomicAdd(&a.part_work[p], work_total);
+    if (threadIdx.x == 0 && a.part_ns) atomicAdd(&a.part_ns[p], (unsigned long long)(globaltimer() - t0));
 }
 
 // K5: fold each touched group's batch delta into its window state, emit
@@ -354,37 +431,62 @@ k_finalize(FinalizeArgs a) {
 }
 
 // MIN/MAX of a full window after a partial eviction: every ring slot is
-// live, so the slot order does not matter.  One CTA per listed group.
+// live, so the slot order does not matter.  Chunk-parallel: the listed
+// groups' windows are cut into kRescanChunk-value chunks spread over the
+// whole grid, folded with atomicMin/Max after a reset, then copied into
+// the result rows.
+constexpr int kRescanChunk = 16384;
+
+__global__ void k_rescan_reset(const int2* __restrict__ rescan, const unsigned* __restrict__ n_rescan,
+                               int32_t* __restrict__ mn, int32_t* __restrict__ mx) {
+    const unsigned n = *n_rescan;
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        mn[rescan[i].x] = 0x7fffffff;
+        mx[rescan[i].x] = (int32_t)0x80000000;
+    }
+}
+
 __global__ void __launch_bounds__(256)
 k_minmax_rescan(const int2* __restrict__ rescan, const unsigned* __restrict__ n_rescan,
                 const int32_t* __restrict__ ring, const int64_t* __restrict__ off, int64_t W,
-                int32_t* __restrict__ mn, int32_t* __restrict__ mx, int32_t* __restrict__ r_mn,
-                int32_t* __restrict__ r_mx) {
+                int32_t* __restrict__ mn, int32_t* __restrict__ mx) {
     __shared__ int32_t s_mn[8], s_mx[8];
     const unsigned n = *n_rescan;
-    for (unsigned i = blockIdx.x; i < n; i += gridDim.x) {
-        const int2 e = rescan[i];
+    const int64_t nch = (W + kRescanChunk - 1) / kRescanChunk;
+    for (int64_t c = blockIdx.x; c < (int64_t)n * nch; c += gridDim.x) {
+        const int2 e = rescan[c / nch];
+        const int64_t lo = (c % nch) * kRescanChunk;
+        const int64_t hi = min64(W, lo + kRescanChunk);
         const int32_t* r = ring + off[e.x];
-        int32_t lo = 0x7fffffff, hi = (int32_t)0x80000000;
-        for (int64_t j = threadIdx.x; j < W; j += blockDim.x) {
+        int32_t a = 0x7fffffff, b = (int32_t)0x80000000;
+        for (int64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) {
             const int32_t v = r[j];
-            lo = min(lo, v);
-            hi = max(hi, v);
+            a = min(a, v);
+            b = max(b, v);
         }
-        lo = warp_min(lo);
-        hi = warp_max(hi);
-        if (lane_id() == 0) { s_mn[warp_id()] = lo; s_mx[warp_id()] = hi; }
+        a = warp_min(a);
+        b = warp_max(b);
+        if (lane_id() == 0) { s_mn[warp_id()] = a; s_mx[warp_id()] = b; }
         __syncthreads();
         if (threadIdx.x == 0) {
-            for (int w = 1; w < 8; ++w) { lo = min(lo, s_mn[w]); hi = max(hi, s_mx[w]); }
-            mn[e.x] = lo;
-            mx[e.x] = hi;
-            if (e.y >= 0) {
-                r_mn[e.y] = lo;
-                r_mx[e.y] = hi;
-            }
+            for (int w = 1; w < 8; ++w) { a = min(a, s_mn[w]); b = max(b, s_mx[w]); }
+            atomicMin(&mn[e.x], a);
+            atomicMax(&mx[e.x], b);
         }
         __syncthreads();
+    }
+}
+
+__global__ void k_rescan_rows(const int2* __restrict__ rescan, const unsigned* __restrict__ n_rescan,
+                              const int32_t* __restrict__ mn, const int32_t* __restrict__ mx,
+                              int32_t* __restrict__ r_mn, int32_t* __restrict__ r_mx) {
+    const unsigned n = *n_rescan;
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int2 e = rescan[i];
+        if (e.y >= 0) {
+            r_mn[e.y] = mn[e.x];
+            r_mx[e.y] = mx[e.x];
+        }
     }
 }
 
