@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(1024)
 k_key_rank_small(KeyTable t) {
     __shared__ unsigned int f[kKeySmall];
     __shared__ int32_t en[kKeySmall];
-    const int nn = *t.n_new;
+    const int nn = min(*t.n_new, t.G);       // entries past G were never listed (overflow)
     if (nn == 0 || nn > kKeySmall) return;
     for (int i = threadIdx.x; i < nn; i += blockDim.x) {
         en[i] = t.new_ent[i];
@@ -109,12 +109,13 @@ k_key_rank_small(KeyTable t) {
         *t.n_new = 0;
     }
 }
+// n_new past kKeySmall is reset by k_key_mark_done
 
 // many new keys: mark[first position] = entry, then an ordered
 // compaction over the batch positions (count / scan / assign)
 __global__ void __launch_bounds__(256)
 k_key_mark(KeyTable t) {
-    const int nn = *t.n_new;
+    const int nn = min(*t.n_new, t.G);
     if (nn <= kKeySmall) return;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nn; i += gridDim.x * blockDim.x) {
         const int e = t.new_ent[i];
@@ -127,7 +128,7 @@ constexpr int kMarkBlk = 4096;
 __global__ void __launch_bounds__(1024)
 k_key_mark_count(KeyTable t, int64_t n, int32_t* __restrict__ bsum) {
     __shared__ int32_t red[33];
-    if (*t.n_new <= kKeySmall) return;
+    if (min(*t.n_new, t.G) <= kKeySmall) return;
     int c = 0;
     for (int q = 0; q < 4; ++q) {
         const int64_t i = (int64_t)blockIdx.x * kMarkBlk + q * 1024 + threadIdx.x;
@@ -141,7 +142,7 @@ k_key_mark_count(KeyTable t, int64_t n, int32_t* __restrict__ bsum) {
 __global__ void __launch_bounds__(1024)
 k_key_mark_scan(KeyTable t, int32_t* __restrict__ bsum, int nblk) {
     __shared__ int32_t red[33];
-    if (*t.n_new <= kKeySmall) return;
+    if (min(*t.n_new, t.G) <= kKeySmall) return;
     int32_t carry = *t.n_slots;
     for (int b0 = 0; b0 < nblk; b0 += 1024) {
         const int b = b0 + threadIdx.x;
@@ -156,7 +157,7 @@ k_key_mark_scan(KeyTable t, int32_t* __restrict__ bsum, int nblk) {
 __global__ void __launch_bounds__(1024)
 k_key_mark_assign(KeyTable t, int64_t n, const int32_t* __restrict__ bsum) {
     __shared__ int32_t red[33];
-    if (*t.n_new <= kKeySmall) return;
+    if (min(*t.n_new, t.G) <= kKeySmall) return;
     int32_t base = bsum[blockIdx.x];
     for (int q = 0; q < 4; ++q) {
         const int64_t i = (int64_t)blockIdx.x * kMarkBlk + q * 1024 + threadIdx.x;
@@ -175,7 +176,7 @@ k_key_mark_assign(KeyTable t, int64_t n, const int32_t* __restrict__ bsum) {
 }
 
 __global__ void k_key_mark_done(KeyTable t) {
-    const int nn = *t.n_new;
+    const int nn = min(*t.n_new, t.G);
     if (nn <= kKeySmall) return;
     *t.n_slots = min(*t.n_slots + nn, t.G);
     *t.n_new = 0;
