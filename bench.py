@@ -47,7 +47,14 @@ CONFIGS = {
            "zipf", 1.5, 100_000, 1_000_000, 1 << 24, ("count", "sum", "avg"), "prob", True),
     "c2split": ("C2 shape with hot-key splitting on top of prob_check",
                 "zipf", 1.0, 10_000, 100_000, 1 << 24, ("count", "sum"), "prob", True),
+    "c4": ("C4 1M groups, W=1e7, MIN/MAX/SUM, int64 keys, Zipf s=1.0, prob_check + hot-key split",
+           "zipf64", 1.0, 1_000_000, 10_000_000, 1 << 24, ("count", "sum", "min", "max"), "prob", True),
+    "c4u": ("C4 uniform twin: 1M groups, W=1e7, MIN/MAX/SUM, int64 keys",
+            "uniform64", 1.0, 1_000_000, 10_000_000, 1 << 24, ("count", "sum", "min", "max"), "prob", True),
+    "c5": ("C5 Zipf s=1.2 drifting (new hot set every 4 batches), 1M groups, W=1e7, SUM+COUNT+AVG",
+           "zipfdrift", 1.2, 1_000_000, 10_000_000, 1 << 24, ("count", "sum", "avg"), "prob", True),
 }
+MIX = 0x9E3779B97F4A7C15 - (1 << 64)     # odd: key = id * MIX (mod 2^64) is a bijection
 P_DEFAULT = 148
 L2_BYTES = 126 * (1 << 20)
 
@@ -69,17 +76,24 @@ def make_batches(kind, s, G, B, nbuf, device, seed):
     gen = torch.Generator(device=device)
     gen.manual_seed(seed)
     out = []
-    if kind == "zipf":
+    if kind.startswith("zipf"):
         w = torch.arange(1, G + 1, dtype=torch.float64, device=device).pow(-s)
         cdf = torch.cumsum(w, 0)
         cdf /= cdf[-1].clone()
         cdf[-1] = 1.0
     for i in range(nbuf):
-        if kind == "zipf":
+        if kind.startswith("zipf"):
             u = torch.rand(B, dtype=torch.float64, device=device, generator=gen)
-            g = torch.searchsorted(cdf, u, right=True).to(torch.int32)
+            g = torch.searchsorted(cdf, u, right=True).clamp_(max=G - 1)
+            if kind == "zipfdrift":
+                # the hot set moves: batch i uses its own seeded relabelling
+                perm = torch.randperm(G, device=device, generator=gen)
+                g = perm[g]
         else:
             g = (torch.arange(B, device=device, dtype=torch.int64) + i * B) % G
+        if kind.endswith("64"):
+            g = g.to(torch.int64) * MIX          # int64 keys (wrapping multiply)
+        else:
             g = g.to(torch.int32)
         a = torch.randint(-(2 ** 31), 2 ** 31, (B,), device=device, generator=gen,
                           dtype=torch.int64).to(torch.int32)
@@ -140,7 +154,7 @@ def cpu_pipeline(cfg_name, seconds=15.0, batch=1 << 20, P=P_DEFAULT):
     from oracle import port as O
     from paper_1309_0634_b200 import datagen as D
     desc, kind, s, G, W, _, aggs, policy, _ = CONFIGS[cfg_name]
-    dk = D.DatasetKind.UNIFORM if kind == "uniform" else D.DatasetKind.ZIPF
+    dk = D.DatasetKind.UNIFORM if kind.startswith("uniform") else D.DatasetKind.ZIPF
     spec = D.DatasetSpec(dk, batch * 64, G, s, 11)
     it = D.batches(D.stream_for(spec), batch)
     asg = O.contiguous_assignment(G, P)
@@ -254,10 +268,12 @@ def main():
         gbal = eng.balancer_struct("prob", thread_threshold=max(1, B // 10), pot=0.5)
     else:
         eng = StreamEngine(G, W, n_partitions=P, aggregates=aggs, device=local, max_batch=B,
-                           sub_batch=args.sub_batch)
+                           sub_batch=args.sub_batch, key_bits=64 if kind.endswith("64") else 32)
     eng.set_stream(stream)
     bal = eng.balancer_struct(policy, thread_threshold=thr, pot=0.5, split=split)
     nbuf = 4
+    if world > 1 and kind.endswith("64"):
+        raise SystemExit("int64 keys are single-GPU in this build (route is u32)")
     batches = make_batches(kind, s, G, B, nbuf, dev, seed=1234 + rank)
     torch.cuda.synchronize()
 
@@ -333,7 +349,7 @@ def main():
     e2e_steps = args.e2e_steps or max(3, args.steps // 4)
     hosts = []
     for g, a in batches[:2]:
-        hg = torch.empty(B, dtype=torch.int32, pin_memory=True)
+        hg = torch.empty(B, dtype=g.dtype, pin_memory=True)
         ha = torch.empty(B, dtype=torch.int32, pin_memory=True)
         hg.copy_(g)
         ha.copy_(a)
@@ -370,12 +386,22 @@ def main():
                "sample": f"{info['batches']} batches x 2^20 tuples ({info['seconds']} s) of the same "
                          f"stream shape through oracle/port.py on {cpu_model()}"}
 
-    # launches per step: count, batch_stats, 3 scans, balance (side), emit,
-    # 3 apply, report + per sub-batch (placement passes + ingest)
+    # our kernel launches per step: count, stats
+    # (+ split loads, + hot-cache select for G > 16K), 3 scans, the side-stream
+    # balancer (split-hot, policy, split-fill), per sub-batch placement
+    # passes + window exchange, ring growth (sparse store), finalize (+ 3
+    # MIN/MAX rescan kernels), 3 apply kernels, report; int64 keys add 8
     n_sub = -(-B // (eng_sub := (args.sub_batch or (1 << 21))))
     npass = 1 if (G - 1).bit_length() <= 11 else 2
-    per_step = 1 + 1 + 3 + (1 if policy != "no" else 0) + 1 + (3 if policy != "no" else 0) + 1 \
-        + n_sub * (npass + 1)
+    has_pol = policy != "no"
+    dense = G * W * 4 <= (24 << 30)
+    per_step = (1 + 1 + (1 if split else 0) + (1 if G > 16384 else 0) + 3
+                + (1 if split else 0) + (1 if has_pol else 0) + (1 if split else 0)
+                + n_sub * (npass + 1) + (0 if dense else 2) + 1
+                + (3 if ("min" in aggs or "max" in aggs) else 0) + (3 if has_pol else 0) + 1
+                + (8 if kind.endswith("64") else 0))
+    if world > 1:
+        per_step += 2          # owner histogram + route pass
     if rank == 0:
         line = {
             "metric": "sustained tuples/s (Zipf skew)",
@@ -383,7 +409,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "i32 keys/values, i64 sums",
             "data": f"synthetic {kind} (s={s}) keys generated on device, uniform int32 attrs; "
-                    f"{nbuf} staged batches of {B * 8 >> 20} MB each (> L2), cycled",
+                    f"{nbuf} staged batches of {B * (12 if kind.endswith('64') else 8) >> 20} MB each (> L2), cycled",
             "config": {"workload": desc, "groups": G, "window": W, "batch": B,
                        "partitions": P, "policy": policy + ("+split" if split else ""), "aggregates": list(aggs),
                        "sub_batch": eng_sub, "l2": "inputs larger than L2 (128 MB per batch)",
@@ -402,7 +428,7 @@ def main():
                            "max": float(np.max(ratios))},
             "moves_last_step": rep.moves,
             "cpu_baseline": cpu,
-            "e2e": {"value": e2e_value, "unit": "tuples/s", "h2d_bytes_per_step": 8 * B,
+            "e2e": {"value": e2e_value, "unit": "tuples/s", "h2d_bytes_per_step": (12 if kind.endswith("64") else 8) * B,
                     "d2h_bytes_per_step": d2h // e2e_steps, "steps": e2e_steps},
             "gpu_launches": per_step * args.steps,
             "clocks": clk,

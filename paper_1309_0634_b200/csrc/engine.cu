@@ -88,6 +88,7 @@ struct ss_engine {
     uint32_t* stage_keys = nullptr;
     int32_t* stage_vals = nullptr;
     int32_t *gcnt = nullptr, *gstart = nullptr, *gcount = nullptr, *bsum = nullptr, *gpre = nullptr;
+    int32_t* n_live = nullptr;             // live tuples per sub-batch (device)
     long long* bdelta = nullptr;           // per-group batch delta
     int32_t *bmin = nullptr, *bmax = nullptr;
     unsigned long long* part_work = nullptr;
@@ -252,25 +253,31 @@ int rb_for(int bits) {
 template <int RB>
 void launch_sort(cudaStream_t st, const uint32_t* kin, const int32_t* vin, uint32_t* kout, int32_t* vout,
                  int n, int shift, uint32_t mask, const uint32_t* base, unsigned long long* status,
-                 uint32_t epoch, uint32_t* ticket, const unsigned long long* bad, int stream_in) {
+                 uint32_t epoch, uint32_t* ticket, const unsigned long long* bad, int stream_in,
+                 const int32_t* live, const int32_t* n_dev) {
     const int tiles = (n + kSortTile - 1) / kSortTile;
     if (tiles == 0) return;
     k_sort_pass<RB><<<tiles, kSortThreads, SortSmem<RB>::bytes, st>>>(kin, vin, kout, vout, n, shift, mask, base,
-                                                                      status, epoch, ticket, bad, stream_in);
+                                                                      status, epoch, ticket, bad, stream_in,
+                                                                      nullptr, live, n_dev);
 }
 
 void sort_dispatch(int rb, cudaStream_t st, const uint32_t* kin, const int32_t* vin, uint32_t* kout,
                    int32_t* vout, int n, int shift, uint32_t mask, const uint32_t* base,
                    unsigned long long* status, uint32_t epoch, uint32_t* ticket,
-                   const unsigned long long* bad, int stream_in) {
+                   const unsigned long long* bad, int stream_in, const int32_t* live = nullptr,
+                   const int32_t* n_dev = nullptr) {
+#define SS_SORT_CASE(R) launch_sort<R>(st, kin, vin, kout, vout, n, shift, mask, base, status, epoch, ticket, bad, \
+                                       stream_in, live, n_dev)
     switch (rb) {
-        case 4: launch_sort<4>(st, kin, vin, kout, vout, n, shift, mask, base, status, epoch, ticket, bad, stream_in); break;
-        case 6: launch_sort<6>(st, kin, vin, kout, vout, n, shift, mask, base, status, epoch, ticket, bad, stream_in); break;
-        case 8: launch_sort<8>(st, kin, vin, kout, vout, n, shift, mask, base, status, epoch, ticket, bad, stream_in); break;
-        case 9: launch_sort<9>(st, kin, vin, kout, vout, n, shift, mask, base, status, epoch, ticket, bad, stream_in); break;
-        case 10: launch_sort<10>(st, kin, vin, kout, vout, n, shift, mask, base, status, epoch, ticket, bad, stream_in); break;
-        default: launch_sort<11>(st, kin, vin, kout, vout, n, shift, mask, base, status, epoch, ticket, bad, stream_in); break;
+        case 4: SS_SORT_CASE(4); break;
+        case 6: SS_SORT_CASE(6); break;
+        case 8: SS_SORT_CASE(8); break;
+        case 9: SS_SORT_CASE(9); break;
+        case 10: SS_SORT_CASE(10); break;
+        default: SS_SORT_CASE(11); break;
     }
+#undef SS_SORT_CASE
 }
 
 __global__ void k_fill_i32(int32_t* p, int64_t n, int32_t v) {
@@ -520,7 +527,7 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
         (rc = dalloc(e, &e->gcount, G)) || (rc = dalloc(e, &e->bsum, (size_t)nsub * e->nblk)) ||
         (rc = dalloc(e, &e->dhist, (size_t)nsub * 2 * kMaxBins)) || (rc = dalloc(e, &e->tpt, e->P)) ||
         (rc = dalloc(e, &e->touched, 1)) || (rc = dalloc(e, &e->bad, 1)) ||
-        (rc = dalloc(e, &e->tickets, (size_t)nsub * 2 + 2)) || (rc = dalloc(e, &e->gpre, (size_t)nsub * G)) ||
+        (rc = dalloc(e, &e->tickets, (size_t)nsub * 2 + 2)) || (rc = dalloc(e, &e->gpre, (size_t)nsub * G)) || (rc = dalloc(e, &e->n_live, nsub + 1)) ||
         (rc = dalloc(e, &e->bdelta, G)) || (rc = dalloc(e, &e->bmin, G)) || (rc = dalloc(e, &e->bmax, G)) ||
         (rc = dalloc(e, &e->hot_of, G)) || (rc = dalloc(e, &e->hot_g, kHotCache)) || (rc = dalloc(e, &e->n_hot_dev, 1)))
         return rc;
@@ -721,7 +728,7 @@ static int launch_scans(ss_engine* e, int n_sub) {
     SS_CUDA(e, cudaMemsetAsync(e->dhist, 0, (size_t)n_sub * 2 * kMaxBins * 4, e->st));
     dim3 g2(e->nblk, n_sub);
     k_scan_reduce<<<g2, 1024, 0, e->st>>>(e->gcnt, (uint32_t)e->G, e->bsum, e->nblk, e->plan, e->dhist, e->bad);
-    k_scan_top<<<n_sub, 1024, 0, e->st>>>(e->bsum, e->nblk, e->plan, e->dhist, e->bad);
+    k_scan_top<<<n_sub, 1024, 0, e->st>>>(e->bsum, e->nblk, e->plan, e->dhist, e->bad, e->n_live);
     k_scan_down<<<g2, 1024, 0, e->st>>>(e->gcnt, (uint32_t)e->G, e->bsum, e->nblk, e->gstart, e->bad);
     SS_CUDA(e, cudaGetLastError());
     return SS_OK;
@@ -743,16 +750,20 @@ static int launch_place(ss_engine* e, int s, const uint32_t* dk, const int32_t* 
         return e->epoch;
     };
     const uint32_t m0 = (1u << e->plan.bits[0]) - 1u;
+    // the step drops tuples that can never be stored (live counts); the
+    // reorder API places every tuple
+    const int32_t* live = want_keys ? nullptr : e->gcnt + (int64_t)s * e->G;
     if (e->plan.npass == 1) {
         sort_dispatch(e->rb[0], e->st, dk, dv, want_keys ? e->kbuf2 : nullptr, e->vbuf[0], (int)ns, 0, m0, base0,
-                      e->status, next_epoch(), t0, e->bad, stream_in);
+                      e->status, next_epoch(), t0, e->bad, stream_in, live);
     } else {
         const uint32_t m1 = (1u << e->plan.bits[1]) - 1u;
-        // pass 0: input -> (kbuf, vbuf1); pass 1: (kbuf, vbuf1) -> vbuf0 [+ kbuf2]
+        // pass 0: input -> (kbuf, vbuf1) [live only]; pass 1: -> vbuf0 [+ kbuf2]
         sort_dispatch(e->rb[0], e->st, dk, dv, e->kbuf, e->vbuf[1], (int)ns, e->plan.shift[0], m0, base0, e->status,
-                      next_epoch(), t0, e->bad, stream_in);
+                      next_epoch(), t0, e->bad, stream_in, live);
         sort_dispatch(e->rb[1], e->st, e->kbuf, e->vbuf[1], want_keys ? e->kbuf2 : nullptr, e->vbuf[0], (int)ns,
-                      e->plan.shift[1], m1, base1, e->status, next_epoch(), t1, e->bad, 0);
+                      e->plan.shift[1], m1, base1, e->status, next_epoch(), t1, e->bad, 0, nullptr,
+                      want_keys ? nullptr : e->n_live + s);
     }
     SS_CUDA(e, cudaGetLastError());
     return SS_OK;
@@ -917,7 +928,7 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
         {
             ProfScope ps(e, SS_K_INGEST, e->st);
             IngestArgs a = ingest_args(e, s, use_plan);
-            k_ingest<<<e->P, kIngestThreads, kIngestSmem, e->st>>>(a);
+            k_ingest<<<e->P * kCtaPerPart, kIngestThreads, kIngestSmem, e->st>>>(a);
         }
         SS_CUDA(e, cudaGetLastError());
     }

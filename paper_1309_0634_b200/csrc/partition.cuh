@@ -116,7 +116,7 @@ k_hot_select(const int32_t* __restrict__ gcount, uint32_t G, long long thr, int3
 // reference's count_batch outputs) and the touched-group count.
 // --------------------------------------------------------------------------
 __global__ void __launch_bounds__(1024)
-k_batch_stats(const int32_t* __restrict__ gcnt, int n_sub, uint32_t G, const int32_t* __restrict__ pmap,
+k_batch_stats(int32_t* __restrict__ gcnt, int n_sub, uint32_t G, const int32_t* __restrict__ pmap,
               int P, int32_t* __restrict__ gcount, unsigned long long* __restrict__ tpt,
               unsigned long long* __restrict__ touched, const unsigned long long* __restrict__ bad,
               const int32_t* __restrict__ fill, int64_t W, unsigned long long* __restrict__ alg_bytes,
@@ -134,6 +134,15 @@ k_batch_stats(const int32_t* __restrict__ gcnt, int n_sub, uint32_t G, const int
             c += gcnt[(int64_t)s * G + g];
         }
         gcount[g] = c;
+        // a sub-batch whose tuples of g all precede the last W of the batch
+        // can never contribute a stored value: its tuples are dropped before
+        // placement (live count 0); partially live sub-batches keep theirs
+        if (c > W) {
+            for (int s = 0; s < n_sub; ++s) {
+                const int64_t idx = (int64_t)s * G + g;
+                if ((int64_t)gpre[idx] + gcnt[idx] <= (int64_t)c - W) gcnt[idx] = 0;
+            }
+        }
         if (c) {
             atomicAdd(&sh_tpt[pmap[g]], (uint32_t)c);
             ++my_touched;
@@ -210,7 +219,7 @@ k_scan_reduce(const int32_t* __restrict__ gcnt, uint32_t G, int32_t* __restrict_
 // digit histogram -> digit bases.  grid = n_sub, block = 1024.
 __global__ void __launch_bounds__(1024)
 k_scan_top(int32_t* __restrict__ bsum, int nblk, DigitPlan plan, uint32_t* __restrict__ dhist,
-           const unsigned long long* __restrict__ bad) {
+           const unsigned long long* __restrict__ bad, int32_t* __restrict__ n_live) {
     __shared__ int32_t sh_red[33];
     __shared__ uint32_t sh_ured[33];
     if (*bad != (unsigned long long)kNoBad) return;
@@ -220,6 +229,7 @@ k_scan_top(int32_t* __restrict__ bsum, int nblk, DigitPlan plan, uint32_t* __res
         int32_t tot;
         int32_t ex = block_excl_scan(v, sh_red, &tot);
         if (threadIdx.x < (unsigned)nblk) bsum[(int64_t)s * nblk + threadIdx.x] = ex;
+        if (threadIdx.x == 0 && n_live) n_live[s] = tot;
     }
     for (int d = 0; d < plan.npass; ++d) {
         uint32_t* h = dhist + ((int64_t)s * 2 + d) * kMaxBins;
@@ -283,7 +293,8 @@ k_sort_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
             uint32_t* __restrict__ kout, int32_t* __restrict__ vout, int n, int shift, uint32_t mask,
             const uint32_t* __restrict__ bin_base, unsigned long long* __restrict__ status,
             uint32_t epoch, uint32_t* __restrict__ ticket, const unsigned long long* __restrict__ bad,
-            int stream_in, const int32_t* __restrict__ dmap = nullptr) {
+            int stream_in, const int32_t* __restrict__ dmap = nullptr,
+            const int32_t* __restrict__ live = nullptr, const int32_t* __restrict__ n_dev = nullptr) {
     constexpr int BINS = 1 << RB;
     constexpr int NW = kSortThreads / 32;
     constexpr int BPT = (BINS + kSortThreads - 1) / kSortThreads;   // bins owned per thread
@@ -301,7 +312,9 @@ k_sort_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
     __syncthreads();
     const uint32_t tile = sh_tile;
     const unsigned w = warp_id(), lane = lane_id();
+    if (n_dev) n = *n_dev;                       // consumes a compacted (live-only) input
     const int64_t tile0 = (int64_t)tile * kSortTile;
+    if (tile0 >= n) return;                      // beyond the input: nobody looks back at it
     const int tile_n = (int)min64(kSortTile, (int64_t)n - tile0);
     const int wbase = (int)w * 32 * kSortItems;
     uint16_t* myh = whist + w * BINS;
@@ -309,26 +322,24 @@ k_sort_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
     uint32_t key[kSortItems];
     int32_t val[kSortItems];
     uint32_t rank[kSortItems];
+    uint32_t ok = 0;                             // bit j: item j is valid (and live)
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
         const int li = wbase + j * 32 + (int)lane;
+        key[j] = 0xffffffffu;
+        val[j] = 0;
         if (li < tile_n) {
-            if (stream_in) {
-                key[j] = ld_stream_u32(kin + tile0 + li);
-                val[j] = (int32_t)ld_stream_u32(vin + tile0 + li);
-            } else {
-                key[j] = kin[tile0 + li];
-                val[j] = vin[tile0 + li];
+            key[j] = stream_in ? ld_stream_u32(kin + tile0 + li) : kin[tile0 + li];
+            if (!live || live[key[j]] > 0) {
+                val[j] = stream_in ? (int32_t)ld_stream_u32(vin + tile0 + li) : vin[tile0 + li];
+                ok |= 1u << j;
             }
-        } else {
-            key[j] = 0xffffffffu;
-            val[j] = 0;
         }
     }
     const unsigned lt = lanemask_lt();
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
-        const bool valid = wbase + j * 32 + (int)lane < tile_n;
+        const bool valid = (ok >> j) & 1u;
         const uint32_t d = valid ? (MAPPED ? (uint32_t)dmap[key[j]] : ((key[j] >> shift) & mask)) : 0xffffffffu;
         const unsigned peers = __match_any_sync(SS_FULL, d);
         uint32_t r = 0;
@@ -397,7 +408,7 @@ k_sort_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
     // tile-local sort into shared memory
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
-        if (wbase + j * 32 + (int)lane < tile_n) {
+        if ((ok >> j) & 1u) {
             const uint32_t d = MAPPED ? (uint32_t)dmap[key[j]] : ((key[j] >> shift) & mask);
             const uint32_t lp = tbin[d] + myh[d] + rank[j];
             skey[lp] = key[j];
@@ -406,7 +417,14 @@ k_sort_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
     }
     __syncthreads();
     // contiguous runs per digit to global memory
-    for (int i = threadIdx.x; i < tile_n; i += kSortThreads) {
+    uint32_t tlive;                              // live items of the tile
+    {
+        uint32_t mine = 0;
+#pragma unroll
+        for (int j = 0; j < kSortItems; ++j) mine += (ok >> j) & 1u;
+        block_excl_scan(mine, sh_red, &tlive);
+    }
+    for (int i = threadIdx.x; i < (int)tlive; i += kSortThreads) {
         const uint32_t k = skey[i];
         const uint32_t pos = gbase[MAPPED ? (uint32_t)dmap[k] : ((k >> shift) & mask)] + (uint32_t)i;
         vout[pos] = sval[i];

@@ -83,6 +83,7 @@ __device__ __forceinline__ void add_delta(uint32_t* lo, uint32_t* hi, long long 
 }
 
 constexpr int kUnit = 32 * kILP;            // values of one warp unit (long members)
+constexpr int kCtaPerPart = 2;              // CTAs sharing one partition's work
 
 __global__ void __launch_bounds__(kIngestThreads, 2)
 k_ingest(IngestArgs a) {
@@ -104,7 +105,10 @@ k_ingest(IngestArgs a) {
     if (*a.bad != (unsigned long long)kNoBad) return;
     uint64_t t0 = 0;
     if (threadIdx.x == 0) t0 = globaltimer();
-    const int p = blockIdx.x;
+    // partition p is processed by kCtaPerPart CTAs that interleave its
+    // warp units and short values (more warps in flight per partition)
+    const int p = blockIdx.x / kCtaPerPart;
+    const int sub = blockIdx.x % kCtaPerPart;
     const int lo = a.offsets[p], hi = a.offsets[p + 1];
     const int s_lo = a.share_off ? a.share_off[p] : 0;
     const int s_hi = a.share_off ? a.share_off[p + 1] : 0;
@@ -167,7 +171,7 @@ k_ingest(IngestArgs a) {
             else wshort[q] = w;
             ssum += wshort[q];
             usum += wunits[q];
-            work_total += (unsigned long long)w;
+            if (sub == 0) work_total += (unsigned long long)w;
         }
         int32_t s_total, u_total;
         int32_t sex = block_excl_scan(ssum, sh_red, &s_total);
@@ -189,7 +193,7 @@ k_ingest(IngestArgs a) {
         __syncthreads();
 
         // ---- long members: one warp per unit of kUnit contiguous values ----
-        for (int u = warp_id(); u < u_total; u += nw) {
+        for (int u = sub * nw + warp_id(); u < u_total; u += kCtaPerPart * nw) {
             int mi = 0;                                 // last member with m_uscan[mi] <= u
 #pragma unroll
             for (int step = kMemberChunk / 2; step >= 1; step >>= 1) {
@@ -249,7 +253,7 @@ k_ingest(IngestArgs a) {
         }
 
         // ---- short members (< 32 values): kILP packed values per thread ----
-        for (int base = 0; base < s_total; base += kIngestThreads * kILP) {
+        for (int base = sub * kIngestThreads * kILP; base < s_total; base += kCtaPerPart * kIngestThreads * kILP) {
             int mi[kILP];
             int32_t v[kILP], old[kILP];
             int64_t cell[kILP];
@@ -318,19 +322,13 @@ k_ingest(IngestArgs a) {
             const int tag = m_g[i];
             if (tag == 0x7fffffff) continue;
             const unsigned long long md = ((unsigned long long)m_dhi[i] << 32) | m_dlo[i];
-            if (tag >= 0) {                 // whole group: this CTA is its only writer
-                a.bdelta[tag] += (long long)md;
-                if (a.minmax) {
-                    a.bmin[tag] = min(a.bmin[tag], m_min[i]);
-                    a.bmax[tag] = max(a.bmax[tag], m_max[i]);
-                }
-            } else {                        // a share of a split hot key
-                const int g = a.split_g[-1 - tag];
-                atomicAdd((unsigned long long*)&a.bdelta[g], md);
-                if (a.minmax) {
-                    atomicMin(&a.bmin[g], m_min[i]);
-                    atomicMax(&a.bmax[g], m_max[i]);
-                }
+            // the partition's CTAs (and a split key's shares) meet here:
+            // native 64-bit global atomics, integer so order-independent
+            const int g = tag >= 0 ? tag : a.split_g[-1 - tag];
+            if (md) atomicAdd((unsigned long long*)&a.bdelta[g], md);
+            if (a.minmax && m_min[i] <= m_max[i]) {
+                atomicMin(&a.bmin[g], m_min[i]);
+                atomicMax(&a.bmax[g], m_max[i]);
             }
         }
         __syncthreads();

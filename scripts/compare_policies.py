@@ -1,0 +1,67 @@
+"""All balancer instantiations compared on one configuration (BASELINE C4:
+"all balancer instantiations compared").  For each policy, with and
+without hot-key splitting: steady-state tuples/s (CUDA events, staged
+batches in HBM), mean/max per-block max/mean load ratio, moves per batch.
+
+    python scripts/compare_policies.py --config c4 --steps 6 --warmup 3
+"""
+
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
+from paper_1309_0634_b200.stream_engine import StreamEngine  # noqa: E402
+
+POLICIES = ("no", "first", "all", "prob", "best", "shift", "shiftlocal")
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--steps", type=int, default=6)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--batch", type=int, default=0)
+    args = ap.parse_args()
+    desc, kind, s, G, W, B, aggs, _, _ = bench.CONFIGS[args.config]
+    B = args.batch or B
+    dev = torch.device("cuda", 0)
+    batches = bench.make_batches(kind, s, G, B, 2, dev, seed=99)
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+    for split in (False, True):
+        for pol in POLICIES:
+            eng = StreamEngine(G, W, n_partitions=148, aggregates=aggs, max_batch=B,
+                               key_bits=64 if kind.endswith("64") else 32)
+            eng.set_stream(stream)
+            bal = eng.balancer_struct(pol, max(1, B // 1480), 0.5, split=split)
+            for i in range(args.warmup):
+                eng.step(*batches[i % 2], bal)
+            ratios, moves = [], []
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record(stream)
+            for i in range(args.steps):
+                eng.step(*batches[i % 2], bal, sync=False)
+            e1.record(stream)
+            e1.synchronize()
+            ms = e0.elapsed_time(e1)
+            for i in range(2):
+                r = eng.step(*batches[i % 2], bal)
+                ratios.append(r.load_ratio)
+                moves.append(r.moves)
+            print(json.dumps({"config": args.config, "policy": pol, "split": split,
+                              "tuples_per_s": B * args.steps / (ms / 1e3),
+                              "ms_per_step": ms / args.steps,
+                              "load_ratio_mean": float(np.mean(ratios)), "load_ratio_max": float(np.max(ratios)),
+                              "moves_per_batch": float(np.mean(moves))}), flush=True)
+            eng.close()
+
+
+if __name__ == "__main__":
+    main()
