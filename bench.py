@@ -228,6 +228,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=0)
+    ap.add_argument("--initial", default="hash", choices=["hash", "contiguous"],
+                    help="initial group->partition map (north star: hash-partitioned groups)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -268,7 +270,8 @@ def main():
         gbal = eng.balancer_struct("prob", thread_threshold=max(1, B // 10), pot=0.5)
     else:
         eng = StreamEngine(G, W, n_partitions=P, aggregates=aggs, device=local, max_batch=B,
-                           sub_batch=args.sub_batch, key_bits=64 if kind.endswith("64") else 32)
+                           sub_batch=args.sub_batch, key_bits=64 if kind.endswith("64") else 32,
+                           initial=args.initial)
     eng.set_stream(stream)
     bal = eng.balancer_struct(policy, thread_threshold=thr, pot=0.5, split=split)
     nbuf = 4
@@ -411,7 +414,7 @@ def main():
             "data": f"synthetic {kind} (s={s}) keys generated on device, uniform int32 attrs; "
                     f"{nbuf} staged batches of {B * (12 if kind.endswith('64') else 8) >> 20} MB each (> L2), cycled",
             "config": {"workload": desc, "groups": G, "window": W, "batch": B,
-                       "partitions": P, "policy": policy + ("+split" if split else ""), "aggregates": list(aggs),
+                       "partitions": P, "initial_map": args.initial, "policy": policy + ("+split" if split else ""), "aggregates": list(aggs),
                        "sub_batch": eng_sub, "l2": "inputs larger than L2 (128 MB per batch)",
                        "parallelism": (f"key-sharded x{world}: NCCL all-to-all routing, GPU-level prob_check"
                                        if world > 1 else "single GPU"),

@@ -755,12 +755,12 @@ static int launch_place(ss_engine* e, int s, const uint32_t* dk, const int32_t* 
     const int32_t* live = want_keys ? nullptr : e->gcnt + (int64_t)s * e->G;
     if (e->plan.npass == 1) {
         sort_dispatch(e->rb[0], e->st, dk, dv, want_keys ? e->kbuf2 : nullptr, e->vbuf[0], (int)ns, 0, m0, base0,
-                      e->status, next_epoch(), t0, e->bad, stream_in, live);
+                      e->status, next_epoch(), t0, e->bad, stream_in, live, live ? e->n_live + s : nullptr);
     } else {
         const uint32_t m1 = (1u << e->plan.bits[1]) - 1u;
         // pass 0: input -> (kbuf, vbuf1) [live only]; pass 1: -> vbuf0 [+ kbuf2]
         sort_dispatch(e->rb[0], e->st, dk, dv, e->kbuf, e->vbuf[1], (int)ns, e->plan.shift[0], m0, base0, e->status,
-                      next_epoch(), t0, e->bad, stream_in, live);
+                      next_epoch(), t0, e->bad, stream_in, live, live ? e->n_live + s : nullptr);
         sort_dispatch(e->rb[1], e->st, e->kbuf, e->vbuf[1], want_keys ? e->kbuf2 : nullptr, e->vbuf[0], (int)ns,
                       e->plan.shift[1], m1, base1, e->status, next_epoch(), t1, e->bad, 0, nullptr,
                       want_keys ? nullptr : e->n_live + s);
@@ -799,6 +799,7 @@ static IngestArgs ingest_args(ss_engine* e, int s, bool with_plan) {
     }
     a.part_ns = e->part_ns;
     a.part_work = e->part_work;
+    a.n_live = e->n_live + s;
     a.bad = e->bad;
     return a;
 }
@@ -847,8 +848,8 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
         if ((rc = launch_stats(e, n_sub))) return rc;
         SS_CUDA(e, cudaMemsetAsync(e->loads, 0, e->P * 8, e->st));
         if (use_plan)
-            k_split_loads<<<2 * kNumSM, 256, 0, e->st>>>(e->gcount, (uint32_t)e->G, e->pmap, e->P,
-                                                         e->plan_buf[e->plan_cur], e->loads, e->bad);
+            k_split_loads<<<2 * kNumSM, 256, e->P * 4, e->st>>>(e->gcount, (uint32_t)e->G, e->pmap, e->P,
+                                                                e->plan_buf[e->plan_cur], e->loads, e->bad);
         if (e->G > 16384) {
             // hot cache for the next batch's count: > 1/(4 kHotCache) of the batch
             SS_CUDA(e, cudaMemsetAsync(e->n_hot_dev, 0, 4, e->st));
@@ -866,8 +867,8 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
             SS_CUDA(e, cudaMemsetAsync(e->spx.base, 0, e->P * 8, e->side));
             SS_CUDA(e, cudaMemsetAsync(e->spx.n_hot, 0, 4, e->side));
             const long long hot_min = std::max<long long>(1, n / (2LL * e->P));
-            k_split_hot<<<2 * kNumSM, 256, 0, e->side>>>(e->gcount, (uint32_t)e->G, e->pmap, hot_min, e->maxS, e->spx,
-                                                         e->bad);
+            k_split_hot<<<2 * kNumSM, 256, e->P * 4, e->side>>>(e->gcount, (uint32_t)e->G, e->pmap, hot_min, e->maxS,
+                                                                e->spx, e->P, e->bad);
         }
         if (has_policy) {
             BalanceArgs a{};

@@ -307,12 +307,13 @@ k_sort_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
     __shared__ uint32_t sh_tile;
     __shared__ uint32_t sh_red[33];
     if (*bad != (unsigned long long)kNoBad) return;
+    if (n_dev && *n_dev == 0) return;            // nothing live in this sub-batch
     if (threadIdx.x == 0) sh_tile = atomicAdd(ticket, 1u);
     for (int i = threadIdx.x; i < NW * BINS / 2; i += kSortThreads) ((uint32_t*)whist)[i] = 0;
     __syncthreads();
     const uint32_t tile = sh_tile;
     const unsigned w = warp_id(), lane = lane_id();
-    if (n_dev) n = *n_dev;                       // consumes a compacted (live-only) input
+    if (n_dev && !live) n = *n_dev;              // consumes a compacted (live-only) input
     const int64_t tile0 = (int64_t)tile * kSortTile;
     if (tile0 >= n) return;                      // beyond the input: nobody looks back at it
     const int tile_n = (int)min64(kSortTile, (int64_t)n - tile0);

@@ -44,11 +44,15 @@ struct SplitScratch {
     uint8_t* hot_flag;     // [G]
 };
 
-// Phase 1: hot detection + cold loads.  grid-stride over G.
+// Phase 1: hot detection + cold loads.  grid-stride over G; cold loads
+// accumulate per CTA in shared memory (P <= 4096) before one flush.
 __global__ void __launch_bounds__(256)
 k_split_hot(const int32_t* __restrict__ gcount, uint32_t G, const int32_t* __restrict__ pmap, long long hot_min,
-            int maxS, SplitScratch sc, const unsigned long long* __restrict__ bad) {
+            int maxS, SplitScratch sc, int P, const unsigned long long* __restrict__ bad) {
+    extern __shared__ uint32_t sh_base[];
     if (*bad != (unsigned long long)kNoBad) return;
+    for (int i = threadIdx.x; i < P; i += blockDim.x) sh_base[i] = 0;
+    __syncthreads();
     for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < G; g += gridDim.x * blockDim.x) {
         const int32_t c = gcount[g];
         uint8_t hot = 0;
@@ -60,8 +64,11 @@ k_split_hot(const int32_t* __restrict__ gcount, uint32_t G, const int32_t* __res
             }
         }
         sc.hot_flag[g] = hot;
-        if (c && !hot) atomicAdd(&sc.base[pmap[g]], (unsigned long long)c);
+        if (c && !hot) atomicAdd(&sh_base[pmap[g]], (uint32_t)c);
     }
+    __syncthreads();
+    for (int i = threadIdx.x; i < P; i += blockDim.x)
+        if (sh_base[i]) atomicAdd(&sc.base[i], (unsigned long long)sh_base[i]);
 }
 
 // Phase 3: water-fill the hot groups onto the loads left by the cold
@@ -206,11 +213,14 @@ k_split_fill(const int32_t* __restrict__ gcount, const long long* __restrict__ l
 __global__ void __launch_bounds__(256)
 k_split_loads(const int32_t* __restrict__ gcount, uint32_t G, const int32_t* __restrict__ pmap, int P,
               SplitPlan cur, unsigned long long* __restrict__ loads, const unsigned long long* __restrict__ bad) {
+    extern __shared__ uint32_t sh_load[];
     if (*bad != (unsigned long long)kNoBad) return;
+    for (int i = threadIdx.x; i < P; i += blockDim.x) sh_load[i] = 0;
+    __syncthreads();
     const int nsh = *cur.n_share;
     for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < G; g += gridDim.x * blockDim.x) {
         const int32_t c = gcount[g];
-        if (c && cur.split_of[g] < 0) atomicAdd(&loads[pmap[g]], (unsigned long long)c);
+        if (c && cur.split_of[g] < 0) atomicAdd(&sh_load[pmap[g]], (uint32_t)c);
     }
     // shares: one thread per share, find its partition by binary search
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nsh; i += gridDim.x * blockDim.x) {
@@ -219,8 +229,11 @@ k_split_loads(const int32_t* __restrict__ gcount, uint32_t G, const int32_t* __r
         const int j = cur.share_grp[i];
         const long long kt = gcount[cur.split_g[j]], den = cur.split_den[j];
         const long long a = kt * cur.share_lo[i] / den, b = kt * cur.share_hi[i] / den;
-        if (b > a) atomicAdd(&loads[l], (unsigned long long)(b - a));
+        if (b > a) atomicAdd(&sh_load[l], (uint32_t)(b - a));
     }
+    __syncthreads();
+    for (int i = threadIdx.x; i < P; i += blockDim.x)
+        if (sh_load[i]) atomicAdd(&loads[i], (unsigned long long)sh_load[i]);
 }
 
 }  // namespace ss

@@ -57,6 +57,7 @@ struct IngestArgs {
     const long long* split_den; // split-group index -> planned count
     unsigned long long* part_ns;       // per-partition (CTA) time, ns
     unsigned long long* part_work;     // per-partition stored values
+    const int32_t* n_live;      // live tuples of this sub-batch (0: nothing to do)
     const unsigned long long* bad;
 };
 
@@ -83,7 +84,7 @@ __device__ __forceinline__ void add_delta(uint32_t* lo, uint32_t* hi, long long 
 }
 
 constexpr int kUnit = 32 * kILP;            // values of one warp unit (long members)
-constexpr int kCtaPerPart = 2;              // CTAs sharing one partition's work
+constexpr int kCtaPerPart = 4;              // CTAs sharing one partition's work
 
 __global__ void __launch_bounds__(kIngestThreads, 2)
 k_ingest(IngestArgs a) {
@@ -103,6 +104,7 @@ k_ingest(IngestArgs a) {
     int32_t* m_max = m_min + kMemberChunk;
     __shared__ int32_t sh_red[33];
     if (*a.bad != (unsigned long long)kNoBad) return;
+    if (a.n_live && *a.n_live == 0) return;      // every tuple of the sub-batch was dropped
     uint64_t t0 = 0;
     if (threadIdx.x == 0) t0 = globaltimer();
     // partition p is processed by kCtaPerPart CTAs that interleave its

@@ -130,6 +130,19 @@ def _attrs_i32(attrs):
     return attrs.to(torch.int32)
 
 
+def hash_lists(n_groups: int, n_partitions: int):
+    """Static hash partitioning: group g -> mix(g) mod P, ids ascending
+    inside each partition (BASELINE C1 "static hash partitioning")."""
+    g = np.arange(n_groups, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        x = (g + np.uint64(0x9E3779B97F4A7C15)) * np.uint64(0xBF58476D1CE4E5B9)
+        x ^= x >> np.uint64(31)
+    part = (x % np.uint64(n_partitions)).astype(np.int64)
+    order = np.lexsort((np.arange(n_groups), part))
+    cuts = np.searchsorted(part[order], np.arange(n_partitions + 1))
+    return [order[cuts[i]:cuts[i + 1]].tolist() for i in range(n_partitions)]
+
+
 class StreamEngine:
     """Device-resident sliding-window GROUP BY with partitioned execution.
 
@@ -140,7 +153,7 @@ class StreamEngine:
     def __init__(self, n_groups: int, window, n_partitions: int = 148,
                  aggregates=("count", "sum", "avg"), device: int = 0,
                  max_batch: int = 1 << 24, sub_batch: int = 0, pool_values: int = 0,
-                 stream=None, key_bits: int = 32):
+                 stream=None, key_bits: int = 32, initial: str = "contiguous"):
         self._lib = L.load()
         if key_bits not in (32, 64):
             raise InvalidConfigError("key_bits must be 32 or 64")
@@ -170,6 +183,10 @@ class StreamEngine:
             self._h = None
             from .errors import raise_for_status
             raise_for_status(rc, msg.decode())
+        if initial == "hash":
+            self.set_lists(hash_lists(self.n_groups, self.n_partitions))
+        elif initial != "contiguous":
+            raise InvalidConfigError(f"unknown initial assignment {initial!r}")
         if stream is not None:
             self.set_stream(stream)
 
