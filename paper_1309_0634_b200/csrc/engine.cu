@@ -241,14 +241,7 @@ int bits_for(int64_t G) {
     return b;
 }
 
-int rb_for(int bits) {
-    if (bits <= 4) return 4;
-    if (bits <= 6) return 6;
-    if (bits <= 8) return 8;
-    if (bits <= 9) return 9;
-    if (bits <= 10) return 10;
-    return 11;
-}
+int rb_for(int bits) { return bits < 4 ? 4 : (bits > 11 ? 11 : bits); }
 
 template <int RB>
 void launch_sort(cudaStream_t st, const uint32_t* kin, const int32_t* vin, uint32_t* kout, int32_t* vout,
@@ -271,7 +264,9 @@ void sort_dispatch(int rb, cudaStream_t st, const uint32_t* kin, const int32_t* 
                                        stream_in, live, n_dev)
     switch (rb) {
         case 4: SS_SORT_CASE(4); break;
+        case 5: SS_SORT_CASE(5); break;
         case 6: SS_SORT_CASE(6); break;
+        case 7: SS_SORT_CASE(7); break;
         case 8: SS_SORT_CASE(8); break;
         case 9: SS_SORT_CASE(9); break;
         case 10: SS_SORT_CASE(10); break;
@@ -500,7 +495,14 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
     }
     // -- batch scratch
     e->max_batch = cfg->max_batch > 0 ? cfg->max_batch : (int64_t(1) << 24);
-    int64_t S = cfg->sub_batch > 0 ? cfg->sub_batch : kDefaultSub;
+    // default sub-batch: L2-sized (2^21), grown for large G so a group sees
+    // ~16 tuples per sub-batch (per-group staging is amortised), capped at
+    // the batch
+    int64_t S = cfg->sub_batch;
+    if (S <= 0) {
+        S = kDefaultSub;
+        while (S < 16 * cfg->n_groups && S < e->max_batch) S <<= 1;
+    }
     S = ((S + kCountChunk - 1) / kCountChunk) * kCountChunk;
     e->S = S;
     e->n_sub_max = (int)((e->max_batch + S - 1) / S);
@@ -609,7 +611,9 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
     e->h_rep->bad = (unsigned long long)kNoBad;
     SS_CUDA(e, cudaFuncSetAttribute(k_count<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     SS_CUDA(e, cudaFuncSetAttribute(k_sort_pass<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SortSmem<4>::bytes));
+    SS_CUDA(e, cudaFuncSetAttribute(k_sort_pass<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SortSmem<5>::bytes));
     SS_CUDA(e, cudaFuncSetAttribute(k_sort_pass<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SortSmem<6>::bytes));
+    SS_CUDA(e, cudaFuncSetAttribute(k_sort_pass<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SortSmem<7>::bytes));
     SS_CUDA(e, cudaFuncSetAttribute(k_sort_pass<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SortSmem<8>::bytes));
     SS_CUDA(e, cudaFuncSetAttribute(k_sort_pass<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SortSmem<9>::bytes));
     SS_CUDA(e, cudaFuncSetAttribute(k_sort_pass<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SortSmem<10>::bytes));

@@ -107,8 +107,8 @@ k_ingest(IngestArgs a) {
     if (a.n_live && *a.n_live == 0) return;      // every tuple of the sub-batch was dropped
     uint64_t t0 = 0;
     if (threadIdx.x == 0) t0 = globaltimer();
-    // partition p is processed by kCtaPerPart CTAs that interleave its
-    // warp units and short values (more warps in flight per partition)
+    // partition p is processed by kCtaPerPart CTAs; its members (and split
+    // shares) are dealt to them round-robin
     const int p = blockIdx.x / kCtaPerPart;
     const int sub = blockIdx.x % kCtaPerPart;
     const int lo = a.offsets[p], hi = a.offsets[p + 1];
@@ -121,8 +121,10 @@ k_ingest(IngestArgs a) {
     const int nw = kIngestThreads / 32;
     unsigned long long work_total = 0;
 
-    for (int c0 = 0; c0 < n_items; c0 += kMemberChunk) {
-        const int m = min(kMemberChunk, n_items - c0);
+    // this CTA's items: it = sub, sub + kCtaPerPart, ... (no duplicated staging)
+    const int my_items = (n_items - sub + kCtaPerPart - 1) / kCtaPerPart;
+    for (int c0 = 0; c0 < my_items; c0 += kMemberChunk) {
+        const int m = min(kMemberChunk, my_items - c0);
         int32_t wshort[kMPT], wunits[kMPT];
         int32_t ssum = 0, usum = 0;
 #pragma unroll
@@ -131,7 +133,7 @@ k_ingest(IngestArgs a) {
             wshort[q] = 0;
             wunits[q] = 0;
             if (i >= m) continue;
-            const int it = c0 + i;
+            const int it = (c0 + i) * kCtaPerPart + sub;
             int g, r_lo, r_hi;            // this item's slice [r_lo, r_hi) of the sub-batch run
             int32_t tag;
             if (it < n_mem) {
@@ -173,7 +175,7 @@ k_ingest(IngestArgs a) {
             else wshort[q] = w;
             ssum += wshort[q];
             usum += wunits[q];
-            if (sub == 0) work_total += (unsigned long long)w;
+            work_total += (unsigned long long)w;
         }
         int32_t s_total, u_total;
         int32_t sex = block_excl_scan(ssum, sh_red, &s_total);
@@ -195,7 +197,7 @@ k_ingest(IngestArgs a) {
         __syncthreads();
 
         // ---- long members: one warp per unit of kUnit contiguous values ----
-        for (int u = sub * nw + warp_id(); u < u_total; u += kCtaPerPart * nw) {
+        for (int u = warp_id(); u < u_total; u += nw) {
             int mi = 0;                                 // last member with m_uscan[mi] <= u
 #pragma unroll
             for (int step = kMemberChunk / 2; step >= 1; step >>= 1) {
@@ -255,7 +257,7 @@ k_ingest(IngestArgs a) {
         }
 
         // ---- short members (< 32 values): kILP packed values per thread ----
-        for (int base = sub * kIngestThreads * kILP; base < s_total; base += kCtaPerPart * kIngestThreads * kILP) {
+        for (int base = 0; base < s_total; base += kIngestThreads * kILP) {
             int mi[kILP];
             int32_t v[kILP], old[kILP];
             int64_t cell[kILP];
