@@ -394,7 +394,12 @@ def main():
     # balancer (split-hot, policy, split-fill), per sub-batch placement
     # passes + window exchange, ring growth (sparse store), finalize (+ 3
     # MIN/MAX rescan kernels), 3 apply kernels, report; int64 keys add 8
-    n_sub = -(-B // (eng_sub := (args.sub_batch or (1 << 21))))
+    eng_sub = args.sub_batch
+    if not eng_sub:                       # the engine's default rule (engine.cu, ss_create)
+        eng_sub = 1 << 21
+        while eng_sub < 16 * G and eng_sub < B:
+            eng_sub <<= 1
+    n_sub = -(-B // eng_sub)
     npass = 1 if (G - 1).bit_length() <= 11 else 2
     has_pol = policy != "no"
     dense = G * W * 4 <= (24 << 30)

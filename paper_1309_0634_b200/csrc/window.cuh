@@ -121,8 +121,14 @@ k_ingest(IngestArgs a) {
     const int nw = kIngestThreads / 32;
     unsigned long long work_total = 0;
 
-    // this CTA's items: it = sub, sub + kCtaPerPart, ... (no duplicated staging)
-    const int my_items = (n_items - sub + kCtaPerPart - 1) / kCtaPerPart;
+    // Few items (<= kMemberChunk): every CTA of the partition stages them all
+    // and the CTAs interleave the warp units / short values (a hot member's
+    // run spreads over all of them).  Many items: they are dealt round-robin
+    // (it = sub, sub + kCtaPerPart, ...) so nothing is staged twice.
+    const bool shared_items = n_items <= kMemberChunk;
+    const int my_items = shared_items ? n_items : (n_items - sub + kCtaPerPart - 1) / kCtaPerPart;
+    const int cstride = shared_items ? kCtaPerPart : 1;   // interleave factor
+    const int csub = shared_items ? sub : 0;
     for (int c0 = 0; c0 < my_items; c0 += kMemberChunk) {
         const int m = min(kMemberChunk, my_items - c0);
         int32_t wshort[kMPT], wunits[kMPT];
@@ -133,7 +139,7 @@ k_ingest(IngestArgs a) {
             wshort[q] = 0;
             wunits[q] = 0;
             if (i >= m) continue;
-            const int it = (c0 + i) * kCtaPerPart + sub;
+            const int it = shared_items ? c0 + i : (c0 + i) * kCtaPerPart + sub;
             int g, r_lo, r_hi;            // this item's slice [r_lo, r_hi) of the sub-batch run
             int32_t tag;
             if (it < n_mem) {
@@ -175,7 +181,7 @@ k_ingest(IngestArgs a) {
             else wshort[q] = w;
             ssum += wshort[q];
             usum += wunits[q];
-            work_total += (unsigned long long)w;
+            if (csub == 0) work_total += (unsigned long long)w;
         }
         int32_t s_total, u_total;
         int32_t sex = block_excl_scan(ssum, sh_red, &s_total);
@@ -197,7 +203,7 @@ k_ingest(IngestArgs a) {
         __syncthreads();
 
         // ---- long members: one warp per unit of kUnit contiguous values ----
-        for (int u = warp_id(); u < u_total; u += nw) {
+        for (int u = csub * nw + warp_id(); u < u_total; u += cstride * nw) {
             int mi = 0;                                 // last member with m_uscan[mi] <= u
 #pragma unroll
             for (int step = kMemberChunk / 2; step >= 1; step >>= 1) {
@@ -257,7 +263,7 @@ k_ingest(IngestArgs a) {
         }
 
         // ---- short members (< 32 values): kILP packed values per thread ----
-        for (int base = 0; base < s_total; base += kIngestThreads * kILP) {
+        for (int base = csub * kIngestThreads * kILP; base < s_total; base += cstride * kIngestThreads * kILP) {
             int mi[kILP];
             int32_t v[kILP], old[kILP];
             int64_t cell[kILP];
@@ -554,10 +560,12 @@ k_reserve(const int32_t* __restrict__ gcount, uint32_t G, int64_t W, const int32
 
 __global__ void __launch_bounds__(256)
 k_ring_copy(const RingCopy* __restrict__ copies, const unsigned* __restrict__ n_copies, int32_t* __restrict__ ring) {
+    // one warp per grown group (most copies are short)
     const unsigned n = *n_copies;
-    for (unsigned i = blockIdx.x; i < n; i += gridDim.x) {
+    const unsigned nwarps = gridDim.x * (blockDim.x >> 5);
+    for (unsigned i = blockIdx.x * (blockDim.x >> 5) + warp_id(); i < n; i += nwarps) {
         const RingCopy c = copies[i];
-        for (int j = threadIdx.x; j < c.len; j += blockDim.x) ring[c.dst + j] = ring[c.src + j];
+        for (int j = lane_id(); j < c.len; j += 32) ring[c.dst + j] = ring[c.src + j];
     }
 }
 
