@@ -351,10 +351,13 @@ def main():
     time.sleep(0.3)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
+    lib = L.load()
+    lib.ss_launch_count(1)
     ev0.record(stream)
     run_steps(args.steps, args.warmup)
     ev1.record(stream)
     ev1.synchronize()
+    launches = int(lib.ss_launch_count(1))
     ms = ev0.elapsed_time(ev1)
     clk = clocks.stop()
     rep = eng.last_report()
@@ -434,27 +437,7 @@ def main():
                          f"same stream shape, group-sharded over {info['cores']} processes through "
                          f"oracle/port.py on {cpu_model()}"}
 
-    # our kernel launches per step: count, stats
-    # (+ split loads, + hot-cache select for G > 16K), 3 scans, the side-stream
-    # balancer (split-hot, policy, split-fill), per sub-batch placement
-    # passes + window exchange, ring growth (sparse store), finalize (+ 3
-    # MIN/MAX rescan kernels), 3 apply kernels, report; int64 keys add 8
-    eng_sub = args.sub_batch
-    if not eng_sub:                       # the engine's default rule (engine.cu, ss_create)
-        eng_sub = 1 << 21
-        while eng_sub < 16 * G and eng_sub < B:
-            eng_sub <<= 1
-    n_sub = -(-B // eng_sub)
-    npass = 1 if (G - 1).bit_length() <= 11 else 2
-    has_pol = policy != "no"
-    dense = G * W * 4 <= (24 << 30)
-    per_step = (1 + 1 + (1 if split else 0) + (1 if G > 16384 else 0) + 3
-                + (1 if split else 0) + (1 if has_pol else 0) + (1 if split else 0)
-                + n_sub * (npass + 1) + (0 if dense else 2) + 1
-                + (3 if ("min" in aggs or "max" in aggs) else 0) + (3 if has_pol else 0) + 1
-                + (8 if kind.endswith("64") else 0))
-    if world > 1:
-        per_step += 2          # owner histogram + route pass
+    eng_sub = eng.sub_batch if hasattr(eng, "sub_batch") else args.sub_batch
     if rank == 0:
         line = {
             "metric": "sustained tuples/s (Zipf skew)",
@@ -483,7 +466,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "tuples/s", "h2d_bytes_per_step": (12 if kind.endswith("64") else 8) * B,
                     "d2h_bytes_per_step": d2h // e2e_steps, "steps": e2e_steps},
-            "gpu_launches": per_step * args.steps,
+            "gpu_launches": launches,
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)

@@ -108,6 +108,10 @@ int  ss_set_stream(ss_engine* e, void* cuda_stream);          /* stream the engi
 int  ss_sync(ss_engine* e);
 const char* ss_last_error(ss_engine* e);
 const char* ss_version(void);
+/* kernels this library has launched (all engines); reset != 0 zeroes it */
+long long ss_launch_count(int reset);
+/* the engine's placement sub-batch size (tuples) */
+long long ss_sub_batch(ss_engine* e);
 
 /* ---- assignment (partition.py:45-114, 181-203) ------------------------ */
 /* order[G]: concatenated per-partition lists; offsets[P+1] into order. */

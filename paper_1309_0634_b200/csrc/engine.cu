@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -34,6 +35,11 @@
 #include "keys.cuh"
 
 using namespace ss;
+
+// every kernel launch of the library goes through `ss_note_launch(), k<<<...>>>`
+// so the benchmark can report how many of our kernels ran (ss_launch_count)
+static std::atomic<long long> g_launches{0};
+static inline void ss_note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 namespace {
 
@@ -87,8 +93,10 @@ struct ss_engine {
     int n_sub_max = 0;
     uint32_t* stage_keys = nullptr;
     int32_t* stage_vals = nullptr;
-    int32_t *gcnt = nullptr, *gstart = nullptr, *gcount = nullptr, *bsum = nullptr, *gpre = nullptr;
-    int32_t* n_live = nullptr;             // live tuples per sub-batch (device)
+    int32_t *gcnt = nullptr, *gstart = nullptr, *gcount = nullptr, *bsum = nullptr;
+    int32_t* gkept = nullptr;              // kept (possibly stored) tuples of each group in the batch
+    int32_t* n_live = nullptr;             // kept tuples of the batch (device)
+    int32_t *chunk_live = nullptr, *lc = nullptr, *n_lc = nullptr;   // live-chunk flags / ordered list
     long long* bdelta = nullptr;           // per-group batch delta
     int32_t *bmin = nullptr, *bmax = nullptr;
     unsigned long long* part_work = nullptr;
@@ -243,25 +251,35 @@ int bits_for(int64_t G) {
 
 int rb_for(int bits) { return bits < 4 ? 4 : (bits > 11 ? 11 : bits); }
 
+// first-pass walk over the live chunks of the fused step (partition.cuh)
+struct ChunkWalk {
+    const int32_t* live;        // per-chunk kept counts [n_chunk][G]
+    const int32_t* lc;          // ordered live-chunk list
+    const int32_t* n_lc;
+    int chunk_shift;
+    uint32_t G;
+};
+
 template <int RB>
 void launch_sort(cudaStream_t st, const uint32_t* kin, const int32_t* vin, uint32_t* kout, int32_t* vout,
                  int n, int shift, uint32_t mask, const uint32_t* base, unsigned long long* status,
                  uint32_t epoch, uint32_t* ticket, const unsigned long long* bad, int stream_in,
-                 const int32_t* live, const int32_t* n_dev) {
+                 const int32_t* n_dev, const ChunkWalk* cw) {
     const int tiles = (n + kSortTile - 1) / kSortTile;
     if (tiles == 0) return;
-    k_sort_pass<RB><<<tiles, kSortThreads, SortSmem<RB>::bytes, st>>>(kin, vin, kout, vout, n, shift, mask, base,
-                                                                      status, epoch, ticket, bad, stream_in,
-                                                                      nullptr, live, n_dev);
+    ss_note_launch(), k_sort_pass<RB><<<tiles, kSortThreads, SortSmem<RB>::bytes, st>>>(
+        kin, vin, kout, vout, n, shift, mask, base, status, epoch, ticket, bad, stream_in, nullptr,
+        cw ? cw->live : nullptr, n_dev, cw ? cw->lc : nullptr, cw ? cw->n_lc : nullptr, cw ? cw->chunk_shift : 0,
+        cw ? cw->G : 0u);
 }
 
 void sort_dispatch(int rb, cudaStream_t st, const uint32_t* kin, const int32_t* vin, uint32_t* kout,
                    int32_t* vout, int n, int shift, uint32_t mask, const uint32_t* base,
                    unsigned long long* status, uint32_t epoch, uint32_t* ticket,
-                   const unsigned long long* bad, int stream_in, const int32_t* live = nullptr,
-                   const int32_t* n_dev = nullptr) {
+                   const unsigned long long* bad, int stream_in, const int32_t* n_dev = nullptr,
+                   const ChunkWalk* cw = nullptr) {
 #define SS_SORT_CASE(R) launch_sort<R>(st, kin, vin, kout, vout, n, shift, mask, base, status, epoch, ticket, bad, \
-                                       stream_in, live, n_dev)
+                                       stream_in, n_dev, cw)
     switch (rb) {
         case 4: SS_SORT_CASE(4); break;
         case 5: SS_SORT_CASE(5); break;
@@ -371,6 +389,12 @@ static int join_side(ss_engine* e);
 // --------------------------------------------------------------------------
 extern "C" const char* ss_version(void) { return "ss_b200 1.0 (sm_100a)"; }
 
+extern "C" long long ss_sub_batch(ss_engine* e) { return e ? (long long)e->S : 0; }
+
+extern "C" long long ss_launch_count(int reset) {
+    return reset ? g_launches.exchange(0) : g_launches.load();
+}
+
 extern "C" const char* ss_last_error(ss_engine* e) { return e ? e->err.c_str() : "null engine"; }
 
 extern "C" void ss_destroy(ss_engine* e) {
@@ -443,7 +467,7 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
     if ((rc = dalloc(e, &e->fill, G)) || (rc = dalloc(e, &e->next_pos, G)) || (rc = dalloc(e, &e->wsum, G)) ||
         (rc = dalloc(e, &e->mn, G)) || (rc = dalloc(e, &e->mx, G)) || (rc = dalloc(e, &e->cap, G)) ||
         (rc = dalloc(e, &e->off, G)) || (rc = dalloc(e, &e->pool_top, 1)) || (rc = dalloc(e, &e->oom, 1)) ||
-        (rc = dalloc(e, &e->copies, G)) || (rc = dalloc(e, &e->n_copies, 1)))
+        (rc = dalloc(e, &e->n_copies, 1)))
         return rc;
     SS_CUDA(e, cudaMemsetAsync(e->fill, 0, G * 4, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->next_pos, 0, G * 4, e->st));
@@ -457,7 +481,7 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
     if (e->dense) {
         e->pool_cap = (unsigned long long)dense_vals;
         if ((rc = dalloc(e, &e->ring, dense_vals))) return rc;
-        k_dense_off<<<296, 256, 0, e->st>>>(e->off, e->cap, G, W);
+        ss_note_launch(), k_dense_off<<<296, 256, 0, e->st>>>(e->off, e->cap, G, W);
     } else {
         int64_t pool = cfg->pool_values;
         if (pool <= 0) {
@@ -470,6 +494,9 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
         if ((rc = dalloc(e, &e->ring, pool))) return rc;
         SS_CUDA(e, cudaMemsetAsync(e->off, 0, G * 8, e->st));
         SS_CUDA(e, cudaMemsetAsync(e->cap, 0, G * 4, e->st));
+        // growth copies are listed in kCopyChunk pieces: at most one partial
+        // piece per group plus the pool's worth of full pieces
+        if ((rc = dalloc(e, &e->copies, G + pool / kCopyChunk + 1))) return rc;
     }
     // -- assignment: contiguous ranges (partition.py:97-114) until set
     if ((rc = dalloc(e, &e->pmap, G)) || (rc = dalloc(e, &e->order, G)) || (rc = dalloc(e, &e->new_order, G)) ||
@@ -495,15 +522,19 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
     }
     // -- batch scratch
     e->max_batch = cfg->max_batch > 0 ? cfg->max_batch : (int64_t(1) << 24);
-    // default sub-batch: L2-sized (2^21), grown for large G so a group sees
-    // ~16 tuples per sub-batch (per-group staging is amortised), capped at
-    // the batch
+    // count chunks: the granularity at which never-stored tuples are dropped
+    // (a chunk with no kept tuple is never read again).  Power of two >=
+    // 2^16, grown until the per-chunk histograms (n_chunk x G) stay <= 2^22
+    // entries and n_chunk <= 4096.
     int64_t S = cfg->sub_batch;
-    if (S <= 0) {
-        S = kDefaultSub;
-        while (S < 16 * cfg->n_groups && S < e->max_batch) S <<= 1;
+    if (S <= 0) S = int64_t(1) << 16;
+    {
+        int64_t p2 = int64_t(1) << 16;
+        while (p2 < S) p2 <<= 1;
+        S = p2;
+        auto nch = [&](int64_t c) { return (e->max_batch + c - 1) / c; };
+        while ((cfg->sub_batch <= 0 && nch(S) * G > (int64_t(1) << 22) && S < e->max_batch) || nch(S) > 4096) S <<= 1;
     }
-    S = ((S + kCountChunk - 1) / kCountChunk) * kCountChunk;
     e->S = S;
     e->n_sub_max = (int)((e->max_batch + S - 1) / S);
     const int nsub = e->n_sub_max;
@@ -529,19 +560,21 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
         (rc = dalloc(e, &e->gcount, G)) || (rc = dalloc(e, &e->bsum, (size_t)nsub * e->nblk)) ||
         (rc = dalloc(e, &e->dhist, (size_t)nsub * 2 * kMaxBins)) || (rc = dalloc(e, &e->tpt, e->P)) ||
         (rc = dalloc(e, &e->touched, 1)) || (rc = dalloc(e, &e->bad, 1)) ||
-        (rc = dalloc(e, &e->tickets, (size_t)nsub * 2 + 2)) || (rc = dalloc(e, &e->gpre, (size_t)nsub * G)) || (rc = dalloc(e, &e->n_live, nsub + 1)) ||
+        (rc = dalloc(e, &e->tickets, (size_t)nsub * 2 + 2)) || (rc = dalloc(e, &e->gkept, G)) || (rc = dalloc(e, &e->n_live, nsub + 1)) ||
+        (rc = dalloc(e, &e->chunk_live, nsub)) || (rc = dalloc(e, &e->lc, nsub)) || (rc = dalloc(e, &e->n_lc, 1)) ||
         (rc = dalloc(e, &e->bdelta, G)) || (rc = dalloc(e, &e->bmin, G)) || (rc = dalloc(e, &e->bmax, G)) ||
         (rc = dalloc(e, &e->hot_of, G)) || (rc = dalloc(e, &e->hot_g, kHotCache)) || (rc = dalloc(e, &e->n_hot_dev, 1)))
         return rc;
     SS_CUDA(e, cudaMemsetAsync(e->hot_of, 0xff, G * 4, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->n_hot_dev, 0, 4, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->bdelta, 0, G * 8, e->st));
-    k_fill_i32<<<296, 256, 0, e->st>>>(e->bmin, G, 0x7fffffff);
-    k_fill_i32<<<296, 256, 0, e->st>>>(e->bmax, G, (int32_t)0x80000000);
+    ss_note_launch(), k_fill_i32<<<296, 256, 0, e->st>>>(e->bmin, G, 0x7fffffff);
+    ss_note_launch(), k_fill_i32<<<296, 256, 0, e->st>>>(e->bmax, G, (int32_t)0x80000000);
     SS_CUDA(e, cudaMemsetAsync(e->gcnt, 0, (size_t)nsub * G * 4, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->gcount, 0, G * 4, e->st));
-    k_set_bad<<<1, 1, 0, e->st>>>(e->bad);
-    if ((rc = engine_alloc_sort(e, S))) return rc;
+    SS_CUDA(e, cudaMemsetAsync(e->chunk_live, 0, (size_t)nsub * 4, e->st));
+    ss_note_launch(), k_set_bad<<<1, 1, 0, e->st>>>(e->bad);
+    if ((rc = engine_alloc_sort(e, e->max_batch))) return rc;
     // -- int64 key table
     e->keys64 = cfg->key_bits == 64;
     if (e->keys64) {
@@ -559,7 +592,7 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
         t.cap_mask = cap - 1;
         t.G = (int)G;
         SS_CUDA(e, cudaMemsetAsync(t.keys, 0, (cap + 1) * 8, e->st));
-        k_fill_u64<<<296, 256, 0, e->st>>>(t.keys, cap + 1, kEmptyKey);
+        ss_note_launch(), k_fill_u64<<<296, 256, 0, e->st>>>(t.keys, cap + 1, kEmptyKey);
         SS_CUDA(e, cudaMemsetAsync(t.slot, 0xff, (cap + 1) * 4, e->st));
         SS_CUDA(e, cudaMemsetAsync(t.first, 0xff, (cap + 1) * 4, e->st));
         SS_CUDA(e, cudaMemsetAsync(t.mark, 0xff, e->max_batch * 4, e->st));
@@ -683,7 +716,8 @@ static int recover_bad(ss_engine* e) {
     e->side_pending = false;
     SS_CUDA(e, cudaMemsetAsync(e->gcnt, 0, (size_t)e->n_sub_max * e->G * 4, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->gcount, 0, e->G * 4, e->st));
-    k_set_bad<<<1, 1, 0, e->st>>>(e->bad);
+    SS_CUDA(e, cudaMemsetAsync(e->chunk_live, 0, (size_t)e->n_sub_max * 4, e->st));
+    ss_note_launch(), k_set_bad<<<1, 1, 0, e->st>>>(e->bad);
     SS_CUDA(e, cudaStreamSynchronize(e->st));
     return SS_OK;
 }
@@ -704,83 +738,107 @@ static int launch_count(ss_engine* e, const uint32_t* dk, int64_t n, int64_t S, 
         // larger chunks amortise the per-CTA flush of the G-bin histogram
         const int64_t chunk = (e->G > 2048 && S % 65536 == 0) ? 65536 : kCountChunk;
         const int64_t grid = (n + chunk - 1) / chunk;
-        k_count<true><<<(unsigned)grid, 512, e->G * 4, e->st>>>(dk, n, (uint32_t)e->G, S, chunk, e->gcnt, e->bad,
+        ss_note_launch(), k_count<true><<<(unsigned)grid, 512, e->G * 4, e->st>>>(dk, n, (uint32_t)e->G, S, chunk, e->gcnt, e->bad,
                                                                vec_ok, nullptr, nullptr, 0);
     } else {
         // the hot cache holds the previous batch's hot groups; its size is
         // fixed at kHotCache slots (unused slots count nothing)
         const int64_t grid = (n + kCountChunk - 1) / kCountChunk;
         const int nh = use_hot ? kHotCache : 0;
-        k_count<false><<<(unsigned)grid, 512, (size_t)nh * 4, e->st>>>(dk, n, (uint32_t)e->G, S, kCountChunk, e->gcnt,
+        ss_note_launch(), k_count<false><<<(unsigned)grid, 512, (size_t)nh * 4, e->st>>>(dk, n, (uint32_t)e->G, S, kCountChunk, e->gcnt,
                                                                       e->bad, vec_ok, e->hot_of, e->hot_g, nh);
     }
     SS_CUDA(e, cudaGetLastError());
     return SS_OK;
 }
 
-static int launch_stats(ss_engine* e, int n_sub) {
+// batch statistics over n_chunk count rows; `step` also derives the kept
+// counts and live chunks of the fused step
+static int launch_stats(ss_engine* e, int n_chunk, bool step = false) {
     SS_CUDA(e, cudaMemsetAsync(e->tpt, 0, e->P * 8, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->touched, 0, 8, e->st));
-    k_batch_stats<<<2 * kNumSM, 1024, e->P * 4, e->st>>>(e->gcnt, n_sub, (uint32_t)e->G, e->pmap, e->P, e->gcount,
-                                                          e->tpt, e->touched, e->bad, e->fill, e->W,
-                                                          e->alg_bytes, e->gpre);
+    // many chunks per group: a warp per group (lanes over chunks)
+    auto kern = n_chunk >= 16 ? k_batch_stats<true> : k_batch_stats<false>;
+    const unsigned grid = n_chunk >= 16 ? (unsigned)std::min<int64_t>((e->G + 31) / 32, 8 * kNumSM) : 2 * kNumSM;
+    ss_note_launch(), kern<<<grid, 1024, e->P * 4, e->st>>>(
+        e->gcnt, n_chunk, (uint32_t)e->G, e->pmap, e->P, e->gcount, step ? e->gkept : nullptr,
+        step ? e->chunk_live : nullptr, e->tpt, e->touched, e->bad, e->fill, e->W, e->alg_bytes);
     SS_CUDA(e, cudaGetLastError());
     return SS_OK;
 }
 
-static int launch_scans(ss_engine* e, int n_sub) {
-    SS_CUDA(e, cudaMemsetAsync(e->dhist, 0, (size_t)n_sub * 2 * kMaxBins * 4, e->st));
-    dim3 g2(e->nblk, n_sub);
-    k_scan_reduce<<<g2, 1024, 0, e->st>>>(e->gcnt, (uint32_t)e->G, e->bsum, e->nblk, e->plan, e->dhist, e->bad);
-    k_scan_top<<<n_sub, 1024, 0, e->st>>>(e->bsum, e->nblk, e->plan, e->dhist, e->bad, e->n_live);
-    k_scan_down<<<g2, 1024, 0, e->st>>>(e->gcnt, (uint32_t)e->G, e->bsum, e->nblk, e->gstart, e->bad);
+// G-sized scan of one count row -> run starts gstart[g] and the digit bases
+// of every placement pass; with n_chunk > 0 also the live-chunk list
+static int launch_scans(ss_engine* e, const int32_t* row, int n_chunk = 0) {
+    SS_CUDA(e, cudaMemsetAsync(e->dhist, 0, (size_t)2 * kMaxBins * 4, e->st));
+    dim3 g2(e->nblk, 1);
+    ss_note_launch(), k_scan_reduce<<<g2, 1024, 0, e->st>>>(row, (uint32_t)e->G, e->bsum, e->nblk, e->plan, e->dhist, e->bad);
+    ss_note_launch(), k_scan_top<<<1, 1024, 0, e->st>>>(e->bsum, e->nblk, e->plan, e->dhist, e->bad, e->n_live,
+                                                        n_chunk ? e->chunk_live : nullptr, n_chunk, e->lc, e->n_lc);
+    ss_note_launch(), k_scan_down<<<g2, 1024, 0, e->st>>>(row, (uint32_t)e->G, e->bsum, e->nblk, e->gstart, e->bad);
     SS_CUDA(e, cudaGetLastError());
     return SS_OK;
 }
 
-// stable placement of sub-batch s (keys/vals at its start, ns tuples) into
-// vbuf[0] (and kbuf with keys when want_keys)
-static int launch_place(ss_engine* e, int s, const uint32_t* dk, const int32_t* dv, int64_t ns, bool want_keys,
-                        bool stream_in) {
-    const uint32_t* base0 = e->dhist + ((int64_t)s * 2 + 0) * kMaxBins;
-    const uint32_t* base1 = e->dhist + ((int64_t)s * 2 + 1) * kMaxBins;
-    uint32_t* t0 = e->tickets + 2 * s;
-    uint32_t* t1 = e->tickets + 2 * s + 1;
-    auto next_epoch = [&]() {
-        if (++e->epoch >= (1u << 30) - 1) {
-            cudaMemsetAsync(e->status, 0, sizeof(unsigned long long) * e->status_tiles * kMaxBins, e->st);
-            e->epoch = 1;
-        }
-        return e->epoch;
-    };
+static uint32_t next_epoch(ss_engine* e) {
+    if (++e->epoch >= (1u << 30) - 1) {
+        cudaMemsetAsync(e->status, 0, sizeof(unsigned long long) * e->status_tiles * kMaxBins, e->st);
+        e->epoch = 1;
+    }
+    return e->epoch;
+}
+
+// reorder API: stable placement of all n tuples (keys -> kbuf2, values ->
+// vbuf[0]); no tuple is dropped
+static int launch_place_all(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_t n) {
+    const uint32_t* base0 = e->dhist;
+    const uint32_t* base1 = e->dhist + kMaxBins;
     const uint32_t m0 = (1u << e->plan.bits[0]) - 1u;
-    // the step drops tuples that can never be stored (live counts); the
-    // reorder API places every tuple
-    const int32_t* live = want_keys ? nullptr : e->gcnt + (int64_t)s * e->G;
     if (e->plan.npass == 1) {
-        sort_dispatch(e->rb[0], e->st, dk, dv, want_keys ? e->kbuf2 : nullptr, e->vbuf[0], (int)ns, 0, m0, base0,
-                      e->status, next_epoch(), t0, e->bad, stream_in, live, live ? e->n_live + s : nullptr);
+        sort_dispatch(e->rb[0], e->st, dk, dv, e->kbuf2, e->vbuf[0], (int)n, 0, m0, base0, e->status,
+                      next_epoch(e), e->tickets, e->bad, 0);
     } else {
         const uint32_t m1 = (1u << e->plan.bits[1]) - 1u;
-        // pass 0: input -> (kbuf, vbuf1) [live only]; pass 1: -> vbuf0 [+ kbuf2]
-        sort_dispatch(e->rb[0], e->st, dk, dv, e->kbuf, e->vbuf[1], (int)ns, e->plan.shift[0], m0, base0, e->status,
-                      next_epoch(), t0, e->bad, stream_in, live, live ? e->n_live + s : nullptr);
-        sort_dispatch(e->rb[1], e->st, e->kbuf, e->vbuf[1], want_keys ? e->kbuf2 : nullptr, e->vbuf[0], (int)ns,
-                      e->plan.shift[1], m1, base1, e->status, next_epoch(), t1, e->bad, 0, nullptr,
-                      want_keys ? nullptr : e->n_live + s);
+        sort_dispatch(e->rb[0], e->st, dk, dv, e->kbuf, e->vbuf[1], (int)n, e->plan.shift[0], m0, base0, e->status,
+                      next_epoch(e), e->tickets, e->bad, 0);
+        sort_dispatch(e->rb[1], e->st, e->kbuf, e->vbuf[1], e->kbuf2, e->vbuf[0], (int)n, e->plan.shift[1], m1, base1,
+                      e->status, next_epoch(e), e->tickets + 1, e->bad, 0);
     }
     SS_CUDA(e, cudaGetLastError());
     return SS_OK;
 }
 
-static IngestArgs ingest_args(ss_engine* e, int s, bool with_plan) {
+// fused step: stable placement of the batch's kept tuples (values only) into
+// vbuf[0].  The first pass walks the live chunks and drops never-stored
+// tuples; a second pass (G > 2^11) consumes the compacted kept set.
+static int launch_place_step(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_t n) {
+    const uint32_t* base0 = e->dhist;
+    const uint32_t* base1 = e->dhist + kMaxBins;
+    const uint32_t m0 = (1u << e->plan.bits[0]) - 1u;
+    int cs = 0;
+    while ((int64_t(1) << cs) < e->S) ++cs;
+    ChunkWalk cw{e->gcnt, e->lc, e->n_lc, cs, (uint32_t)e->G};
+    if (e->plan.npass == 1) {
+        sort_dispatch(e->rb[0], e->st, dk, dv, nullptr, e->vbuf[0], (int)n, 0, m0, base0, e->status, next_epoch(e),
+                      e->tickets, e->bad, 1, e->n_live, &cw);
+    } else {
+        const uint32_t m1 = (1u << e->plan.bits[1]) - 1u;
+        sort_dispatch(e->rb[0], e->st, dk, dv, e->kbuf, e->vbuf[1], (int)n, e->plan.shift[0], m0, base0, e->status,
+                      next_epoch(e), e->tickets, e->bad, 1, e->n_live, &cw);
+        sort_dispatch(e->rb[1], e->st, e->kbuf, e->vbuf[1], nullptr, e->vbuf[0], (int)n, e->plan.shift[1], m1, base1,
+                      e->status, next_epoch(e), e->tickets + 1, e->bad, 0, e->n_live, nullptr);
+    }
+    SS_CUDA(e, cudaGetLastError());
+    return SS_OK;
+}
+
+static IngestArgs ingest_args(ss_engine* e, bool with_plan) {
     IngestArgs a{};
     a.order = e->order;
     a.offsets = e->offsets;
-    a.gcnt = e->gcnt + (int64_t)s * e->G;
-    a.gpre = e->gpre + (int64_t)s * e->G;
-    a.gcount = e->gcount;
-    a.gstart = e->gstart + (int64_t)s * e->G;
+    a.gcnt = e->gkept;          // each group's kept run ...
+    a.gcount = e->gcount;       // ... is the suffix of its K batch tuples
+    a.gstart = e->gstart;
     a.vals = e->vbuf[0];
     a.fill = e->fill;
     a.next_pos = e->next_pos;
@@ -803,7 +861,7 @@ static IngestArgs ingest_args(ss_engine* e, int s, bool with_plan) {
     }
     a.part_ns = e->part_ns;
     a.part_work = e->part_work;
-    a.n_live = e->n_live + s;
+    a.n_live = e->n_live;
     a.bad = e->bad;
     return a;
 }
@@ -821,7 +879,7 @@ static int enqueue_report(ss_engine* e, int64_t n, bool has_policy, cudaStream_t
 // batch t+1; batch t+1's stats wait for it (they read the new map).
 static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_t n, const ss_balancer* bal,
                      bool emit) {
-    const int n_sub = (int)std::max<int64_t>(1, (n + e->S - 1) / e->S);
+    const int n_chunk = (int)std::max<int64_t>(1, (n + e->S - 1) / e->S);
     int rc;
     const bool split = bal && bal->split;
     // split mode: cold groups move by the configured extreme-pair policy
@@ -832,7 +890,7 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
         pol = SS_POLICY_BEST;
     const bool has_policy = pol != SS_POLICY_NO;
     const bool run_side = has_policy || split;
-    SS_CUDA(e, cudaMemsetAsync(e->tickets, 0, (size_t)n_sub * 2 * 4, e->st));
+    SS_CUDA(e, cudaMemsetAsync(e->tickets, 0, 2 * 4, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->part_ns, 0, e->P * 8, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->part_work, 0, e->P * 8, e->st));
     if (emit) SS_CUDA(e, cudaMemsetAsync(e->n_res, 0, 4, e->st));
@@ -849,15 +907,15 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
     e->last_plan = use_plan ? e->plan_cur : -1;
     {
         ProfScope ps(e, SS_K_STATS, e->st);
-        if ((rc = launch_stats(e, n_sub))) return rc;
+        if ((rc = launch_stats(e, n_chunk, true))) return rc;
         SS_CUDA(e, cudaMemsetAsync(e->loads, 0, e->P * 8, e->st));
         if (use_plan)
-            k_split_loads<<<2 * kNumSM, 256, e->P * 4, e->st>>>(e->gcount, (uint32_t)e->G, e->pmap, e->P,
+            ss_note_launch(), k_split_loads<<<2 * kNumSM, 256, e->P * 4, e->st>>>(e->gcount, (uint32_t)e->G, e->pmap, e->P,
                                                                 e->plan_buf[e->plan_cur], e->loads, e->bad);
         if (e->G > 16384) {
             // hot cache for the next batch's count: > 1/(4 kHotCache) of the batch
             SS_CUDA(e, cudaMemsetAsync(e->n_hot_dev, 0, 4, e->st));
-            k_hot_select<<<2 * kNumSM, 256, 0, e->st>>>(e->gcount, (uint32_t)e->G,
+            ss_note_launch(), k_hot_select<<<2 * kNumSM, 256, 0, e->st>>>(e->gcount, (uint32_t)e->G,
                                                         std::max<long long>(32, n / (4 * kHotCache)), e->hot_of,
                                                         e->hot_g, e->n_hot_dev, e->bad);
         }
@@ -871,7 +929,7 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
             SS_CUDA(e, cudaMemsetAsync(e->spx.base, 0, e->P * 8, e->side));
             SS_CUDA(e, cudaMemsetAsync(e->spx.n_hot, 0, 4, e->side));
             const long long hot_min = std::max<long long>(1, n / (2LL * e->P));
-            k_split_hot<<<2 * kNumSM, 256, e->P * 4, e->side>>>(e->gcount, (uint32_t)e->G, e->pmap, hot_min, e->maxS,
+            ss_note_launch(), k_split_hot<<<2 * kNumSM, 256, e->P * 4, e->side>>>(e->gcount, (uint32_t)e->G, e->pmap, hot_min, e->maxS,
                                                                 e->spx, e->P, e->bad);
         }
         if (has_policy) {
@@ -901,40 +959,35 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
                 a.exclude = e->spx.hot_flag;
                 a.stop_load = std::max<long long>(1, (n + e->P - 1) / e->P);
             }
-            k_balance<<<1, kBalThreads, (size_t)e->P * (8 + 8 * 4), e->side>>>(a);
+            ss_note_launch(), k_balance<<<1, kBalThreads, (size_t)e->P * (8 + 8 * 4), e->side>>>(a);
         }
         if (split) {
             const SplitPlan& nx = e->plan_buf[e->plan_cur ^ 1];
-            if (!has_policy) k_u64_to_i64<<<1, 1024, 0, e->side>>>(e->spx.base, e->final_tpt, e->P);
+            if (!has_policy) ss_note_launch(), k_u64_to_i64<<<1, 1024, 0, e->side>>>(e->spx.base, e->final_tpt, e->P);
             const size_t smem = (size_t)e->maxS * 20 + 16 + (size_t)(e->P + 1) * 4;
-            k_split_fill<<<1, 1024, smem, e->side>>>(e->gcount, e->final_tpt, e->P, e->maxS, e->spx, nx, nx, e->bad);
+            ss_note_launch(), k_split_fill<<<1, 1024, smem, e->side>>>(e->gcount, e->final_tpt, e->P, e->maxS, e->spx, nx, nx, e->bad);
         }
         SS_CUDA(e, cudaGetLastError());
     }
     {
         ProfScope ps(e, SS_K_STATS, e->st);
-        if ((rc = launch_scans(e, n_sub))) return rc;
+        if ((rc = launch_scans(e, e->gkept, n_chunk))) return rc;
     }
     if (!e->dense) {
         ProfScope ps(e, SS_K_INGEST, e->st);
         SS_CUDA(e, cudaMemsetAsync(e->n_copies, 0, 4, e->st));
-        k_reserve<<<2 * kNumSM, 256, 0, e->st>>>(e->gcount, (uint32_t)e->G, e->W, e->fill, e->off, e->cap,
+        ss_note_launch(), k_reserve<<<2 * kNumSM, 256, 0, e->st>>>(e->gcount, (uint32_t)e->G, e->W, e->fill, e->off, e->cap,
                                                  e->pool_top, e->pool_cap, e->oom, e->copies, e->n_copies, e->bad);
-        k_ring_copy<<<8 * kNumSM, 256, 0, e->st>>>(e->copies, e->n_copies, e->ring);
+        ss_note_launch(), k_ring_copy<<<8 * kNumSM, 256, 0, e->st>>>(e->copies, e->n_copies, e->ring);
     }
-    for (int s = 0; s < n_sub; ++s) {
-        const int64_t lo = (int64_t)s * e->S;
-        const int64_t ns = std::min<int64_t>(e->S, n - lo);
-        if (ns <= 0) break;
-        {
-            ProfScope ps(e, SS_K_PLACE, e->st);
-            if ((rc = launch_place(e, s, dk + lo, dv + lo, ns, false, true))) return rc;
-        }
-        {
-            ProfScope ps(e, SS_K_INGEST, e->st);
-            IngestArgs a = ingest_args(e, s, use_plan);
-            k_ingest<<<e->P * kCtaPerPart, kIngestThreads, kIngestSmem, e->st>>>(a);
-        }
+    {
+        ProfScope ps(e, SS_K_PLACE, e->st);
+        if ((rc = launch_place_step(e, dk, dv, n))) return rc;
+    }
+    {
+        ProfScope ps(e, SS_K_INGEST, e->st);
+        IngestArgs a = ingest_args(e, use_plan);
+        ss_note_launch(), k_ingest<<<e->P * kCtaPerPart, kIngestThreads, kIngestSmem, e->st>>>(a);
         SS_CUDA(e, cudaGetLastError());
     }
     if (run_side) SS_CUDA(e, cudaEventRecord(e->ev_k4, e->st));
@@ -943,7 +996,9 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
         FinalizeArgs f{};
         f.gcount = e->gcount;
         f.gcnt = e->gcnt;
-        f.n_sub = n_sub;
+        f.n_sub = n_chunk;
+        f.lc = e->lc;
+        f.n_lc = e->n_lc;
         f.G = (uint32_t)e->G;
         f.W = e->W;
         f.fill = e->fill;
@@ -966,12 +1021,12 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
         f.rescan = e->rescan;
         f.n_rescan = e->n_rescan;
         f.bad = e->bad;
-        k_finalize<<<2 * kNumSM, 256, 0, e->st>>>(f);
+        ss_note_launch(), k_finalize<<<2 * kNumSM, 256, 0, e->st>>>(f);
         if (e->minmax) {
-            k_rescan_reset<<<4, 256, 0, e->st>>>(e->rescan, e->n_rescan, e->mn, e->mx);
-            k_minmax_rescan<<<8 * kNumSM, 256, 0, e->st>>>(e->rescan, e->n_rescan, e->ring, e->off, e->W, e->mn,
+            ss_note_launch(), k_rescan_reset<<<4, 256, 0, e->st>>>(e->rescan, e->n_rescan, e->mn, e->mx);
+            ss_note_launch(), k_minmax_rescan<<<8 * kNumSM, 256, 0, e->st>>>(e->rescan, e->n_rescan, e->ring, e->off, e->W, e->mn,
                                                            e->mx);
-            k_rescan_rows<<<4, 256, 0, e->st>>>(e->rescan, e->n_rescan, e->mn, e->mx, e->r_mn, e->r_mx);
+            ss_note_launch(), k_rescan_rows<<<4, 256, 0, e->st>>>(e->rescan, e->n_rescan, e->mn, e->mx, e->r_mn, e->r_mx);
         }
         SS_CUDA(e, cudaGetLastError());
     }
@@ -979,10 +1034,10 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
         SS_CUDA(e, cudaStreamWaitEvent(e->side, e->ev_k4, 0));
         if (has_policy) {
             ProfScope ps(e, SS_K_APPLY, e->side);
-            k_apply_sizes<<<1, 1024, 0, e->side>>>(e->offsets, e->P, e->moves, e->n_moves, e->new_off);
-            k_apply_build<<<e->P, 256, 0, e->side>>>(e->order, e->offsets, e->new_off, e->moves, e->n_moves,
+            ss_note_launch(), k_apply_sizes<<<1, 1024, 0, e->side>>>(e->offsets, e->P, e->moves, e->n_moves, e->new_off);
+            ss_note_launch(), k_apply_build<<<e->P, 256, 0, e->side>>>(e->order, e->offsets, e->new_off, e->moves, e->n_moves,
                                                      e->front_top, e->back_first, e->mv_next, e->moved, e->new_order);
-            k_apply_commit<<<2 * kNumSM, 256, 0, e->side>>>(e->order, e->offsets, e->new_order, e->new_off, (int)e->G,
+            ss_note_launch(), k_apply_commit<<<2 * kNumSM, 256, 0, e->side>>>(e->order, e->offsets, e->new_order, e->new_off, (int)e->G,
                                                             e->P, e->moves, e->n_moves, e->pmap, e->moved);
             SS_CUDA(e, cudaGetLastError());
         }
@@ -1006,7 +1061,7 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
 // --------------------------------------------------------------------------
 static int enqueue_report(ss_engine* e, int64_t n, bool has_policy, cudaStream_t st) {
     const bool used_plan = e->last_plan >= 0;
-    k_report<<<1, 1024, 0, st>>>(e->tpt, used_plan ? e->loads : nullptr, e->P, e->bad, e->touched, e->n_moves,
+    ss_note_launch(), k_report<<<1, 1024, 0, st>>>(e->tpt, used_plan ? e->loads : nullptr, e->P, e->bad, e->touched, e->n_moves,
                                  e->prev_moves, e->scanned,
                                  used_plan ? e->plan_buf[e->last_plan].n_split : nullptr, e->n_res, e->oom,
                                  (long long)n, has_policy ? 1 : 0, e->d_rep);
@@ -1206,14 +1261,14 @@ extern "C" int ss_reorder(ss_engine* e, const uint32_t* groups, const int32_t* a
     if ((rc = stage_input(e, groups, attrs, n, &dk, &dv))) return rc;
     if ((rc = engine_alloc_sort(e, n))) return rc;
     int32_t* rank = g_rank_scratch(e);
-    k_rank_of<<<2 * kNumSM, 256, 0, e->st>>>(e->order, e->G, rank);
-    if (n) k_to_rank<<<2 * kNumSM, 256, 0, e->st>>>(dk, n, rank, (uint32_t)e->G, e->stage_keys, e->bad);
+    ss_note_launch(), k_rank_of<<<2 * kNumSM, 256, 0, e->st>>>(e->order, e->G, rank);
+    if (n) ss_note_launch(), k_to_rank<<<2 * kNumSM, 256, 0, e->st>>>(dk, n, rank, (uint32_t)e->G, e->stage_keys, e->bad);
     const uint32_t* rk = e->stage_keys;
     if ((rc = launch_count(e, rk, n, round_chunk(n)))) return rc;
     SS_CUDA(e, cudaMemsetAsync(e->tickets, 0, 8, e->st));
-    if ((rc = launch_scans(e, 1))) return rc;
-    if (n && (rc = launch_place(e, 0, rk, dv, n, true, false))) return rc;
-    if (n) k_from_rank<<<2 * kNumSM, 256, 0, e->st>>>(e->kbuf2, n, e->order);
+    if ((rc = launch_scans(e, e->gcnt))) return rc;
+    if (n && (rc = launch_place_all(e, rk, dv, n))) return rc;
+    if (n) ss_note_launch(), k_from_rank<<<2 * kNumSM, 256, 0, e->st>>>(e->kbuf2, n, e->order);
     unsigned long long bad;
     SS_CUDA(e, cudaMemcpyAsync(&bad, e->bad, 8, cudaMemcpyDeviceToHost, e->st));
     SS_CUDA(e, cudaStreamSynchronize(e->st));
@@ -1299,9 +1354,9 @@ extern "C" int ss_balance(ss_engine* e, const uint32_t* groups, int64_t n, const
         a.scanned = e->scanned;
         a.final_tpt = e->final_tpt;
         a.bad = e->bad;
-        k_balance<<<1, kBalThreads, (size_t)e->P * (8 + 8 * 4), e->st>>>(a);
+        ss_note_launch(), k_balance<<<1, kBalThreads, (size_t)e->P * (8 + 8 * 4), e->st>>>(a);
         SS_CUDA(e, cudaGetLastError());
-        k_clear_moved<<<4, 256, 0, e->st>>>(e->moves, e->n_moves, e->moved);
+        ss_note_launch(), k_clear_moved<<<4, 256, 0, e->st>>>(e->moves, e->n_moves, e->moved);
         SS_CUDA(e, cudaMemcpyAsync(&nm, e->n_moves, 4, cudaMemcpyDeviceToHost, e->st));
         SS_CUDA(e, cudaMemcpyAsync(&sc, e->scanned, 8, cudaMemcpyDeviceToHost, e->st));
         SS_CUDA(e, cudaMemcpyAsync(ft.data(), e->final_tpt, e->P * 8, cudaMemcpyDeviceToHost, e->st));
@@ -1572,7 +1627,7 @@ extern "C" int ss_route(ss_engine* e, const uint32_t* groups, const int32_t* att
     if ((rc = stage_input(e, groups, attrs, n, &dk, &dv))) return rc;
     if ((rc = engine_alloc_sort(e, n))) return rc;
     SS_CUDA(e, cudaMemsetAsync(e->route_cnt, 0, 16 * 8, e->st));
-    if (n) k_owner_hist<<<2 * kNumSM, 256, 0, e->st>>>(dk, n, (uint32_t)e->G, e->owner, e->route_cnt, e->bad);
+    if (n) ss_note_launch(), k_owner_hist<<<2 * kNumSM, 256, 0, e->st>>>(dk, n, (uint32_t)e->G, e->owner, e->route_cnt, e->bad);
     unsigned long long hc[16];
     unsigned long long bad;
     SS_CUDA(e, cudaMemcpyAsync(hc, e->route_cnt, 16 * 8, cudaMemcpyDeviceToHost, e->st));
@@ -1597,7 +1652,7 @@ extern "C" int ss_route(ss_engine* e, const uint32_t* groups, const int32_t* att
         e->epoch = 1;
     }
     const int tiles = (int)((n + kSortTile - 1) / kSortTile);
-    k_sort_pass<4, true><<<tiles, kSortThreads, SortSmem<4>::bytes, e->st>>>(
+    ss_note_launch(), k_sort_pass<4, true><<<tiles, kSortThreads, SortSmem<4>::bytes, e->st>>>(
         dk, dv, ko, vo, (int)n, 0, 15u, e->route_base, e->status, e->epoch, e->tickets, e->bad, 0, e->owner);
     SS_CUDA(e, cudaGetLastError());
     if (!dev_out) {
@@ -1636,7 +1691,7 @@ extern "C" int ss_balance_counts(ss_engine* e, const int32_t* counts, const ss_b
     SS_CUDA(e, cudaMemcpyAsync(e->gcount, counts, e->G * 4,
                                is_device_ptr(counts) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->tpt, 0, e->P * 8, e->st));
-    k_tpt_from_counts<<<2 * kNumSM, 256, 0, e->st>>>(e->gcount, e->G, e->pmap, e->tpt);
+    ss_note_launch(), k_tpt_from_counts<<<2 * kNumSM, 256, 0, e->st>>>(e->gcount, e->G, e->pmap, e->tpt);
     int nm = 0;
     long long sc = 0;
     std::vector<long long> ft(e->P);
@@ -1665,9 +1720,9 @@ extern "C" int ss_balance_counts(ss_engine* e, const int32_t* counts, const ss_b
         a.scanned = e->scanned;
         a.final_tpt = e->final_tpt;
         a.bad = e->bad;
-        k_balance<<<1, kBalThreads, (size_t)e->P * (8 + 8 * 4), e->st>>>(a);
+        ss_note_launch(), k_balance<<<1, kBalThreads, (size_t)e->P * (8 + 8 * 4), e->st>>>(a);
         SS_CUDA(e, cudaGetLastError());
-        k_clear_moved<<<4, 256, 0, e->st>>>(e->moves, e->n_moves, e->moved);
+        ss_note_launch(), k_clear_moved<<<4, 256, 0, e->st>>>(e->moves, e->n_moves, e->moved);
         SS_CUDA(e, cudaMemcpyAsync(&nm, e->n_moves, 4, cudaMemcpyDeviceToHost, e->st));
         SS_CUDA(e, cudaMemcpyAsync(&sc, e->scanned, 8, cudaMemcpyDeviceToHost, e->st));
         SS_CUDA(e, cudaMemcpyAsync(ft.data(), e->final_tpt, e->P * 8, cudaMemcpyDeviceToHost, e->st));
@@ -1780,14 +1835,14 @@ static int map_keys(ss_engine* e, const int64_t* keys, int64_t n, uint32_t* dout
     if (n == 0) return SS_OK;
     KeyTable& t = e->kt;
     const int nblk = (int)((n + kMarkBlk - 1) / kMarkBlk);
-    k_key_probe<<<4 * kNumSM, 256, 0, e->st>>>(dk, n, t);
-    k_key_rank_small<<<1, 1024, 0, e->st>>>(t);
-    k_key_mark<<<2 * kNumSM, 256, 0, e->st>>>(t);
-    k_key_mark_count<<<nblk, 1024, 0, e->st>>>(t, n, e->kbsum);
-    k_key_mark_scan<<<1, 1024, 0, e->st>>>(t, e->kbsum, nblk);
-    k_key_mark_assign<<<nblk, 1024, 0, e->st>>>(t, n, e->kbsum);
-    k_key_mark_done<<<1, 1, 0, e->st>>>(t);
-    k_key_map<<<4 * kNumSM, 256, 0, e->st>>>(dk, n, t, dout);
+    ss_note_launch(), k_key_probe<<<4 * kNumSM, 256, 0, e->st>>>(dk, n, t);
+    ss_note_launch(), k_key_rank_small<<<1, 1024, 0, e->st>>>(t);
+    ss_note_launch(), k_key_mark<<<2 * kNumSM, 256, 0, e->st>>>(t);
+    ss_note_launch(), k_key_mark_count<<<nblk, 1024, 0, e->st>>>(t, n, e->kbsum);
+    ss_note_launch(), k_key_mark_scan<<<1, 1024, 0, e->st>>>(t, e->kbsum, nblk);
+    ss_note_launch(), k_key_mark_assign<<<nblk, 1024, 0, e->st>>>(t, n, e->kbsum);
+    ss_note_launch(), k_key_mark_done<<<1, 1, 0, e->st>>>(t);
+    ss_note_launch(), k_key_map<<<4 * kNumSM, 256, 0, e->st>>>(dk, n, t, dout);
     SS_CUDA(e, cudaGetLastError());
     return SS_OK;
 }

@@ -112,50 +112,113 @@ k_hot_select(const int32_t* __restrict__ gcount, uint32_t G, long long thr, int3
 }
 
 // --------------------------------------------------------------------------
-// Batch statistics: gcount[g] = sum over sub-batches, tpt[pmap[g]] (the
-// reference's count_batch outputs) and the touched-group count.
+// Batch statistics: gcount[g] = sum over chunks, tpt[pmap[g]] (the
+// reference's count_batch outputs), the touched-group count and, for the
+// fused step, the kept tuples of every group.
+//
+// A group's tuples in chunk c can never be stored when all of them precede
+// the last W of the batch (pre_c + cnt_c <= K - W): their count is zeroed
+// (the placement drops them without reading their attrs).  The kept tuples
+// of a group are therefore a suffix of its batch tuples: gkept[g] of them,
+// the first at batch rank K - gkept.  chunk_live[c] marks chunks with any
+// kept tuple; the others are never read again.
 // --------------------------------------------------------------------------
+__device__ __forceinline__ void stats_account(uint32_t g, int32_t c, const int32_t* __restrict__ pmap,
+                                              uint32_t* sh_tpt, const int32_t* __restrict__ fill, int64_t W,
+                                              uint32_t& my_touched, unsigned long long& my_bytes) {
+    atomicAdd(&sh_tpt[pmap[g]], (uint32_t)c);
+    ++my_touched;
+    // algorithmic bytes: stored values, retracted old values
+    // that must be read, state + result row
+    const int64_t f0 = fill[g];
+    my_bytes += 4ull * (unsigned long long)min64(c, W) + 76ull;
+    if (c < W) my_bytes += 4ull * (unsigned long long)max64(0, f0 + c - W);
+}
+
+// WARP = true: one warp per group, lanes over the chunks (many chunks, few
+// groups); WARP = false: one thread per group (few chunks)
+template <bool WARP>
 __global__ void __launch_bounds__(1024)
-k_batch_stats(int32_t* __restrict__ gcnt, int n_sub, uint32_t G, const int32_t* __restrict__ pmap,
-              int P, int32_t* __restrict__ gcount, unsigned long long* __restrict__ tpt,
-              unsigned long long* __restrict__ touched, const unsigned long long* __restrict__ bad,
-              const int32_t* __restrict__ fill, int64_t W, unsigned long long* __restrict__ alg_bytes,
-              int32_t* __restrict__ gpre) {
+k_batch_stats(int32_t* __restrict__ gcnt, int n_chunk, uint32_t G, const int32_t* __restrict__ pmap,
+              int P, int32_t* __restrict__ gcount, int32_t* __restrict__ gkept, int32_t* __restrict__ chunk_live,
+              unsigned long long* __restrict__ tpt, unsigned long long* __restrict__ touched,
+              const unsigned long long* __restrict__ bad, const int32_t* __restrict__ fill, int64_t W,
+              unsigned long long* __restrict__ alg_bytes) {
     extern __shared__ uint32_t sh_tpt[];     // per-CTA partial loads (< 2^31)
     if (*bad != (unsigned long long)kNoBad) return;
     for (int p = threadIdx.x; p < P; p += blockDim.x) sh_tpt[p] = 0;
     __syncthreads();
     uint32_t my_touched = 0;
     unsigned long long my_bytes = 0;
-    for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < G; g += gridDim.x * blockDim.x) {
-        int32_t c = 0;
-        for (int s = 0; s < n_sub; ++s) {
-            gpre[(int64_t)s * G + g] = c;      // batch rank of the group's first tuple in sub-batch s
-            c += gcnt[(int64_t)s * G + g];
-        }
-        gcount[g] = c;
-        // a sub-batch whose tuples of g all precede the last W of the batch
-        // can never contribute a stored value: its tuples are dropped before
-        // placement (live count 0); partially live sub-batches keep theirs
-        if (c > W) {
-            for (int s = 0; s < n_sub; ++s) {
-                const int64_t idx = (int64_t)s * G + g;
-                if ((int64_t)gpre[idx] + gcnt[idx] <= (int64_t)c - W) gcnt[idx] = 0;
+    const unsigned lane = lane_id();
+    if (WARP) {
+        const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+        for (uint32_t g = blockIdx.x * (blockDim.x >> 5) + warp_id(); g < G; g += nwarps) {
+            int32_t c = 0;
+            for (int s = lane; s < n_chunk; s += 32) c += gcnt[(int64_t)s * G + g];
+            c = warp_sum(c);
+            int32_t kept = c;
+            if (c > W && gkept) {
+                kept = 0;
+                int32_t carry = 0;
+                for (int s0 = 0; s0 < n_chunk; s0 += 32) {
+                    const int s = s0 + (int)lane;
+                    const int64_t idx = (int64_t)s * G + g;
+                    const int32_t k = (s < n_chunk) ? gcnt[idx] : 0;
+                    const int32_t incl = warp_incl_scan(k);
+                    const int32_t pre = carry + incl - k;
+                    if (k) {
+                        if ((int64_t)pre + k <= (int64_t)c - W) gcnt[idx] = 0;
+                        else {
+                            kept += k;
+                            if (chunk_live) chunk_live[s] = 1;
+                        }
+                    }
+                    carry += __shfl_sync(SS_FULL, incl, 31);
+                }
+                kept = warp_sum(kept);
+            } else if (c && chunk_live) {
+                for (int s = lane; s < n_chunk; s += 32)
+                    if (gcnt[(int64_t)s * G + g]) chunk_live[s] = 1;
+            }
+            if (lane == 0) {
+                gcount[g] = c;
+                if (gkept) gkept[g] = kept;
+                if (c) stats_account(g, c, pmap, sh_tpt, fill, W, my_touched, my_bytes);
             }
         }
-        if (c) {
-            atomicAdd(&sh_tpt[pmap[g]], (uint32_t)c);
-            ++my_touched;
-            // algorithmic bytes: stored values, retracted old
-            // values that must be read, state + result row
-            const int64_t f0 = fill[g];
-            my_bytes += 4ull * (unsigned long long)min64(c, W) + 76ull;
-            if (c < W) my_bytes += 4ull * (unsigned long long)max64(0, f0 + c - W);
+    } else {
+        for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < G; g += gridDim.x * blockDim.x) {
+            int32_t c = 0;
+            for (int s = 0; s < n_chunk; ++s) c += gcnt[(int64_t)s * G + g];
+            gcount[g] = c;
+            int32_t kept = c;
+            if (c > W && gkept) {
+                int32_t pre = 0;
+                kept = 0;
+                for (int s = 0; s < n_chunk; ++s) {
+                    const int64_t idx = (int64_t)s * G + g;
+                    const int32_t k = gcnt[idx];
+                    if (k) {
+                        if ((int64_t)pre + k <= (int64_t)c - W) gcnt[idx] = 0;
+                        else {
+                            kept += k;
+                            if (chunk_live) chunk_live[s] = 1;
+                        }
+                    }
+                    pre += k;
+                }
+            } else if (c && chunk_live) {
+                for (int s = 0; s < n_chunk; ++s)
+                    if (gcnt[(int64_t)s * G + g]) chunk_live[s] = 1;
+            }
+            if (gkept) gkept[g] = kept;
+            if (c) stats_account(g, c, pmap, sh_tpt, fill, W, my_touched, my_bytes);
         }
     }
     my_touched = warp_sum(my_touched);
     my_bytes = warp_sum(my_bytes);
-    if (lane_id() == 0 && my_touched) {
+    if (lane == 0 && my_touched) {
         atomicAdd(touched, (unsigned long long)my_touched);
         atomicAdd(alg_bytes, my_bytes);
     }
@@ -216,10 +279,14 @@ k_scan_reduce(const int32_t* __restrict__ gcnt, uint32_t G, int32_t* __restrict_
 }
 
 // exclusive scan of the block sums (<= 1024 blocks) and of each pass's
-// digit histogram -> digit bases.  grid = n_sub, block = 1024.
+// digit histogram -> digit bases.  grid = n_sub, block = 1024.  Block 0 also
+// compacts the live-chunk flags into the ordered live-chunk list the first
+// placement pass walks (and clears the flags for the next batch).
 __global__ void __launch_bounds__(1024)
 k_scan_top(int32_t* __restrict__ bsum, int nblk, DigitPlan plan, uint32_t* __restrict__ dhist,
-           const unsigned long long* __restrict__ bad, int32_t* __restrict__ n_live) {
+           const unsigned long long* __restrict__ bad, int32_t* __restrict__ n_live,
+           int32_t* __restrict__ chunk_live = nullptr, int n_chunk = 0, int32_t* __restrict__ lc = nullptr,
+           int32_t* __restrict__ n_lc = nullptr) {
     __shared__ int32_t sh_red[33];
     __shared__ uint32_t sh_ured[33];
     if (*bad != (unsigned long long)kNoBad) return;
@@ -239,6 +306,25 @@ k_scan_top(int32_t* __restrict__ bsum, int nblk, DigitPlan plan, uint32_t* __res
         uint32_t ex = block_excl_scan(a + b, sh_ured, &tot);
         h[2 * threadIdx.x] = ex;
         h[2 * threadIdx.x + 1] = ex + a;
+    }
+    if (chunk_live && s == 0) {
+        // n_chunk <= 4 * 1024, 4 consecutive chunks per thread
+        int32_t f[4], mine = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int c = 4 * threadIdx.x + q;
+            f[q] = (c < n_chunk) ? chunk_live[c] : 0;
+            mine += f[q] ? 1 : 0;
+        }
+        int32_t tot;
+        int32_t ex = block_excl_scan(mine, sh_red, &tot);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int c = 4 * threadIdx.x + q;
+            if (f[q]) lc[ex++] = c;
+            if (c < n_chunk) chunk_live[c] = 0;
+        }
+        if (threadIdx.x == 0) *n_lc = tot;
     }
 }
 
@@ -294,7 +380,9 @@ k_sort_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
             const uint32_t* __restrict__ bin_base, unsigned long long* __restrict__ status,
             uint32_t epoch, uint32_t* __restrict__ ticket, const unsigned long long* __restrict__ bad,
             int stream_in, const int32_t* __restrict__ dmap = nullptr,
-            const int32_t* __restrict__ live = nullptr, const int32_t* __restrict__ n_dev = nullptr) {
+            const int32_t* __restrict__ live = nullptr, const int32_t* __restrict__ n_dev = nullptr,
+            const int32_t* __restrict__ lc = nullptr, const int32_t* __restrict__ n_lc = nullptr,
+            int chunk_shift = 0, uint32_t G = 0) {
     constexpr int BINS = 1 << RB;
     constexpr int NW = kSortThreads / 32;
     constexpr int BPT = (BINS + kSortThreads - 1) / kSortThreads;   // bins owned per thread
@@ -314,9 +402,23 @@ k_sort_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
     const uint32_t tile = sh_tile;
     const unsigned w = warp_id(), lane = lane_id();
     if (n_dev && !live) n = *n_dev;              // consumes a compacted (live-only) input
-    const int64_t tile0 = (int64_t)tile * kSortTile;
-    if (tile0 >= n) return;                      // beyond the input: nobody looks back at it
-    const int tile_n = (int)min64(kSortTile, (int64_t)n - tile0);
+    int64_t tile0 = (int64_t)tile * kSortTile;   // input offset of this tile
+    int tile_n;
+    if (lc) {
+        // live-chunk walk: tiles of chunks with no kept tuple do not exist;
+        // ticket t is tile (t mod tpc) of the (t / tpc)-th live chunk
+        const int tpc_shift = chunk_shift - 12;  // kSortTile = 2^12
+        const int ci = (int)(tile >> tpc_shift);
+        if (ci >= *n_lc) return;                 // beyond the kept tiles: nobody looks back at it
+        const int64_t c = lc[ci];
+        tile0 = (c << chunk_shift) + ((int64_t)(tile & ((1u << tpc_shift) - 1u)) << 12);
+        if (tile0 >= n) return;                  // past the end of a short last chunk: never waited on
+        tile_n = (int)min64(kSortTile, (int64_t)n - tile0);
+        live += c * (int64_t)G;                  // the chunk's kept counts
+    } else {
+        if (tile0 >= n) return;                  // beyond the input: nobody looks back at it
+        tile_n = (int)min64(kSortTile, (int64_t)n - tile0);
+    }
     const int wbase = (int)w * 32 * kSortItems;
     uint16_t* myh = whist + w * BINS;
 
@@ -324,17 +426,28 @@ k_sort_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
     int32_t val[kSortItems];
     uint32_t rank[kSortItems];
     uint32_t ok = 0;                             // bit j: item j is valid (and live)
+    // three load phases (keys, live flags, values), each with all kSortItems
+    // loads in flight, instead of one dependent key->flag->value chain per item
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
         const int li = wbase + j * 32 + (int)lane;
         key[j] = 0xffffffffu;
+        if (li < tile_n) key[j] = stream_in ? ld_stream_u32(kin + tile0 + li) : kin[tile0 + li];
+    }
+    int32_t lv[kSortItems];
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {
+        const int li = wbase + j * 32 + (int)lane;
+        lv[j] = (li < tile_n) ? 1 : 0;
+        if (live && li < tile_n) lv[j] = __ldg(live + key[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {
+        const int li = wbase + j * 32 + (int)lane;
         val[j] = 0;
-        if (li < tile_n) {
-            key[j] = stream_in ? ld_stream_u32(kin + tile0 + li) : kin[tile0 + li];
-            if (!live || live[key[j]] > 0) {
-                val[j] = stream_in ? (int32_t)ld_stream_u32(vin + tile0 + li) : vin[tile0 + li];
-                ok |= 1u << j;
-            }
+        if (lv[j] > 0) {
+            val[j] = stream_in ? (int32_t)ld_stream_u32(vin + tile0 + li) : vin[tile0 + li];
+            ok |= 1u << j;
         }
     }
     const unsigned lt = lanemask_lt();
@@ -390,15 +503,31 @@ k_sort_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
         if (b < BINS) {
             uint32_t excl = 0;
             if (tile > 0) {
+                // windowed look-back: the status words of up to kLB
+                // predecessors are loaded together, summed from the nearest
+                // back to the first inclusive prefix; an unpublished word
+                // restarts the window at that tile
+                constexpr int kLB = 4;
                 int64_t t = (int64_t)tile - 1;
                 while (true) {
-                    const unsigned long long v = ld_relaxed_u64(&status[t * BINS + b]);
-                    const uint32_t ep = (uint32_t)(v >> 34);
-                    const unsigned long long fl = (v >> 32) & 3ull;
-                    if (ep != epoch || fl == 0) continue;   // not published yet
-                    excl += (uint32_t)v;
-                    if (fl == kFlagInc) break;
-                    --t;
+                    unsigned long long v[kLB];
+#pragma unroll
+                    for (int k = 0; k < kLB; ++k)
+                        v[k] = (t - k >= 0) ? ld_relaxed_u64(&status[(t - k) * BINS + b]) : 0ull;
+                    bool done = false;
+                    int used = 0;
+#pragma unroll
+                    for (int k = 0; k < kLB; ++k) {
+                        if (done || used < k) continue;             // stopped earlier in the window
+                        const uint32_t ep = (uint32_t)(v[k] >> 34);
+                        const unsigned long long fl = (v[k] >> 32) & 3ull;
+                        if (t - k < 0 || ep != epoch || fl == 0) continue;   // not published yet
+                        excl += (uint32_t)v[k];
+                        used = k + 1;
+                        if (fl == kFlagInc) done = true;
+                    }
+                    if (done) break;
+                    t -= used;
                 }
                 st_relaxed_u64(&status[(int64_t)tile * BINS + b], lb_pack(epoch, kFlagInc, excl + tot[q]));
             }

@@ -34,10 +34,9 @@ constexpr size_t kIngestSmem = (size_t)kMemberChunk * (8 + 8 + 4 * 10) + 64;
 struct IngestArgs {
     const int32_t* order;       // partition lists, concatenated   [G]
     const int32_t* offsets;     // CSR offsets                     [P+1]
-    const int32_t* gcnt;        // group counts of this sub-batch  [G]
-    const int32_t* gpre;        // batch rank of each group's first tuple in this sub-batch
+    const int32_t* gcnt;        // kept tuples of each group (a suffix of its batch tuples) [G]
     const int32_t* gcount;      // group counts of the whole batch
-    const int32_t* gstart;      // run start of each group in the placed sub-batch
+    const int32_t* gstart;      // run start of each group in the placed kept set
     const int32_t* vals;        // placed (group-sorted, arrival-stable) values
     const int32_t* fill;        // batch-start state (read only in K4)
     const int32_t* next_pos;
@@ -131,13 +130,12 @@ k_ingest(IngestArgs a) {
     const int csub = shared_items ? sub : 0;
     for (int c0 = 0; c0 < my_items; c0 += kMemberChunk) {
         const int m = min(kMemberChunk, my_items - c0);
-        int32_t wshort[kMPT], wunits[kMPT];
-        int32_t ssum = 0, usum = 0;
+        // phase A: stage the items thread-strided (item i on thread i mod
+        // 512), so a partition with few members costs one dependent load
+        // chain per thread, not kMPT of them on a few threads
 #pragma unroll
         for (int q = 0; q < kMPT; ++q) {
-            const int i = threadIdx.x * kMPT + q;
-            wshort[q] = 0;
-            wunits[q] = 0;
+            const int i = q * kIngestThreads + threadIdx.x;
             if (i >= m) continue;
             const int it = shared_items ? c0 + i : (c0 + i) * kCtaPerPart + sub;
             int g, r_lo, r_hi;            // this item's slice [r_lo, r_hi) of the sub-batch run
@@ -156,32 +154,42 @@ k_ingest(IngestArgs a) {
                 r_lo = (int)(kt * a.share_lo[sh] / den);
                 r_hi = (int)(kt * a.share_hi[sh] / den);
             }
-            m_g[i] = 0x7fffffff;
-            m_w[i] = 0;
-            if (r_hi <= r_lo) continue;
-            const int K = a.gcount[g];                 // batch count
-            const int b = a.gpre[g];                   // batch rank of run index 0
-            const int first = max(r_lo, K - W - b);    // first stored run index
-            if (first >= r_hi) continue;
-            const int f0 = a.fill[g];
-            const int jb = b + first;                  // batch rank of the first stored value
-            const int w = r_hi - first;
-            m_g[i] = tag;
+            int w = 0;
+            if (r_hi > r_lo) {
+                const int K = a.gcount[g];                 // batch count
+                const int b = K - a.gcnt[g];               // batch rank of run index 0
+                const int first = max(r_lo, K - W - b);    // first stored run index
+                if (first < r_hi) {
+                    const int f0 = a.fill[g];
+                    const int jb = b + first;              // batch rank of the first stored value
+                    w = r_hi - first;
+                    m_start[i] = a.gstart[g] + first;
+                    m_q0[i] = (int)(((int64_t)f0 + jb) % W);
+                    m_s0[i] = (int)(((int64_t)a.next_pos[g] + f0 + jb) % W);
+                    m_f0[i] = (K >= W) ? 0 : f0;           // k >= W: nothing old survives
+                    m_off[i] = a.off[g];
+                    m_dlo[i] = 0;
+                    m_dhi[i] = 0;
+                    m_min[i] = 0x7fffffff;
+                    m_max[i] = (int32_t)0x80000000;
+                    if (csub == 0) work_total += (unsigned long long)w;
+                }
+            }
+            m_g[i] = w ? tag : 0x7fffffff;
             m_w[i] = w;
-            m_start[i] = a.gstart[g] + first;
-            m_q0[i] = (int)(((int64_t)f0 + jb) % W);
-            m_s0[i] = (int)(((int64_t)a.next_pos[g] + f0 + jb) % W);
-            m_f0[i] = (K >= W) ? 0 : f0;               // k >= W: nothing old survives
-            m_off[i] = a.off[g];
-            m_dlo[i] = 0;
-            m_dhi[i] = 0;
-            m_min[i] = 0x7fffffff;
-            m_max[i] = (int32_t)0x80000000;
-            if (w >= 32) wunits[q] = (w + kUnit - 1) / kUnit;
-            else wshort[q] = w;
+        }
+        __syncthreads();
+        // phase B: thread-contiguous scans of short values and long units
+        int32_t wshort[kMPT], wunits[kMPT];
+        int32_t ssum = 0, usum = 0;
+#pragma unroll
+        for (int q = 0; q < kMPT; ++q) {
+            const int i = threadIdx.x * kMPT + q;
+            const int w = (i < m) ? m_w[i] : 0;
+            wunits[q] = (w >= 32) ? (w + kUnit - 1) / kUnit : 0;
+            wshort[q] = (w >= 32) ? 0 : w;
             ssum += wshort[q];
             usum += wunits[q];
-            if (csub == 0) work_total += (unsigned long long)w;
         }
         int32_t s_total, u_total;
         int32_t sex = block_excl_scan(ssum, sh_red, &s_total);
@@ -353,8 +361,10 @@ k_ingest(IngestArgs a) {
 // rounded double quotient) and reset the batch accumulators.
 struct FinalizeArgs {
     const int32_t* gcount;
-    int32_t* gcnt;              // [n_sub][G] sub-batch counts, cleared here
+    int32_t* gcnt;              // [n_sub][G] chunk counts, cleared here
     int n_sub;
+    const int32_t* lc;          // live chunks (the only rows still holding counts) or null
+    const int32_t* n_lc;
     uint32_t G;
     int64_t W;
     int32_t* fill;
@@ -423,7 +433,12 @@ k_finalize(FinalizeArgs a) {
             a.bmin[g] = 0x7fffffff;
             a.bmax[g] = (int32_t)0x80000000;
         }
-        for (int s2 = 0; s2 < a.n_sub; ++s2) a.gcnt[(int64_t)s2 * a.G + g] = 0;
+        if (a.lc) {
+            const int nl = *a.n_lc;
+            for (int i = 0; i < nl; ++i) a.gcnt[(int64_t)a.lc[i] * a.G + g] = 0;
+        } else {
+            for (int s2 = 0; s2 < a.n_sub; ++s2) a.gcnt[(int64_t)s2 * a.G + g] = 0;
+        }
         if (need_rescan) a.rescan[atomicAdd(a.n_rescan, 1u)] = make_int2((int)g, a.emit ? (int)slot : -1);
         if (a.emit) {
             a.r_g[slot] = (int32_t)g;
@@ -502,8 +517,11 @@ __global__ void k_rescan_rows(const int2* __restrict__ rescan, const unsigned* _
 // every group whose window will hold more values than its capacity
 // (capacity doubles up to W; a window below W is linear, next_pos == 0,
 // so growth copies `fill` values).  Phase 1 reserves (warp-aggregated
-// atomics on the pool top) and lists the copies; phase 2 copies them with
-// one CTA per grown group.
+// atomics on the pool top) and lists the copies cut into kCopyChunk-value
+// pieces, so a hot group's multi-million-value copy spreads over the whole
+// grid; phase 2 copies one piece per CTA.
+constexpr int kCopyChunk = 8192;
+
 struct RingCopy {
     int64_t src, dst;
     int32_t len, pad;
@@ -544,12 +562,16 @@ k_reserve(const int32_t* __restrict__ gcount, uint32_t G, int64_t W, const int32
                 *oom = 1;
             } else {
                 if (f) {
-                    RingCopy rc;
-                    rc.src = oldoff;
-                    rc.dst = noff;
-                    rc.len = f;
-                    rc.pad = 0;
-                    copies[atomicAdd(n_copies, 1u)] = rc;
+                    const unsigned nch = (unsigned)((f + kCopyChunk - 1) / kCopyChunk);
+                    const unsigned c0 = atomicAdd(n_copies, nch);
+                    for (unsigned c = 0; c < nch; ++c) {
+                        RingCopy rc;
+                        rc.src = oldoff + (int64_t)c * kCopyChunk;
+                        rc.dst = noff + (int64_t)c * kCopyChunk;
+                        rc.len = min(kCopyChunk, f - (int)c * kCopyChunk);
+                        rc.pad = 0;
+                        copies[c0 + c] = rc;
+                    }
                 }
                 off[g] = noff;
                 cap[g] = (int32_t)ncap;
@@ -560,12 +582,10 @@ k_reserve(const int32_t* __restrict__ gcount, uint32_t G, int64_t W, const int32
 
 __global__ void __launch_bounds__(256)
 k_ring_copy(const RingCopy* __restrict__ copies, const unsigned* __restrict__ n_copies, int32_t* __restrict__ ring) {
-    // one warp per grown group (most copies are short)
     const unsigned n = *n_copies;
-    const unsigned nwarps = gridDim.x * (blockDim.x >> 5);
-    for (unsigned i = blockIdx.x * (blockDim.x >> 5) + warp_id(); i < n; i += nwarps) {
+    for (unsigned i = blockIdx.x; i < n; i += gridDim.x) {
         const RingCopy c = copies[i];
-        for (int j = lane_id(); j < c.len; j += 32) ring[c.dst + j] = ring[c.src + j];
+        for (int j = threadIdx.x; j < c.len; j += blockDim.x) ring[c.dst + j] = ring[c.src + j];
     }
 }
 

@@ -189,6 +189,7 @@ class StreamEngine:
             raise InvalidConfigError(f"unknown initial assignment {initial!r}")
         if stream is not None:
             self.set_stream(stream)
+        self.sub_batch = int(self._lib.ss_sub_batch(self._h))
 
     # -- lifecycle ---------------------------------------------------------
     def close(self):
