@@ -13,7 +13,7 @@ import os
 from .errors import ExecutionError, raise_for_status
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libss_b200.so")
+LIB_PATH = os.environ.get("SS_B200_LIB") or os.path.join(HERE, "_lib", "libss_b200.so")
 
 AGG_COUNT, AGG_SUM, AGG_AVG, AGG_MIN, AGG_MAX = 1, 2, 4, 8, 16
 POLICY_CODES = {"no": 0, "first": 1, "all": 2, "prob": 3, "best": 4,

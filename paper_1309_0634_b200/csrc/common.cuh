@@ -59,6 +59,31 @@ __device__ __forceinline__ uint32_t ld_stream_u32(const void* p) {
     return r;
 }
 
+// Ampere-style asynchronous global -> shared copies (4 bytes, any alignment)
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// __match_any_sync for a BITS-bit value built from BITS ballots (plus one
+// for the valid flag): fixed cost, where the MATCH instruction's cost grows
+// with the number of distinct values in the warp
+template <int BITS>
+__device__ __forceinline__ unsigned match_bits(uint32_t v, bool valid) {
+    unsigned m = __ballot_sync(SS_FULL, valid);
+    m = valid ? m : ~m;
+#pragma unroll
+    for (int b = 0; b < BITS; ++b) {
+        const bool bit = (v >> b) & 1u;
+        const unsigned bb = __ballot_sync(SS_FULL, bit);
+        m &= bit ? bb : ~bb;
+    }
+    return m;
+}
+
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll

@@ -97,6 +97,8 @@ struct ss_engine {
     int32_t* gkept = nullptr;              // kept (possibly stored) tuples of each group in the batch
     int32_t* n_live = nullptr;             // kept tuples of the batch (device)
     int32_t *chunk_live = nullptr, *lc = nullptr, *n_lc = nullptr;   // live-chunk flags / ordered list
+    uint32_t *chunk_h = nullptr, *chunk_base = nullptr;   // first-pass digit histograms / bases per live chunk
+    int32_t* btile = nullptr;              // second-pass tile prefix over first-pass buckets
     long long* bdelta = nullptr;           // per-group batch delta
     int32_t *bmin = nullptr, *bmax = nullptr;
     unsigned long long* part_work = nullptr;
@@ -251,35 +253,27 @@ int bits_for(int64_t G) {
 
 int rb_for(int bits) { return bits < 4 ? 4 : (bits > 11 ? 11 : bits); }
 
-// first-pass walk over the live chunks of the fused step (partition.cuh)
-struct ChunkWalk {
-    const int32_t* live;        // per-chunk kept counts [n_chunk][G]
-    const int32_t* lc;          // ordered live-chunk list
-    const int32_t* n_lc;
-    int chunk_shift;
-    uint32_t G;
-};
-
 template <int RB>
 void launch_sort(cudaStream_t st, const uint32_t* kin, const int32_t* vin, uint32_t* kout, int32_t* vout,
                  int n, int shift, uint32_t mask, const uint32_t* base, unsigned long long* status,
                  uint32_t epoch, uint32_t* ticket, const unsigned long long* bad, int stream_in,
-                 const int32_t* n_dev, const ChunkWalk* cw) {
-    const int tiles = (n + kSortTile - 1) / kSortTile;
+                 const int32_t* n_dev, const SortSeg* sg) {
+    // mode 2 adds up to one partial tile per bucket
+    const int tiles = (n + kSortTile - 1) / kSortTile + (sg && sg->mode == 2 ? sg->nb : 0);
     if (tiles == 0) return;
-    ss_note_launch(), k_sort_pass<RB><<<tiles, kSortThreads, SortSmem<RB>::bytes, st>>>(
-        kin, vin, kout, vout, n, shift, mask, base, status, epoch, ticket, bad, stream_in, nullptr,
-        cw ? cw->live : nullptr, n_dev, cw ? cw->lc : nullptr, cw ? cw->n_lc : nullptr, cw ? cw->chunk_shift : 0,
-        cw ? cw->G : 0u);
+    // persistent: at most the co-resident CTAs (2 per SM), each looping over tickets
+    ss_note_launch(), k_sort_pass<RB><<<std::min(tiles, 2 * kNumSM), kSortThreads, SortSmem<RB>::bytes, st>>>(
+        kin, vin, kout, vout, n, shift, mask, base, status, epoch, ticket, bad, stream_in, nullptr, n_dev,
+        sg ? *sg : SortSeg{});
 }
 
 void sort_dispatch(int rb, cudaStream_t st, const uint32_t* kin, const int32_t* vin, uint32_t* kout,
                    int32_t* vout, int n, int shift, uint32_t mask, const uint32_t* base,
                    unsigned long long* status, uint32_t epoch, uint32_t* ticket,
                    const unsigned long long* bad, int stream_in, const int32_t* n_dev = nullptr,
-                   const ChunkWalk* cw = nullptr) {
+                   const SortSeg* sg = nullptr) {
 #define SS_SORT_CASE(R) launch_sort<R>(st, kin, vin, kout, vout, n, shift, mask, base, status, epoch, ticket, bad, \
-                                       stream_in, n_dev, cw)
+                                       stream_in, n_dev, sg)
     switch (rb) {
         case 4: SS_SORT_CASE(4); break;
         case 5: SS_SORT_CASE(5); break;
@@ -389,6 +383,19 @@ static int join_side(ss_engine* e);
 // --------------------------------------------------------------------------
 extern "C" const char* ss_version(void) { return "ss_b200 1.0 (sm_100a)"; }
 
+#ifdef SS_SORT_PROF
+// experiment builds only: clock64 cycles per placement-tile phase, summed over CTAs
+extern "C" int ss_debug_sort_prof(unsigned long long* out, int reset) {
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, g_sort_prof, 8 * sizeof(unsigned long long));
+    if (reset) {
+        unsigned long long z[8] = {0};
+        cudaMemcpyToSymbol(g_sort_prof, z, sizeof(z));
+    }
+    return 0;
+}
+#endif
+
 extern "C" long long ss_sub_batch(ss_engine* e) { return e ? (long long)e->S : 0; }
 
 extern "C" long long ss_launch_count(int reset) {
@@ -418,7 +425,7 @@ static int engine_alloc_sort(ss_engine* e, int64_t n) {
     if ((rc = dalloc(e, &e->kbuf2, cap))) return rc;
     if ((rc = dalloc(e, &e->vbuf[0], cap))) return rc;
     if ((rc = dalloc(e, &e->vbuf[1], cap))) return rc;
-    e->status_tiles = cap / kSortTile;
+    e->status_tiles = cap / kSortTile + kMaxBins;   // + one partial tile per bucket (SortSeg mode 2)
     if ((rc = dalloc(e, &e->status, (size_t)e->status_tiles * kMaxBins))) return rc;
     SS_CUDA(e, cudaMemsetAsync(e->status, 0, sizeof(unsigned long long) * e->status_tiles * kMaxBins, e->st));
     e->sort_cap = cap;
@@ -562,6 +569,8 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
         (rc = dalloc(e, &e->touched, 1)) || (rc = dalloc(e, &e->bad, 1)) ||
         (rc = dalloc(e, &e->tickets, (size_t)nsub * 2 + 2)) || (rc = dalloc(e, &e->gkept, G)) || (rc = dalloc(e, &e->n_live, nsub + 1)) ||
         (rc = dalloc(e, &e->chunk_live, nsub)) || (rc = dalloc(e, &e->lc, nsub)) || (rc = dalloc(e, &e->n_lc, 1)) ||
+        (rc = dalloc(e, &e->chunk_h, (size_t)nsub * kMaxBins)) || (rc = dalloc(e, &e->chunk_base, (size_t)nsub * kMaxBins)) ||
+        (rc = dalloc(e, &e->btile, kMaxBins + 1)) ||
         (rc = dalloc(e, &e->bdelta, G)) || (rc = dalloc(e, &e->bmin, G)) || (rc = dalloc(e, &e->bmax, G)) ||
         (rc = dalloc(e, &e->hot_of, G)) || (rc = dalloc(e, &e->hot_g, kHotCache)) || (rc = dalloc(e, &e->n_hot_dev, 1)))
         return rc;
@@ -774,7 +783,8 @@ static int launch_scans(ss_engine* e, const int32_t* row, int n_chunk = 0) {
     dim3 g2(e->nblk, 1);
     ss_note_launch(), k_scan_reduce<<<g2, 1024, 0, e->st>>>(row, (uint32_t)e->G, e->bsum, e->nblk, e->plan, e->dhist, e->bad);
     ss_note_launch(), k_scan_top<<<1, 1024, 0, e->st>>>(e->bsum, e->nblk, e->plan, e->dhist, e->bad, e->n_live,
-                                                        n_chunk ? e->chunk_live : nullptr, n_chunk, e->lc, e->n_lc);
+                                                        n_chunk ? e->chunk_live : nullptr, n_chunk, e->lc, e->n_lc,
+                                                        n_chunk ? e->btile : nullptr);
     ss_note_launch(), k_scan_down<<<g2, 1024, 0, e->st>>>(row, (uint32_t)e->G, e->bsum, e->nblk, e->gstart, e->bad);
     SS_CUDA(e, cudaGetLastError());
     return SS_OK;
@@ -815,18 +825,43 @@ static int launch_place_step(ss_engine* e, const uint32_t* dk, const int32_t* dv
     const uint32_t* base0 = e->dhist;
     const uint32_t* base1 = e->dhist + kMaxBins;
     const uint32_t m0 = (1u << e->plan.bits[0]) - 1u;
+    const int nb0 = 1 << e->plan.bits[0];
+    const int n_chunk = (int)std::max<int64_t>(1, (n + e->S - 1) / e->S);
     int cs = 0;
     while ((int64_t(1) << cs) < e->S) ++cs;
-    ChunkWalk cw{e->gcnt, e->lc, e->n_lc, cs, (uint32_t)e->G};
+    // per-live-chunk bin bases of the first pass
+    // enough CTAs per chunk that every SM has a slice of ~4K groups or more
+    const int slices = (int)std::max<int64_t>(1, std::min<int64_t>((e->G + 4095) / 4096, (2 * kNumSM + n_chunk - 1) / n_chunk));
+    SS_CUDA(e, cudaMemsetAsync(e->chunk_h, 0, (size_t)n_chunk * nb0 * 4, e->st));
+    ss_note_launch(), k_chunk_hist<<<dim3(n_chunk, slices), 1024, nb0 * 4, e->st>>>(e->gcnt, (uint32_t)e->G, e->lc, e->n_lc,
+                                                                                   m0, nb0, e->chunk_h, e->bad);
+    ss_note_launch(), k_chunk_scan<<<(nb0 + 31) / 32, 1024, 0, e->st>>>(e->chunk_h, e->n_lc, nb0, base0,
+                                                                        e->chunk_base, e->bad);
+    SortSeg s1{};
+    s1.mode = 1;
+    s1.live = e->gcnt;
+    s1.lc = e->lc;
+    s1.n_lc = e->n_lc;
+    s1.chunk_shift = cs;
+    s1.G = (uint32_t)e->G;
+    s1.cbase = e->chunk_base;
     if (e->plan.npass == 1) {
         sort_dispatch(e->rb[0], e->st, dk, dv, nullptr, e->vbuf[0], (int)n, 0, m0, base0, e->status, next_epoch(e),
-                      e->tickets, e->bad, 1, e->n_live, &cw);
+                      e->tickets, e->bad, 1, e->n_live, &s1);
     } else {
         const uint32_t m1 = (1u << e->plan.bits[1]) - 1u;
         sort_dispatch(e->rb[0], e->st, dk, dv, e->kbuf, e->vbuf[1], (int)n, e->plan.shift[0], m0, base0, e->status,
-                      next_epoch(e), e->tickets, e->bad, 1, e->n_live, &cw);
+                      next_epoch(e), e->tickets, e->bad, 1, e->n_live, &s1);
+        SortSeg s2{};
+        s2.mode = 2;
+        s2.G = (uint32_t)e->G;
+        s2.btile = e->btile;
+        s2.bpos = base0;
+        s2.nb = nb0;
+        s2.b0 = e->plan.bits[0];
+        s2.gstart = e->gstart;
         sort_dispatch(e->rb[1], e->st, e->kbuf, e->vbuf[1], nullptr, e->vbuf[0], (int)n, e->plan.shift[1], m1, base1,
-                      e->status, next_epoch(e), e->tickets + 1, e->bad, 0, e->n_live, nullptr);
+                      e->status, next_epoch(e), e->tickets + 1, e->bad, 0, e->n_live, &s2);
     }
     SS_CUDA(e, cudaGetLastError());
     return SS_OK;
@@ -1652,7 +1687,7 @@ extern "C" int ss_route(ss_engine* e, const uint32_t* groups, const int32_t* att
         e->epoch = 1;
     }
     const int tiles = (int)((n + kSortTile - 1) / kSortTile);
-    ss_note_launch(), k_sort_pass<4, true><<<tiles, kSortThreads, SortSmem<4>::bytes, e->st>>>(
+    ss_note_launch(), k_sort_pass<4, true><<<std::min(tiles, 2 * kNumSM), kSortThreads, SortSmem<4>::bytes, e->st>>>(
         dk, dv, ko, vo, (int)n, 0, 15u, e->route_base, e->status, e->epoch, e->tickets, e->bad, 0, e->owner);
     SS_CUDA(e, cudaGetLastError());
     if (!dev_out) {

@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(1024)
 k_scan_top(int32_t* __restrict__ bsum, int nblk, DigitPlan plan, uint32_t* __restrict__ dhist,
            const unsigned long long* __restrict__ bad, int32_t* __restrict__ n_live,
            int32_t* __restrict__ chunk_live = nullptr, int n_chunk = 0, int32_t* __restrict__ lc = nullptr,
-           int32_t* __restrict__ n_lc = nullptr) {
+           int32_t* __restrict__ n_lc = nullptr, int32_t* __restrict__ btile = nullptr) {
     __shared__ int32_t sh_red[33];
     __shared__ uint32_t sh_ured[33];
     if (*bad != (unsigned long long)kNoBad) return;
@@ -306,6 +306,17 @@ k_scan_top(int32_t* __restrict__ bsum, int nblk, DigitPlan plan, uint32_t* __res
         uint32_t ex = block_excl_scan(a + b, sh_ured, &tot);
         h[2 * threadIdx.x] = ex;
         h[2 * threadIdx.x + 1] = ex + a;
+        if (d == 0 && btile && plan.npass == 2) {
+            // tiles of the second pass: each first-pass digit bucket is cut
+            // into 4096-tuple tiles of its own (SortSeg mode 2)
+            const int32_t ta = (int32_t)((a + kSortTile - 1) / kSortTile);
+            const int32_t tb = (int32_t)((b + kSortTile - 1) / kSortTile);
+            int32_t ttot;
+            const int32_t tex = block_excl_scan(ta + tb, sh_red, &ttot);
+            btile[2 * threadIdx.x] = tex;
+            btile[2 * threadIdx.x + 1] = tex + ta;
+            if (threadIdx.x == 0) btile[kMaxBins] = ttot;
+        }
     }
     if (chunk_live && s == 0) {
         // n_chunk <= 4 * 1024, 4 consecutive chunks per thread
@@ -366,11 +377,89 @@ k_scan_down(const int32_t* __restrict__ gcnt, uint32_t G, const int32_t* __restr
 // runs per digit.  Tile ids come from an atomic ticket so a tile only ever
 // waits on tiles that are already resident.
 // --------------------------------------------------------------------------
+// Where a placement tile's bin bases come from.  Long look-back chains
+// (every in-flight tile walking back to the last finished one) are avoided
+// by cutting the tile sequence into segments whose bin bases are known in
+// advance: the first tile of a segment publishes its inclusive prefix at
+// once, later tiles look back only inside their segment.
+//   mode 0: one segment (bin_base), tiles = the input in 4096-tuple steps
+//   mode 1: first pass of the fused step -- segments = live count chunks,
+//           bases from the per-chunk digit histograms (k_chunk_hist/scan)
+//   mode 2: second pass -- segments = the first pass's digit buckets; the
+//           base of bin d in bucket b is the run start of group (d<<b0)|b
+struct SortSeg {
+    int mode;
+    const int32_t* live;        // mode 1: kept counts [n_chunk][G]
+    const int32_t* lc;          // mode 1: ordered live chunks
+    const int32_t* n_lc;
+    int chunk_shift;
+    uint32_t G;
+    const uint32_t* cbase;      // mode 1: [n_lc][BINS]
+    const int32_t* btile;       // mode 2: tile prefix over buckets [nb + 1]
+    const uint32_t* bpos;       // mode 2: bucket starts (previous pass's exclusive bases)
+    int nb;
+    int b0;
+    const int32_t* gstart;      // mode 2: run start of every group
+};
+
+// per-live-chunk histogram of the first digit over the kept counts.
+// grid = (n_chunk, slices): each CTA bins a slice of the chunk's groups in
+// shared memory and adds it to H0 (zeroed before the launch)
+__global__ void __launch_bounds__(1024)
+k_chunk_hist(const int32_t* __restrict__ gcnt, uint32_t G, const int32_t* __restrict__ lc,
+             const int32_t* __restrict__ n_lc, uint32_t m0, int nb, uint32_t* __restrict__ H0,
+             const unsigned long long* __restrict__ bad) {
+    extern __shared__ uint32_t sh_h[];
+    if (*bad != (unsigned long long)kNoBad) return;
+    const int i = blockIdx.x;
+    if (i >= *n_lc) return;
+    const int64_t c = lc[i];
+    for (int d = threadIdx.x; d < nb; d += blockDim.x) sh_h[d] = 0;
+    __syncthreads();
+    const int32_t* row = gcnt + c * (int64_t)G;
+    const uint32_t per = (G + gridDim.y - 1) / gridDim.y;
+    const uint32_t g0 = blockIdx.y * per, g1 = min(G, g0 + per);
+    for (uint32_t g = g0 + threadIdx.x; g < g1; g += blockDim.x) {
+        const int32_t v = row[g];
+        if (v) atomicAdd(&sh_h[g & m0], (uint32_t)v);
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < nb; d += blockDim.x)
+        if (sh_h[d]) atomicAdd(&H0[(int64_t)i * nb + d], sh_h[d]);
+}
+
+// per digit: exclusive scan of the live chunks' histograms + the bin base
+// -> cbase[i][d].  A warp per digit, lanes over chunks.
+__global__ void __launch_bounds__(1024)
+k_chunk_scan(const uint32_t* __restrict__ H0, const int32_t* __restrict__ n_lc, int nb,
+             const uint32_t* __restrict__ bin_base, uint32_t* __restrict__ cbase,
+             const unsigned long long* __restrict__ bad) {
+    if (*bad != (unsigned long long)kNoBad) return;
+    const int d = blockIdx.x * (blockDim.x >> 5) + warp_id();
+    if (d >= nb) return;
+    const int nl = *n_lc;
+    const unsigned lane = lane_id();
+    uint32_t carry = bin_base[d];
+    for (int i0 = 0; i0 < nl; i0 += 32) {
+        const int i = i0 + (int)lane;
+        const uint32_t v = (i < nl) ? H0[(int64_t)i * nb + d] : 0u;
+        const uint32_t incl = warp_incl_scan(v);
+        if (i < nl) cbase[(int64_t)i * nb + d] = carry + incl - v;
+        carry += __shfl_sync(SS_FULL, incl, 31);
+    }
+}
+
+#ifdef SS_SORT_PROF
+__device__ unsigned long long g_sort_prof[8];
+#endif
+
 template <int RB>
 struct SortSmem {
     static constexpr int BINS = 1 << RB;
     static constexpr int NW = kSortThreads / 32;
-    static constexpr size_t bytes = (size_t)NW * BINS * 2 + (size_t)BINS * 8 + (size_t)kSortTile * 8 + 16;
+    // two input stages of keys + values (the current one doubles as the
+    // tile-local sort buffer), per-warp digit histograms, bin starts/bases
+    static constexpr size_t bytes = (size_t)2 * kSortTile * 8 + (size_t)NW * BINS * 2 + (size_t)BINS * 8 + 16;
 };
 
 template <int RB, bool MAPPED = false>
@@ -380,59 +469,126 @@ k_sort_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
             const uint32_t* __restrict__ bin_base, unsigned long long* __restrict__ status,
             uint32_t epoch, uint32_t* __restrict__ ticket, const unsigned long long* __restrict__ bad,
             int stream_in, const int32_t* __restrict__ dmap = nullptr,
-            const int32_t* __restrict__ live = nullptr, const int32_t* __restrict__ n_dev = nullptr,
-            const int32_t* __restrict__ lc = nullptr, const int32_t* __restrict__ n_lc = nullptr,
-            int chunk_shift = 0, uint32_t G = 0) {
+            const int32_t* __restrict__ n_dev = nullptr, SortSeg seg = SortSeg{}) {
     constexpr int BINS = 1 << RB;
     constexpr int NW = kSortThreads / 32;
     constexpr int BPT = (BINS + kSortThreads - 1) / kSortThreads;   // bins owned per thread
     extern __shared__ __align__(16) unsigned char sort_sm[];
-    uint32_t* skey = (uint32_t*)sort_sm;                     // [TILE]
-    int32_t* sval = (int32_t*)(skey + kSortTile);            // [TILE]
-    uint32_t* tbin = (uint32_t*)(sval + kSortTile);          // [BINS] tile-local bin start
+    uint32_t* in_k = (uint32_t*)sort_sm;                     // [2][TILE] staged keys
+    int32_t* in_v = (int32_t*)(in_k + 2 * kSortTile);        // [2][TILE] staged values
+    uint32_t* tbin = (uint32_t*)(in_v + 2 * kSortTile);      // [BINS] tile-local bin start
     uint32_t* gbase = tbin + BINS;                           // [BINS] global pos of local pos 0
     uint16_t* whist = (uint16_t*)(gbase + BINS);             // [NW][BINS]
-    __shared__ uint32_t sh_tile;
     __shared__ uint32_t sh_red[33];
+    __shared__ int64_t sh_t0[2];
+    __shared__ int sh_tn[2], sh_k[2], sh_seg[2];
+    __shared__ uint32_t sh_tile[2];
     if (*bad != (unsigned long long)kNoBad) return;
-    if (n_dev && *n_dev == 0) return;            // nothing live in this sub-batch
-    if (threadIdx.x == 0) sh_tile = atomicAdd(ticket, 1u);
+    if (n_dev && *n_dev == 0) return;            // nothing kept in this batch
+    if (n_dev && seg.mode != 1) n = *n_dev;      // consumes a compacted (kept-only) input
+    const unsigned w = warp_id(), lane = lane_id();
+    const int wbase = (int)w * 32 * kSortItems;
+    // claim the next tile (thread 0): ticket -> input range and segment
+    auto claim = [&](int slot) {
+        const uint32_t t = atomicAdd(ticket, 1u);
+        int64_t t0 = -1;
+        int tn = 0, k = 0, sg = 0;
+        if (seg.mode == 1) {
+            // ticket t is tile (t mod tpc) of the (t / tpc)-th live chunk
+            const int tpc_shift = seg.chunk_shift - 12;          // kSortTile = 2^12
+            const int ci = (int)(t >> tpc_shift);
+            if (ci < *seg.n_lc) {
+                k = (int)(t & ((1u << tpc_shift) - 1u));
+                t0 = ((int64_t)seg.lc[ci] << seg.chunk_shift) + ((int64_t)k << 12);
+                sg = ci;
+                if (t0 >= n) t0 = -1;                             // past a short last chunk
+            }
+        } else if (seg.mode == 2) {
+            if ((int)t < seg.btile[seg.nb]) {
+                int lo2 = 0, hi2 = seg.nb - 1;                     // last bucket with btile <= t
+                while (lo2 < hi2) {
+                    const int mid = (lo2 + hi2 + 1) >> 1;
+                    if (seg.btile[mid] <= (int)t) lo2 = mid; else hi2 = mid - 1;
+                }
+                sg = lo2;
+                k = (int)t - seg.btile[lo2];
+                const int64_t bend = (lo2 + 1 < seg.nb) ? (int64_t)seg.bpos[lo2 + 1] : (int64_t)n;
+                t0 = (int64_t)seg.bpos[lo2] + ((int64_t)k << 12);
+                tn = (int)min64(kSortTile, bend - t0);
+            }
+        } else {
+            k = (int)t;
+            t0 = (int64_t)t * kSortTile;
+            if (t0 >= n) t0 = -1;
+        }
+        if (seg.mode != 2 && t0 >= 0) tn = (int)min64(kSortTile, (int64_t)n - t0);
+        sh_tile[slot] = t;
+        sh_t0[slot] = t0;
+        sh_tn[slot] = tn;
+        sh_k[slot] = k;
+        sh_seg[slot] = sg;
+    };
+    // stage a tile's keys and values into shared memory with cp.async: the
+    // next tile's loads are in flight while the current tile is ranked
+    auto stage = [&](int slot) {
+        const int64_t t0 = sh_t0[slot];
+        const int tn = sh_tn[slot];
+        if (t0 >= 0) {
+            uint32_t* dk = in_k + slot * kSortTile;
+            int32_t* dv = in_v + slot * kSortTile;
+#pragma unroll
+            for (int j = 0; j < kSortItems; ++j) {
+                const int li = wbase + j * 32 + (int)lane;
+                if (li < tn) {
+                    cp_async4(dk + li, kin + t0 + li);
+                    cp_async4(dv + li, vin + t0 + li);
+                }
+            }
+        }
+        cp_async_commit();
+    };
+    const int32_t* live = nullptr;
+    // persistent CTAs: tiles are taken by atomic ticket in arrival order, so
+    // a tile only ever looks back at tiles that are already being processed
+    // (the prefetched ticket is always newer than the one being processed)
+    if (threadIdx.x == 0) claim(0);
+    __syncthreads();
+    stage(0);
+    int cur = 0;
+    while (true) {
+#ifdef SS_SORT_PROF
+    long long _pt = clock64();
+#define SS_PT(i) do { if (threadIdx.x == 0) { const long long _n = clock64(); atomicAdd(&g_sort_prof[i], (unsigned long long)(_n - _pt)); _pt = _n; } } while (0)
+#else
+#define SS_PT(i) do {} while (0)
+#endif
+    const uint32_t tile = sh_tile[cur];
+    const int64_t tile0 = sh_t0[cur];            // input offset of this tile
+    if (tile0 < 0) break;                        // beyond the tiles: nobody looks back at it
+    const int tile_n = sh_tn[cur];
+    const int seg_k = sh_k[cur];                 // index of the tile inside its segment
+    const int seg_id = sh_seg[cur];
+    if (threadIdx.x == 0) claim(cur ^ 1);
     for (int i = threadIdx.x; i < NW * BINS / 2; i += kSortThreads) ((uint32_t*)whist)[i] = 0;
     __syncthreads();
-    const uint32_t tile = sh_tile;
-    const unsigned w = warp_id(), lane = lane_id();
-    if (n_dev && !live) n = *n_dev;              // consumes a compacted (live-only) input
-    int64_t tile0 = (int64_t)tile * kSortTile;   // input offset of this tile
-    int tile_n;
-    if (lc) {
-        // live-chunk walk: tiles of chunks with no kept tuple do not exist;
-        // ticket t is tile (t mod tpc) of the (t / tpc)-th live chunk
-        const int tpc_shift = chunk_shift - 12;  // kSortTile = 2^12
-        const int ci = (int)(tile >> tpc_shift);
-        if (ci >= *n_lc) return;                 // beyond the kept tiles: nobody looks back at it
-        const int64_t c = lc[ci];
-        tile0 = (c << chunk_shift) + ((int64_t)(tile & ((1u << tpc_shift) - 1u)) << 12);
-        if (tile0 >= n) return;                  // past the end of a short last chunk: never waited on
-        tile_n = (int)min64(kSortTile, (int64_t)n - tile0);
-        live += c * (int64_t)G;                  // the chunk's kept counts
-    } else {
-        if (tile0 >= n) return;                  // beyond the input: nobody looks back at it
-        tile_n = (int)min64(kSortTile, (int64_t)n - tile0);
-    }
-    const int wbase = (int)w * 32 * kSortItems;
+    SS_PT(0);
+    stage(cur ^ 1);
+    cp_async_wait_1();                           // this thread's copies of the current tile have landed
+    uint32_t* skey = in_k + cur * kSortTile;     // staged input, then the tile-local sort buffer
+    int32_t* sval = in_v + cur * kSortTile;
+    if (seg.mode == 1) live = seg.live + (int64_t)seg.lc[seg_id] * seg.G;   // the chunk's kept counts
     uint16_t* myh = whist + w * BINS;
 
     uint32_t key[kSortItems];
     int32_t val[kSortItems];
     uint32_t rank[kSortItems];
     uint32_t ok = 0;                             // bit j: item j is valid (and live)
-    // three load phases (keys, live flags, values), each with all kSortItems
-    // loads in flight, instead of one dependent key->flag->value chain per item
+    // keys and values come from the staged tile; the kept-count lookups are
+    // all in flight together
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
         const int li = wbase + j * 32 + (int)lane;
-        key[j] = 0xffffffffu;
-        if (li < tile_n) key[j] = stream_in ? ld_stream_u32(kin + tile0 + li) : kin[tile0 + li];
+        key[j] = (li < tile_n) ? skey[li] : 0xffffffffu;
     }
     int32_t lv[kSortItems];
 #pragma unroll
@@ -446,11 +602,12 @@ k_sort_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
         const int li = wbase + j * 32 + (int)lane;
         val[j] = 0;
         if (lv[j] > 0) {
-            val[j] = stream_in ? (int32_t)ld_stream_u32(vin + tile0 + li) : vin[tile0 + li];
+            val[j] = sval[li];
             ok |= 1u << j;
         }
     }
     const unsigned lt = lanemask_lt();
+    SS_PT(1);
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
         const bool valid = (ok >> j) & 1u;
@@ -466,6 +623,7 @@ k_sort_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
         __syncwarp();
     }
     __syncthreads();
+    SS_PT(2);
     // per owned bin: exclusive prefix across warps and the tile total
     uint32_t tot[BPT];
     uint32_t tsum = 0;
@@ -483,7 +641,7 @@ k_sort_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
             }
             tot[q] = run;
             st_relaxed_u64(&status[(int64_t)tile * BINS + b],
-                           lb_pack(epoch, tile == 0 ? kFlagInc : kFlagAgg, run));
+                           lb_pack(epoch, seg_k == 0 ? kFlagInc : kFlagAgg, run));
         }
         tsum += tot[q];
     }
@@ -497,12 +655,13 @@ k_sort_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
         lex += tot[q];
     }
     // look-back across tiles
+    SS_PT(3);
 #pragma unroll
     for (int q = 0; q < BPT; ++q) {
         const int b = threadIdx.x * BPT + q;
         if (b < BINS) {
             uint32_t excl = 0;
-            if (tile > 0) {
+            if (seg_k > 0) {
                 // windowed look-back: the status words of up to kLB
                 // predecessors are loaded together, summed from the nearest
                 // back to the first inclusive prefix; an unpublished word
@@ -531,10 +690,17 @@ k_sort_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
                 }
                 st_relaxed_u64(&status[(int64_t)tile * BINS + b], lb_pack(epoch, kFlagInc, excl + tot[q]));
             }
-            gbase[b] = bin_base[b] + excl - tbin[b];
+            uint32_t base;
+            if (seg.mode == 1) base = seg.cbase[(int64_t)seg_id * BINS + b];
+            else if (seg.mode == 2) {
+                const uint32_t g = ((uint32_t)b << seg.b0) | (uint32_t)seg_id;
+                base = (g < seg.G) ? (uint32_t)seg.gstart[g] : 0u;
+            } else base = bin_base[b];
+            gbase[b] = base + excl - tbin[b];
         }
     }
     __syncthreads();
+    SS_PT(4);
     // tile-local sort into shared memory
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
@@ -560,6 +726,11 @@ k_sort_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
         vout[pos] = sval[i];
         if (kout) kout[pos] = k;
     }
+    __syncthreads();                             // smem reused by the next tile
+    SS_PT(5);
+    cur ^= 1;
+    }
+    cp_async_wait_0();
 }
 
 // histogram of destination owners for the multi-GPU route (<= 16 owners)
