@@ -383,6 +383,17 @@ static int join_side(ss_engine* e);
 // --------------------------------------------------------------------------
 extern "C" const char* ss_version(void) { return "ss_b200 1.0 (sm_100a)"; }
 
+#ifdef SS_K4_PROF
+extern "C" int ss_debug_k4_prof(unsigned long long* out, int reset) {
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, g_k4_prof, 8 * sizeof(unsigned long long));
+    if (reset) {
+        unsigned long long z[8] = {0};
+        cudaMemcpyToSymbol(g_k4_prof, z, sizeof(z));
+    }
+    return 0;
+}
+#endif
 #ifdef SS_SORT_PROF
 // experiment builds only: clock64 cycles per placement-tile phase, summed over CTAs
 extern "C" int ss_debug_sort_prof(unsigned long long* out, int reset) {

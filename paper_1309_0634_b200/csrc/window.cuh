@@ -82,8 +82,13 @@ __device__ __forceinline__ void add_delta(uint32_t* lo, uint32_t* hi, long long 
     atomicAdd(hi, (uint32_t)(x >> 32) + carry);
 }
 
-constexpr int kUnit = 32 * kILP;            // values of one warp unit (long members)
+constexpr int kLILP = 8;                    // values in flight per lane for long members
+constexpr int kUnit = 32 * kLILP;           // values of one warp unit (long members)
 constexpr int kCtaPerPart = 4;              // CTAs sharing one partition's work
+
+#ifdef SS_K4_PROF
+__device__ unsigned long long g_k4_prof[8];
+#endif
 
 __global__ void __launch_bounds__(kIngestThreads, 2)
 k_ingest(IngestArgs a) {
@@ -106,6 +111,12 @@ k_ingest(IngestArgs a) {
     if (a.n_live && *a.n_live == 0) return;      // every tuple of the sub-batch was dropped
     uint64_t t0 = 0;
     if (threadIdx.x == 0) t0 = globaltimer();
+#ifdef SS_K4_PROF
+    long long _pt = clock64();
+#define SS_PT4(i) do { if (threadIdx.x == 0) { const long long _n = clock64(); atomicAdd(&g_k4_prof[i], (unsigned long long)(_n - _pt)); _pt = _n; } } while (0)
+#else
+#define SS_PT4(i) do {} while (0)
+#endif
     // partition p is processed by kCtaPerPart CTAs; its members (and split
     // shares) are dealt to them round-robin
     const int p = blockIdx.x / kCtaPerPart;
@@ -129,6 +140,7 @@ k_ingest(IngestArgs a) {
     const int cstride = shared_items ? kCtaPerPart : 1;   // interleave factor
     const int csub = shared_items ? sub : 0;
     for (int c0 = 0; c0 < my_items; c0 += kMemberChunk) {
+        SS_PT4(0);
         const int m = min(kMemberChunk, my_items - c0);
         // phase A: stage the items thread-strided (item i on thread i mod
         // 512), so a partition with few members costs one dependent load
@@ -179,6 +191,7 @@ k_ingest(IngestArgs a) {
             m_w[i] = w;
         }
         __syncthreads();
+        SS_PT4(1);
         // phase B: thread-contiguous scans of short values and long units
         int32_t wshort[kMPT], wunits[kMPT];
         int32_t ssum = 0, usum = 0;
@@ -210,6 +223,7 @@ k_ingest(IngestArgs a) {
         }
         __syncthreads();
 
+        SS_PT4(2);
         // ---- long members: one warp per unit of kUnit contiguous values ----
         for (int u = csub * nw + warp_id(); u < u_total; u += cstride * nw) {
             int mi = 0;                                 // last member with m_uscan[mi] <= u
@@ -222,35 +236,35 @@ k_ingest(IngestArgs a) {
             const int w = m_w[mi];
             const int start = m_start[mi], q0 = m_q0[mi], s0 = m_s0[mi], f0 = m_f0[mi];
             const int64_t offg = m_off[mi];
-            int32_t v[kILP], old[kILP];
-            int64_t cell[kILP];
+            // ring cells are recomputed per phase instead of kept in 64-bit
+            // registers: the loads of a unit stay in flight together
+            // instead of being serialised by register spills
+            const int32_t* vsrc = a.vals + start;
+            int32_t* rg = a.ring + offg;
+            int32_t v[kLILP], old[kLILP];
 #pragma unroll
-            for (int k = 0; k < kILP; ++k) {
+            for (int k = 0; k < kLILP; ++k) {
                 const int r = r0 + k * 32 + (int)lane;
-                if (r < w) {
-                    v[k] = a.vals[start + r];
-                    int sl = s0 + r;
-                    if (sl >= W) sl -= W;
-                    cell[k] = offg + sl;
-                }
+                v[k] = (r < w) ? vsrc[r] : 0;
             }
 #pragma unroll
-            for (int k = 0; k < kILP; ++k) {
+            for (int k = 0; k < kLILP; ++k) {
                 const int r = r0 + k * 32 + (int)lane;
-                old[k] = 0;
-                if (r < w) {
-                    int qq = q0 + r;
-                    if (qq >= W) qq -= W;
-                    if (qq < f0) old[k] = a.ring[cell[k]];
-                }
+                int qq = q0 + r;
+                if (qq >= W) qq -= W;
+                int sl = s0 + r;
+                if (sl >= W) sl -= W;
+                old[k] = (r < w && qq < f0) ? rg[sl] : 0;
             }
             long long d = 0;
             int32_t mnv = 0x7fffffff, mxv = (int32_t)0x80000000;
 #pragma unroll
-            for (int k = 0; k < kILP; ++k) {
+            for (int k = 0; k < kLILP; ++k) {
                 const int r = r0 + k * 32 + (int)lane;
                 if (r < w) {
-                    a.ring[cell[k]] = v[k];
+                    int sl = s0 + r;
+                    if (sl >= W) sl -= W;
+                    rg[sl] = v[k];
                     d += (long long)v[k] - (long long)old[k];
                     mnv = min(mnv, v[k]);
                     mxv = max(mxv, v[k]);
@@ -271,14 +285,15 @@ k_ingest(IngestArgs a) {
         }
 
         // ---- short members (< 32 values): kILP packed values per thread ----
+        SS_PT4(3);
         for (int base = csub * kIngestThreads * kILP; base < s_total; base += cstride * kIngestThreads * kILP) {
-            int mi[kILP];
+            int mi[kILP], rr[kILP];
             int32_t v[kILP], old[kILP];
-            int64_t cell[kILP];
 #pragma unroll
             for (int u = 0; u < kILP; ++u) {
                 const int t = base + u * kIngestThreads + threadIdx.x;
                 mi[u] = -1;
+                rr[u] = 0;
                 if (t < s_total) {
                     int l = 0;                 // last member with m_scan[l] <= t
 #pragma unroll
@@ -287,32 +302,29 @@ k_ingest(IngestArgs a) {
                         if (c < m && m_scan[c] <= t) l = c;
                     }
                     mi[u] = l;
+                    rr[u] = t - m_scan[l];
                 }
             }
 #pragma unroll
-            for (int u = 0; u < kILP; ++u) {
-                if (mi[u] >= 0) {
-                    const int t = base + u * kIngestThreads + threadIdx.x;
-                    const int rr = t - m_scan[mi[u]];
-                    v[u] = a.vals[m_start[mi[u]] + rr];
-                    int sl = m_s0[mi[u]] + rr;
-                    if (sl >= W) sl -= W;
-                    cell[u] = m_off[mi[u]] + sl;
-                }
-            }
+            for (int u = 0; u < kILP; ++u) v[u] = (mi[u] >= 0) ? a.vals[m_start[mi[u] < 0 ? 0 : mi[u]] + rr[u]] : 0;
 #pragma unroll
             for (int u = 0; u < kILP; ++u) {
                 old[u] = 0;
                 if (mi[u] >= 0) {
-                    const int t = base + u * kIngestThreads + threadIdx.x;
-                    int q = m_q0[mi[u]] + (t - m_scan[mi[u]]);
+                    int q = m_q0[mi[u]] + rr[u];
                     if (q >= W) q -= W;
-                    if (q < m_f0[mi[u]]) old[u] = a.ring[cell[u]];
+                    int sl = m_s0[mi[u]] + rr[u];
+                    if (sl >= W) sl -= W;
+                    if (q < m_f0[mi[u]]) old[u] = a.ring[m_off[mi[u]] + sl];
                 }
             }
 #pragma unroll
             for (int u = 0; u < kILP; ++u)
-                if (mi[u] >= 0) a.ring[cell[u]] = v[u];
+                if (mi[u] >= 0) {
+                    int sl = m_s0[mi[u]] + rr[u];
+                    if (sl >= W) sl -= W;
+                    a.ring[m_off[mi[u]] + sl] = v[u];
+                }
 #pragma unroll
             for (int u = 0; u < kILP; ++u) {
                 const bool valid = mi[u] >= 0;
@@ -334,6 +346,7 @@ k_ingest(IngestArgs a) {
             }
         }
         __syncthreads();
+        SS_PT4(4);
 
         // ---- fold into the per-group batch accumulators --------------------
         for (int i = threadIdx.x; i < m; i += kIngestThreads) {
@@ -350,6 +363,7 @@ k_ingest(IngestArgs a) {
             }
         }
         __syncthreads();
+        SS_PT4(5);
     }
     work_total = warp_sum(work_total);
     if (lane == 0 && a.part_work && work_total) atomicAdd(&a.part_work[p], work_total);

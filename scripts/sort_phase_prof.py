@@ -18,15 +18,17 @@ eng = StreamEngine(G, W, n_partitions=148, aggregates=aggs, device=0, max_batch=
 bal = eng.balancer_struct(policy, thread_threshold=max(1, B // 1480), pot=0.5, split=split)
 bs = bench.make_batches(kind, s, G, B, 2, dev, 1)
 lib = L.load()
-lib.ss_debug_sort_prof.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
+fn = os.environ.get("SS_PROF_FN", "ss_debug_sort_prof")
+prof = getattr(lib, fn)
+prof.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
 for i in range(4):
     eng.step(*bs[i % 2], bal)
 out = (C.c_ulonglong * 8)()
-lib.ss_debug_sort_prof(out, 1)
+prof(out, 1)
 for i in range(6):
     eng.step(*bs[i % 2], bal)
-lib.ss_debug_sort_prof(out, 1)
-names = ["claim+zero", "stage+loads", "rank", "bins+publish+scan", "lookback", "scatter+write"]
+prof(out, 1)
+names = (["claim+zero", "stage+loads", "rank", "bins+publish+scan", "lookback", "scatter+write"] if fn == "ss_debug_sort_prof" else ["prologue", "stage A", "scan B", "long units", "short units", "fold"])
 tot = sum(out[i] for i in range(6))
 for i, n in enumerate(names):
     print(f"{n:20s} {out[i] / 6 / 1e6:9.2f} Mcycles/step (summed over CTAs) {100 * out[i] / max(1, tot):5.1f}%")
