@@ -96,7 +96,8 @@ struct ss_engine {
     int32_t *gcnt = nullptr, *gstart = nullptr, *gcount = nullptr, *bsum = nullptr;
     int32_t* gkept = nullptr;              // kept (possibly stored) tuples of each group in the batch
     int32_t* n_live = nullptr;             // kept tuples of the batch (device)
-    int32_t *chunk_live = nullptr, *lc = nullptr, *n_lc = nullptr;   // live-chunk flags / ordered list
+    uint32_t* chunk_live = nullptr;        // live-chunk bitmap
+    int32_t *lc = nullptr, *n_lc = nullptr;   // ordered live-chunk list
     uint32_t *chunk_h = nullptr, *chunk_base = nullptr;   // first-pass digit histograms / bases per live chunk
     int32_t* btile = nullptr;              // second-pass tile prefix over first-pass buckets
     long long* bdelta = nullptr;           // per-group batch delta
@@ -663,6 +664,7 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
     memset(e->h_rep, 0, sizeof(DevReport));
     e->h_rep->bad = (unsigned long long)kNoBad;
     SS_CUDA(e, cudaFuncSetAttribute(k_count<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    SS_CUDA(e, cudaFuncSetAttribute(k_count_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     SS_CUDA(e, cudaFuncSetAttribute(k_sort_pass<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SortSmem<4>::bytes));
     SS_CUDA(e, cudaFuncSetAttribute(k_sort_pass<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SortSmem<5>::bytes));
     SS_CUDA(e, cudaFuncSetAttribute(k_sort_pass<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SortSmem<6>::bytes));
@@ -779,8 +781,8 @@ static int launch_stats(ss_engine* e, int n_chunk, bool step = false) {
     SS_CUDA(e, cudaMemsetAsync(e->touched, 0, 8, e->st));
     // many chunks per group: a warp per group (lanes over chunks)
     auto kern = n_chunk >= 16 ? k_batch_stats<true> : k_batch_stats<false>;
-    const unsigned grid = n_chunk >= 16 ? (unsigned)std::min<int64_t>((e->G + 31) / 32, 8 * kNumSM) : 2 * kNumSM;
-    ss_note_launch(), kern<<<grid, 1024, e->P * 4, e->st>>>(
+    const unsigned grid = n_chunk >= 16 ? (unsigned)std::min<int64_t>((e->G + 7) / 8, 32 * kNumSM) : 2 * kNumSM;
+    ss_note_launch(), kern<<<grid, n_chunk >= 16 ? 256 : 1024, e->P * 4, e->st>>>(
         e->gcnt, n_chunk, (uint32_t)e->G, e->pmap, e->P, e->gcount, step ? e->gkept : nullptr,
         step ? e->chunk_live : nullptr, e->tpt, e->touched, e->bad, e->fill, e->W, e->alg_bytes);
     SS_CUDA(e, cudaGetLastError());
@@ -790,6 +792,13 @@ static int launch_stats(ss_engine* e, int n_chunk, bool step = false) {
 // G-sized scan of one count row -> run starts gstart[g] and the digit bases
 // of every placement pass; with n_chunk > 0 also the live-chunk list
 static int launch_scans(ss_engine* e, const int32_t* row, int n_chunk = 0) {
+    if (e->G <= kScanSmallG) {
+        ss_note_launch(), k_scan_small<<<1, 1024, 0, e->st>>>(row, (uint32_t)e->G, e->plan, e->dhist, e->gstart, e->bad,
+                                                              e->n_live, n_chunk ? e->chunk_live : nullptr, n_chunk,
+                                                              e->lc, e->n_lc, n_chunk ? e->btile : nullptr);
+        SS_CUDA(e, cudaGetLastError());
+        return SS_OK;
+    }
     SS_CUDA(e, cudaMemsetAsync(e->dhist, 0, (size_t)2 * kMaxBins * 4, e->st));
     dim3 g2(e->nblk, 1);
     ss_note_launch(), k_scan_reduce<<<g2, 1024, 0, e->st>>>(row, (uint32_t)e->G, e->bsum, e->nblk, e->plan, e->dhist, e->bad);
@@ -943,7 +952,14 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
     if (e->minmax) SS_CUDA(e, cudaMemsetAsync(e->n_rescan, 0, 4, e->st));
     {
         ProfScope ps(e, SS_K_COUNT, e->st);
-        if ((rc = launch_count(e, dk, n, e->S, e->G > 16384))) return rc;
+        if (e->G <= 16384) {
+            // one CTA per count chunk, rows written whole (no zeroing needed)
+            if (n) {
+                ss_note_launch(), k_count_rows<<<n_chunk, 512, e->G * 4, e->st>>>(dk, n, (uint32_t)e->G, e->S, e->gcnt,
+                                                                                 e->bad, ((uintptr_t)dk % 16) == 0);
+                SS_CUDA(e, cudaGetLastError());
+            }
+        } else if ((rc = launch_count(e, dk, n, e->S, true))) return rc;
     }
     if (e->side_pending) {
         SS_CUDA(e, cudaStreamWaitEvent(e->st, e->ev_apply, 0));
@@ -1033,7 +1049,9 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
     {
         ProfScope ps(e, SS_K_INGEST, e->st);
         IngestArgs a = ingest_args(e, use_plan);
-        ss_note_launch(), k_ingest<<<e->P * kCtaPerPart, kIngestThreads, kIngestSmem, e->st>>>(a);
+        // one wave: the co-resident CTAs (2 per SM) are shared out over the partitions
+        a.cpp = std::max(1, (2 * kNumSM) / e->P);
+        ss_note_launch(), k_ingest<<<e->P * a.cpp, kIngestThreads, kIngestSmem, e->st>>>(a);
         SS_CUDA(e, cudaGetLastError());
     }
     if (run_side) SS_CUDA(e, cudaEventRecord(e->ev_k4, e->st));

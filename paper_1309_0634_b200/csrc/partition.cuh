@@ -92,6 +92,48 @@ k_count(const uint32_t* __restrict__ groups, int64_t n, uint32_t G, int64_t S, i
     }
 }
 
+// K2 for the fused step with G <= 16K: one CTA per count chunk of the batch
+// (S = 2^k tuples) builds the chunk's whole histogram in shared memory and
+// writes its row of gcnt with plain stores (no zeroing, no global atomics).
+// Each thread keeps four 128-bit loads in flight; a warp's load instruction
+// covers 512 contiguous bytes.
+__global__ void __launch_bounds__(512)
+k_count_rows(const uint32_t* __restrict__ groups, int64_t n, uint32_t G, int64_t S, int32_t* __restrict__ gcnt,
+             unsigned long long* __restrict__ bad, int vec_ok) {
+    extern __shared__ int32_t sh_hist[];
+    const int64_t c0 = (int64_t)blockIdx.x * S;
+    const int64_t c1 = min(n, c0 + S);
+    for (int i = threadIdx.x; i < (int)G; i += blockDim.x) sh_hist[i] = 0;
+    __syncthreads();
+    constexpr int U = 4;                         // 128-bit loads in flight per thread
+    const int64_t step = (int64_t)U * 4 * blockDim.x;
+    int64_t base = c0;
+    if (vec_ok) {
+        for (; base + step <= c1; base += step) {
+            uint4 v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) v[u] = ld_stream_v4(groups + base + ((int64_t)u * blockDim.x + threadIdx.x) * 4);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t k[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    if (k[q] < G) atomicAdd(&sh_hist[k[q]], 1);
+                    else atomicMin(bad, (unsigned long long)(base + ((int64_t)u * blockDim.x + threadIdx.x) * 4 + q));
+                }
+            }
+        }
+    }
+    for (int64_t i = base + threadIdx.x; i < c1; i += blockDim.x) {
+        const uint32_t g = groups[i];
+        if (g < G) atomicAdd(&sh_hist[g], 1);
+        else atomicMin(bad, (unsigned long long)i);
+    }
+    __syncthreads();
+    int32_t* dst = gcnt + (int64_t)blockIdx.x * G;
+    for (int i = threadIdx.x; i < (int)G; i += blockDim.x) dst[i] = sh_hist[i];
+}
+
 // The hot-group cache of the next batch's count: groups above `thr` in
 // this batch (first kHotCache found).  hot_of is reset for the old list.
 __global__ void __launch_bounds__(256)
@@ -136,58 +178,94 @@ __device__ __forceinline__ void stats_account(uint32_t g, int32_t c, const int32
 }
 
 // WARP = true: one warp per group, lanes over the chunks (many chunks, few
-// groups); WARP = false: one thread per group (few chunks)
+// groups); WARP = false: one thread per group (few chunks).
+// chunk_live is a bitmap (bit c of word c / 32): lanes hold chunk i*32+lane,
+// so a ballot gives a warp's live bits for 32 chunks; warps OR them into a
+// shared bitmap and each CTA ORs its words into the global one once.
+constexpr int kMaxChunkWords = 4096 / 32;
+
 template <bool WARP>
 __global__ void __launch_bounds__(1024)
 k_batch_stats(int32_t* __restrict__ gcnt, int n_chunk, uint32_t G, const int32_t* __restrict__ pmap,
-              int P, int32_t* __restrict__ gcount, int32_t* __restrict__ gkept, int32_t* __restrict__ chunk_live,
+              int P, int32_t* __restrict__ gcount, int32_t* __restrict__ gkept, uint32_t* __restrict__ chunk_live,
               unsigned long long* __restrict__ tpt, unsigned long long* __restrict__ touched,
               const unsigned long long* __restrict__ bad, const int32_t* __restrict__ fill, int64_t W,
               unsigned long long* __restrict__ alg_bytes) {
     extern __shared__ uint32_t sh_tpt[];     // per-CTA partial loads (< 2^31)
+    __shared__ uint32_t sh_live[kMaxChunkWords];
     if (*bad != (unsigned long long)kNoBad) return;
+    const int nwords = (n_chunk + 31) >> 5;
     for (int p = threadIdx.x; p < P; p += blockDim.x) sh_tpt[p] = 0;
+    for (int i = threadIdx.x; i < nwords; i += blockDim.x) sh_live[i] = 0;
     __syncthreads();
     uint32_t my_touched = 0;
     unsigned long long my_bytes = 0;
     const unsigned lane = lane_id();
     if (WARP) {
+        // up to RK x 32 chunk counts per warp stay in registers; the live
+        // bits of those chunks are accumulated per warp in lb[]
+        constexpr int RK = 8;
+        uint32_t lb[RK];
+#pragma unroll
+        for (int i = 0; i < RK; ++i) lb[i] = 0;
         const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
         for (uint32_t g = blockIdx.x * (blockDim.x >> 5) + warp_id(); g < G; g += nwarps) {
+            int32_t kr[RK];
             int32_t c = 0;
-            for (int s = lane; s < n_chunk; s += 32) c += gcnt[(int64_t)s * G + g];
+#pragma unroll
+            for (int i = 0; i < RK; ++i) {
+                const int s = i * 32 + (int)lane;
+                kr[i] = (s < n_chunk) ? gcnt[(int64_t)s * G + g] : 0;
+                c += kr[i];
+            }
+            for (int s = RK * 32 + lane; s < n_chunk; s += 32) c += gcnt[(int64_t)s * G + g];
             c = warp_sum(c);
             int32_t kept = c;
-            if (c > W && gkept) {
-                kept = 0;
-                int32_t carry = 0;
-                for (int s0 = 0; s0 < n_chunk; s0 += 32) {
-                    const int s = s0 + (int)lane;
-                    const int64_t idx = (int64_t)s * G + g;
-                    const int32_t k = (s < n_chunk) ? gcnt[idx] : 0;
+            const bool drop = c > W && gkept;
+            int32_t carry = 0;
+            if (drop) kept = 0;
+            for (int s0 = 0; s0 < n_chunk; s0 += 32) {
+                const int s = s0 + (int)lane;
+                const int64_t idx = (int64_t)s * G + g;
+                int32_t k = 0;
+#pragma unroll
+                for (int i = 0; i < RK; ++i)
+                    if (s0 == i * 32) k = kr[i];
+                if (s0 >= RK * 32) k = (s < n_chunk) ? gcnt[idx] : 0;
+                bool live = k != 0;
+                if (drop) {
                     const int32_t incl = warp_incl_scan(k);
                     const int32_t pre = carry + incl - k;
-                    if (k) {
-                        if ((int64_t)pre + k <= (int64_t)c - W) gcnt[idx] = 0;
-                        else {
-                            kept += k;
-                            if (chunk_live) chunk_live[s] = 1;
-                        }
+                    if (k && (int64_t)pre + k <= (int64_t)c - W) {
+                        gcnt[idx] = 0;
+                        live = false;
                     }
+                    if (live) kept += k;
                     carry += __shfl_sync(SS_FULL, incl, 31);
                 }
-                kept = warp_sum(kept);
-            } else if (c && chunk_live) {
-                for (int s = lane; s < n_chunk; s += 32)
-                    if (gcnt[(int64_t)s * G + g]) chunk_live[s] = 1;
+                const uint32_t bits = __ballot_sync(SS_FULL, live);
+                if (chunk_live && bits) {
+                    bool held = false;
+#pragma unroll
+                    for (int i = 0; i < RK; ++i)
+                        if (s0 == i * 32) { lb[i] |= bits; held = true; }
+                    if (!held && lane == 0) atomicOr(&sh_live[s0 >> 5], bits);
+                }
             }
+            if (drop) kept = warp_sum(kept);
             if (lane == 0) {
                 gcount[g] = c;
                 if (gkept) gkept[g] = kept;
                 if (c) stats_account(g, c, pmap, sh_tpt, fill, W, my_touched, my_bytes);
             }
         }
+        if (chunk_live && lane == 0) {
+#pragma unroll
+            for (int i = 0; i < RK; ++i)
+                if (lb[i]) atomicOr(&sh_live[i], lb[i]);
+        }
     } else {
+        uint32_t lbits = 0;                      // n_chunk < 32 here
         for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < G; g += gridDim.x * blockDim.x) {
             int32_t c = 0;
             for (int s = 0; s < n_chunk; ++s) c += gcnt[(int64_t)s * G + g];
@@ -203,18 +281,20 @@ k_batch_stats(int32_t* __restrict__ gcnt, int n_chunk, uint32_t G, const int32_t
                         if ((int64_t)pre + k <= (int64_t)c - W) gcnt[idx] = 0;
                         else {
                             kept += k;
-                            if (chunk_live) chunk_live[s] = 1;
+                            lbits |= 1u << s;
                         }
                     }
                     pre += k;
                 }
-            } else if (c && chunk_live) {
+            } else if (c) {
                 for (int s = 0; s < n_chunk; ++s)
-                    if (gcnt[(int64_t)s * G + g]) chunk_live[s] = 1;
+                    if (gcnt[(int64_t)s * G + g]) lbits |= 1u << s;
             }
             if (gkept) gkept[g] = kept;
             if (c) stats_account(g, c, pmap, sh_tpt, fill, W, my_touched, my_bytes);
         }
+        lbits = __reduce_or_sync(SS_FULL, lbits);
+        if (chunk_live && lane == 0 && lbits) atomicOr(&sh_live[0], lbits);
     }
     my_touched = warp_sum(my_touched);
     my_bytes = warp_sum(my_bytes);
@@ -225,6 +305,11 @@ k_batch_stats(int32_t* __restrict__ gcnt, int n_chunk, uint32_t G, const int32_t
     __syncthreads();
     for (int p = threadIdx.x; p < P; p += blockDim.x)
         if (sh_tpt[p]) atomicAdd(&tpt[p], (unsigned long long)sh_tpt[p]);
+    if (chunk_live)
+        for (int i = threadIdx.x; i < nwords; i += blockDim.x) {
+            const uint32_t v = sh_live[i];
+            if (v && (chunk_live[i] & v) != v) atomicOr(&chunk_live[i], v);
+        }
 }
 
 // --------------------------------------------------------------------------
@@ -285,7 +370,7 @@ k_scan_reduce(const int32_t* __restrict__ gcnt, uint32_t G, int32_t* __restrict_
 __global__ void __launch_bounds__(1024)
 k_scan_top(int32_t* __restrict__ bsum, int nblk, DigitPlan plan, uint32_t* __restrict__ dhist,
            const unsigned long long* __restrict__ bad, int32_t* __restrict__ n_live,
-           int32_t* __restrict__ chunk_live = nullptr, int n_chunk = 0, int32_t* __restrict__ lc = nullptr,
+           uint32_t* __restrict__ chunk_live = nullptr, int n_chunk = 0, int32_t* __restrict__ lc = nullptr,
            int32_t* __restrict__ n_lc = nullptr, int32_t* __restrict__ btile = nullptr) {
     __shared__ int32_t sh_red[33];
     __shared__ uint32_t sh_ured[33];
@@ -324,7 +409,7 @@ k_scan_top(int32_t* __restrict__ bsum, int nblk, DigitPlan plan, uint32_t* __res
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const int c = 4 * threadIdx.x + q;
-            f[q] = (c < n_chunk) ? chunk_live[c] : 0;
+            f[q] = (c < n_chunk) ? (int32_t)((chunk_live[c >> 5] >> (c & 31)) & 1u) : 0;
             mine += f[q] ? 1 : 0;
         }
         int32_t tot;
@@ -333,9 +418,90 @@ k_scan_top(int32_t* __restrict__ bsum, int nblk, DigitPlan plan, uint32_t* __res
         for (int q = 0; q < 4; ++q) {
             const int c = 4 * threadIdx.x + q;
             if (f[q]) lc[ex++] = c;
-            if (c < n_chunk) chunk_live[c] = 0;
+
         }
         if (threadIdx.x == 0) *n_lc = tot;
+        __syncthreads();                         // every bit read before the words are cleared
+        for (int i = threadIdx.x; i < (n_chunk + 31) / 32; i += blockDim.x) chunk_live[i] = 0;
+    }
+}
+
+// k_scan_reduce + k_scan_top + k_scan_down in one CTA for G <= 16384 (16
+// groups per thread): run starts, digit bases of every pass, the kept total,
+// second-pass bucket tiles and the live-chunk list.
+constexpr int kScanSmallG = 16384;
+
+__global__ void __launch_bounds__(1024)
+k_scan_small(const int32_t* __restrict__ row, uint32_t G, DigitPlan plan, uint32_t* __restrict__ dhist,
+             int32_t* __restrict__ gstart, const unsigned long long* __restrict__ bad, int32_t* __restrict__ n_live,
+             uint32_t* __restrict__ chunk_live, int n_chunk, int32_t* __restrict__ lc, int32_t* __restrict__ n_lc,
+             int32_t* __restrict__ btile) {
+    __shared__ uint32_t sh_dh[2][kMaxBins];
+    __shared__ int32_t sh_red[33];
+    __shared__ uint32_t sh_ured[33];
+    if (*bad != (unsigned long long)kNoBad) return;
+    for (int i = threadIdx.x; i < 2 * kMaxBins; i += blockDim.x) (&sh_dh[0][0])[i] = 0;
+    __syncthreads();
+    constexpr int GPT = kScanSmallG / 1024;
+    const uint32_t g0 = threadIdx.x * GPT;
+    int32_t c[GPT];
+    int32_t tsum = 0;
+#pragma unroll
+    for (int q = 0; q < GPT; ++q) {
+        c[q] = (g0 + q < G) ? row[g0 + q] : 0;
+        tsum += c[q];
+    }
+    for (int d = 0; d < plan.npass; ++d) {
+        const uint32_t mask = (1u << plan.bits[d]) - 1u;
+#pragma unroll
+        for (int q = 0; q < GPT; ++q)
+            if (c[q]) atomicAdd(&sh_dh[d][((g0 + q) >> plan.shift[d]) & mask], (uint32_t)c[q]);
+    }
+    int32_t total;
+    int32_t ex = block_excl_scan(tsum, sh_red, &total);
+#pragma unroll
+    for (int q = 0; q < GPT; ++q) {
+        if (g0 + q < G) gstart[g0 + q] = ex;
+        ex += c[q];
+    }
+    if (threadIdx.x == 0) *n_live = total;
+    __syncthreads();
+    for (int d = 0; d < plan.npass; ++d) {
+        uint32_t* h = dhist + (int64_t)d * kMaxBins;
+        const uint32_t a = sh_dh[d][2 * threadIdx.x], b = sh_dh[d][2 * threadIdx.x + 1];
+        uint32_t tot;
+        const uint32_t e2 = block_excl_scan(a + b, sh_ured, &tot);
+        h[2 * threadIdx.x] = e2;
+        h[2 * threadIdx.x + 1] = e2 + a;
+        if (d == 0 && btile && plan.npass == 2) {
+            const int32_t ta = (int32_t)((a + kSortTile - 1) / kSortTile);
+            const int32_t tb = (int32_t)((b + kSortTile - 1) / kSortTile);
+            int32_t ttot;
+            const int32_t tex = block_excl_scan(ta + tb, sh_red, &ttot);
+            btile[2 * threadIdx.x] = tex;
+            btile[2 * threadIdx.x + 1] = tex + ta;
+            if (threadIdx.x == 0) btile[kMaxBins] = ttot;
+        }
+    }
+    if (chunk_live) {
+        int32_t f[4], mine = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int ch = 4 * threadIdx.x + q;
+            f[q] = (ch < n_chunk) ? (int32_t)((chunk_live[ch >> 5] >> (ch & 31)) & 1u) : 0;
+            mine += f[q] ? 1 : 0;
+        }
+        int32_t tot;
+        int32_t e3 = block_excl_scan(mine, sh_red, &tot);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int ch = 4 * threadIdx.x + q;
+            if (f[q]) lc[e3++] = ch;
+
+        }
+        if (threadIdx.x == 0) *n_lc = tot;
+        __syncthreads();                         // every bit read before the words are cleared
+        for (int i = threadIdx.x; i < (n_chunk + 31) / 32; i += blockDim.x) chunk_live[i] = 0;
     }
 }
 

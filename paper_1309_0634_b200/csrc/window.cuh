@@ -57,6 +57,7 @@ struct IngestArgs {
     unsigned long long* part_ns;       // per-partition (CTA) time, ns
     unsigned long long* part_work;     // per-partition stored values
     const int32_t* n_live;      // live tuples of this sub-batch (0: nothing to do)
+    int cpp;                    // CTAs sharing one partition's work (grid = P * cpp)
     const unsigned long long* bad;
 };
 
@@ -84,7 +85,6 @@ __device__ __forceinline__ void add_delta(uint32_t* lo, uint32_t* hi, long long 
 
 constexpr int kLILP = 8;                    // values in flight per lane for long members
 constexpr int kUnit = 32 * kLILP;           // values of one warp unit (long members)
-constexpr int kCtaPerPart = 4;              // CTAs sharing one partition's work
 
 #ifdef SS_K4_PROF
 __device__ unsigned long long g_k4_prof[8];
@@ -119,6 +119,7 @@ k_ingest(IngestArgs a) {
 #endif
     // partition p is processed by kCtaPerPart CTAs; its members (and split
     // shares) are dealt to them round-robin
+    const int kCtaPerPart = a.cpp;
     const int p = blockIdx.x / kCtaPerPart;
     const int sub = blockIdx.x % kCtaPerPart;
     const int lo = a.offsets[p], hi = a.offsets[p + 1];
