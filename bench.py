@@ -386,17 +386,31 @@ def main():
     peak, peak_kind = peaks()
     cls_ms = {n: kms[i] / args.steps for i, n in enumerate(L.KERNEL_CLASSES)}
     cls_launch = {n: kn[i] for i, n in enumerate(L.KERNEL_CLASSES)}
-    # algorithmic bytes per class and step
-    ingest_bytes = alg_per_step - 8 * B
-    cls_bytes = {"count": 4 * B, "place": 8 * B, "ingest": ingest_bytes}
+    # algorithmic bytes per class and step:
+    # the input is read once in the model -- keys by the count, attrs by the
+    # placement (its re-read of the keys is implementation overhead) -- and
+    # the window update owns the ring and state bytes
+    key_bytes = 8 if kind.endswith("64") else 4
+    ingest_bytes = alg_per_step - (key_bytes + 4) * B
+    cls_bytes = {"count": key_bytes * B, "place": 4 * B, "ingest": ingest_bytes}
     main_cls = max(("count", "place", "ingest"), key=lambda n: cls_ms[n])
     k_ms = cls_ms[main_cls]
     achieved = cls_bytes[main_cls] / (k_ms / 1e3) / 1e9 if k_ms > 0 else 0.0
     step_ms = ms / args.steps
     path_achieved = alg_per_step / (step_ms / 1e3) / 1e9
+    # measured DRAM traffic per launch of that kernel class (ncu --set full of
+    # this config, committed under profiles/), else null
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as fh:
+            tj = json.load(fh)
+        if args.config in tj and main_cls in tj[args.config] and B == (1 << 24) and world == 1:
+            traffic = tj[args.config][main_cls]["bytes_per_launch"]
+    except Exception:
+        traffic = None
 
     # ---- (3) end to end through the public API with host buffers -------------
-    e2e_steps = args.e2e_steps or max(3, args.steps // 4)
+    e2e_steps = args.e2e_steps or max(4, args.steps // 2)
     hosts = []
     for g, a in batches[:2]:
         hg = torch.empty(B, dtype=g.dtype, pin_memory=True)
@@ -404,9 +418,10 @@ def main():
         hg.copy_(g)
         ha.copy_(a)
         hosts.append((hg, ha))
-    res_g = np.empty(G, dtype=np.int32)
-    res_a = np.empty(G, dtype=np.float64)
-    res_n = C.c_int64()
+    # streaming use of the public API: batch i+1 is issued
+    # (its H2D overlaps batch i's compute) before batch i's rows are pulled
+    # from pinned host memory
+    eng.set_host_emit(True)
     d2h = 0
     barrier()
     e0 = torch.cuda.Event(enable_timing=True)
@@ -419,9 +434,11 @@ def main():
             sharded.step(hg, ha, bal, gbal)
         else:
             eng.step(hg, ha, bal, sync=False)
-        lib.ss_results_raw(eng._h, G, res_g.ctypes.data_as(C.c_void_p), res_a.ctypes.data_as(C.c_void_p),
-                           C.byref(res_n))
-        d2h += res_n.value * 12 + 4
+        if i > 0:
+            rg, ra = eng.results_pull()
+            d2h += len(rg) * 12 + 4
+    rg, ra = eng.results_pull()
+    d2h += len(rg) * 12 + 4
     e1.record(stream)
     e1.synchronize()
     e2e_wall = time.perf_counter() - t0
@@ -453,7 +470,9 @@ def main():
                                        if world > 1 else "single GPU"),
                        "global_batch": B * world},
             "roofline": {"bound": "hbm", "kernel": main_cls, "achieved": achieved, "peak": peak,
-                         "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                         "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                         "traffic_source": "profiles/r1_traffic.json (ncu --set full, dram read+write per launch)"
+                                           if traffic is not None else None,
                          "peak_source": peak_kind,
                          "alg_bytes_per_launch": cls_bytes[main_cls] / max(1, cls_launch[main_cls] / args.steps),
                          "ms_per_step": k_ms},

@@ -66,7 +66,8 @@ typedef struct {
     int32_t  device;        /* CUDA ordinal                                           */
     int32_t  reserved;
     int64_t  max_batch;     /* largest n passed to ss_step (0: 1<<24)                 */
-    int64_t  sub_batch;     /* L2-resident ingest unit (0: auto)                      */
+    int64_t  sub_batch;     /* count chunk: tuple granularity at which never-stored   */
+                            /* tuples are dropped (power of two >= 2^16; 0: auto)     */
     int64_t  pool_values;   /* ring pool capacity in values (0: auto)                 */
 } ss_config;
 
@@ -110,7 +111,7 @@ const char* ss_last_error(ss_engine* e);
 const char* ss_version(void);
 /* kernels this library has launched (all engines); reset != 0 zeroes it */
 long long ss_launch_count(int reset);
-/* the engine's placement sub-batch size (tuples) */
+/* the engine's count-chunk size (tuples) */
 long long ss_sub_batch(ss_engine* e);
 
 /* ---- assignment (partition.py:45-114, 181-203) ------------------------ */
@@ -207,6 +208,15 @@ int  ss_profile_read(ss_engine* e, double* ms, int64_t* launches, int reset);
 /* algorithmic HBM bytes of the steps since the last reset:
  * B*(key+attr) + 4*sum min(k,W) + 4*sum_{k<W} max(0,f0+k-W) + 76*touched */
 int  ss_alg_bytes(ss_engine* e, int64_t* bytes, int reset);
+/* streaming emission: when enabled, every ss_step writes its
+ * (group, AVG) rows straight into mapped pinned host memory (double-buffered);
+ * ss_results_pull returns the oldest batch not yet pulled, waiting only for
+ * that batch.  Pull at least every other batch.  With host inputs, ss_step's
+ * H2D runs on a copy stream into alternating staging buffers, so the next
+ * batch's copy overlaps the current batch's compute (host buffers must stay
+ * unchanged until the step after next has been issued). */
+int  ss_set_host_emit(ss_engine* e, int enable);
+int  ss_results_pull(ss_engine* e, int64_t cap, int32_t* groups, double* avg, int64_t* n);
 /* raw per-batch emission (no ordering): group id and AVG of each touched group */
 int  ss_results_raw(ss_engine* e, int64_t cap, int32_t* groups, double* avg, int64_t* n);
 

@@ -136,6 +136,30 @@ struct ss_engine {
     bool keys64 = false;
     KeyTable kt{};
     long long* stage_keys64 = nullptr;
+
+    // streaming input (ss_step / ss_step_keys64 with host buffers): the next
+    // batch's H2D runs on a copy stream into the other staging buffer while
+    // the current batch computes; a buffer is reused once the batch that
+    // read it has finished its first placement pass
+    cudaStream_t cp = nullptr;
+    cudaEvent_t ev_staged[2] = {nullptr, nullptr}, ev_freed[2] = {nullptr, nullptr};
+    bool freed_rec[2] = {false, false};
+    int stg_next = 0, cur_stage = -1;
+    uint32_t* skeys[2] = {nullptr, nullptr};
+    int32_t* svals[2] = {nullptr, nullptr};
+    long long* sk64[2] = {nullptr, nullptr};
+
+    // host emission: each batch's (group, AVG) rows written by a kernel
+    // straight into mapped pinned host memory (double-buffered)
+    bool host_emit = false;
+    int32_t* h_emit_g[2] = {nullptr, nullptr};
+    double* h_emit_avg[2] = {nullptr, nullptr};
+    unsigned* h_emit_n[2] = {nullptr, nullptr};
+    int32_t* d_emit_g[2] = {nullptr, nullptr};
+    double* d_emit_avg[2] = {nullptr, nullptr};
+    unsigned* d_emit_n[2] = {nullptr, nullptr};
+    cudaEvent_t ev_emit[2] = {nullptr, nullptr};
+    long long emit_seq = 0, pull_seq = 0;
     int32_t* kbsum = nullptr;
 
     // multi-GPU routing: group -> owning GPU
@@ -298,6 +322,16 @@ __global__ void k_dense_off(int64_t* off, int32_t* cap, int64_t G, int64_t W) {
     }
 }
 __global__ void k_set_bad(unsigned long long* bad) { *bad = (unsigned long long)kNoBad; }
+// the batch's (group, AVG) rows into mapped pinned host memory (PCIe writes)
+__global__ void k_emit_host(const unsigned* __restrict__ n_res, const int32_t* __restrict__ g,
+                            const double* __restrict__ avg, int32_t* hg, double* havg, unsigned* hn) {
+    const unsigned n = *n_res;
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        hg[i] = g[i];
+        havg[i] = avg[i];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *hn = n;
+}
 __global__ void k_fill_u64(unsigned long long* p, int64_t n, unsigned long long v) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
 }
@@ -420,8 +454,18 @@ extern "C" void ss_destroy(ss_engine* e) {
     if (!e) return;
     cudaSetDevice(e->cfg.device);
     cudaStreamSynchronize(e->st);
+    if (e->cp) cudaStreamSynchronize(e->cp);
     for (void* p : e->allocs) cudaFree(p);
     if (e->h_rep) cudaFreeHost(e->h_rep);
+    for (int b = 0; b < 2; ++b) {
+        if (e->h_emit_g[b]) cudaFreeHost(e->h_emit_g[b]);
+        if (e->h_emit_avg[b]) cudaFreeHost(e->h_emit_avg[b]);
+        if (e->h_emit_n[b]) cudaFreeHost(e->h_emit_n[b]);
+        if (e->ev_staged[b]) cudaEventDestroy(e->ev_staged[b]);
+        if (e->ev_freed[b]) cudaEventDestroy(e->ev_freed[b]);
+        if (e->ev_emit[b]) cudaEventDestroy(e->ev_emit[b]);
+    }
+    if (e->cp) cudaStreamDestroy(e->cp);
     if (e->side) cudaStreamDestroy(e->side);
     if (e->ev_stats) cudaEventDestroy(e->ev_stats);
     if (e->ev_bal) cudaEventDestroy(e->ev_bal);
@@ -479,6 +523,12 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
     SS_CUDA(e, cudaEventCreateWithFlags(&e->ev_bal, cudaEventDisableTiming));
     SS_CUDA(e, cudaEventCreateWithFlags(&e->ev_k4, cudaEventDisableTiming));
     SS_CUDA(e, cudaEventCreateWithFlags(&e->ev_apply, cudaEventDisableTiming));
+    SS_CUDA(e, cudaStreamCreateWithFlags(&e->cp, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) {
+        SS_CUDA(e, cudaEventCreateWithFlags(&e->ev_staged[b], cudaEventDisableTiming));
+        SS_CUDA(e, cudaEventCreateWithFlags(&e->ev_freed[b], cudaEventDisableTiming));
+        SS_CUDA(e, cudaEventCreateWithFlags(&e->ev_emit[b], cudaEventDisableTiming));
+    }
 
     const int64_t G = e->G, W = e->W;
     int rc;
@@ -709,6 +759,46 @@ static int join_side(ss_engine* e) {
         SS_CUDA(e, cudaStreamWaitEvent(e->st, e->ev_apply, 0));
         e->side_pending = false;
     }
+    return SS_OK;
+}
+
+// streaming input: pick the batch's staging buffer; the copy stream waits
+// until the batch that last read it has finished its first placement pass
+static int begin_stage(ss_engine* e, bool keys64) {
+    const int b = e->stg_next;
+    e->stg_next ^= 1;
+    int rc;
+    if (!e->skeys[1]) {
+        e->skeys[0] = e->stage_keys;
+        e->svals[0] = e->stage_vals;
+        if ((rc = dalloc(e, &e->skeys[1], e->max_batch)) || (rc = dalloc(e, &e->svals[1], e->max_batch))) return rc;
+    }
+    if (keys64 && !e->sk64[1]) {
+        e->sk64[0] = e->stage_keys64;
+        if ((rc = dalloc(e, &e->sk64[1], e->max_batch))) return rc;
+    }
+    if (e->freed_rec[b]) SS_CUDA(e, cudaStreamWaitEvent(e->cp, e->ev_freed[b], 0));
+    e->cur_stage = b;
+    return SS_OK;
+}
+
+// host -> staging buffer on the copy stream (device pointers pass through)
+template <typename T>
+static int stage_h2d(ss_engine* e, T* dst, const T* src, int64_t n, const T** out) {
+    if (!src || is_device_ptr(src)) {
+        *out = src;
+        return SS_OK;
+    }
+    if (n) SS_CUDA(e, cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyHostToDevice, e->cp));
+    *out = dst;
+    return SS_OK;
+}
+
+// the engine stream waits for the batch's copies
+static int end_stage(ss_engine* e) {
+    const int b = e->cur_stage;
+    SS_CUDA(e, cudaEventRecord(e->ev_staged[b], e->cp));
+    SS_CUDA(e, cudaStreamWaitEvent(e->st, e->ev_staged[b], 0));
     return SS_OK;
 }
 
@@ -1046,6 +1136,12 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
         ProfScope ps(e, SS_K_PLACE, e->st);
         if ((rc = launch_place_step(e, dk, dv, n))) return rc;
     }
+    if (e->cur_stage >= 0) {
+        // the staged input is not read again: the next-but-one batch may reuse it
+        SS_CUDA(e, cudaEventRecord(e->ev_freed[e->cur_stage], e->st));
+        e->freed_rec[e->cur_stage] = true;
+        e->cur_stage = -1;
+    }
     {
         ProfScope ps(e, SS_K_INGEST, e->st);
         IngestArgs a = ingest_args(e, use_plan);
@@ -1091,6 +1187,13 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
             ss_note_launch(), k_minmax_rescan<<<8 * kNumSM, 256, 0, e->st>>>(e->rescan, e->n_rescan, e->ring, e->off, e->W, e->mn,
                                                            e->mx);
             ss_note_launch(), k_rescan_rows<<<4, 256, 0, e->st>>>(e->rescan, e->n_rescan, e->mn, e->mx, e->r_mn, e->r_mx);
+        }
+        if (emit && e->host_emit) {
+            const int b = (int)(e->emit_seq & 1);
+            ss_note_launch(), k_emit_host<<<kNumSM, 256, 0, e->st>>>(e->n_res, e->r_g, e->r_avg, e->d_emit_g[b],
+                                                                     e->d_emit_avg[b], e->d_emit_n[b]);
+            SS_CUDA(e, cudaEventRecord(e->ev_emit[b], e->st));
+            ++e->emit_seq;
         }
         SS_CUDA(e, cudaGetLastError());
     }
@@ -1450,9 +1553,18 @@ extern "C" int ss_step(ss_engine* e, const uint32_t* groups, const int32_t* attr
     if (!e || n < 0) return SS_E_CONFIG;
     int rc;
     if ((rc = check_balancer(e, cfg))) return rc;
-    const uint32_t* dk;
-    const int32_t* dv;
-    if ((rc = stage_input(e, groups, attrs, n, &dk, &dv))) return rc;
+    if (n > e->max_batch) return fail(e, SS_E_CONFIG, "batch larger than max_batch");
+    const uint32_t* dk = groups;
+    const int32_t* dv = attrs;
+    if (!is_device_ptr(groups) || (attrs && !is_device_ptr(attrs))) {
+        // host buffers: H2D on the copy stream into this batch's staging
+        // buffer, overlapped with the previous batch's compute
+        if ((rc = begin_stage(e, false))) return rc;
+        const int b = e->cur_stage;
+        if ((rc = stage_h2d(e, e->skeys[b], groups, n, &dk)) || (rc = stage_h2d(e, e->svals[b], attrs, n, &dv)) ||
+            (rc = end_stage(e)))
+            return rc;
+    }
     g_last_keys = dk;
     const bool has_policy = cfg && cfg->policy != SS_POLICY_NO;
     e->last_plan = -1;
@@ -1932,8 +2044,55 @@ extern "C" int ss_step_keys64(ss_engine* e, const int64_t* keys, const int32_t* 
     if (!e->keys64) return fail(e, SS_E_CONFIG, "engine was created with key_bits = 32");
     if (n > e->max_batch) return fail(e, SS_E_CONFIG, "batch larger than max_batch");
     int rc;
-    if ((rc = map_keys(e, keys, n, e->stage_keys))) return rc;
-    return ss_step(e, e->stage_keys, attrs, n, cfg, rep);
+    if ((rc = check_balancer(e, cfg))) return rc;
+    const int64_t* dk = keys;
+    const int32_t* dv = attrs;
+    if (!is_device_ptr(keys) || (attrs && !is_device_ptr(attrs))) {
+        if ((rc = begin_stage(e, true))) return rc;
+        const int b = e->cur_stage;
+        const long long* k64 = nullptr;
+        if ((rc = stage_h2d(e, e->sk64[b], (const long long*)keys, n, &k64)) ||
+            (rc = stage_h2d(e, e->svals[b], attrs, n, &dv)) || (rc = end_stage(e)))
+            return rc;
+        dk = (const int64_t*)k64;
+    }
+    if ((rc = map_keys(e, dk, n, e->stage_keys))) return rc;
+    return ss_step(e, e->stage_keys, dv, n, cfg, rep);
+}
+
+extern "C" int ss_set_host_emit(ss_engine* e, int enable) {
+    if (!e) return SS_E_CONFIG;
+    SS_CUDA(e, cudaStreamSynchronize(e->st));
+    if (enable && !e->h_emit_g[0]) {
+        for (int b = 0; b < 2; ++b) {
+            SS_CUDA(e, cudaHostAlloc((void**)&e->h_emit_g[b], e->G * 4, cudaHostAllocMapped));
+            SS_CUDA(e, cudaHostAlloc((void**)&e->h_emit_avg[b], e->G * 8, cudaHostAllocMapped));
+            SS_CUDA(e, cudaHostAlloc((void**)&e->h_emit_n[b], 64, cudaHostAllocMapped));
+            SS_CUDA(e, cudaHostGetDevicePointer((void**)&e->d_emit_g[b], e->h_emit_g[b], 0));
+            SS_CUDA(e, cudaHostGetDevicePointer((void**)&e->d_emit_avg[b], e->h_emit_avg[b], 0));
+            SS_CUDA(e, cudaHostGetDevicePointer((void**)&e->d_emit_n[b], e->h_emit_n[b], 0));
+        }
+    }
+    e->host_emit = enable != 0;
+    e->emit_seq = e->pull_seq = 0;
+    return SS_OK;
+}
+
+extern "C" int ss_results_pull(ss_engine* e, int64_t cap, int32_t* groups, double* avg, int64_t* n) {
+    if (!e) return SS_E_CONFIG;
+    if (!e->host_emit) return fail(e, SS_E_CONFIG, "host emission is off (ss_set_host_emit)");
+    if (e->pull_seq >= e->emit_seq) return fail(e, SS_E_CONFIG, "no emitted batch left to pull");
+    if (e->emit_seq - e->pull_seq > 2)
+        return fail(e, SS_E_EXEC, "emitted rows overwritten: pull at least every other batch");
+    const int b = (int)(e->pull_seq & 1);
+    SS_CUDA(e, cudaEventSynchronize(e->ev_emit[b]));
+    const unsigned nr = *(volatile unsigned*)e->h_emit_n[b];
+    if (n) *n = nr;
+    const int64_t m = std::min<int64_t>(cap, nr);
+    if (m > 0 && groups) memcpy(groups, e->h_emit_g[b], m * 4);
+    if (m > 0 && avg) memcpy(avg, e->h_emit_avg[b], m * 8);
+    ++e->pull_seq;
+    return SS_OK;
 }
 
 extern "C" int ss_slot_keys(ss_engine* e, int64_t* keys, int64_t* n_slots) {

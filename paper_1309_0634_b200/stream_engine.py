@@ -324,7 +324,8 @@ class StreamEngine:
         rep = L.StepReport()
         self._check(self._lib.ss_step(self._h, pg, pa, len(g), C.byref(bal),
                                       C.byref(rep) if sync else None))
-        self._keep = (_k1, _k2)
+        # host inputs are copied asynchronously: keep the last two alive
+        self._keep = (getattr(self, "_keep", (None, None))[-1], (_k1, _k2))
         return self._report(rep) if sync else None
 
     def _step64(self, keys, attrs, balancer, sync):
@@ -340,7 +341,7 @@ class StreamEngine:
         rep = L.StepReport()
         self._check(self._lib.ss_step_keys64(self._h, pk, pa, len(k), C.byref(bal),
                                              C.byref(rep) if sync else None))
-        self._keep = (_k1, _k2)
+        self._keep = (getattr(self, "_keep", (None, None))[-1], (_k1, _k2))
         return self._report(rep) if sync else None
 
     def slot_keys(self) -> np.ndarray:
@@ -350,6 +351,22 @@ class StreamEngine:
         out = np.empty(max(1, n.value), dtype=np.int64)
         self._check(self._lib.ss_slot_keys(self._h, _ptr(out)[0], C.byref(n)))
         return out[:n.value]
+
+    # -- streaming emission ---------------------------------
+    def set_host_emit(self, enable: bool = True):
+        """Every step writes its (group, AVG) rows into pinned host memory;
+        results_pull() returns the oldest batch not yet pulled."""
+        self._check(self._lib.ss_set_host_emit(self._h, int(bool(enable))))
+        self._pull_g = np.empty(self.n_groups, dtype=np.int32)
+        self._pull_avg = np.empty(self.n_groups, dtype=np.float64)
+
+    def results_pull(self):
+        """(groups int32[k], avg float64[k]) of the oldest unpulled batch
+        (views into reused buffers: copy them to keep them)."""
+        n = C.c_int64()
+        self._check(self._lib.ss_results_pull(self._h, self.n_groups, _ptr(self._pull_g)[0],
+                                              _ptr(self._pull_avg)[0], C.byref(n)))
+        return self._pull_g[:n.value], self._pull_avg[:n.value]
 
     def last_report(self) -> StepReport:
         rep = L.StepReport()

@@ -6,7 +6,7 @@ from paper_1309_0634_b200.stream_engine import StreamEngine
 name = sys.argv[1] if len(sys.argv) > 1 else 'c2'
 desc, kind, s, G, W, B, aggs, policy, split = bench.CONFIGS[name]
 dev = torch.device('cuda', 0)
-eng = StreamEngine(G, W, n_partitions=148, aggregates=aggs, max_batch=B)
+eng = StreamEngine(G, W, n_partitions=148, aggregates=aggs, max_batch=B, initial='hash')
 bal = eng.balancer_struct(policy, B // 1480, 0.5, split=split)
 bs = bench.make_batches(kind, s, G, B, 2, dev, 7)
 for i in range(8):
