@@ -656,7 +656,7 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
             (rc = dalloc(e, &t.first, cap + 1)) || (rc = dalloc(e, &t.ent, e->max_batch)) ||
             (rc = dalloc(e, &t.new_ent, G)) || (rc = dalloc(e, &t.n_new, 1)) || (rc = dalloc(e, &t.n_slots, 1)) ||
             (rc = dalloc(e, &t.mark, e->max_batch)) || (rc = dalloc(e, &t.slot_keys, G)) ||
-            (rc = dalloc(e, &t.min_key_entry, 1)) || (rc = dalloc(e, &t.overflow, 1)) ||
+            (rc = dalloc(e, &t.min_key_entry, 1)) || (rc = dalloc(e, &t.overflow, 1)) || (rc = dalloc(e, &t.pending, 1)) ||
             (rc = dalloc(e, &e->stage_keys64, e->max_batch)) ||
             (rc = dalloc(e, &e->kbsum, e->max_batch / kMarkBlk + 2)))
             return rc;
@@ -2011,14 +2011,15 @@ static int map_keys(ss_engine* e, const int64_t* keys, int64_t n, uint32_t* dout
     if (n == 0) return SS_OK;
     KeyTable& t = e->kt;
     const int nblk = (int)((n + kMarkBlk - 1) / kMarkBlk);
-    ss_note_launch(), k_key_probe<<<4 * kNumSM, 256, 0, e->st>>>(dk, n, t);
+    SS_CUDA(e, cudaMemsetAsync(t.pending, 0, 4, e->st));
+    ss_note_launch(), k_key_probe<<<8 * kNumSM, 256, 0, e->st>>>(dk, n, t, dout);
     ss_note_launch(), k_key_rank_small<<<1, 1024, 0, e->st>>>(t);
     ss_note_launch(), k_key_mark<<<2 * kNumSM, 256, 0, e->st>>>(t);
     ss_note_launch(), k_key_mark_count<<<nblk, 1024, 0, e->st>>>(t, n, e->kbsum);
     ss_note_launch(), k_key_mark_scan<<<1, 1024, 0, e->st>>>(t, e->kbsum, nblk);
     ss_note_launch(), k_key_mark_assign<<<nblk, 1024, 0, e->st>>>(t, n, e->kbsum);
     ss_note_launch(), k_key_mark_done<<<1, 1, 0, e->st>>>(t);
-    ss_note_launch(), k_key_map<<<4 * kNumSM, 256, 0, e->st>>>(dk, n, t, dout);
+    ss_note_launch(), k_key_map<<<8 * kNumSM, 256, 0, e->st>>>(dk, n, t, dout);
     SS_CUDA(e, cudaGetLastError());
     return SS_OK;
 }

@@ -41,44 +41,82 @@ struct KeyTable {
     unsigned long long* slot_keys;   // [G] key of each slot
     int* min_key_entry;         // entry index used for INT64_MIN (-1)
     int* overflow;              // more distinct keys than G
+    int* pending;               // some tuple of the batch has a key without a slot yet
     unsigned long long cap_mask;
     int G;
 };
 
 // probe / claim.  The table has >= 2G entries, so probing terminates.
-__global__ void __launch_bounds__(256)
-k_key_probe(const long long* __restrict__ keys, int64_t n, KeyTable t) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const unsigned long long k = (unsigned long long)keys[i];
-        int e;
-        if (k == kEmptyKey) {
-            // the reserved marker value gets a dedicated entry: cap_mask + 1
-            e = (int)(t.cap_mask + 1);
-            if (atomicCAS(t.min_key_entry, -1, e) == -1) {
+// A tuple whose key already has a slot gets it written straight away (the
+// steady state: no second pass); a tuple of a key without a slot yet is
+// marked pending (out = ~0) with its entry remembered for k_key_map.
+constexpr int kProbeILP = 4;
+
+__device__ __forceinline__ int key_entry(KeyTable& t, unsigned long long k, unsigned long long h) {
+    while (true) {
+        const unsigned long long cur = t.keys[h];
+        if (cur == k) return (int)h;
+        if (cur == kEmptyKey) {
+            const unsigned long long prev = atomicCAS(&t.keys[h], kEmptyKey, k);
+            if (prev == kEmptyKey) {
                 const int k2 = atomicAdd(t.n_new, 1);
-                if (k2 < t.G) t.new_ent[k2] = e; else *t.overflow = 1;
+                if (k2 < t.G) t.new_ent[k2] = (int)h; else *t.overflow = 1;
+                return (int)h;
             }
-        } else {
-            unsigned long long h = key_hash(k) & t.cap_mask;
-            while (true) {
-                const unsigned long long cur = t.keys[h];
-                if (cur == k) break;
-                if (cur == kEmptyKey) {
-                    const unsigned long long prev = atomicCAS(&t.keys[h], kEmptyKey, k);
-                    if (prev == kEmptyKey) {
-                        const int k2 = atomicAdd(t.n_new, 1);
-                        if (k2 < t.G) t.new_ent[k2] = (int)h; else *t.overflow = 1;
-                        break;
-                    }
-                    if (prev == k) break;
-                }
-                h = (h + 1) & t.cap_mask;
-            }
-            e = (int)h;
+            if (prev == k) return (int)h;
         }
-        t.ent[i] = e;
-        if (t.slot[e] < 0) atomicMin(&t.first[e], (unsigned int)i);
+        h = (h + 1) & t.cap_mask;
     }
+}
+
+__global__ void __launch_bounds__(256)
+k_key_probe(const long long* __restrict__ keys, int64_t n, KeyTable t, uint32_t* __restrict__ out) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * kProbeILP;
+    bool any_pending = false;
+    for (int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x); i0 < n; i0 += stride) {
+        unsigned long long k[kProbeILP], cur[kProbeILP], h[kProbeILP];
+        // all first probes in flight together
+#pragma unroll
+        for (int u = 0; u < kProbeILP; ++u) {
+            const int64_t i = i0 + (int64_t)u * gridDim.x * blockDim.x;
+            k[u] = (i < n) ? (unsigned long long)keys[i] : kEmptyKey;
+            h[u] = key_hash(k[u]) & t.cap_mask;
+        }
+        // first probes through the read-only path: the hottest keys' entries
+        // are then L1 hits instead of a stream of requests to one L2 slice.
+        // A stale read is harmless -- an entry claimed meanwhile is found
+        // again by key_entry's CAS (prev == k) or probed past
+#pragma unroll
+        for (int u = 0; u < kProbeILP; ++u) cur[u] = __ldg(t.keys + h[u]);
+#pragma unroll
+        for (int u = 0; u < kProbeILP; ++u) {
+            const int64_t i = i0 + (int64_t)u * gridDim.x * blockDim.x;
+            if (i >= n) continue;
+            int e;
+            if (k[u] == kEmptyKey) {
+                // the reserved marker value gets a dedicated entry: cap_mask + 1
+                e = (int)(t.cap_mask + 1);
+                if (atomicCAS(t.min_key_entry, -1, e) == -1) {
+                    const int k2 = atomicAdd(t.n_new, 1);
+                    if (k2 < t.G) t.new_ent[k2] = e; else *t.overflow = 1;
+                }
+            } else {
+                e = (cur[u] == k[u]) ? (int)h[u] : key_entry(t, k[u], h[u]);
+            }
+            const int sl = __ldg(t.slot + e);      // slots are assigned by later kernels only
+            if (sl >= 0) {
+                out[i] = (uint32_t)sl;
+            } else {
+                out[i] = 0xffffffffu;
+                t.ent[i] = e;
+                atomicMin(&t.first[e], (unsigned int)i);
+                any_pending = true;
+            }
+        }
+    }
+    // one flag write per warp (a store per pending tuple would serialise
+    // on the flag's L2 slice)
+    if (__any_sync(SS_FULL, any_pending) && lane_id() == 0) *t.pending = 1;
 }
 
 constexpr int kKeySmall = 2048;     // new keys ranked inside one CTA up to this many
@@ -182,10 +220,13 @@ __global__ void k_key_mark_done(KeyTable t) {
     *t.n_new = 0;
 }
 
-// tuple -> slot; also remember each slot's key
+// pending tuples -> slot; the first tuple of each freshly assigned key
+// also records the slot's key
 __global__ void __launch_bounds__(256)
 k_key_map(const long long* __restrict__ keys, int64_t n, KeyTable t, uint32_t* __restrict__ out) {
+    if (*t.pending == 0) return;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        if (out[i] != 0xffffffffu) continue;
         const int e = t.ent[i];
         const int s = t.slot[e];
         out[i] = (uint32_t)s;
