@@ -654,9 +654,14 @@ k_sort_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
     if (n_dev && seg.mode != 1) n = *n_dev;      // consumes a compacted (kept-only) input
     const unsigned w = warp_id(), lane = lane_id();
     const int wbase = (int)w * 32 * kSortItems;
-    // claim the next tile (thread 0): ticket -> input range and segment
-    auto claim = [&](int slot) {
-        const uint32_t t = atomicAdd(ticket, 1u);
+    // second-pass bucket tile prefix, searched by every claim: staged in
+    // shared memory once per CTA
+    __shared__ int32_t sh_btile[kMaxBins + 1];
+    if (seg.mode == 2)
+        for (int i = threadIdx.x; i <= seg.nb; i += kSortThreads) sh_btile[i] = seg.btile[i];
+    // claim a tile (thread 0): ticket -> input range and segment.  The
+    // ticket's atomic is issued one phase before its result is needed.
+    auto claim = [&](int slot, uint32_t t) {
         int64_t t0 = -1;
         int tn = 0, k = 0, sg = 0;
         if (seg.mode == 1) {
@@ -670,14 +675,14 @@ k_sort_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
                 if (t0 >= n) t0 = -1;                             // past a short last chunk
             }
         } else if (seg.mode == 2) {
-            if ((int)t < seg.btile[seg.nb]) {
+            if ((int)t < sh_btile[seg.nb]) {
                 int lo2 = 0, hi2 = seg.nb - 1;                     // last bucket with btile <= t
                 while (lo2 < hi2) {
                     const int mid = (lo2 + hi2 + 1) >> 1;
-                    if (seg.btile[mid] <= (int)t) lo2 = mid; else hi2 = mid - 1;
+                    if (sh_btile[mid] <= (int)t) lo2 = mid; else hi2 = mid - 1;
                 }
                 sg = lo2;
-                k = (int)t - seg.btile[lo2];
+                k = (int)t - sh_btile[lo2];
                 const int64_t bend = (lo2 + 1 < seg.nb) ? (int64_t)seg.bpos[lo2 + 1] : (int64_t)n;
                 t0 = (int64_t)seg.bpos[lo2] + ((int64_t)k << 12);
                 tn = (int)min64(kSortTile, bend - t0);
@@ -717,7 +722,8 @@ k_sort_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
     // persistent CTAs: tiles are taken by atomic ticket in arrival order, so
     // a tile only ever looks back at tiles that are already being processed
     // (the prefetched ticket is always newer than the one being processed)
-    if (threadIdx.x == 0) claim(0);
+    __syncthreads();                             // sh_btile
+    if (threadIdx.x == 0) claim(0, atomicAdd(ticket, 1u));
     __syncthreads();
     stage(0);
     int cur = 0;
@@ -734,12 +740,12 @@ k_sort_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
     const int tile_n = sh_tn[cur];
     const int seg_k = sh_k[cur];                 // index of the tile inside its segment
     const int seg_id = sh_seg[cur];
-    if (threadIdx.x == 0) claim(cur ^ 1);
+    uint32_t t_next = 0;
+    if (threadIdx.x == 0) t_next = atomicAdd(ticket, 1u);   // consumed after the ranking
     for (int i = threadIdx.x; i < NW * BINS / 2; i += kSortThreads) ((uint32_t*)whist)[i] = 0;
     __syncthreads();
     SS_PT(0);
-    stage(cur ^ 1);
-    cp_async_wait_1();                           // this thread's copies of the current tile have landed
+    cp_async_wait_0();                           // this thread's copies of the current tile have landed
     uint32_t* skey = in_k + cur * kSortTile;     // staged input, then the tile-local sort buffer
     int32_t* sval = in_v + cur * kSortTile;
     if (seg.mode == 1) live = seg.live + (int64_t)seg.lc[seg_id] * seg.G;   // the chunk's kept counts
@@ -788,7 +794,9 @@ k_sort_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
         }
         __syncwarp();
     }
+    if (threadIdx.x == 0) claim(cur ^ 1, t_next);
     __syncthreads();
+    stage(cur ^ 1);                              // next tile's loads overlap the rest of this one
     SS_PT(2);
     // per owned bin: exclusive prefix across warps and the tile total
     uint32_t tot[BPT];
