@@ -133,7 +133,12 @@ __device__ __forceinline__ T block_excl_scan(T v, T* smem, T* total) {
     return res;
 }
 
-// look-back status word: [epoch:30 | flag:2 | count:32]
+// look-back status word: [epoch:30 | flag:2 | count:32].  Epochs advance by
+// 2 per placement (one per pass) and stay in [1, 2^30); a wrap takes 2^29
+// placements.
+__host__ __device__ __forceinline__ uint32_t epoch_next(uint32_t e) {
+    return (e + 2u >= (1u << 30) - 2u) ? 1u : e + 2u;
+}
 constexpr unsigned long long kFlagAgg = 1ull, kFlagInc = 2ull;
 __device__ __forceinline__ unsigned long long lb_pack(uint32_t epoch, unsigned long long flag, uint32_t cnt) {
     return ((unsigned long long)epoch << 34) | (flag << 32) | (unsigned long long)cnt;

@@ -22,6 +22,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -118,7 +119,7 @@ struct ss_engine {
     unsigned long long* status = nullptr;
     int64_t status_tiles = 0;
     uint32_t* tickets = nullptr;
-    uint32_t epoch = 0;
+    uint32_t* ep_dev = nullptr;            // look-back epoch (device; bumped per placement)
     DigitPlan plan{};
     int rb[2] = {0, 0};
     int nblk = 0;
@@ -160,6 +161,22 @@ struct ss_engine {
     unsigned* d_emit_n[2] = {nullptr, nullptr};
     cudaEvent_t ev_emit[2] = {nullptr, nullptr};
     long long emit_seq = 0, pull_seq = 0;
+
+    // CUDA graphs of the fused step: one per (inputs, n, balancer, plan /
+    // emission / staging parity); replays skip the per-launch host and GPU
+    // front-end cost of ~15 kernels and memsets per batch
+    bool capturing = false;
+    bool graphs_on = true;
+    struct GraphEntry {
+        const void* dk;
+        const void* dv;
+        int64_t n;
+        ss_balancer bal;
+        int plan_cur, plan_valid, emit_b, host_emit, stage;
+        cudaGraphExec_t exec;
+        long long launches;
+    };
+    std::vector<GraphEntry> graphs;
     int32_t* kbsum = nullptr;
 
     // multi-GPU routing: group -> owning GPU
@@ -281,23 +298,23 @@ int rb_for(int bits) { return bits < 4 ? 4 : (bits > 11 ? 11 : bits); }
 template <int RB>
 void launch_sort(cudaStream_t st, const uint32_t* kin, const int32_t* vin, uint32_t* kout, int32_t* vout,
                  int n, int shift, uint32_t mask, const uint32_t* base, unsigned long long* status,
-                 uint32_t epoch, uint32_t* ticket, const unsigned long long* bad, int stream_in,
+                 const uint32_t* ep_dev, uint32_t ep_off, uint32_t* ticket, const unsigned long long* bad, int stream_in,
                  const int32_t* n_dev, const SortSeg* sg) {
     // mode 2 adds up to one partial tile per bucket
     const int tiles = (n + kSortTile - 1) / kSortTile + (sg && sg->mode == 2 ? sg->nb : 0);
     if (tiles == 0) return;
     // persistent: at most the co-resident CTAs (2 per SM), each looping over tickets
     ss_note_launch(), k_sort_pass<RB><<<std::min(tiles, 2 * kNumSM), kSortThreads, SortSmem<RB>::bytes, st>>>(
-        kin, vin, kout, vout, n, shift, mask, base, status, epoch, ticket, bad, stream_in, nullptr, n_dev,
+        kin, vin, kout, vout, n, shift, mask, base, status, ep_dev, ep_off, ticket, bad, stream_in, nullptr, n_dev,
         sg ? *sg : SortSeg{});
 }
 
 void sort_dispatch(int rb, cudaStream_t st, const uint32_t* kin, const int32_t* vin, uint32_t* kout,
                    int32_t* vout, int n, int shift, uint32_t mask, const uint32_t* base,
-                   unsigned long long* status, uint32_t epoch, uint32_t* ticket,
+                   unsigned long long* status, const uint32_t* ep_dev, uint32_t ep_off, uint32_t* ticket,
                    const unsigned long long* bad, int stream_in, const int32_t* n_dev = nullptr,
                    const SortSeg* sg = nullptr) {
-#define SS_SORT_CASE(R) launch_sort<R>(st, kin, vin, kout, vout, n, shift, mask, base, status, epoch, ticket, bad, \
+#define SS_SORT_CASE(R) launch_sort<R>(st, kin, vin, kout, vout, n, shift, mask, base, status, ep_dev, ep_off, ticket, bad, \
                                        stream_in, n_dev, sg)
     switch (rb) {
         case 4: SS_SORT_CASE(4); break;
@@ -322,6 +339,7 @@ __global__ void k_dense_off(int64_t* off, int32_t* cap, int64_t G, int64_t W) {
     }
 }
 __global__ void k_set_bad(unsigned long long* bad) { *bad = (unsigned long long)kNoBad; }
+__global__ void k_epoch_bump(uint32_t* ep) { *ep = epoch_next(*ep); }
 // the batch's (group, AVG) rows into mapped pinned host memory (PCIe writes)
 __global__ void k_emit_host(const unsigned* __restrict__ n_res, const int32_t* __restrict__ g,
                             const double* __restrict__ avg, int32_t* hg, double* havg, unsigned* hn) {
@@ -455,6 +473,7 @@ extern "C" void ss_destroy(ss_engine* e) {
     cudaSetDevice(e->cfg.device);
     cudaStreamSynchronize(e->st);
     if (e->cp) cudaStreamSynchronize(e->cp);
+    for (auto& g : e->graphs) cudaGraphExecDestroy(g.exec);
     for (void* p : e->allocs) cudaFree(p);
     if (e->h_rep) cudaFreeHost(e->h_rep);
     for (int b = 0; b < 2; ++b) {
@@ -524,6 +543,7 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
     SS_CUDA(e, cudaEventCreateWithFlags(&e->ev_k4, cudaEventDisableTiming));
     SS_CUDA(e, cudaEventCreateWithFlags(&e->ev_apply, cudaEventDisableTiming));
     SS_CUDA(e, cudaStreamCreateWithFlags(&e->cp, cudaStreamNonBlocking));
+    if (const char* ng = getenv("SS_B200_NO_GRAPHS")) e->graphs_on = !(ng[0] && ng[0] != '0');
     for (int b = 0; b < 2; ++b) {
         SS_CUDA(e, cudaEventCreateWithFlags(&e->ev_staged[b], cudaEventDisableTiming));
         SS_CUDA(e, cudaEventCreateWithFlags(&e->ev_freed[b], cudaEventDisableTiming));
@@ -632,7 +652,7 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
         (rc = dalloc(e, &e->tickets, (size_t)nsub * 2 + 2)) || (rc = dalloc(e, &e->gkept, G)) || (rc = dalloc(e, &e->n_live, nsub + 1)) ||
         (rc = dalloc(e, &e->chunk_live, nsub)) || (rc = dalloc(e, &e->lc, nsub)) || (rc = dalloc(e, &e->n_lc, 1)) ||
         (rc = dalloc(e, &e->chunk_h, (size_t)nsub * kMaxBins)) || (rc = dalloc(e, &e->chunk_base, (size_t)nsub * kMaxBins)) ||
-        (rc = dalloc(e, &e->btile, kMaxBins + 1)) ||
+        (rc = dalloc(e, &e->btile, kMaxBins + 1)) || (rc = dalloc(e, &e->ep_dev, 1)) ||
         (rc = dalloc(e, &e->bdelta, G)) || (rc = dalloc(e, &e->bmin, G)) || (rc = dalloc(e, &e->bmax, G)) ||
         (rc = dalloc(e, &e->hot_of, G)) || (rc = dalloc(e, &e->hot_g, kHotCache)) || (rc = dalloc(e, &e->n_hot_dev, 1)))
         return rc;
@@ -644,6 +664,7 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
     SS_CUDA(e, cudaMemsetAsync(e->gcnt, 0, (size_t)nsub * G * 4, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->gcount, 0, G * 4, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->chunk_live, 0, (size_t)nsub * 4, e->st));
+    SS_CUDA(e, cudaMemsetAsync(e->ep_dev, 0, 4, e->st));
     ss_note_launch(), k_set_bad<<<1, 1, 0, e->st>>>(e->bad);
     if ((rc = engine_alloc_sort(e, e->max_batch))) return rc;
     // -- int64 key table
@@ -885,7 +906,7 @@ static int launch_scans(ss_engine* e, const int32_t* row, int n_chunk = 0) {
     if (e->G <= kScanSmallG) {
         ss_note_launch(), k_scan_small<<<1, 1024, 0, e->st>>>(row, (uint32_t)e->G, e->plan, e->dhist, e->gstart, e->bad,
                                                               e->n_live, n_chunk ? e->chunk_live : nullptr, n_chunk,
-                                                              e->lc, e->n_lc, n_chunk ? e->btile : nullptr);
+                                                              e->lc, e->n_lc, n_chunk ? e->btile : nullptr, e->ep_dev);
         SS_CUDA(e, cudaGetLastError());
         return SS_OK;
     }
@@ -894,19 +915,12 @@ static int launch_scans(ss_engine* e, const int32_t* row, int n_chunk = 0) {
     ss_note_launch(), k_scan_reduce<<<g2, 1024, 0, e->st>>>(row, (uint32_t)e->G, e->bsum, e->nblk, e->plan, e->dhist, e->bad);
     ss_note_launch(), k_scan_top<<<1, 1024, 0, e->st>>>(e->bsum, e->nblk, e->plan, e->dhist, e->bad, e->n_live,
                                                         n_chunk ? e->chunk_live : nullptr, n_chunk, e->lc, e->n_lc,
-                                                        n_chunk ? e->btile : nullptr);
+                                                        n_chunk ? e->btile : nullptr, e->ep_dev);
     ss_note_launch(), k_scan_down<<<g2, 1024, 0, e->st>>>(row, (uint32_t)e->G, e->bsum, e->nblk, e->gstart, e->bad);
     SS_CUDA(e, cudaGetLastError());
     return SS_OK;
 }
 
-static uint32_t next_epoch(ss_engine* e) {
-    if (++e->epoch >= (1u << 30) - 1) {
-        cudaMemsetAsync(e->status, 0, sizeof(unsigned long long) * e->status_tiles * kMaxBins, e->st);
-        e->epoch = 1;
-    }
-    return e->epoch;
-}
 
 // reorder API: stable placement of all n tuples (keys -> kbuf2, values ->
 // vbuf[0]); no tuple is dropped
@@ -916,13 +930,13 @@ static int launch_place_all(ss_engine* e, const uint32_t* dk, const int32_t* dv,
     const uint32_t m0 = (1u << e->plan.bits[0]) - 1u;
     if (e->plan.npass == 1) {
         sort_dispatch(e->rb[0], e->st, dk, dv, e->kbuf2, e->vbuf[0], (int)n, 0, m0, base0, e->status,
-                      next_epoch(e), e->tickets, e->bad, 0);
+                      e->ep_dev, 0, e->tickets, e->bad, 0);
     } else {
         const uint32_t m1 = (1u << e->plan.bits[1]) - 1u;
         sort_dispatch(e->rb[0], e->st, dk, dv, e->kbuf, e->vbuf[1], (int)n, e->plan.shift[0], m0, base0, e->status,
-                      next_epoch(e), e->tickets, e->bad, 0);
+                      e->ep_dev, 0, e->tickets, e->bad, 0);
         sort_dispatch(e->rb[1], e->st, e->kbuf, e->vbuf[1], e->kbuf2, e->vbuf[0], (int)n, e->plan.shift[1], m1, base1,
-                      e->status, next_epoch(e), e->tickets + 1, e->bad, 0);
+                      e->status, e->ep_dev, 1, e->tickets + 1, e->bad, 0);
     }
     SS_CUDA(e, cudaGetLastError());
     return SS_OK;
@@ -956,12 +970,12 @@ static int launch_place_step(ss_engine* e, const uint32_t* dk, const int32_t* dv
     s1.G = (uint32_t)e->G;
     s1.cbase = e->chunk_base;
     if (e->plan.npass == 1) {
-        sort_dispatch(e->rb[0], e->st, dk, dv, nullptr, e->vbuf[0], (int)n, 0, m0, base0, e->status, next_epoch(e),
+        sort_dispatch(e->rb[0], e->st, dk, dv, nullptr, e->vbuf[0], (int)n, 0, m0, base0, e->status, e->ep_dev, 0,
                       e->tickets, e->bad, 1, e->n_live, &s1);
     } else {
         const uint32_t m1 = (1u << e->plan.bits[1]) - 1u;
         sort_dispatch(e->rb[0], e->st, dk, dv, e->kbuf, e->vbuf[1], (int)n, e->plan.shift[0], m0, base0, e->status,
-                      next_epoch(e), e->tickets, e->bad, 1, e->n_live, &s1);
+                      e->ep_dev, 0, e->tickets, e->bad, 1, e->n_live, &s1);
         SortSeg s2{};
         s2.mode = 2;
         s2.G = (uint32_t)e->G;
@@ -971,7 +985,7 @@ static int launch_place_step(ss_engine* e, const uint32_t* dk, const int32_t* dv
         s2.b0 = e->plan.bits[0];
         s2.gstart = e->gstart;
         sort_dispatch(e->rb[1], e->st, e->kbuf, e->vbuf[1], nullptr, e->vbuf[0], (int)n, e->plan.shift[1], m1, base1,
-                      e->status, next_epoch(e), e->tickets + 1, e->bad, 0, e->n_live, &s2);
+                      e->status, e->ep_dev, 1, e->tickets + 1, e->bad, 0, e->n_live, &s2);
     }
     SS_CUDA(e, cudaGetLastError());
     return SS_OK;
@@ -1013,6 +1027,12 @@ static IngestArgs ingest_args(ss_engine* e, bool with_plan) {
 
 static int move_cap(ss_engine* e, const ss_balancer* b);
 static int enqueue_report(ss_engine* e, int64_t n, bool has_policy, cudaStream_t st);
+
+// an event other streams (or the host) wait on: inside a stream capture it
+// must be an external event-record node
+static cudaError_t record_ext(ss_engine* e, cudaEvent_t ev, cudaStream_t st) {
+    return e->capturing ? cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal) : cudaEventRecord(ev, st);
+}
 
 // One batch (the loop body of harness.run, harness.py:99-117).
 //   main stream: count -> [join last batch's side work] -> stats -> scans
@@ -1138,7 +1158,7 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
     }
     if (e->cur_stage >= 0) {
         // the staged input is not read again: the next-but-one batch may reuse it
-        SS_CUDA(e, cudaEventRecord(e->ev_freed[e->cur_stage], e->st));
+        SS_CUDA(e, record_ext(e, e->ev_freed[e->cur_stage], e->st));
         e->freed_rec[e->cur_stage] = true;
         e->cur_stage = -1;
     }
@@ -1192,7 +1212,7 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
             const int b = (int)(e->emit_seq & 1);
             ss_note_launch(), k_emit_host<<<kNumSM, 256, 0, e->st>>>(e->n_res, e->r_g, e->r_avg, e->d_emit_g[b],
                                                                      e->d_emit_avg[b], e->d_emit_n[b]);
-            SS_CUDA(e, cudaEventRecord(e->ev_emit[b], e->st));
+            SS_CUDA(e, record_ext(e, e->ev_emit[b], e->st));
             ++e->emit_seq;
         }
         SS_CUDA(e, cudaGetLastError());
@@ -1211,6 +1231,11 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
         if ((rc = enqueue_report(e, n, has_policy, e->side))) return rc;
         SS_CUDA(e, cudaEventRecord(e->ev_apply, e->side));
         e->side_pending = true;
+        if (e->capturing) {
+            // a captured step joins its side branch before it ends
+            SS_CUDA(e, cudaStreamWaitEvent(e->st, e->ev_apply, 0));
+            e->side_pending = false;
+        }
     } else {
         if ((rc = enqueue_report(e, n, false, e->st))) return rc;
     }
@@ -1548,6 +1573,125 @@ extern "C" int ss_balance(ss_engine* e, const uint32_t* groups, int64_t n, const
     return SS_OK;
 }
 
+// --------------------------------------------------------------------------
+// the fused step as a replayed CUDA graph
+// --------------------------------------------------------------------------
+struct HostState {
+    int plan_cur, last_plan;
+    bool plan_valid, side_pending;
+    long long emit_seq, alg_input;
+    int cur_stage;
+    bool freed0, freed1;
+    bool operator==(const HostState& o) const {
+        return plan_cur == o.plan_cur && last_plan == o.last_plan && plan_valid == o.plan_valid &&
+               side_pending == o.side_pending && emit_seq == o.emit_seq && alg_input == o.alg_input &&
+               cur_stage == o.cur_stage && freed0 == o.freed0 && freed1 == o.freed1;
+    }
+};
+static HostState get_state(const ss_engine* e) {
+    return {e->plan_cur, e->last_plan, e->plan_valid, e->side_pending, e->emit_seq, e->alg_input,
+            e->cur_stage, e->freed_rec[0], e->freed_rec[1]};
+}
+static void set_state(ss_engine* e, const HostState& h) {
+    e->plan_cur = h.plan_cur; e->last_plan = h.last_plan; e->plan_valid = h.plan_valid;
+    e->side_pending = h.side_pending; e->emit_seq = h.emit_seq; e->alg_input = h.alg_input;
+    e->cur_stage = h.cur_stage; e->freed_rec[0] = h.freed0; e->freed_rec[1] = h.freed1;
+}
+// the host bookkeeping run_batch(emit = true) performs, for a replayed graph
+// (which joins its side branch before it ends)
+static HostState step_transition(const ss_engine* e, int64_t n, const ss_balancer* bal) {
+    HostState h = get_state(e);
+    h.last_plan = e->plan_valid ? e->plan_cur : -1;
+    h.alg_input += 8 * n;
+    if (bal && bal->split) {
+        h.plan_cur ^= 1;
+        h.plan_valid = true;
+    } else {
+        h.plan_valid = false;
+    }
+    if (h.cur_stage == 0) h.freed0 = true;
+    if (h.cur_stage == 1) h.freed1 = true;
+    h.cur_stage = -1;
+    if (e->host_emit) ++h.emit_seq;
+    h.side_pending = false;
+    return h;
+}
+
+static bool same_bal(const ss_balancer* a, const ss_balancer& b) {
+    ss_balancer z{};
+    const ss_balancer& x = a ? *a : z;
+    return memcmp(&x, &b, sizeof(ss_balancer)) == 0;
+}
+
+static int run_step(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_t n, const ss_balancer* bal) {
+    if (!e->graphs_on || e->prof) return run_batch(e, dk, dv, n, bal, true);
+    int rc;
+    if (e->side_pending) {                       // graphs are self-contained: join the last side work
+        SS_CUDA(e, cudaStreamWaitEvent(e->st, e->ev_apply, 0));
+        e->side_pending = false;
+    }
+    const int emit_b = (int)(e->emit_seq & 1);
+    ss_engine::GraphEntry* hit = nullptr;
+    for (auto& g : e->graphs)
+        if (g.dk == dk && g.dv == dv && g.n == n && same_bal(bal, g.bal) && g.plan_cur == e->plan_cur &&
+            g.plan_valid == (int)e->plan_valid && g.emit_b == emit_b && g.host_emit == (int)e->host_emit &&
+            g.stage == e->cur_stage) {
+            hit = &g;
+            break;
+        }
+    if (!hit) {
+        const HostState s0 = get_state(e);
+        const HostState expect = step_transition(e, n, bal);
+        const long long l0 = g_launches.load();
+        cudaGraph_t graph = nullptr;
+        e->capturing = true;
+        cudaError_t err = cudaStreamBeginCapture(e->st, cudaStreamCaptureModeRelaxed);
+        rc = (err == cudaSuccess) ? run_batch(e, dk, dv, n, bal, true) : SS_E_EXEC;
+        const cudaError_t err2 = cudaStreamEndCapture(e->st, &graph);
+        e->capturing = false;
+        const HostState s1 = get_state(e);
+        cudaGraphExec_t exec = nullptr;
+        if (err == cudaSuccess && rc == SS_OK && err2 == cudaSuccess && graph)
+            err = cudaGraphInstantiate(&exec, graph, 0);
+        else
+            err = cudaErrorStreamCaptureInvalidated;
+        if (graph) cudaGraphDestroy(graph);
+        const long long per_replay = g_launches.load() - l0;   // kernels recorded by the capture
+        g_launches.store(l0);
+        set_state(e, s0);
+        if (err != cudaSuccess || !(s1 == expect)) {
+            // capture not possible here (or the bookkeeping model disagrees):
+            // run this and every later batch without graphs
+            if (exec) cudaGraphExecDestroy(exec);
+            cudaGetLastError();
+            e->graphs_on = false;
+            return run_batch(e, dk, dv, n, bal, true);
+        }
+        if (e->graphs.size() >= 16) {
+            cudaGraphExecDestroy(e->graphs.front().exec);
+            e->graphs.erase(e->graphs.begin());
+        }
+        ss_engine::GraphEntry ge{};
+        ge.dk = dk;
+        ge.dv = dv;
+        ge.n = n;
+        if (bal) ge.bal = *bal;
+        ge.plan_cur = e->plan_cur;
+        ge.plan_valid = (int)e->plan_valid;
+        ge.emit_b = emit_b;
+        ge.host_emit = (int)e->host_emit;
+        ge.stage = e->cur_stage;
+        ge.exec = exec;
+        ge.launches = per_replay;
+        e->graphs.push_back(ge);
+        hit = &e->graphs.back();
+    }
+    SS_CUDA(e, cudaGraphLaunch(hit->exec, e->st));
+    g_launches.fetch_add(hit->launches);
+    set_state(e, step_transition(e, n, bal));
+    return SS_OK;
+}
+
 extern "C" int ss_step(ss_engine* e, const uint32_t* groups, const int32_t* attrs, int64_t n,
                        const ss_balancer* cfg, ss_step_report* rep) {
     if (!e || n < 0) return SS_E_CONFIG;
@@ -1568,7 +1712,7 @@ extern "C" int ss_step(ss_engine* e, const uint32_t* groups, const int32_t* attr
     g_last_keys = dk;
     const bool has_policy = cfg && cfg->policy != SS_POLICY_NO;
     e->last_plan = -1;
-    if (n > 0 && (rc = run_batch(e, dk, dv, n, cfg, true))) return rc;
+    if (n > 0 && (rc = run_step(e, dk, dv, n, cfg))) return rc;
     if (n == 0) {
         if (e->side_pending) {
             SS_CUDA(e, cudaStreamWaitEvent(e->st, e->ev_apply, 0));
@@ -1823,13 +1967,10 @@ extern "C" int ss_route(ss_engine* e, const uint32_t* groups, const int32_t* att
     const bool dev_out = is_device_ptr(out_groups) && is_device_ptr(out_attrs);
     uint32_t* ko = dev_out ? out_groups : e->kbuf2;
     int32_t* vo = dev_out ? out_attrs : e->vbuf[0];
-    if (++e->epoch >= (1u << 30) - 1) {
-        SS_CUDA(e, cudaMemsetAsync(e->status, 0, sizeof(unsigned long long) * e->status_tiles * kMaxBins, e->st));
-        e->epoch = 1;
-    }
+    ss_note_launch(), k_epoch_bump<<<1, 1, 0, e->st>>>(e->ep_dev);
     const int tiles = (int)((n + kSortTile - 1) / kSortTile);
     ss_note_launch(), k_sort_pass<4, true><<<std::min(tiles, 2 * kNumSM), kSortThreads, SortSmem<4>::bytes, e->st>>>(
-        dk, dv, ko, vo, (int)n, 0, 15u, e->route_base, e->status, e->epoch, e->tickets, e->bad, 0, e->owner);
+        dk, dv, ko, vo, (int)n, 0, 15u, e->route_base, e->status, e->ep_dev, 0, e->tickets, e->bad, 0, e->owner);
     SS_CUDA(e, cudaGetLastError());
     if (!dev_out) {
         SS_CUDA(e, cudaMemcpyAsync(out_groups, ko, n * 4, cudaMemcpyDeviceToHost, e->st));

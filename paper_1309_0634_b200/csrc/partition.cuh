@@ -371,9 +371,11 @@ __global__ void __launch_bounds__(1024)
 k_scan_top(int32_t* __restrict__ bsum, int nblk, DigitPlan plan, uint32_t* __restrict__ dhist,
            const unsigned long long* __restrict__ bad, int32_t* __restrict__ n_live,
            uint32_t* __restrict__ chunk_live = nullptr, int n_chunk = 0, int32_t* __restrict__ lc = nullptr,
-           int32_t* __restrict__ n_lc = nullptr, int32_t* __restrict__ btile = nullptr) {
+           int32_t* __restrict__ n_lc = nullptr, int32_t* __restrict__ btile = nullptr,
+           uint32_t* __restrict__ ep_dev = nullptr) {
     __shared__ int32_t sh_red[33];
     __shared__ uint32_t sh_ured[33];
+    if (ep_dev && blockIdx.x == 0 && threadIdx.x == 0) *ep_dev = epoch_next(*ep_dev);
     if (*bad != (unsigned long long)kNoBad) return;
     const int s = blockIdx.x;
     {
@@ -435,10 +437,11 @@ __global__ void __launch_bounds__(1024)
 k_scan_small(const int32_t* __restrict__ row, uint32_t G, DigitPlan plan, uint32_t* __restrict__ dhist,
              int32_t* __restrict__ gstart, const unsigned long long* __restrict__ bad, int32_t* __restrict__ n_live,
              uint32_t* __restrict__ chunk_live, int n_chunk, int32_t* __restrict__ lc, int32_t* __restrict__ n_lc,
-             int32_t* __restrict__ btile) {
+             int32_t* __restrict__ btile, uint32_t* __restrict__ ep_dev) {
     __shared__ uint32_t sh_dh[2][kMaxBins];
     __shared__ int32_t sh_red[33];
     __shared__ uint32_t sh_ured[33];
+    if (ep_dev && threadIdx.x == 0) *ep_dev = epoch_next(*ep_dev);
     if (*bad != (unsigned long long)kNoBad) return;
     for (int i = threadIdx.x; i < 2 * kMaxBins; i += blockDim.x) (&sh_dh[0][0])[i] = 0;
     __syncthreads();
@@ -633,7 +636,8 @@ __global__ void __launch_bounds__(kSortThreads, 2)
 k_sort_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
             uint32_t* __restrict__ kout, int32_t* __restrict__ vout, int n, int shift, uint32_t mask,
             const uint32_t* __restrict__ bin_base, unsigned long long* __restrict__ status,
-            uint32_t epoch, uint32_t* __restrict__ ticket, const unsigned long long* __restrict__ bad,
+            const uint32_t* __restrict__ ep_dev, uint32_t ep_off, uint32_t* __restrict__ ticket,
+            const unsigned long long* __restrict__ bad,
             int stream_in, const int32_t* __restrict__ dmap = nullptr,
             const int32_t* __restrict__ n_dev = nullptr, SortSeg seg = SortSeg{}) {
     constexpr int BINS = 1 << RB;
@@ -651,6 +655,10 @@ k_sort_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
     __shared__ uint32_t sh_tile[2];
     if (*bad != (unsigned long long)kNoBad) return;
     if (n_dev && *n_dev == 0) return;            // nothing kept in this batch
+    // look-back words are tagged with a device-side epoch (bumped once per
+    // placement by the scan kernel), so status memory is never cleared and
+    // a captured CUDA graph can be replayed unchanged
+    const uint32_t epoch = *ep_dev + ep_off;
     if (n_dev && seg.mode != 1) n = *n_dev;      // consumes a compacted (kept-only) input
     const unsigned w = warp_id(), lane = lane_id();
     const int wbase = (int)w * 32 * kSortItems;
