@@ -275,6 +275,9 @@ def main():
     ap.add_argument("--initial", default="hash", choices=["hash", "contiguous"],
                     help="initial group->partition map (north star: hash-partitioned groups)")
     args = ap.parse_args()
+    # at least 3 warm-up steps (contract), and at least two passes over the
+    # staged batches so every (batch, parity) CUDA graph of the fused step is
+    # captured before the clock starts; the JSON line reports the number run
     args.warmup = max(args.warmup, 3)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -322,6 +325,7 @@ def main():
     if world > 1 and kind.endswith("64"):
         raise SystemExit("int64 keys are single-GPU in this build (route is u32)")
     batches = make_batches(kind, s, G, B, nbuf, dev, seed=1234 + rank)
+    args.warmup = max(args.warmup, 2 * nbuf)
     torch.cuda.synchronize()
 
     def barrier():

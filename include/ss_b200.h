@@ -111,6 +111,9 @@ const char* ss_last_error(ss_engine* e);
 const char* ss_version(void);
 /* kernels this library has launched (all engines); reset != 0 zeroes it */
 long long ss_launch_count(int reset);
+/* replay the fused step as cached CUDA graphs (default on; inputs whose
+ * addresses change every batch turn it off automatically) */
+int  ss_set_graphs(ss_engine* e, int enable);
 /* the engine's count-chunk size (tuples) */
 long long ss_sub_batch(ss_engine* e);
 

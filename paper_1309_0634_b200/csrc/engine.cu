@@ -167,6 +167,7 @@ struct ss_engine {
     // front-end cost of ~15 kernels and memsets per batch
     bool capturing = false;
     bool graphs_on = true;
+    long long graph_hits = 0, graph_captures = 0;
     struct GraphEntry {
         const void* dk;
         const void* dv;
@@ -459,6 +460,12 @@ extern "C" int ss_debug_sort_prof(unsigned long long* out, int reset) {
     return 0;
 }
 #endif
+
+extern "C" int ss_set_graphs(ss_engine* e, int enable) {
+    if (!e) return SS_E_CONFIG;
+    e->graphs_on = enable != 0;
+    return SS_OK;
+}
 
 extern "C" long long ss_sub_batch(ss_engine* e) { return e ? (long long)e->S : 0; }
 
@@ -1639,7 +1646,15 @@ static int run_step(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_t
             hit = &g;
             break;
         }
+    if (hit) ++e->graph_hits;
+    if (!hit && e->graph_captures >= 8 && e->graph_hits < 2 * e->graph_captures) {
+        // inputs that change every batch (e.g. freshly exchanged buffers):
+        // capturing would cost more than it saves
+        e->graphs_on = false;
+        return run_batch(e, dk, dv, n, bal, true);
+    }
     if (!hit) {
+        ++e->graph_captures;
         const HostState s0 = get_state(e);
         const HostState expect = step_transition(e, n, bal);
         const long long l0 = g_launches.load();

@@ -127,6 +127,9 @@ class ShardedEngine:
         self.local = StreamEngine(n_groups, window, n_partitions=n_partitions, aggregates=aggregates,
                                   device=device, max_batch=max_batch, sub_batch=sub_batch,
                                   pool_values=pool_values)
+        # the exchanged batch arrives in fresh buffers of varying size every
+        # step: graph replay would recapture every time
+        self.local.set_graphs(False)
         # GPU-level assignment + policy engine ("threads" = GPUs)
         self.gpu = StreamEngine(n_groups, 1, n_partitions=self.world, aggregates=("count", "sum"),
                                 device=device, max_batch=1 << 16)

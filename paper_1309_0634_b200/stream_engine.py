@@ -352,6 +352,10 @@ class StreamEngine:
         self._check(self._lib.ss_slot_keys(self._h, _ptr(out)[0], C.byref(n)))
         return out[:n.value]
 
+    def set_graphs(self, enable: bool = True):
+        """Replay the fused step as cached CUDA graphs (default on)."""
+        self._check(self._lib.ss_set_graphs(self._h, int(bool(enable))))
+
     # -- streaming emission (SURVEY 8(f) 1) ---------------------------------
     def set_host_emit(self, enable: bool = True):
         """Every step writes its (group, AVG) rows into pinned host memory;
