@@ -898,9 +898,13 @@ static int launch_stats(ss_engine* e, int n_chunk, bool step = false) {
     SS_CUDA(e, cudaMemsetAsync(e->tpt, 0, e->P * 8, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->touched, 0, 8, e->st));
     // many chunks per group: a warp per group (lanes over chunks)
-    auto kern = n_chunk >= 16 ? k_batch_stats<true> : k_batch_stats<false>;
-    const unsigned grid = n_chunk >= 16 ? (unsigned)std::min<int64_t>((e->G + 7) / 8, 32 * kNumSM) : 2 * kNumSM;
-    ss_note_launch(), kern<<<grid, n_chunk >= 16 ? 256 : 1024, e->P * 4, e->st>>>(
+    // many chunks (> 32, hence few groups): a warp per group; otherwise a
+    // thread per group, coalesced over consecutive groups
+    const bool warp = n_chunk > 32;
+    auto kern = warp ? k_batch_stats<true> : k_batch_stats<false>;
+    const unsigned grid = warp ? (unsigned)std::min<int64_t>((e->G + 7) / 8, 32 * kNumSM)
+                               : (unsigned)std::min<int64_t>((e->G + 255) / 256, 16 * kNumSM);
+    ss_note_launch(), kern<<<grid, warp ? 256 : 256, e->P * 4, e->st>>>(
         e->gcnt, n_chunk, (uint32_t)e->G, e->pmap, e->P, e->gcount, step ? e->gkept : nullptr,
         step ? e->chunk_live : nullptr, e->tpt, e->touched, e->bad, e->fill, e->W, e->alg_bytes);
     SS_CUDA(e, cudaGetLastError());

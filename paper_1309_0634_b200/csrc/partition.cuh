@@ -265,7 +265,7 @@ k_batch_stats(int32_t* __restrict__ gcnt, int n_chunk, uint32_t G, const int32_t
                 if (lb[i]) atomicOr(&sh_live[i], lb[i]);
         }
     } else {
-        uint32_t lbits = 0;                      // n_chunk < 32 here
+        uint32_t lbits = 0;                      // n_chunk <= 32 here
         for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < G; g += gridDim.x * blockDim.x) {
             int32_t c = 0;
             for (int s = 0; s < n_chunk; ++s) c += gcnt[(int64_t)s * G + g];
