@@ -80,8 +80,8 @@ k_count(const uint32_t* __restrict__ groups, int64_t n, uint32_t G, int64_t S, i
                     atomicAdd(&sh_hist[h], 1);
                     g = 0xffffffffu;
                 }
-                const unsigned peers = __match_any_sync(SS_FULL, g);
-                if (g != 0xffffffffu && lane == 31u - __clz(peers)) atomicAdd(&dst[g], __popc(peers));
+                // cold keys rarely repeat inside a warp: one reduction per key
+                if (g != 0xffffffffu) atomicAdd(&dst[g], 1);
             }
         }
     }
@@ -344,12 +344,8 @@ k_scan_reduce(const int32_t* __restrict__ gcnt, uint32_t G, int32_t* __restrict_
     for (int d = 0; d < plan.npass; ++d) {
         const uint32_t mask = (1u << plan.bits[d]) - 1u;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const uint32_t dig = ((g0 + q) >> plan.shift[d]) & mask;
-            const unsigned peers = __match_any_sync(SS_FULL, dig);
-            const uint32_t tot = __reduce_add_sync(peers, (uint32_t)c[q]);
-            if (lane_id() == 31u - __clz(peers) && tot) atomicAdd(&sh_dh[d][dig], tot);
-        }
+        for (int q = 0; q < 4; ++q)
+            if (c[q]) atomicAdd(&sh_dh[d][((g0 + q) >> plan.shift[d]) & mask], (uint32_t)c[q]);
     }
     int32_t total;
     block_excl_scan(tsum, sh_red, &total);

@@ -331,8 +331,16 @@ k_ingest(IngestArgs a) {
                 const bool valid = mi[u] >= 0;
                 const long long d = valid ? (long long)v[u] - (long long)old[u] : 0;
                 const unsigned key = valid ? (unsigned)mi[u] : 0xffffffffu;
-                const unsigned peers = __match_any_sync(SS_FULL, key);
-                const unsigned seg_end = 31u - __clz(peers);
+                // members are contiguous lane runs (t grows with the lane), so
+                // the run of a lane comes from one shuffle and one ballot
+                // instead of a MATCH (whose cost grows with distinct values)
+                const unsigned prev = __shfl_up_sync(SS_FULL, key, 1);
+                const unsigned heads = __ballot_sync(SS_FULL, lane == 0 || prev != key);
+                const unsigned le = (lane == 31) ? SS_FULL : ((2u << lane) - 1u);
+                const unsigned start = 31u - __clz(heads & le);
+                const unsigned above = heads & ~le;
+                const unsigned seg_end = above ? (unsigned)(__ffs(above) - 2) : 31u;
+                const unsigned peers = (seg_end == 31u ? SS_FULL : ((2u << seg_end) - 1u)) & ~((1u << start) - 1u);
                 const long long tot = seg_sum(d, seg_end);
                 const bool leader = valid && lane == (unsigned)(__ffs(peers) - 1);
                 if (leader) add_delta(&m_dlo[mi[u]], &m_dhi[mi[u]], tot);
@@ -547,11 +555,15 @@ k_reserve(const int32_t* __restrict__ gcount, uint32_t G, int64_t W, const int32
           int64_t* __restrict__ off, int32_t* __restrict__ cap, unsigned long long* __restrict__ pool_top,
           unsigned long long pool_cap, int* __restrict__ oom, RingCopy* __restrict__ copies,
           unsigned* __restrict__ n_copies, const unsigned long long* __restrict__ bad) {
+    __shared__ long long sh_red[33];
+    __shared__ unsigned long long sh_base;
+    __shared__ unsigned sh_cbase;
+    __shared__ unsigned sh_cred[33];
     if (*bad != (unsigned long long)kNoBad) return;
-    const unsigned lane = lane_id();
-    const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
-    for (uint32_t g0 = (blockIdx.x * (blockDim.x >> 5) + warp_id()) * 32; g0 < G; g0 += nwarps * 32) {
-        const uint32_t g = g0 + lane;
+    // one pool reservation and one copy-list reservation per CTA and round
+    // (a reservation per warp serialises ~G/32 atomics on one address)
+    for (uint32_t g0 = blockIdx.x * blockDim.x; g0 < G; g0 += gridDim.x * blockDim.x) {
+        const uint32_t g = g0 + threadIdx.x;
         int64_t ncap = 0, oldoff = 0;
         int f = 0;
         if (g < G) {
@@ -566,32 +578,35 @@ k_reserve(const int32_t* __restrict__ gcount, uint32_t G, int64_t W, const int32
                 }
             }
         }
-        const int64_t incl = warp_incl_scan(ncap);
-        const int64_t wtot = __shfl_sync(SS_FULL, incl, 31);
-        unsigned long long base = 0;
-        if (lane == 31 && wtot) base = atomicAdd(pool_top, (unsigned long long)wtot);
-        base = __shfl_sync(SS_FULL, base, 31);
+        const unsigned nch = (ncap && f) ? (unsigned)((f + kCopyChunk - 1) / kCopyChunk) : 0u;
+        long long tot;
+        const long long ex = block_excl_scan((long long)ncap, sh_red, &tot);
+        unsigned ctot;
+        const unsigned cex = block_excl_scan(nch, sh_cred, &ctot);
+        if (threadIdx.x == 0) {
+            sh_base = tot ? atomicAdd(pool_top, (unsigned long long)tot) : 0ull;
+            sh_cbase = ctot ? atomicAdd(n_copies, ctot) : 0u;
+        }
+        __syncthreads();
         if (ncap) {
-            const int64_t noff = (int64_t)base + incl - ncap;
+            const int64_t noff = (int64_t)sh_base + ex;
             if ((unsigned long long)(noff + ncap) > pool_cap) {
                 *oom = 1;
             } else {
-                if (f) {
-                    const unsigned nch = (unsigned)((f + kCopyChunk - 1) / kCopyChunk);
-                    const unsigned c0 = atomicAdd(n_copies, nch);
-                    for (unsigned c = 0; c < nch; ++c) {
-                        RingCopy rc;
-                        rc.src = oldoff + (int64_t)c * kCopyChunk;
-                        rc.dst = noff + (int64_t)c * kCopyChunk;
-                        rc.len = min(kCopyChunk, f - (int)c * kCopyChunk);
-                        rc.pad = 0;
-                        copies[c0 + c] = rc;
-                    }
+                const unsigned c0 = sh_cbase + cex;
+                for (unsigned c = 0; c < nch; ++c) {
+                    RingCopy rc;
+                    rc.src = oldoff + (int64_t)c * kCopyChunk;
+                    rc.dst = noff + (int64_t)c * kCopyChunk;
+                    rc.len = min(kCopyChunk, f - (int)c * kCopyChunk);
+                    rc.pad = 0;
+                    copies[c0 + c] = rc;
                 }
                 off[g] = noff;
                 cap[g] = (int32_t)ncap;
             }
         }
+        __syncthreads();
     }
 }
 
