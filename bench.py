@@ -56,6 +56,7 @@ CONFIGS = {
 }
 MIX = 0x9E3779B97F4A7C15 - (1 << 64)     # odd: key = id * MIX (mod 2^64) is a bijection
 P_DEFAULT = 148
+DRIFT_EVERY = 4
 L2_BYTES = 126 * (1 << 20)
 
 
@@ -81,13 +82,16 @@ def make_batches(kind, s, G, B, nbuf, device, seed):
         cdf = torch.cumsum(w, 0)
         cdf /= cdf[-1].clone()
         cdf[-1] = 1.0
+    perm = None
     for i in range(nbuf):
         if kind.startswith("zipf"):
             u = torch.rand(B, dtype=torch.float64, device=device, generator=gen)
             g = torch.searchsorted(cdf, u, right=True).clamp_(max=G - 1)
             if kind == "zipfdrift":
-                # the hot set moves: batch i uses its own seeded relabelling
-                perm = torch.randperm(G, device=device, generator=gen)
+                # the hot set moves every DRIFT_EVERY batches: a new seeded
+                # relabelling of the groups (relabel_groups, datagen.py:181-192)
+                if i % DRIFT_EVERY == 0:
+                    perm = torch.randperm(G, device=device, generator=gen)
                 g = perm[g]
         else:
             g = (torch.arange(B, device=device, dtype=torch.int64) + i * B) % G
@@ -321,7 +325,7 @@ def main():
                            initial=args.initial)
     eng.set_stream(stream)
     bal = eng.balancer_struct(policy, thread_threshold=thr, pot=0.5, split=split)
-    nbuf = 4
+    nbuf = 2 * DRIFT_EVERY if kind == "zipfdrift" else 4
     if world > 1 and kind.endswith("64"):
         raise SystemExit("int64 keys are single-GPU in this build (route is u32)")
     batches = make_batches(kind, s, G, B, nbuf, dev, seed=1234 + rank)

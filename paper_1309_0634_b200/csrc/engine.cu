@@ -204,6 +204,7 @@ struct ss_engine {
     unsigned* n_rescan = nullptr;
     unsigned long long* part_ns = nullptr;
     unsigned long long* loads = nullptr;   // per-partition load incl. split shares
+    long long* fill_loads = nullptr;       // split planner: cold loads of the batch
     DevReport* d_rep = nullptr;
     DevReport* h_rep = nullptr;            // pinned
     unsigned long long* alg_bytes = nullptr;
@@ -731,7 +732,7 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
     if ((rc = dalloc(e, &e->n_res, 1)) || (rc = dalloc(e, &e->r_g, G)) || (rc = dalloc(e, &e->r_cnt, G)) ||
         (rc = dalloc(e, &e->r_sum, G)) || (rc = dalloc(e, &e->r_avg, G)) || (rc = dalloc(e, &e->r_mn, G)) ||
         (rc = dalloc(e, &e->r_mx, G)) || (rc = dalloc(e, &e->rescan, G)) || (rc = dalloc(e, &e->n_rescan, 1)) ||
-        (rc = dalloc(e, &e->part_ns, e->P)) || (rc = dalloc(e, &e->loads, e->P)) || (rc = dalloc(e, &e->d_rep, 1)) ||
+        (rc = dalloc(e, &e->part_ns, e->P)) || (rc = dalloc(e, &e->loads, e->P)) || (rc = dalloc(e, &e->fill_loads, e->P)) || (rc = dalloc(e, &e->d_rep, 1)) ||
         (rc = dalloc(e, &e->part_work, e->P)) ||
         (rc = dalloc(e, &e->alg_bytes, 1)))
         return rc;
@@ -1002,7 +1003,7 @@ static int launch_place_step(ss_engine* e, const uint32_t* dk, const int32_t* dv
     return SS_OK;
 }
 
-static IngestArgs ingest_args(ss_engine* e, bool with_plan) {
+static IngestArgs ingest_args(ss_engine* e, int plan) {
     IngestArgs a{};
     a.order = e->order;
     a.offsets = e->offsets;
@@ -1019,8 +1020,8 @@ static IngestArgs ingest_args(ss_engine* e, bool with_plan) {
     a.bmax = e->bmax;
     a.W = e->W;
     a.minmax = e->minmax;
-    if (with_plan) {
-        const SplitPlan& sp = e->plan_buf[e->plan_cur];
+    if (plan >= 0) {
+        const SplitPlan& sp = e->plan_buf[plan];
         a.split_of = sp.split_of;
         a.share_off = sp.part_soff;
         a.share_grp = sp.share_grp;
@@ -1086,15 +1087,13 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
         SS_CUDA(e, cudaStreamWaitEvent(e->st, e->ev_apply, 0));
         e->side_pending = false;
     }
-    const bool use_plan = e->plan_valid;   // decided by the previous batch
-    e->last_plan = use_plan ? e->plan_cur : -1;
+    // hot-key split: this batch's plan, computed on the side stream from this
+    // batch's counts while the placement runs; the window update waits for it
+    const int plan = split ? (e->plan_cur ^ 1) : -1;
+    e->last_plan = plan;
     {
         ProfScope ps(e, SS_K_STATS, e->st);
         if ((rc = launch_stats(e, n_chunk, true))) return rc;
-        SS_CUDA(e, cudaMemsetAsync(e->loads, 0, e->P * 8, e->st));
-        if (use_plan)
-            ss_note_launch(), k_split_loads<<<2 * kNumSM, 256, e->P * 4, e->st>>>(e->gcount, (uint32_t)e->G, e->pmap, e->P,
-                                                                e->plan_buf[e->plan_cur], e->loads, e->bad);
         if (e->G > 16384) {
             // hot cache for the next batch's count: > 1/(4 kHotCache) of the batch
             SS_CUDA(e, cudaMemsetAsync(e->n_hot_dev, 0, 4, e->st));
@@ -1114,6 +1113,17 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
             const long long hot_min = std::max<long long>(1, n / (2LL * e->P));
             ss_note_launch(), k_split_hot<<<2 * kNumSM, 256, e->P * 4, e->side>>>(e->gcount, (uint32_t)e->G, e->pmap, hot_min, e->maxS,
                                                                 e->spx, e->P, e->bad);
+            // water-fill the hot groups over this batch's cold loads (the
+            // policy's moves apply from the next batch on)
+            const SplitPlan& nx = e->plan_buf[plan];
+            ss_note_launch(), k_u64_to_i64<<<1, 1024, 0, e->side>>>(e->spx.base, e->fill_loads, e->P);
+            const size_t smem = (size_t)e->maxS * 20 + 16 + (size_t)(e->P + 1) * 4;
+            ss_note_launch(), k_split_fill<<<1, 1024, smem, e->side>>>(e->gcount, e->fill_loads, e->P, e->maxS, e->spx, nx, nx,
+                                                                       e->bad);
+            SS_CUDA(e, cudaMemsetAsync(e->loads, 0, e->P * 8, e->side));
+            ss_note_launch(), k_split_loads<<<2 * kNumSM, 256, e->P * 4, e->side>>>(e->gcount, (uint32_t)e->G, e->pmap, e->P,
+                                                                                    nx, e->loads, e->bad);
+            SS_CUDA(e, cudaEventRecord(e->ev_bal, e->side));
         }
         if (has_policy) {
             BalanceArgs a{};
@@ -1144,12 +1154,6 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
             }
             ss_note_launch(), k_balance<<<1, kBalThreads, (size_t)e->P * (8 + 8 * 4), e->side>>>(a);
         }
-        if (split) {
-            const SplitPlan& nx = e->plan_buf[e->plan_cur ^ 1];
-            if (!has_policy) ss_note_launch(), k_u64_to_i64<<<1, 1024, 0, e->side>>>(e->spx.base, e->final_tpt, e->P);
-            const size_t smem = (size_t)e->maxS * 20 + 16 + (size_t)(e->P + 1) * 4;
-            ss_note_launch(), k_split_fill<<<1, 1024, smem, e->side>>>(e->gcount, e->final_tpt, e->P, e->maxS, e->spx, nx, nx, e->bad);
-        }
         SS_CUDA(e, cudaGetLastError());
     }
     {
@@ -1175,7 +1179,8 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
     }
     {
         ProfScope ps(e, SS_K_INGEST, e->st);
-        IngestArgs a = ingest_args(e, use_plan);
+        if (split) SS_CUDA(e, cudaStreamWaitEvent(e->st, e->ev_bal, 0));
+        IngestArgs a = ingest_args(e, plan);
         // one wave: the co-resident CTAs (2 per SM) are shared out over the partitions
         a.cpp = std::max(1, (2 * kNumSM) / e->P);
         ss_note_launch(), k_ingest<<<e->P * a.cpp, kIngestThreads, kIngestSmem, e->st>>>(a);
@@ -1250,12 +1255,8 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
     } else {
         if ((rc = enqueue_report(e, n, false, e->st))) return rc;
     }
-    if (split) {
-        e->plan_cur ^= 1;
-        e->plan_valid = true;
-    } else {
-        e->plan_valid = false;
-    }
+    if (split) e->plan_cur ^= 1;
+    e->plan_valid = split;
     return SS_OK;
 }
 
@@ -1612,14 +1613,11 @@ static void set_state(ss_engine* e, const HostState& h) {
 // (which joins its side branch before it ends)
 static HostState step_transition(const ss_engine* e, int64_t n, const ss_balancer* bal) {
     HostState h = get_state(e);
-    h.last_plan = e->plan_valid ? e->plan_cur : -1;
+    const bool split = bal && bal->split;
+    h.last_plan = split ? (e->plan_cur ^ 1) : -1;
     h.alg_input += 8 * n;
-    if (bal && bal->split) {
-        h.plan_cur ^= 1;
-        h.plan_valid = true;
-    } else {
-        h.plan_valid = false;
-    }
+    if (split) h.plan_cur ^= 1;
+    h.plan_valid = split;
     if (h.cur_stage == 0) h.freed0 = true;
     if (h.cur_stage == 1) h.freed1 = true;
     h.cur_stage = -1;

@@ -80,8 +80,11 @@ k_count(const uint32_t* __restrict__ groups, int64_t n, uint32_t G, int64_t S, i
                     atomicAdd(&sh_hist[h], 1);
                     g = 0xffffffffu;
                 }
-                // cold keys rarely repeat inside a warp: one reduction per key
-                if (g != 0xffffffffu) atomicAdd(&dst[g], 1);
+                // keys outside the hot cache: warp-aggregated (a hot key the
+                // cache missed, e.g. after the skew drifts, still costs one
+                // atomic per warp instead of one per lane)
+                const unsigned peers = __match_any_sync(SS_FULL, g);
+                if (g != 0xffffffffu && lane == 31u - __clz(peers)) atomicAdd(&dst[g], __popc(peers));
             }
         }
     }
