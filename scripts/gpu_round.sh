@@ -8,7 +8,7 @@ nproc > $O/nproc.txt; lscpu > $O/lscpu.txt 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1
 timeout 1200 python -m pytest tests -q -m gpu > $O/gpu_tests.log 2>&1
 timeout 600 python bench.py --steps 20 --warmup 5 > $O/bench_c2.log 2>&1
-for c in c1 c2split c3 c4 c4u; do
+for c in c1 c2split c3 c4 c4u c5; do
   timeout 400 python bench.py --config $c --steps 10 --warmup 3 --no-cpu > $O/bench_$c.log 2>&1
 done
 timeout 400 python bench.py --config c1 --steps 10 --warmup 3 --cpu-seconds 10 > $O/bench_c1_cpu.log 2>&1
