@@ -133,6 +133,25 @@ __device__ __forceinline__ T block_excl_scan(T v, T* smem, T* total) {
     return res;
 }
 
+// block_excl_scan without the trailing barrier: only for a caller whose
+// next use of `smem` is behind another __syncthreads
+template <typename T>
+__device__ __forceinline__ T block_excl_scan_nt(T v, T* smem, T* total) {
+    const unsigned w = warp_id(), l = lane_id(), nw = (blockDim.x + 31) >> 5;
+    T inc = warp_incl_scan(v);
+    if (l == 31) smem[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+        T s = (l < nw) ? smem[l] : T(0);
+        T si = warp_incl_scan(s);
+        if (l < nw) smem[l] = si - s;
+        if (l == nw - 1) smem[32] = si;
+    }
+    __syncthreads();
+    *total = smem[32];
+    return smem[w] + inc - v;
+}
+
 // look-back status word: [epoch:30 | flag:2 | count:32].  Epochs advance by
 // 2 per placement (one per pass) and stay in [1, 2^30); a wrap takes 2^29
 // placements.

@@ -729,7 +729,8 @@ k_sort_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
     // persistent CTAs: tiles are taken by atomic ticket in arrival order, so
     // a tile only ever looks back at tiles that are already being processed
     // (the prefetched ticket is always newer than the one being processed)
-    __syncthreads();                             // sh_btile
+    for (int i = threadIdx.x; i < NW * BINS / 2; i += kSortThreads) ((uint32_t*)whist)[i] = 0;
+    __syncthreads();                             // sh_btile, zeroed histograms
     if (threadIdx.x == 0) claim(0, atomicAdd(ticket, 1u));
     __syncthreads();
     stage(0);
@@ -749,8 +750,7 @@ k_sort_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
     const int seg_id = sh_seg[cur];
     uint32_t t_next = 0;
     if (threadIdx.x == 0) t_next = atomicAdd(ticket, 1u);   // consumed after the ranking
-    for (int i = threadIdx.x; i < NW * BINS / 2; i += kSortThreads) ((uint32_t*)whist)[i] = 0;
-    __syncthreads();
+    // (the warp histograms were zeroed at the end of the previous tile)
     SS_PT(0);
     cp_async_wait_0();                           // this thread's copies of the current tile have landed
     uint32_t* skey = in_k + cur * kSortTile;     // staged input, then the tile-local sort buffer
@@ -828,7 +828,7 @@ k_sort_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
     }
     // tile-local bin starts (bins are owned contiguously, so one block scan)
     uint32_t ttot;
-    uint32_t lex = block_excl_scan(tsum, sh_red, &ttot);
+    uint32_t lex = block_excl_scan_nt(tsum, sh_red, &ttot);   // sh_red is next used after the look-back barrier
 #pragma unroll
     for (int q = 0; q < BPT; ++q) {
         const int b = threadIdx.x * BPT + q;
@@ -894,20 +894,20 @@ k_sort_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
     }
     __syncthreads();
     // contiguous runs per digit to global memory
-    uint32_t tlive;                              // live items of the tile
-    {
-        uint32_t mine = 0;
-#pragma unroll
-        for (int j = 0; j < kSortItems; ++j) mine += (ok >> j) & 1u;
-        block_excl_scan(mine, sh_red, &tlive);
-    }
+    const uint32_t tlive = ttot;                 // live items of the tile
+    // the warp histograms are not read again in this tile: each warp zeroes
+    // its own for the next one (no barrier needed before its next ranking)
+    for (int i = lane; i < BINS / 2; i += 32) ((uint32_t*)myh)[i] = 0;
+    __syncwarp();
     for (int i = threadIdx.x; i < (int)tlive; i += kSortThreads) {
         const uint32_t k = skey[i];
         const uint32_t pos = gbase[MAPPED ? (uint32_t)dmap[k] : ((k >> shift) & mask)] + (uint32_t)i;
         vout[pos] = sval[i];
         if (kout) kout[pos] = k;
     }
-    __syncthreads();                             // smem reused by the next tile
+    // no closing barrier: everything this tile reads (staging buffer, gbase,
+    // tile slots) is rewritten only after the next tile's post-ranking
+    // barrier, which every thread reaches after finishing this tile
     SS_PT(5);
     cur ^= 1;
     }
