@@ -152,6 +152,8 @@ int  ss_last_loads(ss_engine* e, int64_t* loads);
 /* per-partition aggregate-kernel time (ns, summed over sub-batches) of the
  * last step: IterationReport.per_thread_cost (engine.py:395-398) */
 int  ss_last_part_ns(ss_engine* e, int64_t* ns);
+/* values stored by each partition's window update in the last batch */
+int  ss_last_part_work(ss_engine* e, int64_t* work);
 /* moves emitted by the last step */
 int  ss_last_moves(ss_engine* e, ss_move* moves, int64_t cap, int64_t* n);
 

@@ -76,6 +76,7 @@ _SIGS = {
     "ss_last_loads": (C.c_int, [_P, _P]),
     "ss_last_moves": (C.c_int, [_P, _P, _I64, _P]),
     "ss_last_part_ns": (C.c_int, [_P, _P]),
+    "ss_last_part_work": (C.c_int, [_P, C.POINTER(C.c_int64)]),
     "ss_snapshot": (C.c_int, [_P, _P, _P, _P, _P, _P, _P]),
     "ss_export_values": (C.c_int, [_P, _I64, _P, _I64, _P]),
     "ss_results": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _P, _P]),

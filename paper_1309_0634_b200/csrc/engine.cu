@@ -1777,6 +1777,16 @@ extern "C" int ss_last_part_ns(ss_engine* e, int64_t* ns) {
     return SS_OK;
 }
 
+extern "C" int ss_last_part_work(ss_engine* e, int64_t* work) {
+    if (!e || !work) return SS_E_CONFIG;
+    { int jr = join_side(e); if (jr) return jr; }
+    std::vector<unsigned long long> t(e->P);
+    SS_CUDA(e, cudaStreamSynchronize(e->st));
+    SS_CUDA(e, cudaMemcpy(t.data(), e->part_work, e->P * 8, cudaMemcpyDeviceToHost));
+    for (int p = 0; p < e->P; ++p) work[p] = (int64_t)t[p];
+    return SS_OK;
+}
+
 extern "C" int ss_last_moves(ss_engine* e, ss_move* moves, int64_t cap, int64_t* n) {
     if (!e) return SS_E_CONFIG;
     SS_CUDA(e, cudaStreamSynchronize(e->st));

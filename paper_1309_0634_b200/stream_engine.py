@@ -387,6 +387,12 @@ class StreamEngine:
         self._check(self._lib.ss_last_loads(self._h, _ptr(out)[0]))
         return out
 
+    def last_part_work(self) -> np.ndarray:
+        """Values stored by each partition's window update in the last batch."""
+        out = np.empty(self.n_partitions, dtype=np.int64)
+        self._check(self._lib.ss_last_part_work(self._h, out.ctypes.data_as(C.POINTER(C.c_int64))))
+        return out
+
     def last_part_ns(self) -> np.ndarray:
         out = np.empty(self.n_partitions, dtype=np.int64)
         self._check(self._lib.ss_last_part_ns(self._h, _ptr(out)[0]))

@@ -13,10 +13,12 @@ for i in range(8):
     g, a = bs[i % 2]
     rep = eng.step(g, a, bal)
 ns = eng.last_part_ns()
+work = eng.last_part_work()
 g2t, lists = eng.get_lists()
 sizes = np.array([len(l) for l in lists])
 loads = eng.last_loads()
 o = np.argsort(-ns)[:8]
 print(json.dumps({"cfg": name, "ratio": rep.load_ratio, "ns_max": int(ns.max()), "ns_med": int(np.median(ns)),
-                  "top": [[int(p), int(ns[p]), int(sizes[p]), int(loads[p])] for p in o],
+                  "work_max": int(work.max()), "work_med": int(np.median(work)), "work_sum": int(work.sum()),
+                  "top": [[int(p), int(ns[p]), int(sizes[p]), int(loads[p]), int(work[p])] for p in o],
                   "members_max": int(sizes.max()), "members_med": int(np.median(sizes))}))
