@@ -45,7 +45,6 @@ static inline void ss_note_launch() { g_launches.fetch_add(1, std::memory_order_
 namespace {
 
 constexpr int64_t kCountChunk = 16384;
-constexpr int64_t kDefaultSub = int64_t(1) << 21;
 constexpr int64_t kDenseLimitBytes = int64_t(24) << 30;
 
 struct DevReport {            // written by k_report, copied to the host
@@ -108,7 +107,6 @@ struct ss_engine {
     unsigned* n_copies = nullptr;
     int32_t *hot_of = nullptr, *hot_g = nullptr;   // count-kernel hot cache (large G)
     int* n_hot_dev = nullptr;
-    int n_hot = 0;                                 // host copy (read at the report sync)
     bool side_pending = false;             // policy/apply of the last batch still on the side stream
     cudaEvent_t ev_k4 = nullptr, ev_apply = nullptr;
     uint32_t* dhist = nullptr;
@@ -165,6 +163,7 @@ struct ss_engine {
     // CUDA graphs of the fused step: one per (inputs, n, balancer, plan /
     // emission / staging parity); replays skip the per-launch host and GPU
     // front-end cost of ~15 kernels and memsets per batch
+    const uint32_t* last_keys = nullptr;   // the last step's keys (names the bad tuple of a DataError)
     bool capturing = false;
     bool graphs_on = true;
     long long graph_hits = 0, graph_captures = 0;
@@ -521,7 +520,6 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
     ss_engine* e = new ss_engine();
     e->cfg = *cfg;
     e->cfg.reserved = 0;
-    auto bail = [&](int rc) { ss_engine* t = e; *out = nullptr; if (rc != SS_OK) { static std::string keep; keep = t->err; } return rc; };
     if (cfg->n_groups < 1 || cfg->n_groups > (int64_t(1) << 22)) {
         int rc = fail(e, SS_E_CONFIG, "n_groups must be in [1, 2^22]");
         *out = e;
@@ -537,7 +535,6 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
         *out = e;
         return rc;
     }
-    (void)bail;
     *out = e;
     e->G = cfg->n_groups;
     e->W = cfg->window;
@@ -1274,7 +1271,6 @@ static int enqueue_report(ss_engine* e, int64_t n, bool has_policy, cudaStream_t
     return SS_OK;
 }
 
-static const uint32_t* g_last_keys = nullptr;
 
 static int check_report(ss_engine* e, const uint32_t* dk) {
     SS_CUDA(e, cudaStreamSynchronize(e->st));
@@ -1449,12 +1445,6 @@ extern "C" int ss_count(ss_engine* e, const uint32_t* groups, int64_t n, int64_t
     return SS_OK;
 }
 
-static int32_t* g_rank_scratch(ss_engine* e) {
-    static thread_local ss_engine* owner = nullptr;
-    (void)owner;
-    return e->new_order;   // free outside the apply step
-}
-
 extern "C" int ss_reorder(ss_engine* e, const uint32_t* groups, const int32_t* attrs, int64_t n,
                           uint32_t* out_groups, int32_t* out_attrs, int64_t* indicator) {
     if (!e || n < 0) return SS_E_CONFIG;
@@ -1464,7 +1454,7 @@ extern "C" int ss_reorder(ss_engine* e, const uint32_t* groups, const int32_t* a
     int rc;
     if ((rc = stage_input(e, groups, attrs, n, &dk, &dv))) return rc;
     if ((rc = engine_alloc_sort(e, n))) return rc;
-    int32_t* rank = g_rank_scratch(e);
+    int32_t* rank = e->new_order;   // scratch: only the apply kernels use it, inside a step
     ss_note_launch(), k_rank_of<<<2 * kNumSM, 256, 0, e->st>>>(e->order, e->G, rank);
     if (n) ss_note_launch(), k_to_rank<<<2 * kNumSM, 256, 0, e->st>>>(dk, n, rank, (uint32_t)e->G, e->stage_keys, e->bad);
     const uint32_t* rk = e->stage_keys;
@@ -1726,7 +1716,7 @@ extern "C" int ss_step(ss_engine* e, const uint32_t* groups, const int32_t* attr
             (rc = end_stage(e)))
             return rc;
     }
-    g_last_keys = dk;
+    e->last_keys = dk;
     const bool has_policy = cfg && cfg->policy != SS_POLICY_NO;
     e->last_plan = -1;
     if (n > 0 && (rc = run_step(e, dk, dv, n, cfg))) return rc;
@@ -1751,7 +1741,7 @@ extern "C" int ss_step(ss_engine* e, const uint32_t* groups, const int32_t* attr
 
 extern "C" int ss_last_report(ss_engine* e, ss_step_report* rep) {
     if (!e) return SS_E_CONFIG;
-    int rc = check_report(e, g_last_keys);
+    int rc = check_report(e, e->last_keys);
     if (rc) return rc;
     if (rep) fill_report(e, rep);
     return SS_OK;
