@@ -172,6 +172,10 @@ int  ss_results(ss_engine* e, int64_t cap, int32_t* groups, int64_t* count, int6
  * Keys map to dense slots 0..G-1 in order of first appearance in the
  * stream (a device hash table); every other entry point then sees slots. */
 int  ss_map_keys(ss_engine* e, const int64_t* keys, int64_t n, uint32_t* out_slots);
+/* replay ingest: n records of the reference's replay format
+ * (8 bytes: u32 group, i32 attr; datagen.py:29,250-296), host (pinned) or
+ * device (16-byte aligned); otherwise identical to ss_step */
+int  ss_step_records(ss_engine* e, const void* records, int64_t n, const ss_balancer* cfg, ss_step_report* rep);
 int  ss_step_keys64(ss_engine* e, const int64_t* keys, const int32_t* attrs, int64_t n,
                     const ss_balancer* cfg, ss_step_report* rep);
 /* key of every assigned slot (keys[n_slots]) */

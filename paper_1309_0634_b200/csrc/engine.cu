@@ -147,6 +147,7 @@ struct ss_engine {
     uint32_t* skeys[2] = {nullptr, nullptr};
     int32_t* svals[2] = {nullptr, nullptr};
     long long* sk64[2] = {nullptr, nullptr};
+    uint2* srec[2] = {nullptr, nullptr};      // replay records (ss_step_records)
 
     // host emission: each batch's (group, AVG) rows written by a kernel
     // straight into mapped pinned host memory (double-buffered)
@@ -341,6 +342,21 @@ __global__ void k_dense_off(int64_t* off, int32_t* cap, int64_t G, int64_t W) {
 }
 __global__ void k_set_bad(unsigned long long* bad) { *bad = (unsigned long long)kNoBad; }
 __global__ void k_epoch_bump(uint32_t* ep) { *ep = epoch_next(*ep); }
+// replay records (u32 group, i32 attr; datagen.py REPLAY_DTYPE) -> SoA keys / values
+__global__ void k_deinterleave(const uint4* __restrict__ rec, int64_t n, uint32_t* __restrict__ keys,
+                               int32_t* __restrict__ vals) {
+    const int64_t n2 = n / 2;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint4 r = ld_stream_v4(rec + i);
+        reinterpret_cast<uint2*>(keys)[i] = make_uint2(r.x, r.z);
+        reinterpret_cast<int2*>(vals)[i] = make_int2((int)r.y, (int)r.w);
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+        const uint2 last = reinterpret_cast<const uint2*>(rec)[n - 1];
+        keys[n - 1] = last.x;
+        vals[n - 1] = (int32_t)last.y;
+    }
+}
 // the batch's (group, AVG) rows into mapped pinned host memory (PCIe writes)
 __global__ void k_emit_host(const unsigned* __restrict__ n_res, const int32_t* __restrict__ g,
                             const double* __restrict__ avg, int32_t* hg, double* havg, unsigned* hn) {
@@ -1737,6 +1753,34 @@ extern "C" int ss_step(ss_engine* e, const uint32_t* groups, const int32_t* attr
         fill_report(e, rep);
     }
     return SS_OK;
+}
+
+// replay ingest: a batch of 8-byte (u32 group, i32 attr)
+// records -- the reference's replay-file format, datagen.py:29,250-296 --
+// host (pinned: H2D on the copy stream, overlapped) or device; split into
+// the engine's SoA staging buffers on the device, then the fused step
+extern "C" int ss_step_records(ss_engine* e, const void* records, int64_t n, const ss_balancer* cfg,
+                               ss_step_report* rep) {
+    if (!e || n < 0 || (n && !records)) return SS_E_CONFIG;
+    if (e->keys64) return fail(e, SS_E_CONFIG, "replay records carry 32-bit group ids (engine has key_bits = 64)");
+    int rc;
+    if ((rc = check_balancer(e, cfg))) return rc;
+    if (n > e->max_batch) return fail(e, SS_E_CONFIG, "batch larger than max_batch");
+    if ((rc = begin_stage(e, false))) return rc;
+    const int b = e->cur_stage;
+    const uint2* rec = (const uint2*)records;
+    if (n && !is_device_ptr(records)) {
+        if (!e->srec[b] && (rc = dalloc(e, &e->srec[b], e->max_batch + 2))) return rc;
+        SS_CUDA(e, cudaMemcpyAsync(e->srec[b], records, n * 8, cudaMemcpyHostToDevice, e->cp));
+        rec = e->srec[b];
+    }
+    if ((rc = end_stage(e))) return rc;
+    if (n) {
+        if (((uintptr_t)rec & 15) != 0) return fail(e, SS_E_CONFIG, "device records must be 16-byte aligned");
+        ss_note_launch(), k_deinterleave<<<4 * kNumSM, 256, 0, e->st>>>((const uint4*)rec, n, e->skeys[b], e->svals[b]);
+        SS_CUDA(e, cudaGetLastError());
+    }
+    return ss_step(e, e->skeys[b], e->svals[b], n, cfg, rep);
 }
 
 extern "C" int ss_last_report(ss_engine* e, ss_step_report* rep) {

@@ -17,6 +17,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib as L
+from .datagen import REPLAY_DTYPE
 from .errors import DataError, InvalidConfigError
 
 AGG_NAMES = {"count": L.AGG_COUNT, "sum": L.AGG_SUM, "avg": L.AGG_AVG,
@@ -326,6 +327,22 @@ class StreamEngine:
                                       C.byref(rep) if sync else None))
         # host inputs are copied asynchronously: keep the last two alive
         self._keep = (getattr(self, "_keep", (None, None))[-1], (_k1, _k2))
+        return self._report(rep) if sync else None
+
+    def step_records(self, records, balancer=None, sync: bool = True):
+        """One batch given as replay records (datagen.REPLAY_DTYPE: u32 group,
+        i32 attr), host (pinned for overlap) or device; SURVEY 8(f) 3."""
+        if isinstance(records, np.ndarray):
+            rec = np.ascontiguousarray(records)
+            n = len(rec) if rec.dtype == REPLAY_DTYPE else rec.nbytes // 8
+        else:
+            rec = records.contiguous()
+            n = rec.numel() * rec.element_size() // 8
+        pr, _k = _ptr(rec)
+        bal = balancer if balancer is not None else self.balancer_struct()
+        rep = L.StepReport()
+        self._check(self._lib.ss_step_records(self._h, pr, n, C.byref(bal), C.byref(rep) if sync else None))
+        self._keep = (getattr(self, "_keep", (None, None))[-1], (_k,))
         return self._report(rep) if sync else None
 
     def _step64(self, keys, attrs, balancer, sync):

@@ -92,3 +92,32 @@ def test_graph_replay_equals_direct_launches(split):
     assert engs[0].get_lists() [1] == engs[1].get_lists()[1]
     for e in engs:
         e.close()
+
+
+def test_replay_file_ingest_matches_oracle(tmp_path):
+    """a replay file (the reference's 8-byte record format)
+    streamed through pinned double buffers and the device-side record split
+    gives the oracle's per-batch rows and final state."""
+    from paper_1309_0634_b200.replay import ReplayIngest
+    from paper_1309_0634_b200.stream_engine import StreamEngine
+    G, W, P, B = 2500, 400, 16, 90_001            # odd batch: exercises the record tail
+    spec = D.DatasetSpec(D.DatasetKind.ZIPF, 5 * B + 1234, G, 1.1, 44)
+    path = tmp_path / "stream.replay"
+    D.write_replay(D.stream_for(spec), path)
+    eng = StreamEngine(G, W, n_partitions=P, aggregates=("count", "sum", "avg"), max_batch=B)
+    bal = eng.balancer_struct("prob", B // 160, 0.5)
+    rows = {}
+    ri = ReplayIngest(eng, path, B)
+    for _ in ri.batches(bal, on_rows=lambda i, g, a: rows.__setitem__(i, (g.copy(), a.copy()))):
+        pass
+    store = O.OStore(G, W)
+    for i, b in enumerate(D.batches(D.read_replay(path, G), B)):
+        store.ingest(b.groups, b.attrs)
+        g = np.unique(b.groups)
+        pg, pa = rows[i]
+        o = np.argsort(pg)
+        assert np.array_equal(pg[o].astype(np.int64), g)
+        assert np.array_equal(pa[o], store.aggregates()[2][g])
+    s = eng.snapshot()
+    assert np.array_equal(s["fill"], store.fill) and np.array_equal(s["window_sum"], store.window_sum)
+    eng.close()
