@@ -175,6 +175,12 @@ int  ss_map_keys(ss_engine* e, const int64_t* keys, int64_t n, uint32_t* out_slo
 /* replay ingest: n records of the reference's replay format
  * (8 bytes: u32 group, i32 attr; datagen.py:29,250-296), host (pinned) or
  * device (16-byte aligned); otherwise identical to ss_step */
+/* per-tuple trace (AggregateTrace engine.py:125-164): in
+ * trace mode every step keeps all tuples and records, per tuple, its group and
+ * the window sum after it, in grouped-projection order (group ids ascending,
+ * arrival order within a group); ss_trace copies the last batch's records */
+int  ss_set_trace(ss_engine* e, int enable);
+int  ss_trace(ss_engine* e, int64_t cap, int32_t* groups, int64_t* sums, int64_t* n);
 int  ss_step_records(ss_engine* e, const void* records, int64_t n, const ss_balancer* cfg, ss_step_report* rep);
 int  ss_step_keys64(ss_engine* e, const int64_t* keys, const int32_t* attrs, int64_t n,
                     const ss_balancer* cfg, ss_step_report* rep);

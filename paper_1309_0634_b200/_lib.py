@@ -91,6 +91,8 @@ _SIGS = {
     "ss_export_state": (C.c_int, [_P, _P, _I64, _P, _P, _I64, _P]),
     "ss_import_state": (C.c_int, [_P, _P, _I64, _P, _P]),
     "ss_map_keys": (C.c_int, [_P, _P, _I64, _P]),
+    "ss_set_trace": (C.c_int, [_P, C.c_int]),
+    "ss_trace": (C.c_int, [_P, C.c_int64, _P, _P, C.POINTER(C.c_int64)]),
     "ss_step_records": (C.c_int, [_P, _P, C.c_int64, C.POINTER(Balancer), C.POINTER(StepReport)]),
     "ss_step_keys64": (C.c_int, [_P, _P, _P, _I64, C.POINTER(Balancer), C.POINTER(StepReport)]),
     "ss_slot_keys": (C.c_int, [_P, _P, _P]),

@@ -34,6 +34,7 @@
 #include "balance.cuh"
 #include "split.cuh"
 #include "keys.cuh"
+#include "trace.cuh"
 
 using namespace ss;
 
@@ -165,6 +166,11 @@ struct ss_engine {
     // emission / staging parity); replays skip the per-launch host and GPU
     // front-end cost of ~15 kernels and memsets per batch
     const uint32_t* last_keys = nullptr;   // the last step's keys (names the bad tuple of a DataError)
+    // per-tuple trace mode: no dead-tuple dropping, placed
+    // groups kept, trace sums per placed tuple
+    bool trace_on = false;
+    long long* trace_s = nullptr;
+    SegVal* trace_tile = nullptr;
     bool capturing = false;
     bool graphs_on = true;
     long long graph_hits = 0, graph_captures = 0;
@@ -920,7 +926,7 @@ static int launch_stats(ss_engine* e, int n_chunk, bool step = false) {
                                : (unsigned)std::min<int64_t>((e->G + 255) / 256, 16 * kNumSM);
     ss_note_launch(), kern<<<grid, warp ? 256 : 256, e->P * 4, e->st>>>(
         e->gcnt, n_chunk, (uint32_t)e->G, e->pmap, e->P, e->gcount, step ? e->gkept : nullptr,
-        step ? e->chunk_live : nullptr, e->tpt, e->touched, e->bad, e->fill, e->W, e->alg_bytes);
+        step ? e->chunk_live : nullptr, e->tpt, e->touched, e->bad, e->fill, e->W, e->alg_bytes, e->trace_on ? 1 : 0);
     SS_CUDA(e, cudaGetLastError());
     return SS_OK;
 }
@@ -995,7 +1001,8 @@ static int launch_place_step(ss_engine* e, const uint32_t* dk, const int32_t* dv
     s1.G = (uint32_t)e->G;
     s1.cbase = e->chunk_base;
     if (e->plan.npass == 1) {
-        sort_dispatch(e->rb[0], e->st, dk, dv, nullptr, e->vbuf[0], (int)n, 0, m0, base0, e->status, e->ep_dev, 0,
+        sort_dispatch(e->rb[0], e->st, dk, dv, e->trace_on ? e->kbuf2 : nullptr, e->vbuf[0], (int)n, 0, m0, base0,
+                      e->status, e->ep_dev, 0,
                       e->tickets, e->bad, 1, e->n_live, &s1);
     } else {
         const uint32_t m1 = (1u << e->plan.bits[1]) - 1u;
@@ -1009,7 +1016,8 @@ static int launch_place_step(ss_engine* e, const uint32_t* dk, const int32_t* dv
         s2.nb = nb0;
         s2.b0 = e->plan.bits[0];
         s2.gstart = e->gstart;
-        sort_dispatch(e->rb[1], e->st, e->kbuf, e->vbuf[1], nullptr, e->vbuf[0], (int)n, e->plan.shift[1], m1, base1,
+        sort_dispatch(e->rb[1], e->st, e->kbuf, e->vbuf[1], e->trace_on ? e->kbuf2 : nullptr, e->vbuf[0], (int)n,
+                      e->plan.shift[1], m1, base1,
                       e->status, e->ep_dev, 1, e->tickets + 1, e->bad, 0, e->n_live, &s2);
     }
     SS_CUDA(e, cudaGetLastError());
@@ -1183,6 +1191,28 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
     {
         ProfScope ps(e, SS_K_PLACE, e->st);
         if ((rc = launch_place_step(e, dk, dv, n))) return rc;
+    }
+    if (e->trace_on) {
+        // per-tuple trace sums, from the batch-start ring (before the window update)
+        TraceArgs ta{};
+        ta.keys = e->kbuf2;
+        ta.vals = e->vbuf[0];
+        ta.n_dev = e->n_live;
+        ta.gstart = e->gstart;
+        ta.fill = e->fill;
+        ta.next_pos = e->next_pos;
+        ta.wsum = e->wsum;
+        ta.off = e->off;
+        ta.ring = e->ring;
+        ta.W = e->W;
+        ta.out = e->trace_s;
+        ta.tile = e->trace_tile;
+        ta.bad = e->bad;
+        const unsigned tiles = (unsigned)((n + kTraceTile - 1) / kTraceTile);
+        ss_note_launch(), k_trace_local<<<tiles, kTraceTile, 0, e->st>>>(ta);
+        ss_note_launch(), k_trace_tiles<<<1, 1024, 0, e->st>>>(ta);
+        ss_note_launch(), k_trace_apply<<<tiles, kTraceTile, 0, e->st>>>(ta);
+        SS_CUDA(e, cudaGetLastError());
     }
     if (e->cur_stage >= 0) {
         // the staged input is not read again: the next-but-one batch may reuse it
@@ -1639,7 +1669,7 @@ static bool same_bal(const ss_balancer* a, const ss_balancer& b) {
 }
 
 static int run_step(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_t n, const ss_balancer* bal) {
-    if (!e->graphs_on || e->prof) return run_batch(e, dk, dv, n, bal, true);
+    if (!e->graphs_on || e->prof || e->trace_on) return run_batch(e, dk, dv, n, bal, true);
     int rc;
     if (e->side_pending) {                       // graphs are self-contained: join the last side work
         SS_CUDA(e, cudaStreamWaitEvent(e->st, e->ev_apply, 0));
@@ -1781,6 +1811,34 @@ extern "C" int ss_step_records(ss_engine* e, const void* records, int64_t n, con
         SS_CUDA(e, cudaGetLastError());
     }
     return ss_step(e, e->skeys[b], e->svals[b], n, cfg, rep);
+}
+
+extern "C" int ss_set_trace(ss_engine* e, int enable) {
+    if (!e) return SS_E_CONFIG;
+    { int jr = join_side(e); if (jr) return jr; }
+    SS_CUDA(e, cudaStreamSynchronize(e->st));
+    int rc;
+    if (enable && !e->trace_s) {
+        if ((rc = dalloc(e, &e->trace_s, e->max_batch)) ||
+            (rc = dalloc(e, &e->trace_tile, e->max_batch / kTraceTile + 2)))
+            return rc;
+    }
+    e->trace_on = enable != 0;
+    return SS_OK;
+}
+
+extern "C" int ss_trace(ss_engine* e, int64_t cap, int32_t* groups, int64_t* sums, int64_t* n) {
+    if (!e) return SS_E_CONFIG;
+    if (!e->trace_on) return fail(e, SS_E_CONFIG, "trace mode is off (ss_set_trace)");
+    { int jr = join_side(e); if (jr) return jr; }
+    int32_t nl = 0;
+    SS_CUDA(e, cudaMemcpyAsync(&nl, e->n_live, 4, cudaMemcpyDeviceToHost, e->st));
+    SS_CUDA(e, cudaStreamSynchronize(e->st));
+    if (n) *n = nl;
+    const int64_t m = std::min<int64_t>(cap, nl);
+    if (m > 0 && groups) SS_CUDA(e, cudaMemcpy(groups, e->kbuf2, m * 4, cudaMemcpyDeviceToHost));
+    if (m > 0 && sums) SS_CUDA(e, cudaMemcpy(sums, e->trace_s, m * 8, cudaMemcpyDeviceToHost));
+    return SS_OK;
 }
 
 extern "C" int ss_last_report(ss_engine* e, ss_step_report* rep) {

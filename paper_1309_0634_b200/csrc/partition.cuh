@@ -193,7 +193,7 @@ k_batch_stats(int32_t* __restrict__ gcnt, int n_chunk, uint32_t G, const int32_t
               int P, int32_t* __restrict__ gcount, int32_t* __restrict__ gkept, uint32_t* __restrict__ chunk_live,
               unsigned long long* __restrict__ tpt, unsigned long long* __restrict__ touched,
               const unsigned long long* __restrict__ bad, const int32_t* __restrict__ fill, int64_t W,
-              unsigned long long* __restrict__ alg_bytes) {
+              unsigned long long* __restrict__ alg_bytes, int nodrop) {
     extern __shared__ uint32_t sh_tpt[];     // per-CTA partial loads (< 2^31)
     __shared__ uint32_t sh_live[kMaxChunkWords];
     if (*bad != (unsigned long long)kNoBad) return;
@@ -224,7 +224,7 @@ k_batch_stats(int32_t* __restrict__ gcnt, int n_chunk, uint32_t G, const int32_t
             for (int s = RK * 32 + lane; s < n_chunk; s += 32) c += gcnt[(int64_t)s * G + g];
             c = warp_sum(c);
             int32_t kept = c;
-            const bool drop = c > W && gkept;
+            const bool drop = c > W && gkept && !nodrop;
             int32_t carry = 0;
             if (drop) kept = 0;
             for (int s0 = 0; s0 < n_chunk; s0 += 32) {
@@ -274,7 +274,7 @@ k_batch_stats(int32_t* __restrict__ gcnt, int n_chunk, uint32_t G, const int32_t
             for (int s = 0; s < n_chunk; ++s) c += gcnt[(int64_t)s * G + g];
             gcount[g] = c;
             int32_t kept = c;
-            if (c > W && gkept) {
+            if (c > W && gkept && !nodrop) {
                 int32_t pre = 0;
                 kept = 0;
                 for (int s = 0; s < n_chunk; ++s) {

@@ -17,6 +17,45 @@ import numpy as np
 from .errors import ConsistencyError, DataError, InvalidConfigError
 
 
+@dataclass
+class AggregateTrace:
+    """Per-ingest (group, window_sum) pairs (engine.py:125-145).  The CUDA
+    backend records each batch in grouped order (group ids ascending, arrival
+    order within a group), so only per-group projections are meaningful --
+    exactly what the reference compares (grouped_projection)."""
+
+    groups: np.ndarray
+    sums: np.ndarray
+
+    def __len__(self) -> int:
+        return len(self.groups)
+
+    def for_group(self, group: int) -> np.ndarray:
+        return self.sums[self.groups == group]
+
+    def grouped_projection(self) -> tuple[np.ndarray, np.ndarray]:
+        order = np.argsort(self.groups, kind="stable")
+        return self.groups[order], self.sums[order]
+
+
+class TraceBuffer:
+    """Accumulates trace chunks across batches (engine.py:148-164)."""
+
+    def __init__(self) -> None:
+        self._groups: list = []
+        self._sums: list = []
+
+    def append(self, groups, sums) -> None:
+        self._groups.append(np.asarray(groups, dtype=np.int64))
+        self._sums.append(np.asarray(sums, dtype=np.int64))
+
+    def build(self) -> AggregateTrace:
+        if not self._groups:
+            e = np.empty(0, dtype=np.int64)
+            return AggregateTrace(e, e.copy())
+        return AggregateTrace(np.concatenate(self._groups), np.concatenate(self._sums))
+
+
 @dataclass(frozen=True)
 class IterationReport:
     """Execution record of one batch (engine.py:167-176).  On the CUDA
@@ -104,28 +143,67 @@ def ingest_sequence(store: WindowStore, groups, attrs, model=None, *, assume_gro
     per-tuple trace (want_sums) and the simulated cost model (want_costs)
     belong to the reference's CPU backends and are not produced here.
     """
-    if want_sums or want_costs:
-        raise InvalidConfigError("per-tuple sums / costs are not produced by the CUDA backend")
+    if want_costs:
+        raise InvalidConfigError("the simulated cost model belongs to the reference's CPU backends")
     g = np.asarray(groups)
     if len(g) == 0:
-        return None, None
+        return (np.empty(0, dtype=np.int64) if want_sums else None), None
     if assume_grouped:
         starts = np.concatenate(([0], np.flatnonzero(g[1:] != g[:-1]) + 1))
         if g.min() < 0 or g.max() >= store.n_groups:
             raise DataError(f"group id outside [0, {store.n_groups})")
         if len(np.unique(g[starts])) != len(starts):
             raise ConsistencyError("assume_grouped input has a split group run")
-    store.engine.ingest(g, np.asarray(attrs))
-    return None, None
+    if not want_sums:
+        store.engine.ingest(g, np.asarray(attrs))
+        return None, None
+    # per-tuple sums in input order: the device trace is in grouped order
+    # (stable by group), so un-permute with the stable argsort of the groups
+    eng = store.engine
+    eng.set_trace(True)
+    try:
+        eng.ingest(g, np.asarray(attrs))
+        tg, ts = eng.trace()
+    finally:
+        eng.set_trace(False)
+    sums = np.empty(len(g), dtype=np.int64)
+    sums[np.argsort(g, kind="stable")] = ts
+    return sums, None
 
 
 def process_batch_cuda(reordered, store: WindowStore, trace=None) -> IterationReport:
     """CUDA executor for a reordered batch: the slot of process_batch_sim /
     process_batch_parallel (engine.py:299-429)."""
+    eng = store.engine
     if trace is not None:
-        raise InvalidConfigError("per-tuple traces are not produced by the CUDA backend")
-    rep = store.engine.step(np.asarray(reordered.groups), np.asarray(reordered.attrs))
-    ns = store.engine.last_part_ns()
+        eng.set_trace(True)
+    try:
+        rep = eng.step(np.asarray(reordered.groups), np.asarray(reordered.attrs))
+        if trace is not None:
+            trace.append(*eng.trace())
+    finally:
+        if trace is not None:
+            eng.set_trace(False)
+    ns = eng.last_part_ns()
     tpt = np.diff(np.asarray(reordered.indicator))
     return IterationReport(per_thread_cost=ns, makespan=int(ns.max()) if len(ns) else 0,
                            tuples=rep.tuples, imbalance=int(tpt.max() - tpt.min()) if len(tpt) else 0)
+
+
+def serial_reference(stream, window: int, batch_size: int = 1 << 20):
+    """The reference's per-tuple oracle (engine.py:432-445) on the device:
+    the whole stream through the fused step in trace mode.  Returns the
+    final store and the AggregateTrace (compare with grouped_projection;
+    the window state and the per-group projections are batch-independent)."""
+    from .datagen import batches
+    store = WindowStore(stream.n_groups, window, max_batch=batch_size)
+    eng = store.engine
+    buf = TraceBuffer()
+    eng.set_trace(True)
+    try:
+        for b in batches(stream, batch_size):
+            eng.step(b.groups, b.attrs)
+            buf.append(*eng.trace())
+    finally:
+        eng.set_trace(False)
+    return store, buf.build()

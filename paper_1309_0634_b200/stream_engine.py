@@ -369,6 +369,21 @@ class StreamEngine:
         self._check(self._lib.ss_slot_keys(self._h, _ptr(out)[0], C.byref(n)))
         return out[:n.value]
 
+    def set_trace(self, enable: bool = True):
+        """Per-tuple trace mode: every batch keeps all tuples
+        and records (group, window sum after the tuple) per tuple."""
+        self._check(self._lib.ss_set_trace(self._h, int(bool(enable))))
+
+    def trace(self):
+        """The last batch's trace in grouped-projection order (group ids
+        ascending, arrival order within a group): (groups, sums) int64."""
+        n = C.c_int64()
+        self._check(self._lib.ss_trace(self._h, 0, None, None, C.byref(n)))
+        g = np.empty(max(1, n.value), dtype=np.int32)
+        sm = np.empty(max(1, n.value), dtype=np.int64)
+        self._check(self._lib.ss_trace(self._h, n.value, _ptr(g)[0], _ptr(sm)[0], C.byref(n)))
+        return g[:n.value].astype(np.int64), sm[:n.value]
+
     def set_graphs(self, enable: bool = True):
         """Replay the fused step as cached CUDA graphs (default on)."""
         self._check(self._lib.ss_set_graphs(self._h, int(bool(enable))))

@@ -121,3 +121,79 @@ def test_replay_file_ingest_matches_oracle(tmp_path):
     s = eng.snapshot()
     assert np.array_equal(s["fill"], store.fill) and np.array_equal(s["window_sum"], store.window_sum)
     eng.close()
+
+
+def test_device_trace_matches_reference_serial_trace(golden):
+    """the device per-tuple trace equals the reference's
+    serial_reference trace (tests/golden/pipeline.json, produced by the
+    reference) per group, for any batching."""
+    import paper_1309_0634_b200 as ss
+    ser = golden("pipeline.json")["serial"]
+    n, G, s, seed = ser["spec"]
+    W = ser["window"]
+    spec = D.DatasetSpec(D.DatasetKind.ZIPF, n, G, s, seed)
+    groups = np.concatenate([b.groups for b in D.batches(D.stream_for(spec), n)])
+    ref_g = groups[np.argsort(groups, kind="stable")]
+    ref_s = np.asarray(ser["trace_sums"], dtype=np.int64)[np.argsort(groups, kind="stable")]
+    for bsz in (n, 997, 64):
+        store, trace = ss.serial_reference(D.stream_for(spec), W, batch_size=bsz)
+        pg, ps = trace.grouped_projection()
+        assert np.array_equal(pg, ref_g) and np.array_equal(ps, ref_s), bsz
+        assert store.window_sum.tolist() == ser["window_sum"] and store.fill.tolist() == ser["fill"]
+        store.engine.close()
+
+
+@pytest.mark.parametrize("W", [3, 1000])
+def test_trace_and_ingest_sequence_sums(W):
+    """Trace mode on the fused step with evictions from the old window and
+    from the batch itself; ingest_sequence(want_sums) returns them in input
+    order; the windows stay equal to the oracle."""
+    import paper_1309_0634_b200 as ss
+    from paper_1309_0634_b200.stream_engine import StreamEngine
+    G, B = 300, 20_000
+    spec = D.DatasetSpec(D.DatasetKind.ZIPF, 4 * B, G, 1.2, 8)
+    bl = list(D.batches(D.stream_for(spec), B))
+    eng = StreamEngine(G, W, n_partitions=8, max_batch=B)
+    eng.set_trace(True)
+    ref = O.OStore(G, W)
+    for b in bl[:3]:
+        eng.step(b.groups, b.attrs)
+        tg, ts = eng.trace()
+        # oracle per-tuple sums: running window sums per group in arrival order
+        sums = _oracle_sums(ref, b.groups, b.attrs, W)
+        order = np.argsort(b.groups, kind="stable")
+        assert np.array_equal(tg, b.groups[order])
+        assert np.array_equal(ts, sums[order])
+    eng.set_trace(False)
+    store = ss.WindowStore(G, W, n_partitions=8, max_batch=B)
+    b = bl[3]
+    for prev in bl[:3]:
+        ss.ingest_sequence(store, prev.groups, prev.attrs)
+    sums, _ = ss.ingest_sequence(store, b.groups, b.attrs, want_sums=True)
+    assert np.array_equal(sums, _oracle_sums(ref, b.groups, b.attrs, W))
+    s = store.engine.snapshot()
+    assert np.array_equal(s["window_sum"], ref.window_sum) and np.array_equal(s["fill"], ref.fill)
+    store.engine.close()
+    eng.close()
+
+
+def _oracle_sums(store, groups, attrs, W):
+    """Per-tuple window sums (input order) by feeding the oracle tuple runs
+    one at a time per group position -- the reference's per-tuple semantics
+    (engine.py:96-122), vectorised over groups."""
+    out = np.empty(len(groups), dtype=np.int64)
+    order = np.argsort(groups, kind="stable")
+    g_sorted = groups[order]
+    starts = np.concatenate(([0], np.flatnonzero(g_sorted[1:] != g_sorted[:-1]) + 1, [len(groups)]))
+    for a, b in zip(starts[:-1], starts[1:]):
+        g = int(g_sorted[a])
+        old = store.contents(g).astype(np.int64)
+        run = attrs[order[a:b]].astype(np.int64)
+        t = np.concatenate((old, run))
+        c = np.concatenate(([0], np.cumsum(t)))
+        f0 = len(old)
+        idx = f0 + np.arange(1, b - a + 1)
+        lo = np.maximum(0, idx - W)
+        out[order[a:b]] = c[idx] - c[lo]
+    store.ingest(groups, attrs)
+    return out
