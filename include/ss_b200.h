@@ -62,7 +62,8 @@ typedef struct {
     int32_t  n_partitions;  /* P: processing units = aggregate-kernel CTAs           */
     int32_t  key_bits;      /* 32: u32 group ids; 64: int64 keys (ss_step_keys64)     */
     uint32_t agg_mask;      /* SS_AGG_* bits that must be maintained                  */
-    int32_t  scope;         /* 0: per-group window (the reference semantics)          */
+    int32_t  scope;         /* 0: per-group window (the reference semantics);         */
+                            /* 1: the stream's last W tuples, grouped (policy 'no')    */
     int32_t  device;        /* CUDA ordinal                                           */
     int32_t  reserved;
     int64_t  max_batch;     /* largest n passed to ss_step (0: 1<<24)                 */

@@ -35,6 +35,7 @@
 #include "split.cuh"
 #include "keys.cuh"
 #include "trace.cuh"
+#include "streamwin.cuh"
 
 using namespace ss;
 
@@ -166,6 +167,13 @@ struct ss_engine {
     // emission / staging parity); replays skip the per-launch host and GPU
     // front-end cost of ~15 kernels and memsets per batch
     const uint32_t* last_keys = nullptr;   // the last step's keys (names the bad tuple of a DataError)
+    // stream-scope window (scope = 1): ring of the stream's
+    // last W tuples; fill / wsum / mn / mx hold per-group COUNT / SUM / MIN / MAX
+    bool stream_scope = false;
+    uint32_t* sw_k = nullptr;
+    int32_t* sw_v = nullptr;
+    uint8_t* sw_touched = nullptr;
+    int64_t sw_head = 0, sw_fill = 0;
     // per-tuple trace mode: no dead-tuple dropping, placed
     // groups kept, trace sums per placed tuple
     bool trace_on = false;
@@ -592,14 +600,25 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
     SS_CUDA(e, cudaMemsetAsync(e->mx, 0, G * 4, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->oom, 0, 4, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->pool_top, 0, 8, e->st));
-    const int64_t dense_vals = G * W;
-    e->dense = cfg->pool_values == 0 && dense_vals * 4 <= kDenseLimitBytes;
+    e->stream_scope = cfg->scope == 1;
+    if (cfg->scope != 0 && cfg->scope != 1) {
+        *out = e;
+        return fail(e, SS_E_CONFIG, "scope must be 0 (per-group window) or 1 (stream window)");
+    }
+    if (e->stream_scope) {
+        if ((rc = dalloc(e, &e->sw_k, W)) || (rc = dalloc(e, &e->sw_v, W)) || (rc = dalloc(e, &e->sw_touched, G)))
+            return rc;
+        SS_CUDA(e, cudaMemsetAsync(e->sw_touched, 0, G, e->st));
+    }
+    // a stream-scope engine keeps no per-group rings (a token pool)
+    const int64_t dense_vals = e->stream_scope ? 16 : G * W;
+    e->dense = cfg->pool_values == 0 && dense_vals * 4 <= kDenseLimitBytes && !e->stream_scope;
     if (e->dense) {
         e->pool_cap = (unsigned long long)dense_vals;
         if ((rc = dalloc(e, &e->ring, dense_vals))) return rc;
         ss_note_launch(), k_dense_off<<<296, 256, 0, e->st>>>(e->off, e->cap, G, W);
     } else {
-        int64_t pool = cfg->pool_values;
+        int64_t pool = e->stream_scope ? 16 : cfg->pool_values;
         if (pool <= 0) {
             size_t fr = 0, tot = 0;
             cudaMemGetInfo(&fr, &tot);
@@ -1745,6 +1764,79 @@ static int run_step(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_t
     return SS_OK;
 }
 
+// stream-scope window: one batch (see streamwin.cuh)
+__global__ void k_sw_report(const unsigned long long* bad, long long n, const unsigned long long* touched,
+                            const unsigned* n_res, DevReport* rep) {
+    DevReport r{};
+    r.bad = *bad;
+    r.tuples = n;
+    r.touched = (long long)*touched;
+    r.n_res = *n_res;
+    *rep = r;
+}
+
+static int run_stream(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_t n) {
+    const int64_t W = e->W;
+    const int64_t m = std::min<int64_t>(n, W);
+    StreamWinArgs a{};
+    a.keys = dk;
+    a.vals = dv;
+    a.n = n;
+    a.m = m;
+    a.ring_k = e->sw_k;
+    a.ring_v = e->sw_v;
+    a.W = W;
+    a.head = e->sw_head;
+    a.n_evict = std::max<int64_t>(0, e->sw_fill + m - W);
+    a.evict_from = (e->sw_head - e->sw_fill + W) % W;    // the oldest tuple
+    a.fill_after = std::min<int64_t>(W, e->sw_fill + m);
+    a.G = (uint32_t)e->G;
+    a.count = e->fill;
+    a.sum = e->wsum;
+    a.mn = e->mn;
+    a.mx = e->mx;
+    a.touched = e->sw_touched;
+    a.bad = e->bad;
+    SS_CUDA(e, cudaMemsetAsync(e->n_res, 0, 4, e->st));
+    SS_CUDA(e, cudaMemsetAsync(e->touched, 0, 8, e->st));
+    ss_note_launch(), k_sw_check<<<4 * kNumSM, 256, 0, e->st>>>(a);
+    if (a.n_evict) ss_note_launch(), k_sw_evict<<<4 * kNumSM, 256, 0, e->st>>>(a);
+    ss_note_launch(), k_sw_add<<<4 * kNumSM, 256, 0, e->st>>>(a);
+    if (e->minmax) {
+        ss_note_launch(), k_sw_mm_reset<<<2 * kNumSM, 256, 0, e->st>>>(a);
+        ss_note_launch(), k_sw_mm_scan<<<4 * kNumSM, 256, 0, e->st>>>(a);
+    }
+    StreamEmitArgs f{};
+    f.G = (uint32_t)e->G;
+    f.count = e->fill;
+    f.sum = e->wsum;
+    f.mn = e->mn;
+    f.mx = e->mx;
+    f.minmax = e->minmax;
+    f.touched = e->sw_touched;
+    f.n_res = e->n_res;
+    f.r_g = e->r_g;
+    f.r_cnt = e->r_cnt;
+    f.r_sum = e->r_sum;
+    f.r_avg = e->r_avg;
+    f.r_mn = e->r_mn;
+    f.r_mx = e->r_mx;
+    f.touched_total = e->touched;
+    f.bad = e->bad;
+    ss_note_launch(), k_sw_emit<<<2 * kNumSM, 256, 0, e->st>>>(f);
+    ss_note_launch(), k_sw_report<<<1, 1, 0, e->st>>>(e->bad, (long long)n, e->touched, e->n_res, e->d_rep);
+    SS_CUDA(e, cudaMemcpyAsync(e->h_rep, e->d_rep, sizeof(DevReport), cudaMemcpyDeviceToHost, e->st));
+    SS_CUDA(e, cudaGetLastError());
+    if (e->cur_stage >= 0) {
+        SS_CUDA(e, cudaEventRecord(e->ev_freed[e->cur_stage], e->st));
+        e->freed_rec[e->cur_stage] = true;
+        e->cur_stage = -1;
+    }
+    e->sw_head = (e->sw_head + m) % W;
+    e->sw_fill = a.fill_after;
+    return SS_OK;
+}
+
 extern "C" int ss_step(ss_engine* e, const uint32_t* groups, const int32_t* attrs, int64_t n,
                        const ss_balancer* cfg, ss_step_report* rep) {
     if (!e || n < 0) return SS_E_CONFIG;
@@ -1765,6 +1857,19 @@ extern "C" int ss_step(ss_engine* e, const uint32_t* groups, const int32_t* attr
     e->last_keys = dk;
     const bool has_policy = cfg && cfg->policy != SS_POLICY_NO;
     e->last_plan = -1;
+    if (e->stream_scope) {
+        if (cfg && (cfg->policy != SS_POLICY_NO || cfg->split))
+            return fail(e, SS_E_CONFIG, "the balancer works on per-group windows: use policy 'no' with scope 'stream'");
+        if ((rc = run_stream(e, dk, dv, n))) return rc;
+        if (rep) {
+            if ((rc = check_report(e, dk))) {
+                // a bad batch changes nothing: validation runs before any update
+                return rc;
+            }
+            fill_report(e, rep);
+        }
+        return SS_OK;
+    }
     if (n > 0 && (rc = run_step(e, dk, dv, n, cfg))) return rc;
     if (n == 0) {
         if (e->side_pending) {

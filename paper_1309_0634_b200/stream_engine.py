@@ -26,10 +26,12 @@ AGG_NAMES = {"count": L.AGG_COUNT, "sum": L.AGG_SUM, "avg": L.AGG_AVG,
 
 @dataclass(frozen=True)
 class WindowSpec:
-    """Per-group sliding window of the last ``rows`` values.
+    """Sliding window of the last ``rows`` values.
 
-    The reference window is a per-group ring (engine.py:51-70); ``scope``
-    is kept for the stream-wide variant listed as future work.
+    scope='group' (default): each group's last ``rows`` values -- the
+    reference's per-group ring (engine.py:51-70).  scope='stream': the last
+    ``rows`` tuples of the whole stream, grouped (``[ROWS W]``; SURVEY 7.3's
+    D1 alternative, 8(f) 4); COUNT / SUM / AVG / MIN / MAX per group over it.
     """
 
     rows: int
@@ -38,8 +40,8 @@ class WindowSpec:
     def __post_init__(self):
         if self.rows < 1:
             raise InvalidConfigError(f"window must be >= 1, got {self.rows}")
-        if self.scope != "group":
-            raise InvalidConfigError("only scope='group' (the reference semantics) is implemented")
+        if self.scope not in ("group", "stream"):
+            raise InvalidConfigError(f"scope must be 'group' or 'stream', got {self.scope!r}")
 
 
 @dataclass(frozen=True)
@@ -167,12 +169,14 @@ class StreamEngine:
             raise InvalidConfigError(f"n_partitions must be >= 1, got {n_partitions}")
         self.n_groups = int(n_groups)
         self.window = spec.rows
+        self.scope = spec.scope
         self.n_partitions = int(n_partitions)
         self.aggregates = aggs
         self.minmax = bool(aggs.mask & (L.AGG_MIN | L.AGG_MAX))
         cfg = L.Config(n_groups=self.n_groups, window=self.window,
                        n_partitions=self.n_partitions, key_bits=key_bits, agg_mask=aggs.mask,
-                       scope=0, device=device, reserved=0, max_batch=int(max_batch),
+                       scope=1 if spec.scope == "stream" else 0, device=device, reserved=0,
+                       max_batch=int(max_batch),
                        sub_batch=int(sub_batch), pool_values=int(pool_values))
         h = C.c_void_p()
         rc = self._lib.ss_create(C.byref(cfg), C.byref(h))

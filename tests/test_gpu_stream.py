@@ -197,3 +197,38 @@ def _oracle_sums(store, groups, attrs, W):
         out[order[a:b]] = c[idx] - c[lo]
     store.ingest(groups, attrs)
     return out
+
+
+@pytest.mark.parametrize("W,B", [(5000, 2000), (3000, 9000)])
+def test_stream_scope_window(W, B):
+    """scope='stream' -- COUNT / SUM / AVG / MIN / MAX per group
+    over the last W tuples of the whole stream, batch by batch (windows
+    smaller and larger than the batch)."""
+    from paper_1309_0634_b200.stream_engine import StreamEngine, WindowSpec
+    G = 700
+    spec = D.DatasetSpec(D.DatasetKind.ZIPF, 7 * B + 321, G, 1.1, 13)
+    eng = StreamEngine(G, WindowSpec(W, "stream"), n_partitions=8, max_batch=B,
+                       aggregates=("count", "sum", "avg", "min", "max"))
+    seen_g, seen_a = [], []
+    prev_touched = np.zeros(G, dtype=bool)
+    for b in D.batches(D.stream_for(spec), B):
+        rep = eng.step(b.groups, b.attrs)
+        seen_g.append(b.groups)
+        seen_a.append(b.attrs)
+        wg = np.concatenate(seen_g)[-W:]
+        wa = np.concatenate(seen_a)[-W:].astype(np.int64)
+        cnt = np.bincount(wg, minlength=G)
+        sm = np.bincount(wg, weights=wa, minlength=G).astype(np.int64)   # exact: |sum| < 2^53
+        snap = eng.snapshot()
+        assert np.array_equal(snap["fill"], cnt)
+        assert np.array_equal(snap["window_sum"], sm)
+        res = eng.results()
+        for i, g in enumerate(res.groups):
+            assert res.count[i] == cnt[g] and res.sum[i] == sm[g]
+            if cnt[g]:
+                vals = wa[wg == g]
+                assert res.min[i] == vals.min() and res.max[i] == vals.max()
+                assert res.avg[i] == np.float64(sm[g]) / np.float64(cnt[g])
+    with pytest.raises(Exception):
+        eng.step(b.groups, b.attrs, StreamEngine.balancer_struct("prob", 100, 0.5))
+    eng.close()
