@@ -1243,8 +1243,12 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
         ProfScope ps(e, SS_K_INGEST, e->st);
         if (split) SS_CUDA(e, cudaStreamWaitEvent(e->st, e->ev_bal, 0));
         IngestArgs a = ingest_args(e, plan);
-        // one wave: the co-resident CTAs (2 per SM) are shared out over the partitions
-        a.cpp = std::max(1, (2 * kNumSM) / e->P);
+        // CTAs per partition: with hot-key splitting (or no balancer, static
+        // partitions) one resident wave (2 per SM) is best; when the
+        // group-reassignment policy runs alone a few partitions carry several
+        // times the mean, and twice the CTAs per partition (second wave,
+        // partition-minor order) shortens their tail
+        a.cpp = std::max(1, ((split || !has_policy) ? 2 : 4) * kNumSM / e->P);
         ss_note_launch(), k_ingest<<<e->P * a.cpp, kIngestThreads, kIngestSmem, e->st>>>(a);
         SS_CUDA(e, cudaGetLastError());
     }

@@ -120,8 +120,12 @@ k_ingest(IngestArgs a) {
     // partition p is processed by kCtaPerPart CTAs; its members (and split
     // shares) are dealt to them round-robin
     const int kCtaPerPart = a.cpp;
-    const int p = blockIdx.x / kCtaPerPart;
-    const int sub = blockIdx.x % kCtaPerPart;
+    // partition-minor order: the first resident wave holds CTA 0 (and 1) of
+    // every partition, later CTAs of a heavy partition start as light
+    // partitions finish
+    const int P = (int)(gridDim.x / kCtaPerPart);
+    const int p = blockIdx.x % P;
+    const int sub = blockIdx.x / P;
     const int lo = a.offsets[p], hi = a.offsets[p + 1];
     const int s_lo = a.share_off ? a.share_off[p] : 0;
     const int s_hi = a.share_off ? a.share_off[p + 1] : 0;
