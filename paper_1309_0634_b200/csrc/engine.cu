@@ -1246,9 +1246,10 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
         // CTAs per partition: with hot-key splitting (or no balancer, static
         // partitions) one resident wave (2 per SM) is best; when the
         // group-reassignment policy runs alone a few partitions carry several
-        // times the mean, and twice the CTAs per partition (second wave,
-        // partition-minor order) shortens their tail
-        a.cpp = std::max(1, ((split || !has_policy) ? 2 : 4) * kNumSM / e->P);
+        // times the mean, and 4x the CTAs per partition (later waves,
+        // partition-minor order) shortens their tail (measured: 8 CTAs per
+        // partition at P = 148 saturates)
+        a.cpp = std::max(1, ((split || !has_policy) ? 2 : 8) * kNumSM / e->P);
         ss_note_launch(), k_ingest<<<e->P * a.cpp, kIngestThreads, kIngestSmem, e->st>>>(a);
         SS_CUDA(e, cudaGetLastError());
     }
