@@ -97,6 +97,8 @@ struct ss_engine {
     int32_t* stage_vals = nullptr;
     int32_t *gcnt = nullptr, *gstart = nullptr, *gcount = nullptr, *bsum = nullptr;
     int32_t* gkept = nullptr;              // kept (possibly stored) tuples of each group in the batch
+    int32_t* gpre = nullptr;               // [chunk][g] kept-count prefix over chunks (single-pass placement)
+    bool rank_place = false;               // G <= kRankMaxG: k_rank_place instead of the radix passes
     int32_t* n_live = nullptr;             // kept tuples of the batch (device)
     uint32_t* chunk_live = nullptr;        // live-chunk bitmap
     int32_t *lc = nullptr, *n_lc = nullptr;   // ordered live-chunk list
@@ -301,6 +303,22 @@ bool is_device_ptr(const void* p) {
         return false;
     }
     return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+// single-pass placement kernel for keys < 2^bits (ballot matching)
+using RankKernel = void (*)(const uint32_t*, const int32_t*, uint32_t*, int32_t*, int64_t, int, const int32_t*,
+                            const int32_t*, const int32_t*, const int32_t*, uint32_t, const int32_t*,
+                            const unsigned long long*);
+static RankKernel rank_kernel(int bits) {
+    switch (bits) {
+        case 0: case 1: case 2: case 3: case 4: case 5: case 6: case 7: case 8: return k_rank_place<8>;
+        case 9: return k_rank_place<9>;
+        case 10: return k_rank_place<10>;
+        case 11: return k_rank_place<11>;
+        case 12: return k_rank_place<12>;
+        case 13: return k_rank_place<13>;
+        default: return k_rank_place<14>;
+    }
 }
 
 int bits_for(int64_t G) {
@@ -702,6 +720,13 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
         (rc = dalloc(e, &e->bdelta, G)) || (rc = dalloc(e, &e->bmin, G)) || (rc = dalloc(e, &e->bmax, G)) ||
         (rc = dalloc(e, &e->hot_of, G)) || (rc = dalloc(e, &e->hot_g, kHotCache)) || (rc = dalloc(e, &e->n_hot_dev, 1)))
         return rc;
+    // single-pass placement when the cursors fit in shared memory and the
+    // kept set can span the batch (G x W >= batch); with a small kept set
+    // (few live chunks, e.g. C1) one CTA per chunk leaves the GPU idle and
+    // the radix passes over the live chunks are faster
+    e->rank_place = G <= kRankMaxG && G * W >= e->max_batch;
+    if (const char* rp = getenv("SS_B200_RANK_PLACE")) e->rank_place = G <= kRankMaxG && rp[0] != '0';
+    if (e->rank_place && (rc = dalloc(e, &e->gpre, (size_t)nsub * G))) return rc;
     SS_CUDA(e, cudaMemsetAsync(e->hot_of, 0xff, G * 4, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->n_hot_dev, 0, 4, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->bdelta, 0, G * 8, e->st));
@@ -793,6 +818,10 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
     SS_CUDA(e, cudaFuncSetAttribute(k_sort_pass<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)SortSmem<4>::bytes));
     SS_CUDA(e, cudaFuncSetAttribute(k_ingest, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kIngestSmem));
+    for (int b = 0; b <= 14; ++b) {
+        const RankKernel rk = b ? rank_kernel(b) : k_rank_place<0>;
+        SS_CUDA(e, cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rank_smem_bytes(kRankMaxG)));
+    }
     SS_CUDA(e, cudaFuncSetAttribute(k_balance, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     SS_CUDA(e, cudaFuncSetAttribute(k_split_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     SS_CUDA(e, cudaStreamSynchronize(e->st));
@@ -945,7 +974,8 @@ static int launch_stats(ss_engine* e, int n_chunk, bool step = false) {
                                : (unsigned)std::min<int64_t>((e->G + 255) / 256, 16 * kNumSM);
     ss_note_launch(), kern<<<grid, warp ? 256 : 256, e->P * 4, e->st>>>(
         e->gcnt, n_chunk, (uint32_t)e->G, e->pmap, e->P, e->gcount, step ? e->gkept : nullptr,
-        step ? e->chunk_live : nullptr, e->tpt, e->touched, e->bad, e->fill, e->W, e->alg_bytes, e->trace_on ? 1 : 0);
+        step ? e->chunk_live : nullptr, e->tpt, e->touched, e->bad, e->fill, e->W, e->alg_bytes, e->trace_on ? 1 : 0,
+        step && e->rank_place ? e->gpre : nullptr);
     SS_CUDA(e, cudaGetLastError());
     return SS_OK;
 }
@@ -1003,6 +1033,16 @@ static int launch_place_step(ss_engine* e, const uint32_t* dk, const int32_t* dv
     const int n_chunk = (int)std::max<int64_t>(1, (n + e->S - 1) / e->S);
     int cs = 0;
     while ((int64_t(1) << cs) < e->S) ++cs;
+    if (e->rank_place) {
+        // one CTA per live chunk, cursors from the chunk prefix (k_batch_stats)
+        static const int use_match = getenv("SS_B200_RANK_MATCH") ? atoi(getenv("SS_B200_RANK_MATCH")) : 0;
+        auto kern = use_match ? k_rank_place<0> : rank_kernel(bits_for(e->G));
+        ss_note_launch(), kern<<<n_chunk, kRankWarps * 32, rank_smem_bytes((uint32_t)e->G), e->st>>>(
+            dk, dv, e->trace_on ? e->kbuf2 : nullptr, e->vbuf[0], n, cs, e->lc, e->n_lc, e->gpre, e->gstart,
+            (uint32_t)e->G, e->n_live, e->bad);
+        SS_CUDA(e, cudaGetLastError());
+        return SS_OK;
+    }
     // per-live-chunk bin bases of the first pass
     // enough CTAs per chunk that every SM has a slice of ~4K groups or more
     const int slices = (int)std::max<int64_t>(1, std::min<int64_t>((e->G + 4095) / 4096, (2 * kNumSM + n_chunk - 1) / n_chunk));

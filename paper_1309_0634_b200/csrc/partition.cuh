@@ -193,7 +193,7 @@ k_batch_stats(int32_t* __restrict__ gcnt, int n_chunk, uint32_t G, const int32_t
               int P, int32_t* __restrict__ gcount, int32_t* __restrict__ gkept, uint32_t* __restrict__ chunk_live,
               unsigned long long* __restrict__ tpt, unsigned long long* __restrict__ touched,
               const unsigned long long* __restrict__ bad, const int32_t* __restrict__ fill, int64_t W,
-              unsigned long long* __restrict__ alg_bytes, int nodrop) {
+              unsigned long long* __restrict__ alg_bytes, int nodrop, int32_t* __restrict__ gpre = nullptr) {
     extern __shared__ uint32_t sh_tpt[];     // per-CTA partial loads (< 2^31)
     __shared__ uint32_t sh_live[kMaxChunkWords];
     if (*bad != (unsigned long long)kNoBad) return;
@@ -225,7 +225,7 @@ k_batch_stats(int32_t* __restrict__ gcnt, int n_chunk, uint32_t G, const int32_t
             c = warp_sum(c);
             int32_t kept = c;
             const bool drop = c > W && gkept && !nodrop;
-            int32_t carry = 0;
+            int32_t carry = 0, lcarry = 0;
             if (drop) kept = 0;
             for (int s0 = 0; s0 < n_chunk; s0 += 32) {
                 const int s = s0 + (int)lane;
@@ -245,6 +245,13 @@ k_batch_stats(int32_t* __restrict__ gcnt, int n_chunk, uint32_t G, const int32_t
                     }
                     if (live) kept += k;
                     carry += __shfl_sync(SS_FULL, incl, 31);
+                }
+                if (gpre) {
+                    // exclusive prefix of the kept counts over the chunks (-1: not stored)
+                    const int32_t kl = live ? k : 0;
+                    const int32_t il = warp_incl_scan(kl);
+                    if (s < n_chunk) gpre[idx] = live ? lcarry + il - kl : -1;
+                    lcarry += __shfl_sync(SS_FULL, il, 31);
                 }
                 const uint32_t bits = __ballot_sync(SS_FULL, live);
                 if (chunk_live && bits) {
@@ -294,6 +301,15 @@ k_batch_stats(int32_t* __restrict__ gcnt, int n_chunk, uint32_t G, const int32_t
                     if (gcnt[(int64_t)s * G + g]) lbits |= 1u << s;
             }
             if (gkept) gkept[g] = kept;
+            if (gpre) {
+                int32_t pre = 0;
+                for (int s = 0; s < n_chunk; ++s) {
+                    const int64_t idx = (int64_t)s * G + g;
+                    const int32_t k = gcnt[idx];
+                    gpre[idx] = k ? pre : -1;
+                    pre += k;
+                }
+            }
             if (c) stats_account(g, c, pmap, sh_tpt, fill, W, my_touched, my_bytes);
         }
         lbits = __reduce_or_sync(SS_FULL, lbits);
@@ -910,6 +926,144 @@ k_sort_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
     // barrier, which every thread reaches after finishing this tile
     SS_PT(5);
     cur ^= 1;
+    }
+    cp_async_wait_0();
+}
+
+// --------------------------------------------------------------------------
+// Single-pass placement for small group domains (G <= kRankMaxG): the
+// per-group output cursors of one count chunk fit in shared memory, so a
+// chunk's kept tuples are placed by ONE CTA walking the chunk in order --
+// no radix passes, no cross-tile look-back.
+//
+// Cursor of group g in live chunk c: gstart[g] + gpre[c][g], where gpre is
+// the exclusive prefix of g's kept counts over the chunks before c (written
+// by k_batch_stats; -1 marks a never-stored (c, g) run, whose tuples are
+// dropped).  The chunk is cut into sub-tiles of kRankSub tuples dealt
+// round-robin to the warps; each warp ranks its sub-tile with
+// __match_any_sync and advances the shared cursors by one leader atomic per
+// distinct group and round.  The cursor updates are passed from warp to
+// warp in sub-tile order through named barriers (warp w waits on barrier
+// 1 + w, arrived at by the warp holding the previous sub-tile), so every
+// group's tuples get consecutive positions in arrival order; loads (a
+// 3-deep cp.async ring per warp), matching and the scattered stores of the
+// other warps run outside that chain.
+// --------------------------------------------------------------------------
+constexpr int kRankWarps = 16;                     // one named barrier per warp (ids 0..15)
+constexpr int kRankItems = 8;
+constexpr int kRankSub = 32 * kRankItems;          // tuples per sub-tile
+constexpr int kRankStages = 2;
+constexpr int kRankMaxG = 16384;
+
+__host__ __device__ constexpr size_t rank_smem_bytes(uint32_t G) {
+    return (size_t)kRankWarps * kRankStages * kRankSub * 8 + (size_t)G * 4;
+}
+
+// BITS > 0: group matching from BITS ballots (keys < 2^BITS); 0: MATCH
+template <int BITS>
+__global__ void __launch_bounds__(kRankWarps * 32)
+k_rank_place(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin, uint32_t* __restrict__ kout,
+             int32_t* __restrict__ vout, int64_t n, int chunk_shift, const int32_t* __restrict__ lc,
+             const int32_t* __restrict__ n_lc, const int32_t* __restrict__ gpre, const int32_t* __restrict__ gstart,
+             uint32_t G, const int32_t* __restrict__ n_live, const unsigned long long* __restrict__ bad) {
+    extern __shared__ __align__(16) unsigned char rank_sm[];
+    uint32_t* stage_k = (uint32_t*)rank_sm;                            // [warp][stage][kRankSub]
+    int32_t* stage_v = (int32_t*)(stage_k + kRankWarps * kRankStages * kRankSub);
+    uint32_t* cur = (uint32_t*)(stage_v + kRankWarps * kRankStages * kRankSub);   // [G]
+    if (*bad != (unsigned long long)kNoBad) return;
+    if (*n_live == 0) return;
+    if ((int)blockIdx.x >= *n_lc) return;
+    const int64_t c = lc[blockIdx.x];
+    const int32_t* pre = gpre + c * (int64_t)G;
+    for (uint32_t g0 = threadIdx.x; g0 < G; g0 += 4 * blockDim.x) {
+        int32_t p[4], b[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t g = g0 + u * blockDim.x;
+            p[u] = g < G ? pre[g] : -1;
+            b[u] = g < G ? gstart[g] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t g = g0 + u * blockDim.x;
+            if (g < G) cur[g] = p[u] < 0 ? 0x80000000u : (uint32_t)(b[u] + p[u]);
+        }
+    }
+    const int64_t c0 = c << chunk_shift;
+    const int cn = (int)min64((int64_t)1 << chunk_shift, n - c0);
+    const int nsub = (cn + kRankSub - 1) / kRankSub;
+    const int w = (int)warp_id();
+    const unsigned lane = lane_id();
+    uint32_t* my_k = stage_k + w * kRankStages * kRankSub;
+    int32_t* my_v = stage_v + w * kRankStages * kRankSub;
+    // stage sub-tile s of this warp into ring slot q (always commits a group)
+    auto stage = [&](int s, int q) {
+        if (s < nsub) {
+            const int64_t t0 = c0 + (int64_t)s * kRankSub;
+            const int tn = min(kRankSub, cn - s * kRankSub);
+            uint32_t* dk = my_k + q * kRankSub;
+            int32_t* dv = my_v + q * kRankSub;
+            if (tn == kRankSub && (((uintptr_t)(kin + t0) | (uintptr_t)(vin + t0)) & 15) == 0) {
+#pragma unroll
+                for (int i = 0; i < kRankSub / 128; ++i) {
+                    const int li = (i * 32 + (int)lane) * 4;
+                    cp_async16(dk + li, kin + t0 + li);
+                    cp_async16(dv + li, vin + t0 + li);
+                }
+            } else {
+                for (int li = (int)lane; li < tn; li += 32) {
+                    cp_async4(dk + li, kin + t0 + li);
+                    cp_async4(dv + li, vin + t0 + li);
+                }
+            }
+        }
+        cp_async_commit();
+    };
+#pragma unroll
+    for (int q = 0; q < kRankStages; ++q) stage(w + q * kRankWarps, q);
+    __syncthreads();                             // cursors initialised
+    const unsigned lt = lanemask_lt();
+    int q = 0;
+    for (int s = w; s < nsub; s += kRankWarps) {
+        cp_async_wait_n<kRankStages - 1>();
+        __syncwarp();
+        const int tn = min(kRankSub, cn - s * kRankSub);
+        uint32_t key[kRankItems];
+        int32_t val[kRankItems];
+#pragma unroll
+        for (int j = 0; j < kRankItems; ++j) {
+            const int li = j * 32 + (int)lane;
+            key[j] = li < tn ? my_k[q * kRankSub + li] : 0xffffffffu;
+            val[j] = li < tn ? my_v[q * kRankSub + li] : 0;
+        }
+        __syncwarp();                            // slot q is read: refill it
+        stage(s + kRankStages * kRankWarps, q);
+        q = (q + 1 == kRankStages) ? 0 : q + 1;
+        unsigned peers[kRankItems];
+#pragma unroll
+        for (int j = 0; j < kRankItems; ++j)
+            peers[j] = BITS ? match_bits<BITS>(key[j], key[j] != 0xffffffffu) : __match_any_sync(SS_FULL, key[j]);
+        // ---- in sub-tile order across the warps: advance the cursors
+        if (s > 0) named_bar_sync(w, 64);
+        uint32_t old[kRankItems];
+#pragma unroll
+        for (int j = 0; j < kRankItems; ++j) {
+            old[j] = 0;
+            if (key[j] != 0xffffffffu && lane == (unsigned)(__ffs(peers[j]) - 1))
+                old[j] = atomicAdd(&cur[key[j]], (uint32_t)__popc(peers[j]));
+            __syncwarp();
+        }
+        if (s + 1 < nsub) named_bar_arrive((w + 1) % kRankWarps, 64);
+        // ---- scatter
+#pragma unroll
+        for (int j = 0; j < kRankItems; ++j) {
+            const uint32_t base = __shfl_sync(SS_FULL, old[j], __ffs(peers[j]) - 1);
+            const uint32_t pos = base + (uint32_t)__popc(peers[j] & lt);
+            if (key[j] != 0xffffffffu && !(pos & 0x80000000u)) {
+                vout[pos] = val[j];
+                if (kout) kout[pos] = key[j];
+            }
+        }
     }
     cp_async_wait_0();
 }
