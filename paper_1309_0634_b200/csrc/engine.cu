@@ -965,17 +965,21 @@ static int launch_count(ss_engine* e, const uint32_t* dk, int64_t n, int64_t S, 
 static int launch_stats(ss_engine* e, int n_chunk, bool step = false) {
     SS_CUDA(e, cudaMemsetAsync(e->tpt, 0, e->P * 8, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->touched, 0, 8, e->st));
-    // many chunks per group: a warp per group (lanes over chunks)
-    // many chunks (> 32, hence few groups): a warp per group; otherwise a
-    // thread per group, coalesced over consecutive groups
-    const bool warp = n_chunk > 32;
-    auto kern = warp ? k_batch_stats<true> : k_batch_stats<false>;
-    const unsigned grid = warp ? (unsigned)std::min<int64_t>((e->G + 7) / 8, 32 * kNumSM)
-                               : (unsigned)std::min<int64_t>((e->G + 255) / 256, 16 * kNumSM);
-    ss_note_launch(), kern<<<grid, warp ? 256 : 256, e->P * 4, e->st>>>(
-        e->gcnt, n_chunk, (uint32_t)e->G, e->pmap, e->P, e->gcount, step ? e->gkept : nullptr,
-        step ? e->chunk_live : nullptr, e->tpt, e->touched, e->bad, e->fill, e->W, e->alg_bytes, e->trace_on ? 1 : 0,
-        step && e->rank_place ? e->gpre : nullptr);
+    // many chunks (> 32): a CTA per 32 groups, warps over chunk ranges;
+    // otherwise a thread per group, coalesced over consecutive groups
+    if (n_chunk > 32) {
+        const unsigned grid = (unsigned)std::min<int64_t>((e->G + 31) / 32, 8 * kNumSM);
+        ss_note_launch(), k_batch_stats_cols<<<grid, kStatsWarps * 32, e->P * 4, e->st>>>(
+            e->gcnt, n_chunk, (uint32_t)e->G, e->pmap, e->P, e->gcount, step ? e->gkept : nullptr,
+            step ? e->chunk_live : nullptr, e->tpt, e->touched, e->bad, e->fill, e->W, e->alg_bytes, e->trace_on ? 1 : 0,
+            step && e->rank_place ? e->gpre : nullptr);
+    } else {
+        const unsigned grid = (unsigned)std::min<int64_t>((e->G + 255) / 256, 16 * kNumSM);
+        ss_note_launch(), k_batch_stats<false><<<grid, 256, e->P * 4, e->st>>>(
+            e->gcnt, n_chunk, (uint32_t)e->G, e->pmap, e->P, e->gcount, step ? e->gkept : nullptr,
+            step ? e->chunk_live : nullptr, e->tpt, e->touched, e->bad, e->fill, e->W, e->alg_bytes, e->trace_on ? 1 : 0,
+            step && e->rank_place ? e->gpre : nullptr);
+    }
     SS_CUDA(e, cudaGetLastError());
     return SS_OK;
 }

@@ -331,6 +331,113 @@ k_batch_stats(int32_t* __restrict__ gcnt, int n_chunk, uint32_t G, const int32_t
         }
 }
 
+// Many chunks (> 32): one CTA per 32 consecutive groups (lane = group), its
+// warps over contiguous chunk ranges, so every gcnt access is a coalesced
+// 128-byte row segment (a warp per group reading down a column touched 32
+// sectors per request).  Per group: the chunk total and each warp's base
+// (shared memory), the never-stored runs -- a prefix of the group's chunks,
+// ending at the largest inclusive prefix <= K - W -- zeroed, then the kept
+// prefix of every live chunk (gpre, -1 elsewhere) and the live-chunk bits.
+constexpr int kStatsWarps = 8;
+
+__global__ void __launch_bounds__(kStatsWarps * 32)
+k_batch_stats_cols(int32_t* __restrict__ gcnt, int n_chunk, uint32_t G, const int32_t* __restrict__ pmap,
+                   int P, int32_t* __restrict__ gcount, int32_t* __restrict__ gkept,
+                   uint32_t* __restrict__ chunk_live, unsigned long long* __restrict__ tpt,
+                   unsigned long long* __restrict__ touched, const unsigned long long* __restrict__ bad,
+                   const int32_t* __restrict__ fill, int64_t W, unsigned long long* __restrict__ alg_bytes,
+                   int nodrop, int32_t* __restrict__ gpre) {
+    extern __shared__ uint32_t sh_tpt[];     // per-CTA partial loads (< 2^31)
+    __shared__ uint32_t sh_live[kMaxChunkWords];
+    __shared__ int32_t sh_part[kStatsWarps][32];
+    __shared__ int32_t sh_dead[kStatsWarps][32];
+    if (*bad != (unsigned long long)kNoBad) return;
+    const int nwords = (n_chunk + 31) >> 5;
+    for (int p = threadIdx.x; p < P; p += blockDim.x) sh_tpt[p] = 0;
+    for (int i = threadIdx.x; i < nwords; i += blockDim.x) sh_live[i] = 0;
+    const unsigned lane = lane_id(), w = warp_id();
+    const int R = (n_chunk + kStatsWarps - 1) / kStatsWarps;
+    const int c_lo = min(n_chunk, (int)w * R), c_hi = min(n_chunk, c_lo + R);
+    uint32_t my_touched = 0;
+    unsigned long long my_bytes = 0;
+    for (uint32_t g0 = blockIdx.x * 32; g0 < G; g0 += gridDim.x * 32) {
+        const uint32_t g = g0 + lane;
+        const bool gv = g < G;
+        const int32_t* col = gcnt + g;
+        int32_t part = 0;
+        if (gv) {
+            int c = c_lo;
+            for (; c + 8 <= c_hi; c += 8) {
+                int32_t v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = col[(int64_t)(c + u) * G];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) part += v[u];
+            }
+            for (; c < c_hi; ++c) part += col[(int64_t)c * G];
+        }
+        sh_part[w][lane] = part;
+        __syncthreads();
+        int32_t C = 0, base = 0;
+#pragma unroll
+        for (int i = 0; i < kStatsWarps; ++i) {
+            const int32_t v = sh_part[i][lane];
+            base += (i < (int)w) ? v : 0;
+            C += v;
+        }
+        const bool drop = gv && C > W && gkept && !nodrop;
+        int32_t dmax = 0;
+        if (drop) {
+            int32_t pre = base;
+            for (int c = c_lo; c < c_hi; ++c) {
+                const int64_t idx = (int64_t)c * G + g;
+                const int32_t k = gcnt[idx];
+                if (k && (int64_t)pre + k <= (int64_t)C - W) {
+                    gcnt[idx] = 0;
+                    dmax = pre + k;
+                }
+                pre += k;
+            }
+        }
+        sh_dead[w][lane] = dmax;
+        __syncthreads();
+        int32_t D = 0;
+#pragma unroll
+        for (int i = 0; i < kStatsWarps; ++i) D = max(D, sh_dead[i][lane]);
+        // kept prefix: the never-stored runs all precede every live one
+        int32_t pre = base - min(D, base);
+        for (int c = c_lo; c < c_hi; ++c) {
+            const int64_t idx = (int64_t)c * G + g;
+            const int32_t k = gv ? gcnt[idx] : 0;
+            const bool live = k != 0;
+            if (gpre && gv) gpre[idx] = live ? pre : -1;
+            pre += k;
+            const uint32_t bits = __ballot_sync(SS_FULL, live);
+            if (chunk_live && bits && lane == 0) atomicOr(&sh_live[c >> 5], 1u << (c & 31));
+        }
+        if (w == 0 && gv) {
+            gcount[g] = C;
+            if (gkept) gkept[g] = C - D;
+            if (C) stats_account(g, C, pmap, sh_tpt, fill, W, my_touched, my_bytes);
+        }
+        __syncthreads();                         // sh_part / sh_dead reused
+    }
+    my_touched = warp_sum(my_touched);
+    my_bytes = warp_sum(my_bytes);
+    if (lane == 0 && my_touched) {
+        atomicAdd(touched, (unsigned long long)my_touched);
+        atomicAdd(alg_bytes, my_bytes);
+    }
+    __syncthreads();
+    for (int p = threadIdx.x; p < P; p += blockDim.x)
+        if (sh_tpt[p]) atomicAdd(&tpt[p], (unsigned long long)sh_tpt[p]);
+    if (chunk_live)
+        for (int i = threadIdx.x; i < nwords; i += blockDim.x) {
+            const uint32_t v = sh_live[i];
+            if (v && (chunk_live[i] & v) != v) atomicOr(&chunk_live[i], v);
+        }
+}
+
 // --------------------------------------------------------------------------
 // G-sized exclusive scan of the per-sub-batch group histograms -> run
 // starts gstart[s][g], plus the radix digit histograms of every pass.
@@ -954,6 +1061,13 @@ constexpr int kRankItems = 8;
 constexpr int kRankSub = 32 * kRankItems;          // tuples per sub-tile
 constexpr int kRankStages = 2;
 constexpr int kRankMaxG = 16384;
+#ifndef SS_RANK_BALLOT
+#define SS_RANK_BALLOT 1
+#endif
+// of every 2 rounds, how many match keys by ballots (ALU) -- the rest use
+// MATCH (MIO pipe), so both pipes share the ranking (measured at C2: 142 us
+// against 162 all-ballot and 168 all-MATCH)
+constexpr int kRankBallot = SS_RANK_BALLOT;
 
 __host__ __device__ constexpr size_t rank_smem_bytes(uint32_t G) {
     return (size_t)kRankWarps * kRankStages * kRankSub * 8 + (size_t)G * 4;
@@ -1042,22 +1156,34 @@ k_rank_place(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin, 
         unsigned peers[kRankItems];
 #pragma unroll
         for (int j = 0; j < kRankItems; ++j)
-            peers[j] = BITS ? match_bits<BITS>(key[j], key[j] != 0xffffffffu) : __match_any_sync(SS_FULL, key[j]);
-        // ---- in sub-tile order across the warps: advance the cursors
-        if (s > 0) named_bar_sync(w, 64);
-        uint32_t old[kRankItems];
+            peers[j] = (BITS && (j & 1) < kRankBallot) ? match_bits<BITS>(key[j], key[j] != 0xffffffffu)
+                                                        : __match_any_sync(SS_FULL, key[j]);
+        // leader (lowest peer) of each item's group in its round, the
+        // round's count for the leader (0 elsewhere) and the cursor address,
+        // all ready before the ordered section
+        uint32_t lead[kRankItems], cnt[kRankItems], addr[kRankItems], old[kRankItems];
 #pragma unroll
         for (int j = 0; j < kRankItems; ++j) {
+            lead[j] = (uint32_t)(__ffs(peers[j]) - 1);
+            cnt[j] = (key[j] != 0xffffffffu && lane == lead[j]) ? (uint32_t)__popc(peers[j]) : 0u;
+            addr[j] = (uint32_t)__cvta_generic_to_shared(cur + (key[j] & 0x7fffffffu) % G);
             old[j] = 0;
-            if (key[j] != 0xffffffffu && lane == (unsigned)(__ffs(peers[j]) - 1))
-                old[j] = atomicAdd(&cur[key[j]], (uint32_t)__popc(peers[j]));
+            asm volatile("" :: "r"(cnt[j]), "r"(addr[j]));
+        }
+        // ---- in sub-tile order across the warps: advance the cursors with
+        // predicated shared atomics (no divergence inside the section)
+        if (s > 0) named_bar_sync(w, 64);
+#pragma unroll
+        for (int j = 0; j < kRankItems; ++j) {
+            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p atom.shared.add.u32 %0, [%1], %2;\n\t}"
+                         : "+r"(old[j]) : "r"(addr[j]), "r"(cnt[j]) : "memory");
             __syncwarp();
         }
         if (s + 1 < nsub) named_bar_arrive((w + 1) % kRankWarps, 64);
         // ---- scatter
 #pragma unroll
         for (int j = 0; j < kRankItems; ++j) {
-            const uint32_t base = __shfl_sync(SS_FULL, old[j], __ffs(peers[j]) - 1);
+            const uint32_t base = __shfl_sync(SS_FULL, old[j], lead[j]);
             const uint32_t pos = base + (uint32_t)__popc(peers[j] & lt);
             if (key[j] != 0xffffffffu && !(pos & 0x80000000u)) {
                 vout[pos] = val[j];

@@ -41,7 +41,7 @@ for c in ["c2", "c1"]:
             i = h.index(m)
             return float(r[i].replace(",", "")) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u[i], 1)
         b = val("dram__bytes_read.sum") + val("dram__bytes_write.sum")
-        for k, v in {"k_sort_pass": "place", "k_ingest": "ingest", "k_count": "count"}.items():
+        for k, v in {"k_sort_pass": "place", "k_rank_place": "place", "k_ingest": "ingest", "k_count": "count"}.items():
             if k in name:
                 d.setdefault(v, []).append(b)
     traffic[c] = {k: {"bytes_per_launch": sum(v) / len(v), "launches_captured": len(v)} for k, v in d.items()}
