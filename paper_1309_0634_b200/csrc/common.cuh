@@ -85,6 +85,18 @@ __device__ __forceinline__ void named_bar_arrive(int id, int nthreads) {
     asm volatile("bar.arrive %0, %1;" :: "r"(id), "r"(nthreads) : "memory");
 }
 
+// match_bits for a full warp of valid values
+template <int BITS>
+__device__ __forceinline__ unsigned match_bits_all(uint32_t v) {
+    unsigned m = 0xffffffffu;
+#pragma unroll
+    for (int b = 0; b < BITS; ++b) {
+        const unsigned bb = __ballot_sync(SS_FULL, v & (1u << b));
+        m &= (v & (1u << b)) ? bb : ~bb;
+    }
+    return m;
+}
+
 // __match_any_sync for a BITS-bit value built from BITS ballots (plus one
 // for the valid flag): fixed cost, where the MATCH instruction's cost grows
 // with the number of distinct values in the warp

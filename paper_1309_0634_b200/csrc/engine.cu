@@ -988,9 +988,14 @@ static int launch_stats(ss_engine* e, int n_chunk, bool step = false) {
 // of every placement pass; with n_chunk > 0 also the live-chunk list
 static int launch_scans(ss_engine* e, const int32_t* row, int n_chunk = 0) {
     if (e->G <= kScanSmallG) {
-        ss_note_launch(), k_scan_small<<<1, 1024, 0, e->st>>>(row, (uint32_t)e->G, e->plan, e->dhist, e->gstart, e->bad,
+        // the single-pass placement needs no digit bases or bucket tiles
+        DigitPlan plan = e->plan;
+        const bool rank = n_chunk && e->rank_place;
+        if (rank) plan.npass = 0;
+        ss_note_launch(), k_scan_small<<<1, 1024, 0, e->st>>>(row, (uint32_t)e->G, plan, e->dhist, e->gstart, e->bad,
                                                               e->n_live, n_chunk ? e->chunk_live : nullptr, n_chunk,
-                                                              e->lc, e->n_lc, n_chunk ? e->btile : nullptr, e->ep_dev);
+                                                              e->lc, e->n_lc, n_chunk && !rank ? e->btile : nullptr,
+                                                              e->ep_dev);
         SS_CUDA(e, cudaGetLastError());
         return SS_OK;
     }

@@ -17,6 +17,8 @@
 // group as (position - group start), which is all the window update needs.
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace ss {
@@ -1137,41 +1139,43 @@ k_rank_place(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin, 
     for (int q = 0; q < kRankStages; ++q) stage(w + q * kRankWarps, q);
     __syncthreads();                             // cursors initialised
     const unsigned lt = lanemask_lt();
-    int q = 0;
-    for (int s = w; s < nsub; s += kRankWarps) {
-        cp_async_wait_n<kRankStages - 1>();
-        __syncwarp();
-        const int tn = min(kRankSub, cn - s * kRankSub);
+    const uint32_t cur_sa = (uint32_t)__cvta_generic_to_shared(cur);
+    // one sub-tile; FULL: all kRankSub tuples present (every sub-tile but
+    // the batch's last), so no validity tests
+    auto sub_tile = [&](auto full_c, int s, int q, int tn) {
+        constexpr bool FULL = decltype(full_c)::value;
         uint32_t key[kRankItems];
         int32_t val[kRankItems];
 #pragma unroll
         for (int j = 0; j < kRankItems; ++j) {
             const int li = j * 32 + (int)lane;
-            key[j] = li < tn ? my_k[q * kRankSub + li] : 0xffffffffu;
-            val[j] = li < tn ? my_v[q * kRankSub + li] : 0;
+            key[j] = (FULL || li < tn) ? my_k[q * kRankSub + li] : 0xffffffffu;
+            val[j] = (FULL || li < tn) ? my_v[q * kRankSub + li] : 0;
         }
         __syncwarp();                            // slot q is read: refill it
         stage(s + kRankStages * kRankWarps, q);
-        q = (q + 1 == kRankStages) ? 0 : q + 1;
         unsigned peers[kRankItems];
 #pragma unroll
-        for (int j = 0; j < kRankItems; ++j)
-            peers[j] = (BITS && (j & 1) < kRankBallot) ? match_bits<BITS>(key[j], key[j] != 0xffffffffu)
-                                                        : __match_any_sync(SS_FULL, key[j]);
-        // leader (lowest peer) of each item's group in its round, the
+        for (int j = 0; j < kRankItems; ++j) {
+            if (BITS && (j & 1) < kRankBallot)
+                peers[j] = FULL ? match_bits_all<BITS>(key[j]) : match_bits<BITS>(key[j], key[j] != 0xffffffffu);
+            else
+                peers[j] = __match_any_sync(SS_FULL, key[j]);
+        }
+        // leader (highest peer) of each item's group in its round, the
         // round's count for the leader (0 elsewhere) and the cursor address,
         // all ready before the ordered section
         uint32_t lead[kRankItems], cnt[kRankItems], addr[kRankItems], old[kRankItems];
 #pragma unroll
         for (int j = 0; j < kRankItems; ++j) {
-            lead[j] = (uint32_t)(__ffs(peers[j]) - 1);
-            cnt[j] = (key[j] != 0xffffffffu && lane == lead[j]) ? (uint32_t)__popc(peers[j]) : 0u;
-            addr[j] = (uint32_t)__cvta_generic_to_shared(cur + (key[j] & 0x7fffffffu) % G);
+            const bool valid = FULL || key[j] != 0xffffffffu;
+            lead[j] = 31u - (uint32_t)__clz(peers[j]);
+            cnt[j] = (valid && lane == lead[j]) ? (uint32_t)__popc(peers[j]) : 0u;
+            addr[j] = cur_sa + (valid ? key[j] : 0u) * 4u;
             old[j] = 0;
             asm volatile("" :: "r"(cnt[j]), "r"(addr[j]));
         }
-        // ---- in sub-tile order across the warps: advance the cursors with
-        // predicated shared atomics (no divergence inside the section)
+        // ---- in sub-tile order across the warps: advance the cursors
         if (s > 0) named_bar_sync(w, 64);
 #pragma unroll
         for (int j = 0; j < kRankItems; ++j) {
@@ -1180,16 +1184,25 @@ k_rank_place(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin, 
             __syncwarp();
         }
         if (s + 1 < nsub) named_bar_arrive((w + 1) % kRankWarps, 64);
-        // ---- scatter
+        // ---- scatter (never-stored runs have bit 31 set in their cursor)
 #pragma unroll
         for (int j = 0; j < kRankItems; ++j) {
             const uint32_t base = __shfl_sync(SS_FULL, old[j], lead[j]);
             const uint32_t pos = base + (uint32_t)__popc(peers[j] & lt);
-            if (key[j] != 0xffffffffu && !(pos & 0x80000000u)) {
+            if ((FULL || key[j] != 0xffffffffu) && !(pos & 0x80000000u)) {
                 vout[pos] = val[j];
                 if (kout) kout[pos] = key[j];
             }
         }
+    };
+    int q = 0;
+    for (int s = w; s < nsub; s += kRankWarps) {
+        cp_async_wait_n<kRankStages - 1>();
+        __syncwarp();
+        const int tn = min(kRankSub, cn - s * kRankSub);
+        if (tn == kRankSub) sub_tile(std::integral_constant<bool, true>{}, s, q, tn);
+        else sub_tile(std::integral_constant<bool, false>{}, s, q, tn);
+        q = (q + 1 == kRankStages) ? 0 : q + 1;
     }
     cp_async_wait_0();
 }
