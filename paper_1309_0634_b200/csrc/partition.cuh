@@ -573,11 +573,21 @@ k_scan_small(const int32_t* __restrict__ row, uint32_t G, DigitPlan plan, uint32
     const uint32_t g0 = threadIdx.x * GPT;
     int32_t c[GPT];
     int32_t tsum = 0;
+    // each thread owns GPT consecutive groups: 128-bit loads and stores
+    // when the whole run is in range (row and gstart are 16-byte aligned)
+    const bool vec = g0 + GPT <= G;
+    if (vec) {
 #pragma unroll
-    for (int q = 0; q < GPT; ++q) {
-        c[q] = (g0 + q < G) ? row[g0 + q] : 0;
-        tsum += c[q];
+        for (int q = 0; q < GPT; q += 4) {
+            const int4 v = *reinterpret_cast<const int4*>(row + g0 + q);
+            c[q] = v.x; c[q + 1] = v.y; c[q + 2] = v.z; c[q + 3] = v.w;
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < GPT; ++q) c[q] = (g0 + q < G) ? row[g0 + q] : 0;
     }
+#pragma unroll
+    for (int q = 0; q < GPT; ++q) tsum += c[q];
     for (int d = 0; d < plan.npass; ++d) {
         const uint32_t mask = (1u << plan.bits[d]) - 1u;
 #pragma unroll
@@ -586,10 +596,22 @@ k_scan_small(const int32_t* __restrict__ row, uint32_t G, DigitPlan plan, uint32
     }
     int32_t total;
     int32_t ex = block_excl_scan(tsum, sh_red, &total);
+    if (vec) {
 #pragma unroll
-    for (int q = 0; q < GPT; ++q) {
-        if (g0 + q < G) gstart[g0 + q] = ex;
-        ex += c[q];
+        for (int q = 0; q < GPT; q += 4) {
+            int4 v;
+            v.x = ex; ex += c[q];
+            v.y = ex; ex += c[q + 1];
+            v.z = ex; ex += c[q + 2];
+            v.w = ex; ex += c[q + 3];
+            *reinterpret_cast<int4*>(gstart + g0 + q) = v;
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < GPT; ++q) {
+            if (g0 + q < G) gstart[g0 + q] = ex;
+            ex += c[q];
+        }
     }
     if (threadIdx.x == 0) *n_live = total;
     __syncthreads();

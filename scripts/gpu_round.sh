@@ -17,6 +17,6 @@ for c in c1 c2 c3; do
   timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_$c.csv python bench.py --config $c --steps 2 --warmup 3 --no-cpu --e2e-steps 1 > /dev/null 2>&1
 done
 B="python bench.py --steps 2 --warmup 3 --no-cpu --e2e-steps 1"
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_sort_pass|k_ingest|k_count|k_batch_stats|k_balance" -s 25 -c 6 -o $O/full_c2 $B > $O/ncu_c2.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_sort_pass|k_rank_place|k_ingest|k_count|k_batch_stats|k_balance" -s 25 -c 6 -o $O/full_c2 $B > $O/ncu_c2.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_sort_pass|k_ingest|k_count|k_batch_stats|k_scan|k_finalize|k_chunk" -s 21 -c 7 -o $O/full_c1 $B --config c1 > $O/ncu_c1.log 2>&1
 echo done
