@@ -98,6 +98,8 @@ struct ss_engine {
     int32_t *gcnt = nullptr, *gstart = nullptr, *gcount = nullptr, *bsum = nullptr;
     int32_t* gkept = nullptr;              // kept (possibly stored) tuples of each group in the batch
     int32_t* gpre = nullptr;               // [chunk][g] kept-count prefix over chunks (single-pass placement)
+    uint32_t* pwork = nullptr;             // per-partition window-update work of the batch (k_batch_stats)
+    int32_t* cta_map = nullptr;            // work-proportional K4 grid [P+1]
     bool rank_place = false;               // G <= kRankMaxG: k_rank_place instead of the radix passes
     int32_t* n_live = nullptr;             // kept tuples of the batch (device)
     uint32_t* chunk_live = nullptr;        // live-chunk bitmap
@@ -727,6 +729,8 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
     e->rank_place = G <= kRankMaxG && G * W >= e->max_batch;
     if (const char* rp = getenv("SS_B200_RANK_PLACE")) e->rank_place = G <= kRankMaxG && rp[0] != '0';
     if (e->rank_place && (rc = dalloc(e, &e->gpre, (size_t)nsub * G))) return rc;
+    if ((rc = dalloc(e, &e->pwork, e->P)) || (rc = dalloc(e, &e->cta_map, e->P + 1))) return rc;
+    SS_CUDA(e, cudaMemsetAsync(e->pwork, 0, (size_t)e->P * 4, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->hot_of, 0xff, G * 4, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->n_hot_dev, 0, 4, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->bdelta, 0, G * 8, e->st));
@@ -962,23 +966,23 @@ static int launch_count(ss_engine* e, const uint32_t* dk, int64_t n, int64_t S, 
 
 // batch statistics over n_chunk count rows; `step` also derives the kept
 // counts and live chunks of the fused step
-static int launch_stats(ss_engine* e, int n_chunk, bool step = false) {
+static int launch_stats(ss_engine* e, int n_chunk, bool step = false, bool want_work = false) {
     SS_CUDA(e, cudaMemsetAsync(e->tpt, 0, e->P * 8, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->touched, 0, 8, e->st));
     // many chunks (> 32): a CTA per 32 groups, warps over chunk ranges;
     // otherwise a thread per group, coalesced over consecutive groups
     if (n_chunk > 32) {
         const unsigned grid = (unsigned)std::min<int64_t>((e->G + 31) / 32, 8 * kNumSM);
-        ss_note_launch(), k_batch_stats_cols<<<grid, kStatsWarps * 32, e->P * 4, e->st>>>(
+        ss_note_launch(), k_batch_stats_cols<<<grid, kStatsWarps * 32, e->P * 8, e->st>>>(
             e->gcnt, n_chunk, (uint32_t)e->G, e->pmap, e->P, e->gcount, step ? e->gkept : nullptr,
             step ? e->chunk_live : nullptr, e->tpt, e->touched, e->bad, e->fill, e->W, e->alg_bytes, e->trace_on ? 1 : 0,
-            step && e->rank_place ? e->gpre : nullptr);
+            step && e->rank_place ? e->gpre : nullptr, want_work ? e->pwork : nullptr);
     } else {
         const unsigned grid = (unsigned)std::min<int64_t>((e->G + 255) / 256, 16 * kNumSM);
-        ss_note_launch(), k_batch_stats<false><<<grid, 256, e->P * 4, e->st>>>(
+        ss_note_launch(), k_batch_stats<false><<<grid, 256, e->P * 8, e->st>>>(
             e->gcnt, n_chunk, (uint32_t)e->G, e->pmap, e->P, e->gcount, step ? e->gkept : nullptr,
             step ? e->chunk_live : nullptr, e->tpt, e->touched, e->bad, e->fill, e->W, e->alg_bytes, e->trace_on ? 1 : 0,
-            step && e->rank_place ? e->gpre : nullptr);
+            step && e->rank_place ? e->gpre : nullptr, want_work ? e->pwork : nullptr);
     }
     SS_CUDA(e, cudaGetLastError());
     return SS_OK;
@@ -1156,6 +1160,12 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
         pol = SS_POLICY_BEST;
     const bool has_policy = pol != SS_POLICY_NO;
     const bool run_side = has_policy || split;
+    // the reassignment policy alone leaves partitions hosting a top group
+    // with several times the mean work: K4 CTAs in proportion to the work
+    // (measured at C2: 4 x 148 CTAs in total beat 2, 8 and 16 x 148; with
+    // static partitions, C1, the uniform grid is faster)
+    constexpr int k4_waves = 4;
+    const bool work_grid = has_policy && !split && e->P <= 1024;
     SS_CUDA(e, cudaMemsetAsync(e->tickets, 0, 2 * 4, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->part_ns, 0, e->P * 8, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->part_work, 0, e->P * 8, e->st));
@@ -1182,7 +1192,7 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
     e->last_plan = plan;
     {
         ProfScope ps(e, SS_K_STATS, e->st);
-        if ((rc = launch_stats(e, n_chunk, true))) return rc;
+        if ((rc = launch_stats(e, n_chunk, true, work_grid))) return rc;
         if (e->G > 16384) {
             // hot cache for the next batch's count: > 1/(4 kHotCache) of the batch
             SS_CUDA(e, cudaMemsetAsync(e->n_hot_dev, 0, 4, e->st));
@@ -1299,7 +1309,14 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
         // partition-minor order) shortens their tail (measured: 8 CTAs per
         // partition at P = 148 saturates)
         a.cpp = std::max(1, ((split || !has_policy) ? 2 : 8) * kNumSM / e->P);
-        ss_note_launch(), k_ingest<<<e->P * a.cpp, kIngestThreads, kIngestSmem, e->st>>>(a);
+        unsigned grid = (unsigned)(e->P * a.cpp);
+        if (work_grid) {
+            ss_note_launch(), k_cta_map<<<1, 1024, 0, e->st>>>(e->pwork, e->P, k4_waves * kNumSM, e->cta_map);
+            a.cta_map = e->cta_map;
+            a.n_part = e->P;
+            grid = (unsigned)(k4_waves * kNumSM + e->P);
+        }
+        ss_note_launch(), k_ingest<<<grid, kIngestThreads, kIngestSmem, e->st>>>(a);
         SS_CUDA(e, cudaGetLastError());
     }
     if (run_side) SS_CUDA(e, cudaEventRecord(e->ev_k4, e->st));

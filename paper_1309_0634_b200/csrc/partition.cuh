@@ -172,14 +172,19 @@ k_hot_select(const int32_t* __restrict__ gcount, uint32_t G, long long thr, int3
 // --------------------------------------------------------------------------
 __device__ __forceinline__ void stats_account(uint32_t g, int32_t c, const int32_t* __restrict__ pmap,
                                               uint32_t* sh_tpt, const int32_t* __restrict__ fill, int64_t W,
-                                              uint32_t& my_touched, unsigned long long& my_bytes) {
-    atomicAdd(&sh_tpt[pmap[g]], (uint32_t)c);
+                                              uint32_t& my_touched, unsigned long long& my_bytes,
+                                              int P) {
+    const int p = pmap[g];
+    atomicAdd(&sh_tpt[p], (uint32_t)c);
     ++my_touched;
     // algorithmic bytes: stored values, retracted old values
     // that must be read, state + result row
     const int64_t f0 = fill[g];
-    my_bytes += 4ull * (unsigned long long)min64(c, W) + 76ull;
-    if (c < W) my_bytes += 4ull * (unsigned long long)max64(0, f0 + c - W);
+    const int64_t stored = min64(c, W), retracted = c < W ? max64(0, f0 + c - W) : 0;
+    my_bytes += 4ull * (unsigned long long)(stored + retracted) + 76ull;
+    // window-update work of the partition (values moved + a per-group
+    // overhead), for the work-proportional K4 grid
+    atomicAdd(&sh_tpt[P + p], (uint32_t)min64(stored + retracted + 16, 0x3fffffff));
 }
 
 // WARP = true: one warp per group, lanes over the chunks (many chunks, few
@@ -195,12 +200,13 @@ k_batch_stats(int32_t* __restrict__ gcnt, int n_chunk, uint32_t G, const int32_t
               int P, int32_t* __restrict__ gcount, int32_t* __restrict__ gkept, uint32_t* __restrict__ chunk_live,
               unsigned long long* __restrict__ tpt, unsigned long long* __restrict__ touched,
               const unsigned long long* __restrict__ bad, const int32_t* __restrict__ fill, int64_t W,
-              unsigned long long* __restrict__ alg_bytes, int nodrop, int32_t* __restrict__ gpre = nullptr) {
+              unsigned long long* __restrict__ alg_bytes, int nodrop, int32_t* __restrict__ gpre = nullptr,
+              uint32_t* __restrict__ pwork = nullptr) {
     extern __shared__ uint32_t sh_tpt[];     // per-CTA partial loads (< 2^31)
     __shared__ uint32_t sh_live[kMaxChunkWords];
     if (*bad != (unsigned long long)kNoBad) return;
     const int nwords = (n_chunk + 31) >> 5;
-    for (int p = threadIdx.x; p < P; p += blockDim.x) sh_tpt[p] = 0;
+    for (int p = threadIdx.x; p < 2 * P; p += blockDim.x) sh_tpt[p] = 0;
     for (int i = threadIdx.x; i < nwords; i += blockDim.x) sh_live[i] = 0;
     __syncthreads();
     uint32_t my_touched = 0;
@@ -268,7 +274,7 @@ k_batch_stats(int32_t* __restrict__ gcnt, int n_chunk, uint32_t G, const int32_t
             if (lane == 0) {
                 gcount[g] = c;
                 if (gkept) gkept[g] = kept;
-                if (c) stats_account(g, c, pmap, sh_tpt, fill, W, my_touched, my_bytes);
+                if (c) stats_account(g, c, pmap, sh_tpt, fill, W, my_touched, my_bytes, P);
             }
         }
         if (chunk_live && lane == 0) {
@@ -312,7 +318,7 @@ k_batch_stats(int32_t* __restrict__ gcnt, int n_chunk, uint32_t G, const int32_t
                     pre += k;
                 }
             }
-            if (c) stats_account(g, c, pmap, sh_tpt, fill, W, my_touched, my_bytes);
+            if (c) stats_account(g, c, pmap, sh_tpt, fill, W, my_touched, my_bytes, P);
         }
         lbits = __reduce_or_sync(SS_FULL, lbits);
         if (chunk_live && lane == 0 && lbits) atomicOr(&sh_live[0], lbits);
@@ -324,8 +330,10 @@ k_batch_stats(int32_t* __restrict__ gcnt, int n_chunk, uint32_t G, const int32_t
         atomicAdd(alg_bytes, my_bytes);
     }
     __syncthreads();
-    for (int p = threadIdx.x; p < P; p += blockDim.x)
+    for (int p = threadIdx.x; p < P; p += blockDim.x) {
         if (sh_tpt[p]) atomicAdd(&tpt[p], (unsigned long long)sh_tpt[p]);
+        if (pwork && sh_tpt[P + p]) atomicAdd(&pwork[p], sh_tpt[P + p]);
+    }
     if (chunk_live)
         for (int i = threadIdx.x; i < nwords; i += blockDim.x) {
             const uint32_t v = sh_live[i];
@@ -348,14 +356,14 @@ k_batch_stats_cols(int32_t* __restrict__ gcnt, int n_chunk, uint32_t G, const in
                    uint32_t* __restrict__ chunk_live, unsigned long long* __restrict__ tpt,
                    unsigned long long* __restrict__ touched, const unsigned long long* __restrict__ bad,
                    const int32_t* __restrict__ fill, int64_t W, unsigned long long* __restrict__ alg_bytes,
-                   int nodrop, int32_t* __restrict__ gpre) {
-    extern __shared__ uint32_t sh_tpt[];     // per-CTA partial loads (< 2^31)
+                   int nodrop, int32_t* __restrict__ gpre, uint32_t* __restrict__ pwork) {
+    extern __shared__ uint32_t sh_tpt[];     // per-CTA partial loads (< 2^31), then partition work
     __shared__ uint32_t sh_live[kMaxChunkWords];
     __shared__ int32_t sh_part[kStatsWarps][32];
     __shared__ int32_t sh_dead[kStatsWarps][32];
     if (*bad != (unsigned long long)kNoBad) return;
     const int nwords = (n_chunk + 31) >> 5;
-    for (int p = threadIdx.x; p < P; p += blockDim.x) sh_tpt[p] = 0;
+    for (int p = threadIdx.x; p < 2 * P; p += blockDim.x) sh_tpt[p] = 0;
     for (int i = threadIdx.x; i < nwords; i += blockDim.x) sh_live[i] = 0;
     const unsigned lane = lane_id(), w = warp_id();
     const int R = (n_chunk + kStatsWarps - 1) / kStatsWarps;
@@ -420,7 +428,7 @@ k_batch_stats_cols(int32_t* __restrict__ gcnt, int n_chunk, uint32_t G, const in
         if (w == 0 && gv) {
             gcount[g] = C;
             if (gkept) gkept[g] = C - D;
-            if (C) stats_account(g, C, pmap, sh_tpt, fill, W, my_touched, my_bytes);
+            if (C) stats_account(g, C, pmap, sh_tpt, fill, W, my_touched, my_bytes, P);
         }
         __syncthreads();                         // sh_part / sh_dead reused
     }
@@ -431,8 +439,10 @@ k_batch_stats_cols(int32_t* __restrict__ gcnt, int n_chunk, uint32_t G, const in
         atomicAdd(alg_bytes, my_bytes);
     }
     __syncthreads();
-    for (int p = threadIdx.x; p < P; p += blockDim.x)
+    for (int p = threadIdx.x; p < P; p += blockDim.x) {
         if (sh_tpt[p]) atomicAdd(&tpt[p], (unsigned long long)sh_tpt[p]);
+        if (pwork && sh_tpt[P + p]) atomicAdd(&pwork[p], sh_tpt[P + p]);
+    }
     if (chunk_live)
         for (int i = threadIdx.x; i < nwords; i += blockDim.x) {
             const uint32_t v = sh_live[i];

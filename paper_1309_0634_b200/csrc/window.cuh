@@ -58,8 +58,41 @@ struct IngestArgs {
     unsigned long long* part_work;     // per-partition stored values
     const int32_t* n_live;      // live tuples of this sub-batch (0: nothing to do)
     int cpp;                    // CTAs sharing one partition's work (grid = P * cpp)
+    const int32_t* cta_map;     // or: work-proportional CTAs, partition p = [map[p], map[p+1])
+    int n_part;                 // P (with cta_map)
     const unsigned long long* bad;
 };
+
+// Work-proportional K4 grid, for the group-reassignment policy without
+// hot-key splitting (a partition hosting a top group carries several times
+// the mean): partition p gets max(1, floor(total * work_p / sum)) CTAs,
+// partition-major, map[p] = its first CTA, map[P] = CTAs used (<= total +
+// P).  work_p comes from k_batch_stats; it is cleared for the next batch.
+__global__ void __launch_bounds__(1024)
+k_cta_map(uint32_t* __restrict__ pwork, int P, int total, int32_t* __restrict__ map) {
+    __shared__ unsigned long long sh_sum[32];
+    __shared__ int32_t sh_red[33];
+    const int t = threadIdx.x;
+    const unsigned lane = lane_id(), wp = warp_id();
+    const uint32_t w = t < P ? pwork[t] : 0u;
+    if (t < P) pwork[t] = 0;
+    unsigned long long v = warp_sum((unsigned long long)w);
+    if (lane == 0) sh_sum[wp] = v;
+    __syncthreads();
+    if (wp == 0) {
+        v = lane < (blockDim.x >> 5) ? sh_sum[lane] : 0ull;
+        v = warp_sum(v);
+        if (lane == 0) sh_sum[0] = v;
+    }
+    __syncthreads();
+    const unsigned long long tot = sh_sum[0];
+    int c = 0;
+    if (t < P) c = tot ? max(1, (int)((double)total * (double)w / (double)tot)) : 1;
+    int all;
+    const int ex = block_excl_scan(c, sh_red, &all);
+    if (t < P) map[t] = ex;
+    if (t == 0) map[P] = all;
+}
 
 // segmented (contiguous-lane segments) suffix reduction; the first lane
 // of each segment ends with the segment total.
@@ -119,13 +152,28 @@ k_ingest(IngestArgs a) {
 #endif
     // partition p is processed by kCtaPerPart CTAs; its members (and split
     // shares) are dealt to them round-robin
-    const int kCtaPerPart = a.cpp;
-    // partition-minor order: the first resident wave holds CTA 0 (and 1) of
-    // every partition, later CTAs of a heavy partition start as light
-    // partitions finish
-    const int P = (int)(gridDim.x / kCtaPerPart);
-    const int p = blockIdx.x % P;
-    const int sub = blockIdx.x / P;
+    int kCtaPerPart, p, sub;
+    if (a.cta_map) {
+        // work-proportional: partition-major ranges of the CTA map
+        const int bx = (int)blockIdx.x;
+        if (bx >= a.cta_map[a.n_part]) return;
+        int l = 0, h = a.n_part - 1;             // last p with map[p] <= bx
+        while (l < h) {
+            const int mid = (l + h + 1) >> 1;
+            if (a.cta_map[mid] <= bx) l = mid; else h = mid - 1;
+        }
+        p = l;
+        sub = bx - a.cta_map[p];
+        kCtaPerPart = a.cta_map[p + 1] - a.cta_map[p];
+    } else {
+        // partition-minor order: the first resident wave holds CTA 0 (and 1)
+        // of every partition, later CTAs of a heavy partition start as light
+        // partitions finish
+        kCtaPerPart = a.cpp;
+        const int P = (int)(gridDim.x / kCtaPerPart);
+        p = blockIdx.x % P;
+        sub = blockIdx.x / P;
+    }
     const int lo = a.offsets[p], hi = a.offsets[p + 1];
     const int s_lo = a.share_off ? a.share_off[p] : 0;
     const int s_hi = a.share_off ? a.share_off[p + 1] : 0;
