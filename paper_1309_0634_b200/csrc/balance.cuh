@@ -32,6 +32,7 @@ struct BalanceArgs {
     double pot;
     int cap;
     int P;
+    int G;
     const int32_t* order;       // entry lists (CSR)
     const int32_t* offsets;     // [P+1]
     const int32_t* gcount;      // batch group counts
@@ -60,7 +61,18 @@ struct BalSmem {
     int* ehi;
     int* esize;     // live entry members
     int* nin;       // pushed-in members
+    // staged (G <= kBalStageG): entry order, its batch counts by position and
+    // the moved / excluded flag by group, all in shared memory, so a donor
+    // scan is no chain of dependent global loads (nullptr otherwise)
+    int* sorder;
+    int* scnt;
+    uint8_t* smv;
 };
+constexpr int kBalStageG = 16384;
+
+__host__ __device__ inline size_t bal_smem_bytes(int P, int G, bool staged) {
+    return (size_t)P * (8 + 8 * 4) + (staged ? (size_t)G * 9 : 0);
+}
 
 __device__ __forceinline__ int bal_size(const BalSmem& s, int p) { return s.esize[p] + s.nin[p]; }
 
@@ -68,28 +80,32 @@ __device__ __forceinline__ int bal_size(const BalSmem& s, int p) { return s.esiz
 __device__ int bal_head(const BalanceArgs& a, const BalSmem& s, int p) {
     if (s.ftop[p] >= 0) return a.moves[s.ftop[p]].x;
     int c = s.elo[p];
-    while (c < s.ehi[p] && a.moved[a.order[c]]) ++c;
+    if (s.sorder) while (c < s.ehi[p] && s.smv[s.sorder[c]]) ++c;
+    else while (c < s.ehi[p] && a.moved[a.order[c]]) ++c;
     s.elo[p] = c;
-    if (c < s.ehi[p]) return a.order[c];
+    if (c < s.ehi[p]) return s.sorder ? s.sorder[c] : a.order[c];
     if (s.bfirst[p] >= 0) return a.moves[s.bfirst[p]].x;
     return -1;
 }
 __device__ int bal_tail(const BalanceArgs& a, const BalSmem& s, int p) {
     if (s.blast[p] >= 0) return a.moves[s.blast[p]].x;
     int c = s.ehi[p];
-    while (c > s.elo[p] && a.moved[a.order[c - 1]]) --c;
+    if (s.sorder) while (c > s.elo[p] && s.smv[s.sorder[c - 1]]) --c;
+    else while (c > s.elo[p] && a.moved[a.order[c - 1]]) --c;
     s.ehi[p] = c;
-    if (c > s.elo[p]) return a.order[c - 1];
+    if (c > s.elo[p]) return s.sorder ? s.sorder[c - 1] : a.order[c - 1];
     if (s.fbot[p] >= 0) return a.moves[s.fbot[p]].x;
     return -1;
 }
 
-// record a move of g (an un-moved entry member of src) into dst
+// record a move of g (an un-moved entry member of src) into dst; c = its
+// batch count when the caller has it (< 0: read it)
 __device__ void bal_move(const BalanceArgs& a, const BalSmem& s, int* nm, int g, int src, int dst,
-                         int placement) {
+                         int placement, long long c = -1) {
     const int mi = *nm;
     a.moves[mi] = make_int4(g, src, dst, placement);
     a.moved[g] = 1;
+    if (s.smv) s.smv[g] = 1;
     s.esize[src] -= 1;
     s.nin[dst] += 1;
     a.mv_next[mi] = -1;
@@ -102,7 +118,7 @@ __device__ void bal_move(const BalanceArgs& a, const BalSmem& s, int* nm, int g,
         if (s.ftop[dst] < 0) s.fbot[dst] = mi;
         s.ftop[dst] = mi;
     }
-    const long long c = a.gcount[g];
+    if (c < 0) c = a.gcount[g];
     s.loads[src] -= c;
     s.loads[dst] += c;
     *nm = mi + 1;
@@ -186,6 +202,7 @@ __device__ void bal_argmin_key(long long key, int g, long long* red_v, int* red_
     __syncthreads();
 }
 
+template <bool STAGED>
 __global__ void __launch_bounds__(kBalThreads)
 k_balance(BalanceArgs a) {
     extern __shared__ long long bal_sm[];
@@ -199,6 +216,13 @@ k_balance(BalanceArgs a) {
     int* ib = (int*)(bal_sm + P);
     s.ftop = ib; s.fbot = ib + P; s.bfirst = ib + 2 * P; s.blast = ib + 3 * P;
     s.elo = ib + 4 * P; s.ehi = ib + 5 * P; s.esize = ib + 6 * P; s.nin = ib + 7 * P;
+    s.sorder = s.scnt = nullptr;
+    s.smv = nullptr;
+    if (STAGED) {
+        s.sorder = ib + 8 * P;
+        s.scnt = s.sorder + a.G;
+        s.smv = (uint8_t*)(s.scnt + a.G);
+    }
     if (*a.bad != (unsigned long long)kNoBad) {
         if (threadIdx.x == 0) *a.n_moves = 0;
         return;
@@ -211,120 +235,138 @@ k_balance(BalanceArgs a) {
         s.esize[p] = a.offsets[p + 1] - a.offsets[p];
         s.nin[p] = 0;
     }
+    if (STAGED) {
+        for (int i = threadIdx.x; i < a.G; i += blockDim.x) {
+            const int g = a.order[i];
+            s.sorder[i] = g;
+            s.scnt[i] = a.gcount[g];
+            s.smv[i] = a.exclude ? a.exclude[i] : 0;
+        }
+    }
     __syncthreads();
+    auto ORD = [&](int i) { return STAGED ? s.sorder[i] : a.order[i]; };
+    auto CNT = [&](int i, int g) -> long long { return STAGED ? (long long)s.scnt[i] : (long long)a.gcount[g]; };
+    auto MV = [&](int g) -> bool { return STAGED ? s.smv[g] != 0 : (a.moved[g] || (a.exclude && a.exclude[g])); };
     int nm = 0;                // valid in thread 0
     long long scanned = 0;
     const int pol = a.policy;
 
     if (pol == 1 || pol == 2 || pol == 3 || pol == 4) {
-        for (;;) {
-            int hi, lo;
-            bal_extremes(s, P, &hi, &lo, red_v, red_i);
-            if (threadIdx.x == 0) {
-                sh_ctl[0] = nm;
-                sh_ctl[2] = -1;
-            }
-            __syncthreads();
-            const int nm_all = sh_ctl[0];
-            __syncthreads();
-            if (nm_all >= a.cap) break;
-            if (s.loads[hi] - s.loads[lo] <= a.threshold) break;
-            if (a.stop_load > 0 && s.loads[hi] <= a.stop_load) break;
-            const int e0 = a.offsets[hi], e1 = a.offsets[hi + 1];
-            int pick = -1;
-            long long pscan = 0;
-            if (pol == 1) {                       // get_first
-                if (threadIdx.x == 0) {
-                    const int g = bal_head(a, s, hi);
+        // The extreme-pair loop is sequential: one warp runs it with warp
+        // shuffles only (no CTA barriers); the shared-memory state is
+        // updated by lane 0 and published to the warp by __syncwarp.
+        if (warp_id() == 0) {
+            const unsigned lane = lane_id();
+            // lexicographic (key, id) minimum over the warp
+            auto warp_argmin = [&](long long& key, int& id) {
+#pragma unroll
+                for (int o = 16; o; o >>= 1) {
+                    const long long ok = __shfl_xor_sync(SS_FULL, key, o);
+                    const int oi = __shfl_xor_sync(SS_FULL, id, o);
+                    if (ok < key || (ok == key && oi < id)) { key = ok; id = oi; }
+                }
+            };
+            for (;;) {
+                // hottest / coolest partition, lowest index on ties
+                long long vmax = LLONG_MIN, vmin = LLONG_MAX;
+                int imax = 0x7fffffff, imin = 0x7fffffff;
+                for (int p = lane; p < P; p += 32) {
+                    const long long v = s.loads[p];
+                    if (v > vmax) { vmax = v; imax = p; }
+                    if (v < vmin) { vmin = v; imin = p; }
+                }
+                long long nmax = imax == 0x7fffffff ? LLONG_MAX : -vmax;   // argmax as argmin of the negation
+                warp_argmin(nmax, imax);
+                warp_argmin(vmin, imin);
+                const int hi = imax, lo = imin;
+                const int nm_all = __shfl_sync(SS_FULL, nm, 0);
+                if (nm_all >= a.cap) break;
+                if (s.loads[hi] - s.loads[lo] <= a.threshold) break;
+                if (a.stop_load > 0 && s.loads[hi] <= a.stop_load) break;
+                const int e0 = a.offsets[hi], e1 = a.offsets[hi + 1];
+                int pick = -1;
+                long long pscan = 0, pick_c = -1;
+                if (pol == 1) {                       // get_first
                     int r = -1;
-                    if (g >= 0 && !a.moved[g] && a.gcount[g] != 0) r = g;
-                    sh_ctl[2] = r;
-                }
-                __syncthreads();
-                pick = sh_ctl[2];
-            } else if (pol == 2 || pol == 4) {    // check_all / best_balance
-                long long bk = LLONG_MAX;
-                int bg = 0x7fffffff;
-                const long long dmax = s.loads[hi], dmin = s.loads[lo];
-                for (int i = e0 + threadIdx.x; i < e1; i += blockDim.x) {
-                    const int g = a.order[i];
-                    if (a.moved[g] || (a.exclude && a.exclude[g])) continue;
-                    const long long c = a.gcount[g];
-                    long long key;
-                    if (pol == 2) key = -c;      // max count, lowest id
-                    else {
-                        long long d = (dmax - c) - (dmin + c);
-                        key = d < 0 ? -d : d;
+                    if (lane == 0) {
+                        const int g = bal_head(a, s, hi);
+                        if (g >= 0 && !MV(g) && a.gcount[g] != 0) r = g;
                     }
-                    if (key < bk || (key == bk && g < bg)) { bk = key; bg = g; }
-                }
-                long long k;
-                int g;
-                bal_argmin_key(bk, bg, red_v, red_i, &k, &g);
-                if (g != 0x7fffffff) {
-                    if (pol == 2) {
-                        if (-k > 0) { pick = g; pscan = (long long)a.tpt[hi]; }
-                    } else {
-                        if (k < dmax - dmin) pick = g;
+                    pick = __shfl_sync(SS_FULL, r, 0);
+                } else if (pol == 2 || pol == 4) {    // check_all / best_balance
+                    long long bk = LLONG_MAX;
+                    int bg = 0x7fffffff;
+                    const long long dmax = s.loads[hi], dmin = s.loads[lo];
+                    for (int i = e0 + (int)lane; i < e1; i += 32) {
+                        const int g = ORD(i);
+                        if (MV(g)) continue;
+                        const long long c = CNT(i, g);
+                        long long key;
+                        if (pol == 2) key = -c;      // max count, lowest id
+                        else {
+                            const long long d = (dmax - c) - (dmin + c);
+                            key = d < 0 ? -d : d;
+                        }
+                        if (key < bk || (key == bk && g < bg)) { bk = key; bg = g; }
                     }
-                }
-            } else {                               // prob_check
-                const int sz = bal_size(s, hi);
-                if (sz > 0) {
-                    const long long limit =
-                        (long long)ceil(a.pot * (double)s.loads[hi] / (double)sz);
-                    long long run = 0;             // tuples before the current chunk
-                    long long fb_key = LLONG_MAX;  // fallback: max count (as -c), lowest id
-                    int fb_g = 0x7fffffff;
-                    for (int c0 = e0; c0 < e1 && pick < 0; c0 += blockDim.x) {
-                        const int i = c0 + threadIdx.x;
-                        int g = -1;
-                        long long c = 0;
-                        bool cand = false;
-                        if (i < e1) {
-                            g = a.order[i];
-                            c = a.gcount[g];
-                            const bool mv = a.moved[g] || (a.exclude && a.exclude[g]);
-                            cand = (c >= limit) && !mv;
-                            if (!mv && c > 0) {
-                                const long long key = -c;
-                                if (key < fb_key || (key == fb_key && g < fb_g)) { fb_key = key; fb_g = g; }
+                    warp_argmin(bk, bg);
+                    if (bg != 0x7fffffff) {
+                        if (pol == 2) {
+                            if (-bk > 0) { pick = bg; pscan = (long long)a.tpt[hi]; pick_c = -bk; }
+                        } else {
+                            if (bk < dmax - dmin) pick = bg;
+                        }
+                    }
+                } else {                               // prob_check
+                    const int sz = bal_size(s, hi);
+                    if (sz > 0) {
+                        const long long limit = (long long)ceil(a.pot * (double)s.loads[hi] / (double)sz);
+                        long long run = 0;             // tuples of the entries before this chunk
+                        long long fb_key = LLONG_MAX;  // fallback: max count (as -c), lowest id
+                        int fb_g = 0x7fffffff;
+                        for (int c0 = e0; c0 < e1; c0 += 32) {
+                            const int i = c0 + (int)lane;
+                            int g = -1;
+                            long long c = 0;
+                            bool cand = false;
+                            if (i < e1) {
+                                g = ORD(i);
+                                c = CNT(i, g);
+                                const bool mv = MV(g);
+                                cand = (c >= limit) && !mv;
+                                if (!mv && c > 0) {
+                                    const long long key = -c;
+                                    if (key < fb_key || (key == fb_key && g < fb_g)) { fb_key = key; fb_g = g; }
+                                }
+                            }
+                            const long long incl = warp_incl_scan(c);
+                            const unsigned cb = __ballot_sync(SS_FULL, cand);
+                            if (cb) {                  // first candidate in entry order
+                                const int f = __ffs(cb) - 1;
+                                pick = __shfl_sync(SS_FULL, g, f);
+                                pscan = run + __shfl_sync(SS_FULL, incl - c, f) + limit;
+                                pick_c = __shfl_sync(SS_FULL, c, f);
+                                break;
+                            }
+                            run += __shfl_sync(SS_FULL, incl, 31);
+                        }
+                        if (pick < 0) {
+                            warp_argmin(fb_key, fb_g);
+                            if (fb_g != 0x7fffffff && -fb_key > 0) {
+                                pick = fb_g;
+                                pscan = (long long)a.tpt[hi];
+                                pick_c = -fb_key;
                             }
                         }
-                        // inclusive block scan of c (tuples up to and including i)
-                        long long tot;
-                        long long ex = block_excl_scan(c, red_v, &tot);
-                        // first candidate index in this chunk
-                        long long ck;
-                        int cg;
-                        bal_argmin_key(cand ? (long long)i : LLONG_MAX, cand ? g : 0x7fffffff, red_v,
-                                       red_i, &ck, &cg);
-                        if (cand && (long long)i == ck) sh_scan[0] = run + ex + limit;
-                        __syncthreads();
-                        if (ck != LLONG_MAX) {
-                            pick = cg;
-                            pscan = sh_scan[0];
-                        }
-                        __syncthreads();
-                        run += tot;
-                    }
-                    if (pick < 0) {
-                        long long k;
-                        int g;
-                        bal_argmin_key(fb_key, fb_g, red_v, red_i, &k, &g);
-                        if (g != 0x7fffffff && -k > 0) {
-                            pick = g;
-                            pscan = (long long)a.tpt[hi];
-                        }
                     }
                 }
+                if (pick < 0) break;
+                if (lane == 0) {
+                    bal_move(a, s, &nm, pick, hi, lo, 1, pick_c);
+                    scanned += pscan;
+                }
+                __syncwarp();
             }
-            if (pick < 0) break;
-            if (threadIdx.x == 0) {
-                bal_move(a, s, &nm, pick, hi, lo, 1);
-                scanned += pscan;
-            }
-            __syncthreads();
         }
     } else if (threadIdx.x == 0 && pol == 5) {     // shift
         while (nm < a.cap) {
@@ -341,7 +383,7 @@ k_balance(BalanceArgs a) {
                 if (nm >= a.cap) break;
                 if (bal_size(s, i) == 0) continue;
                 const int g = down ? bal_head(a, s, i) : bal_tail(a, s, i);
-                if (g < 0 || a.moved[g]) continue;
+                if (g < 0 || MV(g)) continue;
                 bal_move(a, s, &nm, g, i, down ? i - 1 : i + 1, down ? 1 : 0);
                 ++emitted;
             }
@@ -357,7 +399,7 @@ k_balance(BalanceArgs a) {
             else continue;
             if (bal_size(s, src) == 0) continue;
             const int g = last ? bal_tail(a, s, src) : bal_head(a, s, src);
-            if (g < 0 || a.moved[g]) continue;
+            if (g < 0 || MV(g)) continue;
             bal_move(a, s, &nm, g, src, dst, last ? 0 : 1);
         }
     }

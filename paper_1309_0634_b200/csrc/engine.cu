@@ -307,6 +307,15 @@ bool is_device_ptr(const void* p) {
     return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
 }
 
+// the device policy loop: one CTA; G <= kBalStageG stages the entry lists
+// and counts in shared memory
+static void launch_balance(ss_engine* e, BalanceArgs& a, cudaStream_t st) {
+    a.G = (int)e->G;
+    const bool staged = e->G <= kBalStageG;
+    if (staged) k_balance<true><<<1, kBalThreads, bal_smem_bytes(e->P, (int)e->G, true), st>>>(a);
+    else k_balance<false><<<1, kBalThreads, bal_smem_bytes(e->P, (int)e->G, false), st>>>(a);
+}
+
 // single-pass placement kernel for keys < 2^bits (ballot matching)
 using RankKernel = void (*)(const uint32_t*, const int32_t*, uint32_t*, int32_t*, int64_t, int, const int32_t*,
                             const int32_t*, const int32_t*, const int32_t*, uint32_t, const int32_t*,
@@ -826,7 +835,8 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
         const RankKernel rk = b ? rank_kernel(b) : k_rank_place<0>;
         SS_CUDA(e, cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rank_smem_bytes(kRankMaxG)));
     }
-    SS_CUDA(e, cudaFuncSetAttribute(k_balance, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    SS_CUDA(e, cudaFuncSetAttribute(k_balance<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    SS_CUDA(e, cudaFuncSetAttribute(k_balance<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     SS_CUDA(e, cudaFuncSetAttribute(k_split_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     SS_CUDA(e, cudaStreamSynchronize(e->st));
     return SS_OK;
@@ -1251,7 +1261,7 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
                 a.exclude = e->spx.hot_flag;
                 a.stop_load = std::max<long long>(1, (n + e->P - 1) / e->P);
             }
-            ss_note_launch(), k_balance<<<1, kBalThreads, (size_t)e->P * (8 + 8 * 4), e->side>>>(a);
+            ss_note_launch(), launch_balance(e, a, e->side);
         }
         SS_CUDA(e, cudaGetLastError());
     }
@@ -1684,7 +1694,7 @@ extern "C" int ss_balance(ss_engine* e, const uint32_t* groups, int64_t n, const
         a.scanned = e->scanned;
         a.final_tpt = e->final_tpt;
         a.bad = e->bad;
-        ss_note_launch(), k_balance<<<1, kBalThreads, (size_t)e->P * (8 + 8 * 4), e->st>>>(a);
+        ss_note_launch(), launch_balance(e, a, e->st);
         SS_CUDA(e, cudaGetLastError());
         ss_note_launch(), k_clear_moved<<<4, 256, 0, e->st>>>(e->moves, e->n_moves, e->moved);
         SS_CUDA(e, cudaMemcpyAsync(&nm, e->n_moves, 4, cudaMemcpyDeviceToHost, e->st));
@@ -2332,7 +2342,7 @@ extern "C" int ss_balance_counts(ss_engine* e, const int32_t* counts, const ss_b
         a.scanned = e->scanned;
         a.final_tpt = e->final_tpt;
         a.bad = e->bad;
-        ss_note_launch(), k_balance<<<1, kBalThreads, (size_t)e->P * (8 + 8 * 4), e->st>>>(a);
+        ss_note_launch(), launch_balance(e, a, e->st);
         SS_CUDA(e, cudaGetLastError());
         ss_note_launch(), k_clear_moved<<<4, 256, 0, e->st>>>(e->moves, e->n_moves, e->moved);
         SS_CUDA(e, cudaMemcpyAsync(&nm, e->n_moves, 4, cudaMemcpyDeviceToHost, e->st));

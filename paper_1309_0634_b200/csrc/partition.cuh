@@ -348,7 +348,7 @@ k_batch_stats(int32_t* __restrict__ gcnt, int n_chunk, uint32_t G, const int32_t
 // (shared memory), the never-stored runs -- a prefix of the group's chunks,
 // ending at the largest inclusive prefix <= K - W -- zeroed, then the kept
 // prefix of every live chunk (gpre, -1 elsewhere) and the live-chunk bits.
-constexpr int kStatsWarps = 8;
+constexpr int kStatsWarps = 16;
 
 __global__ void __launch_bounds__(kStatsWarps * 32)
 k_batch_stats_cols(int32_t* __restrict__ gcnt, int n_chunk, uint32_t G, const int32_t* __restrict__ pmap,

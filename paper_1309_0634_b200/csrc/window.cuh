@@ -508,12 +508,6 @@ k_finalize(FinalizeArgs a) {
             a.bmin[g] = 0x7fffffff;
             a.bmax[g] = (int32_t)0x80000000;
         }
-        if (a.lc) {
-            const int nl = *a.n_lc;
-            for (int i = 0; i < nl; ++i) a.gcnt[(int64_t)a.lc[i] * a.G + g] = 0;
-        } else {
-            for (int s2 = 0; s2 < a.n_sub; ++s2) a.gcnt[(int64_t)s2 * a.G + g] = 0;
-        }
         if (need_rescan) a.rescan[atomicAdd(a.n_rescan, 1u)] = make_int2((int)g, a.emit ? (int)slot : -1);
         if (a.emit) {
             a.r_g[slot] = (int32_t)g;
@@ -524,6 +518,23 @@ k_finalize(FinalizeArgs a) {
                 a.r_mn[slot] = lo;
                 a.r_mx[slot] = hi;
             }
+        }
+    }
+    // clear the batch's chunk histograms for the next batch: whole rows of
+    // the live chunks (every other row is already zero), a row per CTA
+    // (few rows of many groups: each row is cut into segments over the grid)
+    const int nrows = a.lc ? *a.n_lc : a.n_sub;
+    const bool v4 = (a.G & 3u) == 0;
+    const uint32_t nq = v4 ? a.G / 4 : a.G;                  // stores per row
+    const int segs = nrows ? max(1, min((int)gridDim.x / nrows, (int)((nq + 1023) / 1024))) : 1;
+    const uint32_t per = (nq + segs - 1) / segs;
+    for (int t = blockIdx.x; t < nrows * segs; t += gridDim.x) {
+        const int i = t / segs, sg = t - i * segs;
+        int32_t* row = a.gcnt + (int64_t)(a.lc ? a.lc[i] : i) * a.G;
+        const uint32_t q1 = min(nq, (sg + 1) * per);
+        for (uint32_t q = sg * per + threadIdx.x; q < q1; q += blockDim.x) {
+            if (v4) reinterpret_cast<int4*>(row)[q] = make_int4(0, 0, 0, 0);
+            else row[q] = 0;
         }
     }
 }
