@@ -49,6 +49,10 @@ struct BalanceArgs {
     const unsigned long long* init_loads;   // split mode: cold-only loads (else tpt)
     const uint8_t* exclude;                 // split mode: hot groups never move
     long long stop_load;                    // split mode: done once max load <= this (0: off)
+    // fused step: the new list layout for k_apply_place (nullptr: not wanted)
+    int32_t* new_off;           // [P+1] offsets of the rebuilt lists
+    int32_t* keep_at;           // [P] where the unmoved entry members start
+    int32_t* mv_pos;            // [cap] position of every move's group
 };
 
 struct BalSmem {
@@ -413,6 +417,32 @@ k_balance(BalanceArgs a) {
         a.front_top[p] = s.ftop[p];
         a.back_first[p] = s.bfirst[p];
     }
+    if (a.new_off) {
+        // new list of p = fronts pushed in (newest first) ++ entry members
+        // not moved ++ backs pushed in (in order): offsets from the final
+        // sizes, every move's position by walking p's push chains (thread p)
+        __shared__ int32_t sh_carry;
+        if (threadIdx.x == 0) sh_carry = 0;
+        __syncthreads();
+        for (int p0 = 0; p0 < P; p0 += blockDim.x) {
+            const int p = p0 + threadIdx.x;
+            const int32_t sz = p < P ? s.esize[p] + s.nin[p] : 0;
+            int32_t tot;
+            const int32_t ex = block_excl_scan(sz, red_i, &tot);
+            if (p < P) {
+                int pos = sh_carry + ex;
+                a.new_off[p] = pos;
+                for (int mi = s.ftop[p]; mi >= 0; mi = a.mv_next[mi]) a.mv_pos[mi] = pos++;
+                a.keep_at[p] = pos;
+                pos += s.esize[p];
+                for (int mi = s.bfirst[p]; mi >= 0; mi = a.mv_next[mi]) a.mv_pos[mi] = pos++;
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) sh_carry += tot;
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) a.new_off[P] = sh_carry;
+    }
 }
 
 // ---- device apply_moves (partition.py:181-203) ------------------------------
@@ -481,6 +511,36 @@ k_apply_build(const int32_t* __restrict__ order, const int32_t* __restrict__ off
     }
     if (threadIdx.x == 0)
         for (int mi = back_first[p]; mi >= 0; mi = mv_next[mi]) new_order[pos++] = moves[mi].x;
+}
+
+// fused step: the rebuilt lists from the layout k_balance computed (one
+// CTA per partition places its unmoved entry members; the moved groups are
+// scattered to their positions by all CTAs)
+__global__ void __launch_bounds__(256)
+k_apply_place(const int32_t* __restrict__ order, const int32_t* __restrict__ offsets,
+              const int32_t* __restrict__ keep_at, const int4* __restrict__ moves, const int* __restrict__ n_moves,
+              const int32_t* __restrict__ mv_pos, const uint8_t* __restrict__ moved, int32_t* __restrict__ new_order) {
+    __shared__ int32_t red[33];
+    const int nm = *n_moves;
+    if (nm == 0) return;
+    const int p = blockIdx.x;
+    for (int mi = blockIdx.x * blockDim.x + threadIdx.x; mi < nm; mi += gridDim.x * blockDim.x)
+        new_order[mv_pos[mi]] = moves[mi].x;
+    int pos = keep_at[p];
+    const int e0 = offsets[p], e1 = offsets[p + 1];
+    for (int c0 = e0; c0 < e1; c0 += blockDim.x) {
+        const int i = c0 + threadIdx.x;
+        int g = -1;
+        int keep = 0;
+        if (i < e1) {
+            g = order[i];
+            keep = !moved[g];
+        }
+        int32_t tot;
+        const int32_t ex = block_excl_scan(keep, red, &tot);
+        if (keep) new_order[pos + ex] = g;
+        pos += tot;
+    }
 }
 
 // commit: copy the rebuilt lists, update the group->partition map, clear

@@ -132,6 +132,7 @@ struct ss_engine {
     int cap_moves = 0;
     int4* moves = nullptr;
     int *front_top = nullptr, *back_first = nullptr, *mv_next = nullptr, *n_moves = nullptr;
+    int32_t *keep_at = nullptr, *mv_pos = nullptr;   // list layout of the fused step's apply
     long long *scanned = nullptr, *final_tpt = nullptr;
     int* prev_moves = nullptr;
 
@@ -779,6 +780,7 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
     }
     // -- balancer
     e->cap_moves = 4 * e->P;
+    if ((rc = dalloc(e, &e->keep_at, e->P)) || (rc = dalloc(e, &e->mv_pos, e->cap_moves))) return rc;
     if ((rc = dalloc(e, &e->moves, e->cap_moves)) || (rc = dalloc(e, &e->front_top, e->P)) ||
         (rc = dalloc(e, &e->back_first, e->P)) || (rc = dalloc(e, &e->mv_next, e->cap_moves)) ||
         (rc = dalloc(e, &e->n_moves, 1)) || (rc = dalloc(e, &e->scanned, 1)) ||
@@ -1250,6 +1252,9 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
             a.front_top = e->front_top;
             a.back_first = e->back_first;
             a.mv_next = e->mv_next;
+            a.new_off = e->new_off;
+            a.keep_at = e->keep_at;
+            a.mv_pos = e->mv_pos;
             a.n_moves = e->n_moves;
             a.scanned = e->scanned;
             a.final_tpt = e->final_tpt;
@@ -1380,9 +1385,9 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
         SS_CUDA(e, cudaStreamWaitEvent(e->side, e->ev_k4, 0));
         if (has_policy) {
             ProfScope ps(e, SS_K_APPLY, e->side);
-            ss_note_launch(), k_apply_sizes<<<1, 1024, 0, e->side>>>(e->offsets, e->P, e->moves, e->n_moves, e->new_off);
-            ss_note_launch(), k_apply_build<<<e->P, 256, 0, e->side>>>(e->order, e->offsets, e->new_off, e->moves, e->n_moves,
-                                                     e->front_top, e->back_first, e->mv_next, e->moved, e->new_order);
+            // (the new offsets and move positions come from k_balance)
+            ss_note_launch(), k_apply_place<<<e->P, 256, 0, e->side>>>(e->order, e->offsets, e->keep_at, e->moves,
+                                                                       e->n_moves, e->mv_pos, e->moved, e->new_order);
             ss_note_launch(), k_apply_commit<<<2 * kNumSM, 256, 0, e->side>>>(e->order, e->offsets, e->new_order, e->new_off, (int)e->G,
                                                             e->P, e->moves, e->n_moves, e->pmap, e->moved);
             SS_CUDA(e, cudaGetLastError());
@@ -1452,8 +1457,12 @@ static int ensure_moves(ss_engine* e, int64_t want) {
     SS_CUDA(e, cudaStreamSynchronize(e->st));
     SS_CUDA(e, cudaStreamSynchronize(e->side));
     int rc;
-    if ((rc = dalloc(e, &e->moves, want)) || (rc = dalloc(e, &e->mv_next, want))) return rc;
+    if ((rc = dalloc(e, &e->moves, want)) || (rc = dalloc(e, &e->mv_next, want)) || (rc = dalloc(e, &e->mv_pos, want)))
+        return rc;
     e->cap_moves = (int)want;
+    // captured step graphs hold the old move buffers
+    for (auto& g : e->graphs) cudaGraphExecDestroy(g.exec);
+    e->graphs.clear();
     return SS_OK;
 }
 
