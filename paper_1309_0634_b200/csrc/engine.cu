@@ -985,7 +985,9 @@ static int launch_stats(ss_engine* e, int n_chunk, bool step = false, bool want_
     // otherwise a thread per group, coalesced over consecutive groups
     if (n_chunk > 32) {
         const unsigned grid = (unsigned)std::min<int64_t>((e->G + 31) / 32, 8 * kNumSM);
-        ss_note_launch(), k_batch_stats_cols<<<grid, kStatsWarps * 32, e->P * 8, e->st>>>(
+        const bool small = e->G <= 4096;
+        auto kern = small ? k_batch_stats_cols<32> : k_batch_stats_cols<16>;
+        ss_note_launch(), kern<<<grid, small ? 1024 : 512, e->P * 8, e->st>>>(
             e->gcnt, n_chunk, (uint32_t)e->G, e->pmap, e->P, e->gcount, step ? e->gkept : nullptr,
             step ? e->chunk_live : nullptr, e->tpt, e->touched, e->bad, e->fill, e->W, e->alg_bytes, e->trace_on ? 1 : 0,
             step && e->rank_place ? e->gpre : nullptr, want_work ? e->pwork : nullptr);

@@ -348,8 +348,10 @@ k_batch_stats(int32_t* __restrict__ gcnt, int n_chunk, uint32_t G, const int32_t
 // (shared memory), the never-stored runs -- a prefix of the group's chunks,
 // ending at the largest inclusive prefix <= K - W -- zeroed, then the kept
 // prefix of every live chunk (gpre, -1 elsewhere) and the live-chunk bits.
-constexpr int kStatsWarps = 16;
-
+// warps per CTA: 32 for small G (few CTAs, so more warps in flight each),
+// 16 otherwise (measured: C1 G=1K 12 -> 9.8 us with 32; C2 G=10K 15 us
+// with 16, slower with 32)
+template <int kStatsWarps>
 __global__ void __launch_bounds__(kStatsWarps * 32)
 k_batch_stats_cols(int32_t* __restrict__ gcnt, int n_chunk, uint32_t G, const int32_t* __restrict__ pmap,
                    int P, int32_t* __restrict__ gcount, int32_t* __restrict__ gkept,
