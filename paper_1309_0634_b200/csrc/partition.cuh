@@ -1098,11 +1098,11 @@ constexpr int kRankSub = 32 * kRankItems;          // tuples per sub-tile
 constexpr int kRankStages = 2;
 constexpr int kRankMaxG = 16384;
 #ifndef SS_RANK_BALLOT
-#define SS_RANK_BALLOT 1
+#define SS_RANK_BALLOT 2
 #endif
-// of every 2 rounds, how many match keys by ballots (ALU) -- the rest use
+// of every 4 rounds, how many match keys by ballots (ALU) -- the rest use
 // MATCH (MIO pipe), so both pipes share the ranking (measured at C2: 142 us
-// against 162 all-ballot and 168 all-MATCH)
+// with 2 of 4, against 162 all-ballot and 168 all-MATCH)
 constexpr int kRankBallot = SS_RANK_BALLOT;
 
 __host__ __device__ constexpr size_t rank_smem_bytes(uint32_t G) {
@@ -1191,7 +1191,7 @@ k_rank_place(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin, 
         unsigned peers[kRankItems];
 #pragma unroll
         for (int j = 0; j < kRankItems; ++j) {
-            if (BITS && (j & 1) < kRankBallot)
+            if (BITS && (j & 3) < kRankBallot)
                 peers[j] = FULL ? match_bits_all<BITS>(key[j]) : match_bits<BITS>(key[j], key[j] != 0xffffffffu);
             else
                 peers[j] = __match_any_sync(SS_FULL, key[j]);
