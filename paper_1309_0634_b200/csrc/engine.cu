@@ -1417,7 +1417,10 @@ static int enqueue_report(ss_engine* e, int64_t n, bool has_policy, cudaStream_t
     const bool used_plan = e->last_plan >= 0;
     ss_note_launch(), k_report<<<1, 1024, 0, st>>>(e->tpt, used_plan ? e->loads : nullptr, e->P, e->bad, e->touched, e->n_moves,
                                  e->prev_moves, e->scanned,
-                                 used_plan ? e->plan_buf[e->last_plan].n_split : nullptr, e->n_res, e->oom,
+                                 used_plan ? e->plan_buf[e->last_plan].n_split : nullptr,
+                                 // (the result-row count is read from n_res by the result calls; the
+                                 // side-stream report may run before finalize, so it is not copied here)
+                                 nullptr, e->oom,
                                  (long long)n, has_policy ? 1 : 0, e->d_rep);
     SS_CUDA(e, cudaGetLastError());
     SS_CUDA(e, cudaMemcpyAsync(e->h_rep, e->d_rep, sizeof(DevReport), cudaMemcpyDeviceToHost, st));
