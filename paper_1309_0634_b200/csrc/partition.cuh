@@ -102,14 +102,9 @@ k_count(const uint32_t* __restrict__ groups, int64_t n, uint32_t G, int64_t S, i
 // writes its row of gcnt with plain stores (no zeroing, no global atomics).
 // Each thread keeps four 128-bit loads in flight; a warp's load instruction
 // covers 512 contiguous bytes.
-__global__ void __launch_bounds__(512)
-k_count_rows(const uint32_t* __restrict__ groups, int64_t n, uint32_t G, int64_t S, int32_t* __restrict__ gcnt,
-             unsigned long long* __restrict__ bad, int vec_ok) {
-    extern __shared__ int32_t sh_hist[];
-    const int64_t c0 = (int64_t)blockIdx.x * S;
-    const int64_t c1 = min(n, c0 + S);
-    for (int i = threadIdx.x; i < (int)G; i += blockDim.x) sh_hist[i] = 0;
-    __syncthreads();
+// histogram of groups[c0, c1) into shared memory (zeroed by the caller)
+__device__ __forceinline__ void count_range(const uint32_t* __restrict__ groups, int64_t c0, int64_t c1, uint32_t G,
+                                            int32_t* sh_hist, unsigned long long* __restrict__ bad, int vec_ok) {
     constexpr int U = 4;                         // 128-bit loads in flight per thread
     const int64_t step = (int64_t)U * 4 * blockDim.x;
     int64_t base = c0;
@@ -134,6 +129,17 @@ k_count_rows(const uint32_t* __restrict__ groups, int64_t n, uint32_t G, int64_t
         if (g < G) atomicAdd(&sh_hist[g], 1);
         else atomicMin(bad, (unsigned long long)i);
     }
+}
+
+__global__ void __launch_bounds__(512)
+k_count_rows(const uint32_t* __restrict__ groups, int64_t n, uint32_t G, int64_t S, int32_t* __restrict__ gcnt,
+             unsigned long long* __restrict__ bad, int vec_ok) {
+    extern __shared__ int32_t sh_hist[];
+    const int64_t c0 = (int64_t)blockIdx.x * S;
+    const int64_t c1 = min(n, c0 + S);
+    for (int i = threadIdx.x; i < (int)G; i += blockDim.x) sh_hist[i] = 0;
+    __syncthreads();
+    count_range(groups, c0, c1, G, sh_hist, bad, vec_ok);
     __syncthreads();
     int32_t* dst = gcnt + (int64_t)blockIdx.x * G;
     for (int i = threadIdx.x; i < (int)G; i += blockDim.x) dst[i] = sh_hist[i];
