@@ -99,7 +99,8 @@ struct ss_engine {
     int32_t* gkept = nullptr;              // kept (possibly stored) tuples of each group in the batch
     int32_t* gpre = nullptr;               // [chunk][g] kept-count prefix over chunks (single-pass placement)
     uint32_t* pwork = nullptr;             // per-partition window-update work of the batch (k_batch_stats)
-    int32_t* cta_map = nullptr;            // work-proportional K4 grid [P+1]
+    int4* cta_map = nullptr;               // work-proportional K4 grid: slot of every CTA
+    int* cta_used = nullptr;
     bool rank_place = false;               // G <= kRankMaxG: k_rank_place instead of the radix passes
     int32_t* n_live = nullptr;             // kept tuples of the batch (device)
     uint32_t* chunk_live = nullptr;        // live-chunk bitmap
@@ -739,7 +740,9 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
     e->rank_place = G <= kRankMaxG && G * W >= e->max_batch;
     if (const char* rp = getenv("SS_B200_RANK_PLACE")) e->rank_place = G <= kRankMaxG && rp[0] != '0';
     if (e->rank_place && (rc = dalloc(e, &e->gpre, (size_t)nsub * G))) return rc;
-    if ((rc = dalloc(e, &e->pwork, e->P)) || (rc = dalloc(e, &e->cta_map, e->P + 1))) return rc;
+    if ((rc = dalloc(e, &e->pwork, e->P)) || (rc = dalloc(e, &e->cta_map, 4 * kNumSM + e->P)) ||
+        (rc = dalloc(e, &e->cta_used, 1)))
+        return rc;
     SS_CUDA(e, cudaMemsetAsync(e->pwork, 0, (size_t)e->P * 4, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->hot_of, 0xff, G * 4, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->n_hot_dev, 0, 4, e->st));
@@ -1328,9 +1331,10 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
         a.cpp = std::max(1, ((split || !has_policy) ? 2 : 8) * kNumSM / e->P);
         unsigned grid = (unsigned)(e->P * a.cpp);
         if (work_grid) {
-            ss_note_launch(), k_cta_map<<<1, 1024, 0, e->st>>>(e->pwork, e->P, k4_waves * kNumSM, e->cta_map);
+            ss_note_launch(), k_cta_map<<<1, 1024, 0, e->st>>>(e->pwork, e->P, k4_waves * kNumSM, e->cta_map,
+                                                               e->cta_used);
             a.cta_map = e->cta_map;
-            a.n_part = e->P;
+            a.n_used = e->cta_used;
             grid = (unsigned)(k4_waves * kNumSM + e->P);
         }
         ss_note_launch(), k_ingest<<<grid, kIngestThreads, kIngestSmem, e->st>>>(a);

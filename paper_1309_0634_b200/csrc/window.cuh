@@ -58,18 +58,19 @@ struct IngestArgs {
     unsigned long long* part_work;     // per-partition stored values
     const int32_t* n_live;      // live tuples of this sub-batch (0: nothing to do)
     int cpp;                    // CTAs sharing one partition's work (grid = P * cpp)
-    const int32_t* cta_map;     // or: work-proportional CTAs, partition p = [map[p], map[p+1])
-    int n_part;                 // P (with cta_map)
+    const int4* cta_map;        // or: work-proportional CTAs, (partition, sub, CTAs of it) per CTA
+    const int* n_used;          // CTAs in use (with cta_map)
     const unsigned long long* bad;
 };
 
 // Work-proportional K4 grid, for the group-reassignment policy without
 // hot-key splitting (a partition hosting a top group carries several times
 // the mean): partition p gets max(1, floor(total * work_p / sum)) CTAs,
-// partition-major, map[p] = its first CTA, map[P] = CTAs used (<= total +
-// P).  work_p comes from k_batch_stats; it is cleared for the next batch.
+// partition-major; map[b] = (partition, sub, its CTA count) of CTA b, so a
+// CTA finds its slot with one load; n_used = CTAs used (<= total + P).
+// work_p comes from k_batch_stats; it is cleared for the next batch.
 __global__ void __launch_bounds__(1024)
-k_cta_map(uint32_t* __restrict__ pwork, int P, int total, int32_t* __restrict__ map) {
+k_cta_map(uint32_t* __restrict__ pwork, int P, int total, int4* __restrict__ map, int* __restrict__ n_used) {
     __shared__ unsigned long long sh_sum[32];
     __shared__ int32_t sh_red[33];
     const int t = threadIdx.x;
@@ -90,8 +91,9 @@ k_cta_map(uint32_t* __restrict__ pwork, int P, int total, int32_t* __restrict__ 
     if (t < P) c = tot ? max(1, (int)((double)total * (double)w / (double)tot)) : 1;
     int all;
     const int ex = block_excl_scan(c, sh_red, &all);
-    if (t < P) map[t] = ex;
-    if (t == 0) map[P] = all;
+    // CTA slots of partition t: (t, sub, c) at [ex, ex + c)
+    for (int k = 0; k < c; ++k) map[ex + k] = make_int4(t, k, c, 0);
+    if (t == 0) *n_used = all;
 }
 
 // segmented (contiguous-lane segments) suffix reduction; the first lane
@@ -154,17 +156,12 @@ k_ingest(IngestArgs a) {
     // shares) are dealt to them round-robin
     int kCtaPerPart, p, sub;
     if (a.cta_map) {
-        // work-proportional: partition-major ranges of the CTA map
-        const int bx = (int)blockIdx.x;
-        if (bx >= a.cta_map[a.n_part]) return;
-        int l = 0, h = a.n_part - 1;             // last p with map[p] <= bx
-        while (l < h) {
-            const int mid = (l + h + 1) >> 1;
-            if (a.cta_map[mid] <= bx) l = mid; else h = mid - 1;
-        }
-        p = l;
-        sub = bx - a.cta_map[p];
-        kCtaPerPart = a.cta_map[p + 1] - a.cta_map[p];
+        // work-proportional: one 16-byte load gives this CTA's slot
+        if ((int)blockIdx.x >= *a.n_used) return;
+        const int4 m = a.cta_map[blockIdx.x];
+        p = m.x;
+        sub = m.y;
+        kCtaPerPart = m.z;
     } else {
         // partition-minor order: the first resident wave holds CTA 0 (and 1)
         // of every partition, later CTAs of a heavy partition start as light
