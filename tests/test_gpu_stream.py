@@ -143,13 +143,15 @@ def test_device_trace_matches_reference_serial_trace(golden):
         store.engine.close()
 
 
+@pytest.mark.parametrize("rank", ["1", "0"])
 @pytest.mark.parametrize("W", [3, 1000])
-def test_trace_and_ingest_sequence_sums(W):
+def test_trace_and_ingest_sequence_sums(monkeypatch, W, rank):
     """Trace mode on the fused step with evictions from the old window and
     from the batch itself; ingest_sequence(want_sums) returns them in input
     order; the windows stay equal to the oracle."""
     import paper_1309_0634_b200 as ss
     from paper_1309_0634_b200.stream_engine import StreamEngine
+    monkeypatch.setenv("SS_B200_RANK_PLACE", rank)     # both placement paths
     G, B = 300, 20_000
     spec = D.DatasetSpec(D.DatasetKind.ZIPF, 4 * B, G, 1.2, 8)
     bl = list(D.batches(D.stream_for(spec), B))
