@@ -692,10 +692,13 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
     // (a chunk with no kept tuple is never read again).  Power of two >=
     // 2^16, grown until the per-chunk histograms (n_chunk x G) stay <= 2^22
     // entries and n_chunk <= 4096.
+    // (2^12..2^14-tuple chunks for few groups measured slower at C1: the
+    // stats cost grows faster than the placement gains)
+    const int s_min_log = 16;
     int64_t S = cfg->sub_batch;
-    if (S <= 0) S = int64_t(1) << 16;
+    if (S <= 0) S = int64_t(1) << s_min_log;
     {
-        int64_t p2 = int64_t(1) << 16;
+        int64_t p2 = int64_t(1) << s_min_log;
         while (p2 < S) p2 <<= 1;
         S = p2;
         auto nch = [&](int64_t c) { return (e->max_batch + c - 1) / c; };
