@@ -9,12 +9,15 @@
 //                                       contiguous placement
 //   ingest_sequence engine.py:274-280   stable regroup preserving arrival order
 //
-// B200 design: a batch is counted once (warp-aggregated atomics, one atomic
-// per distinct key per warp) into per-sub-batch group histograms.  Each
-// L2-sized sub-batch is then placed by a stable LSD multisplit whose passes
-// use decoupled look-back (one pass when G <= 2^11, two up to 2^22).  The
-// stable placement gives every tuple its exact arrival rank inside its
-// group as (position - group start), which is all the window update needs.
+// B200 design: a batch is counted once into per-chunk group histograms
+// (shared memory per chunk for G <= 16K, else warp-aggregated atomics).
+// The kept tuples are then placed stably by group: for G <= 2^14 in ONE
+// pass (k_rank_place: a CTA per live chunk, group cursors in shared
+// memory advanced in arrival order), otherwise by an LSD multisplit whose
+// passes use decoupled look-back (one pass when G <= 2^11, two up to
+// 2^22).  The stable placement gives every tuple its exact arrival rank
+// inside its group as (position - group start), which is all the window
+// update needs.
 #pragma once
 
 #include <type_traits>
