@@ -275,14 +275,24 @@ k_ingest(IngestArgs a) {
 
         SS_PT4(2);
         // ---- long members: one warp per unit of kUnit contiguous values ----
-        for (int u = csub * nw + warp_id(); u < u_total; u += cstride * nw) {
+        // The member lookup of the warp's next unit (a binary search over
+        // the unit scan plus the member's fields, all shared memory) is done
+        // while the current unit's global loads are in flight.
+        struct UnitRef { int mi, r0; };
+        auto find_unit = [&](int u) -> UnitRef {
             int mi = 0;                                 // last member with m_uscan[mi] <= u
 #pragma unroll
             for (int step = kMemberChunk / 2; step >= 1; step >>= 1) {
                 const int c = mi + step;
                 if (c < m && m_uscan[c] <= u) mi = c;
             }
-            const int r0 = (u - m_uscan[mi]) * kUnit;
+            return UnitRef{mi, (u - m_uscan[mi]) * kUnit};
+        };
+        const int ustride = cstride * nw;
+        int u = csub * nw + warp_id();
+        UnitRef cur = u < u_total ? find_unit(u) : UnitRef{0, 0};
+        for (; u < u_total; u += ustride) {
+            const int mi = cur.mi, r0 = cur.r0;
             const int w = m_w[mi];
             const int start = m_start[mi], q0 = m_q0[mi], s0 = m_s0[mi], f0 = m_f0[mi];
             const int64_t offg = m_off[mi];
@@ -306,6 +316,7 @@ k_ingest(IngestArgs a) {
                 if (sl >= W) sl -= W;
                 old[k] = (r < w && qq < f0) ? rg[sl] : 0;
             }
+            if (u + ustride < u_total) cur = find_unit(u + ustride);
             long long d = 0;
             int32_t mnv = 0x7fffffff, mxv = (int32_t)0x80000000;
 #pragma unroll
