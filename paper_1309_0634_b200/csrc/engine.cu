@@ -99,6 +99,7 @@ struct ss_engine {
     int32_t* gkept = nullptr;              // kept (possibly stored) tuples of each group in the batch
     int32_t* gpre = nullptr;               // [chunk][g] kept-count prefix over chunks (single-pass placement)
     uint32_t* pwork = nullptr;             // per-partition window-update work of the batch (k_batch_stats)
+    int* any_dead = nullptr;               // some tuple of the batch is never stored (set by k_batch_stats)
     int4* cta_map = nullptr;               // work-proportional K4 grid: slot of every CTA
     int* cta_used = nullptr;
     bool rank_place = false;               // G <= kRankMaxG: k_rank_place instead of the radix passes
@@ -744,7 +745,7 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
     if (const char* rp = getenv("SS_B200_RANK_PLACE")) e->rank_place = G <= kRankMaxG && rp[0] != '0';
     if (e->rank_place && (rc = dalloc(e, &e->gpre, (size_t)nsub * G))) return rc;
     if ((rc = dalloc(e, &e->pwork, e->P)) || (rc = dalloc(e, &e->cta_map, 4 * kNumSM + e->P)) ||
-        (rc = dalloc(e, &e->cta_used, 1)))
+        (rc = dalloc(e, &e->cta_used, 1)) || (rc = dalloc(e, &e->any_dead, 1)))
         return rc;
     SS_CUDA(e, cudaMemsetAsync(e->pwork, 0, (size_t)e->P * 4, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->hot_of, 0xff, G * 4, e->st));
@@ -987,6 +988,7 @@ static int launch_count(ss_engine* e, const uint32_t* dk, int64_t n, int64_t S, 
 static int launch_stats(ss_engine* e, int n_chunk, bool step = false, bool want_work = false) {
     SS_CUDA(e, cudaMemsetAsync(e->tpt, 0, e->P * 8, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->touched, 0, 8, e->st));
+    if (step) SS_CUDA(e, cudaMemsetAsync(e->any_dead, 0, 4, e->st));
     // many chunks (> 32): a CTA per 32 groups, warps over chunk ranges;
     // otherwise a thread per group, coalesced over consecutive groups
     if (n_chunk > 32) {
@@ -996,13 +998,13 @@ static int launch_stats(ss_engine* e, int n_chunk, bool step = false, bool want_
         ss_note_launch(), kern<<<grid, small ? 1024 : 512, e->P * 8, e->st>>>(
             e->gcnt, n_chunk, (uint32_t)e->G, e->pmap, e->P, e->gcount, step ? e->gkept : nullptr,
             step ? e->chunk_live : nullptr, e->tpt, e->touched, e->bad, e->fill, e->W, e->alg_bytes, e->trace_on ? 1 : 0,
-            step && e->rank_place ? e->gpre : nullptr, want_work ? e->pwork : nullptr);
+            step && e->rank_place ? e->gpre : nullptr, want_work ? e->pwork : nullptr, step ? e->any_dead : nullptr);
     } else {
         const unsigned grid = (unsigned)std::min<int64_t>((e->G + 255) / 256, 16 * kNumSM);
         ss_note_launch(), k_batch_stats<false><<<grid, 256, e->P * 8, e->st>>>(
             e->gcnt, n_chunk, (uint32_t)e->G, e->pmap, e->P, e->gcount, step ? e->gkept : nullptr,
             step ? e->chunk_live : nullptr, e->tpt, e->touched, e->bad, e->fill, e->W, e->alg_bytes, e->trace_on ? 1 : 0,
-            step && e->rank_place ? e->gpre : nullptr, want_work ? e->pwork : nullptr);
+            step && e->rank_place ? e->gpre : nullptr, want_work ? e->pwork : nullptr, step ? e->any_dead : nullptr);
     }
     SS_CUDA(e, cudaGetLastError());
     return SS_OK;
@@ -1092,6 +1094,7 @@ static int launch_place_step(ss_engine* e, const uint32_t* dk, const int32_t* dv
     s1.chunk_shift = cs;
     s1.G = (uint32_t)e->G;
     s1.cbase = e->chunk_base;
+    s1.any_dead = e->any_dead;
     if (e->plan.npass == 1) {
         sort_dispatch(e->rb[0], e->st, dk, dv, e->trace_on ? e->kbuf2 : nullptr, e->vbuf[0], (int)n, 0, m0, base0,
                       e->status, e->ep_dev, 0,

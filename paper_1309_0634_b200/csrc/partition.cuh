@@ -210,7 +210,7 @@ k_batch_stats(int32_t* __restrict__ gcnt, int n_chunk, uint32_t G, const int32_t
               unsigned long long* __restrict__ tpt, unsigned long long* __restrict__ touched,
               const unsigned long long* __restrict__ bad, const int32_t* __restrict__ fill, int64_t W,
               unsigned long long* __restrict__ alg_bytes, int nodrop, int32_t* __restrict__ gpre = nullptr,
-              uint32_t* __restrict__ pwork = nullptr) {
+              uint32_t* __restrict__ pwork = nullptr, int* __restrict__ any_dead = nullptr) {
     extern __shared__ uint32_t sh_tpt[];     // per-CTA partial loads (< 2^31)
     __shared__ uint32_t sh_live[kMaxChunkWords];
     if (*bad != (unsigned long long)kNoBad) return;
@@ -305,8 +305,10 @@ k_batch_stats(int32_t* __restrict__ gcnt, int n_chunk, uint32_t G, const int32_t
                     const int64_t idx = (int64_t)s * G + g;
                     const int32_t k = gcnt[idx];
                     if (k) {
-                        if ((int64_t)pre + k <= (int64_t)c - W) gcnt[idx] = 0;
-                        else {
+                        if ((int64_t)pre + k <= (int64_t)c - W) {
+                            gcnt[idx] = 0;
+                            if (any_dead) *any_dead = 1;
+                        } else {
                             kept += k;
                             lbits |= 1u << s;
                         }
@@ -367,7 +369,7 @@ k_batch_stats_cols(int32_t* __restrict__ gcnt, int n_chunk, uint32_t G, const in
                    uint32_t* __restrict__ chunk_live, unsigned long long* __restrict__ tpt,
                    unsigned long long* __restrict__ touched, const unsigned long long* __restrict__ bad,
                    const int32_t* __restrict__ fill, int64_t W, unsigned long long* __restrict__ alg_bytes,
-                   int nodrop, int32_t* __restrict__ gpre, uint32_t* __restrict__ pwork) {
+                   int nodrop, int32_t* __restrict__ gpre, uint32_t* __restrict__ pwork, int* __restrict__ any_dead) {
     extern __shared__ uint32_t sh_tpt[];     // per-CTA partial loads (< 2^31), then partition work
     __shared__ uint32_t sh_live[kMaxChunkWords];
     __shared__ int32_t sh_part[kStatsWarps][32];
@@ -416,6 +418,7 @@ k_batch_stats_cols(int32_t* __restrict__ gcnt, int n_chunk, uint32_t G, const in
                 if (k && (int64_t)pre + k <= (int64_t)C - W) {
                     gcnt[idx] = 0;
                     dmax = pre + k;
+                    if (any_dead) *any_dead = 1;
                 }
                 pre += k;
             }
@@ -736,6 +739,7 @@ struct SortSeg {
     int nb;
     int b0;
     const int32_t* gstart;      // mode 2: run start of every group
+    const int* any_dead;        // mode 1: 0 = no tuple of the batch is dropped (skip the kept lookups)
 };
 
 // per-live-chunk histogram of the first digit over the kept counts.
@@ -829,6 +833,8 @@ k_sort_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
     if (n_dev && seg.mode != 1) n = *n_dev;      // consumes a compacted (kept-only) input
     const unsigned w = warp_id(), lane = lane_id();
     const int wbase = (int)w * 32 * kSortItems;
+    // nothing dropped in this batch (no group above W): every staged tuple is kept
+    const bool no_dead = seg.mode == 1 && seg.any_dead && *seg.any_dead == 0;
     // second-pass bucket tile prefix, searched by every claim: staged in
     // shared memory once per CTA
     __shared__ int32_t sh_btile[kMaxBins + 1];
@@ -923,7 +929,7 @@ k_sort_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
     cp_async_wait_0();                           // this thread's copies of the current tile have landed
     uint32_t* skey = in_k + cur * kSortTile;     // staged input, then the tile-local sort buffer
     int32_t* sval = in_v + cur * kSortTile;
-    if (seg.mode == 1) live = seg.live + (int64_t)seg.lc[seg_id] * seg.G;   // the chunk's kept counts
+    if (seg.mode == 1 && !no_dead) live = seg.live + (int64_t)seg.lc[seg_id] * seg.G;   // the chunk's kept counts
     uint16_t* myh = whist + w * BINS;
 
     uint32_t key[kSortItems];
