@@ -356,7 +356,19 @@ def main():
     clocks = ClockSampler(local)
     barrier()
     clocks.start()
-    time.sleep(0.3)
+    # keep the GPU busy while the clock sampler starts (>= 0.3 s of further
+    # untimed steps, counted in the reported warm-up), so the timed region
+    # starts from a loaded, steady-state GPU instead of an idle gap
+    # (with several ranks every rank runs the same fixed count: the steps
+    # contain collectives)
+    t_end = time.time() + 0.3
+    extra = 0
+    while (time.time() < t_end) if world == 1 else (extra < 64):
+        run_steps(1, args.warmup + extra)
+        extra += 1
+        torch.cuda.synchronize()
+    args.warmup += extra
+    barrier()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     lib = L.load()
