@@ -11,10 +11,12 @@
 //
 // One CTA runs the policy's sequential loop for the whole GPU while the
 // rest of the chip executes the batch (the moves only take effect at the
-// next batch, harness.py:115-116).  The per-partition loads live in shared
-// memory; donor picks that scan a partition's groups (check_all,
-// prob_check, best_balance) are CTA-wide reductions over the partition's
-// ENTRY list (the list at batch start).  Working lists never need to be
+// next batch, harness.py:115-116).  The per-partition loads (and, for
+// G <= kBalStageG, the entry lists and counts) live in shared memory; the
+// extreme-pair policies run in one warp: donor picks that scan a
+// partition's groups (check_all, prob_check, best_balance) are warp
+// reductions over the partition's ENTRY list (the list at batch start).
+// Working lists never need to be
 // materialised: a group moves at most once per invocation, so a working
 // list is  [fronts pushed into it, newest first] ++ [entry members not yet
 // moved] ++ [backs pushed into it, in order].
@@ -128,92 +130,11 @@ __device__ void bal_move(const BalanceArgs& a, const BalSmem& s, int* nm, int g,
     *nm = mi + 1;
 }
 
-struct ArgPair { long long v; int i; };
-
-// CTA-wide argmax and argmin of loads, lowest index on ties
-__device__ void bal_extremes(const BalSmem& s, int P, int* hi, int* lo, long long* red_v, int* red_i) {
-    long long vmax = LLONG_MIN, vmin = LLONG_MAX;
-    int imax = 0x7fffffff, imin = 0x7fffffff;
-    for (int p = threadIdx.x; p < P; p += blockDim.x) {
-        const long long v = s.loads[p];
-        if (v > vmax) { vmax = v; imax = p; }
-        if (v < vmin) { vmin = v; imin = p; }
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        const long long ov = __shfl_xor_sync(SS_FULL, vmax, o);
-        const int oi = __shfl_xor_sync(SS_FULL, imax, o);
-        if (ov > vmax || (ov == vmax && oi < imax)) { vmax = ov; imax = oi; }
-        const long long nv = __shfl_xor_sync(SS_FULL, vmin, o);
-        const int ni = __shfl_xor_sync(SS_FULL, imin, o);
-        if (nv < vmin || (nv == vmin && ni < imin)) { vmin = nv; imin = ni; }
-    }
-    const int w = warp_id(), nw = blockDim.x >> 5;
-    if (lane_id() == 0) {
-        red_v[w] = vmax; red_i[w] = imax;
-        red_v[32 + w] = vmin; red_i[32 + w] = imin;
-    }
-    __syncthreads();
-    if (w == 0) {
-        vmax = lane_id() < (unsigned)nw ? red_v[lane_id()] : LLONG_MIN;
-        imax = lane_id() < (unsigned)nw ? red_i[lane_id()] : 0x7fffffff;
-        vmin = lane_id() < (unsigned)nw ? red_v[32 + lane_id()] : LLONG_MAX;
-        imin = lane_id() < (unsigned)nw ? red_i[32 + lane_id()] : 0x7fffffff;
-#pragma unroll
-        for (int o = 16; o; o >>= 1) {
-            const long long ov = __shfl_xor_sync(SS_FULL, vmax, o);
-            const int oi = __shfl_xor_sync(SS_FULL, imax, o);
-            if (ov > vmax || (ov == vmax && oi < imax)) { vmax = ov; imax = oi; }
-            const long long nv = __shfl_xor_sync(SS_FULL, vmin, o);
-            const int ni = __shfl_xor_sync(SS_FULL, imin, o);
-            if (nv < vmin || (nv == vmin && ni < imin)) { vmin = nv; imin = ni; }
-        }
-        if (lane_id() == 0) { red_i[64] = imax; red_i[65] = imin; }
-    }
-    __syncthreads();
-    *hi = red_i[64];
-    *lo = red_i[65];
-    __syncthreads();
-}
-
-// Lexicographic CTA reduction of (key, group) -> smallest.  Returns group
-// (or INT_MAX) to every thread.
-__device__ void bal_argmin_key(long long key, int g, long long* red_v, int* red_i, long long* out_key,
-                               int* out_g) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        const long long ok = __shfl_xor_sync(SS_FULL, key, o);
-        const int og = __shfl_xor_sync(SS_FULL, g, o);
-        if (ok < key || (ok == key && og < g)) { key = ok; g = og; }
-    }
-    const int w = warp_id(), nw = blockDim.x >> 5;
-    if (lane_id() == 0) { red_v[w] = key; red_i[w] = g; }
-    __syncthreads();
-    if (w == 0) {
-        key = lane_id() < (unsigned)nw ? red_v[lane_id()] : LLONG_MAX;
-        g = lane_id() < (unsigned)nw ? red_i[lane_id()] : 0x7fffffff;
-#pragma unroll
-        for (int o = 16; o; o >>= 1) {
-            const long long ok = __shfl_xor_sync(SS_FULL, key, o);
-            const int og = __shfl_xor_sync(SS_FULL, g, o);
-            if (ok < key || (ok == key && og < g)) { key = ok; g = og; }
-        }
-        if (lane_id() == 0) { red_v[66] = key; red_i[66] = g; }
-    }
-    __syncthreads();
-    *out_key = red_v[66];
-    *out_g = red_i[66];
-    __syncthreads();
-}
-
 template <bool STAGED>
 __global__ void __launch_bounds__(kBalThreads)
 k_balance(BalanceArgs a) {
     extern __shared__ long long bal_sm[];
-    __shared__ long long red_v[72];
     __shared__ int red_i[72];
-    __shared__ int sh_ctl[4];
-    __shared__ long long sh_scan[2];
     const int P = a.P;
     BalSmem s;
     s.loads = bal_sm;
@@ -447,72 +368,8 @@ k_balance(BalanceArgs a) {
 
 // ---- device apply_moves (partition.py:181-203) ------------------------------
 // new list(p) = fronts pushed into p (newest first) ++ entry members of p
-// that did not move ++ backs pushed into p (in order).  Sizes first:
-__global__ void __launch_bounds__(1024)
-k_apply_sizes(const int32_t* __restrict__ offsets, int P, const int4* __restrict__ moves,
-              const int* __restrict__ n_moves, int32_t* __restrict__ new_off) {
-    __shared__ int32_t red[33];
-    __shared__ int32_t carry;
-    const int nm = *n_moves;
-    if (nm == 0) return;
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
-    for (int p0 = 0; p0 < P; p0 += blockDim.x) {
-        const int p = p0 + threadIdx.x;
-        int32_t sz = 0;
-        if (p < P) {
-            sz = offsets[p + 1] - offsets[p];
-            for (int i = 0; i < nm; ++i) {
-                const int4 m = moves[i];
-                sz += (m.z == p) - (m.y == p);
-            }
-        }
-        int32_t tot;
-        const int32_t ex = block_excl_scan(sz, red, &tot);
-        if (p < P) new_off[p] = carry + ex;
-        __syncthreads();
-        if (threadIdx.x == 0) carry += tot;
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) new_off[P] = carry;
-}
-
-// one CTA per partition
-__global__ void __launch_bounds__(256)
-k_apply_build(const int32_t* __restrict__ order, const int32_t* __restrict__ offsets,
-              const int32_t* __restrict__ new_off, const int4* __restrict__ moves,
-              const int* __restrict__ n_moves, const int* __restrict__ front_top,
-              const int* __restrict__ back_first, const int* __restrict__ mv_next,
-              const uint8_t* __restrict__ moved, int32_t* __restrict__ new_order) {
-    __shared__ int32_t red[33];
-    if (*n_moves == 0) return;
-    const int p = blockIdx.x;
-    int pos = new_off[p];
-    if (threadIdx.x == 0) {
-        for (int mi = front_top[p]; mi >= 0; mi = mv_next[mi]) new_order[pos++] = moves[mi].x;
-        red[32] = pos;
-    }
-    __syncthreads();
-    pos = red[32];
-    __syncthreads();
-    const int e0 = offsets[p], e1 = offsets[p + 1];
-    for (int c0 = e0; c0 < e1; c0 += blockDim.x) {
-        const int i = c0 + threadIdx.x;
-        int g = -1;
-        int keep = 0;
-        if (i < e1) {
-            g = order[i];
-            keep = !moved[g];
-        }
-        int32_t tot;
-        const int32_t ex = block_excl_scan(keep, red, &tot);
-        if (keep) new_order[pos + ex] = g;
-        pos += tot;
-    }
-    if (threadIdx.x == 0)
-        for (int mi = back_first[p]; mi >= 0; mi = mv_next[mi]) new_order[pos++] = moves[mi].x;
-}
-
+// that did not move ++ backs pushed into p (in order); k_balance lays the
+// new lists out (offsets, unmoved-member starts, move positions).
 // fused step: the rebuilt lists from the layout k_balance computed (one
 // CTA per partition places its unmoved entry members; the moved groups are
 // scattered to their positions by all CTAs)

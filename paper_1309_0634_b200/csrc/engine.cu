@@ -1001,7 +1001,7 @@ static int launch_stats(ss_engine* e, int n_chunk, bool step = false, bool want_
             step && e->rank_place ? e->gpre : nullptr, want_work ? e->pwork : nullptr, step ? e->any_dead : nullptr);
     } else {
         const unsigned grid = (unsigned)std::min<int64_t>((e->G + 255) / 256, 16 * kNumSM);
-        ss_note_launch(), k_batch_stats<false><<<grid, 256, e->P * 8, e->st>>>(
+        ss_note_launch(), k_batch_stats<<<grid, 256, e->P * 8, e->st>>>(
             e->gcnt, n_chunk, (uint32_t)e->G, e->pmap, e->P, e->gcount, step ? e->gkept : nullptr,
             step ? e->chunk_live : nullptr, e->tpt, e->touched, e->bad, e->fill, e->W, e->alg_bytes, e->trace_on ? 1 : 0,
             step && e->rank_place ? e->gpre : nullptr, want_work ? e->pwork : nullptr, step ? e->any_dead : nullptr);

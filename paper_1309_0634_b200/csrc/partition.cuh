@@ -196,14 +196,10 @@ __device__ __forceinline__ void stats_account(uint32_t g, int32_t c, const int32
     atomicAdd(&sh_tpt[P + p], (uint32_t)min64(stored + retracted + 16, 0x3fffffff));
 }
 
-// WARP = true: one warp per group, lanes over the chunks (many chunks, few
-// groups); WARP = false: one thread per group (few chunks).
-// chunk_live is a bitmap (bit c of word c / 32): lanes hold chunk i*32+lane,
-// so a ballot gives a warp's live bits for 32 chunks; warps OR them into a
-// shared bitmap and each CTA ORs its words into the global one once.
+// Few chunks (<= 32): one thread per group, coalesced over consecutive
+// groups; chunk_live is a bitmap (bit c of word c / 32).
 constexpr int kMaxChunkWords = 4096 / 32;
 
-template <bool WARP>
 __global__ void __launch_bounds__(1024)
 k_batch_stats(int32_t* __restrict__ gcnt, int n_chunk, uint32_t G, const int32_t* __restrict__ pmap,
               int P, int32_t* __restrict__ gcount, int32_t* __restrict__ gkept, uint32_t* __restrict__ chunk_live,
@@ -221,119 +217,47 @@ k_batch_stats(int32_t* __restrict__ gcnt, int n_chunk, uint32_t G, const int32_t
     uint32_t my_touched = 0;
     unsigned long long my_bytes = 0;
     const unsigned lane = lane_id();
-    if (WARP) {
-        // up to RK x 32 chunk counts per warp stay in registers; the live
-        // bits of those chunks are accumulated per warp in lb[]
-        constexpr int RK = 8;
-        uint32_t lb[RK];
-#pragma unroll
-        for (int i = 0; i < RK; ++i) lb[i] = 0;
-        const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
-        for (uint32_t g = blockIdx.x * (blockDim.x >> 5) + warp_id(); g < G; g += nwarps) {
-            int32_t kr[RK];
-            int32_t c = 0;
-#pragma unroll
-            for (int i = 0; i < RK; ++i) {
-                const int s = i * 32 + (int)lane;
-                kr[i] = (s < n_chunk) ? gcnt[(int64_t)s * G + g] : 0;
-                c += kr[i];
-            }
-            for (int s = RK * 32 + lane; s < n_chunk; s += 32) c += gcnt[(int64_t)s * G + g];
-            c = warp_sum(c);
-            int32_t kept = c;
-            const bool drop = c > W && gkept && !nodrop;
-            int32_t carry = 0, lcarry = 0;
-            if (drop) kept = 0;
-            for (int s0 = 0; s0 < n_chunk; s0 += 32) {
-                const int s = s0 + (int)lane;
+    uint32_t lbits = 0;                      // n_chunk <= 32 here
+    for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < G; g += gridDim.x * blockDim.x) {
+        int32_t c = 0;
+        for (int s = 0; s < n_chunk; ++s) c += gcnt[(int64_t)s * G + g];
+        gcount[g] = c;
+        int32_t kept = c;
+        if (c > W && gkept && !nodrop) {
+            int32_t pre = 0;
+            kept = 0;
+            for (int s = 0; s < n_chunk; ++s) {
                 const int64_t idx = (int64_t)s * G + g;
-                int32_t k = 0;
-#pragma unroll
-                for (int i = 0; i < RK; ++i)
-                    if (s0 == i * 32) k = kr[i];
-                if (s0 >= RK * 32) k = (s < n_chunk) ? gcnt[idx] : 0;
-                bool live = k != 0;
-                if (drop) {
-                    const int32_t incl = warp_incl_scan(k);
-                    const int32_t pre = carry + incl - k;
-                    if (k && (int64_t)pre + k <= (int64_t)c - W) {
+                const int32_t k = gcnt[idx];
+                if (k) {
+                    if ((int64_t)pre + k <= (int64_t)c - W) {
                         gcnt[idx] = 0;
-                        live = false;
+                        if (any_dead) *any_dead = 1;
+                    } else {
+                        kept += k;
+                        lbits |= 1u << s;
                     }
-                    if (live) kept += k;
-                    carry += __shfl_sync(SS_FULL, incl, 31);
                 }
-                if (gpre) {
-                    // exclusive prefix of the kept counts over the chunks (-1: not stored)
-                    const int32_t kl = live ? k : 0;
-                    const int32_t il = warp_incl_scan(kl);
-                    if (s < n_chunk) gpre[idx] = live ? lcarry + il - kl : -1;
-                    lcarry += __shfl_sync(SS_FULL, il, 31);
-                }
-                const uint32_t bits = __ballot_sync(SS_FULL, live);
-                if (chunk_live && bits) {
-                    bool held = false;
-#pragma unroll
-                    for (int i = 0; i < RK; ++i)
-                        if (s0 == i * 32) { lb[i] |= bits; held = true; }
-                    if (!held && lane == 0) atomicOr(&sh_live[s0 >> 5], bits);
-                }
+                pre += k;
             }
-            if (drop) kept = warp_sum(kept);
-            if (lane == 0) {
-                gcount[g] = c;
-                if (gkept) gkept[g] = kept;
-                if (c) stats_account(g, c, pmap, sh_tpt, fill, W, my_touched, my_bytes, P);
+        } else if (c) {
+            for (int s = 0; s < n_chunk; ++s)
+                if (gcnt[(int64_t)s * G + g]) lbits |= 1u << s;
+        }
+        if (gkept) gkept[g] = kept;
+        if (gpre) {
+            int32_t pre = 0;
+            for (int s = 0; s < n_chunk; ++s) {
+                const int64_t idx = (int64_t)s * G + g;
+                const int32_t k = gcnt[idx];
+                gpre[idx] = k ? pre : -1;
+                pre += k;
             }
         }
-        if (chunk_live && lane == 0) {
-#pragma unroll
-            for (int i = 0; i < RK; ++i)
-                if (lb[i]) atomicOr(&sh_live[i], lb[i]);
-        }
-    } else {
-        uint32_t lbits = 0;                      // n_chunk <= 32 here
-        for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < G; g += gridDim.x * blockDim.x) {
-            int32_t c = 0;
-            for (int s = 0; s < n_chunk; ++s) c += gcnt[(int64_t)s * G + g];
-            gcount[g] = c;
-            int32_t kept = c;
-            if (c > W && gkept && !nodrop) {
-                int32_t pre = 0;
-                kept = 0;
-                for (int s = 0; s < n_chunk; ++s) {
-                    const int64_t idx = (int64_t)s * G + g;
-                    const int32_t k = gcnt[idx];
-                    if (k) {
-                        if ((int64_t)pre + k <= (int64_t)c - W) {
-                            gcnt[idx] = 0;
-                            if (any_dead) *any_dead = 1;
-                        } else {
-                            kept += k;
-                            lbits |= 1u << s;
-                        }
-                    }
-                    pre += k;
-                }
-            } else if (c) {
-                for (int s = 0; s < n_chunk; ++s)
-                    if (gcnt[(int64_t)s * G + g]) lbits |= 1u << s;
-            }
-            if (gkept) gkept[g] = kept;
-            if (gpre) {
-                int32_t pre = 0;
-                for (int s = 0; s < n_chunk; ++s) {
-                    const int64_t idx = (int64_t)s * G + g;
-                    const int32_t k = gcnt[idx];
-                    gpre[idx] = k ? pre : -1;
-                    pre += k;
-                }
-            }
-            if (c) stats_account(g, c, pmap, sh_tpt, fill, W, my_touched, my_bytes, P);
-        }
-        lbits = __reduce_or_sync(SS_FULL, lbits);
-        if (chunk_live && lane == 0 && lbits) atomicOr(&sh_live[0], lbits);
+        if (c) stats_account(g, c, pmap, sh_tpt, fill, W, my_touched, my_bytes, P);
     }
+    lbits = __reduce_or_sync(SS_FULL, lbits);
+    if (chunk_live && lane == 0 && lbits) atomicOr(&sh_live[0], lbits);
     my_touched = warp_sum(my_touched);
     my_bytes = warp_sum(my_bytes);
     if (lane == 0 && my_touched) {
