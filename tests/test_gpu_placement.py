@@ -43,3 +43,31 @@ def test_placement_paths(monkeypatch, rank, G, W, s, B, policy, split):
     assert np.array_equal(snap["window_sum"], wsum)
     assert np.array_equal(snap["min"][t], mn[t]) and np.array_equal(snap["max"][t], mx[t])
     eng.close()
+
+
+@pytest.mark.parametrize("P", [148, 700])
+def test_work_grid_extreme_skew(P):
+    """The reassignment policy without splitting under extreme skew (one
+    group holds most of the batch): the window update runs on the
+    work-proportional CTA grid; windows stay exact over several batches."""
+    import torch
+    from paper_1309_0634_b200.stream_engine import StreamEngine
+    G, W, B = 5000, 200_000, 1 << 21
+    rng = np.random.default_rng(P)
+    eng = StreamEngine(G, W, n_partitions=P, aggregates=("count", "sum", "avg", "min", "max"),
+                       max_batch=B, initial="hash")
+    bal = StreamEngine.balancer_struct("prob", max(1, B // (10 * P)), 0.5, split=False)
+    gs, avs = [], []
+    for i in range(4):
+        g = _zipf(B, G, 2.0, rng)
+        a = rng.integers(-2 ** 31, 2 ** 31, B, dtype=np.int64)
+        eng.step(torch.from_numpy(g.astype(np.int32)).cuda(), torch.from_numpy(a.astype(np.int32)).cuda(), bal)
+        gs.append(g)
+        avs.append(a)
+    fill, wsum, mn, mx, nxt, t = _expected(np.concatenate(gs), np.concatenate(avs), G, W)
+    snap = eng.snapshot()
+    assert np.array_equal(snap["fill"], fill)
+    assert np.array_equal(snap["next_pos"], nxt)
+    assert np.array_equal(snap["window_sum"], wsum)
+    assert np.array_equal(snap["min"][t], mn[t]) and np.array_equal(snap["max"][t], mx[t])
+    eng.close()
