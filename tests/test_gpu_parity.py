@@ -182,9 +182,11 @@ def test_pipeline_golden(golden):
 @pytest.mark.parametrize("policy", ["no", "first", "all", "prob", "best", "shift", "shiftlocal"])
 @pytest.mark.parametrize("G,W,P,B,sub", [(1000, 1000, 148, 1 << 17, 1 << 15),
                                          (10_000, 300, 64, 50_000, 16384),
-                                         (5000, 7, 37, 30_000, 0)])
+                                         (5000, 7, 37, 30_000, 0),
+                                         (20_000, 500, 48, 40_000, 0)])
 def test_step_vs_oracle(policy, G, W, P, B, sub):
-    """Multi-sub-batch, one- and two-pass placement, every policy."""
+    """Multi-sub-batch, single-pass and one-/two-pass radix placement, every
+    policy (G > 2^14: the policy CTA reads the lists from global memory)."""
     from paper_1309_0634_b200.stream_engine import StreamEngine
     spec = D.DatasetSpec(D.DatasetKind.ZIPF, 4 * B, G, 1.1, 23)
     eng = _engine(G, W, P=P, sub_batch=sub, aggregates=("count", "sum", "avg", "min", "max"),
