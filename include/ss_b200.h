@@ -225,14 +225,20 @@ int  ss_profile_read(ss_engine* e, double* ms, int64_t* launches, int reset);
  * B*(key+attr) + 4*sum min(k,W) + 4*sum_{k<W} max(0,f0+k-W) + 76*touched */
 int  ss_alg_bytes(ss_engine* e, int64_t* bytes, int reset);
 /* streaming emission: when enabled, every ss_step writes its
- * (group, AVG) rows straight into mapped pinned host memory (double-buffered);
- * ss_results_pull returns the oldest batch not yet pulled, waiting only for
- * that batch.  Pull at least every other batch.  With host inputs, ss_step's
- * H2D runs on a copy stream into alternating staging buffers, so the next
- * batch's copy overlaps the current batch's compute (host buffers must stay
- * unchanged until the step after next has been issued). */
+ * rows -- group id plus the configured aggregate columns (agg_mask: COUNT,
+ * SUM, AVG, MIN, MAX) -- straight into mapped pinned host memory
+ * (double-buffered); ss_results_pull returns the oldest batch not yet pulled,
+ * waiting only for that batch (rows in emission order, unconfigured columns
+ * come back as 0).  Pull at least every other batch.  A batch rejected on the
+ * device (group id outside [0, G)) is reported by the pull of that batch as
+ * SS_E_DATA with its tuple index (partition.py:119-126); it and the batches
+ * issued after it are not applied.  With host inputs, ss_step's H2D runs on
+ * a copy stream into alternating staging buffers, so the next batch's copy
+ * overlaps the current batch's compute (host buffers must stay unchanged
+ * until the step after next has been issued). */
 int  ss_set_host_emit(ss_engine* e, int enable);
-int  ss_results_pull(ss_engine* e, int64_t cap, int32_t* groups, double* avg, int64_t* n);
+int  ss_results_pull(ss_engine* e, int64_t cap, int32_t* groups, int64_t* count, int64_t* sum,
+                     double* avg, int32_t* mn, int32_t* mx, int64_t* n);
 /* raw per-batch emission (no ordering): group id and AVG of each touched group */
 int  ss_results_raw(ss_engine* e, int64_t cap, int32_t* groups, double* avg, int64_t* n);
 

@@ -58,7 +58,7 @@ _SIGS = {
     "ss_sub_batch": (C.c_longlong, [_P]),
     "ss_set_host_emit": (C.c_int, [_P, C.c_int]),
     "ss_set_graphs": (C.c_int, [_P, C.c_int]),
-    "ss_results_pull": (C.c_int, [_P, C.c_int64, _P, _P, C.POINTER(C.c_int64)]),
+    "ss_results_pull": (C.c_int, [_P, C.c_int64, _P, _P, _P, _P, _P, _P, C.POINTER(C.c_int64)]),
     "ss_create": (C.c_int, [C.POINTER(Config), C.POINTER(_P)]),
     "ss_destroy": (None, [_P]),
     "ss_set_stream": (C.c_int, [_P, _P]),

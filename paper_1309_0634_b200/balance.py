@@ -15,7 +15,7 @@ from enum import Enum
 
 import numpy as np
 
-from .errors import InvalidConfigError
+from .errors import ConsistencyError, InvalidConfigError
 from .partition import Assignment, BatchStats, Move, ReorderedBatch, device_for
 
 
@@ -75,8 +75,22 @@ class MoveList:
 def _device_policy(policy: Policy):
     def fn(stats: BatchStats, assignment: Assignment, reordered: ReorderedBatch,
            cfg: BalancerConfig) -> MoveList:
-        eng = device_for(assignment, len(reordered.groups))
-        mv, scanned, final = eng.balance(np.asarray(reordered.groups), cfg.to_c(policy))
+        # the policy reads the caller's BatchStats (balance.py:149-151):
+        # group_counts drive the moves, tpt the loads.  The device derives the
+        # loads from the counts and the assignment, and walks each donor's
+        # entry segment in list order (the layout reorder_batch produced), so
+        # stats / assignment / reordered must describe the same batch
+        counts = np.asarray(stats.group_counts, dtype=np.int64)
+        if len(counts) != assignment.n_groups:
+            raise ConsistencyError(f"stats cover {len(counts)} groups, the assignment {assignment.n_groups}")
+        tpt = np.bincount(assignment.group_to_thread, weights=counts,
+                          minlength=assignment.n_threads).astype(np.int64)
+        if not np.array_equal(tpt, np.asarray(stats.tpt, dtype=np.int64)):
+            raise ConsistencyError("stats.tpt disagrees with group_counts under this assignment")
+        if not np.array_equal(np.diff(np.asarray(reordered.indicator, dtype=np.int64)), tpt):
+            raise ConsistencyError("reordered.indicator disagrees with stats.tpt")
+        eng = device_for(assignment, 1)
+        mv, scanned, final = eng.balance_counts(counts, cfg.to_c(policy))
         return MoveList([Move(g, s, d, pl) for g, s, d, pl in mv], int(scanned), final)
     fn.__name__ = policy.name.lower()
     fn.__doc__ = f"{policy.value!r} policy, executed by k_balance on the GPU."

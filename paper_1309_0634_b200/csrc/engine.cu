@@ -64,6 +64,17 @@ struct DevReport {            // written by k_report, copied to the host
     int pad;
 };
 
+// one emission buffer: columns are null when the aggregate is not configured
+struct HostRows {
+    int32_t* g;
+    int32_t* cnt;
+    long long* sum;
+    double* avg;
+    int32_t* mn;
+    int32_t* mx;
+    unsigned long long* hdr;    // [0] rows, [1] first bad tuple (kNoBad if none), [2] its group
+};
+
 }  // namespace
 
 struct ss_engine {
@@ -158,15 +169,12 @@ struct ss_engine {
     long long* sk64[2] = {nullptr, nullptr};
     uint2* srec[2] = {nullptr, nullptr};      // replay records (ss_step_records)
 
-    // host emission: each batch's (group, AVG) rows written by a kernel
-    // straight into mapped pinned host memory (double-buffered)
+    // host emission: each batch's rows (group + the configured aggregates)
+    // written by a kernel straight into mapped pinned host memory
+    // (double-buffered); h_emit[b] are the host views, d_emit[b] the
+    // device aliases of the same pages
     bool host_emit = false;
-    int32_t* h_emit_g[2] = {nullptr, nullptr};
-    double* h_emit_avg[2] = {nullptr, nullptr};
-    unsigned* h_emit_n[2] = {nullptr, nullptr};
-    int32_t* d_emit_g[2] = {nullptr, nullptr};
-    double* d_emit_avg[2] = {nullptr, nullptr};
-    unsigned* d_emit_n[2] = {nullptr, nullptr};
+    HostRows h_emit[2]{}, d_emit[2]{};
     cudaEvent_t ev_emit[2] = {nullptr, nullptr};
     long long emit_seq = 0, pull_seq = 0;
 
@@ -180,7 +188,7 @@ struct ss_engine {
     uint32_t* sw_k = nullptr;
     int32_t* sw_v = nullptr;
     uint8_t* sw_touched = nullptr;
-    int64_t sw_head = 0, sw_fill = 0;
+    long long* sw_cur = nullptr;           // device ring cursors (head, fill), see streamwin.cuh
     // per-tuple trace mode: no dead-tuple dropping, placed
     // groups kept, trace sums per placed tuple
     bool trace_on = false;
@@ -311,10 +319,11 @@ bool is_device_ptr(const void* p) {
 }
 
 // the device policy loop: one CTA; G <= kBalStageG stages the entry lists
-// and counts in shared memory
+// and counts in shared memory when they fit next to the per-partition state
+constexpr size_t kBalSmemMax = 200 * 1024;   // dynamic shared memory opted in for k_balance
 static void launch_balance(ss_engine* e, BalanceArgs& a, cudaStream_t st) {
     a.G = (int)e->G;
-    const bool staged = e->G <= kBalStageG;
+    const bool staged = e->G <= kBalStageG && bal_smem_bytes(e->P, (int)e->G, true) <= kBalSmemMax;
     if (staged) k_balance<true><<<1, kBalThreads, bal_smem_bytes(e->P, (int)e->G, true), st>>>(a);
     else k_balance<false><<<1, kBalThreads, bal_smem_bytes(e->P, (int)e->G, false), st>>>(a);
 }
@@ -403,15 +412,30 @@ __global__ void k_deinterleave(const uint4* __restrict__ rec, int64_t n, uint32_
         vals[n - 1] = (int32_t)last.y;
     }
 }
-// the batch's (group, AVG) rows into mapped pinned host memory (PCIe writes)
-__global__ void k_emit_host(const unsigned* __restrict__ n_res, const int32_t* __restrict__ g,
-                            const double* __restrict__ avg, int32_t* hg, double* havg, unsigned* hn) {
-    const unsigned n = *n_res;
+// the batch's rows (group + configured aggregate columns) into mapped
+// pinned host memory (PCIe writes).  The header carries the row count and,
+// for a rejected batch, the first bad tuple and its group, so the host
+// raises DataError when it pulls that batch.
+__global__ void k_emit_host(const unsigned* __restrict__ n_res, const unsigned long long* __restrict__ bad,
+                            const uint32_t* __restrict__ keys, long long n_keys, const int32_t* __restrict__ g,
+                            const int32_t* __restrict__ cnt, const long long* __restrict__ sum,
+                            const double* __restrict__ avg, const int32_t* __restrict__ mn,
+                            const int32_t* __restrict__ mx, HostRows h) {
+    const unsigned long long b = *bad;
+    const unsigned n = (b == (unsigned long long)kNoBad) ? *n_res : 0u;
     for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        hg[i] = g[i];
-        havg[i] = avg[i];
+        h.g[i] = g[i];
+        if (h.cnt) h.cnt[i] = cnt[i];
+        if (h.sum) h.sum[i] = sum[i];
+        if (h.avg) h.avg[i] = avg[i];
+        if (h.mn) h.mn[i] = mn[i];
+        if (h.mx) h.mx[i] = mx[i];
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) *hn = n;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        h.hdr[0] = n;
+        h.hdr[1] = b;
+        h.hdr[2] = (b < (unsigned long long)n_keys) ? (unsigned long long)keys[b] : 0ull;
+    }
 }
 __global__ void k_fill_u64(unsigned long long* p, int64_t n, unsigned long long v) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
@@ -546,9 +570,10 @@ extern "C" void ss_destroy(ss_engine* e) {
     for (void* p : e->allocs) cudaFree(p);
     if (e->h_rep) cudaFreeHost(e->h_rep);
     for (int b = 0; b < 2; ++b) {
-        if (e->h_emit_g[b]) cudaFreeHost(e->h_emit_g[b]);
-        if (e->h_emit_avg[b]) cudaFreeHost(e->h_emit_avg[b]);
-        if (e->h_emit_n[b]) cudaFreeHost(e->h_emit_n[b]);
+        for (void* q : {(void*)e->h_emit[b].g, (void*)e->h_emit[b].cnt, (void*)e->h_emit[b].sum,
+                        (void*)e->h_emit[b].avg, (void*)e->h_emit[b].mn, (void*)e->h_emit[b].mx,
+                        (void*)e->h_emit[b].hdr})
+            if (q) cudaFreeHost(q);
         if (e->ev_staged[b]) cudaEventDestroy(e->ev_staged[b]);
         if (e->ev_freed[b]) cudaEventDestroy(e->ev_freed[b]);
         if (e->ev_emit[b]) cudaEventDestroy(e->ev_emit[b]);
@@ -638,9 +663,13 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
         return fail(e, SS_E_CONFIG, "scope must be 0 (per-group window) or 1 (stream window)");
     }
     if (e->stream_scope) {
-        if ((rc = dalloc(e, &e->sw_k, W)) || (rc = dalloc(e, &e->sw_v, W)) || (rc = dalloc(e, &e->sw_touched, G)))
+        if ((rc = dalloc(e, &e->sw_k, W)) || (rc = dalloc(e, &e->sw_v, W)) || (rc = dalloc(e, &e->sw_touched, G)) ||
+            (rc = dalloc(e, &e->sw_cur, 2)))
             return rc;
         SS_CUDA(e, cudaMemsetAsync(e->sw_touched, 0, G, e->st));
+        SS_CUDA(e, cudaMemsetAsync(e->sw_k, 0, W * 4, e->st));
+        SS_CUDA(e, cudaMemsetAsync(e->sw_v, 0, W * 4, e->st));
+        SS_CUDA(e, cudaMemsetAsync(e->sw_cur, 0, 2 * 8, e->st));
     }
     // a stream-scope engine keeps no per-group rings (a token pool)
     const int64_t dense_vals = e->stream_scope ? 16 : G * W;
@@ -844,8 +873,8 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
         const RankKernel rk = b ? rank_kernel(b) : k_rank_place<0>;
         SS_CUDA(e, cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rank_smem_bytes(kRankMaxG)));
     }
-    SS_CUDA(e, cudaFuncSetAttribute(k_balance<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    SS_CUDA(e, cudaFuncSetAttribute(k_balance<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    SS_CUDA(e, cudaFuncSetAttribute(k_balance<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBalSmemMax));
+    SS_CUDA(e, cudaFuncSetAttribute(k_balance<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBalSmemMax));
     SS_CUDA(e, cudaFuncSetAttribute(k_split_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     SS_CUDA(e, cudaStreamSynchronize(e->st));
     return SS_OK;
@@ -1224,7 +1253,7 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
                                                         e->hot_g, e->n_hot_dev, e->bad);
         }
     }
-    e->alg_input += 8 * n;
+    e->alg_input += (e->keys64 ? 12 : 8) * n;   // the batch is read once: key + attr bytes
     if (run_side) {
         SS_CUDA(e, cudaEventRecord(e->ev_stats, e->st));
         SS_CUDA(e, cudaStreamWaitEvent(e->side, e->ev_stats, 0));
@@ -1386,8 +1415,8 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
         }
         if (emit && e->host_emit) {
             const int b = (int)(e->emit_seq & 1);
-            ss_note_launch(), k_emit_host<<<kNumSM, 256, 0, e->st>>>(e->n_res, e->r_g, e->r_avg, e->d_emit_g[b],
-                                                                     e->d_emit_avg[b], e->d_emit_n[b]);
+            ss_note_launch(), k_emit_host<<<kNumSM, 256, 0, e->st>>>(e->n_res, e->bad, dk, (long long)n, e->r_g, e->r_cnt, e->r_sum,
+                                                                     e->r_avg, e->r_mn, e->r_mx, e->d_emit[b]);
             SS_CUDA(e, record_ext(e, e->ev_emit[b], e->st));
             ++e->emit_seq;
         }
@@ -1775,7 +1804,7 @@ static HostState step_transition(const ss_engine* e, int64_t n, const ss_balance
     HostState h = get_state(e);
     const bool split = bal && bal->split;
     h.last_plan = split ? (e->plan_cur ^ 1) : -1;
-    h.alg_input += 8 * n;
+    h.alg_input += (e->keys64 ? 12 : 8) * n;
     if (split) h.plan_cur ^= 1;
     h.plan_valid = split;
     if (h.cur_stage == 0) h.freed0 = true;
@@ -1891,10 +1920,7 @@ static int run_stream(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64
     a.ring_k = e->sw_k;
     a.ring_v = e->sw_v;
     a.W = W;
-    a.head = e->sw_head;
-    a.n_evict = std::max<int64_t>(0, e->sw_fill + m - W);
-    a.evict_from = (e->sw_head - e->sw_fill + W) % W;    // the oldest tuple
-    a.fill_after = std::min<int64_t>(W, e->sw_fill + m);
+    a.cur = e->sw_cur;
     a.G = (uint32_t)e->G;
     a.count = e->fill;
     a.sum = e->wsum;
@@ -1905,7 +1931,7 @@ static int run_stream(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64
     SS_CUDA(e, cudaMemsetAsync(e->n_res, 0, 4, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->touched, 0, 8, e->st));
     ss_note_launch(), k_sw_check<<<4 * kNumSM, 256, 0, e->st>>>(a);
-    if (a.n_evict) ss_note_launch(), k_sw_evict<<<4 * kNumSM, 256, 0, e->st>>>(a);
+    ss_note_launch(), k_sw_evict<<<4 * kNumSM, 256, 0, e->st>>>(a);
     ss_note_launch(), k_sw_add<<<4 * kNumSM, 256, 0, e->st>>>(a);
     if (e->minmax) {
         ss_note_launch(), k_sw_mm_reset<<<2 * kNumSM, 256, 0, e->st>>>(a);
@@ -1929,6 +1955,7 @@ static int run_stream(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64
     f.touched_total = e->touched;
     f.bad = e->bad;
     ss_note_launch(), k_sw_emit<<<2 * kNumSM, 256, 0, e->st>>>(f);
+    ss_note_launch(), k_sw_advance<<<1, 1, 0, e->st>>>(a);
     ss_note_launch(), k_sw_report<<<1, 1, 0, e->st>>>(e->bad, (long long)n, e->touched, e->n_res, e->d_rep);
     SS_CUDA(e, cudaMemcpyAsync(e->h_rep, e->d_rep, sizeof(DevReport), cudaMemcpyDeviceToHost, e->st));
     SS_CUDA(e, cudaGetLastError());
@@ -1937,8 +1964,6 @@ static int run_stream(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64
         e->freed_rec[e->cur_stage] = true;
         e->cur_stage = -1;
     }
-    e->sw_head = (e->sw_head + m) % W;
-    e->sw_fill = a.fill_after;
     return SS_OK;
 }
 
@@ -2534,14 +2559,23 @@ extern "C" int ss_step_keys64(ss_engine* e, const int64_t* keys, const int32_t* 
 extern "C" int ss_set_host_emit(ss_engine* e, int enable) {
     if (!e) return SS_E_CONFIG;
     SS_CUDA(e, cudaStreamSynchronize(e->st));
-    if (enable && !e->h_emit_g[0]) {
+    if (enable && !e->h_emit[0].g) {
+        const uint32_t m = e->cfg.agg_mask;
         for (int b = 0; b < 2; ++b) {
-            SS_CUDA(e, cudaHostAlloc((void**)&e->h_emit_g[b], e->G * 4, cudaHostAllocMapped));
-            SS_CUDA(e, cudaHostAlloc((void**)&e->h_emit_avg[b], e->G * 8, cudaHostAllocMapped));
-            SS_CUDA(e, cudaHostAlloc((void**)&e->h_emit_n[b], 64, cudaHostAllocMapped));
-            SS_CUDA(e, cudaHostGetDevicePointer((void**)&e->d_emit_g[b], e->h_emit_g[b], 0));
-            SS_CUDA(e, cudaHostGetDevicePointer((void**)&e->d_emit_avg[b], e->h_emit_avg[b], 0));
-            SS_CUDA(e, cudaHostGetDevicePointer((void**)&e->d_emit_n[b], e->h_emit_n[b], 0));
+            HostRows& h = e->h_emit[b];
+            HostRows& d = e->d_emit[b];
+            auto mapped = [&](auto** hp, auto** dp, size_t bytes) -> cudaError_t {
+                cudaError_t st = cudaHostAlloc((void**)hp, bytes, cudaHostAllocMapped);
+                if (st == cudaSuccess) st = cudaHostGetDevicePointer((void**)dp, (void*)*hp, 0);
+                return st;
+            };
+            SS_CUDA(e, mapped(&h.g, &d.g, e->G * 4));
+            SS_CUDA(e, mapped(&h.hdr, &d.hdr, 64));
+            if (m & SS_AGG_COUNT) SS_CUDA(e, mapped(&h.cnt, &d.cnt, e->G * 4));
+            if (m & SS_AGG_SUM) SS_CUDA(e, mapped(&h.sum, &d.sum, e->G * 8));
+            if (m & SS_AGG_AVG) SS_CUDA(e, mapped(&h.avg, &d.avg, e->G * 8));
+            if (e->minmax && (m & SS_AGG_MIN)) SS_CUDA(e, mapped(&h.mn, &d.mn, e->G * 4));
+            if (e->minmax && (m & SS_AGG_MAX)) SS_CUDA(e, mapped(&h.mx, &d.mx, e->G * 4));
         }
     }
     e->host_emit = enable != 0;
@@ -2549,7 +2583,8 @@ extern "C" int ss_set_host_emit(ss_engine* e, int enable) {
     return SS_OK;
 }
 
-extern "C" int ss_results_pull(ss_engine* e, int64_t cap, int32_t* groups, double* avg, int64_t* n) {
+extern "C" int ss_results_pull(ss_engine* e, int64_t cap, int32_t* groups, int64_t* count, int64_t* sum,
+                               double* avg, int32_t* mn, int32_t* mx, int64_t* n) {
     if (!e) return SS_E_CONFIG;
     if (!e->host_emit) return fail(e, SS_E_CONFIG, "host emission is off (ss_set_host_emit)");
     if (e->pull_seq >= e->emit_seq) return fail(e, SS_E_CONFIG, "no emitted batch left to pull");
@@ -2557,11 +2592,32 @@ extern "C" int ss_results_pull(ss_engine* e, int64_t cap, int32_t* groups, doubl
         return fail(e, SS_E_EXEC, "emitted rows overwritten: pull at least every other batch");
     const int b = (int)(e->pull_seq & 1);
     SS_CUDA(e, cudaEventSynchronize(e->ev_emit[b]));
-    const unsigned nr = *(volatile unsigned*)e->h_emit_n[b];
+    const HostRows& h = e->h_emit[b];
+    const volatile unsigned long long* hdr = h.hdr;
+    if (hdr[1] != (unsigned long long)kNoBad) {
+        // a rejected batch (engine.py:281-282: nothing of it was applied);
+        // the batches issued after it were no-ops as well and are dropped
+        const unsigned long long idx = hdr[1], g = hdr[2];
+        e->pull_seq = e->emit_seq;
+        int rc = recover_bad(e);
+        if (rc) return rc;
+        return fail(e, SS_E_DATA, "tuple " + std::to_string(idx) + " has group " + std::to_string(g) +
+                                      ", outside [0, " + std::to_string(e->G) + ")");
+    }
+    const unsigned nr = (unsigned)hdr[0];
     if (n) *n = nr;
     const int64_t m = std::min<int64_t>(cap, nr);
-    if (m > 0 && groups) memcpy(groups, e->h_emit_g[b], m * 4);
-    if (m > 0 && avg) memcpy(avg, e->h_emit_avg[b], m * 8);
+    if (m > 0) {
+        if (groups) memcpy(groups, h.g, m * 4);
+        if (count) for (int64_t i = 0; i < m; ++i) count[i] = h.cnt ? h.cnt[i] : 0;
+        if (sum) for (int64_t i = 0; i < m; ++i) sum[i] = h.sum ? h.sum[i] : 0;
+        if (avg) {
+            if (h.avg) memcpy(avg, h.avg, m * 8);
+            else for (int64_t i = 0; i < m; ++i) avg[i] = 0.0;
+        }
+        if (mn) for (int64_t i = 0; i < m; ++i) mn[i] = h.mn ? h.mn[i] : 0;
+        if (mx) for (int64_t i = 0; i < m; ++i) mx[i] = h.mx ? h.mx[i] : 0;
+    }
     ++e->pull_seq;
     return SS_OK;
 }

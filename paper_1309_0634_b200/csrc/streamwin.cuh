@@ -20,10 +20,10 @@ struct StreamWinArgs {
     uint32_t* ring_k;          // [W] window ring
     int32_t* ring_v;
     int64_t W;
-    int64_t head;              // next ring slot to write (oldest slot when full)
-    int64_t evict_from;        // first evicted slot
-    int64_t n_evict;
-    int64_t fill_after;        // window tuples after this batch
+    long long* cur;            // device ring cursors: [0] next slot to write (the
+                               // oldest slot when full), [1] window tuples.  Only
+                               // k_sw_advance moves them, after a valid batch, so
+                               // a rejected batch leaves the window untouched
     uint32_t G;
     int32_t* count;            // per-group COUNT (the engine's fill array)
     long long* sum;            // per-group SUM (the engine's window_sum array)
@@ -33,12 +33,27 @@ struct StreamWinArgs {
     unsigned long long* bad;
 };
 
+// the batch's view of the ring, from the device cursors
+struct SwView {
+    int64_t head, evict_from, n_evict, fill_after;
+};
+__device__ __forceinline__ SwView sw_view(const StreamWinArgs& a) {
+    const int64_t head = a.cur[0], fill = a.cur[1];
+    SwView v;
+    v.head = head;
+    v.n_evict = max64(0, fill + a.m - a.W);
+    v.evict_from = (head - fill + a.W) % a.W;      // the oldest tuple
+    v.fill_after = min64(a.W, fill + a.m);
+    return v;
+}
+
 // tuples leaving the window: before the new tuples overwrite their slots
 __global__ void __launch_bounds__(256)
 k_sw_evict(StreamWinArgs a) {
     if (*a.bad != (unsigned long long)kNoBad) return;
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < a.n_evict; j += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t slot = (a.evict_from + j) % a.W;
+    const SwView w = sw_view(a);
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < w.n_evict; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t slot = (w.evict_from + j) % a.W;
         const uint32_t g = a.ring_k[slot];
         atomicSub(&a.count[g], 1);
         atomicAdd((unsigned long long*)&a.sum[g], (unsigned long long)(-(long long)a.ring_v[slot]));
@@ -57,6 +72,7 @@ k_sw_check(StreamWinArgs a) {
 __global__ void __launch_bounds__(256)
 k_sw_add(StreamWinArgs a) {
     if (*a.bad != (unsigned long long)kNoBad) return;
+    const SwView w = sw_view(a);
     const int64_t lo = a.n - a.m;
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < a.m; k += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t g = a.keys[lo + k];
@@ -64,7 +80,7 @@ k_sw_add(StreamWinArgs a) {
         atomicAdd(&a.count[g], 1);
         atomicAdd((unsigned long long*)&a.sum[g], (unsigned long long)(long long)v);
         a.touched[g] = 1;
-        const int64_t slot = (a.head + k) % a.W;
+        const int64_t slot = (w.head + k) % a.W;
         a.ring_k[slot] = g;
         a.ring_v[slot] = v;
     }
@@ -84,13 +100,22 @@ k_sw_mm_reset(StreamWinArgs a) {
 __global__ void __launch_bounds__(256)
 k_sw_mm_scan(StreamWinArgs a) {
     if (*a.bad != (unsigned long long)kNoBad) return;
-    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < a.fill_after; s += (int64_t)gridDim.x * blockDim.x) {
+    const SwView w = sw_view(a);
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < w.fill_after; s += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t g = a.ring_k[s];
         if (a.touched[g]) {
             atomicMin(&a.mn[g], a.ring_v[s]);
             atomicMax(&a.mx[g], a.ring_v[s]);
         }
     }
+}
+
+// the batch is in: move the ring cursors (a rejected batch changes nothing)
+__global__ void k_sw_advance(StreamWinArgs a) {
+    if (*a.bad != (unsigned long long)kNoBad) return;
+    const SwView w = sw_view(a);
+    a.cur[0] = (w.head + a.m) % a.W;
+    a.cur[1] = w.fill_after;
 }
 
 // one result row per touched group; clears the touched flags

@@ -6,7 +6,8 @@ streams one through a `StreamEngine`: batch i+1 is copied from the
 memory-mapped file into one of two pinned host buffers while batch i runs
 on the device (its H2D overlaps the previous batch's compute inside the
 engine), records are split into keys / values on the device, and each
-batch's (group, AVG) rows are pulled one batch late from pinned memory.
+batch's rows (group + configured aggregates) are pulled one batch late
+from pinned memory.
 """
 
 from __future__ import annotations
@@ -37,10 +38,13 @@ class ReplayIngest:
     def __len__(self) -> int:
         return -(-self.n_tuples // self.batch_size)
 
-    def batches(self, balancer=None, on_rows: Callable[[int, np.ndarray, np.ndarray], None] | None = None
+    def batches(self, balancer=None, on_rows: Callable[[int, object], None] | None = None
                 ) -> Iterator[int]:
         """Run every batch; yields the batch index after issuing it.  `on_rows(i,
-        groups, avg)` receives batch i's emitted rows (one batch late)."""
+        rows)` receives batch i's emitted rows (a stream_engine.Results: groups
+        and the configured aggregates), one batch late.  A record whose group
+        is outside [0, G) raises DataError at the pull of its batch
+        (count_batch, partition.py:119-126)."""
         eng = self.engine
         eng.set_host_emit(True)
         for i in range(len(self)):
@@ -52,11 +56,11 @@ class ReplayIngest:
             buf[: hi - lo].numpy()[:] = self._rec[lo:hi]
             eng.step_records(buf[: hi - lo], balancer, sync=False)
             if i > 0:
-                g, a = eng.results_pull()
+                rows = eng.results_pull()
                 if on_rows is not None:
-                    on_rows(i - 1, g, a)
+                    on_rows(i - 1, rows)
             yield i
         if len(self):
-            g, a = eng.results_pull()
+            rows = eng.results_pull()
             if on_rows is not None:
-                on_rows(len(self) - 1, g, a)
+                on_rows(len(self) - 1, rows)

@@ -106,30 +106,64 @@ def _ptr(x):
     return C.c_void_p(x.data_ptr()), x
 
 
+def _first_bad_group(g, n_groups: int):
+    bad = np.flatnonzero((g < 0) | (g >= n_groups))
+    i = int(bad[0])
+    return DataError(f"tuple {i} has group {int(g[i])}, outside [0, {n_groups})")
+
+
 def _keys_u32(groups, n_groups: int):
+    """Group ids as u32 for the device.  Ids the u32 view cannot carry (< 0 or
+    >= 2^32) raise DataError here, before anything is staged; ids in
+    [G, 2^32) are caught on the device (count_batch, partition.py:119-126)."""
     if isinstance(groups, np.ndarray):
         g = groups
         if g.dtype != np.uint32:
             if g.size and (g.min() < 0 or g.max() > 0xFFFFFFFF):
-                bad = np.flatnonzero((g < 0) | (g >= n_groups))
-                i = int(bad[0])
-                raise DataError(f"tuple {i} has group {int(g[i])}, outside [0, {n_groups})")
+                raise _first_bad_group(g, n_groups)
             g = g.astype(np.uint32)
         return g
     import torch
     if groups.dtype == torch.int32 or groups.dtype == torch.uint32:
         return groups
     if groups.dtype == torch.int64:
+        if groups.numel():
+            lo, hi = torch.aminmax(groups)
+            if int(lo) < 0 or int(hi) > 0xFFFFFFFF:      # would wrap into range as u32
+                raise _first_bad_group(groups.cpu().numpy(), n_groups)
         return groups.to(torch.int32)
     raise InvalidConfigError(f"unsupported group dtype {groups.dtype}")
 
 
+_I32_LO, _I32_HI = -(1 << 31), (1 << 31) - 1
+
+
 def _attrs_i32(attrs):
+    """Attribute values as int32 (the device ring width).  The reference
+    stream's values are int32 (datagen.py:24-26); a wider value cannot be
+    stored exactly and raises DataError before any state changes."""
     if isinstance(attrs, np.ndarray):
-        return attrs if attrs.dtype == np.int32 else attrs.astype(np.int32)
+        if attrs.dtype == np.int32:
+            return attrs
+        if attrs.size and np.issubdtype(attrs.dtype, np.integer) and attrs.dtype.itemsize >= 4:
+            lo, hi = attrs.min(), attrs.max()
+            if lo < _I32_LO or hi > _I32_HI:
+                i = int(np.flatnonzero((attrs < _I32_LO) | (attrs > _I32_HI))[0])
+                raise DataError(f"tuple {i} has attr {int(attrs[i])}, outside the int32 range of the window store")
+        elif attrs.size and not np.issubdtype(attrs.dtype, np.integer):
+            raise DataError(f"attrs must be integers, got {attrs.dtype}")
+        return attrs.astype(np.int32)
     import torch
     if attrs.dtype == torch.int32:
         return attrs
+    if attrs.is_floating_point():
+        raise DataError(f"attrs must be integers, got {attrs.dtype}")
+    if attrs.dtype == torch.int64 and attrs.numel():
+        lo, hi = torch.aminmax(attrs)
+        if int(lo) < _I32_LO or int(hi) > _I32_HI:
+            a = attrs.cpu().numpy()
+            i = int(np.flatnonzero((a < _I32_LO) | (a > _I32_HI))[0])
+            raise DataError(f"tuple {i} has attr {int(a[i])}, outside the int32 range of the window store")
     return attrs.to(torch.int32)
 
 
@@ -221,22 +255,33 @@ class StreamEngine:
 
     # -- assignment --------------------------------------------------------
     def set_lists(self, lists):
-        order = np.asarray([g for lst in lists for g in lst], dtype=np.int32)
+        sizes = [len(x) for x in lists]
         offs = np.zeros(len(lists) + 1, dtype=np.int64)
-        np.cumsum([len(x) for x in lists], out=offs[1:])
-        if len(lists) != self.n_partitions:
+        np.cumsum(sizes, out=offs[1:])
+        self.set_csr(np.fromiter((g for lst in lists for g in lst), dtype=np.int64, count=int(offs[-1])), offs)
+
+    def set_csr(self, order, offsets):
+        """Load an assignment as concatenated ordered lists + offsets[P+1]."""
+        offs = np.ascontiguousarray(offsets, dtype=np.int64)
+        if len(offs) != self.n_partitions + 1:
             raise InvalidConfigError("assignment has a different number of partitions")
+        order = np.ascontiguousarray(order, dtype=np.int32)
         po, _k1 = _ptr(order)
         pf, _k2 = _ptr(offs)
         self._check(self._lib.ss_set_assignment(self._h, po, pf))
 
-    def get_lists(self):
+    def get_csr(self):
+        """(group_to_thread, order, offsets) of the device assignment."""
         g2t = np.empty(self.n_groups, dtype=np.int32)
         order = np.empty(self.n_groups, dtype=np.int32)
         offs = np.empty(self.n_partitions + 1, dtype=np.int64)
         self._check(self._lib.ss_get_assignment(self._h, _ptr(g2t)[0], _ptr(order)[0], _ptr(offs)[0]))
-        lists = [order[offs[p]:offs[p + 1]].astype(np.int64).tolist() for p in range(self.n_partitions)]
-        return g2t.astype(np.int64), lists
+        return g2t.astype(np.int64), order.astype(np.int64), offs
+
+    def get_lists(self):
+        g2t, order, offs = self.get_csr()
+        flat = order.tolist()
+        return g2t, [flat[offs[p]:offs[p + 1]] for p in range(self.n_partitions)]
 
     def apply_moves(self, moves):
         """moves: iterable of (group, src, dst, placement) with placement
@@ -394,19 +439,41 @@ class StreamEngine:
 
     # -- streaming emission ---------------------------------
     def set_host_emit(self, enable: bool = True):
-        """Every step writes its (group, AVG) rows into pinned host memory;
-        results_pull() returns the oldest batch not yet pulled."""
+        """Every step writes its rows (group + the configured aggregates) into
+        pinned host memory; results_pull() returns the oldest batch not yet
+        pulled."""
         self._check(self._lib.ss_set_host_emit(self._h, int(bool(enable))))
-        self._pull_g = np.empty(self.n_groups, dtype=np.int32)
-        self._pull_avg = np.empty(self.n_groups, dtype=np.float64)
+        G = self.n_groups
+        names = set(self.aggregates.names) | {"count", "sum"}
+        self._pull = {
+            "groups": np.empty(G, dtype=np.int32),
+            "count": np.empty(G, dtype=np.int64) if "count" in names else None,
+            "sum": np.empty(G, dtype=np.int64) if "sum" in names else None,
+            "avg": np.empty(G, dtype=np.float64) if "avg" in names else None,
+            "min": np.empty(G, dtype=np.int32) if self.minmax and "min" in names else None,
+            "max": np.empty(G, dtype=np.int32) if self.minmax and "max" in names else None,
+        }
 
-    def results_pull(self):
-        """(groups int32[k], avg float64[k]) of the oldest unpulled batch
-        (views into reused buffers: copy them to keep them)."""
+    def results_pull(self) -> Results:
+        """Rows of the oldest unpulled batch: groups plus the configured
+        aggregate columns (None when not configured).  The arrays are views
+        into reused buffers: copy them to keep them.  A batch the device
+        rejected raises DataError here (it and the batches issued after it
+        were not applied)."""
         n = C.c_int64()
-        self._check(self._lib.ss_results_pull(self._h, self.n_groups, _ptr(self._pull_g)[0],
-                                              _ptr(self._pull_avg)[0], C.byref(n)))
-        return self._pull_g[:n.value], self._pull_avg[:n.value]
+        b = self._pull
+        ptr = lambda k: (_ptr(b[k])[0] if b[k] is not None else None)
+        self._check(self._lib.ss_results_pull(self._h, self.n_groups, ptr("groups"), ptr("count"), ptr("sum"),
+                                              ptr("avg"), ptr("min"), ptr("max"), C.byref(n)))
+        k = n.value
+        cut = lambda a: None if a is None else a[:k]
+        return Results(b["groups"][:k], cut(b["count"]), cut(b["sum"]), cut(b["avg"]), cut(b["min"]),
+                       cut(b["max"]))
+
+    def pulled_row_bytes(self) -> int:
+        """Bytes per emitted row that results_pull moves device -> host."""
+        wire = {"groups": 4, "count": 4, "sum": 8, "avg": 8, "min": 4, "max": 4}   # device column widths
+        return sum(wire[k] for k, a in self._pull.items() if a is not None)
 
     def last_report(self) -> StepReport:
         rep = L.StepReport()

@@ -1,8 +1,8 @@
 """Streaming use of the engine: host input buffers are
 copied on a side stream into alternating staging buffers while the
-previous batch computes, and each batch's (group, AVG) rows are written
-into pinned host memory and pulled one batch late.  Results must equal
-the oracle batch by batch (bit-exact AVG, tolerance 0)."""
+previous batch computes, and each batch's rows (group + the configured
+aggregates) are written into pinned host memory and pulled one batch late.
+Results must equal the oracle batch by batch (bit-exact, tolerance 0)."""
 
 import numpy as np
 import pytest
@@ -13,41 +13,84 @@ from paper_1309_0634_b200 import datagen as D
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("key_bits", [32, 64])
-def test_stream_pipeline_matches_oracle(key_bits):
+def _check_rows(rows, store, g_expected, aggs, to_group=None):
+    """Pulled rows of one batch against the oracle's windows after it."""
+    pg = rows.groups
+    grp = to_group[pg] if to_group is not None else pg.astype(np.int64)
+    o = np.argsort(grp)
+    assert np.array_equal(grp[o], g_expected)
+    cnt, sm, avg, mn, mx = store.aggregates(g_expected)
+    assert np.array_equal(rows.count[o], cnt)
+    assert np.array_equal(rows.sum[o], sm)
+    if "avg" in aggs:
+        assert np.array_equal(rows.avg[o], avg)            # AVG bit-exact
+    else:
+        assert rows.avg is None
+    if "min" in aggs:
+        assert np.array_equal(rows.min[o], mn) and np.array_equal(rows.max[o], mx)
+
+
+@pytest.mark.parametrize("key_bits,aggs", [(32, ("count", "sum", "avg")), (64, ("count", "sum", "avg")),
+                                           (64, ("count", "sum", "min", "max")), (32, ("count", "sum"))])
+def test_stream_pipeline_matches_oracle(key_bits, aggs):
     import torch
     from paper_1309_0634_b200.stream_engine import StreamEngine
     G, W, P, B = 3000, 700, 16, 150_000
-    eng = StreamEngine(G, W, n_partitions=P, aggregates=("count", "sum", "avg"), max_batch=B,
-                       key_bits=key_bits)
+    eng = StreamEngine(G, W, n_partitions=P, aggregates=aggs, max_batch=B, key_bits=key_bits)
     bal = eng.balancer_struct("prob", thread_threshold=B // 160, pot=0.5)
     eng.set_host_emit(True)
+    assert eng.pulled_row_bytes() == 4 + 4 + 8 + 8 * ("avg" in aggs) + 8 * ("min" in aggs)
     spec = D.DatasetSpec(D.DatasetKind.ZIPF, 7 * B, G, 1.1, 5)
     batches = list(D.batches(D.stream_for(spec), B))
-    store = O.OStore(G, W)
-    expected, pulled = [], []
+    to_group = None
     for i, b in enumerate(batches):
         keys = D.mix64(b.groups) if key_bits == 64 else b.groups.astype(np.int32)
         hk = torch.from_numpy(np.ascontiguousarray(keys)).pin_memory()
         ha = torch.from_numpy(b.attrs.astype(np.int32)).pin_memory()
         eng.step(hk, ha, bal, sync=False)            # H2D overlaps the previous batch
-        store.ingest(b.groups, b.attrs)
-        g = np.unique(b.groups)
-        expected.append((g, store.aggregates()[2][g]))
         if i > 0:
-            rg, ra = eng.results_pull()              # the previous batch's rows
-            pulled.append((rg.copy(), ra.copy()))
-    rg, ra = eng.results_pull()
-    pulled.append((rg.copy(), ra.copy()))
-    assert len(pulled) == len(batches)
-    to_group = None
+            rows = eng.results_pull()                # the previous batch's rows
+            if key_bits == 64:
+                to_group = D.unmix64(eng.slot_keys())   # dense slot -> group
+            _check_rows(rows, store, prev_g, aggs, to_group)
+        if i == 0:
+            store = O.OStore(G, W)
+        store.ingest(b.groups, b.attrs)
+        prev_g = np.unique(b.groups)
+    # (the oracle is one batch ahead of the pulls above: re-check the last)
+    rows = eng.results_pull()
     if key_bits == 64:
-        to_group = D.unmix64(eng.slot_keys())       # dense slot -> group
-    for (pg, pa), (eg, ea) in zip(pulled, expected):
-        grp = to_group[pg] if to_group is not None else pg.astype(np.int64)
-        o = np.argsort(grp)
-        assert np.array_equal(grp[o], eg)
-        assert np.array_equal(pa[o], ea)               # AVG bit-exact
+        to_group = D.unmix64(eng.slot_keys())
+    _check_rows(rows, store, prev_g, aggs, to_group)
+    eng.close()
+
+
+def test_pull_reports_a_rejected_batch():
+    """A batch with a group id >= G, issued without a report, is raised as
+    DataError by the pull of that batch (partition.py:119-126); it and the
+    batch issued after it are not applied, and the engine goes on."""
+    from paper_1309_0634_b200.errors import DataError
+    from paper_1309_0634_b200.stream_engine import StreamEngine
+    G, W, B = 500, 50, 20_000
+    spec = D.DatasetSpec(D.DatasetKind.ZIPF, 5 * B, G, 1.1, 3)
+    bl = list(D.batches(D.stream_for(spec), B))
+    eng = StreamEngine(G, W, n_partitions=8, max_batch=B)
+    eng.set_host_emit(True)
+    store = O.OStore(G, W)
+    eng.step(bl[0].groups, bl[0].attrs, sync=False)
+    store.ingest(bl[0].groups, bl[0].attrs)
+    bad = bl[1].groups.astype(np.uint32).copy()
+    bad[777] = G + 5
+    eng.step(bad, bl[1].attrs, sync=False)
+    eng.step(bl[2].groups, bl[2].attrs, sync=False)      # issued behind the bad batch
+    eng.results_pull()                                   # batch 0: fine
+    with pytest.raises(DataError, match="tuple 777 has group 505"):
+        eng.results_pull()
+    s = eng.snapshot()
+    assert np.array_equal(s["fill"], store.fill) and np.array_equal(s["window_sum"], store.window_sum)
+    eng.step(bl[3].groups, bl[3].attrs, sync=False)
+    store.ingest(bl[3].groups, bl[3].attrs)
+    _check_rows(eng.results_pull(), store, np.unique(bl[3].groups), ("count", "sum", "avg"))
     eng.close()
 
 
@@ -108,7 +151,7 @@ def test_replay_file_ingest_matches_oracle(tmp_path):
     bal = eng.balancer_struct("prob", B // 160, 0.5)
     rows = {}
     ri = ReplayIngest(eng, path, B)
-    for _ in ri.batches(bal, on_rows=lambda i, g, a: rows.__setitem__(i, (g.copy(), a.copy()))):
+    for _ in ri.batches(bal, on_rows=lambda i, r: rows.__setitem__(i, (r.groups.copy(), r.avg.copy()))):
         pass
     store = O.OStore(G, W)
     for i, b in enumerate(D.batches(D.read_replay(path, G), B)):
@@ -120,6 +163,29 @@ def test_replay_file_ingest_matches_oracle(tmp_path):
         assert np.array_equal(pa[o], store.aggregates()[2][g])
     s = eng.snapshot()
     assert np.array_equal(s["fill"], store.fill) and np.array_equal(s["window_sum"], store.window_sum)
+    eng.close()
+
+
+def test_replay_file_with_bad_group_raises(tmp_path):
+    """A replay record whose group is >= G raises DataError naming the tuple
+    (batch-relative index) instead of silently emitting nothing."""
+    from paper_1309_0634_b200.errors import DataError
+    from paper_1309_0634_b200.replay import ReplayIngest
+    from paper_1309_0634_b200.stream_engine import StreamEngine
+    G, B = 300, 10_000
+    rec = np.zeros(4 * B, dtype=D.REPLAY_DTYPE)
+    rng = np.random.default_rng(5)
+    rec["group"] = rng.integers(0, G, 4 * B)
+    rec["attr"] = rng.integers(-1000, 1000, 4 * B)
+    rec["group"][2 * B + 17] = G
+    path = tmp_path / "bad.replay"
+    rec.tofile(path)
+    eng = StreamEngine(G, 40, n_partitions=4, max_batch=B)
+    seen = []
+    with pytest.raises(DataError, match=f"tuple 17 has group {G}"):
+        for _ in ReplayIngest(eng, path, B).batches(on_rows=lambda i, r: seen.append(i)):
+            pass
+    assert seen == [0, 1]
     eng.close()
 
 
@@ -233,4 +299,40 @@ def test_stream_scope_window(W, B):
                 assert res.avg[i] == np.float64(sm[g]) / np.float64(cnt[g])
     with pytest.raises(Exception):
         eng.step(b.groups, b.attrs, StreamEngine.balancer_struct("prob", 100, 0.5))
+    eng.close()
+
+
+def test_stream_scope_rejected_batch_changes_nothing():
+    """A stream-scope batch with a bad group (no report requested) leaves the
+    ring cursors and window untouched: later batches see the last W valid
+    tuples (engine.py:281-282, validate before mutate)."""
+    from paper_1309_0634_b200.errors import DataError
+    from paper_1309_0634_b200.stream_engine import StreamEngine, WindowSpec
+    G, W, B = 200, 3000, 1000
+    spec = D.DatasetSpec(D.DatasetKind.ZIPF, 8 * B, G, 1.1, 17)
+    bl = list(D.batches(D.stream_for(spec), B))
+    eng = StreamEngine(G, WindowSpec(W, "stream"), n_partitions=4, max_batch=B,
+                       aggregates=("count", "sum", "min", "max"))
+    good_g, good_a = [], []
+    for i, b in enumerate(bl):
+        if i == 1:                     # not yet full: an early bad batch
+            bad = b.groups.astype(np.uint32).copy()
+            bad[3] = G
+            eng.step(bad, b.attrs, sync=False)
+            with pytest.raises(DataError):
+                eng.last_report()
+            continue
+        eng.step(b.groups, b.attrs)
+        good_g.append(b.groups)
+        good_a.append(b.attrs)
+        wg = np.concatenate(good_g)[-W:]
+        wa = np.concatenate(good_a)[-W:].astype(np.int64)
+        snap = eng.snapshot()
+        assert np.array_equal(snap["fill"], np.bincount(wg, minlength=G))
+        assert np.array_equal(snap["window_sum"], np.bincount(wg, weights=wa, minlength=G).astype(np.int64))
+        res = eng.results()
+        for k, g in enumerate(res.groups):
+            vals = wa[wg == g]
+            if len(vals):
+                assert res.min[k] == vals.min() and res.max[k] == vals.max()
     eng.close()
