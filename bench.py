@@ -5,19 +5,22 @@
 A "step" is one batch of the hot path (harness.run's loop body,
 harness.py:99-117): count -> balancer (device, overlapped) -> stable
 placement -> per-group window update -> per-batch result emission ->
-apply moves.  Default workload = BASELINE.json configs[1] (C2): Zipf
-s=1.0 keys over 10K groups, per-group window W=1e5, SUM+COUNT, the
-paper's prob_check group-reassignment balancer, batch 2^24 tuples,
-P = 148 processing units (one aggregate CTA per SM).
+apply moves.  Default workload = BASELINE.json configs[3] (C4), the
+largest single-GPU configuration: 1M groups with int64 keys, per-group
+window W=1e7, MIN/MAX/SUM (+COUNT), Zipf s=1.0, batch 2^24 tuples,
+prob_check + hot-key splitting, P = 148 processing units.  C2 (configs[1])
+is measured after it under "also".
 
 Printed JSON line (rank 0):
   value      whole-job tuples/s with the staged batches already in HBM
   e2e        the same through StreamEngine.step with pinned HOST buffers:
-             H2D of each batch and D2H of the emitted per-group AVG rows
-             inside the timed region
+             H2D of each batch and D2H of the emitted per-group rows (group
+             + the configured aggregates) inside the timed region
   roofline   dominant kernel class: algorithmic bytes / its CUDA-event time
   path_roofline  whole step: SURVEY 8(d) algorithmic bytes / step time
-  cpu_baseline   the oracle port (oracle/port.py) on the host, bounded sample
+  cpu_baseline   the oracle port (oracle/port.py) on the host, same config,
+                 bounded sample; reference_variants = the reference package
+                 itself (baseline/_ref) on one core at the C2 shape
 --impl reference times that CPU path alone (the reference package is pure
 Python/numpy; its algorithm is restated in oracle/port.py).
 """
@@ -152,34 +155,44 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU path: the oracle port of the reference pipeline, group-sharded over the
-# host cores, bounded sample
+# CPU path: the oracle port of the reference pipeline on the SAME config
+# (G, W, batch, aggregates, policy), group-sharded over the host cores
+# (SURVEY 8(d)(iii)), bounded sample
 # ---------------------------------------------------------------------------
-def _cpu_worker(job):
-    """One group shard: the reference pipeline (count, place, policy, ingest,
-    apply) over the sub-stream of groups g with g % n == r, relabelled to the
-    dense local ids g // n.  Batches are generated before the clock starts and
-    cycled; returns (tuples, seconds) over `n_batches` batches."""
-    cfg_name, r, n, batch, n_batches, seed = job
-    from oracle import port as O
+_CPU_STAGE = []          # (groups, attrs) batches, generated once, shared by fork
+
+
+def _cpu_stage(cfg_name, batch, n_batches, seed=11):
+    """Generate the CPU sample with the reference generators (datagen.py)."""
     from paper_1309_0634_b200 import datagen as D
     desc, kind, s, G, W, _, aggs, policy, _ = CONFIGS[cfg_name]
     dk = D.DatasetKind.UNIFORM if kind.startswith("uniform") else D.DatasetKind.ZIPF
-    nbuf = 4
-    spec = D.DatasetSpec(dk, batch * nbuf, G, s, seed)
+    spec = D.DatasetSpec(dk, batch * n_batches, G, s, seed)
+    _CPU_STAGE.clear()
+    _CPU_STAGE.extend((b.groups, b.attrs) for b in D.batches(D.stream_for(spec), batch))
+
+
+def _cpu_worker(job):
+    """One group shard: the reference pipeline (count, place, policy, ingest,
+    apply) over the sub-stream of groups g with g % n == r, relabelled to the
+    dense local ids g // n, with P/n of the partitions.  Returns (tuples,
+    seconds) over `n_batches` batches cycled from the staged sample."""
+    cfg_name, r, n, n_batches, batch = job
+    from oracle import port as O
+    desc, kind, s, G, W, _, aggs, policy, _ = CONFIGS[cfg_name]
     Gl = (G - r + n - 1) // n
     Pl = max(1, P_DEFAULT // n)
-    staged = []
-    for b in D.batches(D.stream_for(spec), batch):
-        m = (b.groups % n) == r
-        staged.append(((b.groups[m] // n).astype(np.int64), b.attrs[m].astype(np.int64)))
+    shards = []
+    for g, a in _CPU_STAGE:
+        m = (g % n) == r
+        shards.append(((g[m] // n).astype(np.int64), a[m].astype(np.int64)))
     asg = O.contiguous_assignment(Gl, Pl)
     cfg = O.balancer_cfg(policy, max(1, batch // (10 * P_DEFAULT)), 0.5)
     store = O.OStore(Gl, W)
     fn = O.POLICY_FNS[policy]
     done, t_work = 0, 0.0
     for i in range(n_batches):
-        g, a = staged[i % len(staged)]
+        g, a = shards[i % len(shards)]
         t0 = time.perf_counter()
         counts, tpt = O.histogram(g, asg)
         rg, ra, ind = O.place(g, a, asg, counts, tpt)
@@ -198,18 +211,19 @@ def cpu_cores():
         return os.cpu_count() or 1
 
 
-def cpu_pipeline(cfg_name, seconds=15.0, batch=1 << 20, cores=None):
-    """Group-sharded CPU pipeline on `cores` processes.  A calibration batch
-    on one shard sizes the run to about `seconds` of wall time; the value is
-    all tuples / the slowest shard's busy time."""
+def cpu_pipeline(cfg_name, seconds=15.0, cores=None, batch=None):
+    """Group-sharded CPU pipeline on `cores` processes over the config's own
+    batch size.  A calibration batch on one shard sizes the run to about
+    `seconds` of busy time per shard; value = all tuples / the slowest
+    shard's busy time."""
     import multiprocessing as mp
+    B = batch or CONFIGS[cfg_name][5]
     cores = cores or cpu_cores()
-    # shards never get fewer than ~1 batch-slice of 64K tuples
-    cores = max(1, min(cores, batch // 65536))
-    t, s = _cpu_worker((cfg_name, 0, cores, batch, 2, 11))
-    per_batch = max(1e-4, s / 2)
-    n_batches = int(max(3, min(400, seconds / per_batch)))
-    jobs = [(cfg_name, r, cores, batch, n_batches, 11) for r in range(cores)]
+    if not _CPU_STAGE or len(_CPU_STAGE[0][0]) != B:
+        _cpu_stage(cfg_name, B, 2)
+    t, s = _cpu_worker((cfg_name, 0, cores, 1, B))
+    n_batches = int(max(2, min(400, seconds / max(1e-4, s))))
+    jobs = [(cfg_name, r, cores, n_batches, B) for r in range(cores)]
     if cores == 1:
         res = [_cpu_worker(jobs[0])]
     else:
@@ -217,8 +231,52 @@ def cpu_pipeline(cfg_name, seconds=15.0, batch=1 << 20, cores=None):
             res = pool.map(_cpu_worker, jobs)
     tuples = sum(r[0] for r in res)
     t_max = max(r[1] for r in res)
-    return tuples / t_max, {"batches": n_batches, "batch": batch, "tuples": tuples,
+    return tuples / t_max, {"batches": n_batches, "batch": B, "tuples": tuples,
                             "seconds": round(t_max, 2), "cores": cores}
+
+
+def reference_variants(seconds=4.0):
+    """SURVEY 8(d) CPU baselines (i) and (ii) with the reference package
+    itself (baseline/_ref, installed by the driver), on one core.  Its
+    WindowStore is a dense int64 [G, W] array, so they run at the C2 shape
+    (G = 10K, W = 1e5: 8 GB virtual); C3/C4 would need 745 GiB / 72.8 TiB.
+      (i)  serial_reference (engine.py:432-445): the traced per-tuple oracle
+      (ii) run() with the sim backend and prob_check (harness.py:85-140):
+           count -> reorder -> policy -> ingest -> apply, P = 148
+    Returns None when the reference is not installed."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "skewstream")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    try:
+        import skewstream as R
+        from skewstream import datagen as RD, harness as RH, balance as RB
+    except Exception as exc:                           # pragma: no cover
+        return {"error": f"import failed: {exc}"}
+    out = {}
+    G, W = 10_000, 100_000
+    n = 1 << 18
+    spec = RD.DatasetSpec(RD.DatasetKind.ZIPF, n, G, 1.0, 11)
+    t0 = time.perf_counter()
+    R.serial_reference(RD.stream_for(spec), W)
+    dt = time.perf_counter() - t0
+    out["serial_reference"] = {"value": n / dt, "unit": "tuples/s", "cores": 1,
+                               "sample": f"{n} tuples, zipf s=1.0, G={G}, W={W} (C2 shape), traced"}
+    B = 1 << 18
+    nb = max(2, min(16, int(seconds / 0.4)))
+    cfg = RH.RunConfig(dataset=RD.DatasetSpec(RD.DatasetKind.ZIPF, nb * B, G, 1.0, 11), batch_size=B,
+                       window=W, grid_size=1, block_size=P_DEFAULT,
+                       balancer=RB.BalancerConfig(policy=RB.Policy.PROB_CHECK,
+                                                  thread_threshold=max(1, B // (10 * P_DEFAULT)), pot=0.5),
+                       backend=RH.Backend.SIM, seed=11)
+    t0 = time.perf_counter()
+    rep = RH.run(cfg)
+    dt = time.perf_counter() - t0
+    out["run_sim_prob"] = {"value": rep.total_tuples / dt, "unit": "tuples/s", "cores": 1,
+                           "sample": f"{nb} batches x 2^18 tuples, zipf s=1.0, G={G}, W={W}, P={P_DEFAULT} "
+                                     f"(C2 shape), prob_check, sim backend"}
+    return out
 
 
 def cpu_model():
@@ -235,26 +293,31 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     name = args.config
-    desc = CONFIGS[name][0]
+    desc, kind, s, G, W, B, aggs, policy, split = CONFIGS[name]
+    if args.batch:
+        B = args.batch
     per_step = max(2.0, args.cpu_seconds / max(1, args.steps))
+    _cpu_stage(name, B, 2)
     vals, info = [], None
     for i in range(args.steps + args.warmup):
         if i < args.warmup:
-            # warm-up: one short shard pass (page-in, allocator, imports)
-            _cpu_worker((name, 0, 1, 1 << 16, 2, 11))
+            # warm-up: one batch on one shard (page-in, allocator, imports)
+            _cpu_worker((name, 0, cpu_cores(), 1, B))
             continue
-        v, info = cpu_pipeline(name, seconds=per_step)
+        v, info = cpu_pipeline(name, seconds=per_step, batch=B)
         vals.append(v)
     v = float(np.mean(vals))
     line = {
         "impl": "reference", "metric": "sustained tuples/s (Zipf skew)", "value": v,
         "unit": "tuples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "higher_is_better": True, "dtype": "i64", "data": "synthetic (reference generators)",
-        "config": {"workload": desc, "batch": 1 << 20, "partitions": P_DEFAULT},
+        "config": {"workload": desc, "groups": G, "window": W, "batch": B, "partitions": P_DEFAULT,
+                   "policy": policy, "aggregates": list(aggs)},
         "cpu_baseline": {"value": v, "unit": "tuples/s", "cores": info["cores"], "kind": "port",
-                         "sample": f"{args.steps} steps, each {info['batches']} batches of 2^20 tuples per "
-                                   f"group shard on {info['cores']} processes (count, place, policy, ingest, "
-                                   f"apply through oracle/port.py) on {cpu_model()}"},
+                         "sample": f"{args.steps} steps, each {info['batches']} batches of {B} tuples "
+                                   f"(the config's batch) split into {info['cores']} group shards, one process "
+                                   f"each (count, place, policy, ingest, apply through oracle/port.py) "
+                                   f"on {cpu_model()}"},
         "e2e": {"value": v, "unit": "tuples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -263,12 +326,108 @@ def run_reference(args, rank, world):
 # ---------------------------------------------------------------------------
 # GPU path
 # ---------------------------------------------------------------------------
+class Workload:
+    """One configuration on this rank's GPU: the engine, its balancer
+    settings and the staged input batches (already in HBM)."""
+
+    def __init__(self, name, args, dev, world, rank, P, stream):
+        import torch
+        from paper_1309_0634_b200.stream_engine import StreamEngine
+        self.name = name
+        desc, kind, s, G, W, B, aggs, policy, split = CONFIGS[name]
+        if args.batch and name == args.config:
+            B = args.batch
+        self.desc, self.kind, self.s, self.G, self.W, self.B = desc, kind, s, G, W, B
+        self.aggs, self.policy, self.split, self.P = aggs, policy, split, P
+        self.world = world
+        thr = max(1, B // (10 * P))
+        self.sharded = None
+        if world > 1:
+            # key-sharded: each rank's B tuples are its slice of a global batch
+            # of world*B; tuples travel to their owner GPU by NCCL all-to-all,
+            # and the GPU-level balancer moves groups between GPUs (weak
+            # scaling: per-rank input fixed)
+            from paper_1309_0634_b200.sharded import ShardedEngine
+            if kind.endswith("64"):
+                raise SystemExit("int64 keys are single-GPU in this build (route is u32)")
+            self.sharded = ShardedEngine(G, W, n_partitions=P, aggregates=aggs, device=dev.index,
+                                         max_batch=world * B, sub_batch=args.sub_batch)
+            self.eng = self.sharded.local
+            self.gbal = self.eng.balancer_struct("prob", thread_threshold=max(1, B // 10), pot=0.5)
+        else:
+            self.eng = StreamEngine(G, W, n_partitions=P, aggregates=aggs, device=dev.index, max_batch=B,
+                                    sub_batch=args.sub_batch, key_bits=64 if kind.endswith("64") else 32,
+                                    initial=args.initial)
+        self.eng.set_stream(stream)
+        self.bal = self.eng.balancer_struct(policy, thread_threshold=thr, pot=0.5, split=split)
+        self.nbuf = 2 * DRIFT_EVERY if kind == "zipfdrift" else 4
+        self.batches = make_batches(kind, s, G, B, self.nbuf, dev, seed=1234 + rank)
+        torch.cuda.synchronize()
+
+    def step(self, i, hosts=None):
+        g, a = (hosts or self.batches)[i % (len(hosts) if hosts else self.nbuf)]
+        if self.sharded is not None:
+            self.sharded.step(g, a, self.bal, self.gbal)
+        else:
+            self.eng.step(g, a, self.bal, sync=False)
+
+    def close(self):
+        if self.sharded is not None:
+            self.sharded.close()
+        else:
+            self.eng.close()
+
+
+def timed(wl, steps, start, stream, barrier, world, dev):
+    """Device time of `steps` steps (CUDA events on the engine stream, max
+    over ranks) and the library launches inside them."""
+    import torch
+    import torch.distributed as dist
+    from paper_1309_0634_b200 import _lib as L
+    lib = L.load()
+    barrier()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    lib.ss_launch_count(1)
+    ev0.record(stream)
+    for i in range(steps):
+        wl.step(start + i)
+    ev1.record(stream)
+    ev1.synchronize()
+    launches = int(lib.ss_launch_count(1))
+    ms_t = torch.tensor([ev0.elapsed_time(ev1)], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    return float(ms_t.item()), launches
+
+
+def warm(wl, args, world):
+    """W warm-up steps (at least two passes over the staged batches, so every
+    cached CUDA graph is captured), then up to 0.3 s (at most 32 steps) more
+    so the timed region starts from a loaded GPU; returns steps run."""
+    import torch
+    n = max(args.warmup, 2 * wl.nbuf)
+    for i in range(n):
+        wl.step(i)
+        wl.eng.last_report()
+    t_end = time.time() + 0.3
+    extra = 0
+    while extra < 32 and (world > 1 or time.time() < t_end):
+        wl.step(n + extra)
+        extra += 1
+        torch.cuda.synchronize()
+    return n + extra
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS),
+                    help="default: C4, the largest single-GPU configuration of BASELINE.json")
+    ap.add_argument("--also", default="c2",
+                    help="comma-separated extra configs measured briefly (value only) after the headline")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--partitions", type=int, default=P_DEFAULT)
     ap.add_argument("--batch", type=int, default=0)
@@ -279,10 +438,7 @@ def main():
     ap.add_argument("--initial", default="hash", choices=["hash", "contiguous"],
                     help="initial group->partition map (north star: hash-partitioned groups)")
     args = ap.parse_args()
-    # at least 3 warm-up steps (contract), and at least two passes over the
-    # staged batches so every (batch, parity) CUDA graph of the fused step is
-    # captured before the clock starts; the JSON line reports the number run
-    args.warmup = max(args.warmup, 3)
+    args.warmup = max(args.warmup, 3)          # contract: >= 3 warm-up steps
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -299,94 +455,31 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
 
     from paper_1309_0634_b200 import _lib as L
-    from paper_1309_0634_b200.stream_engine import StreamEngine
+    import ctypes as C
 
-    desc, kind, s, G, W, B, aggs, policy, split = CONFIGS[args.config]
-    if args.batch:
-        B = args.batch
     P = args.partitions
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)          # NCCL routing and the engine share one stream
-    thr = max(1, B // (10 * P))
-    sharded = None
-    if world > 1:
-        # key-sharded: each rank's B tuples are its slice of a global batch of
-        # world*B; tuples travel to their owner GPU by NCCL all-to-all, and the
-        # GPU-level balancer (prob_check on all-reduced counts) moves groups
-        # between GPUs (weak scaling: per-rank input fixed)
-        from paper_1309_0634_b200.sharded import ShardedEngine
-        sharded = ShardedEngine(G, W, n_partitions=P, aggregates=aggs, device=local, max_batch=world * B,
-                                sub_batch=args.sub_batch)
-        eng = sharded.local
-        gbal = eng.balancer_struct("prob", thread_threshold=max(1, B // 10), pot=0.5)
-    else:
-        eng = StreamEngine(G, W, n_partitions=P, aggregates=aggs, device=local, max_batch=B,
-                           sub_batch=args.sub_batch, key_bits=64 if kind.endswith("64") else 32,
-                           initial=args.initial)
-    eng.set_stream(stream)
-    bal = eng.balancer_struct(policy, thread_threshold=thr, pot=0.5, split=split)
-    nbuf = 2 * DRIFT_EVERY if kind == "zipfdrift" else 4
-    if world > 1 and kind.endswith("64"):
-        raise SystemExit("int64 keys are single-GPU in this build (route is u32)")
-    batches = make_batches(kind, s, G, B, nbuf, dev, seed=1234 + rank)
-    args.warmup = max(args.warmup, 2 * nbuf)
-    torch.cuda.synchronize()
 
     def barrier():
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
 
-    def run_steps(k, start=0):
-        for i in range(k):
-            g, a = batches[(start + i) % nbuf]
-            if sharded is not None:
-                sharded.step(g, a, bal, gbal)
-            else:
-                eng.step(g, a, bal, sync=False)
-
+    wl = Workload(args.config, args, dev, world, rank, P, stream)
+    eng, B = wl.eng, wl.B
+    lib = L.load()
     # the clock sampler (nvidia-smi) takes ~0.3 s to start: it is started
     # before the warm-up so that it samples the timed region without an
     # idle gap in front of it
     clocks = ClockSampler(local)
     clocks.start()
-    # warm-up (also converges the balancer from the contiguous assignment)
-    for i in range(args.warmup):
-        run_steps(1, i)
-        eng.last_report()
-    lib = L.load()
-    import ctypes as C
+    args.warmup = warm(wl, args, world)
 
     # ---- (1) headline: staged batches in HBM -------------------------------
-    barrier()
-    # up to 0.3 s (at most 32 steps) of further untimed steps, counted in the
-    # reported warm-up, so the timed region starts from a loaded GPU (a step
-    # cap: with a growing window, e.g. the C4 uniform twin, every batch adds
-    # ring storage; with several ranks every rank runs the same count)
-    t_end = time.time() + 0.3
-    extra = 0
-    while extra < 32 and (world > 1 or time.time() < t_end):
-        run_steps(1, args.warmup + extra)
-        extra += 1
-        torch.cuda.synchronize()
-    args.warmup += extra
-    barrier()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    lib = L.load()
-    lib.ss_launch_count(1)
-    ev0.record(stream)
-    run_steps(args.steps, args.warmup)
-    ev1.record(stream)
-    ev1.synchronize()
-    launches = int(lib.ss_launch_count(1))
-    ms = ev0.elapsed_time(ev1)
+    ms, launches = timed(wl, args.steps, args.warmup, stream, barrier, world, dev)
     clk = clocks.stop()
     rep = eng.last_report()
-    ms_t = torch.tensor([ms], device=dev, dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms = float(ms_t.item())
     value = B * args.steps * world / (ms / 1e3)
 
     # ---- (2) kernel classes with CUDA events + algorithmic bytes --------------
@@ -396,11 +489,14 @@ def main():
     lib.ss_profile_read(eng._h, kms, kn, 1)
     ab = C.c_int64()
     lib.ss_alg_bytes(eng._h, C.byref(ab), 1)
-    ratios = []
+    ratios, part_ratio = [], []
     barrier()
     for i in range(args.steps):
-        run_steps(1, args.warmup + i)
+        wl.step(args.warmup + i)
         ratios.append(eng.last_report().load_ratio)
+        ns = eng.last_part_ns().astype(np.float64)
+        if ns.sum() > 0:
+            part_ratio.append(float(ns.max() / ns.mean()))
     lib.ss_profile_read(eng._h, kms, kn, 1)
     lib.ss_alg_bytes(eng._h, C.byref(ab), 1)
     lib.ss_profile(eng._h, 0)
@@ -412,7 +508,7 @@ def main():
     # the input is read once in the model -- keys by the count, attrs by the
     # placement (its re-read of the keys is implementation overhead) -- and
     # the window update owns the ring and state bytes
-    key_bytes = 8 if kind.endswith("64") else 4
+    key_bytes = 8 if wl.kind.endswith("64") else 4
     ingest_bytes = alg_per_step - (key_bytes + 4) * B
     cls_bytes = {"count": key_bytes * B, "place": 4 * B, "ingest": ingest_bytes}
     main_cls = max(("count", "place", "ingest"), key=lambda n: cls_ms[n])
@@ -422,40 +518,34 @@ def main():
     path_achieved = alg_per_step / (step_ms / 1e3) / 1e9
     # measured DRAM traffic per launch of that kernel class (ncu --set full of
     # this config, committed under profiles/), else null
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as fh:
-            tj = json.load(fh)
-        if args.config in tj and main_cls in tj[args.config] and B == (1 << 24) and world == 1:
-            traffic = tj[args.config][main_cls]["bytes_per_launch"]
-    except Exception:
-        traffic = None
+    traffic, traffic_src = None, None
+    for tf in ("r2_traffic.json", "r1_traffic.json"):
+        try:
+            with open(os.path.join(ROOT, "profiles", tf)) as fh:
+                tj = json.load(fh)
+            if args.config in tj and main_cls in tj[args.config] and B == CONFIGS[args.config][5] and world == 1:
+                traffic = tj[args.config][main_cls]["bytes_per_launch"]
+                traffic_src = f"profiles/{tf} (ncu --set full, dram read+write per launch)"
+                break
+        except Exception:
+            continue
 
     # ---- (3) end to end through the public API with host buffers -------------
     e2e_steps = args.e2e_steps or max(4, args.steps // 2)
     hosts = []
-    for g, a in batches[:2]:
+    for g, a in wl.batches[:2]:
         hg = torch.empty(B, dtype=g.dtype, pin_memory=True)
         ha = torch.empty(B, dtype=torch.int32, pin_memory=True)
         hg.copy_(g)
         ha.copy_(a)
         hosts.append((hg, ha))
     # streaming use of the public API: batch i+1 is issued
-    # (its H2D overlaps batch i's compute) before batch i's rows are pulled
-    # from pinned host memory
+    # (its H2D overlaps batch i's compute) before batch i's rows -- group +
+    # the configured aggregates -- are pulled from pinned host memory
     eng.set_host_emit(True)
-
-    def e2e_step(i):
-        hg, ha = hosts[i % 2]
-        if sharded is not None:
-            sharded.step(hg, ha, bal, gbal)
-        else:
-            eng.step(hg, ha, bal, sync=False)
-
-    # warm-up of the streaming path (its second staging buffer is allocated
-    # on first use), not timed
-    for i in range(2):
-        e2e_step(i)
+    row_bytes = eng.pulled_row_bytes()
+    for i in range(2):                 # the second staging buffer is allocated on first use
+        wl.step(i, hosts)
         eng.results_pull()
     d2h = 0
     barrier()
@@ -464,66 +554,75 @@ def main():
     t0 = time.perf_counter()
     e0.record(stream)
     for i in range(e2e_steps):
-        e2e_step(i)
+        wl.step(i, hosts)
         if i > 0:
-            rg, ra = eng.results_pull()
-            d2h += len(rg) * 12 + 4
-    rg, ra = eng.results_pull()
-    d2h += len(rg) * 12 + 4
+            d2h += len(eng.results_pull().groups) * row_bytes + 24
+    d2h += len(eng.results_pull().groups) * row_bytes + 24
     e1.record(stream)
     e1.synchronize()
     e2e_wall = time.perf_counter() - t0
     e2e_ms = max(e0.elapsed_time(e1), e2e_wall * 1e3)
     e2e_value = B * e2e_steps * world / (e2e_ms / 1e3)
+    eng.set_host_emit(False)
+    eng_sub = eng.sub_batch if hasattr(eng, "sub_batch") else args.sub_batch
+    wl.close()
 
-    # ---- CPU baseline (rank 0, N=1 only) ----------------------------------------
+    # ---- (4) further configs, value only -------------------------------------
+    also = {}
+    for name in [x for x in args.also.split(",") if x and x != args.config and x in CONFIGS]:
+        w2 = Workload(name, args, dev, world, rank, P, stream)
+        n2 = warm(w2, args, world)
+        ms2, _ = timed(w2, args.steps, n2, stream, barrier, world, dev)
+        also[name] = {"workload": w2.desc, "value": w2.B * args.steps * world / (ms2 / 1e3),
+                      "ms_per_step": ms2 / args.steps, "unit": "tuples/s"}
+        w2.close()
+
+    # ---- CPU baselines (rank 0, N=1 only) -------------------------------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         v, info = cpu_pipeline(args.config, seconds=args.cpu_seconds)
         cpu = {"value": v, "unit": "tuples/s", "cores": info["cores"], "kind": "port",
-               "sample": f"{info['batches']} batches x 2^20 tuples ({info['seconds']} s busy per shard) of the "
-                         f"same stream shape, group-sharded over {info['cores']} processes through "
-                         f"oracle/port.py on {cpu_model()}"}
+               "sample": f"{info['batches']} batches x {info['batch']} tuples (the config's own batch, G, W, "
+                         f"aggregates and policy) split into {info['cores']} group shards, one process each, "
+                         f"through oracle/port.py on {cpu_model()}; {info['seconds']} s busy per shard",
+               "reference_variants": reference_variants()}
 
-    eng_sub = eng.sub_batch if hasattr(eng, "sub_batch") else args.sub_batch
     if rank == 0:
         line = {
             "metric": "sustained tuples/s (Zipf skew)",
             "value": value, "unit": "tuples/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "i32 keys/values, i64 sums",
-            "data": f"synthetic {kind} (s={s}) keys generated on device, uniform int32 attrs; "
-                    f"{nbuf} staged batches of {B * (12 if kind.endswith('64') else 8) >> 20} MB each (> L2), cycled",
-            "config": {"workload": desc, "groups": G, "window": W, "batch": B,
-                       "partitions": P, "initial_map": args.initial, "policy": policy + ("+split" if split else ""), "aggregates": list(aggs),
-                       "sub_batch": eng_sub, "l2": "inputs larger than L2 (128 MB per batch)",
+            "scaling": "weak", "vs_baseline": None, "dtype": "i32 values, i64 sums" + (", i64 keys" if key_bytes == 8 else ""),
+            "data": f"synthetic {wl.kind} (s={wl.s}) keys generated on device, uniform int32 attrs; "
+                    f"{wl.nbuf} staged batches of {B * (key_bytes + 4) >> 20} MB each (> L2), cycled",
+            "config": {"workload": wl.desc, "groups": wl.G, "window": wl.W, "batch": B,
+                       "partitions": P, "initial_map": args.initial, "policy": wl.policy + ("+split" if wl.split else ""),
+                       "aggregates": list(wl.aggs), "sub_batch": eng_sub,
+                       "l2": f"inputs larger than L2 ({B * (key_bytes + 4) >> 20} MB per batch)",
                        "parallelism": (f"key-sharded x{world}: NCCL all-to-all routing, GPU-level prob_check"
                                        if world > 1 else "single GPU"),
                        "global_batch": B * world},
             "roofline": {"bound": "hbm", "kernel": main_cls, "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-                         "traffic_source": "profiles/r1_traffic.json (ncu --set full, dram read+write per launch)"
-                                           if traffic is not None else None,
-                         "peak_source": peak_kind,
+                         "traffic_source": traffic_src, "peak_source": peak_kind,
                          "alg_bytes_per_launch": cls_bytes[main_cls] / max(1, cls_launch[main_cls] / args.steps),
                          "ms_per_step": k_ms},
             "path_roofline": {"alg_bytes_per_tuple": alg_per_step / B, "achieved": path_achieved,
                               "peak": peak, "unit": "GB/s", "frac": path_achieved / peak},
             "kernel_ms_per_step": cls_ms,
-            "load_ratio": {"last": rep.load_ratio, "mean": float(np.mean(ratios)),
-                           "max": float(np.max(ratios))},
+            "load_ratio": {"plan_last": rep.load_ratio, "plan_mean": float(np.mean(ratios)),
+                           "plan_max": float(np.max(ratios)),
+                           "measured_part_ns_max_over_mean": float(np.mean(part_ratio)) if part_ratio else None},
             "moves_last_step": rep.moves,
+            "also": also,
             "cpu_baseline": cpu,
-            "e2e": {"value": e2e_value, "unit": "tuples/s", "h2d_bytes_per_step": (12 if kind.endswith("64") else 8) * B,
-                    "d2h_bytes_per_step": d2h // e2e_steps, "steps": e2e_steps},
+            "e2e": {"value": e2e_value, "unit": "tuples/s", "h2d_bytes_per_step": (key_bytes + 4) * B,
+                    "d2h_bytes_per_step": d2h // e2e_steps, "steps": e2e_steps,
+                    "d2h_row_bytes": row_bytes},
             "gpu_launches": launches,
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)
-    if sharded is not None:
-        sharded.close()
-    else:
-        eng.close()
     if world > 1:
         dist.destroy_process_group()
 

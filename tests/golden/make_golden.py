@@ -268,7 +268,11 @@ def pipeline_cases():
                 "window": w, "threads": grid * block, "threshold": thr,
                 "policy": pol, "seed": 17,
                 "rows": [[r.tuples, r.imbalance, r.moves, r.scanned] for r in rep.rows],
+                # the sim backend's modelled costs (engine.py:299-321)
+                "makespans": [r.makespan for r in rep.rows],
+                "per_thread_cost": [r.per_thread_cost.tolist() for r in rep.rows],
                 "total_moves": rep.total_moves, "total_scanned": rep.total_scanned,
+                "total_makespan": rep.total_makespan, "throughput": rep.throughput,
                 "fill": st.fill.tolist(), "next_pos": st.next_pos.tolist(),
                 "window_sum": st.window_sum.tolist(),
                 "values_digest": _digest(st.values),

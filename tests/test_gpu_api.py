@@ -10,6 +10,7 @@ import pytest
 
 import paper_1309_0634_b200 as ss
 from oracle import port as O
+from paper_1309_0634_b200 import datagen as D
 
 pytestmark = pytest.mark.gpu
 
@@ -74,7 +75,35 @@ def test_harness_run_matches_golden_rows(golden):
         assert rep.store.fill.tolist() == r["fill"]
         assert rep.store.window_sum.tolist() == r["window_sum"]
         assert rep.final_assignment.thread_to_groups == r["final_lists"]
-        assert rep.total_makespan > 0 and all(x.makespan >= 0 for x in rep.rows)
+        # the sim backend (the reference's default): modelled costs, bit-exact
+        assert [x.makespan for x in rep.rows] == r["makespans"]
+        assert [x.per_thread_cost.tolist() for x in rep.rows] == r["per_thread_cost"]
+        assert rep.total_makespan == r["total_makespan"] and rep.throughput == r["throughput"]
+    # the measured backend: per-partition kernel time in ns, same decisions
+    r = golden("pipeline.json")["runs"][3]
+    spec = ss.DatasetSpec(ss.DatasetKind(r["kind"]), r["n"], r["groups"], r["exponent"], 0)
+    cfg = ss.RunConfig(dataset=spec, batch_size=r["batch"], window=r["window"], grid_size=1,
+                       block_size=r["threads"], seed=r["seed"], backend=ss.Backend.CUDA,
+                       balancer=ss.BalancerConfig(r["policy"], r["threshold"], 0.5))
+    rep = ss.run(cfg)
+    assert [[x.tuples, x.imbalance, x.moves, x.scanned] for x in rep.rows] == r["rows"]
+    assert rep.total_makespan > 0 and all(x.makespan > 0 for x in rep.rows)
+
+
+def test_ingest_tuple_scalar_path():
+    """ingest_tuple (engine.py:96-122): (window_sum, modelled cost) after each
+    insert, equal to the scalar reference semantics."""
+    st = ss.WindowStore(2, 3, n_partitions=1)
+    m = ss.CostModel(window_passes=2, per_element_cost=3, per_tuple_overhead=1)
+    vals, out = [4, -2, 7, 10, 1], []
+    for v in vals:
+        out.append(ss.ingest_tuple(st, 1, v, m))
+    sums = [4, 2, 9, 15, 18]
+    fills = [1, 2, 3, 3, 3]
+    assert out == [(s_, 1 + 2 * 3 * f) for s_, f in zip(sums, fills)]
+    with pytest.raises(ss.DataError):
+        ss.ingest_tuple(st, 2, 1, m)
+    st.engine.close()
 
 
 def test_ingest_sequence_and_contents():
@@ -87,3 +116,89 @@ def test_ingest_sequence_and_contents():
     assert agg["avg"][0] == 7 / 4
     with pytest.raises(ss.ConsistencyError):
         ss.ingest_sequence(st, np.array([0, 1, 0]), np.array([1, 2, 3]), assume_grouped=True)
+
+
+def test_process_batch_cuda_matches_process_batch_sim():
+    """The CUDA executor slot (engine.py:299-321 signature) on the reference
+    pipeline's reordered batches: the store equals the oracle's, the rows'
+    tuples / imbalance equal process_batch_sim's, and the per-thread cost is
+    measured on the partition that holds each segment's groups."""
+    import paper_1309_0634_b200 as ss
+    from oracle import port as O
+    G, W, P, B = 2000, 300, 16, 40_000
+    spec = D.DatasetSpec(D.DatasetKind.ZIPF, 4 * B, G, 1.2, 9)
+    store = ss.WindowStore(G, W, n_partitions=P, max_batch=B)
+    ref = O.OStore(G, W)
+    asg = ss.initial_assignment(G, P)
+    oasg = O.contiguous_assignment(G, P)
+    cfg = O.balancer_cfg("prob", B // (10 * P), 0.5)
+    for b in D.batches(D.stream_for(spec), B):
+        stats = ss.count_batch(b, asg)
+        r = ss.reorder_batch(b, asg, stats)
+        rep = ss.process_batch_cuda(r, store)
+        ref.ingest(r.groups, r.attrs, assume_grouped=True)
+        tpt = np.diff(r.indicator)
+        assert rep.tuples == len(b) and rep.imbalance == int(tpt.max() - tpt.min())
+        assert len(rep.per_thread_cost) == P
+        assert (rep.per_thread_cost[tpt > 0] > 0).all()
+        counts, otpt = O.histogram(b.groups, oasg)
+        rg, ra, ind = O.place(b.groups, b.attrs, oasg, counts, otpt)
+        v = O.POLICY_FNS["prob"](counts, otpt, oasg, rg, ind, cfg)
+        asg = ss.apply_moves(asg, [ss.Move(*m) for m in v.moves])
+        oasg = O.apply_move_list(oasg, v.moves)
+    s = store.engine.snapshot()
+    assert np.array_equal(s["fill"], ref.fill) and np.array_equal(s["window_sum"], ref.window_sum)
+    assert np.array_equal(s["next_pos"], ref.next_pos)
+    for g in (0, 1, 7, G - 1):
+        assert store.contents(g).tolist() == ref.contents(g).tolist()
+    # process_batch_sim: the same execution, costs in the reference's model
+    # units -- per tuple overhead + passes * elem * min(fill after insert, W)
+    m = ss.CostModel(window_passes=3, per_element_cost=2, per_tuple_overhead=5, per_iteration_overhead=7)
+    b = next(iter(D.batches(D.stream_for(spec), B)))
+    stats = ss.count_batch(b, asg)
+    r = ss.reorder_batch(b, asg, stats)
+    f0 = store.engine.snapshot()["fill"]
+    rep = ss.process_batch_sim(r, store, m)
+    rg = np.asarray(r.groups)
+    cost = np.empty(len(rg), dtype=np.int64)
+    seen = {}
+    for i, g in enumerate(rg.tolist()):
+        seen[g] = seen.get(g, 0) + 1
+        cost[i] = 5 + 3 * 2 * min(int(f0[g]) + seen[g], W)
+    c = np.concatenate(([0], np.cumsum(cost)))
+    per_thread = c[np.asarray(r.indicator)[1:]] - c[np.asarray(r.indicator)[:-1]]
+    assert rep.per_thread_cost.tolist() == per_thread.tolist()
+    assert rep.makespan == int(per_thread.max()) + 7
+    ref.ingest(r.groups, r.attrs, assume_grouped=True)
+    assert np.array_equal(store.engine.snapshot()["window_sum"], ref.window_sum)
+    # a split run is refused before anything is ingested
+    bad = ss.ReorderedBatch(np.array([1, 2, 1]), np.array([5, 6, 7]), np.array([0] * P + [3]))
+    before = store.engine.snapshot()["window_sum"].copy()
+    with pytest.raises(ss.ConsistencyError):
+        ss.process_batch_cuda(bad, store)
+    assert np.array_equal(store.engine.snapshot()["window_sum"], before)
+    store.engine.close()
+
+
+def test_large_partition_count_policies():
+    """P = 2048 partitions with G = 16384 groups: the staged policy CTA would
+    need more shared memory than it may use, so the global-list variant runs
+    (every policy still equal to the oracle)."""
+    from oracle import port as O
+    from paper_1309_0634_b200.stream_engine import StreamEngine
+    G, W, P, B = 16384, 50, 2048, 1 << 18
+    spec = D.DatasetSpec(D.DatasetKind.ZIPF, 2 * B, G, 1.1, 3)
+    for policy in ("all", "prob", "best"):
+        eng = StreamEngine(G, W, n_partitions=P, aggregates=("count", "sum"), max_batch=B)
+        thr = max(1, B // (10 * P))
+        bal = StreamEngine.balancer_struct(policy, thr, 0.5)
+        cfg = O.balancer_cfg(policy, thr, 0.5)
+        asg = O.contiguous_assignment(G, P)
+        for b in D.batches(D.stream_for(spec), B):
+            rep = eng.step(b.groups, b.attrs, bal)
+            counts, tpt = O.histogram(b.groups, asg)
+            rg, ra, ind = O.place(b.groups, b.attrs, asg, counts, tpt)
+            v = O.POLICY_FNS[policy](counts, tpt, asg, rg, ind, cfg)
+            assert eng.last_moves() == [tuple(m) for m in v.moves] and rep.scanned == v.scanned
+            asg = O.apply_move_list(asg, v.moves)
+        eng.close()

@@ -97,3 +97,79 @@ def test_full_shape_int64_keys_c4():
     assert np.array_equal(snap["window_sum"][:n], wsum[slot_ids])
     assert np.array_equal(snap["min"][:n], mn[slot_ids]) and np.array_equal(snap["max"][:n], mx[slot_ids])
     eng.close()
+
+
+def test_c4_twelve_batches_wrap_the_top_window():
+    """C4 shape over 12 batches (2^24 each): the top group (~7 % of every
+    batch) fills W = 1e7 after ~9 batches and then evicts part of its window
+    every batch -- ring wrap, next_pos, retraction and the multi-chunk
+    MIN/MAX maintenance all run at W = 1e7.  Checked after the first
+    partial eviction and at the end, every touched group, int64 keys."""
+    import torch
+    from paper_1309_0634_b200.stream_engine import StreamEngine
+    G, W, B, NB = 1_000_000, 10_000_000, 1 << 24, 12
+    rng = np.random.default_rng(31)
+    eng = StreamEngine(G, W, n_partitions=148, aggregates=("count", "sum", "min", "max"), max_batch=B,
+                       key_bits=64, initial="hash")
+    bal = StreamEngine.balancer_struct("prob", B // 1480, 0.5, split=True)
+    ids = np.empty(NB * B, dtype=np.int32)
+    vals = np.empty(NB * B, dtype=np.int32)
+    wrapped_checked = False
+    for i in range(NB):
+        g = _zipf(B, G, 1.0, rng)
+        a = rng.integers(-2 ** 31, 2 ** 31, B, dtype=np.int64).astype(np.int32)
+        ids[i * B:(i + 1) * B] = g
+        vals[i * B:(i + 1) * B] = a
+        rep = eng.step(torch.from_numpy(D.mix64(g)).cuda(), torch.from_numpy(a).cuda(), bal)
+        assert rep.tuples == B
+        n_seen = (i + 1) * B
+        K0 = int(np.count_nonzero(ids[:n_seen] == 0))
+        if (K0 > W and not wrapped_checked) or i == NB - 1:
+            fill, wsum, mn, mx, nxt, t = _expected(ids[:n_seen].astype(np.int64), vals[:n_seen], G, W)
+            slot_ids = D.unmix64(eng.slot_keys())
+            snap = eng.snapshot()
+            n = len(slot_ids)
+            assert n == int(t.sum())
+            assert fill[0] == W and nxt[0] > 0                  # the top window has wrapped
+            for k in ("fill", "next_pos", "window_sum", "min", "max"):
+                ref = {"fill": fill, "next_pos": nxt, "window_sum": wsum, "min": mn, "max": mx}[k]
+                assert np.array_equal(snap[k][:n], ref[slot_ids]), (i, k)
+            # the ring of the top group in arrival order: its last W values
+            s0 = int(np.flatnonzero(slot_ids == 0)[0])
+            last = vals[:n_seen][ids[:n_seen] == 0][-W:]
+            assert np.array_equal(eng.contents(s0), last.astype(np.int64))
+            wrapped_checked = True
+    assert wrapped_checked
+    eng.close()
+
+
+@pytest.mark.parametrize("policy", ["first", "all", "prob", "best"])
+def test_full_shape_movelists(policy):
+    """C2 shape (G = 10K, P = 148, B = 2^24): the fused step's MoveList and
+    scanned count equal the oracle's policy (balance.py:141-293) on the same
+    batch and the assignment in force before it, batch after batch."""
+    import torch
+    from oracle import port as O
+    from paper_1309_0634_b200.stream_engine import StreamEngine
+    G, W, B, P = 10_000, 100_000, 1 << 24, 148
+    rng = np.random.default_rng(41)
+    eng = StreamEngine(G, W, n_partitions=P, aggregates=("count", "sum"), max_batch=B, initial="contiguous")
+    thr = B // (10 * P)
+    bal = StreamEngine.balancer_struct(policy, thr, 0.5)
+    cfg = O.balancer_cfg(policy, thr, 0.5)
+    for i in range(3):
+        g = _zipf(B, G, 1.0, rng)
+        a = rng.integers(-2 ** 31, 2 ** 31, B, dtype=np.int64)
+        g2t, lists = eng.get_lists()
+        asg = O.OAssignment(g2t, [list(x) for x in lists])
+        rep = eng.step(torch.from_numpy(g.astype(np.int32)).cuda(), torch.from_numpy(a.astype(np.int32)).cuda(), bal)
+        counts, tpt = O.histogram(g, asg)
+        if policy == "prob":
+            rg, _, ind = O.place(g, a, asg, counts, tpt)
+        else:                       # these policies read counts / segment lengths only
+            rg, ind = None, np.concatenate(([0], np.cumsum(tpt)))
+        v = O.POLICY_FNS[policy](counts, tpt, asg, rg, ind, cfg)
+        assert eng.last_moves() == [tuple(m) for m in v.moves], i
+        assert rep.scanned == v.scanned and rep.moves == len(v.moves)
+        assert rep.imbalance == int(tpt.max() - tpt.min())
+    eng.close()
