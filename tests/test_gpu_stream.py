@@ -82,8 +82,8 @@ def test_pull_reports_a_rejected_batch():
     bad = bl[1].groups.astype(np.uint32).copy()
     bad[777] = G + 5
     eng.step(bad, bl[1].attrs, sync=False)
-    eng.step(bl[2].groups, bl[2].attrs, sync=False)      # issued behind the bad batch
     eng.results_pull()                                   # batch 0: fine
+    eng.step(bl[2].groups, bl[2].attrs, sync=False)      # issued behind the bad batch
     with pytest.raises(DataError, match="tuple 777 has group 505"):
         eng.results_pull()
     s = eng.snapshot()
