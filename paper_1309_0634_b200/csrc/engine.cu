@@ -34,6 +34,7 @@
 #include "balance.cuh"
 #include "split.cuh"
 #include "keys.cuh"
+#include "bucket.cuh"
 #include "trace.cuh"
 #include "streamwin.cuh"
 
@@ -114,6 +115,8 @@ struct ss_engine {
     int4* cta_map = nullptr;               // work-proportional K4 grid: slot of every CTA
     int* cta_used = nullptr;
     bool rank_place = false;               // G <= kRankMaxG: k_rank_place instead of the radix passes
+    bool bucket = false;                   // G > kRankMaxG: bucketed two-pass placement (bucket.cuh)
+    BucketArgs bk{};
     int32_t* n_live = nullptr;             // kept tuples of the batch (device)
     uint32_t* chunk_live = nullptr;        // live-chunk bitmap
     int32_t *lc = nullptr, *n_lc = nullptr;   // ordered live-chunk list
@@ -153,6 +156,7 @@ struct ss_engine {
 
     // int64 keys (key_bits == 64): key -> dense slot table
     bool keys64 = false;
+    bool pre_counted = false;     // this batch was counted by the int64 key probe
     KeyTable kt{};
     long long* stage_keys64 = nullptr;
 
@@ -202,7 +206,7 @@ struct ss_engine {
         const void* dv;
         int64_t n;
         ss_balancer bal;
-        int plan_cur, plan_valid, emit_b, host_emit, stage;
+        int plan_cur, plan_valid, emit_b, host_emit, stage, pre_counted;
         cudaGraphExec_t exec;
         long long launches;
     };
@@ -229,8 +233,13 @@ struct ss_engine {
     int32_t *r_g = nullptr, *r_cnt = nullptr, *r_mn = nullptr, *r_mx = nullptr;
     long long* r_sum = nullptr;
     double* r_avg = nullptr;
-    int2* rescan = nullptr;
+    int4* rescan = nullptr;
     unsigned* n_rescan = nullptr;
+    // MIN/MAX chunk summaries of full windows (W > kMMSumMinW)
+    int32_t* sum_idx = nullptr;
+    uint8_t* sum_valid = nullptr;
+    int* n_sum = nullptr;
+    int2* sums = nullptr;
     unsigned long long* part_ns = nullptr;
     unsigned long long* loads = nullptr;   // per-partition load incl. split shares
     long long* fill_loads = nullptr;       // split planner: cold loads of the batch
@@ -773,6 +782,23 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
     e->rank_place = G <= kRankMaxG && G * W >= e->max_batch;
     if (const char* rp = getenv("SS_B200_RANK_PLACE")) e->rank_place = G <= kRankMaxG && rp[0] != '0';
     if (e->rank_place && (rc = dalloc(e, &e->gpre, (size_t)nsub * G))) return rc;
+    // bucketed placement: every cold group (batch count < kBkTau) must keep
+    // all its tuples, i.e. W >= kBkTau
+    e->bucket = !e->rank_place && G > kRankMaxG && W >= kBkTau && e->max_batch <= kBkMaxBatch;
+    {
+        // A/B switch while the bucketed passes are tuned: off unless SS_B200_BUCKET=1
+        const char* bp = getenv("SS_B200_BUCKET");
+        e->bucket = e->bucket && bp && bp[0] == '1';
+    }
+    if (e->bucket) {
+        BucketArgs& b = e->bk;
+        if ((rc = dalloc(e, &b.bin_of, G)) || (rc = dalloc(e, &b.bin_first, kBkNBMax + 1)) ||
+            (rc = dalloc(e, &b.bin_hot, kBkNBMax)) || (rc = dalloc(e, &b.n_bins, 1)) ||
+            (rc = dalloc(e, &b.fsum, G / kBkBlk + 2)) || (rc = dalloc(e, &b.tbin, e->max_batch + 8)) ||
+            (rc = dalloc(e, &b.hist, (size_t)kBkSupers * kBkNBMax)) || (rc = dalloc(e, &b.btot, kBkNBMax)) ||
+            (rc = dalloc(e, &b.sbase, kBkNBMax)))
+            return rc;
+    }
     if ((rc = dalloc(e, &e->pwork, e->P)) || (rc = dalloc(e, &e->cta_map, 4 * kNumSM + e->P)) ||
         (rc = dalloc(e, &e->cta_used, 1)) || (rc = dalloc(e, &e->any_dead, 1)))
         return rc;
@@ -794,19 +820,18 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
         uint64_t cap = 1;
         while (cap < 2 * (uint64_t)G) cap <<= 1;
         KeyTable& t = e->kt;
-        if ((rc = dalloc(e, &t.keys, cap + 1)) || (rc = dalloc(e, &t.slot, cap + 1)) ||
-            (rc = dalloc(e, &t.first, cap + 1)) || (rc = dalloc(e, &t.ent, e->max_batch)) ||
+        if ((rc = dalloc(e, &t.ent, cap + 1)) || (rc = dalloc(e, &t.first, cap + 1)) ||
+            (rc = dalloc(e, &t.pend, e->max_batch)) || (rc = dalloc(e, &t.pend_ent, e->max_batch)) ||
+            (rc = dalloc(e, &t.n_pend, 1)) || (rc = dalloc(e, &t.slot_ent, G)) ||
             (rc = dalloc(e, &t.new_ent, G)) || (rc = dalloc(e, &t.n_new, 1)) || (rc = dalloc(e, &t.n_slots, 1)) ||
             (rc = dalloc(e, &t.mark, e->max_batch)) || (rc = dalloc(e, &t.slot_keys, G)) ||
-            (rc = dalloc(e, &t.min_key_entry, 1)) || (rc = dalloc(e, &t.overflow, 1)) || (rc = dalloc(e, &t.pending, 1)) ||
+            (rc = dalloc(e, &t.min_key_entry, 1)) || (rc = dalloc(e, &t.overflow, 1)) ||
             (rc = dalloc(e, &e->stage_keys64, e->max_batch)) ||
             (rc = dalloc(e, &e->kbsum, e->max_batch / kMarkBlk + 2)))
             return rc;
         t.cap_mask = cap - 1;
         t.G = (int)G;
-        SS_CUDA(e, cudaMemsetAsync(t.keys, 0, (cap + 1) * 8, e->st));
-        ss_note_launch(), k_fill_u64<<<296, 256, 0, e->st>>>(t.keys, cap + 1, kEmptyKey);
-        SS_CUDA(e, cudaMemsetAsync(t.slot, 0xff, (cap + 1) * 4, e->st));
+        ss_note_launch(), k_key_init<<<296, 256, 0, e->st>>>(t.ent, (int64_t)cap + 1);
         SS_CUDA(e, cudaMemsetAsync(t.first, 0xff, (cap + 1) * 4, e->st));
         SS_CUDA(e, cudaMemsetAsync(t.mark, 0xff, e->max_batch * 4, e->st));
         SS_CUDA(e, cudaMemsetAsync(t.n_new, 0, 4, e->st));
@@ -853,6 +878,18 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
     SS_CUDA(e, cudaMemsetAsync(e->alg_bytes, 0, 8, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->n_res, 0, 4, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->n_rescan, 0, 4, e->st));
+    if (e->minmax && W > kMMSumMinW) {
+        // every group whose window is full holds W ring values, so at most
+        // (ring pool / W) of them -- the summaries cost pool / kMMChunk x 8 B
+        const int64_t max_full = std::min<int64_t>(G, (int64_t)(e->pool_cap / (uint64_t)W) + 1);
+        const int64_t nch = (W + kMMChunk - 1) / kMMChunk;
+        if ((rc = dalloc(e, &e->sum_idx, G)) || (rc = dalloc(e, &e->sum_valid, G)) || (rc = dalloc(e, &e->n_sum, 1)) ||
+            (rc = dalloc(e, &e->sums, (size_t)max_full * nch)))
+            return rc;
+        SS_CUDA(e, cudaMemsetAsync(e->sum_idx, 0xff, G * 4, e->st));
+        SS_CUDA(e, cudaMemsetAsync(e->sum_valid, 0, G, e->st));
+        SS_CUDA(e, cudaMemsetAsync(e->n_sum, 0, 4, e->st));
+    }
     SS_CUDA(e, cudaMallocHost(&e->h_rep, sizeof(DevReport)));
     memset(e->h_rep, 0, sizeof(DevReport));
     e->h_rep->bad = (unsigned long long)kNoBad;
@@ -869,6 +906,9 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
     SS_CUDA(e, cudaFuncSetAttribute(k_sort_pass<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)SortSmem<4>::bytes));
     SS_CUDA(e, cudaFuncSetAttribute(k_ingest, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kIngestSmem));
+    SS_CUDA(e, cudaFuncSetAttribute(k_bk_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, kBkNBMax * 4));
+    SS_CUDA(e, cudaFuncSetAttribute(k_bk_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BkSmem::bytes));
+    SS_CUDA(e, cudaFuncSetAttribute(k_bk_local, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BkLocSmem::bytes));
     for (int b = 0; b <= 14; ++b) {
         const RankKernel rk = b ? rank_kernel(b) : k_rank_place<0>;
         SS_CUDA(e, cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rank_smem_bytes(kRankMaxG)));
@@ -1097,6 +1137,31 @@ static int launch_place_step(ss_engine* e, const uint32_t* dk, const int32_t* dv
     const int n_chunk = (int)std::max<int64_t>(1, (n + e->S - 1) / e->S);
     int cs = 0;
     while ((int64_t(1) << cs) < e->S) ++cs;
+    if (e->bucket && !e->trace_on) {
+        BucketArgs a = e->bk;
+        a.keys = dk;
+        a.vals = dv;
+        a.n = n;
+        a.G = (uint32_t)e->G;
+        a.gcount = e->gcount;
+        a.gkept = e->gkept;
+        a.gstart = e->gstart;
+        a.skey = e->kbuf;
+        a.sval = e->vbuf[1];
+        a.vout = e->vbuf[0];
+        a.bad = e->bad;
+        const int nblk = (int)((e->G + kBkBlk - 1) / kBkBlk);
+        ss_note_launch(), k_bk_flags_reduce<<<nblk, 1024, 0, e->st>>>(a);
+        ss_note_launch(), k_bk_flags_top<<<1, 1024, 0, e->st>>>(a, nblk);
+        ss_note_launch(), k_bk_flags_down<<<nblk, 1024, 0, e->st>>>(a);
+        ss_note_launch(), k_bk_hist<<<kBkSupers, 1024, kBkNBMax * 4, e->st>>>(a);
+        ss_note_launch(), k_bk_colscan<<<kBkNBMax / 32, 1024, 0, e->st>>>(a);
+        ss_note_launch(), k_bk_binscan<<<1, 1024, 0, e->st>>>(a);
+        ss_note_launch(), k_bk_scatter<<<kBkSupers, kBkThreads, BkSmem::bytes, e->st>>>(a);
+        ss_note_launch(), k_bk_local<<<2 * kNumSM, kBkLocThreads, BkLocSmem::bytes, e->st>>>(a);
+        SS_CUDA(e, cudaGetLastError());
+        return SS_OK;
+    }
     if (e->rank_place) {
         // one CTA per live chunk, cursors from the chunk prefix (k_batch_stats)
         static const int use_match = getenv("SS_B200_RANK_MATCH") ? atoi(getenv("SS_B200_RANK_MATCH")) : 0;
@@ -1232,7 +1297,7 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
                                                                                  e->bad, ((uintptr_t)dk % 16) == 0);
                 SS_CUDA(e, cudaGetLastError());
             }
-        } else if ((rc = launch_count(e, dk, n, e->S, true))) return rc;
+        } else if (!e->pre_counted && (rc = launch_count(e, dk, n, e->S, true))) return rc;
     }
     if (e->side_pending) {
         SS_CUDA(e, cudaStreamWaitEvent(e->st, e->ev_apply, 0));
@@ -1250,7 +1315,8 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
             SS_CUDA(e, cudaMemsetAsync(e->n_hot_dev, 0, 4, e->st));
             ss_note_launch(), k_hot_select<<<2 * kNumSM, 256, 0, e->st>>>(e->gcount, (uint32_t)e->G,
                                                         std::max<long long>(32, n / (4 * kHotCache)), e->hot_of,
-                                                        e->hot_g, e->n_hot_dev, e->bad);
+                                                        e->hot_g, e->n_hot_dev, e->bad,
+                                                        e->keys64 ? (int32_t*)e->kt.ent : nullptr, e->kt.slot_ent);
         }
     }
     e->alg_input += (e->keys64 ? 12 : 8) * n;   // the batch is read once: key + attr bytes
@@ -1405,13 +1471,24 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
         f.r_mx = e->r_mx;
         f.rescan = e->rescan;
         f.n_rescan = e->n_rescan;
+        f.sum_idx = e->sum_idx;
+        f.sum_valid = e->sum_valid;
+        f.n_sum = e->n_sum;
         f.bad = e->bad;
         ss_note_launch(), k_finalize<<<2 * kNumSM, 256, 0, e->st>>>(f);
         if (e->minmax) {
-            ss_note_launch(), k_rescan_reset<<<4, 256, 0, e->st>>>(e->rescan, e->n_rescan, e->mn, e->mx);
-            ss_note_launch(), k_minmax_rescan<<<8 * kNumSM, 256, 0, e->st>>>(e->rescan, e->n_rescan, e->ring, e->off, e->W, e->mn,
-                                                           e->mx);
-            ss_note_launch(), k_rescan_rows<<<4, 256, 0, e->st>>>(e->rescan, e->n_rescan, e->mn, e->mx, e->r_mn, e->r_mx);
+            if (e->sums) {
+                ss_note_launch(), k_mm_refresh<<<8 * kNumSM, 256, 0, e->st>>>(e->rescan, e->n_rescan, e->ring, e->off, e->W,
+                                                                               e->sum_idx, e->sum_valid, e->sums);
+                ss_note_launch(), k_mm_fold<<<2 * kNumSM, 256, 0, e->st>>>(e->rescan, e->n_rescan, e->W, e->sum_idx,
+                                                                            e->sum_valid, e->sums, e->mn, e->mx, e->r_mn,
+                                                                            e->r_mx);
+            } else {
+                ss_note_launch(), k_rescan_reset<<<4, 256, 0, e->st>>>(e->rescan, e->n_rescan, e->mn, e->mx);
+                ss_note_launch(), k_minmax_rescan<<<8 * kNumSM, 256, 0, e->st>>>(e->rescan, e->n_rescan, e->ring, e->off,
+                                                                                 e->W, e->mn, e->mx);
+                ss_note_launch(), k_rescan_rows<<<4, 256, 0, e->st>>>(e->rescan, e->n_rescan, e->mn, e->mx, e->r_mn, e->r_mx);
+            }
         }
         if (emit && e->host_emit) {
             const int b = (int)(e->emit_seq & 1);
@@ -1833,7 +1910,7 @@ static int run_step(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_t
     for (auto& g : e->graphs)
         if (g.dk == dk && g.dv == dv && g.n == n && same_bal(bal, g.bal) && g.plan_cur == e->plan_cur &&
             g.plan_valid == (int)e->plan_valid && g.emit_b == emit_b && g.host_emit == (int)e->host_emit &&
-            g.stage == e->cur_stage) {
+            g.stage == e->cur_stage && g.pre_counted == (int)e->pre_counted) {
             hit = &g;
             break;
         }
@@ -1887,6 +1964,7 @@ static int run_step(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_t
         ge.emit_b = emit_b;
         ge.host_emit = (int)e->host_emit;
         ge.stage = e->cur_stage;
+        ge.pre_counted = (int)e->pre_counted;
         ge.exec = exec;
         ge.launches = per_replay;
         e->graphs.push_back(ge);
@@ -2488,6 +2566,7 @@ extern "C" int ss_import_state(ss_engine* e, const int32_t* groups, int64_t n, c
         SS_CUDA(e, cudaMemcpy(e->wsum + g, &s, 8, cudaMemcpyHostToDevice));
         SS_CUDA(e, cudaMemcpy(e->mn + g, &lo, 4, cudaMemcpyHostToDevice));
         SS_CUDA(e, cudaMemcpy(e->mx + g, &hi, 4, cudaMemcpyHostToDevice));
+        if (e->sum_valid) SS_CUDA(e, cudaMemset(e->sum_valid + g, 0, 1));   // ring rewritten
         pos += span;
     }
     return SS_OK;
@@ -2496,7 +2575,9 @@ extern "C" int ss_import_state(ss_engine* e, const int32_t* groups, int64_t n, c
 // --------------------------------------------------------------------------
 // int64 keys
 // --------------------------------------------------------------------------
-static int map_keys(ss_engine* e, const int64_t* keys, int64_t n, uint32_t* dout) {
+// keys -> slots (and, with `count`, the batch's group histogram: the
+// fused step then skips its count kernel)
+static int map_keys(ss_engine* e, const int64_t* keys, int64_t n, uint32_t* dout, bool count) {
     const long long* dk;
     if (is_device_ptr(keys)) dk = (const long long*)keys;
     else {
@@ -2506,15 +2587,21 @@ static int map_keys(ss_engine* e, const int64_t* keys, int64_t n, uint32_t* dout
     if (n == 0) return SS_OK;
     KeyTable& t = e->kt;
     const int nblk = (int)((n + kMarkBlk - 1) / kMarkBlk);
-    SS_CUDA(e, cudaMemsetAsync(t.pending, 0, 4, e->st));
-    ss_note_launch(), k_key_probe<<<8 * kNumSM, 256, 0, e->st>>>(dk, n, t, dout);
+    const int64_t range = kCountChunk;                   // divides the count chunk S
+    const unsigned grid = (unsigned)((n + range - 1) / range);
+    SS_CUDA(e, cudaMemsetAsync(t.n_pend, 0, 4, e->st));
+    if (count)
+        ss_note_launch(), k_key_count<true><<<grid, 512, kHotCache * 4, e->st>>>(dk, n, t, dout, e->S, range, e->gcnt,
+                                                                              e->hot_g, kHotCache);
+    else
+        ss_note_launch(), k_key_count<false><<<grid, 512, 0, e->st>>>(dk, n, t, dout, e->S, range, nullptr, nullptr, 0);
     ss_note_launch(), k_key_rank_small<<<1, 1024, 0, e->st>>>(t);
     ss_note_launch(), k_key_mark<<<2 * kNumSM, 256, 0, e->st>>>(t);
     ss_note_launch(), k_key_mark_count<<<nblk, 1024, 0, e->st>>>(t, n, e->kbsum);
     ss_note_launch(), k_key_mark_scan<<<1, 1024, 0, e->st>>>(t, e->kbsum, nblk);
     ss_note_launch(), k_key_mark_assign<<<nblk, 1024, 0, e->st>>>(t, n, e->kbsum);
     ss_note_launch(), k_key_mark_done<<<1, 1, 0, e->st>>>(t);
-    ss_note_launch(), k_key_map<<<8 * kNumSM, 256, 0, e->st>>>(dk, n, t, dout);
+    ss_note_launch(), k_key_map<<<4 * kNumSM, 256, 0, e->st>>>(dk, t, dout, e->S, count ? e->gcnt : nullptr, e->bad);
     SS_CUDA(e, cudaGetLastError());
     return SS_OK;
 }
@@ -2527,7 +2614,7 @@ extern "C" int ss_map_keys(ss_engine* e, const int64_t* keys, int64_t n, uint32_
     { int jr = join_side(e); if (jr) return jr; }
     const bool dev = is_device_ptr(out_slots);
     int rc;
-    if ((rc = map_keys(e, keys, n, dev ? out_slots : e->stage_keys))) return rc;
+    if ((rc = map_keys(e, keys, n, dev ? out_slots : e->stage_keys, false))) return rc;
     if (!dev && n) SS_CUDA(e, cudaMemcpyAsync(out_slots, e->stage_keys, n * 4, cudaMemcpyDeviceToHost, e->st));
     SS_CUDA(e, cudaStreamSynchronize(e->st));
     return SS_OK;
@@ -2552,8 +2639,13 @@ extern "C" int ss_step_keys64(ss_engine* e, const int64_t* keys, const int32_t* 
             return rc;
         dk = (const int64_t*)k64;
     }
-    if ((rc = map_keys(e, dk, n, e->stage_keys))) return rc;
-    return ss_step(e, e->stage_keys, dv, n, cfg, rep);
+    // large G: the key probe also counts the batch (one pass over the keys)
+    const bool count = e->G > 16384 && !e->stream_scope;
+    if ((rc = map_keys(e, dk, n, e->stage_keys, count))) return rc;
+    e->pre_counted = count;
+    rc = ss_step(e, e->stage_keys, dv, n, cfg, rep);
+    e->pre_counted = false;
+    return rc;
 }
 
 extern "C" int ss_set_host_emit(ss_engine* e, int enable) {

@@ -8,12 +8,20 @@
 // function of the stream (equivalent to the reference run on the stream
 // relabelled by first appearance, relabel_groups datagen.py:181-192).
 //
-// Per batch: k_key_probe claims entries for unseen keys (CAS on the key
-// word; INT64_MIN is the empty marker and is handled by a dedicated
-// entry) and records each new entry's first stream position with
-// atomicMin; k_key_mark + k_key_compact order the batch's new entries by
-// first position and hand out slots; k_key_map writes the slot of every
-// tuple.  Batches without new keys skip the ordering work.
+// Table entries are 16 bytes -- key, slot and the slot's hot-cache index
+// -- so a probe that hits costs ONE sector read, and the table (32 MB at
+// G = 1M) is read with an L2 evict_last policy while the streamed keys use
+// evict_first, so it stays resident in the 126 MB L2.
+//
+// Per batch: k_key_count probes every tuple, writes its slot and counts it
+// into the batch's group histogram (count_batch, partition.py:117-130):
+// groups hot in the previous batch in shared memory, the rest with
+// warp-aggregated global atomics -- the key lookup and the count are one
+// pass over the keys.  Tuples of keys without a slot yet (new keys) are
+// appended to a pending list and their entries' first stream positions
+// recorded with atomicMin; k_key_mark + k_key_compact order the batch's new
+// entries by first position and hand out slots; k_key_map writes and
+// counts the pending tuples.  Batches without new keys skip that work.
 #pragma once
 
 #include "common.cuh"
@@ -29,35 +37,68 @@ __device__ __forceinline__ unsigned long long key_hash(unsigned long long x) {
     return x;
 }
 
+struct __align__(16) KEntry {
+    unsigned long long key;     // kEmptyKey = free
+    int32_t slot;               // dense slot (-1 until assigned)
+    int32_t hot;                // index in the count kernel's hot cache, -1 if none
+};
+
 struct KeyTable {
-    unsigned long long* keys;   // [cap] kEmptyKey = free
-    int32_t* slot;              // [cap] dense slot (-1 until assigned)
-    unsigned int* first;        // [cap] first position in the current batch (new entries)
-    int32_t* ent;               // [n] entry index of each tuple of the batch
+    KEntry* ent;                // [cap + 1]; entry cap is INT64_MIN's
+    unsigned int* first;        // [cap + 1] first position in the current batch (new entries)
+    int32_t* pend;              // [n] tuples whose key had no slot at probe time
+    int32_t* pend_ent;          // [n] their entries
+    int* n_pend;
     int32_t* new_ent;           // [G] entries claimed in this batch
     int* n_new;
     int* n_slots;               // slots handed out so far
     int32_t* mark;              // [max_batch] entry whose first position is i, or -1
     unsigned long long* slot_keys;   // [G] key of each slot
+    int32_t* slot_ent;          // [G] entry of each slot
     int* min_key_entry;         // entry index used for INT64_MIN (-1)
     int* overflow;              // more distinct keys than G
-    int* pending;               // some tuple of the batch has a key without a slot yet
     unsigned long long cap_mask;
     int G;
 };
 
-// probe / claim.  The table has >= 2G entries, so probing terminates.
-// A tuple whose key already has a slot gets it written straight away (the
-// steady state: no second pass); a tuple of a key without a slot yet is
-// marked pending (out = ~0) with its entry remembered for k_key_map.
-constexpr int kProbeILP = 4;
+// L2 cache policies: the streamed batch leaves first, the table stays
+__device__ __forceinline__ unsigned long long policy_evict_first() {
+    unsigned long long p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ unsigned long long policy_evict_last() {
+    unsigned long long p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ ulonglong2 ld_stream_u64x2(const void* p, unsigned long long pol) {
+    ulonglong2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u64 {%0,%1}, [%2], %3;"
+                 : "=l"(r.x), "=l"(r.y) : "l"(p), "l"(pol));
+    return r;
+}
+// a table entry through the read-only path: the hottest keys' entries are
+// L1 hits.  A stale read is harmless -- an entry claimed meanwhile is found
+// again by key_entry's CAS (prev == k) or probed past; slots and hot
+// indices are only written by later kernels
+__device__ __forceinline__ KEntry ld_entry(const KEntry* p, unsigned long long pol) {
+    ulonglong2 r;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.u64 {%0,%1}, [%2], %3;" : "=l"(r.x), "=l"(r.y) : "l"(p), "l"(pol));
+    KEntry e;
+    e.key = r.x;
+    e.slot = (int32_t)(r.y & 0xffffffffull);
+    e.hot = (int32_t)(r.y >> 32);
+    return e;
+}
 
+// probe / claim.  The table has >= 2G entries, so probing terminates.
 __device__ __forceinline__ int key_entry(KeyTable& t, unsigned long long k, unsigned long long h) {
     while (true) {
-        const unsigned long long cur = t.keys[h];
+        const unsigned long long cur = t.ent[h].key;
         if (cur == k) return (int)h;
         if (cur == kEmptyKey) {
-            const unsigned long long prev = atomicCAS(&t.keys[h], kEmptyKey, k);
+            const unsigned long long prev = atomicCAS(&t.ent[h].key, kEmptyKey, k);
             if (prev == kEmptyKey) {
                 const int k2 = atomicAdd(t.n_new, 1);
                 if (k2 < t.G) t.new_ent[k2] = (int)h; else *t.overflow = 1;
@@ -69,57 +110,136 @@ __device__ __forceinline__ int key_entry(KeyTable& t, unsigned long long k, unsi
     }
 }
 
-__global__ void __launch_bounds__(256)
-k_key_probe(const long long* __restrict__ keys, int64_t n, KeyTable t, uint32_t* __restrict__ out) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x * kProbeILP;
-    bool any_pending = false;
-    for (int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x); i0 < n; i0 += stride) {
-        unsigned long long k[kProbeILP], cur[kProbeILP], h[kProbeILP];
-        // all first probes in flight together
+// K2 for int64 keys: probe + slot + count in one pass.  CTA b covers the
+// contiguous tuple range [b*range, (b+1)*range) inside one count chunk of S
+// tuples (range divides S), counted into row (b*range)/S of gcnt.
+constexpr int kKeyItems = 4;            // consecutive tuples per thread and round (2 x 16-byte loads)
+
+template <bool COUNT>
+__global__ void __launch_bounds__(512)
+k_key_count(const long long* __restrict__ keys, int64_t n, KeyTable t, uint32_t* __restrict__ out, int64_t S,
+            int64_t range, int32_t* __restrict__ gcnt, const int32_t* __restrict__ hot_g, int n_hot) {
+    extern __shared__ int32_t sh_hist[];                  // [n_hot]
+    const int64_t c0 = (int64_t)blockIdx.x * range;
+    if (c0 >= n) return;
+    const int64_t c1 = min64(n, c0 + range);
+    int32_t* dst = COUNT ? gcnt + (c0 / S) * (int64_t)t.G : nullptr;
+    if (COUNT) {
+        for (int i = threadIdx.x; i < n_hot; i += blockDim.x) sh_hist[i] = 0;
+        __syncthreads();
+    }
+    const unsigned long long pol_s = policy_evict_first(), pol_t = policy_evict_last();
+    const unsigned lane = lane_id();
+    const bool vec = ((uintptr_t)keys % 16) == 0 && ((uintptr_t)out % 16) == 0;
+    for (int64_t base = c0; base < c1; base += (int64_t)kKeyItems * blockDim.x) {
+        const int64_t i0 = base + (int64_t)kKeyItems * threadIdx.x;
+        unsigned long long k[kKeyItems];
+        const bool full = vec && i0 + kKeyItems <= c1;
+        if (full) {
+            const ulonglong2 a = ld_stream_u64x2(keys + i0, pol_s);
+            const ulonglong2 b = ld_stream_u64x2(keys + i0 + 2, pol_s);
+            k[0] = a.x; k[1] = a.y; k[2] = b.x; k[3] = b.y;
+        } else {
 #pragma unroll
-        for (int u = 0; u < kProbeILP; ++u) {
-            const int64_t i = i0 + (int64_t)u * gridDim.x * blockDim.x;
-            k[u] = (i < n) ? (unsigned long long)keys[i] : kEmptyKey;
-            h[u] = key_hash(k[u]) & t.cap_mask;
+            for (int u = 0; u < kKeyItems; ++u) k[u] = (i0 + u < c1) ? (unsigned long long)keys[i0 + u] : kEmptyKey;
         }
-        // first probes through the read-only path: the hottest keys' entries
-        // are then L1 hits instead of a stream of requests to one L2 slice.
-        // A stale read is harmless -- an entry claimed meanwhile is found
-        // again by key_entry's CAS (prev == k) or probed past
+        KEntry en[kKeyItems];
+        unsigned long long h[kKeyItems];
 #pragma unroll
-        for (int u = 0; u < kProbeILP; ++u) cur[u] = __ldg(t.keys + h[u]);
+        for (int u = 0; u < kKeyItems; ++u) {
+            h[u] = key_hash(k[u]) & t.cap_mask;
+            en[u] = ld_entry(t.ent + h[u], pol_t);        // all first probes in flight together
+        }
+        uint32_t sl[kKeyItems];
 #pragma unroll
-        for (int u = 0; u < kProbeILP; ++u) {
-            const int64_t i = i0 + (int64_t)u * gridDim.x * blockDim.x;
-            if (i >= n) continue;
-            int e;
-            if (k[u] == kEmptyKey) {
-                // the reserved marker value gets a dedicated entry: cap_mask + 1
-                e = (int)(t.cap_mask + 1);
-                if (atomicCAS(t.min_key_entry, -1, e) == -1) {
-                    const int k2 = atomicAdd(t.n_new, 1);
-                    if (k2 < t.G) t.new_ent[k2] = e; else *t.overflow = 1;
+        for (int u = 0; u < kKeyItems; ++u) {
+            const int64_t i = i0 + u;
+            sl[u] = 0xffffffffu;
+            int hot = -1;
+            bool pending = false;
+            int e = -1;
+            if (i < c1) {
+                if (k[u] == kEmptyKey) {
+                    // the reserved marker value gets a dedicated entry: cap_mask + 1
+                    e = (int)(t.cap_mask + 1);
+                    if (atomicCAS(t.min_key_entry, -1, e) == -1) {
+                        const int k2 = atomicAdd(t.n_new, 1);
+                        if (k2 < t.G) t.new_ent[k2] = e; else *t.overflow = 1;
+                    }
+                    en[u] = ld_entry(t.ent + e, pol_t);
+                } else if (en[u].key != k[u]) {
+                    e = key_entry(t, k[u], h[u]);
+                    en[u] = ld_entry(t.ent + e, pol_t);
+                } else {
+                    e = (int)h[u];
                 }
-            } else {
-                e = (cur[u] == k[u]) ? (int)h[u] : key_entry(t, k[u], h[u]);
+                if (en[u].slot >= 0) {
+                    sl[u] = (uint32_t)en[u].slot;
+                    hot = en[u].hot;
+                } else {
+                    pending = true;
+                    atomicMin(&t.first[e], (unsigned int)i);
+                }
             }
-            const int sl = __ldg(t.slot + e);      // slots are assigned by later kernels only
-            if (sl >= 0) {
-                out[i] = (uint32_t)sl;
-            } else {
-                out[i] = 0xffffffffu;
-                t.ent[i] = e;
-                atomicMin(&t.first[e], (unsigned int)i);
-                any_pending = true;
+            // pending tuples: one warp-aggregated append to the pending list
+            const unsigned pm = __ballot_sync(SS_FULL, pending);
+            if (pm) {
+                int pb = 0;
+                if (lane == (unsigned)(__ffs(pm) - 1)) pb = atomicAdd(t.n_pend, __popc(pm));
+                pb = __shfl_sync(SS_FULL, pb, __ffs(pm) - 1);
+                if (pending) {
+                    const int r = pb + __popc(pm & lanemask_lt());
+                    t.pend[r] = (int32_t)i;
+                    t.pend_ent[r] = e;
+                }
             }
+            // count: hot groups in shared memory, the rest warp-aggregated
+            if (!COUNT) continue;
+            uint32_t g = sl[u];
+            if (hot >= 0 && hot < n_hot) {
+                atomicAdd(&sh_hist[hot], 1);
+                g = 0xffffffffu;
+            }
+            const unsigned peers = __match_any_sync(SS_FULL, g);
+            if (g != 0xffffffffu && lane == 31u - __clz(peers)) atomicAdd(&dst[g], __popc(peers));
+        }
+        if (full) {
+            *(uint4*)(out + i0) = make_uint4(sl[0], sl[1], sl[2], sl[3]);
+        } else {
+#pragma unroll
+            for (int u = 0; u < kKeyItems; ++u)
+                if (i0 + u < c1) out[i0 + u] = sl[u];
         }
     }
-    // one flag write per warp (a store per pending tuple would serialise
-    // on the flag's L2 slice)
-    if (__any_sync(SS_FULL, any_pending) && lane_id() == 0) *t.pending = 1;
+    if (!COUNT) return;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n_hot; i += blockDim.x) {
+        const int32_t c = sh_hist[i];
+        if (c) atomicAdd(&dst[hot_g[i]], c);
+    }
+}
+
+__global__ void k_key_init(KEntry* ent, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        KEntry e;
+        e.key = kEmptyKey;
+        e.slot = -1;
+        e.hot = -1;
+        ent[i] = e;
+    }
 }
 
 constexpr int kKeySmall = 2048;     // new keys ranked inside one CTA up to this many
+
+__device__ __forceinline__ void assign_slot(KeyTable& t, int e, int s) {
+    if (s < t.G) {
+        t.ent[e].slot = s;
+        t.slot_ent[s] = e;
+    } else {
+        *t.overflow = 1;
+    }
+    t.first[e] = 0xffffffffu;
+}
 
 // few new keys: rank them by first position inside one CTA
 __global__ void __launch_bounds__(1024)
@@ -137,9 +257,7 @@ k_key_rank_small(KeyTable t) {
     for (int i = threadIdx.x; i < nn; i += blockDim.x) {
         int r = 0;
         for (int j = 0; j < nn; ++j) r += f[j] < f[i];
-        if (base + r < t.G) t.slot[en[i]] = base + r;
-        else *t.overflow = 1;
-        t.first[en[i]] = 0xffffffffu;
+        assign_slot(t, en[i], base + r);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -204,9 +322,7 @@ k_key_mark_assign(KeyTable t, int64_t n, const int32_t* __restrict__ bsum) {
         int32_t tot;
         const int32_t ex = block_excl_scan(e >= 0 ? 1 : 0, red, &tot);
         if (e >= 0) {
-            if (base + ex < t.G) t.slot[e] = base + ex;
-            else *t.overflow = 1;
-            t.first[e] = 0xffffffffu;
+            assign_slot(t, e, base + ex);
             t.mark[i] = -1;
         }
         base += tot;
@@ -220,19 +336,38 @@ __global__ void k_key_mark_done(KeyTable t) {
     *t.n_new = 0;
 }
 
-// pending tuples -> slot; the first tuple of each freshly assigned key
-// also records the slot's key
+// pending tuples -> slot, counted into their chunk's row (a key without a
+// slot after assignment -- more distinct keys than G -- is a bad tuple);
+// the first tuple of each freshly assigned key records the slot's key
 __global__ void __launch_bounds__(256)
-k_key_map(const long long* __restrict__ keys, int64_t n, KeyTable t, uint32_t* __restrict__ out) {
-    if (*t.pending == 0) return;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        if (out[i] != 0xffffffffu) continue;
-        const int e = t.ent[i];
-        const int s = t.slot[e];
-        out[i] = (uint32_t)s;
-        if (t.first[e] == 0xffffffffu) {      // first tuple of a freshly assigned key writes it
-            if (atomicExch(&t.first[e], 0xfffffffeu) == 0xffffffffu) t.slot_keys[s] = (unsigned long long)keys[i];
+k_key_map(const long long* __restrict__ keys, KeyTable t, uint32_t* __restrict__ out, int64_t S,
+          int32_t* __restrict__ gcnt, unsigned long long* __restrict__ bad) {
+    const int np = *t.n_pend;
+    const int stride = gridDim.x * blockDim.x;
+    // a warp's iterations stay converged (the bound is rounded up to warps)
+    const int np_w = (np + 31) & ~31;
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < np_w; r += stride) {
+        uint32_t g = 0xffffffffu;
+        int64_t row = -1;
+        if (r < np) {
+            const int64_t i = t.pend[r];
+            const int e = t.pend_ent[r];
+            const int s = t.ent[e].slot;
+            out[i] = (uint32_t)s;
+            if (s < 0) {
+                atomicMin(bad, (unsigned long long)i);
+            } else {
+                g = (uint32_t)s;
+                row = i / S;
+                if (t.first[e] == 0xffffffffu) {     // first tuple of a freshly assigned key writes it
+                    if (atomicExch(&t.first[e], 0xfffffffeu) == 0xffffffffu) t.slot_keys[s] = (unsigned long long)keys[i];
+                }
+            }
         }
+        // pending tuples of one chunk row and group: one atomic per warp
+        const unsigned peers = __match_any_sync(SS_FULL, (unsigned long long)row << 32 | g);
+        if (gcnt && g != 0xffffffffu && lane_id() == 31u - __clz(peers))
+            atomicAdd(&gcnt[row * t.G + g], __popc(peers));
     }
 }
 

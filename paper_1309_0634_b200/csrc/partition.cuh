@@ -152,7 +152,8 @@ k_count_rows(const uint32_t* __restrict__ groups, int64_t n, uint32_t G, int64_t
 // this batch (first kHotCache found).  hot_of is reset for the old list.
 __global__ void __launch_bounds__(256)
 k_hot_select(const int32_t* __restrict__ gcount, uint32_t G, long long thr, int32_t* __restrict__ hot_of,
-             int32_t* __restrict__ hot_g, int* __restrict__ n_hot_dev, const unsigned long long* __restrict__ bad) {
+             int32_t* __restrict__ hot_g, int* __restrict__ n_hot_dev, const unsigned long long* __restrict__ bad,
+             int32_t* __restrict__ ent_words = nullptr, const int32_t* __restrict__ slot_ent = nullptr) {
     if (*bad != (unsigned long long)kNoBad) return;
     for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < G; g += gridDim.x * blockDim.x) {
         int h = -1;
@@ -163,6 +164,9 @@ k_hot_select(const int32_t* __restrict__ gcount, uint32_t G, long long thr, int3
                 h = slot;
             }
         }
+        // int64 keys: the hot index also lives in the key's table entry
+        // (word 3 of the 16-byte entry), read by the fused probe + count
+        if (ent_words && hot_of[g] != h) ent_words[4 * (int64_t)slot_ent[g] + 3] = h;
         hot_of[g] = h;
     }
 }

@@ -467,8 +467,11 @@ struct FinalizeArgs {
     double* r_avg;
     int32_t* r_mn;
     int32_t* r_mx;
-    int2* rescan;               // (group, result row) whose MIN/MAX need a rescan
+    int4* rescan;               // (group, result row, old next_pos | -1, batch count) whose MIN/MAX need a rescan
     unsigned* n_rescan;
+    int32_t* sum_idx;           // [G] chunk-summary slot of a group (-1: none), or null (no summaries)
+    uint8_t* sum_valid;         // [G] its summaries describe the current ring
+    int* n_sum;                 // slots handed out
     const unsigned long long* bad;
 };
 
@@ -516,7 +519,14 @@ k_finalize(FinalizeArgs a) {
             a.bmin[g] = 0x7fffffff;
             a.bmax[g] = (int32_t)0x80000000;
         }
-        if (need_rescan) a.rescan[atomicAdd(a.n_rescan, 1u)] = make_int2((int)g, a.emit ? (int)slot : -1);
+        if (need_rescan) {
+            // p0 = -1: the window was not full before this batch (its chunk
+            // summaries, if any, are rebuilt from the whole ring)
+            if (a.sum_idx && a.sum_idx[g] < 0) a.sum_idx[g] = atomicAdd(a.n_sum, 1);
+            a.rescan[atomicAdd(a.n_rescan, 1u)] = make_int4((int)g, a.emit ? (int)slot : -1, f0 == W ? p0 : -1, K);
+        } else if (a.sum_valid && K >= W) {
+            a.sum_valid[g] = 0;                          // the whole window was replaced
+        }
         if (a.emit) {
             a.r_g[slot] = (int32_t)g;
             a.r_cnt[slot] = fill;
@@ -547,14 +557,23 @@ k_finalize(FinalizeArgs a) {
     }
 }
 
-// MIN/MAX of a full window after a partial eviction: every ring slot is
-// live, so the slot order does not matter.  Chunk-parallel: the listed
-// groups' windows are cut into kRescanChunk-value chunks spread over the
-// whole grid, folded with atomicMin/Max after a reset, then copied into
-// the result rows.
+// MIN/MAX of a full window after a partial eviction (hard part
+// 3): every ring slot is live, so the slot order does not matter.
+//  * small windows (W <= kMMSumMinW): chunk-parallel rescan of the whole
+//    window -- the listed groups' windows cut into kRescanChunk-value chunks
+//    over the grid, folded with atomicMin/Max after a reset;
+//  * large windows: per-group chunk summaries (min, max of each kMMChunk
+//    ring slots).  A batch rewrites ring slots [p0, p0 + K) mod W of a full
+//    window, so only the chunks it touched are rescanned (K + 2 kMMChunk
+//    values), then the W / kMMChunk summaries are folded -- instead of W
+//    values per group and batch.  A group's summaries are built from the
+//    whole ring the first time it needs them, and dropped (sum_valid = 0)
+//    when a batch replaces its whole window or its state is imported.
 constexpr int kRescanChunk = 16384;
+constexpr int kMMChunk = 4096;
+constexpr int64_t kMMSumMinW = 1 << 17;
 
-__global__ void k_rescan_reset(const int2* __restrict__ rescan, const unsigned* __restrict__ n_rescan,
+__global__ void k_rescan_reset(const int4* __restrict__ rescan, const unsigned* __restrict__ n_rescan,
                                int32_t* __restrict__ mn, int32_t* __restrict__ mx) {
     const unsigned n = *n_rescan;
     for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -563,23 +582,94 @@ __global__ void k_rescan_reset(const int2* __restrict__ rescan, const unsigned* 
     }
 }
 
+// min / max of ring values [lo, hi) of one group, CTA-wide (256 threads)
+__device__ __forceinline__ int2 cta_minmax(const int32_t* __restrict__ r, int64_t lo, int64_t hi) {
+    __shared__ int32_t s_mn[8], s_mx[8];
+    int32_t a = 0x7fffffff, b = (int32_t)0x80000000;
+    for (int64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) {
+        const int32_t v = r[j];
+        a = min(a, v);
+        b = max(b, v);
+    }
+    a = warp_min(a);
+    b = warp_max(b);
+    if (lane_id() == 0) { s_mn[warp_id()] = a; s_mx[warp_id()] = b; }
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int w = 1; w < 8; ++w) { a = min(a, s_mn[w]); b = max(b, s_mx[w]); }
+    __syncthreads();
+    return make_int2(a, b);         // valid in thread 0
+}
+
 __global__ void __launch_bounds__(256)
-k_minmax_rescan(const int2* __restrict__ rescan, const unsigned* __restrict__ n_rescan,
+k_minmax_rescan(const int4* __restrict__ rescan, const unsigned* __restrict__ n_rescan,
                 const int32_t* __restrict__ ring, const int64_t* __restrict__ off, int64_t W,
                 int32_t* __restrict__ mn, int32_t* __restrict__ mx) {
-    __shared__ int32_t s_mn[8], s_mx[8];
     const unsigned n = *n_rescan;
     const int64_t nch = (W + kRescanChunk - 1) / kRescanChunk;
     for (int64_t c = blockIdx.x; c < (int64_t)n * nch; c += gridDim.x) {
-        const int2 e = rescan[c / nch];
+        const int4 e = rescan[c / nch];
         const int64_t lo = (c % nch) * kRescanChunk;
-        const int64_t hi = min64(W, lo + kRescanChunk);
-        const int32_t* r = ring + off[e.x];
+        const int2 r = cta_minmax(ring + off[e.x], lo, min64(W, lo + kRescanChunk));
+        if (threadIdx.x == 0) {
+            atomicMin(&mn[e.x], r.x);
+            atomicMax(&mx[e.x], r.y);
+        }
+    }
+}
+
+__global__ void k_rescan_rows(const int4* __restrict__ rescan, const unsigned* __restrict__ n_rescan,
+                              const int32_t* __restrict__ mn, const int32_t* __restrict__ mx,
+                              int32_t* __restrict__ r_mn, int32_t* __restrict__ r_mx) {
+    const unsigned n = *n_rescan;
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int4 e = rescan[i];
+        if (e.y >= 0) {
+            r_mn[e.y] = mn[e.x];
+            r_mx[e.y] = mx[e.x];
+        }
+    }
+}
+
+// chunk summaries: rescan the chunks this batch touched (all of them when
+// the group's summaries are not valid)
+__global__ void __launch_bounds__(256)
+k_mm_refresh(const int4* __restrict__ rescan, const unsigned* __restrict__ n_rescan,
+             const int32_t* __restrict__ ring, const int64_t* __restrict__ off, int64_t W,
+             const int32_t* __restrict__ sum_idx, const uint8_t* __restrict__ sum_valid, int2* __restrict__ sums) {
+    const unsigned n = *n_rescan;
+    const int64_t nch = (W + kMMChunk - 1) / kMMChunk;
+    for (int64_t c = blockIdx.x; c < (int64_t)n * nch; c += gridDim.x) {
+        const int4 e = rescan[c / nch];
+        const int64_t ci = c % nch;
+        const int64_t lo = ci * kMMChunk, hi = min64(W, lo + kMMChunk);
+        if (e.z >= 0 && sum_valid[e.x]) {
+            // written slots: (p0 + j) mod W, 0 <= j < K
+            const int64_t p0 = e.z;
+            const bool touched = (p0 >= lo && p0 < hi) || ((lo - p0 + W) % W) < (int64_t)e.w;
+            if (!touched) continue;
+        }
+        const int2 r = cta_minmax(ring + off[e.x], lo, hi);
+        if (threadIdx.x == 0) sums[(int64_t)sum_idx[e.x] * nch + ci] = r;
+    }
+}
+
+// fold a group's summaries -> MIN/MAX state and its result row
+__global__ void __launch_bounds__(256)
+k_mm_fold(const int4* __restrict__ rescan, const unsigned* __restrict__ n_rescan, int64_t W,
+          const int32_t* __restrict__ sum_idx, uint8_t* __restrict__ sum_valid, const int2* __restrict__ sums,
+          int32_t* __restrict__ mn, int32_t* __restrict__ mx, int32_t* __restrict__ r_mn, int32_t* __restrict__ r_mx) {
+    __shared__ int32_t s_mn[8], s_mx[8];
+    const unsigned n = *n_rescan;
+    const int64_t nch = (W + kMMChunk - 1) / kMMChunk;
+    for (unsigned i = blockIdx.x; i < n; i += gridDim.x) {
+        const int4 e = rescan[i];
+        const int2* s = sums + (int64_t)sum_idx[e.x] * nch;
         int32_t a = 0x7fffffff, b = (int32_t)0x80000000;
-        for (int64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) {
-            const int32_t v = r[j];
-            a = min(a, v);
-            b = max(b, v);
+        for (int64_t j = threadIdx.x; j < nch; j += blockDim.x) {
+            const int2 v = s[j];
+            a = min(a, v.x);
+            b = max(b, v.y);
         }
         a = warp_min(a);
         b = warp_max(b);
@@ -587,23 +677,15 @@ k_minmax_rescan(const int2* __restrict__ rescan, const unsigned* __restrict__ n_
         __syncthreads();
         if (threadIdx.x == 0) {
             for (int w = 1; w < 8; ++w) { a = min(a, s_mn[w]); b = max(b, s_mx[w]); }
-            atomicMin(&mn[e.x], a);
-            atomicMax(&mx[e.x], b);
+            mn[e.x] = a;
+            mx[e.x] = b;
+            if (e.y >= 0) {
+                r_mn[e.y] = a;
+                r_mx[e.y] = b;
+            }
+            sum_valid[e.x] = 1;
         }
         __syncthreads();
-    }
-}
-
-__global__ void k_rescan_rows(const int2* __restrict__ rescan, const unsigned* __restrict__ n_rescan,
-                              const int32_t* __restrict__ mn, const int32_t* __restrict__ mx,
-                              int32_t* __restrict__ r_mn, int32_t* __restrict__ r_mx) {
-    const unsigned n = *n_rescan;
-    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const int2 e = rescan[i];
-        if (e.y >= 0) {
-            r_mn[e.y] = mn[e.x];
-            r_mx[e.y] = mx[e.x];
-        }
     }
 }
 
