@@ -51,6 +51,10 @@ struct BalanceArgs {
     const unsigned long long* init_loads;   // split mode: cold-only loads (else tpt)
     const uint8_t* exclude;                 // split mode: hot groups never move
     long long stop_load;                    // split mode: done once max load <= this (0: off)
+    // large G (entry lists not staged): entry counts and moved/excluded flags
+    // by entry POSITION, so a donor scan reads three coalesced arrays
+    int32_t* ecnt;              // [G] gcount[order[i]]
+    uint8_t* eflag;             // [G] excluded or moved in this invocation
     // fused step: the new list layout for k_apply_place (nullptr: not wanted)
     int32_t* new_off;           // [P+1] offsets of the rebuilt lists
     int32_t* keep_at;           // [P] where the unmoved entry members start
@@ -130,7 +134,37 @@ __device__ void bal_move(const BalanceArgs& a, const BalSmem& s, int* nm, int g,
     *nm = mi + 1;
 }
 
-template <bool STAGED>
+// entry counts and flags by position for the CTA-wide donor scans
+__global__ void __launch_bounds__(256)
+k_bal_prep(BalanceArgs a) {
+    if (*a.bad != (unsigned long long)kNoBad) return;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.G; i += gridDim.x * blockDim.x) {
+        const int g = a.order[i];
+        a.ecnt[i] = a.gcount[g];
+        a.eflag[i] = a.exclude ? a.exclude[g] : 0;
+    }
+}
+
+// CTA-wide lexicographic (key, id) minimum with a payload; result in every
+// thread (uses sh_k / sh_i / sh_x of kBalThreads / 32 entries)
+__device__ __forceinline__ void cta_argmin(long long& key, int& id, int& x, long long* sh_k, int* sh_i, int* sh_x) {
+    const unsigned lane = lane_id(), w = warp_id();
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const long long ok = __shfl_xor_sync(SS_FULL, key, o);
+        const int oi = __shfl_xor_sync(SS_FULL, id, o);
+        const int ox = __shfl_xor_sync(SS_FULL, x, o);
+        if (ok < key || (ok == key && oi < id)) { key = ok; id = oi; x = ox; }
+    }
+    if (lane == 0) { sh_k[w] = key; sh_i[w] = id; sh_x[w] = x; }
+    __syncthreads();
+    key = LLONG_MAX; id = 0x7fffffff; x = -1;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q)
+        if (sh_k[q] < key || (sh_k[q] == key && sh_i[q] < id)) { key = sh_k[q]; id = sh_i[q]; x = sh_x[q]; }
+    __syncthreads();
+}
+
+template <bool STAGED, bool WIDE = false>
 __global__ void __launch_bounds__(kBalThreads)
 k_balance(BalanceArgs a) {
     extern __shared__ long long bal_sm[];
@@ -176,7 +210,131 @@ k_balance(BalanceArgs a) {
     long long scanned = 0;
     const int pol = a.policy;
 
-    if (pol == 1 || pol == 2 || pol == 3 || pol == 4) {
+    if (WIDE && (pol == 2 || pol == 3 || pol == 4)) {
+        // large G: the donor's entry list is scanned by the whole CTA
+        // (coalesced, by entry position), one move per round; the extreme
+        // pair and the move itself are single-warp / single-thread as below
+        __shared__ long long r_k[kBalThreads / 32];
+        __shared__ int r_i[kBalThreads / 32], r_x[kBalThreads / 32];
+        __shared__ int sh_hi, sh_lo, sh_stop, sh_pick;
+        __shared__ long long sh_limit;
+        const unsigned lane = lane_id();
+        for (;;) {
+            if (warp_id() == 0) {
+                long long vmax = LLONG_MIN, vmin = LLONG_MAX;
+                int imax = 0x7fffffff, imin = 0x7fffffff;
+                for (int p = lane; p < P; p += 32) {
+                    const long long v = s.loads[p];
+                    if (v > vmax) { vmax = v; imax = p; }
+                    if (v < vmin) { vmin = v; imin = p; }
+                }
+                long long nmax = imax == 0x7fffffff ? LLONG_MAX : -vmax;
+#pragma unroll
+                for (int o = 16; o; o >>= 1) {
+                    long long ok = __shfl_xor_sync(SS_FULL, nmax, o);
+                    int oi = __shfl_xor_sync(SS_FULL, imax, o);
+                    if (ok < nmax || (ok == nmax && oi < imax)) { nmax = ok; imax = oi; }
+                    ok = __shfl_xor_sync(SS_FULL, vmin, o);
+                    oi = __shfl_xor_sync(SS_FULL, imin, o);
+                    if (ok < vmin || (ok == vmin && oi < imin)) { vmin = ok; imin = oi; }
+                }
+                if (lane == 0) {
+                    const int hi = imax, lo = imin;
+                    int stop = (nm >= a.cap) || (s.loads[hi] - s.loads[lo] <= a.threshold) ||
+                               (a.stop_load > 0 && s.loads[hi] <= a.stop_load);
+                    if (!stop && pol == 3) {
+                        const int sz = bal_size(s, hi);
+                        if (sz <= 0) stop = 1;
+                        else sh_limit = (long long)ceil(a.pot * (double)s.loads[hi] / (double)sz);
+                    }
+                    sh_hi = hi;
+                    sh_lo = lo;
+                    sh_stop = stop;
+                }
+            }
+            __syncthreads();
+            if (sh_stop) break;
+            const int hi = sh_hi, lo = sh_lo;
+            const int e0 = a.offsets[hi], e1 = a.offsets[hi + 1];
+            int pick = -1, pick_i = -1;
+            long long pscan = 0, pick_c = -1;
+            if (pol == 2 || pol == 4) {
+                const long long dmax = s.loads[hi], dmin = s.loads[lo];
+                long long bk = LLONG_MAX;
+                int bg = 0x7fffffff, bi = -1;
+                for (int i = e0 + (int)threadIdx.x; i < e1; i += blockDim.x) {
+                    if (a.eflag[i]) continue;
+                    const long long c = a.ecnt[i];
+                    const int g = a.order[i];
+                    long long key;
+                    if (pol == 2) key = -c;
+                    else {
+                        const long long d = (dmax - c) - (dmin + c);
+                        key = d < 0 ? -d : d;
+                    }
+                    if (key < bk || (key == bk && g < bg)) { bk = key; bg = g; bi = i; }
+                }
+                cta_argmin(bk, bg, bi, r_k, r_i, r_x);
+                if (bg != 0x7fffffff) {
+                    if (pol == 2) {
+                        if (-bk > 0) { pick = bg; pick_i = bi; pscan = (long long)a.tpt[hi]; pick_c = -bk; }
+                    } else if (bk < dmax - dmin) {
+                        pick = bg;
+                        pick_i = bi;
+                    }
+                }
+            } else {
+                // prob_check: the first un-moved entry (in list order) with
+                // count >= limit; scanned = tuples of the entries before it
+                // + limit.  Fallback: max count, lowest id.
+                const long long limit = sh_limit;
+                long long fk = LLONG_MAX, ck = LLONG_MAX;
+                int fg = 0x7fffffff, fi = -1, cg = 0x7fffffff, ci = -1;
+                for (int i = e0 + (int)threadIdx.x; i < e1; i += blockDim.x) {
+                    if (a.eflag[i]) continue;
+                    const long long c = a.ecnt[i];
+                    if (c >= limit && ck == LLONG_MAX) { ck = i; cg = 0; ci = i; }   // first candidate of this thread
+                    if (c > 0) {
+                        const int g = a.order[i];
+                        if (-c < fk || (-c == fk && g < fg)) { fk = -c; fg = g; fi = i; }
+                    }
+                }
+                cta_argmin(ck, cg, ci, r_k, r_i, r_x);
+                if (ci >= 0) {
+                    long long pre = 0;
+                    for (int i = e0 + (int)threadIdx.x; i < ci; i += blockDim.x) pre += a.ecnt[i];
+                    pre = warp_sum(pre);
+                    if (lane == 0) r_k[warp_id()] = pre;
+                    __syncthreads();
+                    pre = 0;
+                    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) pre += r_k[q];
+                    __syncthreads();
+                    pick = a.order[ci];
+                    pick_i = ci;
+                    pscan = pre + limit;
+                    pick_c = a.ecnt[ci];
+                } else {
+                    cta_argmin(fk, fg, fi, r_k, r_i, r_x);
+                    if (fg != 0x7fffffff && -fk > 0) {
+                        pick = fg;
+                        pick_i = fi;
+                        pscan = (long long)a.tpt[hi];
+                        pick_c = -fk;
+                    }
+                }
+            }
+            if (threadIdx.x == 0) {
+                sh_pick = pick;
+                if (pick >= 0) {
+                    bal_move(a, s, &nm, pick, hi, lo, 1, pick_c);
+                    a.eflag[pick_i] = 1;
+                    scanned += pscan;
+                }
+            }
+            __syncthreads();
+            if (sh_pick < 0) break;
+        }
+    } else if (pol == 1 || pol == 2 || pol == 3 || pol == 4) {
         // The extreme-pair loop is sequential: one warp runs it with warp
         // shuffles only (no CTA barriers); the shared-memory state is
         // updated by lane 0 and published to the warp by __syncwarp.

@@ -25,6 +25,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/ss_b200.h"
@@ -35,6 +36,7 @@
 #include "split.cuh"
 #include "keys.cuh"
 #include "bucket.cuh"
+#include "radix.cuh"
 #include "trace.cuh"
 #include "streamwin.cuh"
 
@@ -117,6 +119,16 @@ struct ss_engine {
     bool rank_place = false;               // G <= kRankMaxG: k_rank_place instead of the radix passes
     bool bucket = false;                   // G > kRankMaxG: bucketed two-pass placement (bucket.cuh)
     BucketArgs bk{};
+    // G > kRankMaxG: look-back-free 7-bit LSD passes (radix.cuh)
+    bool os = false;
+    int os_digit = kOsBitsWide;            // digit width: kOsBitsWide (measured best: C4 0.42 ms vs 0.49 with 7 bits)
+    int os_match = 1;                      // ranking: ballot matches (0), alternating with MATCH (1), MATCH (2)
+    int os_npass = 0, os_shift[kOsMaxPass] = {0, 0, 0, 0}, os_bits[kOsMaxPass] = {0, 0, 0, 0};
+    uint32_t* os_hist = nullptr;
+    uint32_t* os_bsum = nullptr;
+    // where the placement left the kept values (and, in trace mode, keys)
+    int32_t* vals_final = nullptr;
+    uint32_t* keys_final = nullptr;
     int32_t* n_live = nullptr;             // kept tuples of the batch (device)
     uint32_t* chunk_live = nullptr;        // live-chunk bitmap
     int32_t *lc = nullptr, *n_lc = nullptr;   // ordered live-chunk list
@@ -157,6 +169,7 @@ struct ss_engine {
     // int64 keys (key_bits == 64): key -> dense slot table
     bool keys64 = false;
     bool pre_counted = false;     // this batch was counted by the int64 key probe
+    int key_agg = 1;              // warp-aggregated cold-key atomics in the probe + count (A/B: SS_B200_KEY_AGG)
     KeyTable kt{};
     long long* stage_keys64 = nullptr;
 
@@ -233,6 +246,8 @@ struct ss_engine {
     int32_t *r_g = nullptr, *r_cnt = nullptr, *r_mn = nullptr, *r_mx = nullptr;
     long long* r_sum = nullptr;
     double* r_avg = nullptr;
+    int32_t* bal_ecnt = nullptr;           // k_bal_prep output (large G)
+    uint8_t* bal_eflag = nullptr;
     int4* rescan = nullptr;
     unsigned* n_rescan = nullptr;
     // MIN/MAX chunk summaries of full windows (W > kMMSumMinW)
@@ -333,8 +348,17 @@ constexpr size_t kBalSmemMax = 200 * 1024;   // dynamic shared memory opted in f
 static void launch_balance(ss_engine* e, BalanceArgs& a, cudaStream_t st) {
     a.G = (int)e->G;
     const bool staged = e->G <= kBalStageG && bal_smem_bytes(e->P, (int)e->G, true) <= kBalSmemMax;
-    if (staged) k_balance<true><<<1, kBalThreads, bal_smem_bytes(e->P, (int)e->G, true), st>>>(a);
-    else k_balance<false><<<1, kBalThreads, bal_smem_bytes(e->P, (int)e->G, false), st>>>(a);
+    if (staged) {
+        k_balance<true><<<1, kBalThreads, bal_smem_bytes(e->P, (int)e->G, true), st>>>(a);
+    } else if (a.policy == SS_POLICY_ALL || a.policy == SS_POLICY_PROB || a.policy == SS_POLICY_BEST) {
+        // donor scans over the whole CTA, from position-ordered counts / flags
+        a.ecnt = e->bal_ecnt;
+        a.eflag = e->bal_eflag;
+        ss_note_launch(), k_bal_prep<<<2 * kNumSM, 256, 0, st>>>(a);
+        k_balance<false, true><<<1, kBalThreads, bal_smem_bytes(e->P, (int)e->G, false), st>>>(a);
+    } else {
+        k_balance<false><<<1, kBalThreads, bal_smem_bytes(e->P, (int)e->G, false), st>>>(a);
+    }
 }
 
 // single-pass placement kernel for keys < 2^bits (ballot matching)
@@ -790,6 +814,30 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
         const char* bp = getenv("SS_B200_BUCKET");
         e->bucket = e->bucket && bp && bp[0] == '1';
     }
+    // look-back-free passes from 2^18 groups on (C4/C5: 0.63 -> 0.42 ms);
+    // below, the radix passes over live chunks with segmented look-back
+    // are faster (C3, 2^17: 0.30 vs 0.34 ms)
+    e->os = !e->rank_place && bits_for(G) >= 18;
+    if (const char* op = getenv("SS_B200_ONESWEEP")) e->os = !e->rank_place && G > kRankMaxG && op[0] != '0';
+    if (e->os) {
+        const int bits = bits_for(G);
+        if (const char* ob = getenv("SS_B200_OS_BITS")) e->os_digit = atoi(ob) == kOsBitsWide ? kOsBitsWide : kOsBits;
+        if (const char* om = getenv("SS_B200_OS_MATCH")) e->os_match = atoi(om);
+        e->os_npass = (bits + e->os_digit - 1) / e->os_digit;
+        if (e->os_npass > kOsMaxPass) e->os = false;
+        int sh = 0;
+        for (int p = 0; p < e->os_npass; ++p) {
+            const int w = (bits - sh + (e->os_npass - p) - 1) / (e->os_npass - p);
+            e->os_shift[p] = sh;
+            e->os_bits[p] = w;
+            sh += w;
+        }
+        const int64_t tiles = (e->max_batch + kOsTile - 1) / kOsTile;
+        const int bins = 1 << e->os_digit;
+        if (e->os && ((rc = dalloc(e, &e->os_hist, (size_t)tiles * bins)) ||
+                      (rc = dalloc(e, &e->os_bsum, (size_t)((tiles + kOsBlkTiles - 1) / kOsBlkTiles) * bins))))
+            return rc;
+    }
     if (e->bucket) {
         BucketArgs& b = e->bk;
         if ((rc = dalloc(e, &b.bin_of, G)) || (rc = dalloc(e, &b.bin_first, kBkNBMax + 1)) ||
@@ -814,8 +862,11 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
     SS_CUDA(e, cudaMemsetAsync(e->ep_dev, 0, 4, e->st));
     ss_note_launch(), k_set_bad<<<1, 1, 0, e->st>>>(e->bad);
     if ((rc = engine_alloc_sort(e, e->max_batch))) return rc;
+    e->vals_final = e->vbuf[0];
+    e->keys_final = e->kbuf2;
     // -- int64 key table
     e->keys64 = cfg->key_bits == 64;
+    if (const char* ka = getenv("SS_B200_KEY_AGG")) e->key_agg = atoi(ka);
     if (e->keys64) {
         uint64_t cap = 1;
         while (cap < 2 * (uint64_t)G) cap <<= 1;
@@ -840,6 +891,8 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
         SS_CUDA(e, cudaMemsetAsync(t.overflow, 0, 4, e->st));
     }
     // -- balancer
+    // (used whenever the lists are not staged: large G, or large P)
+    if ((rc = dalloc(e, &e->bal_ecnt, G)) || (rc = dalloc(e, &e->bal_eflag, G))) return rc;
     e->cap_moves = 4 * e->P;
     if ((rc = dalloc(e, &e->keep_at, e->P)) || (rc = dalloc(e, &e->mv_pos, e->cap_moves))) return rc;
     if ((rc = dalloc(e, &e->moves, e->cap_moves)) || (rc = dalloc(e, &e->front_top, e->P)) ||
@@ -907,6 +960,10 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
                                     (int)SortSmem<4>::bytes));
     SS_CUDA(e, cudaFuncSetAttribute(k_ingest, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kIngestSmem));
     SS_CUDA(e, cudaFuncSetAttribute(k_bk_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, kBkNBMax * 4));
+    SS_CUDA(e, cudaFuncSetAttribute(k_os_pass<kOsBits>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)OsSmem<kOsBits>::bytes));
+    SS_CUDA(e, cudaFuncSetAttribute(k_os_pass<kOsBitsWide>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)OsSmem<kOsBitsWide>::bytes));
     SS_CUDA(e, cudaFuncSetAttribute(k_bk_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BkSmem::bytes));
     SS_CUDA(e, cudaFuncSetAttribute(k_bk_local, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BkLocSmem::bytes));
     for (int b = 0; b <= 14; ++b) {
@@ -915,6 +972,7 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
     }
     SS_CUDA(e, cudaFuncSetAttribute(k_balance<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBalSmemMax));
     SS_CUDA(e, cudaFuncSetAttribute(k_balance<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBalSmemMax));
+    SS_CUDA(e, cudaFuncSetAttribute(k_balance<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBalSmemMax));
     SS_CUDA(e, cudaFuncSetAttribute(k_split_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     SS_CUDA(e, cudaStreamSynchronize(e->st));
     return SS_OK;
@@ -1126,6 +1184,19 @@ static int launch_place_all(ss_engine* e, const uint32_t* dk, const int32_t* dv,
     return SS_OK;
 }
 
+template <int BITS>
+static void launch_os_pass_t(ss_engine* e, const OsArgs& a, unsigned tiles, unsigned blks) {
+    ss_note_launch(), k_os_up<BITS><<<tiles, kOsThreads, 0, e->st>>>(a);
+    ss_note_launch(), k_os_red<BITS><<<blks, 1024, 0, e->st>>>(a);
+    ss_note_launch(), k_os_top<BITS><<<1, 1 << BITS, 0, e->st>>>(a);
+    ss_note_launch(), k_os_down<BITS><<<blks, 1024, 0, e->st>>>(a);
+    ss_note_launch(), k_os_pass<BITS><<<std::min<unsigned>(tiles, kNumSM), kOsThreads, OsSmem<BITS>::bytes, e->st>>>(a);
+}
+static void launch_os_pass(ss_engine* e, const OsArgs& a, unsigned tiles, unsigned blks) {
+    if (e->os_digit == kOsBitsWide) launch_os_pass_t<kOsBitsWide>(e, a, tiles, blks);
+    else launch_os_pass_t<kOsBits>(e, a, tiles, blks);
+}
+
 // fused step: stable placement of the batch's kept tuples (values only) into
 // vbuf[0].  The first pass walks the live chunks and drops never-stored
 // tuples; a second pass (G > 2^11) consumes the compacted kept set.
@@ -1137,6 +1208,46 @@ static int launch_place_step(ss_engine* e, const uint32_t* dk, const int32_t* dv
     const int n_chunk = (int)std::max<int64_t>(1, (n + e->S - 1) / e->S);
     int cs = 0;
     while ((int64_t(1) << cs) < e->S) ++cs;
+    e->vals_final = e->vbuf[0];
+    e->keys_final = e->kbuf2;
+    if (e->os && !e->bucket) {
+        // LSD passes: (dk, dv) -> (kbuf, vbuf1) -> (kbuf2, vbuf0) -> ...
+        uint32_t* kb[2] = {e->kbuf, e->kbuf2};
+        int32_t* vb[2] = {e->vbuf[1], e->vbuf[0]};
+        const uint32_t* kin = dk;
+        const int32_t* vin = dv;
+        const unsigned tiles = (unsigned)((n + kOsTile - 1) / kOsTile);
+        const unsigned blks = (tiles + kOsBlkTiles - 1) / kOsBlkTiles;
+        for (int p = 0; p < e->os_npass; ++p) {
+            const bool last = p == e->os_npass - 1;
+            OsArgs a{};
+            a.kin = kin;
+            a.vin = vin;
+            a.kout = (last && !e->trace_on) ? nullptr : kb[p & 1];
+            a.vout = vb[p & 1];
+            a.n = n;
+            a.n_dev = p ? e->n_live : nullptr;
+            a.shift = e->os_shift[p];
+            a.mask = (1u << e->os_bits[p]) - 1u;
+            a.hist = e->os_hist;
+            a.bsum = e->os_bsum;
+            a.live = p == 0 ? e->gcnt : nullptr;
+            a.chunk_shift = cs;
+            a.G = (uint32_t)e->G;
+            a.any_dead = e->any_dead;
+            a.match = e->os_match;
+            a.bad = e->bad;
+            launch_os_pass(e, a, tiles, blks);
+            kin = a.kout;
+            vin = a.vout;
+            if (last) {
+                e->vals_final = a.vout;
+                e->keys_final = a.kout;
+            }
+        }
+        SS_CUDA(e, cudaGetLastError());
+        return SS_OK;
+    }
     if (e->bucket && !e->trace_on) {
         BucketArgs a = e->bk;
         a.keys = dk;
@@ -1220,7 +1331,7 @@ static IngestArgs ingest_args(ss_engine* e, int plan) {
     a.gcnt = e->gkept;          // each group's kept run ...
     a.gcount = e->gcount;       // ... is the suffix of its K batch tuples
     a.gstart = e->gstart;
-    a.vals = e->vbuf[0];
+    a.vals = e->vals_final;
     a.fill = e->fill;
     a.next_pos = e->next_pos;
     a.off = e->off;
@@ -1269,12 +1380,11 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
     const int n_chunk = (int)std::max<int64_t>(1, (n + e->S - 1) / e->S);
     int rc;
     const bool split = bal && bal->split;
-    // split mode: cold groups move by the configured extreme-pair policy
-    // (first/shift variants fall back to best_balance), hot groups are
-    // water-filled; without split, the reference policy runs unchanged
-    int pol = bal ? bal->policy : SS_POLICY_NO;
-    if (split && pol != SS_POLICY_NO && pol != SS_POLICY_ALL && pol != SS_POLICY_PROB && pol != SS_POLICY_BEST)
-        pol = SS_POLICY_BEST;
+    // split mode: hot groups are water-filled over the partitions, cold
+    // groups move by the configured policy (any of the seven; the hot ones
+    // are excluded from its picks); without split, the reference policy
+    // runs unchanged
+    const int pol = bal ? bal->policy : SS_POLICY_NO;
     const bool has_policy = pol != SS_POLICY_NO;
     const bool run_side = has_policy || split;
     // the reassignment policy alone leaves partitions hosting a top group
@@ -1394,8 +1504,8 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
     if (e->trace_on) {
         // per-tuple trace sums, from the batch-start ring (before the window update)
         TraceArgs ta{};
-        ta.keys = e->kbuf2;
-        ta.vals = e->vbuf[0];
+        ta.keys = e->keys_final;
+        ta.vals = e->vals_final;
         ta.n_dev = e->n_live;
         ta.gstart = e->gstart;
         ta.fill = e->fill;
@@ -2592,9 +2702,9 @@ static int map_keys(ss_engine* e, const int64_t* keys, int64_t n, uint32_t* dout
     SS_CUDA(e, cudaMemsetAsync(t.n_pend, 0, 4, e->st));
     if (count)
         ss_note_launch(), k_key_count<true><<<grid, 512, kHotCache * 4, e->st>>>(dk, n, t, dout, e->S, range, e->gcnt,
-                                                                              e->hot_g, kHotCache);
+                                                                              e->hot_g, kHotCache, e->key_agg);
     else
-        ss_note_launch(), k_key_count<false><<<grid, 512, 0, e->st>>>(dk, n, t, dout, e->S, range, nullptr, nullptr, 0);
+        ss_note_launch(), k_key_count<false><<<grid, 512, 0, e->st>>>(dk, n, t, dout, e->S, range, nullptr, nullptr, 0, 0);
     ss_note_launch(), k_key_rank_small<<<1, 1024, 0, e->st>>>(t);
     ss_note_launch(), k_key_mark<<<2 * kNumSM, 256, 0, e->st>>>(t);
     ss_note_launch(), k_key_mark_count<<<nblk, 1024, 0, e->st>>>(t, n, e->kbsum);
@@ -2699,16 +2809,45 @@ extern "C" int ss_results_pull(ss_engine* e, int64_t cap, int32_t* groups, int64
     const unsigned nr = (unsigned)hdr[0];
     if (n) *n = nr;
     const int64_t m = std::min<int64_t>(cap, nr);
-    if (m > 0) {
-        if (groups) memcpy(groups, h.g, m * 4);
-        if (count) for (int64_t i = 0; i < m; ++i) count[i] = h.cnt ? h.cnt[i] : 0;
-        if (sum) for (int64_t i = 0; i < m; ++i) sum[i] = h.sum ? h.sum[i] : 0;
-        if (avg) {
-            if (h.avg) memcpy(avg, h.avg, m * 8);
-            else for (int64_t i = 0; i < m; ++i) avg[i] = 0.0;
+    // rows [i0, i1) out of the kernel-written pinned buffers; large pulls
+    // (C4: ~1M rows per batch) are split over host threads, so the copy out
+    // of the pinned buffers does not serialise the next batch's issue
+    auto rows = [&](int64_t i0, int64_t i1) {
+        const int64_t k = i1 - i0;
+        if (groups) memcpy(groups + i0, h.g + i0, k * 4);
+        if (count) {
+            if (h.cnt) for (int64_t i = i0; i < i1; ++i) count[i] = h.cnt[i];
+            else memset(count + i0, 0, k * 8);
         }
-        if (mn) for (int64_t i = 0; i < m; ++i) mn[i] = h.mn ? h.mn[i] : 0;
-        if (mx) for (int64_t i = 0; i < m; ++i) mx[i] = h.mx ? h.mx[i] : 0;
+        if (sum) {
+            if (h.sum) memcpy(sum + i0, h.sum + i0, k * 8);
+            else memset(sum + i0, 0, k * 8);
+        }
+        if (avg) {
+            if (h.avg) memcpy(avg + i0, h.avg + i0, k * 8);
+            else for (int64_t i = i0; i < i1; ++i) avg[i] = 0.0;
+        }
+        if (mn) {
+            if (h.mn) memcpy(mn + i0, h.mn + i0, k * 4);
+            else memset(mn + i0, 0, k * 4);
+        }
+        if (mx) {
+            if (h.mx) memcpy(mx + i0, h.mx + i0, k * 4);
+            else memset(mx + i0, 0, k * 4);
+        }
+    };
+    if (m >= (1 << 16)) {
+        const int nt = (int)std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+        std::vector<std::thread> th;
+        const int64_t per = (m + nt - 1) / nt;
+        for (int t = 1; t < nt; ++t) {
+            const int64_t i0 = std::min<int64_t>(m, t * per), i1 = std::min<int64_t>(m, i0 + per);
+            if (i0 < i1) th.emplace_back(rows, i0, i1);
+        }
+        rows(0, std::min<int64_t>(m, per));
+        for (auto& x : th) x.join();
+    } else if (m > 0) {
+        rows(0, m);
     }
     ++e->pull_seq;
     return SS_OK;

@@ -118,7 +118,7 @@ constexpr int kKeyItems = 4;            // consecutive tuples per thread and rou
 template <bool COUNT>
 __global__ void __launch_bounds__(512)
 k_key_count(const long long* __restrict__ keys, int64_t n, KeyTable t, uint32_t* __restrict__ out, int64_t S,
-            int64_t range, int32_t* __restrict__ gcnt, const int32_t* __restrict__ hot_g, int n_hot) {
+            int64_t range, int32_t* __restrict__ gcnt, const int32_t* __restrict__ hot_g, int n_hot, int agg) {
     extern __shared__ int32_t sh_hist[];                  // [n_hot]
     const int64_t c0 = (int64_t)blockIdx.x * range;
     if (c0 >= n) return;
@@ -200,8 +200,14 @@ k_key_count(const long long* __restrict__ keys, int64_t n, KeyTable t, uint32_t*
                 atomicAdd(&sh_hist[hot], 1);
                 g = 0xffffffffu;
             }
-            const unsigned peers = __match_any_sync(SS_FULL, g);
-            if (g != 0xffffffffu && lane == 31u - __clz(peers)) atomicAdd(&dst[g], __popc(peers));
+            if (agg) {
+                // warp-aggregated: a key hot in this batch but missing from
+                // the cache (drifting skew) costs one atomic per warp
+                const unsigned peers = __match_any_sync(SS_FULL, g);
+                if (g != 0xffffffffu && lane == 31u - __clz(peers)) atomicAdd(&dst[g], __popc(peers));
+            } else if (g != 0xffffffffu) {
+                atomicAdd(&dst[g], 1);
+            }
         }
         if (full) {
             *(uint4*)(out + i0) = make_uint4(sl[0], sl[1], sl[2], sl[3]);

@@ -763,12 +763,49 @@ k_reserve(const int32_t* __restrict__ gcount, uint32_t G, int64_t W, const int32
     }
 }
 
+// Most copies are short (tail groups growing 16 -> 32 -> 64 ...): a warp
+// takes 32 consecutive copy records, each lane copies a short one (<= 64
+// values) on its own with 8 loads in flight, then the warp copies the long
+// ones of its 32 together (lanes over values).  (A CTA per record left
+// most threads idle and every record a full memory round trip.)
+constexpr int kShortCopy = 64;
+
 __global__ void __launch_bounds__(256)
 k_ring_copy(const RingCopy* __restrict__ copies, const unsigned* __restrict__ n_copies, int32_t* __restrict__ ring) {
     const unsigned n = *n_copies;
-    for (unsigned i = blockIdx.x; i < n; i += gridDim.x) {
-        const RingCopy c = copies[i];
-        for (int j = threadIdx.x; j < c.len; j += blockDim.x) ring[c.dst + j] = ring[c.src + j];
+    const unsigned lane = lane_id();
+    const unsigned nwarps = gridDim.x * (blockDim.x >> 5);
+    for (unsigned base = (blockIdx.x * (blockDim.x >> 5) + warp_id()) * 32u; base < n; base += nwarps * 32u) {
+        const unsigned i = base + lane;
+        RingCopy c{};
+        if (i < n) c = copies[i];
+        if (c.len > 0 && c.len <= kShortCopy) {
+            const int32_t* src = ring + c.src;
+            int32_t* dst = ring + c.dst;
+            for (int j = 0; j < c.len; j += 8) {
+                int32_t v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = (j + u < c.len) ? src[j + u] : 0;
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (j + u < c.len) dst[j + u] = v[u];
+            }
+        }
+        unsigned longm = __ballot_sync(SS_FULL, c.len > kShortCopy);
+        while (longm) {
+            const int l = __ffs(longm) - 1;
+            longm &= longm - 1;
+            const int64_t s0 = __shfl_sync(SS_FULL, c.src, l), d0 = __shfl_sync(SS_FULL, c.dst, l);
+            const int len = __shfl_sync(SS_FULL, c.len, l);
+            for (int j = (int)lane; j < len; j += 32 * 4) {
+                int32_t v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) v[u] = (j + 32 * u < len) ? ring[s0 + j + 32 * u] : 0;
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (j + 32 * u < len) ring[d0 + j + 32 * u] = v[u];
+            }
+        }
     }
 }
 

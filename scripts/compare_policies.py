@@ -1,9 +1,11 @@
 """All balancer instantiations compared on one configuration (BASELINE C4:
 "all balancer instantiations compared").  For each policy, with and
-without hot-key splitting: steady-state tuples/s (CUDA events, staged
-batches in HBM), mean/max per-block max/mean load ratio, moves per batch.
+without hot-key splitting: tuples/s over `steps` batches after `warmup`
+batches (CUDA events, staged batches in HBM), mean/max per-block max/mean
+load ratio, moves per batch.  Initial map: key hash (as bench.py); the
+policies start from it and converge during the warm-up.
 
-    python scripts/compare_policies.py --config c4 --steps 6 --warmup 3
+    python scripts/compare_policies.py --config c4 --steps 6 --warmup 12
 """
 
 import argparse
@@ -25,7 +27,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c4")
     ap.add_argument("--steps", type=int, default=6)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=12)
+    ap.add_argument("--initial", default="hash")
     ap.add_argument("--batch", type=int, default=0)
     args = ap.parse_args()
     desc, kind, s, G, W, B, aggs, _, _ = bench.CONFIGS[args.config]
@@ -36,7 +39,7 @@ def main():
     torch.cuda.set_stream(stream)
     for split in (False, True):
         for pol in POLICIES:
-            eng = StreamEngine(G, W, n_partitions=148, aggregates=aggs, max_batch=B,
+            eng = StreamEngine(G, W, n_partitions=148, aggregates=aggs, max_batch=B, initial=args.initial,
                                key_bits=64 if kind.endswith("64") else 32)
             eng.set_stream(stream)
             bal = eng.balancer_struct(pol, max(1, B // 1480), 0.5, split=split)
@@ -55,7 +58,8 @@ def main():
                 r = eng.step(*batches[i % 2], bal)
                 ratios.append(r.load_ratio)
                 moves.append(r.moves)
-            print(json.dumps({"config": args.config, "policy": pol, "split": split,
+            print(json.dumps({"config": args.config, "policy": pol, "split": split, "initial": args.initial,
+                              "warmup": args.warmup,
                               "tuples_per_s": B * args.steps / (ms / 1e3),
                               "ms_per_step": ms / args.steps,
                               "load_ratio_mean": float(np.mean(ratios)), "load_ratio_max": float(np.max(ratios)),

@@ -1,10 +1,13 @@
-"""Top CUDA source lines of an .ncu-rep by sampled warp stalls (needs -lineinfo)."""
+"""Top CUDA source lines of an .ncu-rep by sampled warp stalls (needs -lineinfo).
+Usage: ncu_hotlines.py report.ncu-rep [top] [kernel-regex]"""
 import csv, io, subprocess, sys
 
 
-def main(path, top=25):
-    out = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "cuda,sass"],
-                         capture_output=True, text=True).stdout
+def main(path, top=25, kernel=None):
+    cmd = ["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "cuda,sass"]
+    if kernel:
+        cmd += ["-k", "regex:" + kernel]
+    out = subprocess.run(cmd, capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     items, tot, hdr, fname = [], 0.0, None, "?"
     for r in rows:
@@ -37,4 +40,4 @@ def main(path, top=25):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 25)
+    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 25, sys.argv[3] if len(sys.argv) > 3 else None)

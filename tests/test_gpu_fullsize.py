@@ -144,14 +144,22 @@ def test_c4_twelve_batches_wrap_the_top_window():
 
 
 @pytest.mark.parametrize("policy", ["first", "all", "prob", "best"])
-def test_full_shape_movelists(policy):
-    """C2 shape (G = 10K, P = 148, B = 2^24): the fused step's MoveList and
-    scanned count equal the oracle's policy (balance.py:141-293) on the same
-    batch and the assignment in force before it, batch after batch."""
+@pytest.mark.parametrize("G,W", [(10_000, 100_000), (1_000_000, 10_000_000)])
+def test_full_shape_movelists(policy, G, W):
+    """C2 and C4 group domains (G = 10K staged in the policy CTA's shared
+    memory; G = 1M scanned CTA-wide from global memory), P = 148, B = 2^24:
+    the fused step's MoveList and scanned count equal the oracle's policy
+    (balance.py:141-293) on the same batch and the assignment in force
+    before it, batch after batch."""
     import torch
     from oracle import port as O
     from paper_1309_0634_b200.stream_engine import StreamEngine
-    G, W, B, P = 10_000, 100_000, 1 << 24, 148
+    B, P = 1 << 24, 148
+    if policy == "prob" and G > 100_000:
+        # the oracle's per-tuple segment scan (balance.py:230-264) takes
+        # minutes per batch here; the CTA-wide prob_check path is checked
+        # against it at G = 20K by test_step_vs_oracle
+        pytest.skip("oracle prob_check too slow at G = 1M")
     rng = np.random.default_rng(41)
     eng = StreamEngine(G, W, n_partitions=P, aggregates=("count", "sum"), max_batch=B, initial="contiguous")
     thr = B // (10 * P)
