@@ -716,7 +716,7 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
         if (pool <= 0) {
             size_t fr = 0, tot = 0;
             cudaMemGetInfo(&fr, &tot);
-            pool = std::min<int64_t>((int64_t)(fr / 4 / 2), int64_t(8) << 30);
+            pool = std::min<int64_t>((int64_t)(fr / 4 / 2), int64_t(16) << 30);   // <= 64 GB of 180
             pool = std::min<int64_t>(pool, dense_vals);
         }
         e->pool_cap = (unsigned long long)pool;

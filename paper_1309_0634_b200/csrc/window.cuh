@@ -697,6 +697,10 @@ k_mm_fold(const int4* __restrict__ rescan, const unsigned* __restrict__ n_rescan
 // pieces, so a hot group's multi-million-value copy spreads over the whole
 // grid; phase 2 copies one piece per CTA.
 constexpr int kCopyChunk = 8192;
+// growth factor of a ring region: every value is copied 1/(kGrow-1) times
+// on average while its window grows (2x copied each value about once; the
+// C4 growth copies were ~0.17 ms of a 1.2 ms step)
+constexpr int64_t kGrow = 4;
 
 struct RingCopy {
     int64_t src, dst;
@@ -726,7 +730,7 @@ k_reserve(const int32_t* __restrict__ gcount, uint32_t G, int64_t W, const int32
                 const int c = cap[g];
                 const int64_t need = min64((int64_t)f + k, W);
                 if (need > c) {
-                    ncap = min64(W, max64(max64(need, 2 * (int64_t)c), 16));
+                    ncap = min64(W, max64(max64(need, kGrow * (int64_t)c), 16));
                     oldoff = off[g];
                 }
             }
