@@ -207,6 +207,34 @@ int  ss_export_state(ss_engine* e, const int32_t* groups, int64_t n, int64_t* me
 int  ss_import_state(ss_engine* e, const int32_t* groups, int64_t n, const int64_t* meta,
                      const int32_t* values);
 
+/* ---- device-resident multi-GPU data plane (no host reads; stream-ordered
+ * on the engine's stream, which the sharded host code sets to the stream
+ * NCCL runs on).  Replaces the host-staged route / count / policy /
+ * migration steps above for ShardedEngine.step (harness.py:99-117 run at
+ * GPU level; balance.py:141-172 with threads = GPUs; moves apply at t+1,
+ * harness.py:115-116). */
+/* stable split by owner into 8-byte (u32 group, i32 attr) records (device);
+ * counts_dev[n_dest] per destination, counts_dev[n_dest] = first bad tuple
+ * index or -1 (device) */
+int  ss_route_records(ss_engine* e, const uint32_t* groups, const int32_t* attrs, int64_t n,
+                      void* out_records, int64_t* counts_dev);
+/* owner map from a device array */
+int  ss_set_owner_dev(ss_engine* e, const int32_t* owner_dev, int n_dest);
+/* policy on device counts, moves applied to this engine's assignment on the
+ * device; moves (int4 group, src, dst, placement)[cap], their count and the
+ * new group -> partition map copied into device buffers */
+int  ss_balance_apply_dev(ss_engine* e, const int32_t* counts_dev, const ss_balancer* cfg, void* moves_dev,
+                          int32_t* n_moves_dev, int32_t* pmap_dev);
+/* window state of the groups this rank gives away (moves with src == rank)
+ * into per-destination blob segments: [n] ++ n x (g, fill, next_pos, sum_lo,
+ * sum_hi, min, max, span) ++ ring images; sizes_dev[n_dest] words each
+ * (-1: blob_cap too small) */
+int  ss_export_moves_dev(ss_engine* e, const void* moves_dev, const int32_t* n_moves_dev, int rank,
+                         int32_t* blob_dev, int64_t blob_cap_words, int64_t* sizes_dev);
+/* received segments (word offsets seg_off[n_seg + 1], host) -> window state */
+int  ss_import_blob_dev(ss_engine* e, const int32_t* blob_dev, const int64_t* seg_off, int n_seg,
+                        int max_groups);
+
 /* ---- measurement ------------------------------------------------------
  * Kernel classes timed with CUDA events on the engine stream while
  * profiling is enabled (bench.py's roofline numbers). */

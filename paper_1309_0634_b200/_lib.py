@@ -90,6 +90,11 @@ _SIGS = {
     "ss_balance_counts": (C.c_int, [_P, _P, C.POINTER(Balancer), _P, _P, _P, _P]),
     "ss_export_state": (C.c_int, [_P, _P, _I64, _P, _P, _I64, _P]),
     "ss_import_state": (C.c_int, [_P, _P, _I64, _P, _P]),
+    "ss_route_records": (C.c_int, [_P, _P, _P, _I64, _P, _P]),
+    "ss_set_owner_dev": (C.c_int, [_P, _P, C.c_int]),
+    "ss_balance_apply_dev": (C.c_int, [_P, _P, C.POINTER(Balancer), _P, _P, _P]),
+    "ss_export_moves_dev": (C.c_int, [_P, _P, _P, C.c_int, _P, _I64, _P]),
+    "ss_import_blob_dev": (C.c_int, [_P, _P, _P, C.c_int, C.c_int]),
     "ss_map_keys": (C.c_int, [_P, _P, _I64, _P]),
     "ss_set_trace": (C.c_int, [_P, C.c_int]),
     "ss_trace": (C.c_int, [_P, C.c_int64, _P, _P, C.POINTER(C.c_int64)]),

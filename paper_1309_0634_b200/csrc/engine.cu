@@ -231,6 +231,8 @@ struct ss_engine {
     int n_dest = 0;
     unsigned long long* route_cnt = nullptr;   // [16]
     uint32_t* route_base = nullptr;            // [16]
+    longlong4* mig_list = nullptr;             // [kMigMax] (ring offset, blob word, span, -) of exported groups
+    int* mig_n = nullptr;
 
     // hot-key split plans (split.cuh), double-buffered: plan[cur] executes
     // batch t while the planner writes plan[cur ^ 1] for batch t+1
@@ -2522,13 +2524,17 @@ extern "C" int ss_route(ss_engine* e, const uint32_t* groups, const int32_t* att
     return SS_OK;
 }
 
-// batch group counts of the last step (valid until the next step)
+// batch group counts of the last step (valid until the next step).  A
+// device destination is filled stream-ordered (no host synchronisation).
 extern "C" int ss_group_counts(ss_engine* e, int32_t* counts) {
     if (!e || !counts) return SS_E_CONFIG;
+    if (is_device_ptr(counts)) {
+        SS_CUDA(e, cudaMemcpyAsync(counts, e->gcount, e->G * 4, cudaMemcpyDeviceToDevice, e->st));
+        return SS_OK;
+    }
     SS_CUDA(e, cudaStreamSynchronize(e->st));
     SS_CUDA(e, cudaStreamSynchronize(e->side));
-    SS_CUDA(e, cudaMemcpy(counts, e->gcount, e->G * 4,
-                          is_device_ptr(counts) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost));
+    SS_CUDA(e, cudaMemcpy(counts, e->gcount, e->G * 4, cudaMemcpyDeviceToHost));
     return SS_OK;
 }
 
@@ -2537,6 +2543,286 @@ __global__ void k_tpt_from_counts(const int32_t* __restrict__ counts, int64_t G,
     for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < G; g += (int64_t)gridDim.x * blockDim.x)
         if (counts[g]) atomicAdd(&tpt[pmap[g]], (unsigned long long)counts[g]);
 }
+
+// ---- device-resident multi-GPU data plane ---------------------------------
+// Everything below is stream-ordered on the engine's stream and reads
+// nothing back to the host: the caller (sharded.py) does one small control
+// read per batch (route counts, the bad-tuple status and migration sizes),
+// which NCCL's host API needs for the all-to-all split sizes.
+
+// route bases from the owner histogram; counts_dev[d] for d < n_dest
+__global__ void k_route_base(const unsigned long long* __restrict__ cnt, int n_dest, uint32_t* __restrict__ base,
+                             int64_t* __restrict__ counts_dev) {
+    if (threadIdx.x != 0) return;
+    uint32_t run = 0;
+    for (int d = 0; d < 16; ++d) {
+        base[d] = run;
+        run += (uint32_t)cnt[d];
+        if (d < n_dest) counts_dev[d] = (int64_t)cnt[d];
+    }
+}
+// counts_dev[n_dest] = first bad tuple index (or -1); the route mutates no
+// engine state, so the flag is cleared for the batch that follows
+__global__ void k_route_done(unsigned long long* __restrict__ bad, int n_dest, int64_t* __restrict__ counts_dev) {
+    if (threadIdx.x != 0) return;
+    const unsigned long long b = *bad;
+    counts_dev[n_dest] = b == (unsigned long long)kNoBad ? -1 : (int64_t)b;
+    *bad = (unsigned long long)kNoBad;
+}
+
+// Stable split by owning GPU into 8-byte (group, attr) records -- the one
+// message the tuple all-to-all ships; counts_dev[n_dest + 1] on the device.
+extern "C" int ss_route_records(ss_engine* e, const uint32_t* groups, const int32_t* attrs, int64_t n,
+                                void* out_records, int64_t* counts_dev) {
+    if (!e || n < 0 || !counts_dev || (n && !out_records)) return SS_E_CONFIG;
+    if (!e->owner) return fail(e, SS_E_CONFIG, "ss_set_owner first");
+    if (!is_device_ptr(counts_dev) || (n && !is_device_ptr(out_records)))
+        return fail(e, SS_E_CONFIG, "ss_route_records: device outputs required");
+    { int jr = join_side(e); if (jr) return jr; }
+    const uint32_t* dk;
+    const int32_t* dv;
+    int rc;
+    if ((rc = stage_input(e, groups, attrs, n, &dk, &dv))) return rc;
+    if ((rc = engine_alloc_sort(e, n))) return rc;
+    SS_CUDA(e, cudaMemsetAsync(e->route_cnt, 0, 16 * 8, e->st));
+    if (n) ss_note_launch(), k_owner_hist<<<2 * kNumSM, 256, 0, e->st>>>(dk, n, (uint32_t)e->G, e->owner, e->route_cnt, e->bad);
+    ss_note_launch(), k_route_base<<<1, 32, 0, e->st>>>(e->route_cnt, e->n_dest, e->route_base, counts_dev);
+    if (n) {
+        SS_CUDA(e, cudaMemsetAsync(e->tickets, 0, 8, e->st));
+        ss_note_launch(), k_epoch_bump<<<1, 1, 0, e->st>>>(e->ep_dev);
+        const int tiles = (int)((n + kSortTile - 1) / kSortTile);
+        ss_note_launch(), k_sort_pass<4, true><<<std::min(tiles, 2 * kNumSM), kSortThreads, SortSmem<4>::bytes, e->st>>>(
+            dk, dv, (uint32_t*)out_records, nullptr, (int)n, 0, 15u, e->route_base, e->status, e->ep_dev, 0,
+            e->tickets, e->bad, 0, e->owner);
+    }
+    ss_note_launch(), k_route_done<<<1, 32, 0, e->st>>>(e->bad, e->n_dest, counts_dev);
+    SS_CUDA(e, cudaGetLastError());
+    return SS_OK;
+}
+
+// The owner map from a device array (the GPU-level engine's own pmap)
+extern "C" int ss_set_owner_dev(ss_engine* e, const int32_t* owner_dev, int n_dest) {
+    if (!e || !owner_dev || n_dest < 1 || n_dest > 16) return fail(e, SS_E_CONFIG, "n_dest must be in [1, 16]");
+    if (!is_device_ptr(owner_dev)) return fail(e, SS_E_CONFIG, "ss_set_owner_dev: device map required");
+    int rc;
+    if (!e->owner) {
+        if ((rc = dalloc(e, &e->owner, e->G)) || (rc = dalloc(e, &e->route_cnt, 16)) ||
+            (rc = dalloc(e, &e->route_base, 16)))
+            return rc;
+    }
+    SS_CUDA(e, cudaMemcpyAsync(e->owner, owner_dev, e->G * 4, cudaMemcpyDeviceToDevice, e->st));
+    e->n_dest = n_dest;
+    return SS_OK;
+}
+
+// The policy on device per-group counts, its moves applied to this
+// engine's assignment on the device (the GPU-level balancer: partitions =
+// GPUs).  Copies the moves (int4 group, src, dst, placement), their count
+// and the new group -> partition map into caller device buffers.
+extern "C" int ss_balance_apply_dev(ss_engine* e, const int32_t* counts_dev, const ss_balancer* cfg, void* moves_dev,
+                                    int32_t* n_moves_dev, int32_t* pmap_dev) {
+    if (!e || !cfg || !counts_dev || !moves_dev || !n_moves_dev || !pmap_dev) return SS_E_CONFIG;
+    int rc;
+    if ((rc = check_balancer(e, cfg))) return rc;
+    if (!is_device_ptr(counts_dev) || !is_device_ptr(moves_dev) || !is_device_ptr(n_moves_dev) ||
+        !is_device_ptr(pmap_dev))
+        return fail(e, SS_E_CONFIG, "ss_balance_apply_dev: device buffers required");
+    { int jr = join_side(e); if (jr) return jr; }
+    SS_CUDA(e, cudaMemcpyAsync(e->gcount, counts_dev, e->G * 4, cudaMemcpyDeviceToDevice, e->st));
+    SS_CUDA(e, cudaMemsetAsync(e->tpt, 0, e->P * 8, e->st));
+    SS_CUDA(e, cudaMemsetAsync(e->n_moves, 0, 4, e->st));
+    ss_note_launch(), k_tpt_from_counts<<<2 * kNumSM, 256, 0, e->st>>>(e->gcount, e->G, e->pmap, e->tpt);
+    const int cap = move_cap(e, cfg);
+    if (cfg->policy != SS_POLICY_NO) {
+        BalanceArgs a{};
+        a.policy = cfg->policy;
+        a.threshold = cfg->thread_threshold;
+        a.pot = cfg->pot;
+        a.cap = cap;
+        a.P = e->P;
+        a.order = e->order;
+        a.offsets = e->offsets;
+        a.gcount = e->gcount;
+        a.tpt = e->tpt;
+        a.moved = e->moved;
+        a.moves = e->moves;
+        a.front_top = e->front_top;
+        a.back_first = e->back_first;
+        a.mv_next = e->mv_next;
+        a.new_off = e->new_off;
+        a.keep_at = e->keep_at;
+        a.mv_pos = e->mv_pos;
+        a.n_moves = e->n_moves;
+        a.scanned = e->scanned;
+        a.final_tpt = e->final_tpt;
+        a.bad = e->bad;
+        ss_note_launch(), launch_balance(e, a, e->st);
+        ss_note_launch(), k_apply_place<<<e->P, 256, 0, e->st>>>(e->order, e->offsets, e->keep_at, e->moves,
+                                                                  e->n_moves, e->mv_pos, e->moved, e->new_order);
+        ss_note_launch(), k_apply_commit<<<2 * kNumSM, 256, 0, e->st>>>(e->order, e->offsets, e->new_order, e->new_off,
+                                                                        (int)e->G, e->P, e->moves, e->n_moves, e->pmap,
+                                                                        e->moved);
+    }
+    SS_CUDA(e, cudaMemcpyAsync(moves_dev, e->moves, (size_t)cap * sizeof(int4), cudaMemcpyDeviceToDevice, e->st));
+    SS_CUDA(e, cudaMemcpyAsync(n_moves_dev, e->n_moves, 4, cudaMemcpyDeviceToDevice, e->st));
+    SS_CUDA(e, cudaMemcpyAsync(pmap_dev, e->pmap, e->G * 4, cudaMemcpyDeviceToDevice, e->st));
+    SS_CUDA(e, cudaMemsetAsync(e->gcount, 0, e->G * 4, e->st));
+    SS_CUDA(e, cudaGetLastError());
+    return SS_OK;
+}
+
+// Window-state migration blobs (int32 words).  Per destination d, a segment
+//   [n] ++ n records (g, fill, next_pos, sum_lo, sum_hi, min, max, span) ++ values
+// (span = the ring image: fill values while filling, else all W slots, so
+// next_pos carries over and the migrated group is bit-identical).
+constexpr int kMigMax = 256;          // exported groups per batch (>= 4 x GPUs)
+constexpr int kMigRec = 8;
+
+__global__ void k_export_plan(const int4* __restrict__ moves, const int32_t* __restrict__ n_moves, int rank, int n_dest,
+                              int64_t W, const int32_t* __restrict__ fill, const int32_t* __restrict__ next_pos,
+                              const long long* __restrict__ wsum, const int32_t* __restrict__ mn,
+                              const int32_t* __restrict__ mx, const int64_t* __restrict__ off, int32_t* __restrict__ blob,
+                              int64_t blob_cap, int64_t* __restrict__ sizes, longlong4* __restrict__ list,
+                              int* __restrict__ n_list) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const int nm = min(*n_moves, kMigMax);
+    int64_t ng[16] = {0}, nv[16] = {0};
+    for (int i = 0; i < nm; ++i) {
+        const int4 m = moves[i];
+        if (m.y != rank || m.z == rank || m.z < 0 || m.z >= n_dest) continue;
+        const int f = fill[m.x];
+        ng[m.z] += 1;
+        nv[m.z] += (int64_t)f < W ? f : W;
+    }
+    int64_t seg[16], base = 0;
+    for (int d = 0; d < n_dest; ++d) {
+        seg[d] = base;
+        const int64_t words = ng[d] ? 1 + kMigRec * ng[d] + nv[d] : 0;
+        sizes[d] = words;
+        base += words;
+    }
+    if (base > blob_cap) {                          // caller raises: blob too small
+        for (int d = 0; d < n_dest; ++d) sizes[d] = -1;
+        *n_list = 0;
+        return;
+    }
+    int64_t rec[16], val[16];
+    for (int d = 0; d < n_dest; ++d) {
+        if (ng[d]) blob[seg[d]] = (int32_t)ng[d];
+        rec[d] = seg[d] + 1;
+        val[d] = seg[d] + 1 + kMigRec * ng[d];
+    }
+    int nl = 0;
+    for (int i = 0; i < nm; ++i) {
+        const int4 m = moves[i];
+        if (m.y != rank || m.z == rank || m.z < 0 || m.z >= n_dest) continue;
+        const int g = m.x, d = m.z;
+        const int f = fill[g];
+        const int64_t span = (int64_t)f < W ? f : W;
+        const unsigned long long s = (unsigned long long)wsum[g];
+        int32_t* r = blob + rec[d];
+        r[0] = g; r[1] = f; r[2] = next_pos[g];
+        r[3] = (int32_t)(uint32_t)s; r[4] = (int32_t)(uint32_t)(s >> 32);
+        r[5] = mn[g]; r[6] = mx[g]; r[7] = (int32_t)span;
+        rec[d] += kMigRec;
+        if (span) list[nl++] = make_longlong4(off[g], val[d], span, 0);
+        val[d] += span;
+    }
+    *n_list = nl;
+}
+
+__global__ void __launch_bounds__(256)
+k_export_vals(const longlong4* __restrict__ list, const int* __restrict__ n_list, const int32_t* __restrict__ ring,
+              int32_t* __restrict__ blob) {
+    if ((int)blockIdx.x >= *n_list) return;
+    const longlong4 c = list[blockIdx.x];
+    for (int64_t j = threadIdx.x; j < c.z; j += blockDim.x) blob[c.y + j] = ring[c.x + j];
+}
+
+extern "C" int ss_export_moves_dev(ss_engine* e, const void* moves_dev, const int32_t* n_moves_dev, int rank,
+                                   int32_t* blob_dev, int64_t blob_cap_words, int64_t* sizes_dev) {
+    if (!e || !moves_dev || !n_moves_dev || !blob_dev || !sizes_dev) return SS_E_CONFIG;
+    if (e->n_dest < 1) return fail(e, SS_E_CONFIG, "ss_set_owner first");
+    int rc;
+    if (!e->mig_list && ((rc = dalloc(e, &e->mig_list, kMigMax)) || (rc = dalloc(e, &e->mig_n, 1)))) return rc;
+    ss_note_launch(), k_export_plan<<<1, 32, 0, e->st>>>((const int4*)moves_dev, n_moves_dev, rank, e->n_dest, e->W,
+                                                         e->fill, e->next_pos, e->wsum, e->mn, e->mx, e->off, blob_dev,
+                                                         blob_cap_words, sizes_dev, e->mig_list, e->mig_n);
+    ss_note_launch(), k_export_vals<<<kMigMax, 256, 0, e->st>>>(e->mig_list, e->mig_n, e->ring, blob_dev);
+    SS_CUDA(e, cudaGetLastError());
+    return SS_OK;
+}
+
+struct MigSegs {
+    int64_t off[17];
+    int n;
+};
+
+// CTA (j, s): record j of the segment from source s -- ring space (a bump
+// reservation when the region is too small), values, state
+__global__ void __launch_bounds__(256)
+k_import(const int32_t* __restrict__ blob, MigSegs segs, int64_t W, int dense, int32_t* __restrict__ fill,
+         int32_t* __restrict__ next_pos, long long* __restrict__ wsum, int32_t* __restrict__ mn,
+         int32_t* __restrict__ mx, int64_t* __restrict__ off, int32_t* __restrict__ cap,
+         unsigned long long* __restrict__ pool_top, unsigned long long pool_cap, int* __restrict__ oom,
+         uint8_t* __restrict__ sum_valid, int32_t* __restrict__ ring, int64_t G) {
+    __shared__ int64_t sh_dst;
+    const int s = blockIdx.y, j = blockIdx.x;
+    if (segs.off[s + 1] == segs.off[s]) return;
+    const int32_t* seg = blob + segs.off[s];
+    const int ng = seg[0];
+    if (j >= ng) return;
+    const int32_t* r = seg + 1 + kMigRec * j;
+    int64_t vpos = 1 + (int64_t)kMigRec * ng;
+    for (int i = 0; i < j; ++i) vpos += seg[1 + kMigRec * i + 7];
+    const int g = r[0];
+    const int64_t span = r[7];
+    if (g < 0 || g >= G) return;
+    if (threadIdx.x == 0) {
+        int64_t o = off[g];
+        if (!dense && cap[g] < span) {
+            const int64_t ncap = min64(W, max64(span, 16));
+            const unsigned long long top = atomicAdd(pool_top, (unsigned long long)ncap);
+            if (top + (unsigned long long)ncap > pool_cap) {
+                *oom = 1;
+                o = -1;
+            } else {
+                o = (int64_t)top;
+                off[g] = o;
+                cap[g] = (int32_t)ncap;
+            }
+        }
+        sh_dst = o;
+        if (o >= 0) {
+            fill[g] = r[1];
+            next_pos[g] = r[2];
+            wsum[g] = (long long)(((unsigned long long)(uint32_t)r[4] << 32) | (uint32_t)r[3]);
+            mn[g] = r[5];
+            mx[g] = r[6];
+            if (sum_valid) sum_valid[g] = 0;        // ring rewritten: chunk summaries stale
+        }
+    }
+    __syncthreads();
+    const int64_t o = sh_dst;
+    if (o < 0) return;
+    for (int64_t i = threadIdx.x; i < span; i += blockDim.x) ring[o + i] = seg[vpos + i];
+}
+
+extern "C" int ss_import_blob_dev(ss_engine* e, const int32_t* blob_dev, const int64_t* seg_off, int n_seg,
+                                  int max_groups) {
+    if (!e || n_seg < 0 || n_seg > 16 || (n_seg && (!blob_dev || !seg_off))) return SS_E_CONFIG;
+    if (n_seg == 0 || max_groups <= 0) return SS_OK;
+    MigSegs s{};
+    for (int i = 0; i <= n_seg; ++i) s.off[i] = seg_off[i];
+    s.n = n_seg;
+    if (s.off[n_seg] == 0) return SS_OK;
+    ss_note_launch(), k_import<<<dim3((unsigned)std::min(max_groups, kMigMax), (unsigned)n_seg), 256, 0, e->st>>>(
+        blob_dev, s, e->W, e->dense ? 1 : 0, e->fill, e->next_pos, e->wsum, e->mn, e->mx, e->off, e->cap,
+        e->pool_top, e->pool_cap, e->oom, e->sum_valid, e->ring, e->G);
+    SS_CUDA(e, cudaGetLastError());
+    return SS_OK;
+}
+
 
 // The policy on given per-group counts (BatchStats.group_counts) against
 // the current assignment; nothing is applied.  Used by the GPU-level

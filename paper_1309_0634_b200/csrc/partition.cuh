@@ -1004,8 +1004,14 @@ k_sort_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
     for (int i = threadIdx.x; i < (int)tlive; i += kSortThreads) {
         const uint32_t k = skey[i];
         const uint32_t pos = gbase[MAPPED ? (uint32_t)dmap[k] : ((k >> shift) & mask)] + (uint32_t)i;
-        vout[pos] = sval[i];
-        if (kout) kout[pos] = k;
+        if (MAPPED && !vout) {
+            // multi-GPU route: one 8-byte (group, attr) record per tuple, the
+            // message the all-to-all ships
+            reinterpret_cast<uint2*>(kout)[pos] = make_uint2(k, (uint32_t)sval[i]);
+        } else {
+            vout[pos] = sval[i];
+            if (kout) kout[pos] = k;
+        }
     }
     // no closing barrier: everything this tile reads (staging buffer, gbase,
     // tile slots) is rewritten only after the next tile's post-ranking

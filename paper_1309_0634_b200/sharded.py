@@ -1,24 +1,42 @@
 """Key-sharded multi-GPU execution: one process per GPU.
 
-Every rank owns the groups whose owner is its rank (a group -> GPU map that
-starts as contiguous id ranges, like initial_assignment with threads =
-GPUs, partition.py:97-114).  Per batch:
+Every rank owns the groups whose owner is its rank.  The group -> GPU map
+is the assignment of a GPU-level engine whose "threads" are the GPUs; it
+starts as a key hash (``initial="hash"``: group g on GPU hash(g) mod N, the
+partitioner's hash option, stream_engine.hash_lists) or as contiguous id
+ranges (initial_assignment with threads = GPUs, partition.py:97-114).
 
-  1. each rank takes its contiguous slice of the global batch (so rank r's
+Per global batch, on the device and stream-ordered on ONE CUDA stream that
+the engines and NCCL share:
+
+  1. each rank takes its contiguous slice of the global batch (rank r's
      tuples all arrived before rank r+1's);
-  2. ``ss_route`` stably splits the slice by owner on the device;
-  3. counts, then tuples, are exchanged with all-to-all (NCCL over
-     NVLink/NVSwitch; gloo for CPU tests); received chunks are concatenated
-     in source-rank order, so every group's tuples arrive in global arrival
-     order -- the only thing the windows depend on;
-  4. the local StreamEngine runs the fused step on its share;
-  5. GPU-level balancing: per-group counts are all-reduced and the same
-     device policy (k_balance, "threads" = GPUs) runs on every rank on
-     identical inputs, so every rank derives the same moves without a
-     broadcast; moved groups' windows migrate from the old to the new
-     owner (exact ring images, next_pos included) before the next batch.
+  2. ``ss_route_records`` stably splits the slice by owner into 8-byte
+     (group, attr) records -- one message per tuple;
+  3. a [world, 3] control block (tuples to each peer, this rank's bad-tuple
+     status, migration words to each peer) is exchanged with one small
+     all-to-all and read back ONCE -- the only host read of the step:
+     NCCL's all-to-all takes its split sizes from the host;
+  4. window state of the groups the previous batch's GPU-level policy moved
+     travels as per-destination blobs (one all-to-all) and is imported on
+     the device (``ss_import_blob_dev``);
+  5. the records travel in one all-to-all (NCCL over NVLink/NVSwitch;
+     gloo in the CPU tests); received chunks are concatenated in source-rank
+     order, so every group's tuples arrive in global arrival order -- the
+     only thing the windows depend on -- and the local
+     fused step runs on them directly (``ss_step_records``);
+  6. GPU-level balancing: the batch's per-group counts are all-reduced on
+     the device, every rank runs the same device policy (k_balance,
+     "threads" = GPUs) on identical inputs -- so every rank derives the same
+     moves without a broadcast -- and applies them to its GPU-level
+     assignment (``ss_balance_apply_dev``); the owner map is refreshed from
+     that assignment on the device and the moved groups' state is exported
+     into the blobs step 4 ships before the next batch.  Moves decided on
+     batch t therefore take effect from batch t+1, the reference's
+     one-iteration delay (harness.py:115-116).
 
-The collectives are plumbing; all compute runs in libss_b200.so.
+The collectives are plumbing; all compute runs in libss_b200.so.  int64
+keys are single-GPU in this build (the route is over dense u32 group ids).
 """
 
 from __future__ import annotations
@@ -28,89 +46,66 @@ import ctypes as C
 import numpy as np
 
 from . import _lib as L
+from .errors import DataError, ExecutionError, InvalidConfigError
 from .stream_engine import StreamEngine, _ptr
 
+_CTRL = 3        # control words per peer: tuples, bad-tuple index (or -1), migration words
 
-def _coll_device(group):
+
+def _is_gloo(group) -> bool:
     import torch.distributed as dist
-    return "cpu" if dist.get_backend(group) == "gloo" else "cuda"
+    return dist.get_backend(group) == "gloo"
 
 
-def exchange_counts(counts, group=None):
-    """all-to-all of the per-destination counts -> per-source counts."""
+def _coll_in(t, group):
+    """Tensor as the collective backend wants it (gloo: host copy)."""
+    return t.cpu() if _is_gloo(group) else t
+
+
+def exchange_control(ctrl, group=None):
+    """all-to-all of the [world, k] control block -> (sent, received) on the
+    host; the one host read of a sharded step."""
     import torch
     import torch.distributed as dist
-    dev = _coll_device(group)
-    send = torch.as_tensor(np.asarray(counts, dtype=np.int64)).to(dev)
+    send = _coll_in(ctrl.contiguous(), group)
     recv = torch.empty_like(send)
     dist.all_to_all_single(recv, send, group=group)
-    return recv.cpu().numpy()
+    both = torch.stack([send, recv]).cpu().numpy()
+    return both[0], both[1]
 
 
-def exchange_tuples(send_g, send_a, send_counts, recv_counts, group=None):
-    """all-to-all of the routed tuples; output is source-rank ordered."""
+def exchange_records(rec, send_counts, recv_counts, group=None):
+    """One all-to-all of 8-byte (group, attr) records (int64 view); output
+    in source-rank order, on the input's device."""
     import torch
     import torch.distributed as dist
-    dev = _coll_device(group)
-    out_dev = send_g.device
-    sg, sa = send_g.to(dev), send_a.to(dev)
-    n = int(np.sum(recv_counts))
-    rg = torch.empty(n, dtype=send_g.dtype, device=dev)
-    ra = torch.empty(n, dtype=send_a.dtype, device=dev)
-    ins, outs = [int(x) for x in send_counts], [int(x) for x in recv_counts]
-    dist.all_to_all_single(rg, sg, outs, ins, group=group)
-    dist.all_to_all_single(ra, sa, outs, ins, group=group)
-    return rg.to(out_dev), ra.to(out_dev)
+    src = _coll_in(rec, group)
+    out = torch.empty(int(np.sum(recv_counts)), dtype=torch.int64, device=src.device)
+    dist.all_to_all_single(out, src, [int(x) for x in recv_counts], [int(x) for x in send_counts], group=group)
+    return out.to(rec.device, non_blocking=True)
 
 
-def allreduce_counts(counts: np.ndarray, group=None) -> np.ndarray:
+def exchange_words(buf, send_words, recv_words, group=None):
+    """All-to-all of int32 word segments (the migration blobs)."""
     import torch
     import torch.distributed as dist
-    t = torch.as_tensor(np.ascontiguousarray(counts, dtype=np.int32)).to(_coll_device(group))
-    dist.all_reduce(t, group=group)
-    return t.cpu().numpy()
+    src = _coll_in(buf[:int(np.sum(send_words))], group)
+    out = torch.empty(int(np.sum(recv_words)), dtype=torch.int32, device=src.device)
+    dist.all_to_all_single(out, src, [int(x) for x in recv_words], [int(x) for x in send_words], group=group)
+    return out.to(buf.device, non_blocking=True)
 
 
-def migrate(moves, rank, world, export_fn, import_fn, group=None):
-    """Ship the window state of moved groups from their old to their new
-    owner.  ``moves`` is identical on every rank; export_fn(groups) ->
-    (meta int64[n,5], values int32[...]); import_fn(groups, meta, values)."""
-    import torch
+def allreduce_counts(counts, group=None):
+    """Sum of per-group counts over the ranks, in place on the device
+    (through the host for gloo)."""
     import torch.distributed as dist
-    dev = _coll_device(group)
-    out = [[] for _ in range(world)]
-    for g, src, dst, _ in moves:
-        if src == rank and dst != rank:
-            out[dst].append(g)
-    payload, sizes = [], np.zeros(world, dtype=np.int64)
-    for d in range(world):
-        if not out[d]:
-            continue
-        gs = np.asarray(out[d], dtype=np.int32)
-        meta, vals = export_fn(gs)
-        blob = np.concatenate([np.asarray([len(gs), len(vals)], dtype=np.int64),
-                               gs.astype(np.int64), meta.reshape(-1).astype(np.int64),
-                               vals.astype(np.int64)])
-        payload.append(blob)
-        sizes[d] = len(blob)
-    recv_sizes = exchange_counts(sizes, group)
-    send = torch.as_tensor(np.concatenate(payload) if payload else np.zeros(0, np.int64)).to(dev)
-    recv = torch.empty(int(recv_sizes.sum()), dtype=torch.int64, device=dev)
-    dist.all_to_all_single(recv, send, [int(x) for x in recv_sizes], [int(x) for x in sizes], group=group)
-    buf = recv.cpu().numpy()
-    pos = 0
-    for s in range(world):
-        end = pos + int(recv_sizes[s])
-        while pos < end:
-            ng, nv = int(buf[pos]), int(buf[pos + 1])
-            pos += 2
-            gs = buf[pos:pos + ng].astype(np.int32)
-            pos += ng
-            meta = buf[pos:pos + 5 * ng].reshape(ng, 5)
-            pos += 5 * ng
-            vals = buf[pos:pos + nv].astype(np.int32)
-            pos += nv
-            import_fn(gs, meta, vals)
+    if _is_gloo(group):
+        h = counts.cpu()
+        dist.all_reduce(h, group=group)
+        counts.copy_(h)
+    else:
+        dist.all_reduce(counts, group=group)
+    return counts
 
 
 class ShardedEngine:
@@ -118,86 +113,127 @@ class ShardedEngine:
 
     def __init__(self, n_groups: int, window, n_partitions: int = 148, aggregates=("count", "sum", "avg"),
                  device: int = 0, max_batch: int = 1 << 24, sub_batch: int = 0, pool_values: int = 0,
-                 group=None):
+                 group=None, initial: str = "hash", stream=None):
+        import torch
         import torch.distributed as dist
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
-        self.n_groups = n_groups
+        if self.world > 16:
+            raise InvalidConfigError("at most 16 GPUs per sharded engine")
+        self.n_groups = int(n_groups)
+        self.dev = torch.device("cuda", device)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.dev)
         self.local = StreamEngine(n_groups, window, n_partitions=n_partitions, aggregates=aggregates,
                                   device=device, max_batch=max_batch, sub_batch=sub_batch,
-                                  pool_values=pool_values)
+                                  pool_values=pool_values, stream=self.stream)
+        self.window = self.local.window
         # the exchanged batch arrives in fresh buffers of varying size every
         # step: graph replay would recapture every time
         self.local.set_graphs(False)
         # GPU-level assignment + policy engine ("threads" = GPUs)
         self.gpu = StreamEngine(n_groups, 1, n_partitions=self.world, aggregates=("count", "sum"),
-                                device=device, max_batch=1 << 16)
-        self.owner, _ = self.gpu.get_lists()
-        self._set_owner()
-        self.last_gpu_moves = []
-
-    def _set_owner(self):
-        o = np.ascontiguousarray(self.owner, dtype=np.int32)
+                                device=device, max_batch=1 << 16, initial=initial, stream=self.stream)
+        owner, _ = self.gpu.get_lists()
+        o = np.ascontiguousarray(owner, dtype=np.int32)
         self.local._check(self.local._lib.ss_set_owner(self.local._h, _ptr(o)[0], self.world))
+        i32, i64 = torch.int32, torch.int64
+        self._route_cnt = torch.zeros(self.world + 1, dtype=i64, device=self.dev)
+        self._counts = torch.zeros(self.n_groups, dtype=i32, device=self.dev)
+        self._owner = torch.as_tensor(o).to(self.dev)
+        self._mig_words = torch.zeros(self.world, dtype=i64, device=self.dev)
+        self._moves = None
+        self._n_moves = torch.zeros(1, dtype=i32, device=self.dev)
+        self._blob = None
+        self._rec = None
+        self._keep = None
 
-    # -- device route --------------------------------------------------------
+    # -- device buffers ------------------------------------------------------
+    def _move_buffers(self, bal):
+        import torch
+        cap = 4 * self.world if bal.max_moves <= 0 else int(bal.max_moves)
+        if self._moves is None or self._moves.numel() < 4 * cap:
+            self._moves = torch.zeros(4 * cap, dtype=torch.int32, device=self.dev)
+        if self._blob is None:
+            # every exported group carries <= W ring values plus its record
+            words = min(cap, 256) * (self.window + 8) + self.world
+            self._blob = torch.empty(words, dtype=torch.int32, device=self.dev)
+        return cap
+
     def route(self, groups, attrs):
+        """Stable split of this rank's slice by owner into 8-byte records
+        (device int64 view) + counts[world + 1] (device; the last entry is
+        the first bad tuple index or -1)."""
         import torch
         n = len(groups)
-        dev = groups.device if isinstance(groups, torch.Tensor) else None
-        if dev is not None and dev.type == "cuda":
-            og = torch.empty(n, dtype=torch.int32, device=dev)
-            oa = torch.empty(n, dtype=torch.int32, device=dev)
-        else:
-            og = torch.empty(n, dtype=torch.int32)
-            oa = torch.empty(n, dtype=torch.int32)
-        counts = np.zeros(self.world, dtype=np.int64)
-        pg, _k1 = _ptr(groups)
-        pa, _k2 = _ptr(attrs)
-        self.local._check(self.local._lib.ss_route(self.local._h, pg, pa, n, _ptr(og)[0], _ptr(oa)[0],
-                                                   _ptr(counts)[0]))
-        return og, oa, counts
-
-    # -- state migration -----------------------------------------------------
-    def export_state(self, groups):
-        g = np.ascontiguousarray(groups, dtype=np.int32)
-        meta = np.zeros((len(g), 5), dtype=np.int64)
-        nv = C.c_int64()
-        lib, h = self.local._lib, self.local._h
-        self.local._check(lib.ss_export_state(h, _ptr(g)[0], len(g), _ptr(meta)[0], None, 0, C.byref(nv)))
-        vals = np.zeros(max(1, nv.value), dtype=np.int32)
-        self.local._check(lib.ss_export_state(h, _ptr(g)[0], len(g), _ptr(meta)[0], _ptr(vals)[0],
-                                              nv.value, C.byref(nv)))
-        return meta, vals[:nv.value]
-
-    def import_state(self, groups, meta, values):
-        g = np.ascontiguousarray(groups, dtype=np.int32)
-        m = np.ascontiguousarray(meta, dtype=np.int64)
-        v = np.ascontiguousarray(values, dtype=np.int32)
-        self.local._check(self.local._lib.ss_import_state(self.local._h, _ptr(g)[0], len(g), _ptr(m)[0],
-                                                          _ptr(v)[0]))
+        if self._rec is None or self._rec.numel() < max(1, n):
+            self._rec = torch.empty(max(1, n), dtype=torch.int64, device=self.dev)
+        pg, k1 = _ptr(groups)
+        pa, k2 = _ptr(attrs)
+        self._keep = (k1, k2, groups, attrs)
+        self.local._check(self.local._lib.ss_route_records(self.local._h, pg, pa, n, _ptr(self._rec)[0],
+                                                           _ptr(self._route_cnt)[0]))
+        return self._rec[:n], self._route_cnt
 
     # -- one global batch ------------------------------------------------------
     def step(self, groups, attrs, balancer=None, gpu_balancer=None):
-        """groups/attrs: this rank's contiguous slice of the global batch."""
-        send_g, send_a, counts = self.route(groups, attrs)
-        recv_counts = exchange_counts(counts, self.group)
-        rg, ra = exchange_tuples(send_g, send_a, counts, recv_counts, self.group)
-        rep = self.local.step(rg, ra, balancer)
-        self.last_gpu_moves = []
+        """groups/attrs: this rank's contiguous slice of the global batch
+        (u32 group ids; host or device).  Returns the tuples this rank ingested."""
+        import torch
+        n = len(groups)
+        rec, cnt = self.route(groups, attrs)
+        ctrl = torch.stack([cnt[:self.world], cnt[self.world].expand(self.world), self._mig_words], dim=1)
+        sent, got = exchange_control(ctrl, self.group)
+        bad = got[:, 1]
+        if (bad >= 0).any():
+            if sent[0, 1] >= 0:
+                i = int(sent[0, 1])
+                g = int(groups[i])
+                raise DataError(f"tuple {i} has group {g}, outside [0, {self.n_groups})")
+            r = int(np.flatnonzero(bad >= 0)[0])
+            raise DataError(f"rank {r} rejected this batch (a tuple outside [0, {self.n_groups}))")
+        send_w, recv_w = sent[:, 2], got[:, 2]
+        if (send_w < 0).any() or (recv_w < 0).any():
+            raise ExecutionError("migration blob too small")
+        if recv_w.any() or send_w.any():
+            blob_in = exchange_words(self._blob, send_w, recv_w, self.group)
+            seg = np.zeros(self.world + 1, dtype=np.int64)
+            np.cumsum(recv_w, out=seg[1:])
+            self.local._check(self.local._lib.ss_import_blob_dev(self.local._h, _ptr(blob_in)[0], _ptr(seg)[0],
+                                                                 self.world, min(256, self._moves.numel() // 4)))
+            self._mig_words.zero_()
+            self._keep_blob = blob_in
+        send_c, recv_c = sent[:, 0], got[:, 0]
+        mine = exchange_records(rec, send_c, recv_c, self.group)
+        self._keep_recv = mine
+        self.local.step_records(mine, balancer, sync=False)
         if gpu_balancer is not None and gpu_balancer.policy != L.POLICY_CODES["no"]:
-            c = np.zeros(self.n_groups, dtype=np.int32)
-            self.local._check(self.local._lib.ss_group_counts(self.local._h, _ptr(c)[0]))
-            total = allreduce_counts(c, self.group)
-            moves, _, _ = self.gpu.balance_counts(total, gpu_balancer)
-            if moves:
-                migrate(moves, self.rank, self.world, self.export_state, self.import_state, self.group)
-                self.gpu.apply_moves(moves)
-                self.owner, _ = self.gpu.get_lists()
-                self._set_owner()
-            self.last_gpu_moves = moves
-        return rep, int(np.sum(recv_counts))
+            lib = self.local._lib
+            self._move_buffers(gpu_balancer)
+            self.local._check(lib.ss_group_counts(self.local._h, _ptr(self._counts)[0]))
+            allreduce_counts(self._counts, self.group)
+            self.gpu._check(lib.ss_balance_apply_dev(self.gpu._h, _ptr(self._counts)[0], C.byref(gpu_balancer),
+                                                     _ptr(self._moves)[0], _ptr(self._n_moves)[0],
+                                                     _ptr(self._owner)[0]))
+            self.local._check(lib.ss_set_owner_dev(self.local._h, _ptr(self._owner)[0], self.world))
+            self.local._check(lib.ss_export_moves_dev(self.local._h, _ptr(self._moves)[0], _ptr(self._n_moves)[0],
+                                                      self.rank, _ptr(self._blob)[0], self._blob.numel(),
+                                                      _ptr(self._mig_words)[0]))
+        return int(np.sum(recv_c))
+
+    # -- inspection (synchronising; tests and reports only) --------------------
+    @property
+    def owner(self) -> np.ndarray:
+        return self._owner.cpu().numpy().astype(np.int64)
+
+    @property
+    def last_gpu_moves(self):
+        """Moves of the last step's GPU-level policy: (group, src, dst, placement)."""
+        if self._moves is None:
+            return []
+        nm = int(self._n_moves.cpu()[0])
+        m = self._moves[:4 * nm].cpu().numpy().reshape(-1, 4)
+        return [(int(g), int(s), int(d), "back" if int(p) == L.BACK_CODE else "front") for g, s, d, p in m]
 
     def close(self):
         self.local.close()

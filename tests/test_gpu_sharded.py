@@ -2,10 +2,13 @@
 
 Only one GPU is available to the tests, so both ranks run their engines
 on cuda:0 and exchange through gloo (host tensors); on an 8-GPU box the
-same ShardedEngine uses NCCL over NVLink.  Route (device), exchange,
-local fused step, GPU-level balancing (device policy on all-reduced
-counts) and window migration are all exercised; the merged state must
-equal the single-stream oracle (aggregates are assignment-independent).
+same ShardedEngine uses NCCL over NVLink.  Route into packed records
+(device), control + record exchange, local fused step on the received
+records, GPU-level balancing (device policy on all-reduced device counts,
+moves applied on the device) and device-blob window migration are all
+exercised, also under a drifting hot set (C5 semantics at a small shape);
+the merged state must equal the single-stream oracle (aggregates are
+assignment-independent).
 """
 
 import os
@@ -25,7 +28,15 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, q, G, W, B, nb, gpu_policy):
+def _stream(G, B, nb, drift):
+    from paper_1309_0634_b200 import datagen as D
+    if drift:
+        # C5 semantics at a small shape: Zipf s=1.2 whose hot set moves every 2 batches
+        return D.drifting_zipf(nb * B, G, 1.2, 2 * B, seed=31)
+    return D.stream_for(D.DatasetSpec(D.DatasetKind.ZIPF, nb * B, G, 1.2, 31))
+
+
+def _worker(rank, world, port, q, G, W, B, nb, gpu_policy, drift):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -34,13 +45,12 @@ def _worker(rank, world, port, q, G, W, B, nb, gpu_policy):
         from paper_1309_0634_b200 import datagen as D
         from paper_1309_0634_b200.sharded import ShardedEngine
         from paper_1309_0634_b200.stream_engine import StreamEngine
-        spec = D.DatasetSpec(D.DatasetKind.ZIPF, nb * B, G, 1.2, 31)
         eng = ShardedEngine(G, W, n_partitions=16, aggregates=("count", "sum", "avg", "min", "max"),
                             device=0, max_batch=B, sub_batch=16384)
         bal = StreamEngine.balancer_struct("prob", max(1, B // 160), 0.5)
         gbal = StreamEngine.balancer_struct(gpu_policy, max(1, B // 20), 0.5)
         n_moves = 0
-        for b in D.batches(D.stream_for(spec), B):
+        for b in D.batches(_stream(G, B, nb, drift), B):
             lo, hi = rank * len(b) // world, (rank + 1) * len(b) // world
             eng.step(b.groups[lo:hi].astype(np.int32), b.attrs[lo:hi].astype(np.int32), bal, gbal)
             n_moves += len(eng.last_gpu_moves)
@@ -56,8 +66,8 @@ def _worker(rank, world, port, q, G, W, B, nb, gpu_policy):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("gpu_policy", ["no", "prob"])
-def test_two_ranks_match_oracle(gpu_policy):
+@pytest.mark.parametrize("gpu_policy,drift", [("no", False), ("prob", False), ("prob", True), ("best", True)])
+def test_two_ranks_match_oracle(gpu_policy, drift):
     import torch.multiprocessing as mp
     from oracle import port as O
     from paper_1309_0634_b200 import datagen as D
@@ -65,7 +75,7 @@ def test_two_ranks_match_oracle(gpu_policy):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, G, W, B, nb, gpu_policy)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, G, W, B, nb, gpu_policy, drift)) for r in range(2)]
     for p in procs:
         p.start()
     res = [q.get(timeout=600) for _ in procs]
@@ -73,9 +83,8 @@ def test_two_ranks_match_oracle(gpu_policy):
         p.join(timeout=120)
     for r in res:
         assert r[5] is None, r[5]
-    spec = D.DatasetSpec(D.DatasetKind.ZIPF, nb * B, G, 1.2, 31)
     store = O.OStore(G, W)
-    for b in D.batches(D.stream_for(spec), B):
+    for b in D.batches(_stream(G, B, nb, drift), B):
         store.ingest(b.groups, b.attrs)
     cnt, sm, avg, mn, mx = store.aggregates()
     seen = np.zeros(G, dtype=bool)
@@ -93,3 +102,54 @@ def test_two_ranks_match_oracle(gpu_policy):
     assert seen.all()
     if gpu_policy != "no":
         assert moves > 0
+
+
+def _worker_bad(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1309_0634_b200.errors import DataError
+        from paper_1309_0634_b200.sharded import ShardedEngine
+        G = 100
+        eng = ShardedEngine(G, 8, n_partitions=4, device=0, max_batch=1000)
+        g = (np.arange(500) % G).astype(np.int32)
+        a = np.arange(500, dtype=np.int32)
+        eng.step(g, a)                                  # a clean batch first
+        snap0 = eng.local.snapshot()["window_sum"].copy()
+        bad = g.copy()
+        if rank == 1:
+            bad[37] = G + 5
+        msg = None
+        try:
+            eng.step(bad, a)
+        except DataError as ex:
+            msg = str(ex)
+        # the rejected batch changed nothing; the next clean one is accepted
+        same = np.array_equal(eng.local.snapshot()["window_sum"], snap0)
+        eng.step(g, a)
+        q.put((rank, msg, same, None))
+        eng.close()
+    except Exception:  # pragma: no cover - reported to the parent
+        import traceback
+        q.put((rank, None, False, traceback.format_exc()))
+    dist.destroy_process_group()
+
+
+def test_two_ranks_bad_tuple_rejected_everywhere():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_bad, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {r[0]: r for r in (q.get(timeout=300) for _ in procs)}
+    for p in procs:
+        p.join(timeout=60)
+    for r in res.values():
+        assert r[3] is None, r[3]
+        assert r[2]
+    assert res[1][1] == "tuple 37 has group 105, outside [0, 100)"
+    assert res[0][1].startswith("rank 1 rejected")
