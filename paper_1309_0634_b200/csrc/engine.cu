@@ -880,10 +880,12 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
             (rc = dalloc(e, &t.mark, e->max_batch)) || (rc = dalloc(e, &t.slot_keys, G)) ||
             (rc = dalloc(e, &t.min_key_entry, 1)) || (rc = dalloc(e, &t.overflow, 1)) ||
             (rc = dalloc(e, &e->stage_keys64, e->max_batch)) ||
-            (rc = dalloc(e, &e->kbsum, e->max_batch / kMarkBlk + 2)))
+            (rc = dalloc(e, &e->kbsum, e->max_batch / kMarkBlk + 2)) || (rc = dalloc(e, &t.hk_key, kHotTab)) ||
+            (rc = dalloc(e, &t.hk_idx, kHotTab)))
             return rc;
         t.cap_mask = cap - 1;
         t.G = (int)G;
+        ss_note_launch(), k_hot_keytab_clear<<<4, 1024, 0, e->st>>>(t);
         ss_note_launch(), k_key_init<<<296, 256, 0, e->st>>>(t.ent, (int64_t)cap + 1);
         SS_CUDA(e, cudaMemsetAsync(t.first, 0xff, (cap + 1) * 4, e->st));
         SS_CUDA(e, cudaMemsetAsync(t.mark, 0xff, e->max_batch * 4, e->st));
@@ -950,6 +952,7 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
     e->h_rep->bad = (unsigned long long)kNoBad;
     SS_CUDA(e, cudaFuncSetAttribute(k_count<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     SS_CUDA(e, cudaFuncSetAttribute(k_count_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    SS_CUDA(e, cudaFuncSetAttribute(k_key_count<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHotCache * 4));
     SS_CUDA(e, cudaFuncSetAttribute(k_sort_pass<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SortSmem<4>::bytes));
     SS_CUDA(e, cudaFuncSetAttribute(k_sort_pass<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SortSmem<5>::bytes));
     SS_CUDA(e, cudaFuncSetAttribute(k_sort_pass<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SortSmem<6>::bytes));
@@ -1429,6 +1432,7 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
                                                         std::max<long long>(32, n / (4 * kHotCache)), e->hot_of,
                                                         e->hot_g, e->n_hot_dev, e->bad,
                                                         e->keys64 ? (int32_t*)e->kt.ent : nullptr, e->kt.slot_ent);
+            if (e->keys64) ss_note_launch(), k_hot_keytab<<<1, 1024, 0, e->st>>>(e->kt, e->hot_g, e->n_hot_dev);
         }
     }
     e->alg_input += (e->keys64 ? 12 : 8) * n;   // the batch is read once: key + attr bytes

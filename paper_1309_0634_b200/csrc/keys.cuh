@@ -59,7 +59,17 @@ struct KeyTable {
     int* overflow;              // more distinct keys than G
     unsigned long long cap_mask;
     int G;
+    // hot-key table image (kHotTab open-addressing slots: key, hot index),
+    // rebuilt per batch from the count cache's hot groups; every count CTA
+    // loads it into shared memory so a hot tuple costs no table probe
+    unsigned long long* hk_key;
+    uint16_t* hk_idx;
 };
+
+constexpr int kHotTab = 4096;                       // >= 2 x kHotCache
+__device__ __forceinline__ unsigned hot_tab_slot(unsigned long long hash) {
+    return (unsigned)(hash >> 52) & (kHotTab - 1);      // high hash bits (the table uses the low ones)
+}
 
 // L2 cache policies: the streamed batch leaves first, the table stays
 __device__ __forceinline__ unsigned long long policy_evict_first() {
@@ -120,12 +130,18 @@ __global__ void __launch_bounds__(512)
 k_key_count(const long long* __restrict__ keys, int64_t n, KeyTable t, uint32_t* __restrict__ out, int64_t S,
             int64_t range, int32_t* __restrict__ gcnt, const int32_t* __restrict__ hot_g, int n_hot, int agg) {
     extern __shared__ int32_t sh_hist[];                  // [n_hot]
+    __shared__ __align__(16) unsigned long long hk[COUNT ? kHotTab : 1];
+    __shared__ __align__(16) uint16_t hi[COUNT ? kHotTab : 1];
     const int64_t c0 = (int64_t)blockIdx.x * range;
     if (c0 >= n) return;
     const int64_t c1 = min64(n, c0 + range);
     int32_t* dst = COUNT ? gcnt + (c0 / S) * (int64_t)t.G : nullptr;
     if (COUNT) {
         for (int i = threadIdx.x; i < n_hot; i += blockDim.x) sh_hist[i] = 0;
+        for (int i = threadIdx.x; i < kHotTab / 2; i += blockDim.x)
+            reinterpret_cast<ulonglong2*>(hk)[i] = reinterpret_cast<const ulonglong2*>(t.hk_key)[i];
+        for (int i = threadIdx.x; i < kHotTab / 8; i += blockDim.x)
+            reinterpret_cast<uint4*>(hi)[i] = reinterpret_cast<const uint4*>(t.hk_idx)[i];
         __syncthreads();
     }
     const unsigned long long pol_s = policy_evict_first(), pol_t = policy_evict_last();
@@ -145,10 +161,23 @@ k_key_count(const long long* __restrict__ keys, int64_t n, KeyTable t, uint32_t*
         }
         KEntry en[kKeyItems];
         unsigned long long h[kKeyItems];
+        int hot_hit[kKeyItems];
 #pragma unroll
         for (int u = 0; u < kKeyItems; ++u) {
-            h[u] = key_hash(k[u]) & t.cap_mask;
-            en[u] = ld_entry(t.ent + h[u], pol_t);        // all first probes in flight together
+            const unsigned long long hh = key_hash(k[u]);
+            h[u] = hh & t.cap_mask;
+            hot_hit[u] = -1;
+            if (COUNT && k[u] != kEmptyKey) {
+                // hot keys resolve in shared memory
+                unsigned s2 = hot_tab_slot(hh);
+                while (true) {
+                    const unsigned long long sk = hk[s2];
+                    if (sk == k[u]) { hot_hit[u] = hi[s2]; break; }
+                    if (sk == kEmptyKey) break;
+                    s2 = (s2 + 1) & (kHotTab - 1);
+                }
+            }
+            if (hot_hit[u] < 0) en[u] = ld_entry(t.ent + h[u], pol_t);   // the other first probes in flight together
         }
         uint32_t sl[kKeyItems];
 #pragma unroll
@@ -158,7 +187,10 @@ k_key_count(const long long* __restrict__ keys, int64_t n, KeyTable t, uint32_t*
             int hot = -1;
             bool pending = false;
             int e = -1;
-            if (i < c1) {
+            if (i < c1 && hot_hit[u] >= 0) {
+                hot = hot_hit[u];
+                sl[u] = (uint32_t)hot_g[hot];
+            } else if (i < c1) {
                 if (k[u] == kEmptyKey) {
                     // the reserved marker value gets a dedicated entry: cap_mask + 1
                     e = (int)(t.cap_mask + 1);
@@ -232,6 +264,44 @@ __global__ void k_key_init(KEntry* ent, int64_t n) {
         e.slot = -1;
         e.hot = -1;
         ent[i] = e;
+    }
+}
+
+__global__ void k_hot_keytab_clear(KeyTable t) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < kHotTab; i += gridDim.x * blockDim.x) {
+        t.hk_key[i] = kEmptyKey;
+        t.hk_idx[i] = 0xffff;
+    }
+}
+
+// the hot-key table image for the next batch's count (after k_hot_select)
+__global__ void __launch_bounds__(1024)
+k_hot_keytab(KeyTable t, const int32_t* __restrict__ hot_g, const int* __restrict__ n_hot_dev) {
+    __shared__ unsigned long long sk[kHotTab];
+    __shared__ uint16_t si[kHotTab];
+    for (int i = threadIdx.x; i < kHotTab; i += blockDim.x) {
+        sk[i] = kEmptyKey;
+        si[i] = 0xffff;
+    }
+    __syncthreads();
+    const int nh = min(*n_hot_dev, kHotCache);
+    for (int i = threadIdx.x; i < nh; i += blockDim.x) {
+        const unsigned long long k = t.slot_keys[hot_g[i]];
+        if (k == kEmptyKey) continue;                   // the reserved key keeps its table entry
+        unsigned h = hot_tab_slot(key_hash(k));
+        while (true) {
+            const unsigned long long prev = atomicCAS(&sk[h], kEmptyKey, k);
+            if (prev == kEmptyKey || prev == k) {
+                si[h] = (uint16_t)i;
+                break;
+            }
+            h = (h + 1) & (kHotTab - 1);
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kHotTab; i += blockDim.x) {
+        t.hk_key[i] = sk[i];
+        t.hk_idx[i] = si[i];
     }
 }
 

@@ -15,7 +15,7 @@
 //              digit -> hist[tile][128] (pass 0 also drops the tuples that
 //              are never stored, from the kept-count rows of k_batch_stats)
 //   k_os_red / k_os_top / k_os_down
-//              column scan of hist over the tiles (blocks of 128 tiles),
+//              column scan of hist over the tiles (blocks of 16 tiles),
 //              digit bases from the digit totals -> the global output base
 //              of every (tile, digit)
 //   k_os_pass  persistent, one CTA per SM walking tiles c, c + 148, ...:
@@ -41,7 +41,7 @@ constexpr int kOsTile = 8192;
 constexpr int kOsThreads = 1024;
 constexpr int kOsItems = kOsTile / kOsThreads;          // 8 per thread
 constexpr int kOsWarps = kOsThreads / 32;
-constexpr int kOsBlkTiles = 128;                        // tiles per block of the column scan
+constexpr int kOsBlkTiles = 16;                         // tiles per block of the column scan (C4: 128 blocks)
 constexpr int kOsMaxPass = 4;
 
 template <int BITS>
@@ -156,16 +156,30 @@ k_os_top(OsArgs a) {
     const int64_t ntile = (os_count(a) + kOsTile - 1) / kOsTile;
     const int nblk = (int)((ntile + kOsBlkTiles - 1) / kOsBlkTiles);
     const int d = threadIdx.x;
+    // 16 block sums in flight per thread (a serial load -> store chain over
+    // 128 blocks cost ~40 us)
+    constexpr int U = 16;
     uint32_t run = 0;
-    for (int b = 0; b < nblk; ++b) {
-        uint32_t* p = a.bsum + (int64_t)b * BINS + d;
-        const uint32_t c = *p;
-        *p = run;
-        run += c;
+    for (int b0 = 0; b0 < nblk; b0 += U) {
+        uint32_t c[U];
+#pragma unroll
+        for (int q = 0; q < U; ++q) c[q] = (b0 + q < nblk) ? a.bsum[(int64_t)(b0 + q) * BINS + d] : 0u;
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+            if (b0 + q < nblk) a.bsum[(int64_t)(b0 + q) * BINS + d] = run;
+            run += c[q];
+        }
     }
     uint32_t tot;
     const uint32_t dbase = block_excl_scan(run, red, &tot);
-    for (int b = 0; b < nblk; ++b) a.bsum[(int64_t)b * BINS + d] += dbase;
+    for (int b0 = 0; b0 < nblk; b0 += U) {
+        uint32_t c[U];
+#pragma unroll
+        for (int q = 0; q < U; ++q) c[q] = (b0 + q < nblk) ? a.bsum[(int64_t)(b0 + q) * BINS + d] : 0u;
+#pragma unroll
+        for (int q = 0; q < U; ++q)
+            if (b0 + q < nblk) a.bsum[(int64_t)(b0 + q) * BINS + d] = c[q] + dbase;
+    }
 }
 
 // per tile and digit: global output base (in place over hist)
