@@ -112,6 +112,9 @@ struct ss_engine {
     int32_t *gcnt = nullptr, *gstart = nullptr, *gcount = nullptr, *bsum = nullptr;
     int32_t* gkept = nullptr;              // kept (possibly stored) tuples of each group in the batch
     int32_t* gpre = nullptr;               // [chunk][g] kept-count prefix over chunks (single-pass placement)
+    int32_t* gsub = nullptr;               // [unit][g] sub-chunk prefixes (few live chunks)
+    int32_t* subh = nullptr;               // [unit][g] sub-chunk counts
+    int* sub_shift = nullptr;              // device: sub-chunks per live chunk = 2^sub_shift
     uint32_t* pwork = nullptr;             // per-partition window-update work of the batch (k_batch_stats)
     int* any_dead = nullptr;               // some tuple of the batch is never stored (set by k_batch_stats)
     int4* cta_map = nullptr;               // work-proportional K4 grid: slot of every CTA
@@ -366,7 +369,7 @@ static void launch_balance(ss_engine* e, BalanceArgs& a, cudaStream_t st) {
 // single-pass placement kernel for keys < 2^bits (ballot matching)
 using RankKernel = void (*)(const uint32_t*, const int32_t*, uint32_t*, int32_t*, int64_t, int, const int32_t*,
                             const int32_t*, const int32_t*, const int32_t*, uint32_t, const int32_t*,
-                            const unsigned long long*);
+                            const unsigned long long*, const int*, const int32_t*);
 static RankKernel rank_kernel(int bits) {
     switch (bits) {
         case 0: case 1: case 2: case 3: case 4: case 5: case 6: case 7: case 8: return k_rank_place<8>;
@@ -801,13 +804,18 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
         (rc = dalloc(e, &e->bdelta, G)) || (rc = dalloc(e, &e->bmin, G)) || (rc = dalloc(e, &e->bmax, G)) ||
         (rc = dalloc(e, &e->hot_of, G)) || (rc = dalloc(e, &e->hot_g, kHotCache)) || (rc = dalloc(e, &e->n_hot_dev, 1)))
         return rc;
-    // single-pass placement when the cursors fit in shared memory and the
-    // kept set can span the batch (G x W >= batch); with a small kept set
-    // (few live chunks, e.g. C1) one CTA per chunk leaves the GPU idle and
-    // the radix passes over the live chunks are faster
-    e->rank_place = G <= kRankMaxG && G * W >= e->max_batch;
+    // single-pass placement whenever the cursors fit in shared memory; with
+    // a small kept set (few live chunks, e.g. C1) every live chunk is cut
+    // into sub-chunks so the placement still fills the GPU (one CTA per
+    // live chunk left it idle, and the radix passes over the live chunks
+    // were used instead: C1 placement 33 us)
+    e->rank_place = G <= kRankMaxG;
     if (const char* rp = getenv("SS_B200_RANK_PLACE")) e->rank_place = G <= kRankMaxG && rp[0] != '0';
-    if (e->rank_place && (rc = dalloc(e, &e->gpre, (size_t)nsub * G))) return rc;
+    if (e->rank_place &&
+        ((rc = dalloc(e, &e->gpre, (size_t)nsub * G)) || (rc = dalloc(e, &e->gsub, (size_t)kSubUnitsMax * G)) ||
+         (rc = dalloc(e, &e->subh, (size_t)kSubUnitsMax * G)) || (rc = dalloc(e, &e->sub_shift, 1))))
+        return rc;
+    if (e->rank_place) SS_CUDA(e, cudaMemsetAsync(e->sub_shift, 0, 4, e->st));
     // bucketed placement: every cold group (batch count < kBkTau) must keep
     // all its tuples, i.e. W >= kBkTau
     e->bucket = !e->rank_place && G > kRankMaxG && W >= kBkTau && e->max_batch <= kBkMaxBatch;
@@ -953,6 +961,7 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
     SS_CUDA(e, cudaFuncSetAttribute(k_count<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     SS_CUDA(e, cudaFuncSetAttribute(k_count_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     SS_CUDA(e, cudaFuncSetAttribute(k_key_count<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHotCache * 4));
+    SS_CUDA(e, cudaFuncSetAttribute(k_sub_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, kRankMaxG * 4));
     SS_CUDA(e, cudaFuncSetAttribute(k_sort_pass<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SortSmem<4>::bytes));
     SS_CUDA(e, cudaFuncSetAttribute(k_sort_pass<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SortSmem<5>::bytes));
     SS_CUDA(e, cudaFuncSetAttribute(k_sort_pass<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SortSmem<6>::bytes));
@@ -1153,7 +1162,7 @@ static int launch_scans(ss_engine* e, const int32_t* row, int n_chunk = 0) {
         ss_note_launch(), k_scan_small<<<1, 1024, 0, e->st>>>(row, (uint32_t)e->G, plan, e->dhist, e->gstart, e->bad,
                                                               e->n_live, n_chunk ? e->chunk_live : nullptr, n_chunk,
                                                               e->lc, e->n_lc, n_chunk && !rank ? e->btile : nullptr,
-                                                              e->ep_dev);
+                                                              e->ep_dev, rank ? e->sub_shift : nullptr);
         SS_CUDA(e, cudaGetLastError());
         return SS_OK;
     }
@@ -1282,9 +1291,14 @@ static int launch_place_step(ss_engine* e, const uint32_t* dk, const int32_t* dv
         // one CTA per live chunk, cursors from the chunk prefix (k_batch_stats)
         static const int use_match = getenv("SS_B200_RANK_MATCH") ? atoi(getenv("SS_B200_RANK_MATCH")) : 0;
         auto kern = use_match ? k_rank_place<0> : rank_kernel(bits_for(e->G));
-        ss_note_launch(), kern<<<n_chunk, kRankWarps * 32, rank_smem_bytes((uint32_t)e->G), e->st>>>(
+        // sub-chunk prefixes (no-ops unless k_scan_small chose sub-chunks)
+        ss_note_launch(), k_sub_hist<<<kSubUnitsMax, 512, e->G * 4, e->st>>>(dk, n, cs, e->lc, e->n_lc, e->sub_shift,
+                                                                            (uint32_t)e->G, e->subh, e->bad);
+        ss_note_launch(), k_sub_scan<<<2 * kNumSM, 256, 0, e->st>>>(e->gpre, e->lc, e->n_lc, e->sub_shift,
+                                                                   (uint32_t)e->G, e->subh, e->gsub, e->bad);
+        ss_note_launch(), kern<<<std::max(n_chunk, kSubUnitsMax), kRankWarps * 32, rank_smem_bytes((uint32_t)e->G), e->st>>>(
             dk, dv, e->trace_on ? e->kbuf2 : nullptr, e->vbuf[0], n, cs, e->lc, e->n_lc, e->gpre, e->gstart,
-            (uint32_t)e->G, e->n_live, e->bad);
+            (uint32_t)e->G, e->n_live, e->bad, e->sub_shift, e->gsub);
         SS_CUDA(e, cudaGetLastError());
         return SS_OK;
     }

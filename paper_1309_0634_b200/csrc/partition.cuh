@@ -513,7 +513,7 @@ __global__ void __launch_bounds__(1024)
 k_scan_small(const int32_t* __restrict__ row, uint32_t G, DigitPlan plan, uint32_t* __restrict__ dhist,
              int32_t* __restrict__ gstart, const unsigned long long* __restrict__ bad, int32_t* __restrict__ n_live,
              uint32_t* __restrict__ chunk_live, int n_chunk, int32_t* __restrict__ lc, int32_t* __restrict__ n_lc,
-             int32_t* __restrict__ btile, uint32_t* __restrict__ ep_dev) {
+             int32_t* __restrict__ btile, uint32_t* __restrict__ ep_dev, int* __restrict__ sub_shift_dev = nullptr) {
     __shared__ uint32_t sh_dh[2][kMaxBins];
     __shared__ int32_t sh_red[33];
     __shared__ uint32_t sh_ured[33];
@@ -600,7 +600,15 @@ k_scan_small(const int32_t* __restrict__ row, uint32_t G, DigitPlan plan, uint32
             if (f[q]) lc[e3++] = ch;
 
         }
-        if (threadIdx.x == 0) *n_lc = tot;
+        if (threadIdx.x == 0) {
+            *n_lc = tot;
+            if (sub_shift_dev) {
+                // sub-chunks until the live units fill two CTAs per SM
+                int ssh = 0;
+                while (tot > 0 && (tot << ssh) < 2 * kNumSM && ssh < 4) ++ssh;
+                *sub_shift_dev = ssh;
+            }
+        }
         __syncthreads();                         // every bit read before the words are cleared
         for (int i = threadIdx.x; i < (n_chunk + 31) / 32; i += blockDim.x) chunk_live[i] = 0;
     }
@@ -1054,6 +1062,56 @@ constexpr int kRankMaxG = 16384;
 // with 2 of 4, against 162 all-ballot and 168 all-MATCH)
 constexpr int kRankBallot = SS_RANK_BALLOT;
 
+// Sub-chunk prefixes for the single-pass placement when few chunks are
+// live: k_scan_small picks ss (live chunks x 2^ss >= 2 x 148, ss <= 4);
+// k_sub_hist counts every live sub-chunk's keys, k_sub_scan turns them into
+// gsub[u][g] = gpre[c][g] + g's count in the chunk's earlier sub-chunks
+// (-1 for a never-stored run).  Unit u = live chunk index << ss | sub-chunk.
+constexpr int kSubUnitsMax = 2 * 2 * kNumSM;        // (n_lc << ss) < 2 x 296
+
+__global__ void __launch_bounds__(512)
+k_sub_hist(const uint32_t* __restrict__ keys, int64_t n, int chunk_shift, const int32_t* __restrict__ lc,
+           const int32_t* __restrict__ n_lc, const int* __restrict__ sub_shift_dev, uint32_t G,
+           int32_t* __restrict__ subh, const unsigned long long* __restrict__ bad) {
+    extern __shared__ int32_t sh_hist[];
+    if (*bad != (unsigned long long)kNoBad) return;
+    const int ss = *sub_shift_dev;
+    if (ss == 0 || (int)blockIdx.x >= (*n_lc << ss)) return;
+    const int64_t c = lc[blockIdx.x >> ss];
+    const int sb = (int)blockIdx.x & ((1 << ss) - 1);
+    const int64_t c0 = (c << chunk_shift) + ((int64_t)sb << (chunk_shift - ss));
+    const int64_t c1 = min64(n, c0 + ((int64_t)1 << (chunk_shift - ss)));
+    for (int i = threadIdx.x; i < (int)G; i += blockDim.x) sh_hist[i] = 0;
+    __syncthreads();
+    for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
+        const uint32_t g = keys[i];
+        if (g < G) atomicAdd(&sh_hist[g], 1);
+    }
+    __syncthreads();
+    int32_t* dst = subh + (int64_t)blockIdx.x * G;
+    for (int i = threadIdx.x; i < (int)G; i += blockDim.x) dst[i] = sh_hist[i];
+}
+
+__global__ void __launch_bounds__(256)
+k_sub_scan(const int32_t* __restrict__ gpre, const int32_t* __restrict__ lc, const int32_t* __restrict__ n_lc,
+           const int* __restrict__ sub_shift_dev, uint32_t G, const int32_t* __restrict__ subh,
+           int32_t* __restrict__ gsub, const unsigned long long* __restrict__ bad) {
+    if (*bad != (unsigned long long)kNoBad) return;
+    const int ss = *sub_shift_dev;
+    if (ss == 0) return;
+    const int64_t total = (int64_t)*n_lc * G;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int li = (int)(i / G);
+        const uint32_t g = (uint32_t)(i - (int64_t)li * G);
+        int32_t run = gpre[(int64_t)lc[li] * G + g];
+        for (int sb = 0; sb < (1 << ss); ++sb) {
+            const int64_t u = ((int64_t)li << ss) | sb;
+            gsub[u * G + g] = run;
+            if (run >= 0) run += subh[u * G + g];
+        }
+    }
+}
+
 __host__ __device__ constexpr size_t rank_smem_bytes(uint32_t G) {
     return (size_t)kRankWarps * kRankStages * kRankSub * 8 + (size_t)G * 4;
 }
@@ -1064,16 +1122,23 @@ __global__ void __launch_bounds__(kRankWarps * 32)
 k_rank_place(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin, uint32_t* __restrict__ kout,
              int32_t* __restrict__ vout, int64_t n, int chunk_shift, const int32_t* __restrict__ lc,
              const int32_t* __restrict__ n_lc, const int32_t* __restrict__ gpre, const int32_t* __restrict__ gstart,
-             uint32_t G, const int32_t* __restrict__ n_live, const unsigned long long* __restrict__ bad) {
+             uint32_t G, const int32_t* __restrict__ n_live, const unsigned long long* __restrict__ bad,
+             const int* __restrict__ sub_shift_dev = nullptr, const int32_t* __restrict__ gsub = nullptr) {
     extern __shared__ __align__(16) unsigned char rank_sm[];
     uint32_t* stage_k = (uint32_t*)rank_sm;                            // [warp][stage][kRankSub]
     int32_t* stage_v = (int32_t*)(stage_k + kRankWarps * kRankStages * kRankSub);
     uint32_t* cur = (uint32_t*)(stage_v + kRankWarps * kRankStages * kRankSub);   // [G]
     if (*bad != (unsigned long long)kNoBad) return;
     if (*n_live == 0) return;
-    if ((int)blockIdx.x >= *n_lc) return;
-    const int64_t c = lc[blockIdx.x];
-    const int32_t* pre = gpre + c * (int64_t)G;
+    // few live chunks (a small kept set, e.g. C1): each is cut into 2^ss
+    // sub-chunks placed by CTAs of their own, from sub-chunk prefixes (gsub)
+    const int ss = sub_shift_dev ? *sub_shift_dev : 0;
+    if ((int)blockIdx.x >= (*n_lc << ss)) return;
+    const int64_t c = lc[blockIdx.x >> ss];
+    const int sb = (int)blockIdx.x & ((1 << ss) - 1);
+    const int32_t* pre = ss ? gsub + (int64_t)blockIdx.x * G : gpre + c * (int64_t)G;
+    const int64_t c0 = (c << chunk_shift) + ((int64_t)sb << (chunk_shift - ss));
+    if (c0 >= n) return;
     for (uint32_t g0 = threadIdx.x; g0 < G; g0 += 4 * blockDim.x) {
         int32_t p[4], b[4];
 #pragma unroll
@@ -1088,8 +1153,7 @@ k_rank_place(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin, 
             if (g < G) cur[g] = p[u] < 0 ? 0x80000000u : (uint32_t)(b[u] + p[u]);
         }
     }
-    const int64_t c0 = c << chunk_shift;
-    const int cn = (int)min64((int64_t)1 << chunk_shift, n - c0);
+    const int cn = (int)min64((int64_t)1 << (chunk_shift - ss), n - c0);
     const int nsub = (cn + kRankSub - 1) / kRankSub;
     const int w = (int)warp_id();
     const unsigned lane = lane_id();

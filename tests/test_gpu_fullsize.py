@@ -48,6 +48,7 @@ def _expected(groups, attrs, G, W):
 
 
 @pytest.mark.parametrize("name,G,W,s,split,nb", [
+    ("C1", 1_000, 1_000, 0.0, False, 3),        # few live chunks: sub-chunk placement
     ("C2", 10_000, 100_000, 1.0, False, 2),
     ("C3", 100_000, 1_000_000, 1.5, True, 2),
 ])
@@ -61,7 +62,7 @@ def test_full_shape_windows(name, G, W, s, split, nb):
     bal = StreamEngine.balancer_struct("prob", B // 1480, 0.5, split=split)
     gs, avs = [], []
     for i in range(nb):
-        g = _zipf(B, G, s, rng)
+        g = _zipf(B, G, s, rng) if s > 0 else rng.integers(0, G, B)
         a = rng.integers(-2 ** 31, 2 ** 31, B, dtype=np.int64)
         rep = eng.step(torch.from_numpy(g.astype(np.int32)).cuda(), torch.from_numpy(a.astype(np.int32)).cuda(), bal)
         assert rep.tuples == B
