@@ -136,7 +136,7 @@ __device__ void bal_move(const BalanceArgs& a, const BalSmem& s, int* nm, int g,
 
 // entry counts and flags by position for the CTA-wide donor scans
 __global__ void __launch_bounds__(256)
-k_bal_prep(BalanceArgs a) {
+k_bal_prep(BalanceArgs a) { SS_PDL_ENTRY();
     if (*a.bad != (unsigned long long)kNoBad) return;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.G; i += gridDim.x * blockDim.x) {
         const int g = a.order[i];
@@ -166,7 +166,7 @@ __device__ __forceinline__ void cta_argmin(long long& key, int& id, int& x, long
 
 template <bool STAGED, bool WIDE = false>
 __global__ void __launch_bounds__(kBalThreads)
-k_balance(BalanceArgs a) {
+k_balance(BalanceArgs a) { SS_PDL_ENTRY();
     extern __shared__ long long bal_sm[];
     __shared__ int red_i[72];
     const int P = a.P;
@@ -534,7 +534,7 @@ k_balance(BalanceArgs a) {
 __global__ void __launch_bounds__(256)
 k_apply_place(const int32_t* __restrict__ order, const int32_t* __restrict__ offsets,
               const int32_t* __restrict__ keep_at, const int4* __restrict__ moves, const int* __restrict__ n_moves,
-              const int32_t* __restrict__ mv_pos, const uint8_t* __restrict__ moved, int32_t* __restrict__ new_order) {
+              const int32_t* __restrict__ mv_pos, const uint8_t* __restrict__ moved, int32_t* __restrict__ new_order) { SS_PDL_ENTRY();
     __shared__ int32_t red[33];
     const int nm = *n_moves;
     if (nm == 0) return;
@@ -563,7 +563,7 @@ k_apply_place(const int32_t* __restrict__ order, const int32_t* __restrict__ off
 __global__ void __launch_bounds__(256)
 k_apply_commit(int32_t* __restrict__ order, int32_t* __restrict__ offsets, const int32_t* __restrict__ new_order,
                const int32_t* __restrict__ new_off, int G, int P, const int4* __restrict__ moves,
-               const int* __restrict__ n_moves, int32_t* __restrict__ pmap, uint8_t* __restrict__ moved) {
+               const int* __restrict__ n_moves, int32_t* __restrict__ pmap, uint8_t* __restrict__ moved) { SS_PDL_ENTRY();
     const int nm = *n_moves;
     if (nm == 0) return;
     const int tid = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;

@@ -123,7 +123,7 @@ __device__ __forceinline__ int bk_flag(const BucketArgs& a, uint32_t g) {
 }
 
 __global__ void __launch_bounds__(1024)
-k_bk_flags_reduce(BucketArgs a) {
+k_bk_flags_reduce(BucketArgs a) { SS_PDL_ENTRY();
     __shared__ int32_t red[33];
     if (*a.bad != (unsigned long long)kNoBad) return;
     const uint32_t g0 = blockIdx.x * kBkBlk;
@@ -135,7 +135,7 @@ k_bk_flags_reduce(BucketArgs a) {
 }
 
 __global__ void __launch_bounds__(1024)
-k_bk_flags_top(BucketArgs a, int nblk) {
+k_bk_flags_top(BucketArgs a, int nblk) { SS_PDL_ENTRY();
     __shared__ int32_t red[33];
     if (*a.bad != (unsigned long long)kNoBad) return;
     int32_t carry = 0;
@@ -157,7 +157,7 @@ k_bk_flags_top(BucketArgs a, int nblk) {
 
 // bin ids: groups in block order, 4 consecutive groups per thread
 __global__ void __launch_bounds__(1024)
-k_bk_flags_down(BucketArgs a) {
+k_bk_flags_down(BucketArgs a) { SS_PDL_ENTRY();
     __shared__ int32_t red[33];
     if (*a.bad != (unsigned long long)kNoBad) return;
     const uint32_t g0 = blockIdx.x * kBkBlk + threadIdx.x * 4;
@@ -196,7 +196,7 @@ __device__ __forceinline__ int bk_range(int64_t n, int c, int64_t* t0) {
 
 // per-bin counts of one super-tile; the tuples' bin ids are written out
 __global__ void __launch_bounds__(1024)
-k_bk_hist(BucketArgs a) {
+k_bk_hist(BucketArgs a) { SS_PDL_ENTRY();
     extern __shared__ uint32_t bk_sm[];
     if (*a.bad != (unsigned long long)kNoBad) return;
     const int nb = *a.n_bins;
@@ -245,7 +245,7 @@ k_bk_hist(BucketArgs a) {
 // per bin (lane), the super-tiles split over the warps: exclusive prefix
 // over the super-tiles in place, the bin total
 __global__ void __launch_bounds__(1024)
-k_bk_colscan(BucketArgs a) {
+k_bk_colscan(BucketArgs a) { SS_PDL_ENTRY();
     __shared__ uint32_t part[32][33];
     if (*a.bad != (unsigned long long)kNoBad) return;
     const int nb = *a.n_bins;
@@ -274,7 +274,7 @@ k_bk_colscan(BucketArgs a) {
 
 // staging base of each cold bucket (hot bins take no staging space)
 __global__ void __launch_bounds__(1024)
-k_bk_binscan(BucketArgs a) {
+k_bk_binscan(BucketArgs a) { SS_PDL_ENTRY();
     __shared__ uint32_t red[33];
     if (*a.bad != (unsigned long long)kNoBad) return;
     const int nb = *a.n_bins;
@@ -386,7 +386,7 @@ struct BkSmem {
 
 // pass 1
 __global__ void __launch_bounds__(kBkThreads, 1)
-k_bk_scatter(BucketArgs a) {
+k_bk_scatter(BucketArgs a) { SS_PDL_ENTRY();
     extern __shared__ __align__(16) unsigned char bsm[];
     uint32_t* cursor = (uint32_t*)(bsm + BkSmem::cursor);
     uint16_t* runst = (uint16_t*)(bsm + BkSmem::runst);
@@ -508,7 +508,7 @@ struct BkLocSmem {
 };
 
 __global__ void __launch_bounds__(kBkLocThreads, 2)
-k_bk_local(BucketArgs a) {
+k_bk_local(BucketArgs a) { SS_PDL_ENTRY();
     extern __shared__ __align__(16) unsigned char lsm[];
     uint32_t* ka = (uint32_t*)(lsm + BkLocSmem::ka);
     uint32_t* kb = (uint32_t*)(lsm + BkLocSmem::kb);

@@ -12,6 +12,15 @@
 #define SS_WARP 32
 #define SS_FULL 0xffffffffu
 
+// Programmatic dependent launch: every kernel of the library is launched
+// with programmatic stream serialisation (engine.cu ss_launch), so its CTAs
+// may be scheduled while the previous kernel of the stream drains; the
+// first thing each kernel does is wait for that predecessor to complete
+// (griddepcontrol.wait -- a no-op without a programmatic predecessor) and
+// let its own successor be scheduled (launch_dependents).  The successor
+// still waits for this grid's completion and memory flush before it runs.
+#define SS_PDL_ENTRY() asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory")
+
 namespace ss {
 
 constexpr int kNumSM = 148;                 // B200: 2 dies x 74 SMs

@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <utility>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -46,6 +47,26 @@ using namespace ss;
 // so the benchmark can report how many of our kernels ran (ss_launch_count)
 static std::atomic<long long> g_launches{0};
 static inline void ss_note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+// every launch: programmatic stream serialisation (SS_PDL_ENTRY in each
+// kernel), so a kernel's launch and CTA rasterisation overlap the tail of
+// its predecessor; SS_B200_NO_PDL=1 launches plainly (A/B)
+static const bool g_pdl = !(getenv("SS_B200_NO_PDL") && getenv("SS_B200_NO_PDL")[0] == '1');
+template <typename... KArgs, typename... Args>
+static inline void ss_launch(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+    static_assert(sizeof...(KArgs) == sizeof...(Args), "every kernel argument is passed explicitly");
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = g_pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
 
 namespace {
 
@@ -129,6 +150,7 @@ struct ss_engine {
     int os_npass = 0, os_shift[kOsMaxPass] = {0, 0, 0, 0}, os_bits[kOsMaxPass] = {0, 0, 0, 0};
     uint32_t* os_hist = nullptr;
     uint32_t* os_bsum = nullptr;
+    uint32_t* os_dtot = nullptr;
     // where the placement left the kept values (and, in trace mode, keys)
     int32_t* vals_final = nullptr;
     uint32_t* keys_final = nullptr;
@@ -354,15 +376,15 @@ static void launch_balance(ss_engine* e, BalanceArgs& a, cudaStream_t st) {
     a.G = (int)e->G;
     const bool staged = e->G <= kBalStageG && bal_smem_bytes(e->P, (int)e->G, true) <= kBalSmemMax;
     if (staged) {
-        k_balance<true><<<1, kBalThreads, bal_smem_bytes(e->P, (int)e->G, true), st>>>(a);
+        ss_launch(k_balance<true>, 1, kBalThreads, bal_smem_bytes(e->P, (int)e->G, true), st, a);
     } else if (a.policy == SS_POLICY_ALL || a.policy == SS_POLICY_PROB || a.policy == SS_POLICY_BEST) {
         // donor scans over the whole CTA, from position-ordered counts / flags
         a.ecnt = e->bal_ecnt;
         a.eflag = e->bal_eflag;
-        ss_note_launch(), k_bal_prep<<<2 * kNumSM, 256, 0, st>>>(a);
-        k_balance<false, true><<<1, kBalThreads, bal_smem_bytes(e->P, (int)e->G, false), st>>>(a);
+        ss_note_launch(), ss_launch(k_bal_prep, 2 * kNumSM, 256, 0, st, a);
+        ss_launch(k_balance<false, true>, 1, kBalThreads, bal_smem_bytes(e->P, (int)e->G, false), st, a);
     } else {
-        k_balance<false><<<1, kBalThreads, bal_smem_bytes(e->P, (int)e->G, false), st>>>(a);
+        ss_launch(k_balance<false>, 1, kBalThreads, bal_smem_bytes(e->P, (int)e->G, false), st, a);
     }
 }
 
@@ -399,8 +421,7 @@ void launch_sort(cudaStream_t st, const uint32_t* kin, const int32_t* vin, uint3
     const int tiles = (n + kSortTile - 1) / kSortTile + (sg && sg->mode == 2 ? sg->nb : 0);
     if (tiles == 0) return;
     // persistent: at most the co-resident CTAs (2 per SM), each looping over tickets
-    ss_note_launch(), k_sort_pass<RB><<<std::min(tiles, 2 * kNumSM), kSortThreads, SortSmem<RB>::bytes, st>>>(
-        kin, vin, kout, vout, n, shift, mask, base, status, ep_dev, ep_off, ticket, bad, stream_in, nullptr, n_dev,
+    ss_note_launch(), ss_launch(k_sort_pass<RB>, std::min(tiles, 2 * kNumSM), kSortThreads, SortSmem<RB>::bytes, st, kin, vin, kout, vout, n, shift, mask, base, status, ep_dev, ep_off, ticket, bad, stream_in, nullptr, n_dev,
         sg ? *sg : SortSeg{});
 }
 
@@ -424,20 +445,20 @@ void sort_dispatch(int rb, cudaStream_t st, const uint32_t* kin, const int32_t* 
 #undef SS_SORT_CASE
 }
 
-__global__ void k_fill_i32(int32_t* p, int64_t n, int32_t v) {
+__global__ void k_fill_i32(int32_t* p, int64_t n, int32_t v) { SS_PDL_ENTRY();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
 }
-__global__ void k_dense_off(int64_t* off, int32_t* cap, int64_t G, int64_t W) {
+__global__ void k_dense_off(int64_t* off, int32_t* cap, int64_t G, int64_t W) { SS_PDL_ENTRY();
     for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < G; g += (int64_t)gridDim.x * blockDim.x) {
         off[g] = g * W;
         cap[g] = (int32_t)W;
     }
 }
-__global__ void k_set_bad(unsigned long long* bad) { *bad = (unsigned long long)kNoBad; }
-__global__ void k_epoch_bump(uint32_t* ep) { *ep = epoch_next(*ep); }
+__global__ void k_set_bad(unsigned long long* bad) { SS_PDL_ENTRY(); *bad = (unsigned long long)kNoBad; }
+__global__ void k_epoch_bump(uint32_t* ep) { SS_PDL_ENTRY(); *ep = epoch_next(*ep); }
 // replay records (u32 group, i32 attr; datagen.py REPLAY_DTYPE) -> SoA keys / values
 __global__ void k_deinterleave(const uint4* __restrict__ rec, int64_t n, uint32_t* __restrict__ keys,
-                               int32_t* __restrict__ vals) {
+                               int32_t* __restrict__ vals) { SS_PDL_ENTRY();
     const int64_t n2 = n / 2;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2; i += (int64_t)gridDim.x * blockDim.x) {
         const uint4 r = ld_stream_v4(rec + i);
@@ -458,7 +479,7 @@ __global__ void k_emit_host(const unsigned* __restrict__ n_res, const unsigned l
                             const uint32_t* __restrict__ keys, long long n_keys, const int32_t* __restrict__ g,
                             const int32_t* __restrict__ cnt, const long long* __restrict__ sum,
                             const double* __restrict__ avg, const int32_t* __restrict__ mn,
-                            const int32_t* __restrict__ mx, HostRows h) {
+                            const int32_t* __restrict__ mx, HostRows h) { SS_PDL_ENTRY();
     const unsigned long long b = *bad;
     const unsigned n = (b == (unsigned long long)kNoBad) ? *n_res : 0u;
     for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -475,16 +496,16 @@ __global__ void k_emit_host(const unsigned* __restrict__ n_res, const unsigned l
         h.hdr[2] = (b < (unsigned long long)n_keys) ? (unsigned long long)keys[b] : 0ull;
     }
 }
-__global__ void k_fill_u64(unsigned long long* p, int64_t n, unsigned long long v) {
+__global__ void k_fill_u64(unsigned long long* p, int64_t n, unsigned long long v) { SS_PDL_ENTRY();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
 }
-__global__ void k_u64_to_i64(const unsigned long long* a, long long* b, int n) {
+__global__ void k_u64_to_i64(const unsigned long long* a, long long* b, int n) { SS_PDL_ENTRY();
     for (int i = threadIdx.x; i < n; i += blockDim.x) b[i] = (long long)a[i];
 }
 
 // map group ids to placement ranks (reorder_batch sorts by rank)
 __global__ void k_to_rank(const uint32_t* __restrict__ g, int64_t n, const int32_t* __restrict__ rank,
-                          uint32_t G, uint32_t* __restrict__ out, unsigned long long* bad) {
+                          uint32_t G, uint32_t* __restrict__ out, unsigned long long* bad) { SS_PDL_ENTRY();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t v = g[i];
         if (v >= G) {
@@ -495,15 +516,15 @@ __global__ void k_to_rank(const uint32_t* __restrict__ g, int64_t n, const int32
         }
     }
 }
-__global__ void k_rank_of(const int32_t* __restrict__ order, int64_t G, int32_t* __restrict__ rank) {
+__global__ void k_rank_of(const int32_t* __restrict__ order, int64_t G, int32_t* __restrict__ rank) { SS_PDL_ENTRY();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < G; i += (int64_t)gridDim.x * blockDim.x)
         rank[order[i]] = (int32_t)i;
 }
-__global__ void k_from_rank(uint32_t* __restrict__ k, int64_t n, const int32_t* __restrict__ order) {
+__global__ void k_from_rank(uint32_t* __restrict__ k, int64_t n, const int32_t* __restrict__ order) { SS_PDL_ENTRY();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         k[i] = (uint32_t)order[k[i]];
 }
-__global__ void k_clear_moved(const int4* __restrict__ moves, const int* __restrict__ n_moves, uint8_t* moved) {
+__global__ void k_clear_moved(const int4* __restrict__ moves, const int* __restrict__ n_moves, uint8_t* moved) { SS_PDL_ENTRY();
     const int n = *n_moves;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) moved[moves[i].x] = 0;
 }
@@ -515,7 +536,7 @@ k_report(const unsigned long long* __restrict__ tpt, const unsigned long long* _
          const unsigned long long* __restrict__ bad, const unsigned long long* __restrict__ touched,
          const int* __restrict__ n_moves, int* __restrict__ prev_moves, const long long* __restrict__ scanned,
          const int* __restrict__ n_split, const unsigned* __restrict__ n_res, const int* __restrict__ oom,
-         long long tuples, int has_policy, DevReport* __restrict__ rep) {
+         long long tuples, int has_policy, DevReport* __restrict__ rep) { SS_PDL_ENTRY();
     __shared__ long long r[3][32];
     long long mx = 0, mnv = LLONG_MAX, ml = 0;
     for (int p = threadIdx.x; p < P; p += blockDim.x) {
@@ -715,7 +736,7 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
     if (e->dense) {
         e->pool_cap = (unsigned long long)dense_vals;
         if ((rc = dalloc(e, &e->ring, dense_vals))) return rc;
-        ss_note_launch(), k_dense_off<<<296, 256, 0, e->st>>>(e->off, e->cap, G, W);
+        ss_note_launch(), ss_launch(k_dense_off, 296, 256, 0, e->st, e->off, e->cap, G, W);
     } else {
         int64_t pool = e->stream_scope ? 16 : cfg->pool_values;
         if (pool <= 0) {
@@ -845,7 +866,8 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
         const int64_t tiles = (e->max_batch + kOsTile - 1) / kOsTile;
         const int bins = 1 << e->os_digit;
         if (e->os && ((rc = dalloc(e, &e->os_hist, (size_t)tiles * bins)) ||
-                      (rc = dalloc(e, &e->os_bsum, (size_t)((tiles + kOsBlkTiles - 1) / kOsBlkTiles) * bins))))
+                      (rc = dalloc(e, &e->os_bsum, (size_t)((tiles + kOsBlkTiles - 1) / kOsBlkTiles) * bins)) ||
+                      (rc = dalloc(e, &e->os_dtot, (size_t)bins))))
             return rc;
     }
     if (e->bucket) {
@@ -864,13 +886,13 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
     SS_CUDA(e, cudaMemsetAsync(e->hot_of, 0xff, G * 4, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->n_hot_dev, 0, 4, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->bdelta, 0, G * 8, e->st));
-    ss_note_launch(), k_fill_i32<<<296, 256, 0, e->st>>>(e->bmin, G, 0x7fffffff);
-    ss_note_launch(), k_fill_i32<<<296, 256, 0, e->st>>>(e->bmax, G, (int32_t)0x80000000);
+    ss_note_launch(), ss_launch(k_fill_i32, 296, 256, 0, e->st, e->bmin, G, 0x7fffffff);
+    ss_note_launch(), ss_launch(k_fill_i32, 296, 256, 0, e->st, e->bmax, G, (int32_t)0x80000000);
     SS_CUDA(e, cudaMemsetAsync(e->gcnt, 0, (size_t)nsub * G * 4, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->gcount, 0, G * 4, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->chunk_live, 0, (size_t)nsub * 4, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->ep_dev, 0, 4, e->st));
-    ss_note_launch(), k_set_bad<<<1, 1, 0, e->st>>>(e->bad);
+    ss_note_launch(), ss_launch(k_set_bad, 1, 1, 0, e->st, e->bad);
     if ((rc = engine_alloc_sort(e, e->max_batch))) return rc;
     e->vals_final = e->vbuf[0];
     e->keys_final = e->kbuf2;
@@ -888,13 +910,11 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
             (rc = dalloc(e, &t.mark, e->max_batch)) || (rc = dalloc(e, &t.slot_keys, G)) ||
             (rc = dalloc(e, &t.min_key_entry, 1)) || (rc = dalloc(e, &t.overflow, 1)) ||
             (rc = dalloc(e, &e->stage_keys64, e->max_batch)) ||
-            (rc = dalloc(e, &e->kbsum, e->max_batch / kMarkBlk + 2)) || (rc = dalloc(e, &t.hk_key, kHotTab)) ||
-            (rc = dalloc(e, &t.hk_idx, kHotTab)))
+            (rc = dalloc(e, &e->kbsum, e->max_batch / kMarkBlk + 2)))
             return rc;
         t.cap_mask = cap - 1;
         t.G = (int)G;
-        ss_note_launch(), k_hot_keytab_clear<<<4, 1024, 0, e->st>>>(t);
-        ss_note_launch(), k_key_init<<<296, 256, 0, e->st>>>(t.ent, (int64_t)cap + 1);
+        ss_note_launch(), ss_launch(k_key_init, 296, 256, 0, e->st, t.ent, (int64_t)cap + 1);
         SS_CUDA(e, cudaMemsetAsync(t.first, 0xff, (cap + 1) * 4, e->st));
         SS_CUDA(e, cudaMemsetAsync(t.mark, 0xff, e->max_batch * 4, e->st));
         SS_CUDA(e, cudaMemsetAsync(t.n_new, 0, 4, e->st));
@@ -960,7 +980,6 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
     e->h_rep->bad = (unsigned long long)kNoBad;
     SS_CUDA(e, cudaFuncSetAttribute(k_count<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     SS_CUDA(e, cudaFuncSetAttribute(k_count_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-    SS_CUDA(e, cudaFuncSetAttribute(k_key_count<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHotCache * 4));
     SS_CUDA(e, cudaFuncSetAttribute(k_sub_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, kRankMaxG * 4));
     SS_CUDA(e, cudaFuncSetAttribute(k_sort_pass<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SortSmem<4>::bytes));
     SS_CUDA(e, cudaFuncSetAttribute(k_sort_pass<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SortSmem<5>::bytes));
@@ -1089,7 +1108,7 @@ static int recover_bad(ss_engine* e) {
     SS_CUDA(e, cudaMemsetAsync(e->gcnt, 0, (size_t)e->n_sub_max * e->G * 4, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->gcount, 0, e->G * 4, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->chunk_live, 0, (size_t)e->n_sub_max * 4, e->st));
-    ss_note_launch(), k_set_bad<<<1, 1, 0, e->st>>>(e->bad);
+    ss_note_launch(), ss_launch(k_set_bad, 1, 1, 0, e->st, e->bad);
     SS_CUDA(e, cudaStreamSynchronize(e->st));
     return SS_OK;
 }
@@ -1110,14 +1129,14 @@ static int launch_count(ss_engine* e, const uint32_t* dk, int64_t n, int64_t S, 
         // larger chunks amortise the per-CTA flush of the G-bin histogram
         const int64_t chunk = (e->G > 2048 && S % 65536 == 0) ? 65536 : kCountChunk;
         const int64_t grid = (n + chunk - 1) / chunk;
-        ss_note_launch(), k_count<true><<<(unsigned)grid, 512, e->G * 4, e->st>>>(dk, n, (uint32_t)e->G, S, chunk, e->gcnt, e->bad,
+        ss_note_launch(), ss_launch(k_count<true>, (unsigned)grid, 512, e->G * 4, e->st, dk, n, (uint32_t)e->G, S, chunk, e->gcnt, e->bad,
                                                                vec_ok, nullptr, nullptr, 0);
     } else {
         // the hot cache holds the previous batch's hot groups; its size is
         // fixed at kHotCache slots (unused slots count nothing)
         const int64_t grid = (n + kCountChunk - 1) / kCountChunk;
         const int nh = use_hot ? kHotCache : 0;
-        ss_note_launch(), k_count<false><<<(unsigned)grid, 512, (size_t)nh * 4, e->st>>>(dk, n, (uint32_t)e->G, S, kCountChunk, e->gcnt,
+        ss_note_launch(), ss_launch(k_count<false>, (unsigned)grid, 512, (size_t)nh * 4, e->st, dk, n, (uint32_t)e->G, S, kCountChunk, e->gcnt,
                                                                       e->bad, vec_ok, e->hot_of, e->hot_g, nh);
     }
     SS_CUDA(e, cudaGetLastError());
@@ -1136,14 +1155,12 @@ static int launch_stats(ss_engine* e, int n_chunk, bool step = false, bool want_
         const unsigned grid = (unsigned)std::min<int64_t>((e->G + 31) / 32, 8 * kNumSM);
         const bool small = e->G <= 4096;
         auto kern = small ? k_batch_stats_cols<32> : k_batch_stats_cols<16>;
-        ss_note_launch(), kern<<<grid, small ? 1024 : 512, e->P * 8, e->st>>>(
-            e->gcnt, n_chunk, (uint32_t)e->G, e->pmap, e->P, e->gcount, step ? e->gkept : nullptr,
+        ss_note_launch(), ss_launch(kern, grid, small ? 1024 : 512, e->P * 8, e->st, e->gcnt, n_chunk, (uint32_t)e->G, e->pmap, e->P, e->gcount, step ? e->gkept : nullptr,
             step ? e->chunk_live : nullptr, e->tpt, e->touched, e->bad, e->fill, e->W, e->alg_bytes, e->trace_on ? 1 : 0,
             step && e->rank_place ? e->gpre : nullptr, want_work ? e->pwork : nullptr, step ? e->any_dead : nullptr);
     } else {
         const unsigned grid = (unsigned)std::min<int64_t>((e->G + 255) / 256, 16 * kNumSM);
-        ss_note_launch(), k_batch_stats<<<grid, 256, e->P * 8, e->st>>>(
-            e->gcnt, n_chunk, (uint32_t)e->G, e->pmap, e->P, e->gcount, step ? e->gkept : nullptr,
+        ss_note_launch(), ss_launch(k_batch_stats, grid, 256, e->P * 8, e->st, e->gcnt, n_chunk, (uint32_t)e->G, e->pmap, e->P, e->gcount, step ? e->gkept : nullptr,
             step ? e->chunk_live : nullptr, e->tpt, e->touched, e->bad, e->fill, e->W, e->alg_bytes, e->trace_on ? 1 : 0,
             step && e->rank_place ? e->gpre : nullptr, want_work ? e->pwork : nullptr, step ? e->any_dead : nullptr);
     }
@@ -1159,7 +1176,7 @@ static int launch_scans(ss_engine* e, const int32_t* row, int n_chunk = 0) {
         DigitPlan plan = e->plan;
         const bool rank = n_chunk && e->rank_place;
         if (rank) plan.npass = 0;
-        ss_note_launch(), k_scan_small<<<1, 1024, 0, e->st>>>(row, (uint32_t)e->G, plan, e->dhist, e->gstart, e->bad,
+        ss_note_launch(), ss_launch(k_scan_small, 1, 1024, 0, e->st, row, (uint32_t)e->G, plan, e->dhist, e->gstart, e->bad,
                                                               e->n_live, n_chunk ? e->chunk_live : nullptr, n_chunk,
                                                               e->lc, e->n_lc, n_chunk && !rank ? e->btile : nullptr,
                                                               e->ep_dev, rank ? e->sub_shift : nullptr);
@@ -1168,11 +1185,11 @@ static int launch_scans(ss_engine* e, const int32_t* row, int n_chunk = 0) {
     }
     SS_CUDA(e, cudaMemsetAsync(e->dhist, 0, (size_t)2 * kMaxBins * 4, e->st));
     dim3 g2(e->nblk, 1);
-    ss_note_launch(), k_scan_reduce<<<g2, 1024, 0, e->st>>>(row, (uint32_t)e->G, e->bsum, e->nblk, e->plan, e->dhist, e->bad);
-    ss_note_launch(), k_scan_top<<<1, 1024, 0, e->st>>>(e->bsum, e->nblk, e->plan, e->dhist, e->bad, e->n_live,
+    ss_note_launch(), ss_launch(k_scan_reduce, g2, 1024, 0, e->st, row, (uint32_t)e->G, e->bsum, e->nblk, e->plan, e->dhist, e->bad);
+    ss_note_launch(), ss_launch(k_scan_top, 1, 1024, 0, e->st, e->bsum, e->nblk, e->plan, e->dhist, e->bad, e->n_live,
                                                         n_chunk ? e->chunk_live : nullptr, n_chunk, e->lc, e->n_lc,
                                                         n_chunk ? e->btile : nullptr, e->ep_dev);
-    ss_note_launch(), k_scan_down<<<g2, 1024, 0, e->st>>>(row, (uint32_t)e->G, e->bsum, e->nblk, e->gstart, e->bad);
+    ss_note_launch(), ss_launch(k_scan_down, g2, 1024, 0, e->st, row, (uint32_t)e->G, e->bsum, e->nblk, e->gstart, e->bad);
     SS_CUDA(e, cudaGetLastError());
     return SS_OK;
 }
@@ -1200,11 +1217,11 @@ static int launch_place_all(ss_engine* e, const uint32_t* dk, const int32_t* dv,
 
 template <int BITS>
 static void launch_os_pass_t(ss_engine* e, const OsArgs& a, unsigned tiles, unsigned blks) {
-    ss_note_launch(), k_os_up<BITS><<<tiles, kOsThreads, 0, e->st>>>(a);
-    ss_note_launch(), k_os_red<BITS><<<blks, 1024, 0, e->st>>>(a);
-    ss_note_launch(), k_os_top<BITS><<<1, 1 << BITS, 0, e->st>>>(a);
-    ss_note_launch(), k_os_down<BITS><<<blks, 1024, 0, e->st>>>(a);
-    ss_note_launch(), k_os_pass<BITS><<<std::min<unsigned>(tiles, kNumSM), kOsThreads, OsSmem<BITS>::bytes, e->st>>>(a);
+    ss_note_launch(), ss_launch(k_os_up<BITS>, tiles, kOsThreads, 0, e->st, a);
+    ss_note_launch(), ss_launch(k_os_red<BITS>, blks, 1024, 0, e->st, a);
+    ss_note_launch(), ss_launch(k_os_top<BITS>, (1 << BITS) / 32, 1024, 0, e->st, a);
+    ss_note_launch(), ss_launch(k_os_down<BITS>, blks, 1024, 0, e->st, a);
+    ss_note_launch(), ss_launch(k_os_pass<BITS>, std::min<unsigned>(tiles, kNumSM), kOsThreads, OsSmem<BITS>::bytes, e->st, a);
 }
 static void launch_os_pass(ss_engine* e, const OsArgs& a, unsigned tiles, unsigned blks) {
     if (e->os_digit == kOsBitsWide) launch_os_pass_t<kOsBitsWide>(e, a, tiles, blks);
@@ -1245,6 +1262,7 @@ static int launch_place_step(ss_engine* e, const uint32_t* dk, const int32_t* dv
             a.mask = (1u << e->os_bits[p]) - 1u;
             a.hist = e->os_hist;
             a.bsum = e->os_bsum;
+            a.dtot = e->os_dtot;
             a.live = p == 0 ? e->gcnt : nullptr;
             a.chunk_shift = cs;
             a.G = (uint32_t)e->G;
@@ -1276,14 +1294,14 @@ static int launch_place_step(ss_engine* e, const uint32_t* dk, const int32_t* dv
         a.vout = e->vbuf[0];
         a.bad = e->bad;
         const int nblk = (int)((e->G + kBkBlk - 1) / kBkBlk);
-        ss_note_launch(), k_bk_flags_reduce<<<nblk, 1024, 0, e->st>>>(a);
-        ss_note_launch(), k_bk_flags_top<<<1, 1024, 0, e->st>>>(a, nblk);
-        ss_note_launch(), k_bk_flags_down<<<nblk, 1024, 0, e->st>>>(a);
-        ss_note_launch(), k_bk_hist<<<kBkSupers, 1024, kBkNBMax * 4, e->st>>>(a);
-        ss_note_launch(), k_bk_colscan<<<kBkNBMax / 32, 1024, 0, e->st>>>(a);
-        ss_note_launch(), k_bk_binscan<<<1, 1024, 0, e->st>>>(a);
-        ss_note_launch(), k_bk_scatter<<<kBkSupers, kBkThreads, BkSmem::bytes, e->st>>>(a);
-        ss_note_launch(), k_bk_local<<<2 * kNumSM, kBkLocThreads, BkLocSmem::bytes, e->st>>>(a);
+        ss_note_launch(), ss_launch(k_bk_flags_reduce, nblk, 1024, 0, e->st, a);
+        ss_note_launch(), ss_launch(k_bk_flags_top, 1, 1024, 0, e->st, a, nblk);
+        ss_note_launch(), ss_launch(k_bk_flags_down, nblk, 1024, 0, e->st, a);
+        ss_note_launch(), ss_launch(k_bk_hist, kBkSupers, 1024, kBkNBMax * 4, e->st, a);
+        ss_note_launch(), ss_launch(k_bk_colscan, kBkNBMax / 32, 1024, 0, e->st, a);
+        ss_note_launch(), ss_launch(k_bk_binscan, 1, 1024, 0, e->st, a);
+        ss_note_launch(), ss_launch(k_bk_scatter, kBkSupers, kBkThreads, BkSmem::bytes, e->st, a);
+        ss_note_launch(), ss_launch(k_bk_local, 2 * kNumSM, kBkLocThreads, BkLocSmem::bytes, e->st, a);
         SS_CUDA(e, cudaGetLastError());
         return SS_OK;
     }
@@ -1292,12 +1310,11 @@ static int launch_place_step(ss_engine* e, const uint32_t* dk, const int32_t* dv
         static const int use_match = getenv("SS_B200_RANK_MATCH") ? atoi(getenv("SS_B200_RANK_MATCH")) : 0;
         auto kern = use_match ? k_rank_place<0> : rank_kernel(bits_for(e->G));
         // sub-chunk prefixes (no-ops unless k_scan_small chose sub-chunks)
-        ss_note_launch(), k_sub_hist<<<kSubUnitsMax, 512, e->G * 4, e->st>>>(dk, n, cs, e->lc, e->n_lc, e->sub_shift,
+        ss_note_launch(), ss_launch(k_sub_hist, kSubUnitsMax, 512, e->G * 4, e->st, dk, n, cs, e->lc, e->n_lc, e->sub_shift,
                                                                             (uint32_t)e->G, e->subh, e->bad);
-        ss_note_launch(), k_sub_scan<<<2 * kNumSM, 256, 0, e->st>>>(e->gpre, e->lc, e->n_lc, e->sub_shift,
+        ss_note_launch(), ss_launch(k_sub_scan, 2 * kNumSM, 256, 0, e->st, e->gpre, e->lc, e->n_lc, e->sub_shift,
                                                                    (uint32_t)e->G, e->subh, e->gsub, e->bad);
-        ss_note_launch(), kern<<<std::max(n_chunk, kSubUnitsMax), kRankWarps * 32, rank_smem_bytes((uint32_t)e->G), e->st>>>(
-            dk, dv, e->trace_on ? e->kbuf2 : nullptr, e->vbuf[0], n, cs, e->lc, e->n_lc, e->gpre, e->gstart,
+        ss_note_launch(), ss_launch(kern, std::max(n_chunk, kSubUnitsMax), kRankWarps * 32, rank_smem_bytes((uint32_t)e->G), e->st, dk, dv, e->trace_on ? e->kbuf2 : nullptr, e->vbuf[0], n, cs, e->lc, e->n_lc, e->gpre, e->gstart,
             (uint32_t)e->G, e->n_live, e->bad, e->sub_shift, e->gsub);
         SS_CUDA(e, cudaGetLastError());
         return SS_OK;
@@ -1306,9 +1323,9 @@ static int launch_place_step(ss_engine* e, const uint32_t* dk, const int32_t* dv
     // enough CTAs per chunk that every SM has a slice of ~4K groups or more
     const int slices = (int)std::max<int64_t>(1, std::min<int64_t>((e->G + 4095) / 4096, (2 * kNumSM + n_chunk - 1) / n_chunk));
     SS_CUDA(e, cudaMemsetAsync(e->chunk_h, 0, (size_t)n_chunk * nb0 * 4, e->st));
-    ss_note_launch(), k_chunk_hist<<<dim3(n_chunk, slices), 1024, nb0 * 4, e->st>>>(e->gcnt, (uint32_t)e->G, e->lc, e->n_lc,
+    ss_note_launch(), ss_launch(k_chunk_hist, dim3(n_chunk, slices), 1024, nb0 * 4, e->st, e->gcnt, (uint32_t)e->G, e->lc, e->n_lc,
                                                                                    m0, nb0, e->chunk_h, e->bad);
-    ss_note_launch(), k_chunk_scan<<<(nb0 + 31) / 32, 1024, 0, e->st>>>(e->chunk_h, e->n_lc, nb0, base0,
+    ss_note_launch(), ss_launch(k_chunk_scan, (nb0 + 31) / 32, 1024, 0, e->st, e->chunk_h, e->n_lc, nb0, base0,
                                                                         e->chunk_base, e->bad);
     SortSeg s1{};
     s1.mode = 1;
@@ -1422,7 +1439,7 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
         if (e->G <= 16384) {
             // one CTA per count chunk, rows written whole (no zeroing needed)
             if (n) {
-                ss_note_launch(), k_count_rows<<<n_chunk, 512, e->G * 4, e->st>>>(dk, n, (uint32_t)e->G, e->S, e->gcnt,
+                ss_note_launch(), ss_launch(k_count_rows, n_chunk, 512, e->G * 4, e->st, dk, n, (uint32_t)e->G, e->S, e->gcnt,
                                                                                  e->bad, ((uintptr_t)dk % 16) == 0);
                 SS_CUDA(e, cudaGetLastError());
             }
@@ -1442,11 +1459,10 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
         if (e->G > 16384) {
             // hot cache for the next batch's count: > 1/(4 kHotCache) of the batch
             SS_CUDA(e, cudaMemsetAsync(e->n_hot_dev, 0, 4, e->st));
-            ss_note_launch(), k_hot_select<<<2 * kNumSM, 256, 0, e->st>>>(e->gcount, (uint32_t)e->G,
+            ss_note_launch(), ss_launch(k_hot_select, 2 * kNumSM, 256, 0, e->st, e->gcount, (uint32_t)e->G,
                                                         std::max<long long>(32, n / (4 * kHotCache)), e->hot_of,
                                                         e->hot_g, e->n_hot_dev, e->bad,
                                                         e->keys64 ? (int32_t*)e->kt.ent : nullptr, e->kt.slot_ent);
-            if (e->keys64) ss_note_launch(), k_hot_keytab<<<1, 1024, 0, e->st>>>(e->kt, e->hot_g, e->n_hot_dev);
         }
     }
     e->alg_input += (e->keys64 ? 12 : 8) * n;   // the batch is read once: key + attr bytes
@@ -1458,17 +1474,17 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
             SS_CUDA(e, cudaMemsetAsync(e->spx.base, 0, e->P * 8, e->side));
             SS_CUDA(e, cudaMemsetAsync(e->spx.n_hot, 0, 4, e->side));
             const long long hot_min = std::max<long long>(1, n / (2LL * e->P));
-            ss_note_launch(), k_split_hot<<<2 * kNumSM, 256, e->P * 4, e->side>>>(e->gcount, (uint32_t)e->G, e->pmap, hot_min, e->maxS,
+            ss_note_launch(), ss_launch(k_split_hot, 2 * kNumSM, 256, e->P * 4, e->side, e->gcount, (uint32_t)e->G, e->pmap, hot_min, e->maxS,
                                                                 e->spx, e->P, e->bad);
             // water-fill the hot groups over this batch's cold loads (the
             // policy's moves apply from the next batch on)
             const SplitPlan& nx = e->plan_buf[plan];
-            ss_note_launch(), k_u64_to_i64<<<1, 1024, 0, e->side>>>(e->spx.base, e->fill_loads, e->P);
+            ss_note_launch(), ss_launch(k_u64_to_i64, 1, 1024, 0, e->side, e->spx.base, e->fill_loads, e->P);
             const size_t smem = (size_t)e->maxS * 20 + 16 + (size_t)(e->P + 1) * 4;
-            ss_note_launch(), k_split_fill<<<1, 1024, smem, e->side>>>(e->gcount, e->fill_loads, e->P, e->maxS, e->spx, nx, nx,
+            ss_note_launch(), ss_launch(k_split_fill, 1, 1024, smem, e->side, e->gcount, e->fill_loads, e->P, e->maxS, e->spx, nx, nx,
                                                                        e->bad);
             SS_CUDA(e, cudaMemsetAsync(e->loads, 0, e->P * 8, e->side));
-            ss_note_launch(), k_split_loads<<<2 * kNumSM, 256, e->P * 4, e->side>>>(e->gcount, (uint32_t)e->G, e->pmap, e->P,
+            ss_note_launch(), ss_launch(k_split_loads, 2 * kNumSM, 256, e->P * 4, e->side, e->gcount, (uint32_t)e->G, e->pmap, e->P,
                                                                                     nx, e->loads, e->bad);
             SS_CUDA(e, cudaEventRecord(e->ev_bal, e->side));
         }
@@ -1513,9 +1529,9 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
     if (!e->dense) {
         ProfScope ps(e, SS_K_INGEST, e->st);
         SS_CUDA(e, cudaMemsetAsync(e->n_copies, 0, 4, e->st));
-        ss_note_launch(), k_reserve<<<2 * kNumSM, 256, 0, e->st>>>(e->gcount, (uint32_t)e->G, e->W, e->fill, e->off, e->cap,
+        ss_note_launch(), ss_launch(k_reserve, 2 * kNumSM, 256, 0, e->st, e->gcount, (uint32_t)e->G, e->W, e->fill, e->off, e->cap,
                                                  e->pool_top, e->pool_cap, e->oom, e->copies, e->n_copies, e->bad);
-        ss_note_launch(), k_ring_copy<<<8 * kNumSM, 256, 0, e->st>>>(e->copies, e->n_copies, e->ring);
+        ss_note_launch(), ss_launch(k_ring_copy, 8 * kNumSM, 256, 0, e->st, e->copies, e->n_copies, e->ring);
     }
     {
         ProfScope ps(e, SS_K_PLACE, e->st);
@@ -1538,9 +1554,9 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
         ta.tile = e->trace_tile;
         ta.bad = e->bad;
         const unsigned tiles = (unsigned)((n + kTraceTile - 1) / kTraceTile);
-        ss_note_launch(), k_trace_local<<<tiles, kTraceTile, 0, e->st>>>(ta);
-        ss_note_launch(), k_trace_tiles<<<1, 1024, 0, e->st>>>(ta);
-        ss_note_launch(), k_trace_apply<<<tiles, kTraceTile, 0, e->st>>>(ta);
+        ss_note_launch(), ss_launch(k_trace_local, tiles, kTraceTile, 0, e->st, ta);
+        ss_note_launch(), ss_launch(k_trace_tiles, 1, 1024, 0, e->st, ta);
+        ss_note_launch(), ss_launch(k_trace_apply, tiles, kTraceTile, 0, e->st, ta);
         SS_CUDA(e, cudaGetLastError());
     }
     if (e->cur_stage >= 0) {
@@ -1562,13 +1578,13 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
         a.cpp = std::max(1, ((split || !has_policy) ? 2 : 8) * kNumSM / e->P);
         unsigned grid = (unsigned)(e->P * a.cpp);
         if (work_grid) {
-            ss_note_launch(), k_cta_map<<<1, 1024, 0, e->st>>>(e->pwork, e->P, k4_waves * kNumSM, e->cta_map,
+            ss_note_launch(), ss_launch(k_cta_map, 1, 1024, 0, e->st, e->pwork, e->P, k4_waves * kNumSM, e->cta_map,
                                                                e->cta_used);
             a.cta_map = e->cta_map;
             a.n_used = e->cta_used;
             grid = (unsigned)(k4_waves * kNumSM + e->P);
         }
-        ss_note_launch(), k_ingest<<<grid, kIngestThreads, kIngestSmem, e->st>>>(a);
+        ss_note_launch(), ss_launch(k_ingest, grid, kIngestThreads, kIngestSmem, e->st, a);
         SS_CUDA(e, cudaGetLastError());
     }
     if (run_side) SS_CUDA(e, cudaEventRecord(e->ev_k4, e->st));
@@ -1605,24 +1621,24 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
         f.sum_valid = e->sum_valid;
         f.n_sum = e->n_sum;
         f.bad = e->bad;
-        ss_note_launch(), k_finalize<<<2 * kNumSM, 256, 0, e->st>>>(f);
+        ss_note_launch(), ss_launch(k_finalize, 2 * kNumSM, 256, 0, e->st, f);
         if (e->minmax) {
             if (e->sums) {
-                ss_note_launch(), k_mm_refresh<<<8 * kNumSM, 256, 0, e->st>>>(e->rescan, e->n_rescan, e->ring, e->off, e->W,
+                ss_note_launch(), ss_launch(k_mm_refresh, 8 * kNumSM, 256, 0, e->st, e->rescan, e->n_rescan, e->ring, e->off, e->W,
                                                                                e->sum_idx, e->sum_valid, e->sums);
-                ss_note_launch(), k_mm_fold<<<2 * kNumSM, 256, 0, e->st>>>(e->rescan, e->n_rescan, e->W, e->sum_idx,
+                ss_note_launch(), ss_launch(k_mm_fold, 2 * kNumSM, 256, 0, e->st, e->rescan, e->n_rescan, e->W, e->sum_idx,
                                                                             e->sum_valid, e->sums, e->mn, e->mx, e->r_mn,
                                                                             e->r_mx);
             } else {
-                ss_note_launch(), k_rescan_reset<<<4, 256, 0, e->st>>>(e->rescan, e->n_rescan, e->mn, e->mx);
-                ss_note_launch(), k_minmax_rescan<<<8 * kNumSM, 256, 0, e->st>>>(e->rescan, e->n_rescan, e->ring, e->off,
+                ss_note_launch(), ss_launch(k_rescan_reset, 4, 256, 0, e->st, e->rescan, e->n_rescan, e->mn, e->mx);
+                ss_note_launch(), ss_launch(k_minmax_rescan, 8 * kNumSM, 256, 0, e->st, e->rescan, e->n_rescan, e->ring, e->off,
                                                                                  e->W, e->mn, e->mx);
-                ss_note_launch(), k_rescan_rows<<<4, 256, 0, e->st>>>(e->rescan, e->n_rescan, e->mn, e->mx, e->r_mn, e->r_mx);
+                ss_note_launch(), ss_launch(k_rescan_rows, 4, 256, 0, e->st, e->rescan, e->n_rescan, e->mn, e->mx, e->r_mn, e->r_mx);
             }
         }
         if (emit && e->host_emit) {
             const int b = (int)(e->emit_seq & 1);
-            ss_note_launch(), k_emit_host<<<kNumSM, 256, 0, e->st>>>(e->n_res, e->bad, dk, (long long)n, e->r_g, e->r_cnt, e->r_sum,
+            ss_note_launch(), ss_launch(k_emit_host, kNumSM, 256, 0, e->st, e->n_res, e->bad, dk, (long long)n, e->r_g, e->r_cnt, e->r_sum,
                                                                      e->r_avg, e->r_mn, e->r_mx, e->d_emit[b]);
             SS_CUDA(e, record_ext(e, e->ev_emit[b], e->st));
             ++e->emit_seq;
@@ -1634,9 +1650,9 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
         if (has_policy) {
             ProfScope ps(e, SS_K_APPLY, e->side);
             // (the new offsets and move positions come from k_balance)
-            ss_note_launch(), k_apply_place<<<e->P, 256, 0, e->side>>>(e->order, e->offsets, e->keep_at, e->moves,
+            ss_note_launch(), ss_launch(k_apply_place, e->P, 256, 0, e->side, e->order, e->offsets, e->keep_at, e->moves,
                                                                        e->n_moves, e->mv_pos, e->moved, e->new_order);
-            ss_note_launch(), k_apply_commit<<<2 * kNumSM, 256, 0, e->side>>>(e->order, e->offsets, e->new_order, e->new_off, (int)e->G,
+            ss_note_launch(), ss_launch(k_apply_commit, 2 * kNumSM, 256, 0, e->side, e->order, e->offsets, e->new_order, e->new_off, (int)e->G,
                                                             e->P, e->moves, e->n_moves, e->pmap, e->moved);
             SS_CUDA(e, cudaGetLastError());
         }
@@ -1661,7 +1677,7 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
 // --------------------------------------------------------------------------
 static int enqueue_report(ss_engine* e, int64_t n, bool has_policy, cudaStream_t st) {
     const bool used_plan = e->last_plan >= 0;
-    ss_note_launch(), k_report<<<1, 1024, 0, st>>>(e->tpt, used_plan ? e->loads : nullptr, e->P, e->bad, e->touched, e->n_moves,
+    ss_note_launch(), ss_launch(k_report, 1, 1024, 0, st, e->tpt, used_plan ? e->loads : nullptr, e->P, e->bad, e->touched, e->n_moves,
                                  e->prev_moves, e->scanned,
                                  used_plan ? e->plan_buf[e->last_plan].n_split : nullptr,
                                  // (the result-row count is read from n_res by the result calls; the
@@ -1861,14 +1877,14 @@ extern "C" int ss_reorder(ss_engine* e, const uint32_t* groups, const int32_t* a
     if ((rc = stage_input(e, groups, attrs, n, &dk, &dv))) return rc;
     if ((rc = engine_alloc_sort(e, n))) return rc;
     int32_t* rank = e->new_order;   // scratch: only the apply kernels use it, inside a step
-    ss_note_launch(), k_rank_of<<<2 * kNumSM, 256, 0, e->st>>>(e->order, e->G, rank);
-    if (n) ss_note_launch(), k_to_rank<<<2 * kNumSM, 256, 0, e->st>>>(dk, n, rank, (uint32_t)e->G, e->stage_keys, e->bad);
+    ss_note_launch(), ss_launch(k_rank_of, 2 * kNumSM, 256, 0, e->st, e->order, e->G, rank);
+    if (n) ss_note_launch(), ss_launch(k_to_rank, 2 * kNumSM, 256, 0, e->st, dk, n, rank, (uint32_t)e->G, e->stage_keys, e->bad);
     const uint32_t* rk = e->stage_keys;
     if ((rc = launch_count(e, rk, n, round_chunk(n)))) return rc;
     SS_CUDA(e, cudaMemsetAsync(e->tickets, 0, 8, e->st));
     if ((rc = launch_scans(e, e->gcnt))) return rc;
     if (n && (rc = launch_place_all(e, rk, dv, n))) return rc;
-    if (n) ss_note_launch(), k_from_rank<<<2 * kNumSM, 256, 0, e->st>>>(e->kbuf2, n, e->order);
+    if (n) ss_note_launch(), ss_launch(k_from_rank, 2 * kNumSM, 256, 0, e->st, e->kbuf2, n, e->order);
     unsigned long long bad;
     SS_CUDA(e, cudaMemcpyAsync(&bad, e->bad, 8, cudaMemcpyDeviceToHost, e->st));
     SS_CUDA(e, cudaStreamSynchronize(e->st));
@@ -1956,7 +1972,7 @@ extern "C" int ss_balance(ss_engine* e, const uint32_t* groups, int64_t n, const
         a.bad = e->bad;
         ss_note_launch(), launch_balance(e, a, e->st);
         SS_CUDA(e, cudaGetLastError());
-        ss_note_launch(), k_clear_moved<<<4, 256, 0, e->st>>>(e->moves, e->n_moves, e->moved);
+        ss_note_launch(), ss_launch(k_clear_moved, 4, 256, 0, e->st, e->moves, e->n_moves, e->moved);
         SS_CUDA(e, cudaMemcpyAsync(&nm, e->n_moves, 4, cudaMemcpyDeviceToHost, e->st));
         SS_CUDA(e, cudaMemcpyAsync(&sc, e->scanned, 8, cudaMemcpyDeviceToHost, e->st));
         SS_CUDA(e, cudaMemcpyAsync(ft.data(), e->final_tpt, e->P * 8, cudaMemcpyDeviceToHost, e->st));
@@ -2108,7 +2124,7 @@ static int run_step(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_t
 
 // stream-scope window: one batch (see streamwin.cuh)
 __global__ void k_sw_report(const unsigned long long* bad, long long n, const unsigned long long* touched,
-                            const unsigned* n_res, DevReport* rep) {
+                            const unsigned* n_res, DevReport* rep) { SS_PDL_ENTRY();
     DevReport r{};
     r.bad = *bad;
     r.tuples = n;
@@ -2138,12 +2154,12 @@ static int run_stream(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64
     a.bad = e->bad;
     SS_CUDA(e, cudaMemsetAsync(e->n_res, 0, 4, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->touched, 0, 8, e->st));
-    ss_note_launch(), k_sw_check<<<4 * kNumSM, 256, 0, e->st>>>(a);
-    ss_note_launch(), k_sw_evict<<<4 * kNumSM, 256, 0, e->st>>>(a);
-    ss_note_launch(), k_sw_add<<<4 * kNumSM, 256, 0, e->st>>>(a);
+    ss_note_launch(), ss_launch(k_sw_check, 4 * kNumSM, 256, 0, e->st, a);
+    ss_note_launch(), ss_launch(k_sw_evict, 4 * kNumSM, 256, 0, e->st, a);
+    ss_note_launch(), ss_launch(k_sw_add, 4 * kNumSM, 256, 0, e->st, a);
     if (e->minmax) {
-        ss_note_launch(), k_sw_mm_reset<<<2 * kNumSM, 256, 0, e->st>>>(a);
-        ss_note_launch(), k_sw_mm_scan<<<4 * kNumSM, 256, 0, e->st>>>(a);
+        ss_note_launch(), ss_launch(k_sw_mm_reset, 2 * kNumSM, 256, 0, e->st, a);
+        ss_note_launch(), ss_launch(k_sw_mm_scan, 4 * kNumSM, 256, 0, e->st, a);
     }
     StreamEmitArgs f{};
     f.G = (uint32_t)e->G;
@@ -2162,9 +2178,9 @@ static int run_stream(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64
     f.r_mx = e->r_mx;
     f.touched_total = e->touched;
     f.bad = e->bad;
-    ss_note_launch(), k_sw_emit<<<2 * kNumSM, 256, 0, e->st>>>(f);
-    ss_note_launch(), k_sw_advance<<<1, 1, 0, e->st>>>(a);
-    ss_note_launch(), k_sw_report<<<1, 1, 0, e->st>>>(e->bad, (long long)n, e->touched, e->n_res, e->d_rep);
+    ss_note_launch(), ss_launch(k_sw_emit, 2 * kNumSM, 256, 0, e->st, f);
+    ss_note_launch(), ss_launch(k_sw_advance, 1, 1, 0, e->st, a);
+    ss_note_launch(), ss_launch(k_sw_report, 1, 1, 0, e->st, e->bad, (long long)n, e->touched, e->n_res, e->d_rep);
     SS_CUDA(e, cudaMemcpyAsync(e->h_rep, e->d_rep, sizeof(DevReport), cudaMemcpyDeviceToHost, e->st));
     SS_CUDA(e, cudaGetLastError());
     if (e->cur_stage >= 0) {
@@ -2250,7 +2266,7 @@ extern "C" int ss_step_records(ss_engine* e, const void* records, int64_t n, con
     if ((rc = end_stage(e))) return rc;
     if (n) {
         if (((uintptr_t)rec & 15) != 0) return fail(e, SS_E_CONFIG, "device records must be 16-byte aligned");
-        ss_note_launch(), k_deinterleave<<<4 * kNumSM, 256, 0, e->st>>>((const uint4*)rec, n, e->skeys[b], e->svals[b]);
+        ss_note_launch(), ss_launch(k_deinterleave, 4 * kNumSM, 256, 0, e->st, (const uint4*)rec, n, e->skeys[b], e->svals[b]);
         SS_CUDA(e, cudaGetLastError());
     }
     return ss_step(e, e->skeys[b], e->svals[b], n, cfg, rep);
@@ -2509,7 +2525,7 @@ extern "C" int ss_route(ss_engine* e, const uint32_t* groups, const int32_t* att
     if ((rc = stage_input(e, groups, attrs, n, &dk, &dv))) return rc;
     if ((rc = engine_alloc_sort(e, n))) return rc;
     SS_CUDA(e, cudaMemsetAsync(e->route_cnt, 0, 16 * 8, e->st));
-    if (n) ss_note_launch(), k_owner_hist<<<2 * kNumSM, 256, 0, e->st>>>(dk, n, (uint32_t)e->G, e->owner, e->route_cnt, e->bad);
+    if (n) ss_note_launch(), ss_launch(k_owner_hist, 2 * kNumSM, 256, 0, e->st, dk, n, (uint32_t)e->G, e->owner, e->route_cnt, e->bad);
     unsigned long long hc[16];
     unsigned long long bad;
     SS_CUDA(e, cudaMemcpyAsync(hc, e->route_cnt, 16 * 8, cudaMemcpyDeviceToHost, e->st));
@@ -2529,10 +2545,9 @@ extern "C" int ss_route(ss_engine* e, const uint32_t* groups, const int32_t* att
     const bool dev_out = is_device_ptr(out_groups) && is_device_ptr(out_attrs);
     uint32_t* ko = dev_out ? out_groups : e->kbuf2;
     int32_t* vo = dev_out ? out_attrs : e->vbuf[0];
-    ss_note_launch(), k_epoch_bump<<<1, 1, 0, e->st>>>(e->ep_dev);
+    ss_note_launch(), ss_launch(k_epoch_bump, 1, 1, 0, e->st, e->ep_dev);
     const int tiles = (int)((n + kSortTile - 1) / kSortTile);
-    ss_note_launch(), k_sort_pass<4, true><<<std::min(tiles, 2 * kNumSM), kSortThreads, SortSmem<4>::bytes, e->st>>>(
-        dk, dv, ko, vo, (int)n, 0, 15u, e->route_base, e->status, e->ep_dev, 0, e->tickets, e->bad, 0, e->owner);
+    ss_note_launch(), ss_launch(k_sort_pass<4, true>, std::min(tiles, 2 * kNumSM), kSortThreads, SortSmem<4>::bytes, e->st, dk, dv, ko, vo, (int)n, 0, 15u, e->route_base, e->status, e->ep_dev, 0, e->tickets, e->bad, 0, e->owner, nullptr, SortSeg{});
     SS_CUDA(e, cudaGetLastError());
     if (!dev_out) {
         SS_CUDA(e, cudaMemcpyAsync(out_groups, ko, n * 4, cudaMemcpyDeviceToHost, e->st));
@@ -2557,7 +2572,7 @@ extern "C" int ss_group_counts(ss_engine* e, int32_t* counts) {
 }
 
 __global__ void k_tpt_from_counts(const int32_t* __restrict__ counts, int64_t G, const int32_t* __restrict__ pmap,
-                                  unsigned long long* __restrict__ tpt) {
+                                  unsigned long long* __restrict__ tpt) { SS_PDL_ENTRY();
     for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < G; g += (int64_t)gridDim.x * blockDim.x)
         if (counts[g]) atomicAdd(&tpt[pmap[g]], (unsigned long long)counts[g]);
 }
@@ -2570,7 +2585,7 @@ __global__ void k_tpt_from_counts(const int32_t* __restrict__ counts, int64_t G,
 
 // route bases from the owner histogram; counts_dev[d] for d < n_dest
 __global__ void k_route_base(const unsigned long long* __restrict__ cnt, int n_dest, uint32_t* __restrict__ base,
-                             int64_t* __restrict__ counts_dev) {
+                             int64_t* __restrict__ counts_dev) { SS_PDL_ENTRY();
     if (threadIdx.x != 0) return;
     uint32_t run = 0;
     for (int d = 0; d < 16; ++d) {
@@ -2581,7 +2596,7 @@ __global__ void k_route_base(const unsigned long long* __restrict__ cnt, int n_d
 }
 // counts_dev[n_dest] = first bad tuple index (or -1); the route mutates no
 // engine state, so the flag is cleared for the batch that follows
-__global__ void k_route_done(unsigned long long* __restrict__ bad, int n_dest, int64_t* __restrict__ counts_dev) {
+__global__ void k_route_done(unsigned long long* __restrict__ bad, int n_dest, int64_t* __restrict__ counts_dev) { SS_PDL_ENTRY();
     if (threadIdx.x != 0) return;
     const unsigned long long b = *bad;
     counts_dev[n_dest] = b == (unsigned long long)kNoBad ? -1 : (int64_t)b;
@@ -2603,17 +2618,16 @@ extern "C" int ss_route_records(ss_engine* e, const uint32_t* groups, const int3
     if ((rc = stage_input(e, groups, attrs, n, &dk, &dv))) return rc;
     if ((rc = engine_alloc_sort(e, n))) return rc;
     SS_CUDA(e, cudaMemsetAsync(e->route_cnt, 0, 16 * 8, e->st));
-    if (n) ss_note_launch(), k_owner_hist<<<2 * kNumSM, 256, 0, e->st>>>(dk, n, (uint32_t)e->G, e->owner, e->route_cnt, e->bad);
-    ss_note_launch(), k_route_base<<<1, 32, 0, e->st>>>(e->route_cnt, e->n_dest, e->route_base, counts_dev);
+    if (n) ss_note_launch(), ss_launch(k_owner_hist, 2 * kNumSM, 256, 0, e->st, dk, n, (uint32_t)e->G, e->owner, e->route_cnt, e->bad);
+    ss_note_launch(), ss_launch(k_route_base, 1, 32, 0, e->st, e->route_cnt, e->n_dest, e->route_base, counts_dev);
     if (n) {
         SS_CUDA(e, cudaMemsetAsync(e->tickets, 0, 8, e->st));
-        ss_note_launch(), k_epoch_bump<<<1, 1, 0, e->st>>>(e->ep_dev);
+        ss_note_launch(), ss_launch(k_epoch_bump, 1, 1, 0, e->st, e->ep_dev);
         const int tiles = (int)((n + kSortTile - 1) / kSortTile);
-        ss_note_launch(), k_sort_pass<4, true><<<std::min(tiles, 2 * kNumSM), kSortThreads, SortSmem<4>::bytes, e->st>>>(
-            dk, dv, (uint32_t*)out_records, nullptr, (int)n, 0, 15u, e->route_base, e->status, e->ep_dev, 0,
-            e->tickets, e->bad, 0, e->owner);
+        ss_note_launch(), ss_launch(k_sort_pass<4, true>, std::min(tiles, 2 * kNumSM), kSortThreads, SortSmem<4>::bytes, e->st, dk, dv, (uint32_t*)out_records, nullptr, (int)n, 0, 15u, e->route_base, e->status, e->ep_dev, 0,
+            e->tickets, e->bad, 0, e->owner, nullptr, SortSeg{});
     }
-    ss_note_launch(), k_route_done<<<1, 32, 0, e->st>>>(e->bad, e->n_dest, counts_dev);
+    ss_note_launch(), ss_launch(k_route_done, 1, 32, 0, e->st, e->bad, e->n_dest, counts_dev);
     SS_CUDA(e, cudaGetLastError());
     return SS_OK;
 }
@@ -2649,7 +2663,7 @@ extern "C" int ss_balance_apply_dev(ss_engine* e, const int32_t* counts_dev, con
     SS_CUDA(e, cudaMemcpyAsync(e->gcount, counts_dev, e->G * 4, cudaMemcpyDeviceToDevice, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->tpt, 0, e->P * 8, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->n_moves, 0, 4, e->st));
-    ss_note_launch(), k_tpt_from_counts<<<2 * kNumSM, 256, 0, e->st>>>(e->gcount, e->G, e->pmap, e->tpt);
+    ss_note_launch(), ss_launch(k_tpt_from_counts, 2 * kNumSM, 256, 0, e->st, e->gcount, e->G, e->pmap, e->tpt);
     const int cap = move_cap(e, cfg);
     if (cfg->policy != SS_POLICY_NO) {
         BalanceArgs a{};
@@ -2675,9 +2689,9 @@ extern "C" int ss_balance_apply_dev(ss_engine* e, const int32_t* counts_dev, con
         a.final_tpt = e->final_tpt;
         a.bad = e->bad;
         ss_note_launch(), launch_balance(e, a, e->st);
-        ss_note_launch(), k_apply_place<<<e->P, 256, 0, e->st>>>(e->order, e->offsets, e->keep_at, e->moves,
+        ss_note_launch(), ss_launch(k_apply_place, e->P, 256, 0, e->st, e->order, e->offsets, e->keep_at, e->moves,
                                                                   e->n_moves, e->mv_pos, e->moved, e->new_order);
-        ss_note_launch(), k_apply_commit<<<2 * kNumSM, 256, 0, e->st>>>(e->order, e->offsets, e->new_order, e->new_off,
+        ss_note_launch(), ss_launch(k_apply_commit, 2 * kNumSM, 256, 0, e->st, e->order, e->offsets, e->new_order, e->new_off,
                                                                         (int)e->G, e->P, e->moves, e->n_moves, e->pmap,
                                                                         e->moved);
     }
@@ -2701,7 +2715,7 @@ __global__ void k_export_plan(const int4* __restrict__ moves, const int32_t* __r
                               const long long* __restrict__ wsum, const int32_t* __restrict__ mn,
                               const int32_t* __restrict__ mx, const int64_t* __restrict__ off, int32_t* __restrict__ blob,
                               int64_t blob_cap, int64_t* __restrict__ sizes, longlong4* __restrict__ list,
-                              int* __restrict__ n_list) {
+                              int* __restrict__ n_list) { SS_PDL_ENTRY();
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     const int nm = min(*n_moves, kMigMax);
     int64_t ng[16] = {0}, nv[16] = {0};
@@ -2751,7 +2765,7 @@ __global__ void k_export_plan(const int4* __restrict__ moves, const int32_t* __r
 
 __global__ void __launch_bounds__(256)
 k_export_vals(const longlong4* __restrict__ list, const int* __restrict__ n_list, const int32_t* __restrict__ ring,
-              int32_t* __restrict__ blob) {
+              int32_t* __restrict__ blob) { SS_PDL_ENTRY();
     if ((int)blockIdx.x >= *n_list) return;
     const longlong4 c = list[blockIdx.x];
     for (int64_t j = threadIdx.x; j < c.z; j += blockDim.x) blob[c.y + j] = ring[c.x + j];
@@ -2763,10 +2777,10 @@ extern "C" int ss_export_moves_dev(ss_engine* e, const void* moves_dev, const in
     if (e->n_dest < 1) return fail(e, SS_E_CONFIG, "ss_set_owner first");
     int rc;
     if (!e->mig_list && ((rc = dalloc(e, &e->mig_list, kMigMax)) || (rc = dalloc(e, &e->mig_n, 1)))) return rc;
-    ss_note_launch(), k_export_plan<<<1, 32, 0, e->st>>>((const int4*)moves_dev, n_moves_dev, rank, e->n_dest, e->W,
+    ss_note_launch(), ss_launch(k_export_plan, 1, 32, 0, e->st, (const int4*)moves_dev, n_moves_dev, rank, e->n_dest, e->W,
                                                          e->fill, e->next_pos, e->wsum, e->mn, e->mx, e->off, blob_dev,
                                                          blob_cap_words, sizes_dev, e->mig_list, e->mig_n);
-    ss_note_launch(), k_export_vals<<<kMigMax, 256, 0, e->st>>>(e->mig_list, e->mig_n, e->ring, blob_dev);
+    ss_note_launch(), ss_launch(k_export_vals, kMigMax, 256, 0, e->st, e->mig_list, e->mig_n, e->ring, blob_dev);
     SS_CUDA(e, cudaGetLastError());
     return SS_OK;
 }
@@ -2783,7 +2797,7 @@ k_import(const int32_t* __restrict__ blob, MigSegs segs, int64_t W, int dense, i
          int32_t* __restrict__ next_pos, long long* __restrict__ wsum, int32_t* __restrict__ mn,
          int32_t* __restrict__ mx, int64_t* __restrict__ off, int32_t* __restrict__ cap,
          unsigned long long* __restrict__ pool_top, unsigned long long pool_cap, int* __restrict__ oom,
-         uint8_t* __restrict__ sum_valid, int32_t* __restrict__ ring, int64_t G) {
+         uint8_t* __restrict__ sum_valid, int32_t* __restrict__ ring, int64_t G) { SS_PDL_ENTRY();
     __shared__ int64_t sh_dst;
     const int s = blockIdx.y, j = blockIdx.x;
     if (segs.off[s + 1] == segs.off[s]) return;
@@ -2828,14 +2842,14 @@ k_import(const int32_t* __restrict__ blob, MigSegs segs, int64_t W, int dense, i
 
 extern "C" int ss_import_blob_dev(ss_engine* e, const int32_t* blob_dev, const int64_t* seg_off, int n_seg,
                                   int max_groups) {
-    if (!e || n_seg < 0 || n_seg > 16 || (n_seg && (!blob_dev || !seg_off))) return SS_E_CONFIG;
-    if (n_seg == 0 || max_groups <= 0) return SS_OK;
+    if (!e || n_seg < 0 || n_seg > 16 || (n_seg && !seg_off)) return SS_E_CONFIG;
+    if (n_seg == 0 || max_groups <= 0 || seg_off[n_seg] == 0) return SS_OK;     // nothing received
+    if (!blob_dev) return fail(e, SS_E_CONFIG, "ss_import_blob_dev: null blob");
     MigSegs s{};
     for (int i = 0; i <= n_seg; ++i) s.off[i] = seg_off[i];
     s.n = n_seg;
     if (s.off[n_seg] == 0) return SS_OK;
-    ss_note_launch(), k_import<<<dim3((unsigned)std::min(max_groups, kMigMax), (unsigned)n_seg), 256, 0, e->st>>>(
-        blob_dev, s, e->W, e->dense ? 1 : 0, e->fill, e->next_pos, e->wsum, e->mn, e->mx, e->off, e->cap,
+    ss_note_launch(), ss_launch(k_import, dim3((unsigned)std::min(max_groups, kMigMax), (unsigned)n_seg), 256, 0, e->st, blob_dev, s, e->W, e->dense ? 1 : 0, e->fill, e->next_pos, e->wsum, e->mn, e->mx, e->off, e->cap,
         e->pool_top, e->pool_cap, e->oom, e->sum_valid, e->ring, e->G);
     SS_CUDA(e, cudaGetLastError());
     return SS_OK;
@@ -2854,7 +2868,7 @@ extern "C" int ss_balance_counts(ss_engine* e, const int32_t* counts, const ss_b
     SS_CUDA(e, cudaMemcpyAsync(e->gcount, counts, e->G * 4,
                                is_device_ptr(counts) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, e->st));
     SS_CUDA(e, cudaMemsetAsync(e->tpt, 0, e->P * 8, e->st));
-    ss_note_launch(), k_tpt_from_counts<<<2 * kNumSM, 256, 0, e->st>>>(e->gcount, e->G, e->pmap, e->tpt);
+    ss_note_launch(), ss_launch(k_tpt_from_counts, 2 * kNumSM, 256, 0, e->st, e->gcount, e->G, e->pmap, e->tpt);
     int nm = 0;
     long long sc = 0;
     std::vector<long long> ft(e->P);
@@ -2885,7 +2899,7 @@ extern "C" int ss_balance_counts(ss_engine* e, const int32_t* counts, const ss_b
         a.bad = e->bad;
         ss_note_launch(), launch_balance(e, a, e->st);
         SS_CUDA(e, cudaGetLastError());
-        ss_note_launch(), k_clear_moved<<<4, 256, 0, e->st>>>(e->moves, e->n_moves, e->moved);
+        ss_note_launch(), ss_launch(k_clear_moved, 4, 256, 0, e->st, e->moves, e->n_moves, e->moved);
         SS_CUDA(e, cudaMemcpyAsync(&nm, e->n_moves, 4, cudaMemcpyDeviceToHost, e->st));
         SS_CUDA(e, cudaMemcpyAsync(&sc, e->scanned, 8, cudaMemcpyDeviceToHost, e->st));
         SS_CUDA(e, cudaMemcpyAsync(ft.data(), e->final_tpt, e->P * 8, cudaMemcpyDeviceToHost, e->st));
@@ -3005,17 +3019,17 @@ static int map_keys(ss_engine* e, const int64_t* keys, int64_t n, uint32_t* dout
     const unsigned grid = (unsigned)((n + range - 1) / range);
     SS_CUDA(e, cudaMemsetAsync(t.n_pend, 0, 4, e->st));
     if (count)
-        ss_note_launch(), k_key_count<true><<<grid, 512, kHotCache * 4, e->st>>>(dk, n, t, dout, e->S, range, e->gcnt,
+        ss_note_launch(), ss_launch(k_key_count<true>, grid, 512, kHotCache * 4, e->st, dk, n, t, dout, e->S, range, e->gcnt,
                                                                               e->hot_g, kHotCache, e->key_agg);
     else
-        ss_note_launch(), k_key_count<false><<<grid, 512, 0, e->st>>>(dk, n, t, dout, e->S, range, nullptr, nullptr, 0, 0);
-    ss_note_launch(), k_key_rank_small<<<1, 1024, 0, e->st>>>(t);
-    ss_note_launch(), k_key_mark<<<2 * kNumSM, 256, 0, e->st>>>(t);
-    ss_note_launch(), k_key_mark_count<<<nblk, 1024, 0, e->st>>>(t, n, e->kbsum);
-    ss_note_launch(), k_key_mark_scan<<<1, 1024, 0, e->st>>>(t, e->kbsum, nblk);
-    ss_note_launch(), k_key_mark_assign<<<nblk, 1024, 0, e->st>>>(t, n, e->kbsum);
-    ss_note_launch(), k_key_mark_done<<<1, 1, 0, e->st>>>(t);
-    ss_note_launch(), k_key_map<<<4 * kNumSM, 256, 0, e->st>>>(dk, t, dout, e->S, count ? e->gcnt : nullptr, e->bad);
+        ss_note_launch(), ss_launch(k_key_count<false>, grid, 512, 0, e->st, dk, n, t, dout, e->S, range, nullptr, nullptr, 0, 0);
+    ss_note_launch(), ss_launch(k_key_rank_small, 1, 1024, 0, e->st, t);
+    ss_note_launch(), ss_launch(k_key_mark, 2 * kNumSM, 256, 0, e->st, t);
+    ss_note_launch(), ss_launch(k_key_mark_count, nblk, 1024, 0, e->st, t, n, e->kbsum);
+    ss_note_launch(), ss_launch(k_key_mark_scan, 1, 1024, 0, e->st, t, e->kbsum, nblk);
+    ss_note_launch(), ss_launch(k_key_mark_assign, nblk, 1024, 0, e->st, t, n, e->kbsum);
+    ss_note_launch(), ss_launch(k_key_mark_done, 1, 1, 0, e->st, t);
+    ss_note_launch(), ss_launch(k_key_map, 4 * kNumSM, 256, 0, e->st, dk, t, dout, e->S, count ? e->gcnt : nullptr, e->bad);
     SS_CUDA(e, cudaGetLastError());
     return SS_OK;
 }

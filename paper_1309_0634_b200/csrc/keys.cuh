@@ -59,17 +59,7 @@ struct KeyTable {
     int* overflow;              // more distinct keys than G
     unsigned long long cap_mask;
     int G;
-    // hot-key table image (kHotTab open-addressing slots: key, hot index),
-    // rebuilt per batch from the count cache's hot groups; every count CTA
-    // loads it into shared memory so a hot tuple costs no table probe
-    unsigned long long* hk_key;
-    uint16_t* hk_idx;
 };
-
-constexpr int kHotTab = 4096;                       // >= 2 x kHotCache
-__device__ __forceinline__ unsigned hot_tab_slot(unsigned long long hash) {
-    return (unsigned)(hash >> 52) & (kHotTab - 1);      // high hash bits (the table uses the low ones)
-}
 
 // L2 cache policies: the streamed batch leaves first, the table stays
 __device__ __forceinline__ unsigned long long policy_evict_first() {
@@ -128,20 +118,14 @@ constexpr int kKeyItems = 4;            // consecutive tuples per thread and rou
 template <bool COUNT>
 __global__ void __launch_bounds__(512)
 k_key_count(const long long* __restrict__ keys, int64_t n, KeyTable t, uint32_t* __restrict__ out, int64_t S,
-            int64_t range, int32_t* __restrict__ gcnt, const int32_t* __restrict__ hot_g, int n_hot, int agg) {
+            int64_t range, int32_t* __restrict__ gcnt, const int32_t* __restrict__ hot_g, int n_hot, int agg) { SS_PDL_ENTRY();
     extern __shared__ int32_t sh_hist[];                  // [n_hot]
-    __shared__ __align__(16) unsigned long long hk[COUNT ? kHotTab : 1];
-    __shared__ __align__(16) uint16_t hi[COUNT ? kHotTab : 1];
     const int64_t c0 = (int64_t)blockIdx.x * range;
     if (c0 >= n) return;
     const int64_t c1 = min64(n, c0 + range);
     int32_t* dst = COUNT ? gcnt + (c0 / S) * (int64_t)t.G : nullptr;
     if (COUNT) {
         for (int i = threadIdx.x; i < n_hot; i += blockDim.x) sh_hist[i] = 0;
-        for (int i = threadIdx.x; i < kHotTab / 2; i += blockDim.x)
-            reinterpret_cast<ulonglong2*>(hk)[i] = reinterpret_cast<const ulonglong2*>(t.hk_key)[i];
-        for (int i = threadIdx.x; i < kHotTab / 8; i += blockDim.x)
-            reinterpret_cast<uint4*>(hi)[i] = reinterpret_cast<const uint4*>(t.hk_idx)[i];
         __syncthreads();
     }
     const unsigned long long pol_s = policy_evict_first(), pol_t = policy_evict_last();
@@ -161,23 +145,10 @@ k_key_count(const long long* __restrict__ keys, int64_t n, KeyTable t, uint32_t*
         }
         KEntry en[kKeyItems];
         unsigned long long h[kKeyItems];
-        int hot_hit[kKeyItems];
 #pragma unroll
         for (int u = 0; u < kKeyItems; ++u) {
-            const unsigned long long hh = key_hash(k[u]);
-            h[u] = hh & t.cap_mask;
-            hot_hit[u] = -1;
-            if (COUNT && k[u] != kEmptyKey) {
-                // hot keys resolve in shared memory
-                unsigned s2 = hot_tab_slot(hh);
-                while (true) {
-                    const unsigned long long sk = hk[s2];
-                    if (sk == k[u]) { hot_hit[u] = hi[s2]; break; }
-                    if (sk == kEmptyKey) break;
-                    s2 = (s2 + 1) & (kHotTab - 1);
-                }
-            }
-            if (hot_hit[u] < 0) en[u] = ld_entry(t.ent + h[u], pol_t);   // the other first probes in flight together
+            h[u] = key_hash(k[u]) & t.cap_mask;
+            en[u] = ld_entry(t.ent + h[u], pol_t);        // all first probes in flight together
         }
         uint32_t sl[kKeyItems];
 #pragma unroll
@@ -187,10 +158,7 @@ k_key_count(const long long* __restrict__ keys, int64_t n, KeyTable t, uint32_t*
             int hot = -1;
             bool pending = false;
             int e = -1;
-            if (i < c1 && hot_hit[u] >= 0) {
-                hot = hot_hit[u];
-                sl[u] = (uint32_t)hot_g[hot];
-            } else if (i < c1) {
+            if (i < c1) {
                 if (k[u] == kEmptyKey) {
                     // the reserved marker value gets a dedicated entry: cap_mask + 1
                     e = (int)(t.cap_mask + 1);
@@ -257,51 +225,13 @@ k_key_count(const long long* __restrict__ keys, int64_t n, KeyTable t, uint32_t*
     }
 }
 
-__global__ void k_key_init(KEntry* ent, int64_t n) {
+__global__ void k_key_init(KEntry* ent, int64_t n) { SS_PDL_ENTRY();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         KEntry e;
         e.key = kEmptyKey;
         e.slot = -1;
         e.hot = -1;
         ent[i] = e;
-    }
-}
-
-__global__ void k_hot_keytab_clear(KeyTable t) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < kHotTab; i += gridDim.x * blockDim.x) {
-        t.hk_key[i] = kEmptyKey;
-        t.hk_idx[i] = 0xffff;
-    }
-}
-
-// the hot-key table image for the next batch's count (after k_hot_select)
-__global__ void __launch_bounds__(1024)
-k_hot_keytab(KeyTable t, const int32_t* __restrict__ hot_g, const int* __restrict__ n_hot_dev) {
-    __shared__ unsigned long long sk[kHotTab];
-    __shared__ uint16_t si[kHotTab];
-    for (int i = threadIdx.x; i < kHotTab; i += blockDim.x) {
-        sk[i] = kEmptyKey;
-        si[i] = 0xffff;
-    }
-    __syncthreads();
-    const int nh = min(*n_hot_dev, kHotCache);
-    for (int i = threadIdx.x; i < nh; i += blockDim.x) {
-        const unsigned long long k = t.slot_keys[hot_g[i]];
-        if (k == kEmptyKey) continue;                   // the reserved key keeps its table entry
-        unsigned h = hot_tab_slot(key_hash(k));
-        while (true) {
-            const unsigned long long prev = atomicCAS(&sk[h], kEmptyKey, k);
-            if (prev == kEmptyKey || prev == k) {
-                si[h] = (uint16_t)i;
-                break;
-            }
-            h = (h + 1) & (kHotTab - 1);
-        }
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < kHotTab; i += blockDim.x) {
-        t.hk_key[i] = sk[i];
-        t.hk_idx[i] = si[i];
     }
 }
 
@@ -319,7 +249,7 @@ __device__ __forceinline__ void assign_slot(KeyTable& t, int e, int s) {
 
 // few new keys: rank them by first position inside one CTA
 __global__ void __launch_bounds__(1024)
-k_key_rank_small(KeyTable t) {
+k_key_rank_small(KeyTable t) { SS_PDL_ENTRY();
     __shared__ unsigned int f[kKeySmall];
     __shared__ int32_t en[kKeySmall];
     const int nn = min(*t.n_new, t.G);       // entries past G were never listed (overflow)
@@ -346,7 +276,7 @@ k_key_rank_small(KeyTable t) {
 // many new keys: mark[first position] = entry, then an ordered
 // compaction over the batch positions (count / scan / assign)
 __global__ void __launch_bounds__(256)
-k_key_mark(KeyTable t) {
+k_key_mark(KeyTable t) { SS_PDL_ENTRY();
     const int nn = min(*t.n_new, t.G);
     if (nn <= kKeySmall) return;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nn; i += gridDim.x * blockDim.x) {
@@ -358,7 +288,7 @@ k_key_mark(KeyTable t) {
 constexpr int kMarkBlk = 4096;
 
 __global__ void __launch_bounds__(1024)
-k_key_mark_count(KeyTable t, int64_t n, int32_t* __restrict__ bsum) {
+k_key_mark_count(KeyTable t, int64_t n, int32_t* __restrict__ bsum) { SS_PDL_ENTRY();
     __shared__ int32_t red[33];
     if (min(*t.n_new, t.G) <= kKeySmall) return;
     int c = 0;
@@ -372,7 +302,7 @@ k_key_mark_count(KeyTable t, int64_t n, int32_t* __restrict__ bsum) {
 }
 
 __global__ void __launch_bounds__(1024)
-k_key_mark_scan(KeyTable t, int32_t* __restrict__ bsum, int nblk) {
+k_key_mark_scan(KeyTable t, int32_t* __restrict__ bsum, int nblk) { SS_PDL_ENTRY();
     __shared__ int32_t red[33];
     if (min(*t.n_new, t.G) <= kKeySmall) return;
     int32_t carry = *t.n_slots;
@@ -387,7 +317,7 @@ k_key_mark_scan(KeyTable t, int32_t* __restrict__ bsum, int nblk) {
 }
 
 __global__ void __launch_bounds__(1024)
-k_key_mark_assign(KeyTable t, int64_t n, const int32_t* __restrict__ bsum) {
+k_key_mark_assign(KeyTable t, int64_t n, const int32_t* __restrict__ bsum) { SS_PDL_ENTRY();
     __shared__ int32_t red[33];
     if (min(*t.n_new, t.G) <= kKeySmall) return;
     int32_t base = bsum[blockIdx.x];
@@ -405,7 +335,7 @@ k_key_mark_assign(KeyTable t, int64_t n, const int32_t* __restrict__ bsum) {
     }
 }
 
-__global__ void k_key_mark_done(KeyTable t) {
+__global__ void k_key_mark_done(KeyTable t) { SS_PDL_ENTRY();
     const int nn = min(*t.n_new, t.G);
     if (nn <= kKeySmall) return;
     *t.n_slots = min(*t.n_slots + nn, t.G);
@@ -417,7 +347,7 @@ __global__ void k_key_mark_done(KeyTable t) {
 // the first tuple of each freshly assigned key records the slot's key
 __global__ void __launch_bounds__(256)
 k_key_map(const long long* __restrict__ keys, KeyTable t, uint32_t* __restrict__ out, int64_t S,
-          int32_t* __restrict__ gcnt, unsigned long long* __restrict__ bad) {
+          int32_t* __restrict__ gcnt, unsigned long long* __restrict__ bad) { SS_PDL_ENTRY();
     const int np = *t.n_pend;
     const int stride = gridDim.x * blockDim.x;
     // a warp's iterations stay converged (the bound is rounded up to warps)

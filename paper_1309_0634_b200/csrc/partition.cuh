@@ -47,7 +47,7 @@ template <bool SMEM>
 __global__ void __launch_bounds__(512)
 k_count(const uint32_t* __restrict__ groups, int64_t n, uint32_t G, int64_t S, int64_t chunk,
         int32_t* __restrict__ gcnt, unsigned long long* __restrict__ bad, int vec_ok,
-        const int32_t* __restrict__ hot_of, const int32_t* __restrict__ hot_g, int n_hot) {
+        const int32_t* __restrict__ hot_of, const int32_t* __restrict__ hot_g, int n_hot) { SS_PDL_ENTRY();
     extern __shared__ int32_t sh_hist[];
     const int64_t c0 = (int64_t)blockIdx.x * chunk;
     if (c0 >= n) return;
@@ -136,7 +136,7 @@ __device__ __forceinline__ void count_range(const uint32_t* __restrict__ groups,
 
 __global__ void __launch_bounds__(512)
 k_count_rows(const uint32_t* __restrict__ groups, int64_t n, uint32_t G, int64_t S, int32_t* __restrict__ gcnt,
-             unsigned long long* __restrict__ bad, int vec_ok) {
+             unsigned long long* __restrict__ bad, int vec_ok) { SS_PDL_ENTRY();
     extern __shared__ int32_t sh_hist[];
     const int64_t c0 = (int64_t)blockIdx.x * S;
     const int64_t c1 = min(n, c0 + S);
@@ -153,7 +153,7 @@ k_count_rows(const uint32_t* __restrict__ groups, int64_t n, uint32_t G, int64_t
 __global__ void __launch_bounds__(256)
 k_hot_select(const int32_t* __restrict__ gcount, uint32_t G, long long thr, int32_t* __restrict__ hot_of,
              int32_t* __restrict__ hot_g, int* __restrict__ n_hot_dev, const unsigned long long* __restrict__ bad,
-             int32_t* __restrict__ ent_words = nullptr, const int32_t* __restrict__ slot_ent = nullptr) {
+             int32_t* __restrict__ ent_words = nullptr, const int32_t* __restrict__ slot_ent = nullptr) { SS_PDL_ENTRY();
     if (*bad != (unsigned long long)kNoBad) return;
     for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < G; g += gridDim.x * blockDim.x) {
         int h = -1;
@@ -210,7 +210,7 @@ k_batch_stats(int32_t* __restrict__ gcnt, int n_chunk, uint32_t G, const int32_t
               unsigned long long* __restrict__ tpt, unsigned long long* __restrict__ touched,
               const unsigned long long* __restrict__ bad, const int32_t* __restrict__ fill, int64_t W,
               unsigned long long* __restrict__ alg_bytes, int nodrop, int32_t* __restrict__ gpre = nullptr,
-              uint32_t* __restrict__ pwork = nullptr, int* __restrict__ any_dead = nullptr) {
+              uint32_t* __restrict__ pwork = nullptr, int* __restrict__ any_dead = nullptr) { SS_PDL_ENTRY();
     extern __shared__ uint32_t sh_tpt[];     // per-CTA partial loads (< 2^31)
     __shared__ uint32_t sh_live[kMaxChunkWords];
     if (*bad != (unsigned long long)kNoBad) return;
@@ -297,7 +297,7 @@ k_batch_stats_cols(int32_t* __restrict__ gcnt, int n_chunk, uint32_t G, const in
                    uint32_t* __restrict__ chunk_live, unsigned long long* __restrict__ tpt,
                    unsigned long long* __restrict__ touched, const unsigned long long* __restrict__ bad,
                    const int32_t* __restrict__ fill, int64_t W, unsigned long long* __restrict__ alg_bytes,
-                   int nodrop, int32_t* __restrict__ gpre, uint32_t* __restrict__ pwork, int* __restrict__ any_dead) {
+                   int nodrop, int32_t* __restrict__ gpre, uint32_t* __restrict__ pwork, int* __restrict__ any_dead) { SS_PDL_ENTRY();
     extern __shared__ uint32_t sh_tpt[];     // per-CTA partial loads (< 2^31), then partition work
     __shared__ uint32_t sh_live[kMaxChunkWords];
     __shared__ int32_t sh_part[kStatsWarps][32];
@@ -405,7 +405,7 @@ struct DigitPlan {
 
 __global__ void __launch_bounds__(1024)
 k_scan_reduce(const int32_t* __restrict__ gcnt, uint32_t G, int32_t* __restrict__ bsum, int nblk,
-              DigitPlan plan, uint32_t* __restrict__ dhist, const unsigned long long* __restrict__ bad) {
+              DigitPlan plan, uint32_t* __restrict__ dhist, const unsigned long long* __restrict__ bad) { SS_PDL_ENTRY();
     __shared__ uint32_t sh_dh[2][kMaxBins];
     __shared__ int32_t sh_red[33];
     if (*bad != (unsigned long long)kNoBad) return;
@@ -448,7 +448,7 @@ k_scan_top(int32_t* __restrict__ bsum, int nblk, DigitPlan plan, uint32_t* __res
            const unsigned long long* __restrict__ bad, int32_t* __restrict__ n_live,
            uint32_t* __restrict__ chunk_live = nullptr, int n_chunk = 0, int32_t* __restrict__ lc = nullptr,
            int32_t* __restrict__ n_lc = nullptr, int32_t* __restrict__ btile = nullptr,
-           uint32_t* __restrict__ ep_dev = nullptr) {
+           uint32_t* __restrict__ ep_dev = nullptr) { SS_PDL_ENTRY();
     __shared__ int32_t sh_red[33];
     __shared__ uint32_t sh_ured[33];
     if (ep_dev && blockIdx.x == 0 && threadIdx.x == 0) *ep_dev = epoch_next(*ep_dev);
@@ -513,7 +513,7 @@ __global__ void __launch_bounds__(1024)
 k_scan_small(const int32_t* __restrict__ row, uint32_t G, DigitPlan plan, uint32_t* __restrict__ dhist,
              int32_t* __restrict__ gstart, const unsigned long long* __restrict__ bad, int32_t* __restrict__ n_live,
              uint32_t* __restrict__ chunk_live, int n_chunk, int32_t* __restrict__ lc, int32_t* __restrict__ n_lc,
-             int32_t* __restrict__ btile, uint32_t* __restrict__ ep_dev, int* __restrict__ sub_shift_dev = nullptr) {
+             int32_t* __restrict__ btile, uint32_t* __restrict__ ep_dev, int* __restrict__ sub_shift_dev = nullptr) { SS_PDL_ENTRY();
     __shared__ uint32_t sh_dh[2][kMaxBins];
     __shared__ int32_t sh_red[33];
     __shared__ uint32_t sh_ured[33];
@@ -617,7 +617,7 @@ k_scan_small(const int32_t* __restrict__ row, uint32_t G, DigitPlan plan, uint32
 // block-local exclusive scan + block base -> gstart[s][g]
 __global__ void __launch_bounds__(1024)
 k_scan_down(const int32_t* __restrict__ gcnt, uint32_t G, const int32_t* __restrict__ bsum, int nblk,
-            int32_t* __restrict__ gstart, const unsigned long long* __restrict__ bad) {
+            int32_t* __restrict__ gstart, const unsigned long long* __restrict__ bad) { SS_PDL_ENTRY();
     __shared__ int32_t sh_red[33];
     if (*bad != (unsigned long long)kNoBad) return;
     const int s = blockIdx.y;
@@ -684,7 +684,7 @@ struct SortSeg {
 __global__ void __launch_bounds__(1024)
 k_chunk_hist(const int32_t* __restrict__ gcnt, uint32_t G, const int32_t* __restrict__ lc,
              const int32_t* __restrict__ n_lc, uint32_t m0, int nb, uint32_t* __restrict__ H0,
-             const unsigned long long* __restrict__ bad) {
+             const unsigned long long* __restrict__ bad) { SS_PDL_ENTRY();
     extern __shared__ uint32_t sh_h[];
     if (*bad != (unsigned long long)kNoBad) return;
     const int i = blockIdx.x;
@@ -709,7 +709,7 @@ k_chunk_hist(const int32_t* __restrict__ gcnt, uint32_t G, const int32_t* __rest
 __global__ void __launch_bounds__(1024)
 k_chunk_scan(const uint32_t* __restrict__ H0, const int32_t* __restrict__ n_lc, int nb,
              const uint32_t* __restrict__ bin_base, uint32_t* __restrict__ cbase,
-             const unsigned long long* __restrict__ bad) {
+             const unsigned long long* __restrict__ bad) { SS_PDL_ENTRY();
     if (*bad != (unsigned long long)kNoBad) return;
     const int d = blockIdx.x * (blockDim.x >> 5) + warp_id();
     if (d >= nb) return;
@@ -746,7 +746,7 @@ k_sort_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
             const uint32_t* __restrict__ ep_dev, uint32_t ep_off, uint32_t* __restrict__ ticket,
             const unsigned long long* __restrict__ bad,
             int stream_in, const int32_t* __restrict__ dmap = nullptr,
-            const int32_t* __restrict__ n_dev = nullptr, SortSeg seg = SortSeg{}) {
+            const int32_t* __restrict__ n_dev = nullptr, SortSeg seg = SortSeg{}) { SS_PDL_ENTRY();
     constexpr int BINS = 1 << RB;
     constexpr int NW = kSortThreads / 32;
     constexpr int BPT = (BINS + kSortThreads - 1) / kSortThreads;   // bins owned per thread
@@ -1072,7 +1072,7 @@ constexpr int kSubUnitsMax = 2 * 2 * kNumSM;        // (n_lc << ss) < 2 x 296
 __global__ void __launch_bounds__(512)
 k_sub_hist(const uint32_t* __restrict__ keys, int64_t n, int chunk_shift, const int32_t* __restrict__ lc,
            const int32_t* __restrict__ n_lc, const int* __restrict__ sub_shift_dev, uint32_t G,
-           int32_t* __restrict__ subh, const unsigned long long* __restrict__ bad) {
+           int32_t* __restrict__ subh, const unsigned long long* __restrict__ bad) { SS_PDL_ENTRY();
     extern __shared__ int32_t sh_hist[];
     if (*bad != (unsigned long long)kNoBad) return;
     const int ss = *sub_shift_dev;
@@ -1095,7 +1095,7 @@ k_sub_hist(const uint32_t* __restrict__ keys, int64_t n, int chunk_shift, const 
 __global__ void __launch_bounds__(256)
 k_sub_scan(const int32_t* __restrict__ gpre, const int32_t* __restrict__ lc, const int32_t* __restrict__ n_lc,
            const int* __restrict__ sub_shift_dev, uint32_t G, const int32_t* __restrict__ subh,
-           int32_t* __restrict__ gsub, const unsigned long long* __restrict__ bad) {
+           int32_t* __restrict__ gsub, const unsigned long long* __restrict__ bad) { SS_PDL_ENTRY();
     if (*bad != (unsigned long long)kNoBad) return;
     const int ss = *sub_shift_dev;
     if (ss == 0) return;
@@ -1123,7 +1123,7 @@ k_rank_place(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin, 
              int32_t* __restrict__ vout, int64_t n, int chunk_shift, const int32_t* __restrict__ lc,
              const int32_t* __restrict__ n_lc, const int32_t* __restrict__ gpre, const int32_t* __restrict__ gstart,
              uint32_t G, const int32_t* __restrict__ n_live, const unsigned long long* __restrict__ bad,
-             const int* __restrict__ sub_shift_dev = nullptr, const int32_t* __restrict__ gsub = nullptr) {
+             const int* __restrict__ sub_shift_dev = nullptr, const int32_t* __restrict__ gsub = nullptr) { SS_PDL_ENTRY();
     extern __shared__ __align__(16) unsigned char rank_sm[];
     uint32_t* stage_k = (uint32_t*)rank_sm;                            // [warp][stage][kRankSub]
     int32_t* stage_v = (int32_t*)(stage_k + kRankWarps * kRankStages * kRankSub);
@@ -1257,7 +1257,7 @@ k_rank_place(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin, 
 // histogram of destination owners for the multi-GPU route (<= 16 owners)
 __global__ void __launch_bounds__(256)
 k_owner_hist(const uint32_t* __restrict__ keys, int64_t n, uint32_t G, const int32_t* __restrict__ owner,
-             unsigned long long* __restrict__ counts, unsigned long long* __restrict__ bad) {
+             unsigned long long* __restrict__ counts, unsigned long long* __restrict__ bad) { SS_PDL_ENTRY();
     __shared__ uint32_t h[16];
     if (threadIdx.x < 16) h[threadIdx.x] = 0;
     __syncthreads();

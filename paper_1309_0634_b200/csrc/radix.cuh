@@ -67,6 +67,7 @@ struct OsArgs {
     uint32_t mask;
     uint32_t* hist;             // [tiles][BINS] counts -> output bases
     uint32_t* bsum;             // [blocks][BINS]
+    uint32_t* dtot;             // [BINS] digit totals
     // pass 0: drop never-stored tuples (live = kept counts per count chunk)
     const int32_t* live;
     int chunk_shift;
@@ -84,7 +85,7 @@ __device__ __forceinline__ bool os_live(const OsArgs& a, bool drop, int64_t i, u
 
 template <int BITS>
 __global__ void __launch_bounds__(kOsThreads)
-k_os_up(OsArgs a) {
+k_os_up(OsArgs a) { SS_PDL_ENTRY();
     constexpr int BINS = 1 << BITS;
     constexpr int NH = BINS <= 128 ? kOsWarps : 4;      // sub-histograms (one per warp for narrow digits)
     __shared__ uint32_t wh[NH][BINS];
@@ -123,7 +124,7 @@ k_os_up(OsArgs a) {
 // (t / BINS) -- 1024 / BINS slices of the block's tiles
 template <int BITS>
 __global__ void __launch_bounds__(1024)
-k_os_red(OsArgs a) {
+k_os_red(OsArgs a) { SS_PDL_ENTRY();
     constexpr int BINS = 1 << BITS, J = 1024 / BINS, per = kOsBlkTiles / J;
     __shared__ uint32_t part[J][BINS];
     if (*a.bad != (unsigned long long)kNoBad) return;
@@ -146,46 +147,49 @@ k_os_red(OsArgs a) {
     }
 }
 
-// per digit: exclusive scan over the blocks, then the digit bases
+// per digit: exclusive scan of the block sums (in place) and the digit's
+// total (dtot).  CTA x owns 32 digits (lane = digit); its 32 warps own
+// contiguous block ranges, so every load is a coalesced 128-byte row
+// segment and the scan over the blocks is one pass plus a cross-warp
+// prefix (a thread per digit walking all blocks serially cost ~29 us per
+// pass at C4).  The digit bases (scan over the totals) are formed by every
+// k_os_down CTA from dtot.
 template <int BITS>
-__global__ void __launch_bounds__(1 << BITS)
-k_os_top(OsArgs a) {
-    constexpr int BINS = 1 << BITS;
-    __shared__ uint32_t red[33];
+__global__ void __launch_bounds__(1024)
+k_os_top(OsArgs a) { SS_PDL_ENTRY();
+    __shared__ uint32_t part[32][33];
     if (*a.bad != (unsigned long long)kNoBad) return;
     const int64_t ntile = (os_count(a) + kOsTile - 1) / kOsTile;
     const int nblk = (int)((ntile + kOsBlkTiles - 1) / kOsBlkTiles);
-    const int d = threadIdx.x;
-    // 16 block sums in flight per thread (a serial load -> store chain over
-    // 128 blocks cost ~40 us)
-    constexpr int U = 16;
-    uint32_t run = 0;
-    for (int b0 = 0; b0 < nblk; b0 += U) {
-        uint32_t c[U];
-#pragma unroll
-        for (int q = 0; q < U; ++q) c[q] = (b0 + q < nblk) ? a.bsum[(int64_t)(b0 + q) * BINS + d] : 0u;
-#pragma unroll
-        for (int q = 0; q < U; ++q) {
-            if (b0 + q < nblk) a.bsum[(int64_t)(b0 + q) * BINS + d] = run;
-            run += c[q];
-        }
+    const unsigned lane = lane_id(), w = warp_id();
+    const int d = (int)blockIdx.x * 32 + (int)lane;
+    constexpr int BINS = 1 << BITS;
+    const int per = (nblk + 31) / 32;
+    const int b0 = min(nblk, (int)w * per), b1 = min(nblk, b0 + per);
+    uint32_t s = 0;
+    for (int b = b0; b < b1; ++b) s += a.bsum[(int64_t)b * BINS + d];
+    part[w][lane] = s;
+    __syncthreads();
+    uint32_t run = 0, tot = 0;
+#pragma unroll 8
+    for (int q = 0; q < 32; ++q) {
+        const uint32_t v = part[q][lane];
+        run += (q < (int)w) ? v : 0u;
+        tot += v;
     }
-    uint32_t tot;
-    const uint32_t dbase = block_excl_scan(run, red, &tot);
-    for (int b0 = 0; b0 < nblk; b0 += U) {
-        uint32_t c[U];
-#pragma unroll
-        for (int q = 0; q < U; ++q) c[q] = (b0 + q < nblk) ? a.bsum[(int64_t)(b0 + q) * BINS + d] : 0u;
-#pragma unroll
-        for (int q = 0; q < U; ++q)
-            if (b0 + q < nblk) a.bsum[(int64_t)(b0 + q) * BINS + d] = c[q] + dbase;
+    for (int b = b0; b < b1; ++b) {
+        uint32_t* p = a.bsum + (int64_t)b * BINS + d;
+        const uint32_t c = *p;
+        *p = run;
+        run += c;
     }
+    if (w == 0) a.dtot[d] = tot;
 }
 
 // per tile and digit: global output base (in place over hist)
 template <int BITS>
 __global__ void __launch_bounds__(1024)
-k_os_down(OsArgs a) {
+k_os_down(OsArgs a) { SS_PDL_ENTRY();
     constexpr int BINS = 1 << BITS, J = 1024 / BINS, per = kOsBlkTiles / J;
     __shared__ uint32_t part[J][BINS];
     if (*a.bad != (unsigned long long)kNoBad) return;
@@ -199,8 +203,17 @@ k_os_down(OsArgs a) {
         if (t < ntile) s += a.hist[t * BINS + d];
     }
     part[j][d] = s;
+    // digit bases: exclusive scan of the digit totals
+    __shared__ uint32_t sdb[BINS];
+    __shared__ uint32_t red[33];
+    {
+        const uint32_t t = threadIdx.x < BINS ? a.dtot[threadIdx.x] : 0u;
+        uint32_t all;
+        const uint32_t ex = block_excl_scan(t, red, &all);
+        if (threadIdx.x < BINS) sdb[threadIdx.x] = ex;
+    }
     __syncthreads();
-    uint32_t run = a.bsum[(int64_t)blockIdx.x * BINS + d];
+    uint32_t run = a.bsum[(int64_t)blockIdx.x * BINS + d] + sdb[d];
     for (int q = 0; q < j; ++q) run += part[q][d];
     for (int q = 0; q < per; ++q) {
         const int64_t t = tb + j * per + q;
@@ -243,7 +256,7 @@ __device__ __forceinline__ void os_wait(uint64_t* bar, unsigned parity) {
 // bulk copies are in flight while the current one is ranked and written
 template <int BITS>
 __global__ void __launch_bounds__(kOsThreads, 1)
-k_os_pass(OsArgs a) {
+k_os_pass(OsArgs a) { SS_PDL_ENTRY();
     constexpr int BINS = 1 << BITS;
     using OsSmem = ss::OsSmem<BITS>;
     extern __shared__ __align__(16) unsigned char osm[];

@@ -48,7 +48,7 @@ struct SplitScratch {
 // accumulate per CTA in shared memory (P <= 4096) before one flush.
 __global__ void __launch_bounds__(256)
 k_split_hot(const int32_t* __restrict__ gcount, uint32_t G, const int32_t* __restrict__ pmap, long long hot_min,
-            int maxS, SplitScratch sc, int P, const unsigned long long* __restrict__ bad) {
+            int maxS, SplitScratch sc, int P, const unsigned long long* __restrict__ bad) { SS_PDL_ENTRY();
     extern __shared__ uint32_t sh_base[];
     if (*bad != (unsigned long long)kNoBad) return;
     for (int i = threadIdx.x; i < P; i += blockDim.x) sh_base[i] = 0;
@@ -75,7 +75,7 @@ k_split_hot(const int32_t* __restrict__ gcount, uint32_t G, const int32_t* __res
 // moves and write the next plan.  One CTA.
 __global__ void __launch_bounds__(1024)
 k_split_fill(const int32_t* __restrict__ gcount, const long long* __restrict__ loads, int P, int maxS,
-             SplitScratch sc, SplitPlan prev, SplitPlan nx, const unsigned long long* __restrict__ bad) {
+             SplitScratch sc, SplitPlan prev, SplitPlan nx, const unsigned long long* __restrict__ bad) { SS_PDL_ENTRY();
     extern __shared__ long long fsm[];
     long long* hot_c = fsm;                 // [maxS]
     long long* hot_s = hot_c + maxS;        // [maxS + 1] axis starts
@@ -212,7 +212,7 @@ k_split_fill(const int32_t* __restrict__ gcount, const long long* __restrict__ l
 // Loads of the current batch under the current plan (report / max-mean).
 __global__ void __launch_bounds__(256)
 k_split_loads(const int32_t* __restrict__ gcount, uint32_t G, const int32_t* __restrict__ pmap, int P,
-              SplitPlan cur, unsigned long long* __restrict__ loads, const unsigned long long* __restrict__ bad) {
+              SplitPlan cur, unsigned long long* __restrict__ loads, const unsigned long long* __restrict__ bad) { SS_PDL_ENTRY();
     extern __shared__ uint32_t sh_load[];
     if (*bad != (unsigned long long)kNoBad) return;
     for (int i = threadIdx.x; i < P; i += blockDim.x) sh_load[i] = 0;

@@ -49,7 +49,7 @@ __device__ __forceinline__ SwView sw_view(const StreamWinArgs& a) {
 
 // tuples leaving the window: before the new tuples overwrite their slots
 __global__ void __launch_bounds__(256)
-k_sw_evict(StreamWinArgs a) {
+k_sw_evict(StreamWinArgs a) { SS_PDL_ENTRY();
     if (*a.bad != (unsigned long long)kNoBad) return;
     const SwView w = sw_view(a);
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < w.n_evict; j += (int64_t)gridDim.x * blockDim.x) {
@@ -63,14 +63,14 @@ k_sw_evict(StreamWinArgs a) {
 
 // validation of the whole batch (first bad tuple wins) -- before any state change
 __global__ void __launch_bounds__(256)
-k_sw_check(StreamWinArgs a) {
+k_sw_check(StreamWinArgs a) { SS_PDL_ENTRY();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x)
         if (a.keys[i] >= a.G) atomicMin(a.bad, (unsigned long long)i);
 }
 
 // tuples entering the window
 __global__ void __launch_bounds__(256)
-k_sw_add(StreamWinArgs a) {
+k_sw_add(StreamWinArgs a) { SS_PDL_ENTRY();
     if (*a.bad != (unsigned long long)kNoBad) return;
     const SwView w = sw_view(a);
     const int64_t lo = a.n - a.m;
@@ -88,7 +88,7 @@ k_sw_add(StreamWinArgs a) {
 
 // MIN / MAX of touched groups: reset, then one pass over the window
 __global__ void __launch_bounds__(256)
-k_sw_mm_reset(StreamWinArgs a) {
+k_sw_mm_reset(StreamWinArgs a) { SS_PDL_ENTRY();
     if (*a.bad != (unsigned long long)kNoBad) return;
     for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < a.G; g += gridDim.x * blockDim.x)
         if (a.touched[g]) {
@@ -98,7 +98,7 @@ k_sw_mm_reset(StreamWinArgs a) {
 }
 
 __global__ void __launch_bounds__(256)
-k_sw_mm_scan(StreamWinArgs a) {
+k_sw_mm_scan(StreamWinArgs a) { SS_PDL_ENTRY();
     if (*a.bad != (unsigned long long)kNoBad) return;
     const SwView w = sw_view(a);
     for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < w.fill_after; s += (int64_t)gridDim.x * blockDim.x) {
@@ -111,7 +111,7 @@ k_sw_mm_scan(StreamWinArgs a) {
 }
 
 // the batch is in: move the ring cursors (a rejected batch changes nothing)
-__global__ void k_sw_advance(StreamWinArgs a) {
+__global__ void k_sw_advance(StreamWinArgs a) { SS_PDL_ENTRY();
     if (*a.bad != (unsigned long long)kNoBad) return;
     const SwView w = sw_view(a);
     a.cur[0] = (w.head + a.m) % a.W;
@@ -139,7 +139,7 @@ struct StreamEmitArgs {
 };
 
 __global__ void __launch_bounds__(256)
-k_sw_emit(StreamEmitArgs a) {
+k_sw_emit(StreamEmitArgs a) { SS_PDL_ENTRY();
     if (*a.bad != (unsigned long long)kNoBad) return;
     const unsigned lane = lane_id();
     for (uint32_t g0 = blockIdx.x * blockDim.x; g0 < a.G; g0 += gridDim.x * blockDim.x) {

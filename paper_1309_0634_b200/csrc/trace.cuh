@@ -79,7 +79,7 @@ struct TraceArgs {
 // phase 1: per tuple delta (heads carry the group's prior sum), tile-local
 // segmented scan, tile aggregate
 __global__ void __launch_bounds__(kTraceTile)
-k_trace_local(TraceArgs a) {
+k_trace_local(TraceArgs a) { SS_PDL_ENTRY();
     __shared__ SegVal sh[33];
     if (*a.bad != (unsigned long long)kNoBad) return;
     const int n = *a.n_dev;
@@ -107,7 +107,7 @@ k_trace_local(TraceArgs a) {
 // phase 2: exclusive segmented scan over the tile aggregates (one CTA,
 // rounds of 1024 tiles): tile[t] becomes the carry-in of tile t
 __global__ void __launch_bounds__(1024)
-k_trace_tiles(TraceArgs a) {
+k_trace_tiles(TraceArgs a) { SS_PDL_ENTRY();
     __shared__ SegVal sh[33];
     __shared__ SegVal sinc[1024];
     if (*a.bad != (unsigned long long)kNoBad) return;
@@ -130,7 +130,7 @@ k_trace_tiles(TraceArgs a) {
 
 // phase 3: add each tile's carry-in to its elements before the tile's first head
 __global__ void __launch_bounds__(kTraceTile)
-k_trace_apply(TraceArgs a) {
+k_trace_apply(TraceArgs a) { SS_PDL_ENTRY();
     if (*a.bad != (unsigned long long)kNoBad) return;
     const int n = *a.n_dev;
     const int64_t i = (int64_t)blockIdx.x * kTraceTile + threadIdx.x;

@@ -70,7 +70,7 @@ struct IngestArgs {
 // CTA finds its slot with one load; n_used = CTAs used (<= total + P).
 // work_p comes from k_batch_stats; it is cleared for the next batch.
 __global__ void __launch_bounds__(1024)
-k_cta_map(uint32_t* __restrict__ pwork, int P, int total, int4* __restrict__ map, int* __restrict__ n_used) {
+k_cta_map(uint32_t* __restrict__ pwork, int P, int total, int4* __restrict__ map, int* __restrict__ n_used) { SS_PDL_ENTRY();
     __shared__ unsigned long long sh_sum[32];
     __shared__ int32_t sh_red[33];
     const int t = threadIdx.x;
@@ -126,7 +126,7 @@ __device__ unsigned long long g_k4_prof[8];
 #endif
 
 __global__ void __launch_bounds__(kIngestThreads, 2)
-k_ingest(IngestArgs a) {
+k_ingest(IngestArgs a) { SS_PDL_ENTRY();
     extern __shared__ __align__(16) unsigned char ingest_sm[];
     int64_t* m_off = (int64_t*)ingest_sm;
     uint32_t* m_dlo = (uint32_t*)(m_off + kMemberChunk);
@@ -476,7 +476,7 @@ struct FinalizeArgs {
 };
 
 __global__ void __launch_bounds__(256)
-k_finalize(FinalizeArgs a) {
+k_finalize(FinalizeArgs a) { SS_PDL_ENTRY();
     if (*a.bad != (unsigned long long)kNoBad) return;
     const unsigned lane = lane_id();
     const int W = (int)a.W;
@@ -574,7 +574,7 @@ constexpr int kMMChunk = 4096;
 constexpr int64_t kMMSumMinW = 1 << 17;
 
 __global__ void k_rescan_reset(const int4* __restrict__ rescan, const unsigned* __restrict__ n_rescan,
-                               int32_t* __restrict__ mn, int32_t* __restrict__ mx) {
+                               int32_t* __restrict__ mn, int32_t* __restrict__ mx) { SS_PDL_ENTRY();
     const unsigned n = *n_rescan;
     for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         mn[rescan[i].x] = 0x7fffffff;
@@ -604,7 +604,7 @@ __device__ __forceinline__ int2 cta_minmax(const int32_t* __restrict__ r, int64_
 __global__ void __launch_bounds__(256)
 k_minmax_rescan(const int4* __restrict__ rescan, const unsigned* __restrict__ n_rescan,
                 const int32_t* __restrict__ ring, const int64_t* __restrict__ off, int64_t W,
-                int32_t* __restrict__ mn, int32_t* __restrict__ mx) {
+                int32_t* __restrict__ mn, int32_t* __restrict__ mx) { SS_PDL_ENTRY();
     const unsigned n = *n_rescan;
     const int64_t nch = (W + kRescanChunk - 1) / kRescanChunk;
     for (int64_t c = blockIdx.x; c < (int64_t)n * nch; c += gridDim.x) {
@@ -620,7 +620,7 @@ k_minmax_rescan(const int4* __restrict__ rescan, const unsigned* __restrict__ n_
 
 __global__ void k_rescan_rows(const int4* __restrict__ rescan, const unsigned* __restrict__ n_rescan,
                               const int32_t* __restrict__ mn, const int32_t* __restrict__ mx,
-                              int32_t* __restrict__ r_mn, int32_t* __restrict__ r_mx) {
+                              int32_t* __restrict__ r_mn, int32_t* __restrict__ r_mx) { SS_PDL_ENTRY();
     const unsigned n = *n_rescan;
     for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const int4 e = rescan[i];
@@ -636,7 +636,7 @@ __global__ void k_rescan_rows(const int4* __restrict__ rescan, const unsigned* _
 __global__ void __launch_bounds__(256)
 k_mm_refresh(const int4* __restrict__ rescan, const unsigned* __restrict__ n_rescan,
              const int32_t* __restrict__ ring, const int64_t* __restrict__ off, int64_t W,
-             const int32_t* __restrict__ sum_idx, const uint8_t* __restrict__ sum_valid, int2* __restrict__ sums) {
+             const int32_t* __restrict__ sum_idx, const uint8_t* __restrict__ sum_valid, int2* __restrict__ sums) { SS_PDL_ENTRY();
     const unsigned n = *n_rescan;
     const int64_t nch = (W + kMMChunk - 1) / kMMChunk;
     for (int64_t c = blockIdx.x; c < (int64_t)n * nch; c += gridDim.x) {
@@ -658,7 +658,7 @@ k_mm_refresh(const int4* __restrict__ rescan, const unsigned* __restrict__ n_res
 __global__ void __launch_bounds__(256)
 k_mm_fold(const int4* __restrict__ rescan, const unsigned* __restrict__ n_rescan, int64_t W,
           const int32_t* __restrict__ sum_idx, uint8_t* __restrict__ sum_valid, const int2* __restrict__ sums,
-          int32_t* __restrict__ mn, int32_t* __restrict__ mx, int32_t* __restrict__ r_mn, int32_t* __restrict__ r_mx) {
+          int32_t* __restrict__ mn, int32_t* __restrict__ mx, int32_t* __restrict__ r_mn, int32_t* __restrict__ r_mx) { SS_PDL_ENTRY();
     __shared__ int32_t s_mn[8], s_mx[8];
     const unsigned n = *n_rescan;
     const int64_t nch = (W + kMMChunk - 1) / kMMChunk;
@@ -711,7 +711,7 @@ __global__ void __launch_bounds__(256)
 k_reserve(const int32_t* __restrict__ gcount, uint32_t G, int64_t W, const int32_t* __restrict__ fill,
           int64_t* __restrict__ off, int32_t* __restrict__ cap, unsigned long long* __restrict__ pool_top,
           unsigned long long pool_cap, int* __restrict__ oom, RingCopy* __restrict__ copies,
-          unsigned* __restrict__ n_copies, const unsigned long long* __restrict__ bad) {
+          unsigned* __restrict__ n_copies, const unsigned long long* __restrict__ bad) { SS_PDL_ENTRY();
     __shared__ long long sh_red[33];
     __shared__ unsigned long long sh_base;
     __shared__ unsigned sh_cbase;
@@ -775,7 +775,7 @@ k_reserve(const int32_t* __restrict__ gcount, uint32_t G, int64_t W, const int32
 constexpr int kShortCopy = 64;
 
 __global__ void __launch_bounds__(256)
-k_ring_copy(const RingCopy* __restrict__ copies, const unsigned* __restrict__ n_copies, int32_t* __restrict__ ring) {
+k_ring_copy(const RingCopy* __restrict__ copies, const unsigned* __restrict__ n_copies, int32_t* __restrict__ ring) { SS_PDL_ENTRY();
     const unsigned n = *n_copies;
     const unsigned lane = lane_id();
     const unsigned nwarps = gridDim.x * (blockDim.x >> 5);

@@ -49,7 +49,6 @@ from . import _lib as L
 from .errors import DataError, ExecutionError, InvalidConfigError
 from .stream_engine import StreamEngine, _ptr
 
-_CTRL = 3        # control words per peer: tuples, bad-tuple index (or -1), migration words
 
 
 def _is_gloo(group) -> bool:
@@ -197,10 +196,11 @@ class ShardedEngine:
             raise ExecutionError("migration blob too small")
         if recv_w.any() or send_w.any():
             blob_in = exchange_words(self._blob, send_w, recv_w, self.group)
-            seg = np.zeros(self.world + 1, dtype=np.int64)
-            np.cumsum(recv_w, out=seg[1:])
-            self.local._check(self.local._lib.ss_import_blob_dev(self.local._h, _ptr(blob_in)[0], _ptr(seg)[0],
-                                                                 self.world, min(256, self._moves.numel() // 4)))
+            if recv_w.any():
+                seg = np.zeros(self.world + 1, dtype=np.int64)
+                np.cumsum(recv_w, out=seg[1:])
+                self.local._check(self.local._lib.ss_import_blob_dev(self.local._h, _ptr(blob_in)[0], _ptr(seg)[0],
+                                                                     self.world, min(256, self._moves.numel() // 4)))
             self._mig_words.zero_()
             self._keep_blob = blob_in
         send_c, recv_c = sent[:, 0], got[:, 0]
