@@ -604,8 +604,11 @@ k_scan_small(const int32_t* __restrict__ row, uint32_t G, DigitPlan plan, uint32
             *n_lc = tot;
             if (sub_shift_dev) {
                 // sub-chunks until the live units fill two CTAs per SM
+                // (only with fewer live chunks than half the SMs: at C2 all
+                // 256 chunks are live, and 2 sub-chunks each cost more in
+                // the extra count and cursor set-up than the finer grid won)
                 int ssh = 0;
-                while (tot > 0 && (tot << ssh) < 2 * kNumSM && ssh < 4) ++ssh;
+                while (tot > 0 && tot < kNumSM / 2 && (tot << ssh) < 2 * kNumSM && ssh < 4) ++ssh;
                 *sub_shift_dev = ssh;
             }
         }
@@ -1104,10 +1107,14 @@ k_sub_scan(const int32_t* __restrict__ gpre, const int32_t* __restrict__ lc, con
         const int li = (int)(i / G);
         const uint32_t g = (uint32_t)(i - (int64_t)li * G);
         int32_t run = gpre[(int64_t)lc[li] * G + g];
-        for (int sb = 0; sb < (1 << ss); ++sb) {
-            const int64_t u = ((int64_t)li << ss) | sb;
-            gsub[u * G + g] = run;
-            if (run >= 0) run += subh[u * G + g];
+        const int64_t u0 = (int64_t)li << ss;
+        int32_t h[16];
+#pragma unroll
+        for (int sb = 0; sb < 16; ++sb) h[sb] = sb < (1 << ss) ? subh[(u0 + sb) * G + g] : 0;   // all in flight
+#pragma unroll
+        for (int sb = 0; sb < 16; ++sb) {
+            if (sb < (1 << ss)) gsub[(u0 + sb) * G + g] = run;
+            if (run >= 0) run += h[sb];
         }
     }
 }

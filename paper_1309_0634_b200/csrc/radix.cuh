@@ -288,6 +288,9 @@ k_os_pass(OsArgs a) { SS_PDL_ENTRY();
     unsigned phase[2] = {0u, 0u};
     int k = 0;
     for (int64_t tile = blockIdx.x; tile * kOsTile < n; tile += gridDim.x, ++k) {
+#ifdef SS_SORT_PROF
+    long long _pt = clock64();
+#endif
     const int st = k & 1;
     uint32_t* sk = (uint32_t*)(osm + OsSmem::keys + (size_t)st * kOsTile * 4);
     int32_t* sv = (int32_t*)(osm + OsSmem::vals + (size_t)st * kOsTile * 4);
@@ -303,6 +306,7 @@ k_os_pass(OsArgs a) { SS_PDL_ENTRY();
             sv[i] = a.vin[t0 + i];
         }
     }
+    SS_PT(0);
     // the other stage was last read by the previous tile (closing barrier)
     if (threadIdx.x == 0) issue(tile + gridDim.x, st ^ 1);
     uint16_t* my = wh + w * BINS;
@@ -337,6 +341,7 @@ k_os_pass(OsArgs a) { SS_PDL_ENTRY();
         __syncwarp();
     }
     __syncthreads();
+    SS_PT(1);
     // per (digit, warp) exclusive offsets: thread (d = t >> 3, j = t & 7)
     // owns warps [4j, 4j+4) of digit d; the 8 threads of a digit are
     // consecutive lanes, so one shuffle scan gives their prefix
@@ -365,6 +370,7 @@ k_os_pass(OsArgs a) { SS_PDL_ENTRY();
         if (j == J - 1) lst[d] = inc;    // the digit's tile count (scanned below)
     }
     __syncthreads();
+    SS_PT(2);
     if (threadIdx.x < BINS) {
         // exclusive scan of the digit counts (BINS threads, named barrier)
         const uint32_t cnt = lst[threadIdx.x];
@@ -379,6 +385,7 @@ k_os_pass(OsArgs a) { SS_PDL_ENTRY();
         if (threadIdx.x == BINS - 1) s_total = ls + cnt;
     }
     __syncthreads();
+    SS_PT(3);
     // local sort by digit into shared memory (every item is in registers)
 #pragma unroll
     for (int r = 0; r < kOsItems; ++r) {
@@ -390,6 +397,7 @@ k_os_pass(OsArgs a) { SS_PDL_ENTRY();
         }
     }
     __syncthreads();
+    SS_PT(4);
     // contiguous runs per digit to global memory (the tile's kept tuples)
     const int total = (int)s_total;
     for (int i = threadIdx.x; i < total; i += blockDim.x) {
@@ -399,6 +407,7 @@ k_os_pass(OsArgs a) { SS_PDL_ENTRY();
         if (a.kout) a.kout[pos] = k;
     }
     __syncthreads();                     // this stage and the histograms are free again
+    SS_PT(5);
     }
 }
 

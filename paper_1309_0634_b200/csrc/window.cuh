@@ -345,8 +345,79 @@ k_ingest(IngestArgs a) { SS_PDL_ENTRY();
             }
         }
 
-        // ---- short members (< 32 values): kILP packed values per thread ----
+        // ---- short members (< 32 values): kILP consecutive values per thread
         SS_PT4(3);
+#ifndef SS_K4_SHORT_LANES
+        // Thread-contiguous: one binary search per thread (not per value),
+        // member fields re-read from shared memory only when the member
+        // changes, and the delta / MIN / MAX of each member run accumulated
+        // in registers -- one shared flush per (thread, member) instead of
+        // a segmented warp reduction per value round.
+        for (int base = csub * kIngestThreads * kILP; base < s_total; base += cstride * kIngestThreads * kILP) {
+            const int t0 = base + (int)threadIdx.x * kILP;
+            if (t0 >= s_total) continue;
+            int l = 0;                                 // last member with m_scan[l] <= t0
+#pragma unroll
+            for (int step = kMemberChunk / 2; step >= 1; step >>= 1) {
+                const int c = l + step;
+                if (c < m && m_scan[c] <= t0) l = c;
+            }
+            int f_scan = m_scan[l], f_next = m_scan[l + 1];
+            int mi[kILP], sl[kILP];
+            int32_t v[kILP], old[kILP];
+#pragma unroll
+            for (int u = 0; u < kILP; ++u) {
+                const int t = t0 + u;
+                mi[u] = -1;
+                sl[u] = 0;
+                v[u] = 0;
+                old[u] = 0;
+                if (t < s_total) {
+                    if (t >= f_next) {
+                        while (m_scan[l + 1] <= t) ++l;
+                        f_scan = m_scan[l];
+                        f_next = m_scan[l + 1];
+                    }
+                    const int rr = t - f_scan;
+                    mi[u] = l;
+                    v[u] = a.vals[m_start[l] + rr];
+                    int q = m_q0[l] + rr;
+                    if (q >= W) q -= W;
+                    int s2 = m_s0[l] + rr;
+                    if (s2 >= W) s2 -= W;
+                    sl[u] = s2;
+                    if (q < m_f0[l]) old[u] = a.ring[m_off[l] + s2];
+                }
+            }
+            long long d = 0;
+            int32_t mnv = 0x7fffffff, mxv = (int32_t)0x80000000;
+            int cur = mi[0];
+#pragma unroll
+            for (int u = 0; u < kILP; ++u) {
+                if (mi[u] < 0) break;
+                if (mi[u] != cur) {
+                    add_delta(&m_dlo[cur], &m_dhi[cur], d);
+                    if (a.minmax) {
+                        atomicMin(&m_min[cur], mnv);
+                        atomicMax(&m_max[cur], mxv);
+                    }
+                    cur = mi[u];
+                    d = 0;
+                    mnv = 0x7fffffff;
+                    mxv = (int32_t)0x80000000;
+                }
+                a.ring[m_off[mi[u]] + sl[u]] = v[u];
+                d += (long long)v[u] - (long long)old[u];
+                mnv = min(mnv, v[u]);
+                mxv = max(mxv, v[u]);
+            }
+            add_delta(&m_dlo[cur], &m_dhi[cur], d);
+            if (a.minmax) {
+                atomicMin(&m_min[cur], mnv);
+                atomicMax(&m_max[cur], mxv);
+            }
+        }
+#else
         for (int base = csub * kIngestThreads * kILP; base < s_total; base += cstride * kIngestThreads * kILP) {
             int mi[kILP], rr[kILP];
             int32_t v[kILP], old[kILP];
@@ -414,6 +485,7 @@ k_ingest(IngestArgs a) { SS_PDL_ENTRY();
                 }
             }
         }
+#endif
         __syncthreads();
         SS_PT4(4);
 

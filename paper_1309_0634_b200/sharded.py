@@ -174,6 +174,32 @@ class ShardedEngine:
                                                            _ptr(self._route_cnt)[0]))
         return self._rec[:n], self._route_cnt
 
+    def _migrate(self, send_w, recv_w):
+        """Ship and import the window state of the groups the last GPU-level
+        policy moved (sizes from the control exchange)."""
+        if (send_w < 0).any() or (recv_w < 0).any():
+            raise ExecutionError("migration blob too small")
+        if not (recv_w.any() or send_w.any()):
+            return
+        blob_in = exchange_words(self._blob, send_w, recv_w, self.group)
+        if recv_w.any():
+            seg = np.zeros(self.world + 1, dtype=np.int64)
+            np.cumsum(recv_w, out=seg[1:])
+            self.local._check(self.local._lib.ss_import_blob_dev(self.local._h, _ptr(blob_in)[0], _ptr(seg)[0],
+                                                                 self.world, min(256, self._moves.numel() // 4)))
+        self._mig_words.zero_()
+        self._keep_blob = blob_in
+
+    def settle(self):
+        """Complete the migration the last batch's GPU-level moves started
+        (a collective: every rank calls it).  Needed only to read the window
+        state between batches -- the next step does it on its own."""
+        import torch
+        z = torch.zeros(self.world, dtype=torch.int64, device=self.dev)
+        ctrl = torch.stack([z, z - 1, self._mig_words], dim=1)
+        sent, got = exchange_control(ctrl, self.group)
+        self._migrate(sent[:, 2], got[:, 2])
+
     # -- one global batch ------------------------------------------------------
     def step(self, groups, attrs, balancer=None, gpu_balancer=None):
         """groups/attrs: this rank's contiguous slice of the global batch
@@ -191,18 +217,7 @@ class ShardedEngine:
                 raise DataError(f"tuple {i} has group {g}, outside [0, {self.n_groups})")
             r = int(np.flatnonzero(bad >= 0)[0])
             raise DataError(f"rank {r} rejected this batch (a tuple outside [0, {self.n_groups}))")
-        send_w, recv_w = sent[:, 2], got[:, 2]
-        if (send_w < 0).any() or (recv_w < 0).any():
-            raise ExecutionError("migration blob too small")
-        if recv_w.any() or send_w.any():
-            blob_in = exchange_words(self._blob, send_w, recv_w, self.group)
-            if recv_w.any():
-                seg = np.zeros(self.world + 1, dtype=np.int64)
-                np.cumsum(recv_w, out=seg[1:])
-                self.local._check(self.local._lib.ss_import_blob_dev(self.local._h, _ptr(blob_in)[0], _ptr(seg)[0],
-                                                                     self.world, min(256, self._moves.numel() // 4)))
-            self._mig_words.zero_()
-            self._keep_blob = blob_in
+        self._migrate(sent[:, 2], got[:, 2])
         send_c, recv_c = sent[:, 0], got[:, 0]
         mine = exchange_records(rec, send_c, recv_c, self.group)
         self._keep_recv = mine

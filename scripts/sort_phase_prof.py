@@ -28,7 +28,12 @@ prof(out, 1)
 for i in range(6):
     eng.step(*bs[i % 2], bal)
 prof(out, 1)
-names = (["claim+zero", "stage+loads", "rank", "bins+publish+scan", "lookback", "scatter+write"] if fn == "ss_debug_sort_prof" else ["prologue", "stage A", "scan B", "long units", "short units", "fold"])
+if fn != "ss_debug_sort_prof":
+    names = ["prologue", "stage A", "scan B", "long units", "short units", "fold"]
+elif os.environ.get("SS_PROF_OS"):
+    names = ["tile copy wait", "zero+rank", "warp offsets", "digit scan+bases", "local scatter", "write-out"]
+else:
+    names = ["claim+zero", "stage+loads", "rank", "bins+publish+scan", "lookback", "scatter+write"]
 tot = sum(out[i] for i in range(6))
 for i, n in enumerate(names):
     print(f"{n:20s} {out[i] / 6 / 1e6:9.2f} Mcycles/step (summed over CTAs) {100 * out[i] / max(1, tot):5.1f}%")

@@ -54,6 +54,7 @@ def _worker(rank, world, port, q, G, W, B, nb, gpu_policy, drift):
             lo, hi = rank * len(b) // world, (rank + 1) * len(b) // world
             eng.step(b.groups[lo:hi].astype(np.int32), b.attrs[lo:hi].astype(np.int32), bal, gbal)
             n_moves += len(eng.last_gpu_moves)
+        eng.settle()                                    # the last batch's moves land
         snap = eng.local.snapshot()
         owned = np.flatnonzero(eng.owner == rank)
         contents = {int(g): eng.local.contents(int(g)).tolist() for g in owned if g % 13 == 0}
