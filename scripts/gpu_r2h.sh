@@ -7,7 +7,7 @@ F="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -shared -Xco
 nvcc $F -DSS_K4_SHORT_LANES paper_1309_0634_b200/csrc/engine.cu -o $L/libss_b200_oldshort.so > $O/b1.log 2>&1
 nvcc $F -DSS_SORT_PROF paper_1309_0634_b200/csrc/engine.cu -o $L/libss_b200_sortprof.so > $O/b2.log 2>&1
 nvcc $F -DSS_K4_PROF paper_1309_0634_b200/csrc/engine.cu -o $L/libss_b200_k4prof.so > $O/b3.log 2>&1
-for c in c4 c2 c3 c5; do
+for c in c4 c2 c1 c5; do
   timeout 400 python bench.py --config $c --steps 10 --warmup 3 --no-cpu > $O/bench_$c.log 2>&1
   SS_B200_LIB=$L/libss_b200_oldshort.so timeout 400 python bench.py --config $c --steps 10 --warmup 3 --no-cpu > $O/bench_${c}_old.log 2>&1
 done
