@@ -30,12 +30,20 @@ namespace ss {
 
 constexpr unsigned long long kEmptyKey = 0x8000000000000000ull;   // INT64_MIN
 
+#ifdef SS_KEY_HASH32
+// (A/B variant) one 32-bit multiply: fold, Fibonacci-scramble, spread
+__device__ __forceinline__ unsigned long long key_hash(unsigned long long x) {
+    const uint32_t f = ((uint32_t)x ^ (uint32_t)(x >> 32)) * 0x9E3779B1u;
+    return (unsigned long long)(f ^ (f >> 15)) * 0x85EBCA6Bu;
+}
+#else
 __device__ __forceinline__ unsigned long long key_hash(unsigned long long x) {
     x ^= x >> 30; x *= 0xbf58476d1ce4e5b9ull;
     x ^= x >> 27; x *= 0x94d049bb133111ebull;
     x ^= x >> 31;
     return x;
 }
+#endif
 
 struct __align__(16) KEntry {
     unsigned long long key;     // kEmptyKey = free

@@ -310,7 +310,8 @@ k_os_pass(OsArgs a) { SS_PDL_ENTRY();
     // the other stage was last read by the previous tile (closing barrier)
     if (threadIdx.x == 0) issue(tile + gridDim.x, st ^ 1);
     uint16_t* my = wh + w * BINS;
-    for (int i = lane; i < BINS; i += 32) my[i] = 0;
+    // 16-byte stores (a 10-bit digit's per-warp histogram is 2 KB)
+    for (int i = lane; i < BINS / 8; i += 32) reinterpret_cast<uint4*>(my)[i] = make_uint4(0u, 0u, 0u, 0u);
     __syncthreads();                     // plain loads and zeroed histograms visible
     // rank: warp w owns tuples [w*256, (w+1)*256), round r = w*256 + 32r + lane
     uint32_t key[kOsItems];

@@ -347,7 +347,6 @@ k_ingest(IngestArgs a) { SS_PDL_ENTRY();
 
         // ---- short members (< 32 values): kILP consecutive values per thread
         SS_PT4(3);
-#ifndef SS_K4_SHORT_LANES
         // Thread-contiguous: one binary search per thread (not per value),
         // member fields re-read from shared memory only when the member
         // changes, and the delta / MIN / MAX of each member run accumulated
@@ -417,75 +416,6 @@ k_ingest(IngestArgs a) { SS_PDL_ENTRY();
                 atomicMax(&m_max[cur], mxv);
             }
         }
-#else
-        for (int base = csub * kIngestThreads * kILP; base < s_total; base += cstride * kIngestThreads * kILP) {
-            int mi[kILP], rr[kILP];
-            int32_t v[kILP], old[kILP];
-#pragma unroll
-            for (int u = 0; u < kILP; ++u) {
-                const int t = base + u * kIngestThreads + threadIdx.x;
-                mi[u] = -1;
-                rr[u] = 0;
-                if (t < s_total) {
-                    int l = 0;                 // last member with m_scan[l] <= t
-#pragma unroll
-                    for (int step = kMemberChunk / 2; step >= 1; step >>= 1) {
-                        const int c = l + step;
-                        if (c < m && m_scan[c] <= t) l = c;
-                    }
-                    mi[u] = l;
-                    rr[u] = t - m_scan[l];
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < kILP; ++u) v[u] = (mi[u] >= 0) ? a.vals[m_start[mi[u] < 0 ? 0 : mi[u]] + rr[u]] : 0;
-#pragma unroll
-            for (int u = 0; u < kILP; ++u) {
-                old[u] = 0;
-                if (mi[u] >= 0) {
-                    int q = m_q0[mi[u]] + rr[u];
-                    if (q >= W) q -= W;
-                    int sl = m_s0[mi[u]] + rr[u];
-                    if (sl >= W) sl -= W;
-                    if (q < m_f0[mi[u]]) old[u] = a.ring[m_off[mi[u]] + sl];
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < kILP; ++u)
-                if (mi[u] >= 0) {
-                    int sl = m_s0[mi[u]] + rr[u];
-                    if (sl >= W) sl -= W;
-                    a.ring[m_off[mi[u]] + sl] = v[u];
-                }
-#pragma unroll
-            for (int u = 0; u < kILP; ++u) {
-                const bool valid = mi[u] >= 0;
-                const long long d = valid ? (long long)v[u] - (long long)old[u] : 0;
-                const unsigned key = valid ? (unsigned)mi[u] : 0xffffffffu;
-                // members are contiguous lane runs (t grows with the lane), so
-                // the run of a lane comes from one shuffle and one ballot
-                // instead of a MATCH (whose cost grows with distinct values)
-                const unsigned prev = __shfl_up_sync(SS_FULL, key, 1);
-                const unsigned heads = __ballot_sync(SS_FULL, lane == 0 || prev != key);
-                const unsigned le = (lane == 31) ? SS_FULL : ((2u << lane) - 1u);
-                const unsigned start = 31u - __clz(heads & le);
-                const unsigned above = heads & ~le;
-                const unsigned seg_end = above ? (unsigned)(__ffs(above) - 2) : 31u;
-                const unsigned peers = (seg_end == 31u ? SS_FULL : ((2u << seg_end) - 1u)) & ~((1u << start) - 1u);
-                const long long tot = seg_sum(d, seg_end);
-                const bool leader = valid && lane == (unsigned)(__ffs(peers) - 1);
-                if (leader) add_delta(&m_dlo[mi[u]], &m_dhi[mi[u]], tot);
-                if (a.minmax && valid) {
-                    const int32_t mnv = __reduce_min_sync(peers, v[u]);
-                    const int32_t mxv = __reduce_max_sync(peers, v[u]);
-                    if (leader) {
-                        atomicMin(&m_min[mi[u]], mnv);
-                        atomicMax(&m_max[mi[u]], mxv);
-                    }
-                }
-            }
-        }
-#endif
         __syncthreads();
         SS_PT4(4);
 

@@ -167,10 +167,18 @@ def _attrs_i32(attrs):
     return attrs.to(torch.int32)
 
 
-def hash_lists(n_groups: int, n_partitions: int):
-    """Static hash partitioning: group g -> mix(g) mod P, ids ascending
-    inside each partition (BASELINE C1 "static hash partitioning")."""
-    g = np.arange(n_groups, dtype=np.uint64)
+def hash_lists(n_groups: int, n_partitions: int, block: int | None = None):
+    """Static hash partitioning: group g -> mix(g // block) mod P, ids
+    ascending inside each partition (BASELINE C1 "static hash partitioning").
+
+    Large domains hash blocks of 8 consecutive ids (one 32-byte sector of
+    every per-group int32 array) instead of single ids, so the window
+    update's per-member state reads of a partition come 8 to a sector; small
+    domains (fewer than 64 groups per partition) hash single ids to keep
+    every partition populated."""
+    if block is None:
+        block = 8 if n_groups >= 64 * n_partitions else 1
+    g = np.arange(n_groups, dtype=np.uint64) // np.uint64(block)
     with np.errstate(over="ignore"):
         x = (g + np.uint64(0x9E3779B97F4A7C15)) * np.uint64(0xBF58476D1CE4E5B9)
         x ^= x >> np.uint64(31)
