@@ -66,7 +66,7 @@ typedef struct {
                             /* 1: the stream's last W tuples, grouped (policy 'no')    */
     int32_t  device;        /* CUDA ordinal                                           */
     int32_t  reserved;
-    int64_t  max_batch;     /* largest n passed to ss_step (0: 1<<24)                 */
+    int64_t  max_batch;     /* largest n passed to ss_step (0: 1<<24; <= 2^30)        */
     int64_t  sub_batch;     /* count chunk: tuple granularity at which never-stored   */
                             /* tuples are dropped (power of two >= 2^16; 0: auto)     */
     int64_t  pool_values;   /* ring pool capacity in values (0: auto)                 */

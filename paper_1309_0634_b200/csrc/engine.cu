@@ -676,6 +676,12 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
         *out = e;
         return rc;
     }
+    if (cfg->max_batch > (int64_t(1) << 30)) {
+        // batch ranks, ring positions and window fills are summed in 32 bits
+        int rc = fail(e, SS_E_CONFIG, "max_batch must be <= 2^30");
+        *out = e;
+        return rc;
+    }
     if (cfg->n_partitions < 1 || cfg->n_partitions > 4096) {
         int rc = fail(e, SS_E_CONFIG, "n_partitions must be in [1, 4096]");
         *out = e;

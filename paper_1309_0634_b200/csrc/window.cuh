@@ -226,8 +226,13 @@ k_ingest(IngestArgs a) { SS_PDL_ENTRY();
                     const int jb = b + first;              // batch rank of the first stored value
                     w = r_hi - first;
                     m_start[i] = a.gstart[g] + first;
-                    m_q0[i] = (int)(((int64_t)f0 + jb) % W);
-                    m_s0[i] = (int)(((int64_t)a.next_pos[g] + f0 + jb) % W);
+                    // 32-bit unsigned remainders (f0, next_pos < W <= 2^30
+                    // and jb < 2^31 - 2^30 keep the sums in range; a 64-bit
+                    // % is a ~70-instruction sequence)
+                    const uint32_t uw = (uint32_t)W;
+                    const uint32_t q0 = (uint32_t)f0 + (uint32_t)jb;
+                    m_q0[i] = (int)(q0 % uw);
+                    m_s0[i] = (int)(((uint32_t)a.next_pos[g] + q0) % uw);
                     m_f0[i] = (K >= W) ? 0 : f0;           // k >= W: nothing old survives
                     m_off[i] = a.off[g];
                     m_dlo[i] = 0;
