@@ -202,3 +202,30 @@ def test_large_partition_count_policies():
             assert eng.last_moves() == [tuple(m) for m in v.moves] and rep.scanned == v.scanned
             asg = O.apply_move_list(asg, v.moves)
         eng.close()
+
+
+def test_sweep_window_passes_and_gpu_csv_columns(tmp_path):
+    """The reference's window_passes sweep axis (harness.py:143-156): the SIM
+    backend's modelled makespan grows with the passes, no-balance points are
+    pinned to 1; the CSV keeps the reference schema and adds the device
+    columns (step time, tuples/s, algorithmic GB/s, partition makespan)."""
+    import csv
+    spec = D.DatasetSpec(D.DatasetKind.ZIPF, 60_000, 500, 1.1, 3)
+    base = ss.RunConfig(dataset=spec, batch_size=20_000, window=64, grid_size=1, block_size=16,
+                        balancer=ss.BalancerConfig(ss.Policy.NO_BALANCE, 100, 0.5))
+    reps = ss.sweep(base, "window_passes", [1, 3])
+    assert reps[1].total_makespan > reps[0].total_makespan
+    assert all(r.normalized_throughput == 1.0 for r in reps)
+    path = tmp_path / "run.csv"
+    ss.write_csv(reps[0], path)
+    rows = list(csv.reader(open(path)))
+    assert tuple(rows[0][:10]) == ("iter", "policy", "grid", "makespan", "imbalance", "moves", "scanned",
+                                   "tuples", "throughput", "normalized_throughput")
+    hdr = rows[0]
+    for r in rows[1:-1]:
+        assert float(r[hdr.index("gpu_step_ns")]) > 0
+        assert float(r[hdr.index("gpu_tuples_per_s")]) > 0
+        assert float(r[hdr.index("gpu_alg_gbs")]) > 0
+    assert rows[-1][0] == "total" and float(rows[-1][hdr.index("gpu_tuples_per_s")]) > 0
+    with pytest.raises(ss.InvalidConfigError):
+        ss.sweep(base, "bogus", [1])
