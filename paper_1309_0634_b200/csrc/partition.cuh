@@ -1145,7 +1145,7 @@ k_rank_small(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin, 
              int32_t* __restrict__ vout, int64_t n, int chunk_shift, const int32_t* __restrict__ lc,
              const int32_t* __restrict__ n_lc, const int32_t* __restrict__ gpre, const int32_t* __restrict__ gstart,
              uint32_t G, const int32_t* __restrict__ n_live, const unsigned long long* __restrict__ bad,
-             const int* __restrict__ sub_shift_dev, const int32_t* __restrict__ gsub) {
+             const int* __restrict__ sub_shift_dev, const int32_t* __restrict__ gsub) { SS_PDL_ENTRY();
     extern __shared__ __align__(16) unsigned char rs_sm[];
     const uint32_t pitch = rs_pitch(G);
     uint32_t* cur = (uint32_t*)rs_sm;                         // [pitch]

@@ -49,3 +49,40 @@ def test_no_cpu_fallback_when_library_missing(tmp_path, monkeypatch):
     monkeypatch.setattr(_lib, "_lib", None)
     with pytest.raises(ExecutionError):
         _lib.load()
+
+
+def test_every_kernel_waits_for_its_programmatic_predecessor():
+    """Every launch is a programmatic dependent launch (engine.cu
+    ss_launch), so every __global__ function must begin with SS_PDL_ENTRY()
+    (griddepcontrol.wait) before it reads what the previous kernel wrote."""
+    import glob
+    import re
+    root = os.path.join(ROOT, "paper_1309_0634_b200", "csrc")
+    missing = []
+    for f in sorted(glob.glob(os.path.join(root, "*.cu*"))):
+        s = open(f).read()
+        for m in re.finditer(r"__global__", s):
+            line = s[s.rfind("\n", 0, m.start()) + 1:m.start()]
+            if line.strip().startswith("//"):
+                continue
+            i = m.end()
+            # skip __launch_bounds__(...) and find the parameter list
+            p = s.index("(", i)
+            while s[:p].rstrip().endswith("__launch_bounds__"):
+                depth, j = 0, p
+                while True:
+                    depth += {"(": 1, ")": -1}.get(s[j], 0)
+                    if depth == 0:
+                        break
+                    j += 1
+                p = s.index("(", j + 1)
+            depth, j = 0, p
+            while True:
+                depth += {"(": 1, ")": -1}.get(s[j], 0)
+                if depth == 0:
+                    break
+                j += 1
+            body = s[s.index("{", j):s.index("{", j) + 40]
+            if "SS_PDL_ENTRY()" not in body:
+                missing.append(os.path.basename(f) + ":" + s[s.rfind(" ", 0, p) + 1:p])
+    assert not missing, missing
