@@ -392,14 +392,6 @@ static void launch_balance(ss_engine* e, BalanceArgs& a, cudaStream_t st) {
 using RankKernel = void (*)(const uint32_t*, const int32_t*, uint32_t*, int32_t*, int64_t, int, const int32_t*,
                             const int32_t*, const int32_t*, const int32_t*, uint32_t, const int32_t*,
                             const unsigned long long*, const int*, const int32_t*);
-static RankKernel rank_small_kernel(int bits) {
-    switch (bits) {
-        case 9: return k_rank_small<9>;
-        case 10: return k_rank_small<10>;
-        case 11: return k_rank_small<11>;
-        default: return k_rank_small<8>;
-    }
-}
 static RankKernel rank_kernel(int bits) {
     switch (bits) {
         case 0: case 1: case 2: case 3: case 4: case 5: case 6: case 7: case 8: return k_rank_place<8>;
@@ -1017,9 +1009,6 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
         const RankKernel rk = b ? rank_kernel(b) : k_rank_place<0>;
         SS_CUDA(e, cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rank_smem_bytes(kRankMaxG)));
     }
-    for (int b = 8; b <= 11; ++b)
-        SS_CUDA(e, cudaFuncSetAttribute(rank_small_kernel(b), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)rank_small_smem_bytes(kRankSmallG)));
     SS_CUDA(e, cudaFuncSetAttribute(k_balance<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBalSmemMax));
     SS_CUDA(e, cudaFuncSetAttribute(k_balance<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBalSmemMax));
     SS_CUDA(e, cudaFuncSetAttribute(k_balance<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBalSmemMax));
@@ -1325,10 +1314,11 @@ static int launch_place_step(ss_engine* e, const uint32_t* dk, const int32_t* dv
     if (e->rank_place) {
         // one CTA per live chunk, cursors from the chunk prefix (k_batch_stats)
         static const int use_match = getenv("SS_B200_RANK_MATCH") ? atoi(getenv("SS_B200_RANK_MATCH")) : 0;
-        // small domains: the chain-free per-warp-histogram variant
-        const bool small = (uint32_t)e->G <= kRankSmallG && !use_match;
-        auto kern = use_match ? k_rank_place<0> : small ? rank_small_kernel(bits_for(e->G)) : rank_kernel(bits_for(e->G));
-        const size_t rsm = small ? rank_small_smem_bytes((uint32_t)e->G) : rank_smem_bytes((uint32_t)e->G);
+        // (a chain-free variant with per-warp histograms of all G groups
+        // per 4096-tuple piece, for G <= 2048, measured slower at C1: 21.4
+        // against 16.7 us, and was dropped)
+        auto kern = use_match ? k_rank_place<0> : rank_kernel(bits_for(e->G));
+        const size_t rsm = rank_smem_bytes((uint32_t)e->G);
         // sub-chunk prefixes (no-ops unless k_scan_small chose sub-chunks)
         ss_note_launch(), ss_launch(k_sub_hist, kSubUnitsMax, 512, e->G * 4, e->st, dk, n, cs, e->lc, e->n_lc, e->sub_shift,
                                                                             (uint32_t)e->G, e->subh, e->bad);

@@ -1123,110 +1123,6 @@ __host__ __device__ constexpr size_t rank_smem_bytes(uint32_t G) {
     return (size_t)kRankWarps * kRankStages * kRankSub * 8 + (size_t)G * 4;
 }
 
-// Small domains (G <= 2048): the same placement without the cross-warp
-// cursor chain.  The chunk (or sub-chunk) is walked in pieces of 4096
-// tuples; every warp counts its 256 tuples into a private u16 histogram
-// of all G groups (ranks inside the warp in arrival order come from the
-// matches), one exclusive scan over the 16 warps per group gives each
-// warp's base, and the tuples are written from cursor + warp base + rank;
-// the cursors then advance by the piece's totals.  With one 4096-tuple
-// sub-chunk per CTA (C1) the chain version serialised all 16 warps.
-constexpr uint32_t kRankSmallG = 2048;
-constexpr int kRSPiece = kRankWarps * kRankSub;       // 4096
-
-__host__ __device__ constexpr uint32_t rs_pitch(uint32_t G) { return (G + 7u) & ~7u; }
-__host__ __device__ constexpr size_t rank_small_smem_bytes(uint32_t G) {
-    return (size_t)rs_pitch(G) * 4 + (size_t)kRankWarps * rs_pitch(G) * 2;
-}
-
-template <int BITS>
-__global__ void __launch_bounds__(kRankWarps * 32)
-k_rank_small(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin, uint32_t* __restrict__ kout,
-             int32_t* __restrict__ vout, int64_t n, int chunk_shift, const int32_t* __restrict__ lc,
-             const int32_t* __restrict__ n_lc, const int32_t* __restrict__ gpre, const int32_t* __restrict__ gstart,
-             uint32_t G, const int32_t* __restrict__ n_live, const unsigned long long* __restrict__ bad,
-             const int* __restrict__ sub_shift_dev, const int32_t* __restrict__ gsub) { SS_PDL_ENTRY();
-    extern __shared__ __align__(16) unsigned char rs_sm[];
-    const uint32_t pitch = rs_pitch(G);
-    uint32_t* cur = (uint32_t*)rs_sm;                         // [pitch]
-    uint16_t* wh = (uint16_t*)(cur + pitch);                  // [warp][pitch]
-    if (*bad != (unsigned long long)kNoBad) return;
-    if (*n_live == 0) return;
-    const int ss = sub_shift_dev ? *sub_shift_dev : 0;
-    if ((int)blockIdx.x >= (*n_lc << ss)) return;
-    const int64_t c = lc[blockIdx.x >> ss];
-    const int sb = (int)blockIdx.x & ((1 << ss) - 1);
-    const int32_t* pre = ss ? gsub + (int64_t)blockIdx.x * G : gpre + c * (int64_t)G;
-    const int64_t c0 = (c << chunk_shift) + ((int64_t)sb << (chunk_shift - ss));
-    if (c0 >= n) return;
-    const int cn = (int)min64((int64_t)1 << (chunk_shift - ss), n - c0);
-    for (uint32_t g = threadIdx.x; g < G; g += blockDim.x) {
-        const int32_t pv = pre[g];
-        cur[g] = pv < 0 ? 0x80000000u : (uint32_t)(gstart[g] + pv);
-    }
-    const int w = (int)warp_id();
-    const unsigned lane = lane_id(), lt = lanemask_lt();
-    uint16_t* my = wh + w * pitch;
-    for (int p0 = 0; p0 < cn; p0 += kRSPiece) {
-        for (uint32_t i = threadIdx.x; i < kRankWarps * pitch / 8; i += blockDim.x)
-            reinterpret_cast<uint4*>(wh)[i] = make_uint4(0u, 0u, 0u, 0u);
-        uint32_t key[kRankItems];
-        int32_t val[kRankItems];
-        uint16_t rk[kRankItems];
-#pragma unroll
-        for (int r = 0; r < kRankItems; ++r) {
-            const int it = p0 + w * kRankSub + r * 32 + (int)lane;     // arrival order: warp, round, lane
-            const bool valid = it < cn;
-            key[r] = valid ? kin[c0 + it] : 0xffffffffu;
-            val[r] = valid ? vin[c0 + it] : 0;
-        }
-        __syncthreads();                          // histograms zeroed (and cursors initialised)
-#pragma unroll
-        for (int r = 0; r < kRankItems; ++r) {
-            const bool valid = key[r] != 0xffffffffu;
-            const unsigned peers = (r & 1) ? __match_any_sync(SS_FULL, key[r]) : match_bits<BITS>(key[r], valid);
-            uint16_t before = 0;
-            if (valid) before = my[key[r]];
-            __syncwarp();
-            rk[r] = (uint16_t)(before + __popc(peers & lt));
-            if (valid && lane == 31u - __clz(peers)) my[key[r]] = (uint16_t)(before + __popc(peers));
-            __syncwarp();
-        }
-        __syncthreads();
-        // per group: exclusive scan over the warps (in place), piece total
-        uint32_t tot[(kRankSmallG + kRankWarps * 32 - 1) / (kRankWarps * 32)];
-#pragma unroll
-        for (int q = 0; q < (int)(sizeof(tot) / sizeof(tot[0])); ++q) {
-            const uint32_t g = threadIdx.x + q * blockDim.x;
-            uint32_t run = 0;
-            if (g < G) {
-#pragma unroll
-                for (int v = 0; v < kRankWarps; ++v) {
-                    const uint32_t cnt = wh[v * pitch + g];
-                    wh[v * pitch + g] = (uint16_t)run;
-                    run += cnt;
-                }
-            }
-            tot[q] = run;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int r = 0; r < kRankItems; ++r) {
-            if (key[r] == 0xffffffffu) continue;
-            const uint32_t base = cur[key[r]];
-            if (base & 0x80000000u) continue;     // a never-stored run
-            const uint32_t pos = base + my[key[r]] + rk[r];
-            vout[pos] = val[r];
-            if (kout) kout[pos] = key[r];
-        }
-        __syncthreads();                          // cursors and histograms read
-#pragma unroll
-        for (int q = 0; q < (int)(sizeof(tot) / sizeof(tot[0])); ++q) {
-            const uint32_t g = threadIdx.x + q * blockDim.x;
-            if (g < G) cur[g] += tot[q];
-        }
-    }
-}
 
 // BITS > 0: group matching from BITS ballots (keys < 2^BITS); 0: MATCH
 template <int BITS>
