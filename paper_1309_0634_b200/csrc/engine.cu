@@ -392,6 +392,12 @@ static void launch_balance(ss_engine* e, BalanceArgs& a, cudaStream_t st) {
 using RankKernel = void (*)(const uint32_t*, const int32_t*, uint32_t*, int32_t*, int64_t, int, const int32_t*,
                             const int32_t*, const int32_t*, const int32_t*, uint32_t, const int32_t*,
                             const unsigned long long*, const int*, const int32_t*);
+// grid of a per-group kernel (a thread per group and round): one group per
+// thread up to 16 CTAs per SM -- G = 1M groups on 2 x 148 CTAs left each
+// thread a chain of ~13 dependent load rounds (k_finalize 47 us at C4)
+static unsigned group_grid(int64_t G) {
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>((G + 255) / 256, 16 * kNumSM));
+}
 static RankKernel rank_kernel(int bits) {
     switch (bits) {
         case 0: case 1: case 2: case 3: case 4: case 5: case 6: case 7: case 8: return k_rank_place<8>;
@@ -1469,7 +1475,7 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
         if (e->G > 16384) {
             // hot cache for the next batch's count: > 1/(4 kHotCache) of the batch
             SS_CUDA(e, cudaMemsetAsync(e->n_hot_dev, 0, 4, e->st));
-            ss_note_launch(), ss_launch(k_hot_select, 2 * kNumSM, 256, 0, e->st, e->gcount, (uint32_t)e->G,
+            ss_note_launch(), ss_launch(k_hot_select, group_grid(e->G), 256, 0, e->st, e->gcount, (uint32_t)e->G,
                                                         std::max<long long>(32, n / (4 * kHotCache)), e->hot_of,
                                                         e->hot_g, e->n_hot_dev, e->bad,
                                                         e->keys64 ? (int32_t*)e->kt.ent : nullptr, e->kt.slot_ent);
@@ -1539,7 +1545,7 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
     if (!e->dense) {
         ProfScope ps(e, SS_K_INGEST, e->st);
         SS_CUDA(e, cudaMemsetAsync(e->n_copies, 0, 4, e->st));
-        ss_note_launch(), ss_launch(k_reserve, 2 * kNumSM, 256, 0, e->st, e->gcount, (uint32_t)e->G, e->W, e->fill, e->off, e->cap,
+        ss_note_launch(), ss_launch(k_reserve, group_grid(e->G), 256, 0, e->st, e->gcount, (uint32_t)e->G, e->W, e->fill, e->off, e->cap,
                                                  e->pool_top, e->pool_cap, e->oom, e->copies, e->n_copies, e->bad);
         ss_note_launch(), ss_launch(k_ring_copy, 8 * kNumSM, 256, 0, e->st, e->copies, e->n_copies, e->ring);
     }
@@ -1576,8 +1582,10 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
         e->cur_stage = -1;
     }
     {
-        ProfScope ps(e, SS_K_INGEST, e->st);
+        // (the wait for the split plan is outside the timed scope: the
+        // class time is the window update's own device time)
         if (split) SS_CUDA(e, cudaStreamWaitEvent(e->st, e->ev_bal, 0));
+        ProfScope ps(e, SS_K_INGEST, e->st);
         IngestArgs a = ingest_args(e, plan);
         // CTAs per partition: with hot-key splitting (or no balancer, static
         // partitions) one resident wave (2 per SM) is best; when the
@@ -1631,7 +1639,7 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
         f.sum_valid = e->sum_valid;
         f.n_sum = e->n_sum;
         f.bad = e->bad;
-        ss_note_launch(), ss_launch(k_finalize, 2 * kNumSM, 256, 0, e->st, f);
+        ss_note_launch(), ss_launch(k_finalize, group_grid(e->G), 256, 0, e->st, f);
         if (e->minmax) {
             if (e->sums) {
                 ss_note_launch(), ss_launch(k_mm_refresh, 8 * kNumSM, 256, 0, e->st, e->rescan, e->n_rescan, e->ring, e->off, e->W,

@@ -505,7 +505,8 @@ k_finalize(FinalizeArgs a) { SS_PDL_ENTRY();
         const int p0 = a.next_pos[g];
         const int fill = (int)min64(tot, W);
         a.fill[g] = fill;
-        a.next_pos[g] = (int32_t)((p0 + max64(tot - W, 0)) % W);
+        // 32-bit remainder: p0 < W <= 2^30 and tot - W <= K <= 2^30
+        a.next_pos[g] = (int32_t)(((uint32_t)p0 + (uint32_t)max64(tot - W, 0)) % (uint32_t)W);
         const long long d = a.bdelta[g];
         const long long s = (K >= W) ? d : a.wsum[g] + d;
         a.wsum[g] = s;

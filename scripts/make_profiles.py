@@ -1,11 +1,15 @@
-"""Summarise gpurun_out/round (scripts/gpu_round.sh) into profiles/:
-launch lists per config, ncu --set full summaries, per-launch DRAM traffic."""
+"""Summarise a measurement pass (scripts/gpu_round.sh -> gpurun_out/round,
+scripts/gpu_r2p.sh -> gpurun_out/round2) into profiles/: launch lists per
+config, ncu --set full summaries, per-launch DRAM traffic.
+
+    python scripts/make_profiles.py r2 round2"""
 import csv, io, json, os, shutil, subprocess, sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-R = os.path.join(ROOT, "gpurun_out", "round")
-P = os.path.join(ROOT, "profiles")
 tag = sys.argv[1] if len(sys.argv) > 1 else "r1"
+R = os.path.join(ROOT, "gpurun_out", sys.argv[2] if len(sys.argv) > 2 else "round")
+P = os.path.join(ROOT, "profiles")
+CONFIGS = ["c1", "c2", "c3", "c4", "c5"]
 
 
 def run(*a):
@@ -19,13 +23,13 @@ md = [f"# {tag} profiles (B200, sm_100a)\n",
       "launches: per-kernel SHARES carry over to the timed run, absolute times do not).",
       "Full captures: `ncu --set full --clock-control none --import-source on`,",
       "steady state (after warm-up).\n"]
-for c in ["c1", "c2", "c3"]:
+for c in CONFIGS:
     f = os.path.join(R, f"launches_{c}.csv")
     if os.path.exists(f):
         shutil.copy(f, os.path.join(P, f"{tag}_launches_{c}.csv"))
         md.append(f"## Launch list per step, {c}\n\n```\n{run('python', 'scripts/launch_summary.py', f)}```\n")
 traffic = {}
-for c in ["c2", "c1"]:
+for c in CONFIGS:
     rep = os.path.join(R, f"full_{c}.ncu-rep")
     if not os.path.exists(rep):
         continue
@@ -41,12 +45,13 @@ for c in ["c2", "c1"]:
             i = h.index(m)
             return float(r[i].replace(",", "")) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u[i], 1)
         b = val("dram__bytes_read.sum") + val("dram__bytes_write.sum")
-        for k, v in {"k_sort_pass": "place", "k_rank_place": "place", "k_ingest": "ingest", "k_count": "count"}.items():
+        for k, v in {"k_sort_pass": "place", "k_rank_place": "place", "k_os_pass": "place", "k_ingest": "ingest",
+                     "k_count": "count", "k_key_count": "count"}.items():
             if k in name:
                 d.setdefault(v, []).append(b)
     traffic[c] = {k: {"bytes_per_launch": sum(v) / len(v), "launches_captured": len(v)} for k, v in d.items()}
 traffic["_source"] = ("dram__bytes_read.sum + dram__bytes_write.sum per launch, ncu --set full "
-                      "--clock-control none of bench.py (scripts/gpu_round.sh), " + tag)
+                      "--clock-control none of bench.py (scripts/gpu_round.sh / gpu_r2p.sh), " + tag)
 bench = ["## Bench lines (this round)\n", "```"]
 for f in sorted(os.listdir(R)):
     if f.startswith("bench_") and f.endswith(".log"):
@@ -54,7 +59,9 @@ for f in sorted(os.listdir(R)):
         if lines:
             d = json.loads(lines[-1])
             bench.append(f"{f:22s} value={d.get('value', 0) / 1e9:8.3f} G/s  e2e={d.get('e2e', {}).get('value', 0) / 1e9:6.3f} G/s  "
-                         f"ms/step={d.get('ms_per_step', 0) or 0:.3f}  load_ratio={d.get('load_ratio', {}).get('mean', '-')}")
+                         f"ms/step={d.get('ms_per_step', 0) or 0:.3f}  path={d.get('path_roofline', {}).get('frac', 0):.3f}  "
+                         f"load(plan)={d.get('load_ratio', {}).get('plan_mean', '-')}  "
+                         f"load(part_ns)={d.get('load_ratio', {}).get('measured_part_ns_max_over_mean', '-')}")
 bench.append("```\n")
 md[7:7] = bench
 open(os.path.join(P, f"{tag}_summary.md"), "w").write("\n".join(md))
