@@ -921,6 +921,7 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
             (rc = dalloc(e, &t.new_ent, G)) || (rc = dalloc(e, &t.n_new, 1)) || (rc = dalloc(e, &t.n_slots, 1)) ||
             (rc = dalloc(e, &t.mark, e->max_batch)) || (rc = dalloc(e, &t.slot_keys, G)) ||
             (rc = dalloc(e, &t.min_key_entry, 1)) || (rc = dalloc(e, &t.overflow, 1)) ||
+            (rc = dalloc(e, &t.prev_slots, 1)) ||
             (rc = dalloc(e, &e->stage_keys64, e->max_batch)) ||
             (rc = dalloc(e, &e->kbsum, e->max_batch / kMarkBlk + 2)))
             return rc;
@@ -1708,16 +1709,31 @@ static int enqueue_report(ss_engine* e, int64_t n, bool has_policy, cudaStream_t
 }
 
 
+// free the key-table entries a rejected int64-key batch claimed
+static void key_rollback(ss_engine* e) {
+    const int64_t n_ent = (int64_t)e->kt.cap_mask + 2;
+    ss_note_launch(), ss_launch(k_key_rollback, (unsigned)std::min<int64_t>((n_ent + 255) / 256, 16 * kNumSM), 256, 0,
+                                e->st, e->kt, n_ent);
+    cudaStreamSynchronize(e->st);
+}
+
 static int check_report(ss_engine* e, const uint32_t* dk) {
     SS_CUDA(e, cudaStreamSynchronize(e->st));
     SS_CUDA(e, cudaStreamSynchronize(e->side));
     SS_CUDA(e, cudaGetLastError());
-    if (e->h_rep->bad != (unsigned long long)kNoBad) return data_error(e, e->h_rep->bad, dk);
+    if (e->h_rep->bad != (unsigned long long)kNoBad) {
+        if (e->keys64) key_rollback(e);
+        return data_error(e, e->h_rep->bad, dk);
+    }
     if (e->h_rep->oom) return fail(e, SS_E_EXEC, "window ring pool exhausted (raise pool_values)");
     if (e->keys64) {
         int ov = 0;
         SS_CUDA(e, cudaMemcpy(&ov, e->kt.overflow, 4, cudaMemcpyDeviceToHost));
-        if (ov) return fail(e, SS_E_DATA, "more than n_groups distinct keys");
+        if (ov) {
+            key_rollback(e);
+            recover_bad(e);
+            return fail(e, SS_E_DATA, "more than n_groups distinct keys");
+        }
     }
     return SS_OK;
 }
@@ -3032,6 +3048,7 @@ static int map_keys(ss_engine* e, const int64_t* keys, int64_t n, uint32_t* dout
     }
     if (n == 0) return SS_OK;
     KeyTable& t = e->kt;
+    SS_CUDA(e, cudaMemcpyAsync(t.prev_slots, t.n_slots, 4, cudaMemcpyDeviceToDevice, e->st));
     const int nblk = (int)((n + kMarkBlk - 1) / kMarkBlk);
     const int64_t range = kCountChunk;                   // divides the count chunk S
     const unsigned grid = (unsigned)((n + range - 1) / range);

@@ -65,6 +65,7 @@ struct KeyTable {
     int32_t* slot_ent;          // [G] entry of each slot
     int* min_key_entry;         // entry index used for INT64_MIN (-1)
     int* overflow;              // more distinct keys than G
+    int* prev_slots;            // n_slots when the batch began (rollback of a rejected batch)
     unsigned long long cap_mask;
     int G;
 };
@@ -280,6 +281,35 @@ k_key_rank_small(KeyTable t) { SS_PDL_ENTRY();
     }
 }
 // n_new past kKeySmall is reset by k_key_mark_done
+
+// A rejected batch (a bad tuple, or more distinct keys than G) must leave
+// the engine as it was (validate before mutate, engine.py:281-282): the
+// entries its new keys claimed are freed.  They were all claimed after
+// every older key, so no older key's probe sequence passes through them
+// (linear probing only ever inserts at free entries).
+__global__ void __launch_bounds__(256)
+k_key_rollback(KeyTable t, int64_t n_ent) { SS_PDL_ENTRY();
+    const int keep = *t.prev_slots;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_ent; e += (int64_t)gridDim.x * blockDim.x) {
+        const KEntry en = t.ent[e];
+        if (en.key == kEmptyKey && e != (int64_t)t.cap_mask + 1) continue;
+        if (en.slot >= 0 && en.slot < keep) continue;
+        if (e == (int64_t)t.cap_mask + 1 && en.slot < 0 && *t.min_key_entry < 0) continue;
+        KEntry z;
+        z.key = kEmptyKey;
+        z.slot = -1;
+        z.hot = -1;
+        t.ent[e] = z;
+        t.first[e] = 0xffffffffu;
+        if (e == (int64_t)t.cap_mask + 1) *t.min_key_entry = -1;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        *t.n_slots = keep;
+        *t.n_new = 0;
+        *t.n_pend = 0;
+        *t.overflow = 0;
+    }
+}
 
 // many new keys: mark[first position] = entry, then an ordered
 // compaction over the batch positions (count / scan / assign)

@@ -358,4 +358,18 @@ def test_int64_keys_match_oracle(policy):
     assert np.array_equal(s["min"], mn) and np.array_equal(s["max"], mx)
     with pytest.raises(DataError):
         eng.step(D.mix64(np.arange(G, 2 * G + 100)), np.zeros(G + 100, dtype=np.int64), bal)
+    # the rejected batch claimed nothing (validate before mutate,
+    # engine.py:281-282): same slots, same windows, and the next batch lands
+    # exactly as on an engine that never saw it
+    assert np.array_equal(eng.slot_keys(), sk)
+    s2 = eng.snapshot()
+    assert np.array_equal(s2["window_sum"], s["window_sum"]) and np.array_equal(s2["fill"], s["fill"])
+    b = bl[0]
+    eng.step(D.mix64(b.groups), b.attrs, bal)
+    rg = slot_of[b.groups]
+    counts, tpt = O.histogram(rg, asg)
+    pg, pa, ind = O.place(rg, b.attrs, asg, counts, tpt)
+    store.ingest(pg, pa, assume_grouped=True)
+    s3 = eng.snapshot()
+    assert np.array_equal(s3["fill"], store.fill) and np.array_equal(s3["window_sum"], store.window_sum)
     eng.close()
