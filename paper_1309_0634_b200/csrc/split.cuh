@@ -5,20 +5,23 @@
 // so the best any reference policy can reach is max/mean = P x (hottest
 // group's share) -- 56.85 at Zipf s=1.5, P=148.
 //
-// Split mode plans, from batch t's counts, how batch t+1 executes:
+// Split mode plans, from batch t's OWN counts (on the side stream while
+// batch t's placement runs; the window update waits for it), how batch t
+// executes:
 //   1. hot groups: count > mean/2 (so at most 2P of them); everything else
 //      is cold and stays whole on its partition;
 //   2. the configured policy moves COLD groups between partitions on the
-//      cold-only loads (same device loop as the reference policies);
+//      cold-only loads (same device loop as the reference policies); those
+//      moves keep the reference's one-batch delay (in force from t+1);
 //   3. the hot groups' tuples are water-filled onto the least loaded
 //      partitions: find the level L with sum_p max(0, L - load_p) >= hot
 //      tuples, lay partition capacities and hot groups' runs on one axis
 //      and cut -- each overlap is a share (group, partition, run slice).
-// A share covers the run slice [k*lo/den, k*hi/den) of its group in the
-// sub-batch (den = the planned count), so shares tile each run exactly
-// whatever the next batch's count is.  Every share does independent
-// window exchanges (window.cuh) and adds its delta to the group's
-// accumulator; K5 (k_split_finalize) combines them after the sub-batch.
+// A share covers the run slice [k*lo/den, k*hi/den) of its group's kept
+// run (den = the planned count), so the shares tile each run exactly.
+// Every share does independent window exchanges (window.cuh) and adds its
+// delta to the group's batch accumulator; K5 (k_finalize) folds them once
+// per batch.
 #pragma once
 
 #include "common.cuh"
