@@ -4,17 +4,24 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -shared
 //        -Xcompiler -fPIC -cudart static engine.cu -o libss_b200.so
 //
-// Pipeline of one batch (the loop body of harness.run, harness.py:99-117):
-//   K2  k_count          per-sub-batch group histograms   (count_batch)
-//       k_batch_stats    gcount, tpt                      (BatchStats)
-//   K7  k_balance        policy on a side stream, overlapped with the rest
-//       k_scan_*         run starts + radix digit bases
-//   per L2-resident sub-batch:
+// Pipeline of one batch (the loop body of harness.run, harness.py:99-117),
+// every kernel a programmatic dependent launch (ss_launch), the whole step
+// replayed as a CUDA graph:
+//   K2  k_count_rows / k_count / k_key_count   per-chunk group histograms
+//                                              (count_batch; int64 keys probed)
+//       k_batch_stats*   gcount, gkept (never-stored runs dropped), tpt
+//   K7  k_balance        policy on a side stream, overlapped with the rest;
+//       k_split_*        hot-key split plan from the batch's own counts
+//       k_scan_*         run starts (+ digit bases / live-chunk list)
 //       k_reserve        grow occupancy-proportional rings (sparse store)
-//   K3  k_sort_pass x1-2 stable placement -> arrival rank within group
-//   K4  k_ingest         one CTA per partition: window exchange + state
-//   K5  k_split_finalize split hot keys; k_minmax_rescan
-//       k_emit           per-batch result rows
+//   K3  k_rank_place     single-pass stable placement (G <= 2^14; few live
+//                        chunks: sub-chunks via k_sub_hist / k_sub_scan), or
+//       k_sort_pass      radix passes over the live chunks (G <= 2^17), or
+//       k_os_*           look-back-free LSD passes (G >= 2^18)
+//   K4  k_ingest         partition-parallel window exchange (+ split shares)
+//   K5  k_finalize       fold deltas into the state, result rows;
+//       k_mm_* / k_minmax_rescan   MIN/MAX of partially evicted windows
+//       k_emit_host      rows into pinned host memory (streaming use)
 //       k_apply_*        apply the policy's moves (in force from batch t+1)
 #include <cuda_runtime.h>
 
