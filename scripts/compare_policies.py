@@ -2,7 +2,8 @@
 "all balancer instantiations compared").  For each policy, with and
 without hot-key splitting: tuples/s over `steps` batches after `warmup`
 batches (CUDA events, staged batches in HBM), mean/max per-block max/mean
-load ratio, moves per batch.  Initial map: key hash (as bench.py); the
+load ratio (the plan's tuple loads), the measured per-partition window
+update time max/mean, moves per batch.  Initial map: key hash (as bench.py); the
 policies start from it and converge during the warm-up.
 
     python scripts/compare_policies.py --config c4 --steps 6 --warmup 12
@@ -54,16 +55,21 @@ def main():
             e1.record(stream)
             e1.synchronize()
             ms = e0.elapsed_time(e1)
+            part = []
             for i in range(2):
                 r = eng.step(*batches[i % 2], bal)
                 ratios.append(r.load_ratio)
                 moves.append(r.moves)
+                ns = eng.last_part_ns().astype(np.float64)
+                if ns.sum() > 0:
+                    part.append(float(ns.max() / ns.mean()))
             print(json.dumps({"config": args.config, "policy": pol, "split": split, "initial": args.initial,
                               "warmup": args.warmup,
                               "tuples_per_s": B * args.steps / (ms / 1e3),
                               "ms_per_step": ms / args.steps,
                               "load_ratio_mean": float(np.mean(ratios)), "load_ratio_max": float(np.max(ratios)),
-                              "moves_per_batch": float(np.mean(moves))}), flush=True)
+                              "moves_per_batch": float(np.mean(moves)),
+                              "part_ns_max_over_mean": float(np.mean(part)) if part else None}), flush=True)
             eng.close()
 
 
