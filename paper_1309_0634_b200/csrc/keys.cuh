@@ -160,62 +160,78 @@ k_key_count(const long long* __restrict__ keys, int64_t n, KeyTable t, uint32_t*
             en[u] = ld_entry(t.ent + h[u], pol_t);        // all first probes in flight together
         }
         uint32_t sl[kKeyItems];
+        int hot[kKeyItems];
+        // fast path: every key of the round at its home entry with a slot
+        // (all but a batch's first appearances and probe collisions) --
+        // branch-free; anything else goes through one warp-uniform slow path
+        bool slow = false;
 #pragma unroll
         for (int u = 0; u < kKeyItems; ++u) {
-            const int64_t i = i0 + u;
-            sl[u] = 0xffffffffu;
-            int hot = -1;
-            bool pending = false;
-            int e = -1;
-            if (i < c1) {
-                if (k[u] == kEmptyKey) {
-                    // the reserved marker value gets a dedicated entry: cap_mask + 1
-                    e = (int)(t.cap_mask + 1);
-                    if (atomicCAS(t.min_key_entry, -1, e) == -1) {
-                        const int k2 = atomicAdd(t.n_new, 1);
-                        if (k2 < t.G) t.new_ent[k2] = e; else *t.overflow = 1;
+            const bool valid = i0 + u < c1;
+            const bool ok = !valid || (en[u].key == k[u] && k[u] != kEmptyKey && en[u].slot >= 0);
+            slow |= !ok;
+            sl[u] = valid ? (uint32_t)en[u].slot : 0xffffffffu;
+            hot[u] = valid ? en[u].hot : -1;
+        }
+        if (__any_sync(SS_FULL, slow)) {
+#pragma unroll
+            for (int u = 0; u < kKeyItems; ++u) {
+                const int64_t i = i0 + u;
+                bool pending = false;
+                int e = -1;
+                if (i < c1 && !(en[u].key == k[u] && k[u] != kEmptyKey && en[u].slot >= 0)) {
+                    if (k[u] == kEmptyKey) {
+                        // the reserved marker value gets a dedicated entry: cap_mask + 1
+                        e = (int)(t.cap_mask + 1);
+                        if (atomicCAS(t.min_key_entry, -1, e) == -1) {
+                            const int k2 = atomicAdd(t.n_new, 1);
+                            if (k2 < t.G) t.new_ent[k2] = e; else *t.overflow = 1;
+                        }
+                    } else {
+                        e = key_entry(t, k[u], h[u]);
                     }
                     en[u] = ld_entry(t.ent + e, pol_t);
-                } else if (en[u].key != k[u]) {
-                    e = key_entry(t, k[u], h[u]);
-                    en[u] = ld_entry(t.ent + e, pol_t);
-                } else {
-                    e = (int)h[u];
+                    if (en[u].slot >= 0) {
+                        sl[u] = (uint32_t)en[u].slot;
+                        hot[u] = en[u].hot;
+                    } else {
+                        sl[u] = 0xffffffffu;
+                        hot[u] = -1;
+                        pending = true;
+                        atomicMin(&t.first[e], (unsigned int)i);
+                    }
                 }
-                if (en[u].slot >= 0) {
-                    sl[u] = (uint32_t)en[u].slot;
-                    hot = en[u].hot;
-                } else {
-                    pending = true;
-                    atomicMin(&t.first[e], (unsigned int)i);
-                }
-            }
-            // pending tuples: one warp-aggregated append to the pending list
-            const unsigned pm = __ballot_sync(SS_FULL, pending);
-            if (pm) {
-                int pb = 0;
-                if (lane == (unsigned)(__ffs(pm) - 1)) pb = atomicAdd(t.n_pend, __popc(pm));
-                pb = __shfl_sync(SS_FULL, pb, __ffs(pm) - 1);
-                if (pending) {
-                    const int r = pb + __popc(pm & lanemask_lt());
-                    t.pend[r] = (int32_t)i;
-                    t.pend_ent[r] = e;
+                // pending tuples: one warp-aggregated append to the pending list
+                const unsigned pm = __ballot_sync(SS_FULL, pending);
+                if (pm) {
+                    int pb = 0;
+                    if (lane == (unsigned)(__ffs(pm) - 1)) pb = atomicAdd(t.n_pend, __popc(pm));
+                    pb = __shfl_sync(SS_FULL, pb, __ffs(pm) - 1);
+                    if (pending) {
+                        const int r = pb + __popc(pm & lanemask_lt());
+                        t.pend[r] = (int32_t)i;
+                        t.pend_ent[r] = e;
+                    }
                 }
             }
-            // count: hot groups in shared memory, the rest warp-aggregated
-            if (!COUNT) continue;
-            uint32_t g = sl[u];
-            if (hot >= 0 && hot < n_hot) {
-                atomicAdd(&sh_hist[hot], 1);
-                g = 0xffffffffu;
-            }
-            if (agg) {
-                // warp-aggregated: a key hot in this batch but missing from
-                // the cache (drifting skew) costs one atomic per warp
-                const unsigned peers = __match_any_sync(SS_FULL, g);
-                if (g != 0xffffffffu && lane == 31u - __clz(peers)) atomicAdd(&dst[g], __popc(peers));
-            } else if (g != 0xffffffffu) {
-                atomicAdd(&dst[g], 1);
+        }
+        if (COUNT) {
+            // count: hot groups in shared memory, the rest one global atomic
+            // each (or warp-aggregated, agg: a key hot in this batch but
+            // missing from the cache -- drifting skew -- costs one per warp)
+#pragma unroll
+            for (int u = 0; u < kKeyItems; ++u) {
+                uint32_t g = sl[u];
+                if (hot[u] >= 0 && hot[u] < n_hot) {
+                    atomicAdd(&sh_hist[hot[u]], 1);
+                    g = 0xffffffffu;
+                }
+                if (agg) {
+                    const unsigned peers = __match_any_sync(SS_FULL, g);
+                    if (g != 0xffffffffu && lane == 31u - __clz(peers)) atomicAdd(&dst[g], __popc(peers));
+                } else if (g != 0xffffffffu) {
+                    atomicAdd(&dst[g], 1);
+                }
             }
         }
         if (full) {
