@@ -444,6 +444,7 @@ k_balance(BalanceArgs a) { SS_PDL_ENTRY();
                     }
                 }
                 if (pick < 0) break;
+                __syncwarp();                          // every lane's reads of the moved flags precede the move
                 if (lane == 0) {
                     bal_move(a, s, &nm, pick, hi, lo, 1, pick_c);
                     scanned += pscan;
