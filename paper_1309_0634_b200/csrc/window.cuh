@@ -185,8 +185,17 @@ k_ingest(IngestArgs a) { SS_PDL_ENTRY();
     // and the CTAs interleave the warp units / short values (a hot member's
     // run spreads over all of them).  Many items: they are dealt round-robin
     // (it = sub, sub + kCtaPerPart, ...) so nothing is staged twice.
-    const bool shared_items = n_items <= kMemberChunk;
-    const int my_items = shared_items ? n_items : (n_items - sub + kCtaPerPart - 1) / kCtaPerPart;
+    // With many items the members are dealt round-robin but the split
+    // shares (few, long: a hot group's slices) get a round of their own in
+    // which every CTA of the partition stages them all and the CTAs
+    // interleave their units -- dealt whole, one CTA of a partition could
+    // draw twice the other's share work (C4: CTA times ~2x apart).
+    const bool all_shared = n_items <= kMemberChunk;
+    for (int ph = 0; ph < (all_shared ? 1 : 2); ++ph) {
+    const int ibase = (all_shared || ph == 0) ? 0 : n_mem;
+    const int icount = all_shared ? n_items : (ph == 0 ? n_mem : n_items - n_mem);
+    const bool shared_items = all_shared || ph == 1;
+    const int my_items = shared_items ? icount : (icount - sub + kCtaPerPart - 1) / kCtaPerPart;
     const int cstride = shared_items ? kCtaPerPart : 1;   // interleave factor
     const int csub = shared_items ? sub : 0;
     for (int c0 = 0; c0 < my_items; c0 += kMemberChunk) {
@@ -199,7 +208,7 @@ k_ingest(IngestArgs a) { SS_PDL_ENTRY();
         for (int q = 0; q < kMPT; ++q) {
             const int i = q * kIngestThreads + threadIdx.x;
             if (i >= m) continue;
-            const int it = shared_items ? c0 + i : (c0 + i) * kCtaPerPart + sub;
+            const int it = ibase + (shared_items ? c0 + i : (c0 + i) * kCtaPerPart + sub);
             int g, r_lo, r_hi;            // this item's slice [r_lo, r_hi) of the sub-batch run
             int32_t tag;
             if (it < n_mem) {
@@ -440,6 +449,7 @@ k_ingest(IngestArgs a) { SS_PDL_ENTRY();
         }
         __syncthreads();
         SS_PT4(5);
+    }
     }
     work_total = warp_sum(work_total);
     if (lane == 0 && a.part_work && work_total) atomicAdd(&a.part_work[p], work_total);

@@ -177,7 +177,9 @@ def hash_lists(n_groups: int, n_partitions: int, block: int | None = None):
     domains (fewer than 64 groups per partition) hash single ids to keep
     every partition populated."""
     if block is None:
+        import os
         block = 8 if n_groups >= 64 * n_partitions else 1
+        block = int(os.environ.get("SS_B200_HASH_BLOCK", block))     # A/B measurement only
     g = np.arange(n_groups, dtype=np.uint64) // np.uint64(block)
     with np.errstate(over="ignore"):
         x = (g + np.uint64(0x9E3779B97F4A7C15)) * np.uint64(0xBF58476D1CE4E5B9)
