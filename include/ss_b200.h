@@ -96,10 +96,10 @@ typedef struct {
     int64_t moves;           /* moves emitted by this batch's policy                   */
     int64_t moves_applied_before; /* harness.py:113 row.moves                           */
     int64_t scanned;         /* MoveList.scanned_tuples (balance.py:68-80)             */
-    int64_t max_load;        /* max per-block tuple load incl. split shares            */
+    int64_t max_load;        /* max per-block load incl. split shares (same unit)       */
     int64_t touched;         /* groups with >= 1 tuple in the batch                    */
     int64_t split_groups;    /* groups executed as split shares this batch            */
-    double  mean_load;       /* tuples / P                                             */
+    double  mean_load;       /* sum of block loads / P (tuples; values to store with split) */
     double  load_ratio;      /* max_load / mean_load                                    */
 } ss_step_report;
 

@@ -91,6 +91,7 @@ struct DevReport {            // written by k_report, copied to the host
     long long touched;
     long long split_groups;
     long long n_res;
+    long long load_sum;      // sum of the per-block loads max_load is taken over
     int oom;
     int pad;
 };
@@ -550,26 +551,30 @@ k_report(const unsigned long long* __restrict__ tpt, const unsigned long long* _
          const int* __restrict__ n_moves, int* __restrict__ prev_moves, const long long* __restrict__ scanned,
          const int* __restrict__ n_split, const unsigned* __restrict__ n_res, const int* __restrict__ oom,
          long long tuples, int has_policy, DevReport* __restrict__ rep) { SS_PDL_ENTRY();
-    __shared__ long long r[3][32];
-    long long mx = 0, mnv = LLONG_MAX, ml = 0;
+    __shared__ long long r[4][32];
+    long long mx = 0, mnv = LLONG_MAX, ml = 0, ls = 0;
     for (int p = threadIdx.x; p < P; p += blockDim.x) {
         const long long t = (long long)tpt[p];
         mx = max(mx, t);
         mnv = min(mnv, t);
-        ml = max(ml, (long long)(loads ? loads[p] : tpt[p]));
+        const long long l = (long long)(loads ? loads[p] : tpt[p]);
+        ml = max(ml, l);
+        ls += l;
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
         mx = max(mx, __shfl_xor_sync(SS_FULL, mx, o));
         mnv = min(mnv, __shfl_xor_sync(SS_FULL, mnv, o));
         ml = max(ml, __shfl_xor_sync(SS_FULL, ml, o));
+        ls += __shfl_xor_sync(SS_FULL, ls, o);
     }
-    if (lane_id() == 0) { r[0][warp_id()] = mx; r[1][warp_id()] = mnv; r[2][warp_id()] = ml; }
+    if (lane_id() == 0) { r[0][warp_id()] = mx; r[1][warp_id()] = mnv; r[2][warp_id()] = ml; r[3][warp_id()] = ls; }
     __syncthreads();
     if (threadIdx.x == 0) {
         for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
-            mx = max(mx, r[0][w]); mnv = min(mnv, r[1][w]); ml = max(ml, r[2][w]);
+            mx = max(mx, r[0][w]); mnv = min(mnv, r[1][w]); ml = max(ml, r[2][w]); ls += r[3][w];
         }
+        rep->load_sum = ls;
         rep->bad = *bad;
         rep->tuples = tuples;
         rep->imbalance = P ? mx - mnv : 0;
@@ -1499,17 +1504,17 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
             SS_CUDA(e, cudaMemsetAsync(e->spx.n_hot, 0, 4, e->side));
             const long long hot_min = std::max<long long>(1, n / (2LL * e->P));
             ss_note_launch(), ss_launch(k_split_hot, 2 * kNumSM, 256, e->P * 4, e->side, e->gcount, (uint32_t)e->G, e->pmap, hot_min, e->maxS,
-                                                                e->spx, e->P, e->bad);
+                                                                e->spx, e->P, e->bad, e->W);
             // water-fill the hot groups over this batch's cold loads (the
             // policy's moves apply from the next batch on)
             const SplitPlan& nx = e->plan_buf[plan];
             ss_note_launch(), ss_launch(k_u64_to_i64, 1, 1024, 0, e->side, e->spx.base, e->fill_loads, e->P);
             const size_t smem = (size_t)e->maxS * 20 + 16 + (size_t)(e->P + 1) * 4;
             ss_note_launch(), ss_launch(k_split_fill, 1, 1024, smem, e->side, e->gcount, e->fill_loads, e->P, e->maxS, e->spx, nx, nx,
-                                                                       e->bad);
+                                                                       e->bad, e->W);
             SS_CUDA(e, cudaMemsetAsync(e->loads, 0, e->P * 8, e->side));
             ss_note_launch(), ss_launch(k_split_loads, 2 * kNumSM, 256, e->P * 4, e->side, e->gcount, (uint32_t)e->G, e->pmap, e->P,
-                                                                                    nx, e->loads, e->bad);
+                                                                                    nx, e->loads, e->bad, e->W);
             SS_CUDA(e, cudaEventRecord(e->ev_bal, e->side));
         }
         if (has_policy) {
@@ -1755,8 +1760,10 @@ static void fill_report(const ss_engine* e, ss_step_report* r) {
     r->max_load = d.max_load;
     r->touched = d.touched;
     r->split_groups = d.split_groups;
-    r->mean_load = e->P ? (double)d.tuples / (double)e->P : 0.0;
-    r->load_ratio = (d.tuples > 0) ? (double)d.max_load / r->mean_load : 0.0;
+    // max / mean over one unit: tuples without a split plan, values to
+    // store (min(count, W) per group) with one (split.cuh)
+    r->mean_load = e->P ? (double)d.load_sum / (double)e->P : 0.0;
+    r->load_ratio = (d.load_sum > 0) ? (double)d.max_load / r->mean_load : 0.0;
 }
 
 static int ensure_moves(ss_engine* e, int64_t want) {

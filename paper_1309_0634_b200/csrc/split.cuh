@@ -17,8 +17,13 @@
 //      partitions: find the level L with sum_p max(0, L - load_p) >= hot
 //      tuples, lay partition capacities and hot groups' runs on one axis
 //      and cut -- each overlap is a share (group, partition, run slice).
-// A share covers the run slice [k*lo/den, k*hi/den) of its group's kept
-// run (den = the planned count), so the shares tile each run exactly.
+// Loads are in values to store, min(count, W) per group: a hot group's
+// tuples before its last W are never stored, so planning on tuple counts
+// left partitions holding those slices idle (C3, W = 1e6 and a top group
+// of ~6M tuples per batch: measured partition time max/mean 1.7 with a
+// tuple-balanced plan).  A share covers the slice [s*lo/den, s*hi/den) of
+// its group's s = min(count, W) stored values (den = the planned s), so
+// the shares tile the stored range exactly.
 // Every share does independent window exchanges (window.cuh) and adds its
 // delta to the group's batch accumulator; K5 (k_finalize) folds them once
 // per batch.
@@ -51,7 +56,7 @@ struct SplitScratch {
 // accumulate per CTA in shared memory (P <= 4096) before one flush.
 __global__ void __launch_bounds__(256)
 k_split_hot(const int32_t* __restrict__ gcount, uint32_t G, const int32_t* __restrict__ pmap, long long hot_min,
-            int maxS, SplitScratch sc, int P, const unsigned long long* __restrict__ bad) { SS_PDL_ENTRY();
+            int maxS, SplitScratch sc, int P, const unsigned long long* __restrict__ bad, int64_t W) { SS_PDL_ENTRY();
     extern __shared__ uint32_t sh_base[];
     if (*bad != (unsigned long long)kNoBad) return;
     for (int i = threadIdx.x; i < P; i += blockDim.x) sh_base[i] = 0;
@@ -67,7 +72,7 @@ k_split_hot(const int32_t* __restrict__ gcount, uint32_t G, const int32_t* __res
             }
         }
         sc.hot_flag[g] = hot;
-        if (c && !hot) atomicAdd(&sh_base[pmap[g]], (uint32_t)c);
+        if (c && !hot) atomicAdd(&sh_base[pmap[g]], (uint32_t)min64(c, W));
     }
     __syncthreads();
     for (int i = threadIdx.x; i < P; i += blockDim.x)
@@ -78,7 +83,7 @@ k_split_hot(const int32_t* __restrict__ gcount, uint32_t G, const int32_t* __res
 // moves and write the next plan.  One CTA.
 __global__ void __launch_bounds__(1024)
 k_split_fill(const int32_t* __restrict__ gcount, const long long* __restrict__ loads, int P, int maxS,
-             SplitScratch sc, SplitPlan prev, SplitPlan nx, const unsigned long long* __restrict__ bad) { SS_PDL_ENTRY();
+             SplitScratch sc, SplitPlan prev, SplitPlan nx, const unsigned long long* __restrict__ bad, int64_t W) { SS_PDL_ENTRY();
     extern __shared__ long long fsm[];
     long long* hot_c = fsm;                 // [maxS]
     long long* hot_s = hot_c + maxS;        // [maxS + 1] axis starts
@@ -95,11 +100,11 @@ k_split_fill(const int32_t* __restrict__ gcount, const long long* __restrict__ l
     // sort hot groups by (count desc, id asc): rank by counting (nh <= 2P+1)
     for (int i = threadIdx.x; i < nh; i += blockDim.x) {
         const int g = sc.hot_g[i];
-        const long long c = gcount[g];
+        const long long c = min64(gcount[g], W);
         int r = 0;
         for (int j = 0; j < nh; ++j) {
             const int g2 = sc.hot_g[j];
-            const long long c2 = gcount[g2];
+            const long long c2 = min64(gcount[g2], W);
             r += (c2 > c) || (c2 == c && g2 < g);
         }
         hot_g[r] = g;
@@ -215,7 +220,8 @@ k_split_fill(const int32_t* __restrict__ gcount, const long long* __restrict__ l
 // Loads of the current batch under the current plan (report / max-mean).
 __global__ void __launch_bounds__(256)
 k_split_loads(const int32_t* __restrict__ gcount, uint32_t G, const int32_t* __restrict__ pmap, int P,
-              SplitPlan cur, unsigned long long* __restrict__ loads, const unsigned long long* __restrict__ bad) { SS_PDL_ENTRY();
+              SplitPlan cur, unsigned long long* __restrict__ loads, const unsigned long long* __restrict__ bad,
+              int64_t W) { SS_PDL_ENTRY();
     extern __shared__ uint32_t sh_load[];
     if (*bad != (unsigned long long)kNoBad) return;
     for (int i = threadIdx.x; i < P; i += blockDim.x) sh_load[i] = 0;
@@ -223,14 +229,14 @@ k_split_loads(const int32_t* __restrict__ gcount, uint32_t G, const int32_t* __r
     const int nsh = *cur.n_share;
     for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < G; g += gridDim.x * blockDim.x) {
         const int32_t c = gcount[g];
-        if (c && cur.split_of[g] < 0) atomicAdd(&sh_load[pmap[g]], (uint32_t)c);
+        if (c && cur.split_of[g] < 0) atomicAdd(&sh_load[pmap[g]], (uint32_t)min64(c, W));
     }
     // shares: one thread per share, find its partition by binary search
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nsh; i += gridDim.x * blockDim.x) {
         int l = 0, r = P - 1;
         while (l < r) { const int m = (l + r + 1) >> 1; if (cur.part_soff[m] <= i) l = m; else r = m - 1; }
         const int j = cur.share_grp[i];
-        const long long kt = gcount[cur.split_g[j]], den = cur.split_den[j];
+        const long long kt = min64(gcount[cur.split_g[j]], W), den = cur.split_den[j];
         const long long a = kt * cur.share_lo[i] / den, b = kt * cur.share_hi[i] / den;
         if (b > a) atomicAdd(&sh_load[l], (uint32_t)(b - a));
     }

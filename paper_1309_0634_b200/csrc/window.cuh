@@ -221,9 +221,12 @@ k_ingest(IngestArgs a) { SS_PDL_ENTRY();
                 const int sg = a.share_grp[sh];
                 g = a.split_g[sg];
                 tag = -1 - sg;
+                // shares tile the stored values: the last min(K, W) of the
+                // kept run (split.cuh)
                 const long long kt = a.gcnt[g], den = a.split_den[sg];
-                r_lo = (int)(kt * a.share_lo[sh] / den);
-                r_hi = (int)(kt * a.share_hi[sh] / den);
+                const long long sto = min64(a.gcount[g], a.W), off0 = kt - sto;
+                r_lo = (int)(off0 + sto * a.share_lo[sh] / den);
+                r_hi = (int)(off0 + sto * a.share_hi[sh] / den);
             }
             int w = 0;
             if (r_hi > r_lo) {
