@@ -80,7 +80,7 @@ namespace {
 constexpr int64_t kCountChunk = 16384;
 constexpr int64_t kDenseLimitBytes = int64_t(24) << 30;
 
-struct DevReport {            // written by k_report, copied to the host
+struct DevReport {            // written by report_body (window.cuh) as 64-bit words, copied to the host
     unsigned long long bad;
     long long tuples;
     long long imbalance;
@@ -264,6 +264,7 @@ struct ss_engine {
     int n_dest = 0;
     unsigned long long* route_cnt = nullptr;   // [16]
     uint32_t* route_base = nullptr;            // [16]
+    unsigned* fin_ticket = nullptr;            // k_finalize CTAs done (report fold)
     longlong4* mig_list = nullptr;             // [kMigMax] (ring offset, blob word, span, -) of exported groups
     int* mig_n = nullptr;
 
@@ -546,49 +547,8 @@ __global__ void k_clear_moved(const int4* __restrict__ moves, const int* __restr
 // load monitor (K6): imbalance of the entry loads, max per-block load
 // including split shares, and the report the host reads back.
 __global__ void __launch_bounds__(1024)
-k_report(const unsigned long long* __restrict__ tpt, const unsigned long long* __restrict__ loads, int P,
-         const unsigned long long* __restrict__ bad, const unsigned long long* __restrict__ touched,
-         const int* __restrict__ n_moves, int* __restrict__ prev_moves, const long long* __restrict__ scanned,
-         const int* __restrict__ n_split, const unsigned* __restrict__ n_res, const int* __restrict__ oom,
-         long long tuples, int has_policy, DevReport* __restrict__ rep) { SS_PDL_ENTRY();
-    __shared__ long long r[4][32];
-    long long mx = 0, mnv = LLONG_MAX, ml = 0, ls = 0;
-    for (int p = threadIdx.x; p < P; p += blockDim.x) {
-        const long long t = (long long)tpt[p];
-        mx = max(mx, t);
-        mnv = min(mnv, t);
-        const long long l = (long long)(loads ? loads[p] : tpt[p]);
-        ml = max(ml, l);
-        ls += l;
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        mx = max(mx, __shfl_xor_sync(SS_FULL, mx, o));
-        mnv = min(mnv, __shfl_xor_sync(SS_FULL, mnv, o));
-        ml = max(ml, __shfl_xor_sync(SS_FULL, ml, o));
-        ls += __shfl_xor_sync(SS_FULL, ls, o);
-    }
-    if (lane_id() == 0) { r[0][warp_id()] = mx; r[1][warp_id()] = mnv; r[2][warp_id()] = ml; r[3][warp_id()] = ls; }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
-            mx = max(mx, r[0][w]); mnv = min(mnv, r[1][w]); ml = max(ml, r[2][w]); ls += r[3][w];
-        }
-        rep->load_sum = ls;
-        rep->bad = *bad;
-        rep->tuples = tuples;
-        rep->imbalance = P ? mx - mnv : 0;
-        rep->max_load = ml;
-        rep->touched = (long long)*touched;
-        const int nm = has_policy ? *n_moves : 0;
-        rep->moves = nm;
-        rep->moves_before = *prev_moves;
-        *prev_moves = (*bad == (unsigned long long)kNoBad) ? nm : 0;
-        rep->scanned = has_policy ? *scanned : 0;
-        rep->split_groups = n_split ? *n_split : 0;
-        rep->n_res = n_res ? *n_res : 0;
-        rep->oom = *oom;
-    }
+k_report(ReportArgs a) { SS_PDL_ENTRY();
+    report_body(a);
 }
 
 }  // namespace
@@ -847,8 +807,10 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
         (rc = dalloc(e, &e->chunk_h, (size_t)nsub * kMaxBins)) || (rc = dalloc(e, &e->chunk_base, (size_t)nsub * kMaxBins)) ||
         (rc = dalloc(e, &e->btile, kMaxBins + 1)) || (rc = dalloc(e, &e->ep_dev, 1)) ||
         (rc = dalloc(e, &e->bdelta, G)) || (rc = dalloc(e, &e->bmin, G)) || (rc = dalloc(e, &e->bmax, G)) ||
-        (rc = dalloc(e, &e->hot_of, G)) || (rc = dalloc(e, &e->hot_g, kHotCache)) || (rc = dalloc(e, &e->n_hot_dev, 1)))
+        (rc = dalloc(e, &e->hot_of, G)) || (rc = dalloc(e, &e->hot_g, kHotCache)) || (rc = dalloc(e, &e->n_hot_dev, 1)) ||
+        (rc = dalloc(e, &e->fin_ticket, 1)))
         return rc;
+    SS_CUDA(e, cudaMemsetAsync(e->fin_ticket, 0, 4, e->st));
     // single-pass placement whenever the cursors fit in shared memory; with
     // a small kept set (few live chunks, e.g. C1) every live chunk is cut
     // into sub-chunks so the placement still fills the GPU (one CTA per
@@ -1425,6 +1387,8 @@ static IngestArgs ingest_args(ss_engine* e, int plan) {
 
 static int move_cap(ss_engine* e, const ss_balancer* b);
 static int enqueue_report(ss_engine* e, int64_t n, bool has_policy, cudaStream_t st);
+static ReportArgs report_args(ss_engine* e, int64_t n, bool has_policy);
+static int copy_report(ss_engine* e, cudaStream_t st);
 
 // an event other streams (or the host) wait on: inside a stream capture it
 // must be an external event-record node
@@ -1652,6 +1616,11 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
         f.sum_valid = e->sum_valid;
         f.n_sum = e->n_sum;
         f.bad = e->bad;
+        if (!run_side) {
+            // no side-stream work: the last finalize CTA writes the report
+            f.report = report_args(e, n, false);
+            f.ticket = e->fin_ticket;
+        }
         ss_note_launch(), ss_launch(k_finalize, group_grid(e->G), 256, 0, e->st, f);
         if (e->minmax) {
             if (e->sums) {
@@ -1696,7 +1665,7 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
             e->side_pending = false;
         }
     } else {
-        if ((rc = enqueue_report(e, n, false, e->st))) return rc;
+        if ((rc = copy_report(e, e->st))) return rc;
     }
     if (split) e->plan_cur ^= 1;
     e->plan_valid = split;
@@ -1706,18 +1675,39 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
 // --------------------------------------------------------------------------
 // report
 // --------------------------------------------------------------------------
-static int enqueue_report(ss_engine* e, int64_t n, bool has_policy, cudaStream_t st) {
+static ReportArgs report_args(ss_engine* e, int64_t n, bool has_policy) {
     const bool used_plan = e->last_plan >= 0;
-    ss_note_launch(), ss_launch(k_report, 1, 1024, 0, st, e->tpt, used_plan ? e->loads : nullptr, e->P, e->bad, e->touched, e->n_moves,
-                                 e->prev_moves, e->scanned,
-                                 used_plan ? e->plan_buf[e->last_plan].n_split : nullptr,
-                                 // (the result-row count is read from n_res by the result calls; the
-                                 // side-stream report may run before finalize, so it is not copied here)
-                                 nullptr, e->oom,
-                                 (long long)n, has_policy ? 1 : 0, e->d_rep);
-    SS_CUDA(e, cudaGetLastError());
+    ReportArgs r{};
+    r.tpt = e->tpt;
+    r.loads = used_plan ? e->loads : nullptr;
+    r.P = e->P;
+    r.bad = e->bad;
+    r.touched = e->touched;
+    r.n_moves = e->n_moves;
+    r.prev_moves = e->prev_moves;
+    r.scanned = e->scanned;
+    r.n_split = used_plan ? e->plan_buf[e->last_plan].n_split : nullptr;
+    // (the result-row count is read from n_res by the result calls; the
+    // side-stream report may run before finalize, so it is not copied here)
+    r.n_res = nullptr;
+    r.oom = e->oom;
+    r.tuples = (long long)n;
+    r.has_policy = has_policy ? 1 : 0;
+    r.rep = (long long*)e->d_rep;
+    return r;
+}
+
+// copy of the device report to the host (after k_report, or after the
+// k_finalize that wrote it when no side-stream work ran)
+static int copy_report(ss_engine* e, cudaStream_t st) {
     SS_CUDA(e, cudaMemcpyAsync(e->h_rep, e->d_rep, sizeof(DevReport), cudaMemcpyDeviceToHost, st));
     return SS_OK;
+}
+
+static int enqueue_report(ss_engine* e, int64_t n, bool has_policy, cudaStream_t st) {
+    ss_note_launch(), ss_launch(k_report, 1, 1024, 0, st, report_args(e, n, has_policy));
+    SS_CUDA(e, cudaGetLastError());
+    return copy_report(e, st);
 }
 
 

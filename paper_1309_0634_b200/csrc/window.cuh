@@ -459,10 +459,77 @@ k_ingest(IngestArgs a) { SS_PDL_ENTRY();
     if (threadIdx.x == 0 && a.part_ns) atomicAdd(&a.part_ns[p], (unsigned long long)(globaltimer() - t0));
 }
 
+// The per-batch report (tuples, tpt imbalance, max / sum of block loads,
+// moves, ...) -- k_report on the side stream when a policy or split plan
+// runs, else folded into k_finalize's last CTA (one launch fewer on C1's
+// critical path).  Layout of the host-visible struct: engine.cu DevReport.
+struct ReportArgs {
+    const unsigned long long* tpt;
+    const unsigned long long* loads;     // null: tpt
+    int P;
+    const unsigned long long* bad;
+    const unsigned long long* touched;
+    const int* n_moves;
+    int* prev_moves;
+    const long long* scanned;
+    const int* n_split;
+    const unsigned* n_res;
+    const int* oom;
+    long long tuples;
+    int has_policy;
+    long long* rep;                      // DevReport as 64-bit words (engine.cu)
+};
+
+// any blockDim <= 1024 (a multiple of 32); every thread of the CTA calls it
+__device__ __forceinline__ void report_body(const ReportArgs& a) {
+    __shared__ long long r[4][32];
+    long long mx = 0, mnv = LLONG_MAX, ml = 0, ls = 0;
+    for (int p = threadIdx.x; p < a.P; p += blockDim.x) {
+        const long long t = (long long)a.tpt[p];
+        mx = max(mx, t);
+        mnv = min(mnv, t);
+        const long long l = (long long)(a.loads ? a.loads[p] : a.tpt[p]);
+        ml = max(ml, l);
+        ls += l;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        mx = max(mx, __shfl_xor_sync(SS_FULL, mx, o));
+        mnv = min(mnv, __shfl_xor_sync(SS_FULL, mnv, o));
+        ml = max(ml, __shfl_xor_sync(SS_FULL, ml, o));
+        ls += __shfl_xor_sync(SS_FULL, ls, o);
+    }
+    if (lane_id() == 0) { r[0][warp_id()] = mx; r[1][warp_id()] = mnv; r[2][warp_id()] = ml; r[3][warp_id()] = ls; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+            mx = max(mx, r[0][w]); mnv = min(mnv, r[1][w]); ml = max(ml, r[2][w]); ls += r[3][w];
+        }
+        const unsigned long long bad = *a.bad;
+        const int nm = a.has_policy ? *a.n_moves : 0;
+        long long* o = a.rep;
+        o[0] = (long long)bad;
+        o[1] = a.tuples;
+        o[2] = a.P ? mx - mnv : 0;
+        o[3] = nm;
+        o[4] = *a.prev_moves;
+        o[5] = a.has_policy ? *a.scanned : 0;
+        o[6] = ml;
+        o[7] = (long long)*a.touched;
+        o[8] = a.n_split ? *a.n_split : 0;
+        o[9] = a.n_res ? *a.n_res : 0;
+        o[10] = ls;
+        reinterpret_cast<int*>(o + 11)[0] = *a.oom;
+        *a.prev_moves = (bad == (unsigned long long)kNoBad) ? nm : 0;
+    }
+}
+
 // K5: fold each touched group's batch delta into its window state, emit
 // its result row (group, COUNT, SUM, AVG, MIN, MAX; AVG = correctly
 // rounded double quotient) and reset the batch accumulators.
 struct FinalizeArgs {
+    ReportArgs report;          // used when ticket != null (no side-stream work)
+    unsigned* ticket;           // finished CTAs; the last one writes the report
     const int32_t* gcount;
     int32_t* gcnt;              // [n_sub][G] chunk counts, cleared here
     int n_sub;
@@ -495,9 +562,25 @@ struct FinalizeArgs {
     const unsigned long long* bad;
 };
 
+__device__ __forceinline__ void finalize_body(const FinalizeArgs& a);
+
 __global__ void __launch_bounds__(256)
 k_finalize(FinalizeArgs a) { SS_PDL_ENTRY();
-    if (*a.bad != (unsigned long long)kNoBad) return;
+    if (*a.bad == (unsigned long long)kNoBad) finalize_body(a);
+    if (!a.ticket) return;
+    // the last CTA to finish writes the batch report
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    report_body(a.report);
+    if (threadIdx.x == 0) *a.ticket = 0;
+}
+
+__device__ __forceinline__ void finalize_body(const FinalizeArgs& a) {
     const unsigned lane = lane_id();
     const int W = (int)a.W;
     for (uint32_t g0 = blockIdx.x * blockDim.x; g0 < a.G; g0 += gridDim.x * blockDim.x) {
