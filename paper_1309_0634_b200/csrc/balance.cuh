@@ -51,6 +51,7 @@ struct BalanceArgs {
     const unsigned long long* init_loads;   // split mode: cold-only loads (else tpt)
     const uint8_t* exclude;                 // split mode: hot groups never move
     long long stop_load;                    // split mode: done once max load <= this (0: off)
+    const unsigned long long* stop_sum;     // or: ceil(*stop_sum / P), the mean block load (device)
     // large G (entry lists not staged): entry counts and moved/excluded flags
     // by entry POSITION, so a donor scan reads three coalesced arrays
     int32_t* ecnt;              // [G] gcount[order[i]]
@@ -209,6 +210,7 @@ k_balance(BalanceArgs a) { SS_PDL_ENTRY();
     int nm = 0;                // valid in thread 0
     long long scanned = 0;
     const int pol = a.policy;
+    const long long stop_load = a.stop_sum ? (long long)((*a.stop_sum + P - 1) / P) : a.stop_load;
 
     if (WIDE && (pol == 2 || pol == 3 || pol == 4)) {
         // large G: the donor's entry list is scanned by the whole CTA
@@ -241,7 +243,7 @@ k_balance(BalanceArgs a) { SS_PDL_ENTRY();
                 if (lane == 0) {
                     const int hi = imax, lo = imin;
                     int stop = (nm >= a.cap) || (s.loads[hi] - s.loads[lo] <= a.threshold) ||
-                               (a.stop_load > 0 && s.loads[hi] <= a.stop_load);
+                               (stop_load > 0 && s.loads[hi] <= stop_load);
                     if (!stop && pol == 3) {
                         const int sz = bal_size(s, hi);
                         if (sz <= 0) stop = 1;
@@ -365,7 +367,7 @@ k_balance(BalanceArgs a) { SS_PDL_ENTRY();
                 const int nm_all = __shfl_sync(SS_FULL, nm, 0);
                 if (nm_all >= a.cap) break;
                 if (s.loads[hi] - s.loads[lo] <= a.threshold) break;
-                if (a.stop_load > 0 && s.loads[hi] <= a.stop_load) break;
+                if (stop_load > 0 && s.loads[hi] <= stop_load) break;
                 const int e0 = a.offsets[hi], e1 = a.offsets[hi + 1];
                 int pick = -1;
                 long long pscan = 0, pick_c = -1;

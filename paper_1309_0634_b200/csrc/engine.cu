@@ -937,7 +937,8 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
         SS_CUDA(e, cudaMemsetAsync(sp.part_soff, 0, (e->P + 1) * 4, e->st));
     }
     if ((rc = dalloc(e, &e->spx.hot_g, e->maxS)) || (rc = dalloc(e, &e->spx.n_hot, 1)) ||
-        (rc = dalloc(e, &e->spx.base, e->P)) || (rc = dalloc(e, &e->spx.hot_flag, G)))
+        (rc = dalloc(e, &e->spx.base, e->P)) || (rc = dalloc(e, &e->spx.hot_flag, G)) ||
+        (rc = dalloc(e, &e->spx.n_stored, 1)))
         return rc;
     // -- emission
     if ((rc = dalloc(e, &e->n_res, 1)) || (rc = dalloc(e, &e->r_g, G)) || (rc = dalloc(e, &e->r_cnt, G)) ||
@@ -1466,9 +1467,11 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
         if (split) {
             SS_CUDA(e, cudaMemsetAsync(e->spx.base, 0, e->P * 8, e->side));
             SS_CUDA(e, cudaMemsetAsync(e->spx.n_hot, 0, 4, e->side));
-            const long long hot_min = std::max<long long>(1, n / (2LL * e->P));
-            ss_note_launch(), ss_launch(k_split_hot, 2 * kNumSM, 256, e->P * 4, e->side, e->gcount, (uint32_t)e->G, e->pmap, hot_min, e->maxS,
-                                                                e->spx, e->P, e->bad, e->W);
+            SS_CUDA(e, cudaMemsetAsync(e->spx.n_stored, 0, 8, e->side));
+            ss_note_launch(), ss_launch(k_split_sum, group_grid(e->G), 256, 0, e->side, e->gcount, (uint32_t)e->G, e->W,
+                                        e->spx.n_stored, e->bad);
+            ss_note_launch(), ss_launch(k_split_hot, 2 * kNumSM, 256, e->P * 4, e->side, e->gcount, (uint32_t)e->G, e->pmap,
+                                        (const unsigned long long*)e->spx.n_stored, e->maxS, e->spx, e->P, e->bad, e->W);
             // water-fill the hot groups over this batch's cold loads (the
             // policy's moves apply from the next batch on)
             const SplitPlan& nx = e->plan_buf[plan];
@@ -1509,7 +1512,7 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
                 // the water level of the hot shares is >= the mean
                 a.init_loads = e->spx.base;
                 a.exclude = e->spx.hot_flag;
-                a.stop_load = std::max<long long>(1, (n + e->P - 1) / e->P);
+                a.stop_sum = e->spx.n_stored;      // the mean block load in values to store
             }
             ss_note_launch(), launch_balance(e, a, e->side);
         }

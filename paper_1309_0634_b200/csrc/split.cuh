@@ -8,8 +8,8 @@
 // Split mode plans, from batch t's OWN counts (on the side stream while
 // batch t's placement runs; the window update waits for it), how batch t
 // executes:
-//   1. hot groups: count > mean/2 (so at most 2P of them); everything else
-//      is cold and stays whole on its partition;
+//   1. hot groups: min(count, W) > mean/2 (so at most 2P of them);
+//      everything else is cold and stays whole on its partition;
 //   2. the configured policy moves COLD groups between partitions on the
 //      cold-only loads (same device loop as the reference policies); those
 //      moves keep the reference's one-batch delay (in force from t+1);
@@ -50,21 +50,38 @@ struct SplitScratch {
     int* n_hot;
     unsigned long long* base;   // [P] cold loads
     uint8_t* hot_flag;     // [G]
+    unsigned long long* n_stored;   // sum of min(count, W) of the batch
 };
+
+// Phase 0: the batch's values to store, sum of min(count, W) (the hot
+// threshold is half the mean block load in these units)
+__global__ void __launch_bounds__(256)
+k_split_sum(const int32_t* __restrict__ gcount, uint32_t G, int64_t W, unsigned long long* __restrict__ n_stored,
+            const unsigned long long* __restrict__ bad) { SS_PDL_ENTRY();
+    if (*bad != (unsigned long long)kNoBad) return;
+    unsigned long long s = 0;
+    for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < G; g += gridDim.x * blockDim.x)
+        s += (unsigned long long)min64(gcount[g], W);
+    s = warp_sum(s);
+    if (lane_id() == 0 && s) atomicAdd(n_stored, s);
+}
 
 // Phase 1: hot detection + cold loads.  grid-stride over G; cold loads
 // accumulate per CTA in shared memory (P <= 4096) before one flush.
 __global__ void __launch_bounds__(256)
-k_split_hot(const int32_t* __restrict__ gcount, uint32_t G, const int32_t* __restrict__ pmap, long long hot_min,
-            int maxS, SplitScratch sc, int P, const unsigned long long* __restrict__ bad, int64_t W) { SS_PDL_ENTRY();
+k_split_hot(const int32_t* __restrict__ gcount, uint32_t G, const int32_t* __restrict__ pmap,
+            const unsigned long long* __restrict__ n_stored, int maxS, SplitScratch sc, int P,
+            const unsigned long long* __restrict__ bad, int64_t W) { SS_PDL_ENTRY();
     extern __shared__ uint32_t sh_base[];
     if (*bad != (unsigned long long)kNoBad) return;
+    // hot: more values to store than half the mean block load
+    const long long hot_min = max(1LL, (long long)(*n_stored / (2ull * (unsigned long long)P)));
     for (int i = threadIdx.x; i < P; i += blockDim.x) sh_base[i] = 0;
     __syncthreads();
     for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < G; g += gridDim.x * blockDim.x) {
         const int32_t c = gcount[g];
         uint8_t hot = 0;
-        if (c > hot_min) {
+        if (min64(c, W) > hot_min) {
             const int slot = atomicAdd(sc.n_hot, 1);
             if (slot < maxS) {
                 sc.hot_g[slot] = (int32_t)g;
