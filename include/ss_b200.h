@@ -234,6 +234,21 @@ int  ss_export_moves_dev(ss_engine* e, const void* moves_dev, const int32_t* n_m
 /* received segments (word offsets seg_off[n_seg + 1], host) -> window state */
 int  ss_import_blob_dev(ss_engine* e, const int32_t* blob_dev, const int64_t* seg_off, int n_seg,
                         int max_groups);
+/* int64 keys across GPUs: keys shard by a 16-bit hash bucket; the GPU-level
+ * engine assigns the 2^16 buckets ("groups") to GPUs.  Bucket -> GPU map
+ * (host or device, 65536 entries); route into 12-byte (key lo, key hi,
+ * attr) records; the step on received records; per-bucket counts of the
+ * last batch; migration of the keys of moved buckets (segments per
+ * destination: [n] ++ n x (key lo, key hi, fill, next_pos, sum lo, sum hi,
+ * min, max, span) ++ ring images); import (keys claim slots at once). */
+int  ss_set_bucket_owner(ss_engine* e, const int32_t* owner, int n_dest);
+int  ss_route_records64(ss_engine* e, const int64_t* keys, const int32_t* attrs, int64_t n, void* out_records,
+                        int64_t* counts_dev);
+int  ss_step_records64(ss_engine* e, const void* records, int64_t n, const ss_balancer* cfg, ss_step_report* rep);
+int  ss_bucket_counts_dev(ss_engine* e, int32_t* counts_dev);
+int  ss_export_moves64_dev(ss_engine* e, const void* moves_dev, const int32_t* n_moves_dev, int rank,
+                           int32_t* blob_dev, int64_t blob_cap_words, int64_t* sizes_dev);
+int  ss_import_blob64_dev(ss_engine* e, const int32_t* blob_dev, const int64_t* seg_off, int n_seg);
 
 /* ---- measurement ------------------------------------------------------
  * Kernel classes timed with CUDA events on the engine stream while

@@ -95,6 +95,12 @@ _SIGS = {
     "ss_balance_apply_dev": (C.c_int, [_P, _P, C.POINTER(Balancer), _P, _P, _P]),
     "ss_export_moves_dev": (C.c_int, [_P, _P, _P, C.c_int, _P, _I64, _P]),
     "ss_import_blob_dev": (C.c_int, [_P, _P, _P, C.c_int, C.c_int]),
+    "ss_set_bucket_owner": (C.c_int, [_P, _P, C.c_int]),
+    "ss_route_records64": (C.c_int, [_P, _P, _P, _I64, _P, _P]),
+    "ss_step_records64": (C.c_int, [_P, _P, C.c_int64, C.POINTER(Balancer), C.POINTER(StepReport)]),
+    "ss_bucket_counts_dev": (C.c_int, [_P, _P]),
+    "ss_export_moves64_dev": (C.c_int, [_P, _P, _P, C.c_int, _P, _I64, _P]),
+    "ss_import_blob64_dev": (C.c_int, [_P, _P, _P, C.c_int]),
     "ss_map_keys": (C.c_int, [_P, _P, _I64, _P]),
     "ss_set_trace": (C.c_int, [_P, C.c_int]),
     "ss_trace": (C.c_int, [_P, C.c_int64, _P, _P, C.POINTER(C.c_int64)]),

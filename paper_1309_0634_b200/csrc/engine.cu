@@ -265,6 +265,12 @@ struct ss_engine {
     unsigned long long* route_cnt = nullptr;   // [16]
     uint32_t* route_base = nullptr;            // [16]
     unsigned* fin_ticket = nullptr;            // k_finalize CTAs done (report fold)
+    int32_t* bowner = nullptr;                 // int64 keys across GPUs: bucket -> GPU [kKeyBuckets]
+    int32_t* bdst = nullptr;                   // moved bucket -> destination (export), -1 else
+    int2* mig64 = nullptr;                     // exported (slot, destination) [kMig64Max]
+    longlong4* mig64_copies = nullptr;         // their ring images (ring offset, blob word, span) [kMig64Max]
+    int* n_mig64 = nullptr;
+    int32_t* rec_vals = nullptr;               // attrs of a received int64-key record batch
     longlong4* mig_list = nullptr;             // [kMigMax] (ring offset, blob word, span, -) of exported groups
     int* mig_n = nullptr;
 
@@ -3038,6 +3044,254 @@ extern "C" int ss_import_state(ss_engine* e, const int32_t* groups, int64_t n, c
         if (e->sum_valid) SS_CUDA(e, cudaMemset(e->sum_valid + g, 0, 1));   // ring rewritten
         pos += span;
     }
+    return SS_OK;
+}
+
+// ---- int64 keys across GPUs (keys.cuh: buckets) ------------------------------
+constexpr int kMig64Max = 8192;          // keys migrated per batch and GPU (4 x GPUs buckets of ~G/2^16 keys)
+
+static int ensure_bucket_owner(ss_engine* e) {
+    if (!e->keys64) return fail(e, SS_E_CONFIG, "engine was created with key_bits = 32");
+    int rc;
+    if (!e->bowner) {
+        if ((rc = dalloc(e, &e->bowner, kKeyBuckets)) || (rc = dalloc(e, &e->bdst, kKeyBuckets)) ||
+            (rc = dalloc(e, &e->mig64, kMig64Max)) || (rc = dalloc(e, &e->mig64_copies, kMig64Max)) ||
+            (rc = dalloc(e, &e->n_mig64, 1)) ||
+            (rc = dalloc(e, &e->rec_vals, e->max_batch)))
+            return rc;
+        if (!e->route_cnt && ((rc = dalloc(e, &e->route_cnt, 16)) || (rc = dalloc(e, &e->route_base, 16)))) return rc;
+        if (!e->mig_list && ((rc = dalloc(e, &e->mig_list, kMigMax)) || (rc = dalloc(e, &e->mig_n, 1)))) return rc;
+    }
+    return SS_OK;
+}
+
+// bucket -> GPU map (kKeyBuckets entries in [0, n_dest)), host or device
+extern "C" int ss_set_bucket_owner(ss_engine* e, const int32_t* owner, int n_dest) {
+    if (!e || !owner || n_dest < 1 || n_dest > 16) return fail(e, SS_E_CONFIG, "n_dest must be in [1, 16]");
+    int rc;
+    if ((rc = ensure_bucket_owner(e))) return rc;
+    if (!is_device_ptr(owner))
+        for (int b = 0; b < kKeyBuckets; ++b)
+            if (owner[b] < 0 || owner[b] >= n_dest) return fail(e, SS_E_CONFIG, "owner out of range");
+    SS_CUDA(e, cudaMemcpyAsync(e->bowner, owner, kKeyBuckets * 4, cudaMemcpyDefault, e->st));
+    e->n_dest = n_dest;
+    return SS_OK;
+}
+
+// stable split of an int64-key batch (device keys / attrs) by the owner of
+// each key's bucket into 12-byte (key lo, key hi, attr) records (device);
+// counts_dev[n_dest] per destination, counts_dev[n_dest] = -1 (no bad keys)
+extern "C" int ss_route_records64(ss_engine* e, const int64_t* keys, const int32_t* attrs, int64_t n, void* out_records,
+                                  int64_t* counts_dev) {
+    if (!e || n < 0 || !counts_dev || (n && (!out_records || !keys || !attrs))) return SS_E_CONFIG;
+    if (!e->bowner) return fail(e, SS_E_CONFIG, "ss_set_bucket_owner first");
+    if (n > e->max_batch) return fail(e, SS_E_CONFIG, "batch larger than max_batch");
+    if (n && (!is_device_ptr(keys) || !is_device_ptr(attrs) || !is_device_ptr(out_records)) || !is_device_ptr(counts_dev))
+        return fail(e, SS_E_CONFIG, "ss_route_records64: device buffers required");
+    { int jr = join_side(e); if (jr) return jr; }
+    int rc;
+    if ((rc = engine_alloc_sort(e, n))) return rc;
+    SS_CUDA(e, cudaMemsetAsync(e->route_cnt, 0, 16 * 8, e->st));
+    if (n) {
+        ss_note_launch(), ss_launch(k_key_route_prep, 4 * kNumSM, 256, 0, e->st, (const long long*)keys, n, e->kbuf,
+                                    e->vbuf[1]);
+        ss_note_launch(), ss_launch(k_owner_hist, 2 * kNumSM, 256, 0, e->st, (const uint32_t*)e->kbuf, n,
+                                    (uint32_t)kKeyBuckets, (const int32_t*)e->bowner, e->route_cnt, e->bad);
+    }
+    ss_note_launch(), ss_launch(k_route_base, 1, 32, 0, e->st, (const unsigned long long*)e->route_cnt, e->n_dest,
+                                e->route_base, counts_dev);
+    if (n) {
+        SS_CUDA(e, cudaMemsetAsync(e->tickets, 0, 8, e->st));
+        ss_note_launch(), ss_launch(k_epoch_bump, 1, 1, 0, e->st, e->ep_dev);
+        const int tiles = (int)((n + kSortTile - 1) / kSortTile);
+        ss_note_launch(), ss_launch(k_sort_pass<4, true>, std::min(tiles, 2 * kNumSM), kSortThreads, SortSmem<4>::bytes,
+                                    e->st, (const uint32_t*)e->kbuf, (const int32_t*)e->vbuf[1], e->kbuf2, e->vbuf[0],
+                                    (int)n, 0, 15u, (const uint32_t*)e->route_base, e->status,
+                                    (const uint32_t*)e->ep_dev, 0u, e->tickets, (const unsigned long long*)e->bad, 0,
+                                    (const int32_t*)e->bowner, (const int32_t*)nullptr, SortSeg{});
+        ss_note_launch(), ss_launch(k_key_route_gather, 4 * kNumSM, 256, 0, e->st, (const long long*)keys, attrs,
+                                    (const int32_t*)e->vbuf[0], n, (int32_t*)out_records);
+    }
+    ss_note_launch(), ss_launch(k_route_done, 1, 32, 0, e->st, e->bad, e->n_dest, counts_dev);
+    SS_CUDA(e, cudaGetLastError());
+    return SS_OK;
+}
+
+extern "C" int ss_step_keys64(ss_engine* e, const int64_t* keys, const int32_t* attrs, int64_t n,
+                              const ss_balancer* cfg, ss_step_report* rep);
+
+// one batch of received 12-byte records (device) through the int64-key step
+extern "C" int ss_step_records64(ss_engine* e, const void* records, int64_t n, const ss_balancer* cfg,
+                                 ss_step_report* rep) {
+    if (!e || n < 0 || (n && !records)) return SS_E_CONFIG;
+    int rc;
+    if ((rc = ensure_bucket_owner(e))) return rc;
+    if (n > e->max_batch) return fail(e, SS_E_CONFIG, "batch larger than max_batch");
+    if (n && !is_device_ptr(records)) return fail(e, SS_E_CONFIG, "ss_step_records64: device records required");
+    if (n) ss_note_launch(), ss_launch(k_key_rec_split, 4 * kNumSM, 256, 0, e->st, (const int32_t*)records, n,
+                                       e->stage_keys64, e->rec_vals);
+    return ss_step_keys64(e, (const int64_t*)e->stage_keys64, e->rec_vals, n, cfg, rep);
+}
+
+// per-bucket counts of the last batch (device, kKeyBuckets entries)
+extern "C" int ss_bucket_counts_dev(ss_engine* e, int32_t* out) {
+    if (!e || !out) return SS_E_CONFIG;
+    int rc;
+    if ((rc = ensure_bucket_owner(e))) return rc;
+    SS_CUDA(e, cudaMemsetAsync(out, 0, kKeyBuckets * 4, e->st));
+    ss_note_launch(), ss_launch(k_key_bucket_counts, group_grid(e->G), 256, 0, e->st, e->kt,
+                                (const int32_t*)e->gcount, out);
+    SS_CUDA(e, cudaGetLastError());
+    return SS_OK;
+}
+
+// segments per destination: [n] ++ n x (key lo, key hi, fill, next_pos,
+// sum lo, sum hi, min, max, span) ++ ring images
+constexpr int kMigRec64 = 9;
+
+__global__ void k_export_plan64(const int2* __restrict__ list, const int* __restrict__ n_list, int cap, int n_dest,
+                                int64_t W, const unsigned long long* __restrict__ slot_keys,
+                                const int32_t* __restrict__ fill, const int32_t* __restrict__ next_pos,
+                                const long long* __restrict__ wsum, const int32_t* __restrict__ mn,
+                                const int32_t* __restrict__ mx, const int64_t* __restrict__ off,
+                                int32_t* __restrict__ blob, int64_t blob_cap, int64_t* __restrict__ sizes,
+                                longlong4* __restrict__ copies, int* __restrict__ n_copies) { SS_PDL_ENTRY();
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const int nl = min(*n_list, cap);
+    int64_t ng[16] = {0}, nv[16] = {0};
+    for (int i = 0; i < nl; ++i) {
+        const int2 m = list[i];
+        const int f = fill[m.x];
+        ng[m.y] += 1;
+        nv[m.y] += (int64_t)f < W ? f : W;
+    }
+    int64_t seg[16], base = 0;
+    for (int d = 0; d < n_dest; ++d) {
+        seg[d] = base;
+        const int64_t words = ng[d] ? 1 + kMigRec64 * ng[d] + nv[d] : 0;
+        sizes[d] = words;
+        base += words;
+    }
+    if (base > blob_cap || *n_list > cap) {
+        for (int d = 0; d < n_dest; ++d) sizes[d] = -1;
+        *n_copies = 0;
+        return;
+    }
+    int64_t rec[16], val[16];
+    for (int d = 0; d < n_dest; ++d) {
+        if (ng[d]) blob[seg[d]] = (int32_t)ng[d];
+        rec[d] = seg[d] + 1;
+        val[d] = seg[d] + 1 + kMigRec64 * ng[d];
+    }
+    int nc = 0;
+    for (int i = 0; i < nl; ++i) {
+        const int g = list[i].x, d = list[i].y;
+        const int f = fill[g];
+        const int64_t span = (int64_t)f < W ? f : W;
+        const unsigned long long k = slot_keys[g];
+        const unsigned long long sm = (unsigned long long)wsum[g];
+        int32_t* r = blob + rec[d];
+        r[0] = (int32_t)(uint32_t)k; r[1] = (int32_t)(uint32_t)(k >> 32);
+        r[2] = f; r[3] = next_pos[g];
+        r[4] = (int32_t)(uint32_t)sm; r[5] = (int32_t)(uint32_t)(sm >> 32);
+        r[6] = mn[g]; r[7] = mx[g]; r[8] = (int32_t)span;
+        rec[d] += kMigRec64;
+        if (span) copies[nc++] = make_longlong4(off[g], val[d], span, 0);
+        val[d] += span;
+    }
+    *n_copies = nc;
+}
+
+// window state of the keys in the buckets this GPU gives away
+extern "C" int ss_export_moves64_dev(ss_engine* e, const void* moves_dev, const int32_t* n_moves_dev, int rank,
+                                     int32_t* blob_dev, int64_t blob_cap_words, int64_t* sizes_dev) {
+    if (!e || !moves_dev || !n_moves_dev || !blob_dev || !sizes_dev) return SS_E_CONFIG;
+    int rc;
+    if ((rc = ensure_bucket_owner(e))) return rc;
+    SS_CUDA(e, cudaMemsetAsync(e->bdst, 0xff, kKeyBuckets * 4, e->st));
+    SS_CUDA(e, cudaMemsetAsync(e->n_mig64, 0, 4, e->st));
+    ss_note_launch(), ss_launch(k_key_mig_mark, 4, 256, 0, e->st, (const int4*)moves_dev, n_moves_dev, rank, e->n_dest,
+                                e->bdst);
+    ss_note_launch(), ss_launch(k_key_mig_collect, group_grid(e->G), 256, 0, e->st, e->kt, (const int32_t*)e->bdst,
+                                e->mig64, e->n_mig64, kMig64Max);
+    ss_note_launch(), ss_launch(k_export_plan64, 1, 32, 0, e->st, (const int2*)e->mig64, (const int*)e->n_mig64, kMig64Max,
+                                e->n_dest, e->W, (const unsigned long long*)e->kt.slot_keys, (const int32_t*)e->fill,
+                                (const int32_t*)e->next_pos, (const long long*)e->wsum, (const int32_t*)e->mn,
+                                (const int32_t*)e->mx, (const int64_t*)e->off, blob_dev, blob_cap_words, sizes_dev,
+                                e->mig64_copies, e->n_mig64);
+    ss_note_launch(), ss_launch(k_export_vals, kMig64Max, 256, 0, e->st, (const longlong4*)e->mig64_copies,
+                                (const int*)e->n_mig64, (const int32_t*)e->ring, blob_dev);
+    SS_CUDA(e, cudaGetLastError());
+    return SS_OK;
+}
+
+// CTA s: the records of segment s, one warp per record (value offsets from
+// a serial prefix over the segment's spans by the warp itself)
+__global__ void __launch_bounds__(256)
+k_import64(const int32_t* __restrict__ blob, MigSegs segs, int64_t W, int dense, KeyTable t,
+           int32_t* __restrict__ fill, int32_t* __restrict__ next_pos, long long* __restrict__ wsum,
+           int32_t* __restrict__ mn, int32_t* __restrict__ mx, int64_t* __restrict__ off, int32_t* __restrict__ cap,
+           unsigned long long* __restrict__ pool_top, unsigned long long pool_cap, int* __restrict__ oom,
+           uint8_t* __restrict__ sum_valid, int32_t* __restrict__ ring) { SS_PDL_ENTRY();
+    const int s = blockIdx.x;
+    if (segs.off[s + 1] == segs.off[s]) return;
+    const int32_t* seg = blob + segs.off[s];
+    const int ng = seg[0];
+    const unsigned lane = lane_id();
+    const int nw = blockDim.x >> 5;
+    for (int j = (int)warp_id(); j < ng; j += nw) {
+        const int32_t* r = seg + 1 + kMigRec64 * j;
+        int64_t part = 0;                       // spans of the records before j
+        for (int i = (int)lane; i < j; i += 32) part += seg[1 + kMigRec64 * i + 8];
+        const int64_t vpos = 1 + (int64_t)kMigRec64 * ng + warp_sum(part);
+        const unsigned long long k = ((unsigned long long)(uint32_t)r[1] << 32) | (uint32_t)r[0];
+        const int64_t span = r[8];
+        int64_t o = -1;
+        if (lane == 0) {
+            const int g = key_claim_slot(t, k);
+            if (g >= 0) {
+                o = off[g];
+                if (!dense && cap[g] < span) {
+                    const int64_t ncap = min64(W, max64(span, 16));
+                    const unsigned long long top = atomicAdd(pool_top, (unsigned long long)ncap);
+                    if (top + (unsigned long long)ncap > pool_cap) {
+                        *oom = 1;
+                        o = -1;
+                    } else {
+                        o = (int64_t)top;
+                        off[g] = o;
+                        cap[g] = (int32_t)ncap;
+                    }
+                }
+                if (o >= 0) {
+                    fill[g] = r[2];
+                    next_pos[g] = r[3];
+                    wsum[g] = (long long)(((unsigned long long)(uint32_t)r[5] << 32) | (uint32_t)r[4]);
+                    mn[g] = r[6];
+                    mx[g] = r[7];
+                    if (sum_valid) sum_valid[g] = 0;
+                }
+            }
+        }
+        o = __shfl_sync(SS_FULL, o, 0);
+        if (o < 0) continue;
+        for (int64_t i = lane; i < span; i += 32) ring[o + i] = seg[vpos + i];
+    }
+}
+
+extern "C" int ss_import_blob64_dev(ss_engine* e, const int32_t* blob_dev, const int64_t* seg_off, int n_seg) {
+    if (!e || n_seg < 0 || n_seg > 16 || (n_seg && !seg_off)) return SS_E_CONFIG;
+    int rc;
+    if ((rc = ensure_bucket_owner(e))) return rc;
+    if (n_seg == 0 || seg_off[n_seg] == 0) return SS_OK;
+    if (!blob_dev) return fail(e, SS_E_CONFIG, "ss_import_blob64_dev: null blob");
+    MigSegs sg{};
+    for (int i = 0; i <= n_seg; ++i) sg.off[i] = seg_off[i];
+    sg.n = n_seg;
+    ss_note_launch(), ss_launch(k_import64, (unsigned)n_seg, 256, 0, e->st, blob_dev, sg, e->W, e->dense ? 1 : 0, e->kt,
+                                e->fill, e->next_pos, e->wsum, e->mn, e->mx, e->off, e->cap, e->pool_top, e->pool_cap,
+                                e->oom, e->sum_valid, e->ring);
+    SS_CUDA(e, cudaGetLastError());
     return SS_OK;
 }
 

@@ -431,4 +431,107 @@ k_key_map(const long long* __restrict__ keys, KeyTable t, uint32_t* __restrict__
     }
 }
 
+// ---- int64 keys across GPUs -------------------------------------------------
+// Keys shard by a hash bucket: bucket(k) = top 16 bits of key_hash(k), and
+// the GPU-level engine assigns BUCKETS to GPUs (its "groups" are the 2^16
+// buckets), so routing needs no global key -> group dictionary and moving a
+// bucket migrates every key of it.  Each GPU keeps its own key table.
+constexpr int kKeyBuckets = 1 << 16;
+__device__ __forceinline__ uint32_t key_bucket(unsigned long long k) { return (uint32_t)(key_hash(k) >> 48); }
+
+__global__ void __launch_bounds__(256)
+k_key_route_prep(const long long* __restrict__ keys, int64_t n, uint32_t* __restrict__ bkt,
+                 int32_t* __restrict__ idx) { SS_PDL_ENTRY();
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        bkt[i] = key_bucket((unsigned long long)keys[i]);
+        idx[i] = (int32_t)i;
+    }
+}
+
+// 12-byte records (key lo, key hi, attr) in the routed order
+__global__ void __launch_bounds__(256)
+k_key_route_gather(const long long* __restrict__ keys, const int32_t* __restrict__ attrs,
+                   const int32_t* __restrict__ idx, int64_t n, int32_t* __restrict__ rec) { SS_PDL_ENTRY();
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t i = idx[j];
+        const unsigned long long k = (unsigned long long)keys[i];
+        rec[3 * j] = (int32_t)(uint32_t)k;
+        rec[3 * j + 1] = (int32_t)(uint32_t)(k >> 32);
+        rec[3 * j + 2] = attrs[i];
+    }
+}
+
+__global__ void __launch_bounds__(256)
+k_key_rec_split(const int32_t* __restrict__ rec, int64_t n, long long* __restrict__ keys,
+                int32_t* __restrict__ attrs) { SS_PDL_ENTRY();
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        keys[j] = (long long)(((unsigned long long)(uint32_t)rec[3 * j + 1] << 32) | (uint32_t)rec[3 * j]);
+        attrs[j] = rec[3 * j + 2];
+    }
+}
+
+// per-bucket counts of the last batch (the GPU-level policy's group counts)
+__global__ void __launch_bounds__(256)
+k_key_bucket_counts(KeyTable t, const int32_t* __restrict__ gcount, int32_t* __restrict__ out) { SS_PDL_ENTRY();
+    const int ns = min(*t.n_slots, t.G);
+    for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < ns; g += gridDim.x * blockDim.x) {
+        const int32_t c = gcount[g];
+        if (c) atomicAdd(&out[key_bucket(t.slot_keys[g])], c);
+    }
+}
+
+// migration of moved buckets: mark them with their destination, list this
+// GPU's slots whose key falls in one
+__global__ void __launch_bounds__(256)
+k_key_mig_mark(const int4* __restrict__ moves, const int32_t* __restrict__ n_moves, int rank, int n_dest,
+               int32_t* __restrict__ bdst) { SS_PDL_ENTRY();
+    const int nm = *n_moves;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nm; i += gridDim.x * blockDim.x) {
+        const int4 m = moves[i];
+        if (m.y == rank && m.z != rank && m.z >= 0 && m.z < n_dest && m.x >= 0 && m.x < kKeyBuckets) bdst[m.x] = m.z;
+    }
+}
+__global__ void __launch_bounds__(256)
+k_key_mig_collect(KeyTable t, const int32_t* __restrict__ bdst, int2* __restrict__ list, int* __restrict__ n_list,
+                  int cap) { SS_PDL_ENTRY();
+    const int ns = min(*t.n_slots, t.G);
+    for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < ns; g += gridDim.x * blockDim.x) {
+        const int d = bdst[key_bucket(t.slot_keys[g])];
+        if (d >= 0) {
+            const int i = atomicAdd(n_list, 1);
+            if (i < cap) list[i] = make_int2(g, d);
+        }
+    }
+}
+
+// claim (or find) the entry of a migrated key and give it a slot at once
+// (not through the batch's first-appearance ranking); -1: table full
+__device__ __forceinline__ int key_claim_slot(KeyTable& t, unsigned long long k) {
+    int e;
+    if (k == kEmptyKey) {
+        e = (int)(t.cap_mask + 1);
+        atomicCAS(t.min_key_entry, -1, e);
+    } else {
+        unsigned long long h = key_hash(k) & t.cap_mask;
+        while (true) {
+            const unsigned long long prev = atomicCAS(&t.ent[h].key, kEmptyKey, k);
+            if (prev == kEmptyKey || prev == k) break;
+            h = (h + 1) & t.cap_mask;
+        }
+        e = (int)h;
+    }
+    int s = t.ent[e].slot;
+    if (s < 0) {
+        s = atomicAdd(t.n_slots, 1);
+        if (s >= t.G) {
+            *t.overflow = 1;
+            return -1;
+        }
+        t.ent[e].slot = s;
+        t.slot_ent[s] = e;
+        t.slot_keys[s] = k;
+    }
+    return s;
+}
+
 }  // namespace ss

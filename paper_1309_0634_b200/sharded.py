@@ -35,8 +35,12 @@ the engines and NCCL share:
      batch t therefore take effect from batch t+1, the reference's
      one-iteration delay (harness.py:115-116).
 
-The collectives are plumbing; all compute runs in libss_b200.so.  int64
-keys are single-GPU in this build (the route is over dense u32 group ids).
+int64 keys (``key_bits=64``) shard by a 16-bit key-hash bucket: the GPU-level
+engine's groups are the 2^16 buckets, the route ships 12-byte (key, attr)
+records, every GPU keeps its own key table, and moving a bucket migrates
+all of its keys (each claims a slot on its new GPU at import).
+
+The collectives are plumbing; all compute runs in libss_b200.so.
 """
 
 from __future__ import annotations
@@ -110,9 +114,11 @@ def allreduce_counts(counts, group=None):
 class ShardedEngine:
     """One rank of a key-sharded engine (torch.distributed process group)."""
 
+    KEY_BUCKETS = 1 << 16        # int64 keys: GPU-level "groups" are key-hash buckets (keys.cuh)
+
     def __init__(self, n_groups: int, window, n_partitions: int = 148, aggregates=("count", "sum", "avg"),
                  device: int = 0, max_batch: int = 1 << 24, sub_batch: int = 0, pool_values: int = 0,
-                 group=None, initial: str = "hash", stream=None):
+                 group=None, initial: str = "hash", stream=None, key_bits: int = 32):
         import torch
         import torch.distributed as dist
         self.group = group
@@ -123,22 +129,29 @@ class ShardedEngine:
         self.n_groups = int(n_groups)
         self.dev = torch.device("cuda", device)
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.dev)
+        self.key_bits = int(key_bits)
         self.local = StreamEngine(n_groups, window, n_partitions=n_partitions, aggregates=aggregates,
                                   device=device, max_batch=max_batch, sub_batch=sub_batch,
-                                  pool_values=pool_values, stream=self.stream)
+                                  pool_values=pool_values, stream=self.stream, key_bits=self.key_bits)
         self.window = self.local.window
         # the exchanged batch arrives in fresh buffers of varying size every
         # step: graph replay would recapture every time
         self.local.set_graphs(False)
-        # GPU-level assignment + policy engine ("threads" = GPUs)
-        self.gpu = StreamEngine(n_groups, 1, n_partitions=self.world, aggregates=("count", "sum"),
+        # GPU-level assignment + policy engine ("threads" = GPUs); its groups
+        # are the group ids (u32) or the key-hash buckets (int64 keys)
+        self.n_units = self.n_groups if self.key_bits == 32 else self.KEY_BUCKETS
+        self.gpu = StreamEngine(self.n_units, 1, n_partitions=self.world, aggregates=("count", "sum"),
                                 device=device, max_batch=1 << 16, initial=initial, stream=self.stream)
         owner, _ = self.gpu.get_lists()
         o = np.ascontiguousarray(owner, dtype=np.int32)
-        self.local._check(self.local._lib.ss_set_owner(self.local._h, _ptr(o)[0], self.world))
+        lib = self.local._lib
+        if self.key_bits == 32:
+            self.local._check(lib.ss_set_owner(self.local._h, _ptr(o)[0], self.world))
+        else:
+            self.local._check(lib.ss_set_bucket_owner(self.local._h, _ptr(o)[0], self.world))
         i32, i64 = torch.int32, torch.int64
         self._route_cnt = torch.zeros(self.world + 1, dtype=i64, device=self.dev)
-        self._counts = torch.zeros(self.n_groups, dtype=i32, device=self.dev)
+        self._counts = torch.zeros(self.n_units, dtype=i32, device=self.dev)
         self._owner = torch.as_tensor(o).to(self.dev)
         self._mig_words = torch.zeros(self.world, dtype=i64, device=self.dev)
         self._moves = None
@@ -154,17 +167,30 @@ class ShardedEngine:
         if self._moves is None or self._moves.numel() < 4 * cap:
             self._moves = torch.zeros(4 * cap, dtype=torch.int32, device=self.dev)
         if self._blob is None:
-            # every exported group carries <= W ring values plus its record
-            words = min(cap, 256) * (self.window + 8) + self.world
+            # every exported group carries <= W ring values plus its record;
+            # int64 keys: a moved bucket carries ~G / 2^16 keys (at most 2^28
+            # words in all -- a larger migration raises ExecutionError)
+            per_unit = 1 if self.key_bits == 32 else self.n_groups // self.KEY_BUCKETS + 4
+            words = min(1 << 28, min(cap, 256) * per_unit * (self.window + 9) + self.world)
             self._blob = torch.empty(words, dtype=torch.int32, device=self.dev)
         return cap
 
     def route(self, groups, attrs):
         """Stable split of this rank's slice by owner into 8-byte records
-        (device int64 view) + counts[world + 1] (device; the last entry is
-        the first bad tuple index or -1)."""
+        (device int64 view; int64 keys: 12-byte records as int32 words) +
+        counts[world + 1] (device; the last entry is the first bad tuple
+        index or -1)."""
         import torch
         n = len(groups)
+        if self.key_bits == 64:
+            k = torch.as_tensor(groups).to(self.dev, torch.int64).contiguous()
+            a = torch.as_tensor(attrs).to(self.dev, torch.int32).contiguous()
+            if self._rec is None or self._rec.numel() < max(1, 3 * n):
+                self._rec = torch.empty(max(1, 3 * n), dtype=torch.int32, device=self.dev)
+            self._keep = (k, a)
+            self.local._check(self.local._lib.ss_route_records64(self.local._h, _ptr(k)[0], _ptr(a)[0], n,
+                                                                 _ptr(self._rec)[0], _ptr(self._route_cnt)[0]))
+            return self._rec[:3 * n], self._route_cnt
         if self._rec is None or self._rec.numel() < max(1, n):
             self._rec = torch.empty(max(1, n), dtype=torch.int64, device=self.dev)
         pg, k1 = _ptr(groups)
@@ -185,8 +211,12 @@ class ShardedEngine:
         if recv_w.any():
             seg = np.zeros(self.world + 1, dtype=np.int64)
             np.cumsum(recv_w, out=seg[1:])
-            self.local._check(self.local._lib.ss_import_blob_dev(self.local._h, _ptr(blob_in)[0], _ptr(seg)[0],
-                                                                 self.world, min(256, self._moves.numel() // 4)))
+            lib, h = self.local._lib, self.local._h
+            if self.key_bits == 64:
+                self.local._check(lib.ss_import_blob64_dev(h, _ptr(blob_in)[0], _ptr(seg)[0], self.world))
+            else:
+                self.local._check(lib.ss_import_blob_dev(h, _ptr(blob_in)[0], _ptr(seg)[0], self.world,
+                                                         min(256, self._moves.numel() // 4)))
         self._mig_words.zero_()
         self._keep_blob = blob_in
 
@@ -203,7 +233,8 @@ class ShardedEngine:
     # -- one global batch ------------------------------------------------------
     def step(self, groups, attrs, balancer=None, gpu_balancer=None):
         """groups/attrs: this rank's contiguous slice of the global batch
-        (u32 group ids; host or device).  Returns the tuples this rank ingested."""
+        (u32 group ids, or int64 keys with key_bits=64; host or device).
+        Returns the tuples this rank ingested."""
         import torch
         n = len(groups)
         rec, cnt = self.route(groups, attrs)
@@ -219,21 +250,36 @@ class ShardedEngine:
             raise DataError(f"rank {r} rejected this batch (a tuple outside [0, {self.n_groups}))")
         self._migrate(sent[:, 2], got[:, 2])
         send_c, recv_c = sent[:, 0], got[:, 0]
-        mine = exchange_records(rec, send_c, recv_c, self.group)
-        self._keep_recv = mine
-        self.local.step_records(mine, balancer, sync=False)
+        lib, h = self.local._lib, self.local._h
+        if self.key_bits == 64:
+            mine = exchange_words(rec, 3 * send_c, 3 * recv_c, self.group)
+            self._keep_recv = mine
+            bal = balancer if balancer is not None else self.local.balancer_struct()
+            self.local._check(lib.ss_step_records64(h, _ptr(mine)[0], int(np.sum(recv_c)), C.byref(bal), None))
+        else:
+            mine = exchange_records(rec, send_c, recv_c, self.group)
+            self._keep_recv = mine
+            self.local.step_records(mine, balancer, sync=False)
         if gpu_balancer is not None and gpu_balancer.policy != L.POLICY_CODES["no"]:
-            lib = self.local._lib
             self._move_buffers(gpu_balancer)
-            self.local._check(lib.ss_group_counts(self.local._h, _ptr(self._counts)[0]))
+            if self.key_bits == 64:
+                self.local._check(lib.ss_bucket_counts_dev(h, _ptr(self._counts)[0]))
+            else:
+                self.local._check(lib.ss_group_counts(h, _ptr(self._counts)[0]))
             allreduce_counts(self._counts, self.group)
             self.gpu._check(lib.ss_balance_apply_dev(self.gpu._h, _ptr(self._counts)[0], C.byref(gpu_balancer),
                                                      _ptr(self._moves)[0], _ptr(self._n_moves)[0],
                                                      _ptr(self._owner)[0]))
-            self.local._check(lib.ss_set_owner_dev(self.local._h, _ptr(self._owner)[0], self.world))
-            self.local._check(lib.ss_export_moves_dev(self.local._h, _ptr(self._moves)[0], _ptr(self._n_moves)[0],
-                                                      self.rank, _ptr(self._blob)[0], self._blob.numel(),
-                                                      _ptr(self._mig_words)[0]))
+            if self.key_bits == 64:
+                self.local._check(lib.ss_set_bucket_owner(h, _ptr(self._owner)[0], self.world))
+                self.local._check(lib.ss_export_moves64_dev(h, _ptr(self._moves)[0], _ptr(self._n_moves)[0],
+                                                            self.rank, _ptr(self._blob)[0], self._blob.numel(),
+                                                            _ptr(self._mig_words)[0]))
+            else:
+                self.local._check(lib.ss_set_owner_dev(h, _ptr(self._owner)[0], self.world))
+                self.local._check(lib.ss_export_moves_dev(h, _ptr(self._moves)[0], _ptr(self._n_moves)[0],
+                                                          self.rank, _ptr(self._blob)[0], self._blob.numel(),
+                                                          _ptr(self._mig_words)[0]))
         return int(np.sum(recv_c))
 
     # -- inspection (synchronising; tests and reports only) --------------------

@@ -154,3 +154,71 @@ def test_two_ranks_bad_tuple_rejected_everywhere():
         assert r[2]
     assert res[1][1] == "tuple 37 has group 105, outside [0, 100)"
     assert res[0][1].startswith("rank 1 rejected")
+
+
+def _worker64(rank, world, port, q, G, W, B, nb):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1309_0634_b200 import datagen as D
+        from paper_1309_0634_b200.sharded import ShardedEngine
+        from paper_1309_0634_b200.stream_engine import StreamEngine
+        eng = ShardedEngine(G, W, n_partitions=16, aggregates=("count", "sum", "avg", "min", "max"),
+                            device=0, max_batch=B, sub_batch=16384, key_bits=64)
+        bal = StreamEngine.balancer_struct("prob", max(1, B // 160), 0.5)
+        gbal = StreamEngine.balancer_struct("prob", max(1, B // 20), 0.5)
+        n_moves = 0
+        for b in D.batches(_stream(G, B, nb, True), B):
+            lo, hi = rank * len(b) // world, (rank + 1) * len(b) // world
+            eng.step(D.mix64(b.groups[lo:hi]), b.attrs[lo:hi].astype(np.int32), bal, gbal)
+            n_moves += len(eng.last_gpu_moves)
+        eng.settle()
+        snap = eng.local.snapshot()
+        keys = eng.local.slot_keys()
+        q.put((rank, keys, eng.owner, {k: snap[k][:len(keys)] for k in ("fill", "next_pos", "window_sum", "min", "max")},
+               n_moves, None))
+        eng.close()
+    except Exception:  # pragma: no cover - reported to the parent
+        import traceback
+        q.put((rank, None, None, None, 0, traceback.format_exc()))
+    dist.destroy_process_group()
+
+
+def test_two_ranks_int64_keys_match_oracle():
+    """C5 semantics at a small shape: int64 keys routed by key-hash bucket,
+    drifting skew, GPU-level moves of buckets with their keys' windows; every
+    key's state on the GPU owning its bucket equals the oracle's."""
+    import torch.multiprocessing as mp
+    from oracle import port as O
+    from paper_1309_0634_b200 import datagen as D
+    G, W, B, nb = 3000, 40, 40_000, 6
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker64, args=(r, 2, port, q, G, W, B, nb)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in procs]
+    for p in procs:
+        p.join(timeout=120)
+    for r in res:
+        assert r[5] is None, r[5]
+    store = O.OStore(G, W)
+    for b in D.batches(_stream(G, B, nb, True), B):
+        store.ingest(b.groups, b.attrs)
+    cnt, sm, avg, mn, mx = store.aggregates()
+    seen = np.zeros(G, dtype=np.int64)
+    for rank, keys, owner, snap, n_moves, _ in res:
+        bucket = (D.mix64(keys).view(np.uint64) >> np.uint64(48)).astype(np.int64)
+        mine = owner[bucket] == rank
+        g = D.unmix64(keys[mine])
+        seen[g] += 1
+        assert np.array_equal(snap["fill"][mine], cnt[g])
+        assert np.array_equal(snap["next_pos"][mine], store.next_pos[g])
+        assert np.array_equal(snap["window_sum"][mine], sm[g])
+        assert np.array_equal(snap["min"][mine], mn[g]) and np.array_equal(snap["max"][mine], mx[g])
+    touched = np.flatnonzero(cnt > 0)
+    assert (seen[touched] == 1).all()
+    assert max(r[4] for r in res) > 0
