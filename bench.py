@@ -348,10 +348,10 @@ class Workload:
             # and the GPU-level balancer moves groups between GPUs (weak
             # scaling: per-rank input fixed)
             from paper_1309_0634_b200.sharded import ShardedEngine
-            if kind.endswith("64"):
-                raise SystemExit("int64 keys are single-GPU in this build (route is u32)")
+            # int64 keys route by key-hash bucket (the GPU-level groups)
             self.sharded = ShardedEngine(G, W, n_partitions=P, aggregates=aggs, device=dev.index,
-                                         max_batch=world * B, sub_batch=args.sub_batch)
+                                         max_batch=world * B, sub_batch=args.sub_batch,
+                                         key_bits=64 if kind.endswith("64") else 32)
             self.eng = self.sharded.local
             self.gbal = self.eng.balancer_struct("prob", thread_threshold=max(1, B // 10), pot=0.5)
         else:
