@@ -3321,9 +3321,9 @@ static int map_keys(ss_engine* e, const int64_t* keys, int64_t n, uint32_t* dout
         ss_note_launch(), ss_launch(k_key_count<false>, grid, 512, 0, e->st, dk, n, t, dout, e->S, range, nullptr, nullptr, 0, 0);
     ss_note_launch(), ss_launch(k_key_rank_small, 1, 1024, 0, e->st, t);
     ss_note_launch(), ss_launch(k_key_mark, 2 * kNumSM, 256, 0, e->st, t);
-    ss_note_launch(), ss_launch(k_key_mark_count, nblk, 1024, 0, e->st, t, n, e->kbsum);
+    ss_note_launch(), ss_launch(k_key_mark_count, std::min(nblk, 2 * kNumSM), 1024, 0, e->st, t, n, e->kbsum);
     ss_note_launch(), ss_launch(k_key_mark_scan, 1, 1024, 0, e->st, t, e->kbsum, nblk);
-    ss_note_launch(), ss_launch(k_key_mark_assign, nblk, 1024, 0, e->st, t, n, e->kbsum);
+    ss_note_launch(), ss_launch(k_key_mark_assign, std::min(nblk, 2 * kNumSM), 1024, 0, e->st, t, n, e->kbsum);
     ss_note_launch(), ss_launch(k_key_mark_done, 1, 1, 0, e->st, t);
     ss_note_launch(), ss_launch(k_key_map, 4 * kNumSM, 256, 0, e->st, dk, t, dout, e->S, count ? e->gcnt : nullptr, e->bad);
     SS_CUDA(e, cudaGetLastError());

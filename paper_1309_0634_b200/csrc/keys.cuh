@@ -345,14 +345,19 @@ __global__ void __launch_bounds__(1024)
 k_key_mark_count(KeyTable t, int64_t n, int32_t* __restrict__ bsum) { SS_PDL_ENTRY();
     __shared__ int32_t red[33];
     if (min(*t.n_new, t.G) <= kKeySmall) return;
-    int c = 0;
-    for (int q = 0; q < 4; ++q) {
-        const int64_t i = (int64_t)blockIdx.x * kMarkBlk + q * 1024 + threadIdx.x;
-        c += (i < n && t.mark[i] >= 0);
+    // grid-stride over the 4096-position blocks (a grid of one CTA per
+    // block cost ~7 us of launches per batch even when nothing is new)
+    const int64_t nblk = (n + kMarkBlk - 1) / kMarkBlk;
+    for (int64_t b = blockIdx.x; b < nblk; b += gridDim.x) {
+        int c = 0;
+        for (int q = 0; q < 4; ++q) {
+            const int64_t i = b * kMarkBlk + q * 1024 + threadIdx.x;
+            c += (i < n && t.mark[i] >= 0);
+        }
+        int32_t tot;
+        block_excl_scan(c, red, &tot);
+        if (threadIdx.x == 0) bsum[b] = tot;
     }
-    int32_t tot;
-    block_excl_scan(c, red, &tot);
-    if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
 }
 
 __global__ void __launch_bounds__(1024)
@@ -374,18 +379,21 @@ __global__ void __launch_bounds__(1024)
 k_key_mark_assign(KeyTable t, int64_t n, const int32_t* __restrict__ bsum) { SS_PDL_ENTRY();
     __shared__ int32_t red[33];
     if (min(*t.n_new, t.G) <= kKeySmall) return;
-    int32_t base = bsum[blockIdx.x];
-    for (int q = 0; q < 4; ++q) {
-        const int64_t i = (int64_t)blockIdx.x * kMarkBlk + q * 1024 + threadIdx.x;
-        int e = -1;
-        if (i < n) e = t.mark[i];
-        int32_t tot;
-        const int32_t ex = block_excl_scan(e >= 0 ? 1 : 0, red, &tot);
-        if (e >= 0) {
-            assign_slot(t, e, base + ex);
-            t.mark[i] = -1;
+    const int64_t nblk = (n + kMarkBlk - 1) / kMarkBlk;
+    for (int64_t b = blockIdx.x; b < nblk; b += gridDim.x) {
+        int32_t base = bsum[b];
+        for (int q = 0; q < 4; ++q) {
+            const int64_t i = b * kMarkBlk + q * 1024 + threadIdx.x;
+            int e = -1;
+            if (i < n) e = t.mark[i];
+            int32_t tot;
+            const int32_t ex = block_excl_scan(e >= 0 ? 1 : 0, red, &tot);
+            if (e >= 0) {
+                assign_slot(t, e, base + ex);
+                t.mark[i] = -1;
+            }
+            base += tot;
         }
-        base += tot;
     }
 }
 

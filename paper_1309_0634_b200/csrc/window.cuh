@@ -379,6 +379,9 @@ k_ingest(IngestArgs a) { SS_PDL_ENTRY();
                 if (c < m && m_scan[c] <= t0) l = c;
             }
             int f_scan = m_scan[l], f_next = m_scan[l + 1];
+            // the member's fields stay in registers until the member changes
+            int f_start = m_start[l], f_q0 = m_q0[l], f_s0 = m_s0[l], f_f0 = m_f0[l];
+            int64_t f_off = m_off[l];
             int mi[kILP], sl[kILP];
             int32_t v[kILP], old[kILP];
 #pragma unroll
@@ -393,16 +396,21 @@ k_ingest(IngestArgs a) { SS_PDL_ENTRY();
                         while (m_scan[l + 1] <= t) ++l;
                         f_scan = m_scan[l];
                         f_next = m_scan[l + 1];
+                        f_start = m_start[l];
+                        f_q0 = m_q0[l];
+                        f_s0 = m_s0[l];
+                        f_f0 = m_f0[l];
+                        f_off = m_off[l];
                     }
                     const int rr = t - f_scan;
                     mi[u] = l;
-                    v[u] = a.vals[m_start[l] + rr];
-                    int q = m_q0[l] + rr;
+                    v[u] = a.vals[f_start + rr];
+                    int q = f_q0 + rr;
                     if (q >= W) q -= W;
-                    int s2 = m_s0[l] + rr;
+                    int s2 = f_s0 + rr;
                     if (s2 >= W) s2 -= W;
                     sl[u] = s2;
-                    if (q < m_f0[l]) old[u] = a.ring[m_off[l] + s2];
+                    if (q < f_f0) old[u] = a.ring[f_off + s2];
                 }
             }
             long long d = 0;
