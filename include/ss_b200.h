@@ -185,6 +185,11 @@ int  ss_trace(ss_engine* e, int64_t cap, int32_t* groups, int64_t* sums, int64_t
 int  ss_step_records(ss_engine* e, const void* records, int64_t n, const ss_balancer* cfg, ss_step_report* rep);
 int  ss_step_keys64(ss_engine* e, const int64_t* keys, const int32_t* attrs, int64_t n,
                     const ss_balancer* cfg, ss_step_report* rep);
+/* int64 keys, large G: the probe + count of batch t+1 runs on its own
+ * stream while batch t finishes.  Host inputs always overlap; device key
+ * inputs overlap only when declared ready at call time (ready_inputs = 1:
+ * not produced by work still pending on the engine stream). */
+int  ss_set_key_pipeline(ss_engine* e, int ready_inputs);
 /* key of every assigned slot (keys[n_slots]) */
 int  ss_slot_keys(ss_engine* e, int64_t* keys, int64_t* n_slots);
 

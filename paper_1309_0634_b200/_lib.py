@@ -107,6 +107,7 @@ _SIGS = {
     "ss_step_records": (C.c_int, [_P, _P, C.c_int64, C.POINTER(Balancer), C.POINTER(StepReport)]),
     "ss_step_keys64": (C.c_int, [_P, _P, _P, _I64, C.POINTER(Balancer), C.POINTER(StepReport)]),
     "ss_slot_keys": (C.c_int, [_P, _P, _P]),
+    "ss_set_key_pipeline": (C.c_int, [_P, C.c_int]),
 }
 KERNEL_CLASSES = ("count", "stats", "place", "ingest", "emit", "apply", "balance")
 EXPORTS = tuple(_SIGS)

@@ -265,6 +265,16 @@ struct ss_engine {
     unsigned long long* route_cnt = nullptr;   // [16]
     uint32_t* route_base = nullptr;            // [16]
     unsigned* fin_ticket = nullptr;            // k_finalize CTAs done (report fold)
+    // int64 keys: the probe + count of batch t+1 on its own stream (kst)
+    cudaStream_t kst = nullptr;
+    cudaEvent_t ev_keys[2] = {nullptr, nullptr}, ev_fin[2] = {nullptr, nullptr}, ev_hot = nullptr;
+    bool fin_rec[2] = {false, false}, hot_rec = false;
+    bool key_pipe_dev = false;                 // device key inputs are ready when passed (ss_set_key_pipeline)
+    cudaEvent_t ev_in = nullptr;
+    int32_t* gcnt_buf[2] = {nullptr, nullptr};
+    uint32_t* skeys_buf[2] = {nullptr, nullptr};
+    unsigned long long* key_bad = nullptr;
+    int kpar = 0;
     int32_t* bowner = nullptr;                 // int64 keys across GPUs: bucket -> GPU [kKeyBuckets]
     int32_t* bdst = nullptr;                   // moved bucket -> destination (export), -1 else
     int2* mig64 = nullptr;                     // exported (slot, destination) [kMig64Max]
@@ -609,6 +619,7 @@ extern "C" void ss_destroy(ss_engine* e) {
     cudaSetDevice(e->cfg.device);
     cudaStreamSynchronize(e->st);
     if (e->cp) cudaStreamSynchronize(e->cp);
+    if (e->kst) cudaStreamSynchronize(e->kst);
     for (auto& g : e->graphs) cudaGraphExecDestroy(g.exec);
     for (void* p : e->allocs) cudaFree(p);
     if (e->h_rep) cudaFreeHost(e->h_rep);
@@ -621,6 +632,13 @@ extern "C" void ss_destroy(ss_engine* e) {
         if (e->ev_freed[b]) cudaEventDestroy(e->ev_freed[b]);
         if (e->ev_emit[b]) cudaEventDestroy(e->ev_emit[b]);
     }
+    for (int b = 0; b < 2; ++b) {
+        if (e->ev_keys[b]) cudaEventDestroy(e->ev_keys[b]);
+        if (e->ev_fin[b]) cudaEventDestroy(e->ev_fin[b]);
+    }
+    if (e->ev_hot) cudaEventDestroy(e->ev_hot);
+    if (e->ev_in) cudaEventDestroy(e->ev_in);
+    if (e->kst) cudaStreamDestroy(e->kst);
     if (e->cp) cudaStreamDestroy(e->cp);
     if (e->side) cudaStreamDestroy(e->side);
     if (e->ev_stats) cudaEventDestroy(e->ev_stats);
@@ -907,6 +925,23 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
             return rc;
         t.cap_mask = cap - 1;
         t.G = (int)G;
+        // pipelined key probe (large G: the probe also counts the batch)
+        if (G > 16384 && !e->stream_scope && !getenv("SS_B200_NO_KEY_PIPE")) {
+            SS_CUDA(e, cudaStreamCreateWithFlags(&e->kst, cudaStreamNonBlocking));
+            for (int b = 0; b < 2; ++b) {
+                SS_CUDA(e, cudaEventCreateWithFlags(&e->ev_keys[b], cudaEventDisableTiming));
+                SS_CUDA(e, cudaEventCreateWithFlags(&e->ev_fin[b], cudaEventDisableTiming));
+            }
+            SS_CUDA(e, cudaEventCreateWithFlags(&e->ev_hot, cudaEventDisableTiming));
+            SS_CUDA(e, cudaEventCreateWithFlags(&e->ev_in, cudaEventDisableTiming));
+            e->gcnt_buf[0] = e->gcnt;
+            e->skeys_buf[0] = e->stage_keys;
+            if ((rc = dalloc(e, &e->gcnt_buf[1], (size_t)e->n_sub_max * G)) ||
+                (rc = dalloc(e, &e->skeys_buf[1], e->max_batch)) || (rc = dalloc(e, &e->key_bad, 1)))
+                return rc;
+            SS_CUDA(e, cudaMemsetAsync(e->gcnt_buf[1], 0, (size_t)e->n_sub_max * G * 4, e->st));
+            ss_note_launch(), ss_launch(k_set_bad, 1, 1, 0, e->st, e->key_bad);
+        }
         ss_note_launch(), ss_launch(k_key_init, 296, 256, 0, e->st, t.ent, (int64_t)cap + 1);
         SS_CUDA(e, cudaMemsetAsync(t.first, 0xff, (cap + 1) * 4, e->st));
         SS_CUDA(e, cudaMemsetAsync(t.mark, 0xff, e->max_batch * 4, e->st));
@@ -1014,9 +1049,19 @@ extern "C" int ss_set_stream(ss_engine* e, void* stream) {
     return SS_OK;
 }
 
+// int64 keys: device key inputs are complete when ss_step_keys64 is called
+// (not produced by pending engine-stream work), so the next batch's probe
+// may run ahead on the key stream (host inputs always may)
+extern "C" int ss_set_key_pipeline(ss_engine* e, int ready_inputs) {
+    if (!e) return SS_E_CONFIG;
+    e->key_pipe_dev = ready_inputs != 0;
+    return SS_OK;
+}
+
 extern "C" int ss_sync(ss_engine* e) {
     if (!e) return SS_E_CONFIG;
     { int jr = join_side(e); if (jr) return jr; }
+    if (e->kst) SS_CUDA(e, cudaStreamSynchronize(e->kst));
     SS_CUDA(e, cudaStreamSynchronize(e->st));
     SS_CUDA(e, cudaGetLastError());
     return SS_OK;
@@ -1463,6 +1508,11 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
                                                         std::max<long long>(32, n / (4 * kHotCache)), e->hot_of,
                                                         e->hot_g, e->n_hot_dev, e->bad,
                                                         e->keys64 ? (int32_t*)e->kt.ent : nullptr, e->kt.slot_ent);
+            // the next batch's key probe (key stream) may start: it reads the hot cache
+            if (e->kst) {
+                SS_CUDA(e, record_ext(e, e->ev_hot, e->st));
+                e->hot_rec = true;
+            }
         }
     }
     e->alg_input += (e->keys64 ? 12 : 8) * n;   // the batch is read once: key + attr bytes
@@ -1720,6 +1770,16 @@ static int enqueue_report(ss_engine* e, int64_t n, bool has_policy, cudaStream_t
 }
 
 
+// the key stream's bad-tuple flag into the batch's (engine stream)
+__global__ void k_merge_bad(unsigned long long* __restrict__ bad, unsigned long long* __restrict__ key_bad) { SS_PDL_ENTRY();
+    if (threadIdx.x != 0) return;
+    const unsigned long long k = *key_bad;
+    if (k != (unsigned long long)kNoBad) {
+        if (k < *bad) *bad = k;
+        *key_bad = (unsigned long long)kNoBad;
+    }
+}
+
 // free the key-table entries a rejected int64-key batch claimed
 static void key_rollback(ss_engine* e) {
     const int64_t n_ent = (int64_t)e->kt.cap_mask + 2;
@@ -1731,6 +1791,7 @@ static void key_rollback(ss_engine* e) {
 static int check_report(ss_engine* e, const uint32_t* dk) {
     SS_CUDA(e, cudaStreamSynchronize(e->st));
     SS_CUDA(e, cudaStreamSynchronize(e->side));
+    if (e->kst) SS_CUDA(e, cudaStreamSynchronize(e->kst));
     SS_CUDA(e, cudaGetLastError());
     if (e->h_rep->bad != (unsigned long long)kNoBad) {
         if (e->keys64) key_rollback(e);
@@ -3300,32 +3361,33 @@ extern "C" int ss_import_blob64_dev(ss_engine* e, const int32_t* blob_dev, const
 // --------------------------------------------------------------------------
 // keys -> slots (and, with `count`, the batch's group histogram: the
 // fused step then skips its count kernel)
-static int map_keys(ss_engine* e, const int64_t* keys, int64_t n, uint32_t* dout, bool count) {
+static int map_keys(ss_engine* e, const int64_t* keys, int64_t n, uint32_t* dout, bool count, cudaStream_t st,
+                    int32_t* gcnt, unsigned long long* bad) {
     const long long* dk;
     if (is_device_ptr(keys)) dk = (const long long*)keys;
     else {
-        if (n) SS_CUDA(e, cudaMemcpyAsync(e->stage_keys64, keys, n * 8, cudaMemcpyHostToDevice, e->st));
+        if (n) SS_CUDA(e, cudaMemcpyAsync(e->stage_keys64, keys, n * 8, cudaMemcpyHostToDevice, st));
         dk = e->stage_keys64;
     }
     if (n == 0) return SS_OK;
     KeyTable& t = e->kt;
-    SS_CUDA(e, cudaMemcpyAsync(t.prev_slots, t.n_slots, 4, cudaMemcpyDeviceToDevice, e->st));
+    SS_CUDA(e, cudaMemcpyAsync(t.prev_slots, t.n_slots, 4, cudaMemcpyDeviceToDevice, st));
     const int nblk = (int)((n + kMarkBlk - 1) / kMarkBlk);
     const int64_t range = kCountChunk;                   // divides the count chunk S
     const unsigned grid = (unsigned)((n + range - 1) / range);
-    SS_CUDA(e, cudaMemsetAsync(t.n_pend, 0, 4, e->st));
+    SS_CUDA(e, cudaMemsetAsync(t.n_pend, 0, 4, st));
     if (count)
-        ss_note_launch(), ss_launch(k_key_count<true>, grid, 512, kHotCache * 4, e->st, dk, n, t, dout, e->S, range, e->gcnt,
+        ss_note_launch(), ss_launch(k_key_count<true>, grid, 512, kHotCache * 4, st, dk, n, t, dout, e->S, range, gcnt,
                                                                               e->hot_g, kHotCache, e->key_agg);
     else
-        ss_note_launch(), ss_launch(k_key_count<false>, grid, 512, 0, e->st, dk, n, t, dout, e->S, range, nullptr, nullptr, 0, 0);
-    ss_note_launch(), ss_launch(k_key_rank_small, 1, 1024, 0, e->st, t);
-    ss_note_launch(), ss_launch(k_key_mark, 2 * kNumSM, 256, 0, e->st, t);
-    ss_note_launch(), ss_launch(k_key_mark_count, std::min(nblk, 2 * kNumSM), 1024, 0, e->st, t, n, e->kbsum);
-    ss_note_launch(), ss_launch(k_key_mark_scan, 1, 1024, 0, e->st, t, e->kbsum, nblk);
-    ss_note_launch(), ss_launch(k_key_mark_assign, std::min(nblk, 2 * kNumSM), 1024, 0, e->st, t, n, e->kbsum);
-    ss_note_launch(), ss_launch(k_key_mark_done, 1, 1, 0, e->st, t);
-    ss_note_launch(), ss_launch(k_key_map, 4 * kNumSM, 256, 0, e->st, dk, t, dout, e->S, count ? e->gcnt : nullptr, e->bad);
+        ss_note_launch(), ss_launch(k_key_count<false>, grid, 512, 0, st, dk, n, t, dout, e->S, range, nullptr, nullptr, 0, 0);
+    ss_note_launch(), ss_launch(k_key_rank_small, 1, 1024, 0, st, t);
+    ss_note_launch(), ss_launch(k_key_mark, 2 * kNumSM, 256, 0, st, t);
+    ss_note_launch(), ss_launch(k_key_mark_count, std::min(nblk, 2 * kNumSM), 1024, 0, st, t, n, e->kbsum);
+    ss_note_launch(), ss_launch(k_key_mark_scan, 1, 1024, 0, st, t, e->kbsum, nblk);
+    ss_note_launch(), ss_launch(k_key_mark_assign, std::min(nblk, 2 * kNumSM), 1024, 0, st, t, n, e->kbsum);
+    ss_note_launch(), ss_launch(k_key_mark_done, 1, 1, 0, st, t);
+    ss_note_launch(), ss_launch(k_key_map, 4 * kNumSM, 256, 0, st, dk, t, dout, e->S, count ? gcnt : nullptr, bad);
     SS_CUDA(e, cudaGetLastError());
     return SS_OK;
 }
@@ -3338,7 +3400,7 @@ extern "C" int ss_map_keys(ss_engine* e, const int64_t* keys, int64_t n, uint32_
     { int jr = join_side(e); if (jr) return jr; }
     const bool dev = is_device_ptr(out_slots);
     int rc;
-    if ((rc = map_keys(e, keys, n, dev ? out_slots : e->stage_keys, false))) return rc;
+    if ((rc = map_keys(e, keys, n, dev ? out_slots : e->stage_keys, false, e->st, e->gcnt, e->bad))) return rc;
     if (!dev && n) SS_CUDA(e, cudaMemcpyAsync(out_slots, e->stage_keys, n * 4, cudaMemcpyDeviceToHost, e->st));
     SS_CUDA(e, cudaStreamSynchronize(e->st));
     return SS_OK;
@@ -3365,10 +3427,46 @@ extern "C" int ss_step_keys64(ss_engine* e, const int64_t* keys, const int32_t* 
     }
     // large G: the key probe also counts the batch (one pass over the keys)
     const bool count = e->G > 16384 && !e->stream_scope;
-    if ((rc = map_keys(e, dk, n, e->stage_keys, count))) return rc;
+    if (!e->kst) {
+        if ((rc = map_keys(e, dk, n, e->stage_keys, count, e->st, e->gcnt, e->bad))) return rc;
+        e->pre_counted = count;
+        rc = ss_step(e, e->stage_keys, dv, n, cfg, rep);
+        e->pre_counted = false;
+        return rc;
+    }
+    // Pipelined: the probe + count of this batch runs on the key stream,
+    // overlapping the previous batch's placement and window update, into
+    // its own slot buffer and count rows (alternating).  It waits for the
+    // previous batch's hot-group cache (k_hot_select) and for the batch
+    // that last used these count rows (finalize clears them); the engine
+    // stream waits for it.  A bad tuple is flagged on the key stream's own
+    // flag and merged into the batch's flag on the engine stream.
+    const int b = e->kpar;
+    e->kpar ^= 1;
+    if (e->cur_stage >= 0) {
+        SS_CUDA(e, cudaStreamWaitEvent(e->kst, e->ev_staged[e->cur_stage], 0));
+    } else if (!e->key_pipe_dev) {
+        // device keys may be produced by work already on the engine stream
+        // (e.g. the multi-GPU record split): wait for it -- no overlap
+        SS_CUDA(e, cudaEventRecord(e->ev_in, e->st));
+        SS_CUDA(e, cudaStreamWaitEvent(e->kst, e->ev_in, 0));
+    }
+    if (e->hot_rec) SS_CUDA(e, cudaStreamWaitEvent(e->kst, e->ev_hot, 0));
+    if (e->fin_rec[b]) SS_CUDA(e, cudaStreamWaitEvent(e->kst, e->ev_fin[b], 0));
+    if ((rc = map_keys(e, dk, n, e->skeys_buf[b], count, e->kst, e->gcnt_buf[b], e->key_bad))) return rc;
+    SS_CUDA(e, cudaEventRecord(e->ev_keys[b], e->kst));
+    SS_CUDA(e, cudaStreamWaitEvent(e->st, e->ev_keys[b], 0));
+    ss_note_launch(), ss_launch(k_merge_bad, 1, 32, 0, e->st, e->bad, e->key_bad);
+    int32_t* const gcnt0 = e->gcnt;
+    e->gcnt = e->gcnt_buf[b];
     e->pre_counted = count;
-    rc = ss_step(e, e->stage_keys, dv, n, cfg, rep);
+    rc = ss_step(e, e->skeys_buf[b], dv, n, cfg, rep);
     e->pre_counted = false;
+    e->gcnt = gcnt0;
+    if (rc == SS_OK) {
+        SS_CUDA(e, cudaEventRecord(e->ev_fin[b], e->st));
+        e->fin_rec[b] = true;
+    }
     return rc;
 }
 

@@ -428,6 +428,12 @@ class StreamEngine:
         self._check(self._lib.ss_slot_keys(self._h, _ptr(out)[0], C.byref(n)))
         return out[:n.value]
 
+    def set_key_pipeline(self, ready_inputs: bool = True):
+        """int64 keys: declare device key inputs complete when step() is
+        called, so the next batch's key probe may overlap this one (host
+        inputs always do)."""
+        self._check(self._lib.ss_set_key_pipeline(self._h, int(bool(ready_inputs))))
+
     def set_trace(self, enable: bool = True):
         """Per-tuple trace mode: every batch keeps all tuples
         and records (group, window sum after the tuple) per tuple."""
