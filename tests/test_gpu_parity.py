@@ -381,3 +381,37 @@ def test_int64_keys_match_oracle(policy):
     s3 = eng.snapshot()
     assert np.array_equal(s3["fill"], store.fill) and np.array_equal(s3["window_sum"], store.window_sum)
     eng.close()
+
+
+@pytest.mark.parametrize("ready", [True, False])
+def test_int64_keys_pipelined_probe(ready):
+    """Large G: the key probe + count of batch t+1 runs on its own stream
+    while batch t finishes (alternating slot buffers and count rows).  Device
+    inputs declared ready overlap; the rest wait.  Unsynchronised steps, one
+    host-input batch in the middle, windows checked against the oracle."""
+    import torch
+    from paper_1309_0634_b200.stream_engine import StreamEngine
+    G, W, P, B = 20_000, 100, 64, 200_000
+    spec = D.DatasetSpec(D.DatasetKind.PERMUTED_ZIPF, 6 * B, G, 1.1, 5)
+    bl = list(D.batches(D.stream_for(spec), B))
+    slot_of = _first_appearance_ids([b.groups for b in bl], G)
+    eng = _engine(G, W, P=P, key_bits=64, max_batch=B, aggregates=("count", "sum", "avg", "min", "max"))
+    eng.set_key_pipeline(ready)
+    bal = StreamEngine.balancer_struct("prob", max(1, B // (10 * P)), 0.5, split=True)
+    dev = [(torch.as_tensor(D.mix64(b.groups)).cuda(), torch.as_tensor(b.attrs.astype(np.int32)).cuda()) for b in bl]
+    torch.cuda.synchronize()
+    for i, b in enumerate(bl):
+        if i == 3:
+            eng.step(D.mix64(b.groups), b.attrs, bal, sync=False)       # host input
+        else:
+            eng.step(*dev[i], bal, sync=False)
+    store = O.OStore(G, W)
+    for b in bl:
+        store.ingest(slot_of[b.groups], b.attrs)
+    s = eng.snapshot()
+    n = int((slot_of >= 0).sum())
+    assert np.array_equal(s["fill"][:n], store.fill[:n]) and np.array_equal(s["window_sum"][:n], store.window_sum[:n])
+    assert np.array_equal(s["next_pos"][:n], store.next_pos[:n])
+    cnt, sm, avg, mn, mx = store.aggregates()
+    assert np.array_equal(s["min"][:n], mn[:n]) and np.array_equal(s["max"][:n], mx[:n])
+    eng.close()
