@@ -25,4 +25,7 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_c
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_count|k_sort_pass|k_ingest|k_chunk|k_finalize' -s 120 -c 7 -o $O/full_c3 $B --config c3 > $O/ncu_c3.log 2>&1
 timeout 1200 compute-sanitizer --tool memcheck --print-limit 20 python scripts/sanitize_cases.py > $O/memcheck.log 2>&1
 timeout 1200 compute-sanitizer --tool racecheck --racecheck-report hazard --print-limit 20 python scripts/sanitize_cases.py > $O/racecheck.log 2>&1
+
+timeout 1500 python scripts/compare_policies.py --config c4 --steps 6 --warmup 12 > $O/compare_c4.log 2>&1
+timeout 900 python scripts/compare_policies.py --config c3 --steps 6 --warmup 12 > $O/compare_c3.log 2>&1
 echo done
