@@ -36,7 +36,7 @@ def _stream(G, B, nb, drift):
     return D.stream_for(D.DatasetSpec(D.DatasetKind.ZIPF, nb * B, G, 1.2, 31))
 
 
-def _worker(rank, world, port, q, G, W, B, nb, gpu_policy, drift):
+def _worker(rank, world, port, q, G, W, B, nb, gpu_policy, drift, pool=0):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -46,7 +46,7 @@ def _worker(rank, world, port, q, G, W, B, nb, gpu_policy, drift):
         from paper_1309_0634_b200.sharded import ShardedEngine
         from paper_1309_0634_b200.stream_engine import StreamEngine
         eng = ShardedEngine(G, W, n_partitions=16, aggregates=("count", "sum", "avg", "min", "max"),
-                            device=0, max_batch=B, sub_batch=16384)
+                            device=0, max_batch=B, sub_batch=16384, pool_values=pool)
         bal = StreamEngine.balancer_struct("prob", max(1, B // 160), 0.5)
         gbal = StreamEngine.balancer_struct(gpu_policy, max(1, B // 20), 0.5)
         n_moves = 0
@@ -67,8 +67,11 @@ def _worker(rank, world, port, q, G, W, B, nb, gpu_policy, drift):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("gpu_policy,drift", [("no", False), ("prob", False), ("prob", True), ("best", True)])
-def test_two_ranks_match_oracle(gpu_policy, drift):
+@pytest.mark.parametrize("gpu_policy,drift,pool", [("no", False, 0), ("prob", False, 0), ("prob", True, 0),
+                                                    ("best", True, 0), ("prob", True, 3000 * 40 * 4)])
+def test_two_ranks_match_oracle(gpu_policy, drift, pool):
+    """(pool > 0: occupancy-proportional rings, so imported windows reserve
+    ring space on the device)"""
     import torch.multiprocessing as mp
     from oracle import port as O
     from paper_1309_0634_b200 import datagen as D
@@ -76,7 +79,7 @@ def test_two_ranks_match_oracle(gpu_policy, drift):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, G, W, B, nb, gpu_policy, drift)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, G, W, B, nb, gpu_policy, drift, pool)) for r in range(2)]
     for p in procs:
         p.start()
     res = [q.get(timeout=600) for _ in procs]
@@ -156,7 +159,7 @@ def test_two_ranks_bad_tuple_rejected_everywhere():
     assert res[0][1].startswith("rank 1 rejected")
 
 
-def _worker64(rank, world, port, q, G, W, B, nb):
+def _worker64(rank, world, port, q, G, W, B, nb, pool=0):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -166,7 +169,7 @@ def _worker64(rank, world, port, q, G, W, B, nb):
         from paper_1309_0634_b200.sharded import ShardedEngine
         from paper_1309_0634_b200.stream_engine import StreamEngine
         eng = ShardedEngine(G, W, n_partitions=16, aggregates=("count", "sum", "avg", "min", "max"),
-                            device=0, max_batch=B, sub_batch=16384, key_bits=64)
+                            device=0, max_batch=B, sub_batch=16384, key_bits=64, pool_values=pool)
         bal = StreamEngine.balancer_struct("prob", max(1, B // 160), 0.5)
         gbal = StreamEngine.balancer_struct("prob", max(1, B // 20), 0.5)
         n_moves = 0
@@ -186,7 +189,8 @@ def _worker64(rank, world, port, q, G, W, B, nb):
     dist.destroy_process_group()
 
 
-def test_two_ranks_int64_keys_match_oracle():
+@pytest.mark.parametrize("pool", [0, 3000 * 40 * 4])
+def test_two_ranks_int64_keys_match_oracle(pool):
     """C5 semantics at a small shape: int64 keys routed by key-hash bucket,
     drifting skew, GPU-level moves of buckets with their keys' windows; every
     key's state on the GPU owning its bucket equals the oracle's."""
@@ -197,7 +201,7 @@ def test_two_ranks_int64_keys_match_oracle():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker64, args=(r, 2, port, q, G, W, B, nb)) for r in range(2)]
+    procs = [ctx.Process(target=_worker64, args=(r, 2, port, q, G, W, B, nb, pool)) for r in range(2)]
     for p in procs:
         p.start()
     res = [q.get(timeout=600) for _ in procs]
