@@ -45,3 +45,25 @@ def test_wide_group_ids_raise_instead_of_wrapping():
         _keys_u32(np.array([0, 1, -7], dtype=np.int64), 100)
     ok = _keys_u32(torch.tensor([0, 99], dtype=torch.int64), 100)
     assert ok.dtype == torch.int32 and ok.tolist() == [0, 99]
+
+
+def test_hash_lists_blocks_and_balance():
+    """Static hash partitioning (stream_engine.hash_lists): a partition of
+    every id, ids ascending inside each list; large domains hash blocks of 8
+    consecutive ids (one 32-byte sector of each per-group array), small ones
+    single ids."""
+    import numpy as np
+    from paper_1309_0634_b200.stream_engine import hash_lists
+    for G, P, block in ((1_000_000, 148, 8), (1000, 148, 1), (100_000, 148, 8), (5000, 64, 1)):
+        lists = hash_lists(G, P)
+        flat = np.concatenate([np.asarray(l, dtype=np.int64) for l in lists])
+        assert np.array_equal(np.sort(flat), np.arange(G))
+        assert all(np.all(np.diff(l) > 0) for l in lists if len(l) > 1)
+        owner = np.empty(G, dtype=np.int64)
+        for p, l in enumerate(lists):
+            owner[l] = p
+        blocks = owner[: G // block * block].reshape(-1, block)
+        assert (blocks == blocks[:, :1]).all()              # a block never straddles partitions
+        if G >= 1_000_000:
+            sizes = np.array([len(l) for l in lists])
+            assert sizes.max() <= 1.15 * G / P
