@@ -155,6 +155,7 @@ struct ss_engine {
     bool os = false;
     int os_digit = kOsBitsWide;            // digit width: kOsBitsWide (measured best: C4 0.42 ms vs 0.49 with 7 bits)
     int os_match = 1;                      // ranking: ballot matches (0), alternating with MATCH (1), MATCH (2)
+    bool os2 = false;                      // 10-bit passes: 512-thread, 2-CTA-per-SM variant (SS_B200_OS2)
     int os_npass = 0, os_shift[kOsMaxPass] = {0, 0, 0, 0}, os_bits[kOsMaxPass] = {0, 0, 0, 0};
     uint32_t* os_hist = nullptr;
     uint32_t* os_bsum = nullptr;
@@ -864,6 +865,7 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
         const int bits = bits_for(G);
         if (const char* ob = getenv("SS_B200_OS_BITS")) e->os_digit = atoi(ob) == kOsBitsWide ? kOsBitsWide : kOsBits;
         if (const char* om = getenv("SS_B200_OS_MATCH")) e->os_match = atoi(om);
+        if (const char* o2 = getenv("SS_B200_OS2")) e->os2 = o2[0] == '1';
         e->os_npass = (bits + e->os_digit - 1) / e->os_digit;
         if (e->os_npass > kOsMaxPass) e->os = false;
         int sh = 0;
@@ -1026,6 +1028,8 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
                                     (int)OsSmem<kOsBits>::bytes));
     SS_CUDA(e, cudaFuncSetAttribute(k_os_pass<kOsBitsWide>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)OsSmem<kOsBitsWide>::bytes));
+    SS_CUDA(e, cudaFuncSetAttribute(k_os_pass2<kOsBitsWide>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)Os2Smem<kOsBitsWide>::bytes));
     SS_CUDA(e, cudaFuncSetAttribute(k_bk_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BkSmem::bytes));
     SS_CUDA(e, cudaFuncSetAttribute(k_bk_local, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BkLocSmem::bytes));
     for (int b = 0; b <= 14; ++b) {
@@ -1260,6 +1264,13 @@ static void launch_os_pass_t(ss_engine* e, const OsArgs& a, unsigned tiles, unsi
     ss_note_launch(), ss_launch(k_os_red<BITS>, blks, 1024, 0, e->st, a);
     ss_note_launch(), ss_launch(k_os_top<BITS>, (1 << BITS) / 32, 1024, 0, e->st, a);
     ss_note_launch(), ss_launch(k_os_down<BITS>, blks, 1024, 0, e->st, a);
+    if constexpr (BITS == kOsBitsWide) {
+        if (e->os2) {
+            ss_note_launch(), ss_launch(k_os_pass2<BITS>, std::min<unsigned>(tiles, 2 * kNumSM), kOs2Threads,
+                                        Os2Smem<BITS>::bytes, e->st, a);
+            return;
+        }
+    }
     ss_note_launch(), ss_launch(k_os_pass<BITS>, std::min<unsigned>(tiles, kNumSM), kOsThreads, OsSmem<BITS>::bytes, e->st, a);
 }
 static void launch_os_pass(ss_engine* e, const OsArgs& a, unsigned tiles, unsigned blks) {

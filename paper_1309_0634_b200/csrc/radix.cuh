@@ -412,4 +412,157 @@ k_os_pass(OsArgs a) { SS_PDL_ENTRY();
     }
 }
 
+// Variant for wide digits: 512 threads x 16 items per 8192-tuple tile, a
+// single staged tile and 16 per-warp histograms (104 KB of shared memory,
+// 64 registers), so TWO CTAs share an SM and one's ranking overlaps the
+// other's copies and write-out (the 1024-thread kernel above holds a whole
+// SM and double-buffers instead).  Same ranking / scan / local sort.
+constexpr int kOs2Threads = 512;
+constexpr int kOs2Warps = kOs2Threads / 32;
+constexpr int kOs2Items = kOsTile / kOs2Threads;     // 16
+
+template <int BITS>
+struct Os2Smem {
+    static constexpr int BINS = 1 << BITS;
+    static constexpr size_t keys = 0;                                   // u32[kOsTile]
+    static constexpr size_t vals = keys + (size_t)kOsTile * 4;          // i32[kOsTile]
+    static constexpr size_t wh = vals + (size_t)kOsTile * 4;            // u16[kOs2Warps][BINS]
+    static constexpr size_t base = wh + (size_t)kOs2Warps * BINS * 2;   // u32[BINS]
+    static constexpr size_t lst = base + (size_t)BINS * 4;              // u32[BINS]
+    static constexpr size_t bar = lst + (size_t)BINS * 4;               // u64
+    static constexpr size_t bytes = bar + 16;
+};
+
+template <int BITS>
+__global__ void __launch_bounds__(kOs2Threads, 2)
+k_os_pass2(OsArgs a) { SS_PDL_ENTRY();
+    constexpr int BINS = 1 << BITS;
+    constexpr int DPT = (BINS + kOs2Threads - 1) / kOs2Threads;        // digits per thread (scans)
+    using SM = ss::Os2Smem<BITS>;
+    extern __shared__ __align__(16) unsigned char osm[];
+    uint32_t* sk = (uint32_t*)(osm + SM::keys);
+    int32_t* sv = (int32_t*)(osm + SM::vals);
+    uint16_t* wh = (uint16_t*)(osm + SM::wh);
+    uint32_t* gb = (uint32_t*)(osm + SM::base);
+    uint32_t* lst = (uint32_t*)(osm + SM::lst);
+    uint64_t* bar = (uint64_t*)(osm + SM::bar);
+    __shared__ uint32_t red[33];
+    __shared__ uint32_t s_total;
+    if (*a.bad != (unsigned long long)kNoBad) return;
+    const int64_t n = os_count(a);
+    const bool drop = a.live && *a.any_dead;
+    const unsigned w = warp_id(), lane = lane_id();
+    const bool aligned = ((uintptr_t)a.kin % 16) == 0 && ((uintptr_t)a.vin % 16) == 0;
+    if (threadIdx.x == 0) os_mbar_init(&bar[0]);
+    __syncthreads();
+    unsigned phase = 0u;
+    for (int64_t tile = blockIdx.x; tile * kOsTile < n; tile += gridDim.x) {
+        const int64_t t0 = tile * kOsTile;
+        const int tn = (int)min64(kOsTile, n - t0);
+        if (aligned && tn == kOsTile) {
+            if (threadIdx.x == 0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                os_load_tile(sk, a.kin + t0, sv, a.vin + t0, kOsTile * 4, &bar[0]);
+            }
+            uint16_t* my = wh + w * BINS;
+            for (int i = lane; i < BINS / 8; i += 32) reinterpret_cast<uint4*>(my)[i] = make_uint4(0u, 0u, 0u, 0u);
+            os_wait(&bar[0], phase);
+            phase ^= 1u;
+        } else {
+            for (int i = threadIdx.x; i < tn; i += blockDim.x) {
+                sk[i] = a.kin[t0 + i];
+                sv[i] = a.vin[t0 + i];
+            }
+            uint16_t* my = wh + w * BINS;
+            for (int i = lane; i < BINS / 8; i += 32) reinterpret_cast<uint4*>(my)[i] = make_uint4(0u, 0u, 0u, 0u);
+        }
+        __syncthreads();                     // tile and zeroed histograms visible
+        uint16_t* my = wh + w * BINS;
+        uint32_t key[kOs2Items];
+        int32_t val[kOs2Items];
+        uint16_t rk[kOs2Items];
+        uint32_t ok = 0;
+        const unsigned lt = lanemask_lt();
+#pragma unroll
+        for (int r = 0; r < kOs2Items; ++r) {
+            const int it = (int)w * (kOs2Items * 32) + r * 32 + (int)lane;
+            bool valid = it < tn;
+            key[r] = valid ? sk[it] : 0u;
+            val[r] = valid ? sv[it] : 0;
+            valid = valid && os_live(a, drop, t0 + it, key[r]);
+            const uint32_t d = (key[r] >> a.shift) & a.mask;
+            const bool use_match = a.match == 2 || (a.match == 1 && !(r & 1));
+            const unsigned peers = use_match ? __match_any_sync(SS_FULL, valid ? d : 0xffffffffu) : match_bits<BITS>(d, valid);
+            uint16_t before = 0;
+            if (valid) before = my[d];
+            __syncwarp();
+            if (valid) {
+                ok |= 1u << r;
+                rk[r] = (uint16_t)(before + __popc(peers & lt));
+                if (lane == 31u - __clz(peers)) my[d] = (uint16_t)(before + __popc(peers));
+            }
+            __syncwarp();
+        }
+        __syncthreads();
+        // per digit: exclusive offsets over the 16 warps, the digit's count
+#pragma unroll
+        for (int q = 0; q < DPT; ++q) {
+            const int d = (int)threadIdx.x + q * kOs2Threads;
+            if (d < BINS) {
+                uint32_t run = 0;
+#pragma unroll
+                for (int v = 0; v < kOs2Warps; ++v) {
+                    const uint32_t c = wh[v * BINS + d];
+                    wh[v * BINS + d] = (uint16_t)run;
+                    run += c;
+                }
+                lst[d] = run;
+            }
+        }
+        __syncthreads();
+        // exclusive scan of the digit counts: DPT consecutive digits per thread
+        {
+            uint32_t c[DPT], s = 0;
+#pragma unroll
+            for (int q = 0; q < DPT; ++q) {
+                const int d = (int)threadIdx.x * DPT + q;
+                c[q] = d < BINS ? lst[d] : 0u;
+                s += c[q];
+            }
+            uint32_t tot;
+            uint32_t ex = block_excl_scan(s, red, &tot);
+#pragma unroll
+            for (int q = 0; q < DPT; ++q) {
+                const int d = (int)threadIdx.x * DPT + q;
+                if (d < BINS) {
+                    lst[d] = ex;
+                    gb[d] = a.hist[tile * BINS + d] - ex;
+                }
+                ex += c[q];
+            }
+            if (threadIdx.x == 0) s_total = tot;
+        }
+        __syncthreads();
+        // local sort by digit into shared memory (every item is in registers)
+#pragma unroll
+        for (int r = 0; r < kOs2Items; ++r) {
+            if ((ok >> r) & 1u) {
+                const uint32_t d = (key[r] >> a.shift) & a.mask;
+                const uint32_t p = lst[d] + my[d] + rk[r];
+                sk[p] = key[r];
+                sv[p] = val[r];
+            }
+        }
+        __syncthreads();
+        const int total = (int)s_total;
+        for (int i = threadIdx.x; i < total; i += blockDim.x) {
+            const uint32_t k = sk[i];
+            const uint32_t pos = gb[(k >> a.shift) & a.mask] + (uint32_t)i;
+            a.vout[pos] = sv[i];
+            if (a.kout) a.kout[pos] = k;
+        }
+        __syncthreads();                     // the tile buffer and histograms are free again
+    }
+}
+
 }  // namespace ss
