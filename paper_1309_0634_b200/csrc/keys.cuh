@@ -122,10 +122,13 @@ __device__ __forceinline__ int key_entry(KeyTable& t, unsigned long long k, unsi
 // K2 for int64 keys: probe + slot + count in one pass.  CTA b covers the
 // contiguous tuple range [b*range, (b+1)*range) inside one count chunk of S
 // tuples (range divides S), counted into row (b*range)/S of gcnt.
-constexpr int kKeyItems = 4;            // consecutive tuples per thread and round (2 x 16-byte loads)
+constexpr int kKeyItems = 4;
+#ifndef SS_KEY_MINB
+#define SS_KEY_MINB 2                   // CTAs per SM the register budget allows (A/B build switch)
+#endif            // consecutive tuples per thread and round (2 x 16-byte loads)
 
 template <bool COUNT>
-__global__ void __launch_bounds__(512)
+__global__ void __launch_bounds__(512, SS_KEY_MINB)
 k_key_count(const long long* __restrict__ keys, int64_t n, KeyTable t, uint32_t* __restrict__ out, int64_t S,
             int64_t range, int32_t* __restrict__ gcnt, const int32_t* __restrict__ hot_g, int n_hot, int agg) { SS_PDL_ENTRY();
     extern __shared__ int32_t sh_hist[];                  // [n_hot]
