@@ -1701,7 +1701,8 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
             f.report = report_args(e, n, false);
             f.ticket = e->fin_ticket;
         }
-        ss_note_launch(), ss_launch(k_finalize, group_grid(e->G), 256, 0, e->st, f);
+        // (at least one CTA per SM: finalize also clears the live chunks' count rows)
+        ss_note_launch(), ss_launch(k_finalize, std::max<unsigned>(group_grid(e->G), kNumSM), 256, 0, e->st, f);
         if (e->minmax) {
             if (e->sums) {
                 ss_note_launch(), ss_launch(k_mm_refresh, 8 * kNumSM, 256, 0, e->st, e->rescan, e->n_rescan, e->ring, e->off, e->W,
