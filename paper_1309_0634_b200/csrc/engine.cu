@@ -1013,7 +1013,6 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
     SS_CUDA(e, cudaFuncSetAttribute(k_count<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     SS_CUDA(e, cudaFuncSetAttribute(k_count_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     SS_CUDA(e, cudaFuncSetAttribute(k_sub_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, kRankMaxG * 4));
-    SS_CUDA(e, cudaFuncSetAttribute(k_sub_prefix, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * kSubFusedG * 4));
     SS_CUDA(e, cudaFuncSetAttribute(k_sort_pass<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SortSmem<4>::bytes));
     SS_CUDA(e, cudaFuncSetAttribute(k_sort_pass<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SortSmem<5>::bytes));
     SS_CUDA(e, cudaFuncSetAttribute(k_sort_pass<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SortSmem<6>::bytes));
@@ -1366,18 +1365,10 @@ static int launch_place_step(ss_engine* e, const uint32_t* dk, const int32_t* dv
         auto kern = use_match ? k_rank_place<0> : rank_kernel(bits_for(e->G));
         const size_t rsm = rank_smem_bytes((uint32_t)e->G);
         // sub-chunk prefixes (no-ops unless k_scan_small chose sub-chunks)
-        if ((uint32_t)e->G <= kSubFusedG) {
-            // sub-chunks exist only below kNumSM / 2 live chunks
-            ss_note_launch(), ss_launch(k_sub_prefix, (unsigned)std::min(n_chunk, kNumSM / 2), 1024,
-                                        (size_t)16 * e->G * 4, e->st, dk, n, cs, (const int32_t*)e->lc,
-                                        (const int32_t*)e->n_lc, (const int*)e->sub_shift, (uint32_t)e->G,
-                                        (const int32_t*)e->gpre, e->gsub, (const unsigned long long*)e->bad);
-        } else {
-            ss_note_launch(), ss_launch(k_sub_hist, kSubUnitsMax, 512, e->G * 4, e->st, dk, n, cs, e->lc, e->n_lc, e->sub_shift,
-                                                                                (uint32_t)e->G, e->subh, e->bad);
-            ss_note_launch(), ss_launch(k_sub_scan, 2 * kNumSM, 256, 0, e->st, e->gpre, e->lc, e->n_lc, e->sub_shift,
-                                                                       (uint32_t)e->G, e->subh, e->gsub, e->bad);
-        }
+        ss_note_launch(), ss_launch(k_sub_hist, kSubUnitsMax, 512, e->G * 4, e->st, dk, n, cs, e->lc, e->n_lc, e->sub_shift,
+                                                                            (uint32_t)e->G, e->subh, e->bad);
+        ss_note_launch(), ss_launch(k_sub_scan, 2 * kNumSM, 256, 0, e->st, e->gpre, e->lc, e->n_lc, e->sub_shift,
+                                                                   (uint32_t)e->G, e->subh, e->gsub, e->bad);
         ss_note_launch(), ss_launch(kern, std::max(n_chunk, kSubUnitsMax), kRankWarps * 32, rsm, e->st, dk, dv, e->trace_on ? e->kbuf2 : nullptr, e->vbuf[0], n, cs, e->lc, e->n_lc, e->gpre, e->gstart,
             (uint32_t)e->G, e->n_live, e->bad, e->sub_shift, e->gsub);
         SS_CUDA(e, cudaGetLastError());

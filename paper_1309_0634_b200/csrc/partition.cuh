@@ -1119,43 +1119,6 @@ k_sub_scan(const int32_t* __restrict__ gpre, const int32_t* __restrict__ lc, con
     }
 }
 
-// Small G (<= kSubFusedG): counts and prefixes of all sub-chunks of one
-// live chunk in one CTA -- 2^ss shared histograms, then the column scan --
-// one launch instead of k_sub_hist + k_sub_scan (each ~3-6 us, most of it
-// launch and tail, and both launched even when no chunk is subdivided)
-constexpr uint32_t kSubFusedG = 2048;
-
-__global__ void __launch_bounds__(1024)
-k_sub_prefix(const uint32_t* __restrict__ keys, int64_t n, int chunk_shift, const int32_t* __restrict__ lc,
-             const int32_t* __restrict__ n_lc, const int* __restrict__ sub_shift_dev, uint32_t G,
-             const int32_t* __restrict__ gpre, int32_t* __restrict__ gsub,
-             const unsigned long long* __restrict__ bad) { SS_PDL_ENTRY();
-    extern __shared__ int32_t sh_sub[];                     // [2^ss][G]
-    if (*bad != (unsigned long long)kNoBad) return;
-    const int ss = *sub_shift_dev;
-    if (ss == 0 || (int)blockIdx.x >= *n_lc) return;
-    const int li = blockIdx.x;
-    const int64_t c = lc[li];
-    const int nsub = 1 << ss;
-    for (int i = threadIdx.x; i < nsub * (int)G; i += blockDim.x) sh_sub[i] = 0;
-    __syncthreads();
-    const int64_t c0 = c << chunk_shift;
-    const int64_t c1 = min64(n, c0 + ((int64_t)1 << chunk_shift));
-    const int sshift = chunk_shift - ss;
-    for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
-        const uint32_t g = keys[i];
-        if (g < G) atomicAdd(&sh_sub[(int)((i - c0) >> sshift) * (int)G + (int)g], 1);
-    }
-    __syncthreads();
-    for (uint32_t g = threadIdx.x; g < G; g += blockDim.x) {
-        int32_t run = gpre[c * (int64_t)G + g];
-        for (int sb = 0; sb < nsub; ++sb) {
-            gsub[(((int64_t)li << ss) + sb) * G + g] = run;
-            if (run >= 0) run += sh_sub[sb * (int)G + (int)g];
-        }
-    }
-}
-
 __host__ __device__ constexpr size_t rank_smem_bytes(uint32_t G) {
     return (size_t)kRankWarps * kRankStages * kRankSub * 8 + (size_t)G * 4;
 }
