@@ -36,6 +36,8 @@
 #include <thread>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/ss_b200.h"
 #include "common.cuh"
 #include "partition.cuh"
@@ -328,12 +330,26 @@ struct ss_engine {
 };
 
 namespace {
+// NVTX ranges on the host timeline of a profiler (nsys / ncu --nvtx): the
+// public entry points and every kernel class of a step, named as in
+// DESIGN.md.  Enabled by SS_B200_NVTX=1 (header-only NVTX3: without a tool
+// attached a push is one branch).
+static const bool g_nvtx = getenv("SS_B200_NVTX") && getenv("SS_B200_NVTX")[0] == '1';
+struct NvtxRange {
+    bool on;
+    explicit NvtxRange(const char* name) : on(g_nvtx) { if (on) nvtxRangePushA(name); }
+    ~NvtxRange() { if (on) nvtxRangePop(); }
+};
+static const char* const kClassName[SS_K_NCLASS] = {"ss count", "ss stats+scan", "ss placement", "ss window update",
+                                                     "ss finalize+emit", "ss apply moves", "ss policy / split plan"};
+
 struct ProfScope {
     ss_engine* e;
     int cls;
     cudaStream_t s;
     cudaEvent_t a = nullptr;
-    ProfScope(ss_engine* e_, int c, cudaStream_t st) : e(e_), cls(c), s(st) {
+    NvtxRange nv;
+    ProfScope(ss_engine* e_, int c, cudaStream_t st) : e(e_), cls(c), s(st), nv(kClassName[c]) {
         if (!e->prof) return;
         a = take();
         cudaEventRecord(a, s);
@@ -2314,6 +2330,7 @@ static int run_stream(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64
 
 extern "C" int ss_step(ss_engine* e, const uint32_t* groups, const int32_t* attrs, int64_t n,
                        const ss_balancer* cfg, ss_step_report* rep) {
+    NvtxRange nv_("ss_step");
     if (!e || n < 0) return SS_E_CONFIG;
     int rc;
     if ((rc = check_balancer(e, cfg))) return rc;
@@ -2728,6 +2745,7 @@ __global__ void k_route_done(unsigned long long* __restrict__ bad, int n_dest, i
 // message the tuple all-to-all ships; counts_dev[n_dest + 1] on the device.
 extern "C" int ss_route_records(ss_engine* e, const uint32_t* groups, const int32_t* attrs, int64_t n,
                                 void* out_records, int64_t* counts_dev) {
+    NvtxRange nv_("ss_route_records");
     if (!e || n < 0 || !counts_dev || (n && !out_records)) return SS_E_CONFIG;
     if (!e->owner) return fail(e, SS_E_CONFIG, "ss_set_owner first");
     if (!is_device_ptr(counts_dev) || (n && !is_device_ptr(out_records)))
@@ -3157,6 +3175,7 @@ extern "C" int ss_set_bucket_owner(ss_engine* e, const int32_t* owner, int n_des
 // counts_dev[n_dest] per destination, counts_dev[n_dest] = -1 (no bad keys)
 extern "C" int ss_route_records64(ss_engine* e, const int64_t* keys, const int32_t* attrs, int64_t n, void* out_records,
                                   int64_t* counts_dev) {
+    NvtxRange nv_("ss_route_records64");
     if (!e || n < 0 || !counts_dev || (n && (!out_records || !keys || !attrs))) return SS_E_CONFIG;
     if (!e->bowner) return fail(e, SS_E_CONFIG, "ss_set_bucket_owner first");
     if (n > e->max_batch) return fail(e, SS_E_CONFIG, "batch larger than max_batch");
@@ -3384,6 +3403,7 @@ static int map_keys(ss_engine* e, const int64_t* keys, int64_t n, uint32_t* dout
     }
     if (n == 0) return SS_OK;
     KeyTable& t = e->kt;
+    NvtxRange nv_("ss key probe + count");
     SS_CUDA(e, cudaMemcpyAsync(t.prev_slots, t.n_slots, 4, cudaMemcpyDeviceToDevice, st));
     const int nblk = (int)((n + kMarkBlk - 1) / kMarkBlk);
     const int64_t range = kCountChunk;                   // divides the count chunk S
@@ -3422,6 +3442,7 @@ extern "C" int ss_map_keys(ss_engine* e, const int64_t* keys, int64_t n, uint32_
 // the fused step on int64 keys: map to slots, then ss_step on the slots
 extern "C" int ss_step_keys64(ss_engine* e, const int64_t* keys, const int32_t* attrs, int64_t n,
                               const ss_balancer* cfg, ss_step_report* rep) {
+    NvtxRange nv_("ss_step_keys64");
     if (!e || n < 0) return SS_E_CONFIG;
     if (!e->keys64) return fail(e, SS_E_CONFIG, "engine was created with key_bits = 32");
     if (n > e->max_batch) return fail(e, SS_E_CONFIG, "batch larger than max_batch");
