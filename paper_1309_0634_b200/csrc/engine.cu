@@ -873,10 +873,11 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
         const char* bp = getenv("SS_B200_BUCKET");
         e->bucket = e->bucket && bp && bp[0] == '1';
     }
-    // look-back-free passes from 2^18 groups on (C4/C5: 0.63 -> 0.42 ms);
-    // below, the radix passes over live chunks with segmented look-back
-    // are faster (C3, 2^17: 0.30 vs 0.34 ms)
-    e->os = !e->rank_place && bits_for(G) >= 18;
+    // look-back-free passes from 2^17 groups on (C4/C5: 0.63 -> 0.42 ms;
+    // C3, 2^17: with the two-CTA pass and the parallel column scan 37.7 vs
+    // 37.1 G tuples/s for the segmented radix passes over live chunks,
+    // which stay in use for 2^14 < G <= 2^16)
+    e->os = !e->rank_place && bits_for(G) >= 17;
     if (const char* op = getenv("SS_B200_ONESWEEP")) e->os = !e->rank_place && G > kRankMaxG && op[0] != '0';
     if (e->os) {
         const int bits = bits_for(G);
