@@ -1709,8 +1709,9 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
             f.report = report_args(e, n, false);
             f.ticket = e->fin_ticket;
         }
-        // (at least one CTA per SM: finalize also clears the live chunks' count rows)
-        ss_note_launch(), ss_launch(k_finalize, std::max<unsigned>(group_grid(e->G), kNumSM), 256, 0, e->st, f);
+        // (at least two CTAs per SM: finalize also clears the live chunks' count rows,
+        // 10 MB at C2)
+        ss_note_launch(), ss_launch(k_finalize, std::max<unsigned>(group_grid(e->G), 2 * kNumSM), 256, 0, e->st, f);
         if (e->minmax) {
             if (e->sums) {
                 ss_note_launch(), ss_launch(k_mm_refresh, 8 * kNumSM, 256, 0, e->st, e->rescan, e->n_rescan, e->ring, e->off, e->W,
