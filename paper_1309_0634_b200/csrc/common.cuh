@@ -201,4 +201,32 @@ __device__ __forceinline__ unsigned long long lb_pack(uint32_t epoch, unsigned l
     return ((unsigned long long)epoch << 34) | (flag << 32) | (unsigned long long)cnt;
 }
 
+// ---- bulk asynchronous copies (TMA engine, no tensor map) on an mbarrier --
+__device__ __forceinline__ void mbar_init1(uint64_t* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"((unsigned)__cvta_generic_to_shared(bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// two equal-size global -> shared copies completing on `bar` (16-byte
+// aligned, size a multiple of 16); the streamed input leaves L2 first
+__device__ __forceinline__ void bulk_load2(void* d0, const void* s0, void* d1, const void* s1, unsigned bytes,
+                                           uint64_t* bar) {
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(b), "r"(2 * bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+                 :: "r"((unsigned)__cvta_generic_to_shared(d0)), "l"(s0), "r"(bytes), "r"(b), "l"(pol) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+                 :: "r"((unsigned)__cvta_generic_to_shared(d1)), "l"(s1), "r"(bytes), "r"(b), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, unsigned parity) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "MBW_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra MBW_%=;\n}" :: "r"(a), "r"(parity) : "memory");
+}
+
 }  // namespace ss

@@ -1167,6 +1167,13 @@ k_rank_place(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin, 
     const unsigned lane = lane_id();
     uint32_t* my_k = stage_k + w * kRankStages * kRankSub;
     int32_t* my_v = stage_v + w * kRankStages * kRankSub;
+    // full, aligned sub-tiles arrive by two bulk copies (1 KB each) on the
+    // warp's mbarrier of the slot; the rest by per-lane cp.async
+    __shared__ uint64_t rbar[kRankWarps][kRankStages];
+    unsigned bulk_slots = 0, bulk_phase = 0;       // warp-uniform bit per slot
+    if (lane == 0)
+        for (int q = 0; q < kRankStages; ++q) mbar_init1(&rbar[w][q]);
+    __syncwarp();
     // stage sub-tile s of this warp into ring slot q (always commits a group)
     auto stage = [&](int s, int q) {
         if (s < nsub) {
@@ -1175,13 +1182,10 @@ k_rank_place(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin, 
             uint32_t* dk = my_k + q * kRankSub;
             int32_t* dv = my_v + q * kRankSub;
             if (tn == kRankSub && (((uintptr_t)(kin + t0) | (uintptr_t)(vin + t0)) & 15) == 0) {
-#pragma unroll
-                for (int i = 0; i < kRankSub / 128; ++i) {
-                    const int li = (i * 32 + (int)lane) * 4;
-                    cp_async16(dk + li, kin + t0 + li);
-                    cp_async16(dv + li, vin + t0 + li);
-                }
+                if (lane == 0) bulk_load2(dk, kin + t0, dv, vin + t0, kRankSub * 4, &rbar[w][q]);
+                bulk_slots |= 1u << q;
             } else {
+                bulk_slots &= ~(1u << q);
                 for (int li = (int)lane; li < tn; li += 32) {
                     cp_async4(dk + li, kin + t0 + li);
                     cp_async4(dv + li, vin + t0 + li);
@@ -1253,6 +1257,10 @@ k_rank_place(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin, 
     int q = 0;
     for (int s = w; s < nsub; s += kRankWarps) {
         cp_async_wait_n<kRankStages - 1>();
+        if ((bulk_slots >> q) & 1u) {
+            mbar_wait_parity(&rbar[w][q], (bulk_phase >> q) & 1u);
+            bulk_phase ^= 1u << q;
+        }
         __syncwarp();
         const int tn = min(kRankSub, cn - s * kRankSub);
         if (tn == kRankSub) sub_tile(std::integral_constant<bool, true>{}, s, q, tn);
