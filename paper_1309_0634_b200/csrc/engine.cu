@@ -257,6 +257,7 @@ struct ss_engine {
         int64_t n;
         ss_balancer bal;
         int plan_cur, plan_valid, emit_b, host_emit, stage, pre_counted;
+        const void* gcnt;          // count rows the graph reads (alternating when the count is pipelined)
         cudaGraphExec_t exec;
         long long launches;
     };
@@ -274,6 +275,7 @@ struct ss_engine {
     cudaEvent_t ev_keys[2] = {nullptr, nullptr}, ev_fin[2] = {nullptr, nullptr}, ev_hot = nullptr;
     bool fin_rec[2] = {false, false}, hot_rec = false;
     bool key_pipe_dev = false;                 // device key inputs are ready when passed (ss_set_key_pipeline)
+    bool inputs_on_stream = false;             // this step's device inputs are engine-stream work (records)
     cudaEvent_t ev_in = nullptr;
     int32_t* gcnt_buf[2] = {nullptr, nullptr};
     uint32_t* skeys_buf[2] = {nullptr, nullptr};
@@ -588,6 +590,7 @@ k_report(ReportArgs a) { SS_PDL_ENTRY();
 }  // namespace
 
 static int join_side(ss_engine* e);
+static int create_count_pipe(ss_engine* e);
 
 // --------------------------------------------------------------------------
 // lifecycle
@@ -946,22 +949,8 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
         t.cap_mask = cap - 1;
         t.G = (int)G;
         // pipelined key probe (large G: the probe also counts the batch)
-        if (G > 16384 && !e->stream_scope && !getenv("SS_B200_NO_KEY_PIPE")) {
-            SS_CUDA(e, cudaStreamCreateWithFlags(&e->kst, cudaStreamNonBlocking));
-            for (int b = 0; b < 2; ++b) {
-                SS_CUDA(e, cudaEventCreateWithFlags(&e->ev_keys[b], cudaEventDisableTiming));
-                SS_CUDA(e, cudaEventCreateWithFlags(&e->ev_fin[b], cudaEventDisableTiming));
-            }
-            SS_CUDA(e, cudaEventCreateWithFlags(&e->ev_hot, cudaEventDisableTiming));
-            SS_CUDA(e, cudaEventCreateWithFlags(&e->ev_in, cudaEventDisableTiming));
-            e->gcnt_buf[0] = e->gcnt;
-            e->skeys_buf[0] = e->stage_keys;
-            if ((rc = dalloc(e, &e->gcnt_buf[1], (size_t)e->n_sub_max * G)) ||
-                (rc = dalloc(e, &e->skeys_buf[1], e->max_batch)) || (rc = dalloc(e, &e->key_bad, 1)))
-                return rc;
-            SS_CUDA(e, cudaMemsetAsync(e->gcnt_buf[1], 0, (size_t)e->n_sub_max * G * 4, e->st));
-            ss_note_launch(), ss_launch(k_set_bad, 1, 1, 0, e->st, e->key_bad);
-        }
+        if (G > 16384 && !e->stream_scope && !getenv("SS_B200_NO_KEY_PIPE") && (rc = create_count_pipe(e)))
+            return rc;
         ss_note_launch(), ss_launch(k_key_init, 296, 256, 0, e->st, t.ent, (int64_t)cap + 1);
         SS_CUDA(e, cudaMemsetAsync(t.first, 0xff, (cap + 1) * 4, e->st));
         SS_CUDA(e, cudaMemsetAsync(t.mark, 0xff, e->max_batch * 4, e->st));
@@ -970,6 +959,9 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
         SS_CUDA(e, cudaMemsetAsync(t.min_key_entry, 0xff, 4, e->st));
         SS_CUDA(e, cudaMemsetAsync(t.overflow, 0, 4, e->st));
     }
+    // u32 groups, small G: the count of batch t+1 likewise runs ahead
+    if (!e->keys64 && G <= 16384 && !e->stream_scope && !getenv("SS_B200_NO_KEY_PIPE") && (rc = create_count_pipe(e)))
+        return rc;
     // -- balancer
     // (used whenever the lists are not staged: large G, or large P)
     if ((rc = dalloc(e, &e->bal_ecnt, G)) || (rc = dalloc(e, &e->bal_eflag, G))) return rc;
@@ -1512,7 +1504,7 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
         ProfScope ps(e, SS_K_COUNT, e->st);
         if (e->G <= 16384) {
             // one CTA per count chunk, rows written whole (no zeroing needed)
-            if (n) {
+            if (n && !e->pre_counted) {
                 ss_note_launch(), ss_launch(k_count_rows, n_chunk, 512, e->G * 4, e->st, dk, n, (uint32_t)e->G, e->S, e->gcnt,
                                                                                  e->bad, ((uintptr_t)dk % 16) == 0);
                 SS_CUDA(e, cudaGetLastError());
@@ -1857,6 +1849,28 @@ static void fill_report(const ss_engine* e, ss_step_report* r) {
     r->load_ratio = (d.load_sum > 0) ? (double)d.max_load / r->mean_load : 0.0;
 }
 
+// the count (or int64 probe + count) of batch t+1 on its own stream while
+// batch t finishes: alternating count rows (and slot buffers for int64
+// keys), the events ordering it, a separate bad-tuple flag
+static int create_count_pipe(ss_engine* e) {
+    int rc;
+    SS_CUDA(e, cudaStreamCreateWithFlags(&e->kst, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) {
+        SS_CUDA(e, cudaEventCreateWithFlags(&e->ev_keys[b], cudaEventDisableTiming));
+        SS_CUDA(e, cudaEventCreateWithFlags(&e->ev_fin[b], cudaEventDisableTiming));
+    }
+    SS_CUDA(e, cudaEventCreateWithFlags(&e->ev_hot, cudaEventDisableTiming));
+    SS_CUDA(e, cudaEventCreateWithFlags(&e->ev_in, cudaEventDisableTiming));
+    e->gcnt_buf[0] = e->gcnt;
+    e->skeys_buf[0] = e->stage_keys;
+    if ((rc = dalloc(e, &e->gcnt_buf[1], (size_t)e->n_sub_max * e->G)) || (rc = dalloc(e, &e->key_bad, 1)) ||
+        (e->keys64 && (rc = dalloc(e, &e->skeys_buf[1], e->max_batch))))
+        return rc;
+    SS_CUDA(e, cudaMemsetAsync(e->gcnt_buf[1], 0, (size_t)e->n_sub_max * e->G * 4, e->st));
+    ss_note_launch(), ss_launch(k_set_bad, 1, 1, 0, e->st, e->key_bad);
+    return SS_OK;
+}
+
 static int ensure_moves(ss_engine* e, int64_t want) {
     want = std::min<int64_t>(want, e->G);
     if (want <= e->cap_moves) return SS_OK;
@@ -2195,7 +2209,7 @@ static int run_step(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_t
     for (auto& g : e->graphs)
         if (g.dk == dk && g.dv == dv && g.n == n && same_bal(bal, g.bal) && g.plan_cur == e->plan_cur &&
             g.plan_valid == (int)e->plan_valid && g.emit_b == emit_b && g.host_emit == (int)e->host_emit &&
-            g.stage == e->cur_stage && g.pre_counted == (int)e->pre_counted) {
+            g.stage == e->cur_stage && g.pre_counted == (int)e->pre_counted && g.gcnt == (const void*)e->gcnt) {
             hit = &g;
             break;
         }
@@ -2250,6 +2264,7 @@ static int run_step(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_t
         ge.host_emit = (int)e->host_emit;
         ge.stage = e->cur_stage;
         ge.pre_counted = (int)e->pre_counted;
+        ge.gcnt = e->gcnt;
         ge.exec = exec;
         ge.launches = per_replay;
         e->graphs.push_back(ge);
@@ -2339,9 +2354,11 @@ extern "C" int ss_step(ss_engine* e, const uint32_t* groups, const int32_t* attr
     if (n > e->max_batch) return fail(e, SS_E_CONFIG, "batch larger than max_batch");
     const uint32_t* dk = groups;
     const int32_t* dv = attrs;
+    bool staged_here = false;
     if (!is_device_ptr(groups) || (attrs && !is_device_ptr(attrs))) {
         // host buffers: H2D on the copy stream into this batch's staging
         // buffer, overlapped with the previous batch's compute
+        staged_here = true;
         if ((rc = begin_stage(e, false))) return rc;
         const int b = e->cur_stage;
         if ((rc = stage_h2d(e, e->skeys[b], groups, n, &dk)) || (rc = stage_h2d(e, e->svals[b], attrs, n, &dv)) ||
@@ -2364,7 +2381,42 @@ extern "C" int ss_step(ss_engine* e, const uint32_t* groups, const int32_t* attr
         }
         return SS_OK;
     }
-    if (n > 0 && (rc = run_step(e, dk, dv, n, cfg))) return rc;
+    if (n > 0 && e->kst && !e->keys64 && !e->pre_counted) {
+        // the count rows of this batch on the count stream (overlapping the
+        // previous batch's tail), into the alternate rows (see ss_step_keys64)
+        const int b = e->kpar;
+        e->kpar ^= 1;
+        if (staged_here) {
+            SS_CUDA(e, cudaStreamWaitEvent(e->kst, e->ev_staged[e->cur_stage], 0));
+        } else if (!e->key_pipe_dev || e->inputs_on_stream) {
+            // device keys may be produced by work already on the engine
+            // stream (replay records split there): wait for it -- no overlap
+            SS_CUDA(e, cudaEventRecord(e->ev_in, e->st));
+            SS_CUDA(e, cudaStreamWaitEvent(e->kst, e->ev_in, 0));
+        }
+        if (e->fin_rec[b]) SS_CUDA(e, cudaStreamWaitEvent(e->kst, e->ev_fin[b], 0));
+        const int n_chunk = (int)std::max<int64_t>(1, (n + e->S - 1) / e->S);
+        {
+            NvtxRange nv2("ss count (ahead)");
+            ss_note_launch(), ss_launch(k_count_rows, n_chunk, 512, e->G * 4, e->kst, dk, n, (uint32_t)e->G, e->S,
+                                        e->gcnt_buf[b], e->key_bad, ((uintptr_t)dk % 16) == 0);
+        }
+        SS_CUDA(e, cudaGetLastError());
+        SS_CUDA(e, cudaEventRecord(e->ev_keys[b], e->kst));
+        SS_CUDA(e, cudaStreamWaitEvent(e->st, e->ev_keys[b], 0));
+        ss_note_launch(), ss_launch(k_merge_bad, 1, 32, 0, e->st, e->bad, e->key_bad);
+        int32_t* const gcnt0 = e->gcnt;
+        e->gcnt = e->gcnt_buf[b];
+        e->pre_counted = true;
+        rc = run_step(e, dk, dv, n, cfg);
+        e->pre_counted = false;
+        e->gcnt = gcnt0;
+        if (rc) return rc;
+        SS_CUDA(e, cudaEventRecord(e->ev_fin[b], e->st));
+        e->fin_rec[b] = true;
+    } else if (n > 0 && (rc = run_step(e, dk, dv, n, cfg))) {
+        return rc;
+    }
     if (n == 0) {
         if (e->side_pending) {
             SS_CUDA(e, cudaStreamWaitEvent(e->st, e->ev_apply, 0));
@@ -2409,7 +2461,10 @@ extern "C" int ss_step_records(ss_engine* e, const void* records, int64_t n, con
         ss_note_launch(), ss_launch(k_deinterleave, 4 * kNumSM, 256, 0, e->st, (const uint4*)rec, n, e->skeys[b], e->svals[b]);
         SS_CUDA(e, cudaGetLastError());
     }
-    return ss_step(e, e->skeys[b], e->svals[b], n, cfg, rep);
+    e->inputs_on_stream = true;           // the split keys are engine-stream work
+    rc = ss_step(e, e->skeys[b], e->svals[b], n, cfg, rep);
+    e->inputs_on_stream = false;
+    return rc;
 }
 
 extern "C" int ss_set_trace(ss_engine* e, int enable) {
@@ -3225,7 +3280,10 @@ extern "C" int ss_step_records64(ss_engine* e, const void* records, int64_t n, c
     if (n && !is_device_ptr(records)) return fail(e, SS_E_CONFIG, "ss_step_records64: device records required");
     if (n) ss_note_launch(), ss_launch(k_key_rec_split, 4 * kNumSM, 256, 0, e->st, (const int32_t*)records, n,
                                        e->stage_keys64, e->rec_vals);
-    return ss_step_keys64(e, (const int64_t*)e->stage_keys64, e->rec_vals, n, cfg, rep);
+    e->inputs_on_stream = true;           // the split keys are engine-stream work
+    rc = ss_step_keys64(e, (const int64_t*)e->stage_keys64, e->rec_vals, n, cfg, rep);
+    e->inputs_on_stream = false;
+    return rc;
 }
 
 // per-bucket counts of the last batch (device, kKeyBuckets entries)
@@ -3481,7 +3539,7 @@ extern "C" int ss_step_keys64(ss_engine* e, const int64_t* keys, const int32_t* 
     e->kpar ^= 1;
     if (e->cur_stage >= 0) {
         SS_CUDA(e, cudaStreamWaitEvent(e->kst, e->ev_staged[e->cur_stage], 0));
-    } else if (!e->key_pipe_dev) {
+    } else if (!e->key_pipe_dev || e->inputs_on_stream) {
         // device keys may be produced by work already on the engine stream
         // (e.g. the multi-GPU record split): wait for it -- no overlap
         SS_CUDA(e, cudaEventRecord(e->ev_in, e->st));
