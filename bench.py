@@ -359,9 +359,9 @@ class Workload:
                                     sub_batch=args.sub_batch, key_bits=64 if kind.endswith("64") else 32,
                                     initial=args.initial)
         self.eng.set_stream(stream)
-        if kind.endswith("64") and world == 1:
+        if world == 1:
             # the staged batches are complete before the timed region: the
-            # next batch's key probe may run ahead on the key stream
+            # next batch's count (int64: key probe + count) may run ahead
             self.eng.set_key_pipeline(True)
         self.bal = self.eng.balancer_struct(policy, thread_threshold=thr, pot=0.5, split=split)
         self.nbuf = 2 * DRIFT_EVERY if kind == "zipfdrift" else 4

@@ -415,3 +415,41 @@ def test_int64_keys_pipelined_probe(ready):
     cnt, sm, avg, mn, mx = store.aggregates()
     assert np.array_equal(s["min"][:n], mn[:n]) and np.array_equal(s["max"][:n], mx[:n])
     eng.close()
+
+
+@pytest.mark.parametrize("ready", [True, False])
+def test_u32_pipelined_count(ready):
+    """G <= 2^14: the count of batch t+1 runs on its own stream while batch
+    t finishes (alternating count rows; captured graphs keyed by them).
+    Unsynchronised device batches, a host batch and a replay-record batch
+    (split on the engine stream, so never overlapped), checked against the
+    oracle."""
+    import torch
+    from paper_1309_0634_b200.stream_engine import StreamEngine
+    G, W, P, B = 1000, 100, 32, 300_000
+    spec = D.DatasetSpec(D.DatasetKind.ZIPF, 8 * B, G, 1.1, 21)
+    bl = list(D.batches(D.stream_for(spec), B))
+    eng = _engine(G, W, P=P, max_batch=B, aggregates=("count", "sum", "avg", "min", "max"))
+    eng.set_key_pipeline(ready)
+    bal = StreamEngine.balancer_struct("prob", max(1, B // (10 * P)), 0.5)
+    dev = [(torch.as_tensor(b.groups.astype(np.int32)).cuda(), torch.as_tensor(b.attrs.astype(np.int32)).cuda())
+           for b in bl]
+    torch.cuda.synchronize()
+    for i, b in enumerate(bl):
+        if i == 3:
+            eng.step(b.groups, b.attrs, bal, sync=False)                 # host input
+        elif i == 5:
+            rec = np.empty(len(b), dtype=D.REPLAY_DTYPE)
+            rec["group"], rec["attr"] = b.groups, b.attrs
+            eng.step_records(torch.as_tensor(rec.view(np.int64)).cuda(), bal, sync=False)
+        else:
+            eng.step(*dev[i], bal, sync=False)
+    store = O.OStore(G, W)
+    for b in bl:
+        store.ingest(b.groups, b.attrs)
+    s = eng.snapshot()
+    assert np.array_equal(s["fill"], store.fill) and np.array_equal(s["window_sum"], store.window_sum)
+    assert np.array_equal(s["next_pos"], store.next_pos)
+    cnt, sm, avg, mn, mx = store.aggregates()
+    assert np.array_equal(s["min"], mn) and np.array_equal(s["max"], mx)
+    eng.close()
