@@ -959,8 +959,8 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
         SS_CUDA(e, cudaMemsetAsync(t.min_key_entry, 0xff, 4, e->st));
         SS_CUDA(e, cudaMemsetAsync(t.overflow, 0, 4, e->st));
     }
-    // u32 groups, small G: the count of batch t+1 likewise runs ahead
-    if (!e->keys64 && G <= 16384 && !e->stream_scope && !getenv("SS_B200_NO_KEY_PIPE") && (rc = create_count_pipe(e)))
+    // u32 groups: the count of batch t+1 likewise runs ahead
+    if (!e->keys64 && !e->stream_scope && !getenv("SS_B200_NO_KEY_PIPE") && (rc = create_count_pipe(e)))
         return rc;
     // -- balancer
     // (used whenever the lists are not staged: large G, or large P)
@@ -2398,8 +2398,19 @@ extern "C" int ss_step(ss_engine* e, const uint32_t* groups, const int32_t* attr
         const int n_chunk = (int)std::max<int64_t>(1, (n + e->S - 1) / e->S);
         {
             NvtxRange nv2("ss count (ahead)");
-            ss_note_launch(), ss_launch(k_count_rows, n_chunk, 512, e->G * 4, e->kst, dk, n, (uint32_t)e->G, e->S,
-                                        e->gcnt_buf[b], e->key_bad, ((uintptr_t)dk % 16) == 0);
+            if (e->G <= 16384) {
+                ss_note_launch(), ss_launch(k_count_rows, n_chunk, 512, e->G * 4, e->kst, dk, n, (uint32_t)e->G, e->S,
+                                            e->gcnt_buf[b], e->key_bad, ((uintptr_t)dk % 16) == 0);
+            } else {
+                // large G: the previous batch's hot-group cache (k_hot_select)
+                // must be complete; the rows are zero (finalize / stats keep them so)
+                if (e->hot_rec) SS_CUDA(e, cudaStreamWaitEvent(e->kst, e->ev_hot, 0));
+                const int64_t grid = (n + kCountChunk - 1) / kCountChunk;
+                ss_note_launch(), ss_launch(k_count<false>, (unsigned)grid, 512, (size_t)kHotCache * 4, e->kst, dk, n,
+                                            (uint32_t)e->G, e->S, kCountChunk, e->gcnt_buf[b], e->key_bad,
+                                            (int)(((uintptr_t)dk % 16) == 0), (const int32_t*)e->hot_of,
+                                            (const int32_t*)e->hot_g, kHotCache);
+            }
         }
         SS_CUDA(e, cudaGetLastError());
         SS_CUDA(e, cudaEventRecord(e->ev_keys[b], e->kst));

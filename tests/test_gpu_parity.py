@@ -417,16 +417,18 @@ def test_int64_keys_pipelined_probe(ready):
     eng.close()
 
 
+@pytest.mark.parametrize("G", [1000, 20_000])
 @pytest.mark.parametrize("ready", [True, False])
-def test_u32_pipelined_count(ready):
-    """G <= 2^14: the count of batch t+1 runs on its own stream while batch
-    t finishes (alternating count rows; captured graphs keyed by them).
+def test_u32_pipelined_count(ready, G):
+    """The count of batch t+1 runs on its own stream while batch t finishes
+    (alternating count rows; captured graphs keyed by them; large G: after
+    the previous batch's hot-group cache).
     Unsynchronised device batches, a host batch and a replay-record batch
     (split on the engine stream, so never overlapped), checked against the
     oracle."""
     import torch
     from paper_1309_0634_b200.stream_engine import StreamEngine
-    G, W, P, B = 1000, 100, 32, 300_000
+    W, P, B = 100, 32, 300_000
     spec = D.DatasetSpec(D.DatasetKind.ZIPF, 8 * B, G, 1.1, 21)
     bl = list(D.batches(D.stream_for(spec), B))
     eng = _engine(G, W, P=P, max_batch=B, aggregates=("count", "sum", "avg", "min", "max"))
