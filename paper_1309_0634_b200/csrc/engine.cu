@@ -276,6 +276,16 @@ struct ss_engine {
     bool fin_rec[2] = {false, false}, hot_rec = false;
     bool key_pipe_dev = false;                 // device key inputs are ready when passed (ss_set_key_pipeline)
     bool inputs_on_stream = false;             // this step's device inputs are engine-stream work (records)
+    // "ahead" mode (u32, G <= 2^14, single-pass placement, no policy or
+    // split): count + statistics + scans + sub-chunk prefixes of batch t+1
+    // run on the count stream while batch t places and updates windows;
+    // the per-batch arrays they write alternate
+    bool ahead_ok = false, ahead = false;
+    struct AheadSet {
+        int32_t *gcount, *gkept, *gpre, *gstart, *n_live, *lc, *n_lc, *gsub;
+        int* sub_shift;
+        unsigned long long *tpt, *touched;
+    } aset[2] = {};
     cudaEvent_t ev_in = nullptr;
     int32_t* gcnt_buf[2] = {nullptr, nullptr};
     uint32_t* skeys_buf[2] = {nullptr, nullptr};
@@ -962,6 +972,23 @@ extern "C" int ss_create(const ss_config* cfg, ss_engine** out) {
     // u32 groups: the count of batch t+1 likewise runs ahead
     if (!e->keys64 && !e->stream_scope && !getenv("SS_B200_NO_KEY_PIPE") && (rc = create_count_pipe(e)))
         return rc;
+    // small G without a policy: statistics, scans and sub-chunk prefixes too
+    if (e->kst && !e->keys64 && e->rank_place && !getenv("SS_B200_NO_AHEAD")) {
+        const int nsub = e->n_sub_max;
+        ss_engine::AheadSet& a0 = e->aset[0];
+        a0 = {e->gcount, e->gkept, e->gpre, e->gstart, e->n_live, e->lc, e->n_lc, e->gsub, e->sub_shift,
+              e->tpt, e->touched};
+        ss_engine::AheadSet& a1 = e->aset[1];
+        if ((rc = dalloc(e, &a1.gcount, G)) || (rc = dalloc(e, &a1.gkept, G)) ||
+            (rc = dalloc(e, &a1.gpre, (size_t)nsub * G)) || (rc = dalloc(e, &a1.gstart, (size_t)nsub * G)) ||
+            (rc = dalloc(e, &a1.n_live, nsub + 1)) || (rc = dalloc(e, &a1.lc, nsub)) || (rc = dalloc(e, &a1.n_lc, 1)) ||
+            (rc = dalloc(e, &a1.gsub, (size_t)kSubUnitsMax * G)) || (rc = dalloc(e, &a1.sub_shift, 1)) ||
+            (rc = dalloc(e, &a1.tpt, e->P)) || (rc = dalloc(e, &a1.touched, 1)))
+            return rc;
+        SS_CUDA(e, cudaMemsetAsync(a1.sub_shift, 0, 4, e->st));
+        SS_CUDA(e, cudaMemsetAsync(a1.gcount, 0, G * 4, e->st));
+        e->ahead_ok = true;
+    }
     // -- balancer
     // (used whenever the lists are not staged: large G, or large P)
     if ((rc = dalloc(e, &e->bal_ecnt, G)) || (rc = dalloc(e, &e->bal_eflag, G))) return rc;
@@ -1291,6 +1318,23 @@ static void launch_os_pass(ss_engine* e, const OsArgs& a, unsigned tiles, unsign
 // fused step: stable placement of the batch's kept tuples (values only) into
 // vbuf[0].  The first pass walks the live chunks and drops never-stored
 // tuples; a second pass (G > 2^11) consumes the compacted kept set.
+static void use_ahead_set(ss_engine* e, int b) {
+    const ss_engine::AheadSet& a = e->aset[b];
+    e->gcount = a.gcount; e->gkept = a.gkept; e->gpre = a.gpre; e->gstart = a.gstart; e->n_live = a.n_live;
+    e->lc = a.lc; e->n_lc = a.n_lc; e->gsub = a.gsub; e->sub_shift = a.sub_shift; e->tpt = a.tpt;
+    e->touched = a.touched;
+    e->gcnt = e->gcnt_buf[b];
+}
+
+// sub-chunk counts and prefixes of the single-pass placement (no-ops
+// unless k_scan_small chose sub-chunks)
+static void launch_sub_prefix(ss_engine* e, const uint32_t* dk, int64_t n, int cs) {
+    ss_note_launch(), ss_launch(k_sub_hist, kSubUnitsMax, 512, e->G * 4, e->st, dk, n, cs, e->lc, e->n_lc, e->sub_shift,
+                                (uint32_t)e->G, e->subh, e->bad);
+    ss_note_launch(), ss_launch(k_sub_scan, 2 * kNumSM, 256, 0, e->st, e->gpre, e->lc, e->n_lc, e->sub_shift,
+                                (uint32_t)e->G, e->subh, e->gsub, e->bad);
+}
+
 static int launch_place_step(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_t n) {
     const uint32_t* base0 = e->dhist;
     const uint32_t* base1 = e->dhist + kMaxBins;
@@ -1374,10 +1418,7 @@ static int launch_place_step(ss_engine* e, const uint32_t* dk, const int32_t* dv
         auto kern = use_match ? k_rank_place<0> : rank_kernel(bits_for(e->G));
         const size_t rsm = rank_smem_bytes((uint32_t)e->G);
         // sub-chunk prefixes (no-ops unless k_scan_small chose sub-chunks)
-        ss_note_launch(), ss_launch(k_sub_hist, kSubUnitsMax, 512, e->G * 4, e->st, dk, n, cs, e->lc, e->n_lc, e->sub_shift,
-                                                                            (uint32_t)e->G, e->subh, e->bad);
-        ss_note_launch(), ss_launch(k_sub_scan, 2 * kNumSM, 256, 0, e->st, e->gpre, e->lc, e->n_lc, e->sub_shift,
-                                                                   (uint32_t)e->G, e->subh, e->gsub, e->bad);
+        if (!e->ahead) launch_sub_prefix(e, dk, n, cs);
         ss_note_launch(), ss_launch(kern, std::max(n_chunk, kSubUnitsMax), kRankWarps * 32, rsm, e->st, dk, dv, e->trace_on ? e->kbuf2 : nullptr, e->vbuf[0], n, cs, e->lc, e->n_lc, e->gpre, e->gstart,
             (uint32_t)e->G, e->n_live, e->bad, e->sub_shift, e->gsub);
         SS_CUDA(e, cudaGetLastError());
@@ -1521,7 +1562,7 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
     e->last_plan = plan;
     {
         ProfScope ps(e, SS_K_STATS, e->st);
-        if ((rc = launch_stats(e, n_chunk, true, work_grid))) return rc;
+        if (!e->ahead && (rc = launch_stats(e, n_chunk, true, work_grid))) return rc;
         if (e->G > 16384) {
             // hot cache for the next batch's count: > 1/(4 kHotCache) of the batch
             SS_CUDA(e, cudaMemsetAsync(e->n_hot_dev, 0, 4, e->st));
@@ -1595,7 +1636,7 @@ static int run_batch(ss_engine* e, const uint32_t* dk, const int32_t* dv, int64_
         }
         SS_CUDA(e, cudaGetLastError());
     }
-    {
+    if (!e->ahead) {
         ProfScope ps(e, SS_K_STATS, e->st);
         if ((rc = launch_scans(e, e->gkept, n_chunk))) return rc;
     }
@@ -2381,7 +2422,54 @@ extern "C" int ss_step(ss_engine* e, const uint32_t* groups, const int32_t* attr
         }
         return SS_OK;
     }
-    if (n > 0 && e->kst && !e->keys64 && !e->pre_counted) {
+    const bool ahead = n > 0 && e->ahead_ok && !has_policy && !(cfg && cfg->split) && !e->trace_on && !e->prof &&
+                       !e->pre_counted;
+    if (ahead) {
+        // count + statistics + scans + sub-chunk prefixes of this batch on
+        // the count stream into the alternate per-batch arrays, while the
+        // previous batch places and updates windows on the engine stream
+        const int b = e->kpar;
+        e->kpar ^= 1;
+        if (staged_here) {
+            SS_CUDA(e, cudaStreamWaitEvent(e->kst, e->ev_staged[e->cur_stage], 0));
+        } else if (!e->key_pipe_dev || e->inputs_on_stream) {
+            SS_CUDA(e, cudaEventRecord(e->ev_in, e->st));
+            SS_CUDA(e, cudaStreamWaitEvent(e->kst, e->ev_in, 0));
+        }
+        if (e->fin_rec[b]) SS_CUDA(e, cudaStreamWaitEvent(e->kst, e->ev_fin[b], 0));
+        use_ahead_set(e, b);
+        const int n_chunk = (int)std::max<int64_t>(1, (n + e->S - 1) / e->S);
+        int cs = 0;
+        while ((int64_t(1) << cs) < e->S) ++cs;
+        cudaStream_t const st0 = e->st;
+        e->st = e->kst;                      // the launch helpers enqueue on e->st
+        {
+            NvtxRange nv2("ss count + stats + scans (ahead)");
+            ss_note_launch(), ss_launch(k_count_rows, n_chunk, 512, e->G * 4, e->kst, dk, n, (uint32_t)e->G, e->S,
+                                        e->gcnt, e->key_bad, ((uintptr_t)dk % 16) == 0);
+            rc = launch_stats(e, n_chunk, true, false);
+            if (!rc) rc = launch_scans(e, e->gkept, n_chunk);
+            if (!rc) launch_sub_prefix(e, dk, n, cs);
+        }
+        e->st = st0;
+        if (rc) {
+            use_ahead_set(e, 0);
+            return rc;
+        }
+        SS_CUDA(e, cudaGetLastError());
+        SS_CUDA(e, cudaEventRecord(e->ev_keys[b], e->kst));
+        SS_CUDA(e, cudaStreamWaitEvent(e->st, e->ev_keys[b], 0));
+        ss_note_launch(), ss_launch(k_merge_bad, 1, 32, 0, e->st, e->bad, e->key_bad);
+        e->ahead = true;
+        e->pre_counted = true;
+        rc = run_step(e, dk, dv, n, cfg);
+        e->pre_counted = false;
+        e->ahead = false;
+        use_ahead_set(e, 0);
+        if (rc) return rc;
+        SS_CUDA(e, cudaEventRecord(e->ev_fin[b], e->st));
+        e->fin_rec[b] = true;
+    } else if (n > 0 && e->kst && !e->keys64 && !e->pre_counted) {
         // the count rows of this batch on the count stream (overlapping the
         // previous batch's tail), into the alternate rows (see ss_step_keys64)
         const int b = e->kpar;

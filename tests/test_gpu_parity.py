@@ -417,9 +417,10 @@ def test_int64_keys_pipelined_probe(ready):
     eng.close()
 
 
+@pytest.mark.parametrize("policy", ["prob", "no"])
 @pytest.mark.parametrize("G", [1000, 20_000])
 @pytest.mark.parametrize("ready", [True, False])
-def test_u32_pipelined_count(ready, G):
+def test_u32_pipelined_count(ready, G, policy):
     """The count of batch t+1 runs on its own stream while batch t finishes
     (alternating count rows; captured graphs keyed by them; large G: after
     the previous batch's hot-group cache).
@@ -433,7 +434,9 @@ def test_u32_pipelined_count(ready, G):
     bl = list(D.batches(D.stream_for(spec), B))
     eng = _engine(G, W, P=P, max_batch=B, aggregates=("count", "sum", "avg", "min", "max"))
     eng.set_key_pipeline(ready)
-    bal = StreamEngine.balancer_struct("prob", max(1, B // (10 * P)), 0.5)
+    # policy 'no' with G <= 2^14: statistics, scans and sub-chunk prefixes
+    # run ahead on the count stream as well (alternating per-batch arrays)
+    bal = StreamEngine.balancer_struct(policy, max(1, B // (10 * P)), 0.5)
     dev = [(torch.as_tensor(b.groups.astype(np.int32)).cuda(), torch.as_tensor(b.attrs.astype(np.int32)).cuda())
            for b in bl]
     torch.cuda.synchronize()
