@@ -1120,7 +1120,7 @@ k_sub_scan(const int32_t* __restrict__ gpre, const int32_t* __restrict__ lc, con
 }
 
 __host__ __device__ constexpr size_t rank_smem_bytes(uint32_t G) {
-    return (size_t)kRankWarps * kRankStages * kRankSub * 8 + (size_t)G * 4;
+    return (size_t)kRankWarps * kRankStages * kRankSub * 8 + (size_t)((G + 31) & ~31u) * 4 + 128;
 }
 
 
@@ -1199,6 +1199,7 @@ k_rank_place(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin, 
     __syncthreads();                             // cursors initialised
     const unsigned lt = lanemask_lt();
     const uint32_t cur_sa = (uint32_t)__cvta_generic_to_shared(cur);
+    const uint32_t dummy_sa = cur_sa + ((G + 31u) & ~31u) * 4u;     // [32], 128-B aligned
     // one sub-tile; FULL: all kRankSub tuples present (every sub-tile but
     // the batch's last), so no validity tests
     auto sub_tile = [&](auto full_c, int s, int q, int tn) {
@@ -1230,18 +1231,34 @@ k_rank_place(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin, 
             const bool valid = FULL || key[j] != 0xffffffffu;
             lead[j] = 31u - (uint32_t)__clz(peers[j]);
             cnt[j] = (valid && lane == lead[j]) ? (uint32_t)__popc(peers[j]) : 0u;
-            addr[j] = cur_sa + (valid ? key[j] : 0u) * 4u;
+            addr[j] = cnt[j] ? cur_sa + key[j] * 4u : dummy_sa + lane * 4u;
             old[j] = 0;
             asm volatile("" :: "r"(cnt[j]), "r"(addr[j]));
         }
         // ---- in sub-tile order across the warps: advance the cursors
+        // one asm block of unpredicated atomics in round order: non-leaders
+        // add 0 to a private dummy word (bank = lane), so the warp issues 8
+        // ATOMS back to back with no branches (a per-round predicated asm +
+        // __syncwarp compiled to a divergent branch per round, ~9 dependent
+        // instructions each on this serial chain)
         if (s > 0) named_bar_sync(w, 64);
-#pragma unroll
-        for (int j = 0; j < kRankItems; ++j) {
-            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p atom.shared.add.u32 %0, [%1], %2;\n\t}"
-                         : "+r"(old[j]) : "r"(addr[j]), "r"(cnt[j]) : "memory");
-            __syncwarp();
-        }
+        static_assert(kRankItems == 8, "the ordered section below is written for 8 rounds");
+        asm volatile("{\n\t"
+                     "atom.shared.add.u32 %0, [%8], %16;\n\t"
+                     "atom.shared.add.u32 %1, [%9], %17;\n\t"
+                     "atom.shared.add.u32 %2, [%10], %18;\n\t"
+                     "atom.shared.add.u32 %3, [%11], %19;\n\t"
+                     "atom.shared.add.u32 %4, [%12], %20;\n\t"
+                     "atom.shared.add.u32 %5, [%13], %21;\n\t"
+                     "atom.shared.add.u32 %6, [%14], %22;\n\t"
+                     "atom.shared.add.u32 %7, [%15], %23;\n\t}"
+                     : "+r"(old[0]), "+r"(old[1]), "+r"(old[2]), "+r"(old[3]),
+                       "+r"(old[4]), "+r"(old[5]), "+r"(old[6]), "+r"(old[7])
+                     : "r"(addr[0]), "r"(addr[1]), "r"(addr[2]), "r"(addr[3]),
+                       "r"(addr[4]), "r"(addr[5]), "r"(addr[6]), "r"(addr[7]),
+                       "r"(cnt[0]), "r"(cnt[1]), "r"(cnt[2]), "r"(cnt[3]),
+                       "r"(cnt[4]), "r"(cnt[5]), "r"(cnt[6]), "r"(cnt[7])
+                     : "memory");
         if (s + 1 < nsub) named_bar_arrive((w + 1) % kRankWarps, 64);
         // ---- scatter (never-stored runs have bit 31 set in their cursor)
 #pragma unroll
