@@ -243,6 +243,20 @@ __device__ __forceinline__ void os_load_tile(void* dk, const void* sk, void* dv,
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
                  :: "r"((unsigned)__cvta_generic_to_shared(dv)), "l"(sv), "r"(bytes), "r"(b), "l"(pol) : "memory");
 }
+// one more bulk copy on the same mbarrier transaction (caller adds its
+// bytes to the expected count first)
+__device__ __forceinline__ void os_load_extra(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 :: "r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src), "r"(bytes),
+                    "r"((unsigned)__cvta_generic_to_shared(bar)) : "memory");
+}
+__device__ __forceinline__ void os_expect(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;"
+                 :: "r"((unsigned)__cvta_generic_to_shared(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void l2_prefetch(const void* src, unsigned bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void os_wait(uint64_t* bar, unsigned parity) {
     const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
     asm volatile(
@@ -459,10 +473,22 @@ k_os_pass2(OsArgs a) { SS_PDL_ENTRY();
     for (int64_t tile = blockIdx.x; tile * kOsTile < n; tile += gridDim.x) {
         const int64_t t0 = tile * kOsTile;
         const int tn = (int)min64(kOsTile, n - t0);
-        if (aligned && tn == kOsTile) {
+        const bool bulk = aligned && tn == kOsTile;
+        if (bulk) {
             if (threadIdx.x == 0) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                // the tile's digit bases (hist row, 4 B x BINS) ride on the
+                // same transaction into gb; the expect_tx precedes the
+                // arrive in os_load_tile so the phase cannot complete early
+                os_expect(&bar[0], BINS * 4);
+                os_load_extra(gb, a.hist + tile * BINS, BINS * 4, &bar[0]);
                 os_load_tile(sk, a.kin + t0, sv, a.vin + t0, kOsTile * 4, &bar[0]);
+                // the CTA's next tile into L2 while this one is ranked
+                const int64_t t1 = t0 + (int64_t)gridDim.x * kOsTile;
+                if (t1 + kOsTile <= n) {
+                    l2_prefetch(a.kin + t1, kOsTile * 4);
+                    l2_prefetch(a.vin + t1, kOsTile * 4);
+                }
             }
             uint16_t* my = wh + w * BINS;
             for (int i = lane; i < BINS / 8; i += 32) reinterpret_cast<uint4*>(my)[i] = make_uint4(0u, 0u, 0u, 0u);
@@ -473,10 +499,11 @@ k_os_pass2(OsArgs a) { SS_PDL_ENTRY();
                 sk[i] = a.kin[t0 + i];
                 sv[i] = a.vin[t0 + i];
             }
+            for (int i = threadIdx.x; i < BINS; i += blockDim.x) gb[i] = a.hist[tile * BINS + i];
             uint16_t* my = wh + w * BINS;
             for (int i = lane; i < BINS / 8; i += 32) reinterpret_cast<uint4*>(my)[i] = make_uint4(0u, 0u, 0u, 0u);
         }
-        __syncthreads();                     // tile and zeroed histograms visible
+        __syncthreads();                     // tile, digit bases and zeroed histograms visible
         uint16_t* my = wh + w * BINS;
         uint32_t key[kOs2Items];
         int32_t val[kOs2Items];
@@ -536,7 +563,7 @@ k_os_pass2(OsArgs a) { SS_PDL_ENTRY();
                 const int d = (int)threadIdx.x * DPT + q;
                 if (d < BINS) {
                     lst[d] = ex;
-                    gb[d] = a.hist[tile * BINS + d] - ex;
+                    gb[d] -= ex;             // gb holds the tile's hist row
                 }
                 ex += c[q];
             }
@@ -555,6 +582,8 @@ k_os_pass2(OsArgs a) { SS_PDL_ENTRY();
         }
         __syncthreads();
         const int total = (int)s_total;
+        // 4 independent LDS -> LDS -> STG chains per thread in flight
+#pragma unroll 4
         for (int i = threadIdx.x; i < total; i += blockDim.x) {
             const uint32_t k = sk[i];
             const uint32_t pos = gb[(k >> a.shift) & a.mask] + (uint32_t)i;
