@@ -523,7 +523,7 @@ def main():
     # measured DRAM traffic per launch of that kernel class (ncu --set full of
     # this config, committed under profiles/), else null
     traffic, traffic_src = None, None
-    for tf in ("r2_traffic.json", "r1_traffic.json"):
+    for tf in ("r2f_traffic.json", "r2_traffic.json", "r1_traffic.json"):
         try:
             with open(os.path.join(ROOT, "profiles", tf)) as fh:
                 tj = json.load(fh)

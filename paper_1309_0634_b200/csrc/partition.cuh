@@ -204,6 +204,32 @@ __device__ __forceinline__ void stats_account(uint32_t g, int32_t c, const int32
 // groups; chunk_live is a bitmap (bit c of word c / 32).
 constexpr int kMaxChunkWords = 4096 / 32;
 
+// the CTA's touched-group and byte totals: one global atomic each per CTA
+// (per warp, 2368 CTAs x 8 warps queued ~19K atomics on each of the two
+// words at 1M groups); every thread of the CTA calls it
+__device__ __forceinline__ void stats_flush(uint32_t my_touched, unsigned long long my_bytes,
+                                            unsigned long long* touched, unsigned long long* alg_bytes) {
+    __shared__ unsigned long long sh_t[32], sh_b[32];
+    my_touched = warp_sum(my_touched);
+    my_bytes = warp_sum(my_bytes);
+    if (lane_id() == 0) {
+        sh_t[warp_id()] = my_touched;
+        sh_b[warp_id()] = my_bytes;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t = 0, b = 0;
+        for (int q = 0; q < (int)(blockDim.x >> 5); ++q) {
+            t += sh_t[q];
+            b += sh_b[q];
+        }
+        if (t) {
+            atomicAdd(touched, t);
+            atomicAdd(alg_bytes, b);
+        }
+    }
+}
+
 __global__ void __launch_bounds__(1024)
 k_batch_stats(int32_t* __restrict__ gcnt, int n_chunk, uint32_t G, const int32_t* __restrict__ pmap,
               int P, int32_t* __restrict__ gcount, int32_t* __restrict__ gkept, uint32_t* __restrict__ chunk_live,
@@ -262,13 +288,7 @@ k_batch_stats(int32_t* __restrict__ gcnt, int n_chunk, uint32_t G, const int32_t
     }
     lbits = __reduce_or_sync(SS_FULL, lbits);
     if (chunk_live && lane == 0 && lbits) atomicOr(&sh_live[0], lbits);
-    my_touched = warp_sum(my_touched);
-    my_bytes = warp_sum(my_bytes);
-    if (lane == 0 && my_touched) {
-        atomicAdd(touched, (unsigned long long)my_touched);
-        atomicAdd(alg_bytes, my_bytes);
-    }
-    __syncthreads();
+    stats_flush(my_touched, my_bytes, touched, alg_bytes);   // (ends with a CTA barrier)
     for (int p = threadIdx.x; p < P; p += blockDim.x) {
         if (sh_tpt[p]) atomicAdd(&tpt[p], (unsigned long long)sh_tpt[p]);
         if (pwork && sh_tpt[P + p]) atomicAdd(&pwork[p], sh_tpt[P + p]);
@@ -374,13 +394,7 @@ k_batch_stats_cols(int32_t* __restrict__ gcnt, int n_chunk, uint32_t G, const in
         }
         __syncthreads();                         // sh_part / sh_dead reused
     }
-    my_touched = warp_sum(my_touched);
-    my_bytes = warp_sum(my_bytes);
-    if (lane == 0 && my_touched) {
-        atomicAdd(touched, (unsigned long long)my_touched);
-        atomicAdd(alg_bytes, my_bytes);
-    }
-    __syncthreads();
+    stats_flush(my_touched, my_bytes, touched, alg_bytes);   // (ends with a CTA barrier)
     for (int p = threadIdx.x; p < P; p += blockDim.x) {
         if (sh_tpt[p]) atomicAdd(&tpt[p], (unsigned long long)sh_tpt[p]);
         if (pwork && sh_tpt[P + p]) atomicAdd(&pwork[p], sh_tpt[P + p]);

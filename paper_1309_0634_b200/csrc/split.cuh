@@ -62,8 +62,17 @@ k_split_sum(const int32_t* __restrict__ gcount, uint32_t G, int64_t W, unsigned 
     unsigned long long s = 0;
     for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < G; g += gridDim.x * blockDim.x)
         s += (unsigned long long)min64(gcount[g], W);
+    // one atomic per CTA (one per warp serialised ~31K same-address
+    // atomics at 1M groups)
+    __shared__ unsigned long long sh[8];
     s = warp_sum(s);
-    if (lane_id() == 0 && s) atomicAdd(n_stored, s);
+    if (lane_id() == 0) sh[warp_id()] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t = 0;
+        for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += sh[q];
+        if (t) atomicAdd(n_stored, t);
+    }
 }
 
 // Phase 1: hot detection + cold loads.  grid-stride over G; cold loads

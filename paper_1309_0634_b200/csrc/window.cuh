@@ -589,8 +589,11 @@ k_finalize(FinalizeArgs a) { SS_PDL_ENTRY();
 }
 
 __device__ __forceinline__ void finalize_body(const FinalizeArgs& a) {
-    const unsigned lane = lane_id();
+    const unsigned lane = lane_id(), wp = warp_id();
     const int W = (int)a.W;
+    // result rows: one atomic per CTA round on the row counter (one per warp
+    // serialised 31K same-address atomics at 1M groups)
+    __shared__ unsigned s_wcnt[8], s_base;
     for (uint32_t g0 = blockIdx.x * blockDim.x; g0 < a.G; g0 += gridDim.x * blockDim.x) {
         const uint32_t g = g0 + threadIdx.x;
         const int K = (g < a.G) ? a.gcount[g] : 0;
@@ -598,10 +601,18 @@ __device__ __forceinline__ void finalize_body(const FinalizeArgs& a) {
         unsigned slot = 0;
         if (a.emit) {
             const unsigned bal = __ballot_sync(SS_FULL, t);
-            unsigned base = 0;
-            if (lane == 0 && bal) base = atomicAdd(a.n_res, (unsigned)__popc(bal));
-            base = __shfl_sync(SS_FULL, base, 0);
-            slot = base + __popc(bal & lanemask_lt());
+            if (lane == 0) s_wcnt[wp] = (unsigned)__popc(bal);
+            __syncthreads();
+            unsigned pre = 0, all = 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const unsigned c = s_wcnt[q];
+                pre += (q < (int)wp) ? c : 0u;
+                all += c;
+            }
+            if (threadIdx.x == 0) s_base = all ? atomicAdd(a.n_res, all) : 0u;
+            __syncthreads();
+            slot = s_base + pre + __popc(bal & lanemask_lt());
         }
         if (!t) continue;
         const int f0 = a.fill[g];
