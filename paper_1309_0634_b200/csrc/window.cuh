@@ -203,50 +203,75 @@ k_ingest(IngestArgs a) { SS_PDL_ENTRY();
         const int m = min(kMemberChunk, my_items - c0);
         // phase A: stage the items thread-strided (item i on thread i mod
         // 512), so a partition with few members costs one dependent load
-        // chain per thread, not kMPT of them on a few threads
+        // chain per thread, not kMPT of them on a few threads.  Two load
+        // levels for all kMPT items together: the groups, then every field
+        // of each group (loaded whether or not the member stores anything --
+        // the fields of a hash block's 8 ids share a sector), instead of a
+        // 4-deep chain per item behind its branches.
+        int q_g[kMPT], q_sh[kMPT];
 #pragma unroll
         for (int q = 0; q < kMPT; ++q) {
             const int i = q * kIngestThreads + threadIdx.x;
+            q_g[q] = -1;
+            q_sh[q] = -1;
             if (i >= m) continue;
             const int it = ibase + (shared_items ? c0 + i : (c0 + i) * kCtaPerPart + sub);
-            int g, r_lo, r_hi;            // this item's slice [r_lo, r_hi) of the sub-batch run
-            int32_t tag;
             if (it < n_mem) {
-                g = a.order[lo + it];
+                q_g[q] = a.order[lo + it];
+            } else {
+                q_sh[q] = s_lo + (it - n_mem);
+                q_g[q] = a.split_g[a.share_grp[q_sh[q]]];
+            }
+        }
+        // then per item: every field of its group at once (loaded whether or
+        // not the member stores anything -- the fields of a hash block's 8
+        // ids share a sector), not behind the item's branches
+#pragma unroll
+        for (int q = 0; q < kMPT; ++q) {
+            const int i = q * kIngestThreads + threadIdx.x;
+            const int g = q_g[q];
+            if (g < 0) continue;
+            const bool is_split = a.split_of && a.split_of[g] >= 0;
+            const int kt0 = a.gcnt[g];
+            const int K = a.gcount[g];                     // batch count
+            const int f0 = a.fill[g];
+            const int np = a.next_pos[g];
+            const int gs = a.gstart[g];
+            const int64_t offg = a.off[g];
+            int r_lo, r_hi;               // this item's slice [r_lo, r_hi) of the sub-batch run
+            int32_t tag;
+            if (q_sh[q] < 0) {
                 tag = g;
                 r_lo = 0;
-                r_hi = (a.split_of && a.split_of[g] >= 0) ? 0 : a.gcnt[g];
+                r_hi = is_split ? 0 : kt0;
             } else {
-                const int sh = s_lo + (it - n_mem);
+                const int sh = q_sh[q];
                 const int sg = a.share_grp[sh];
-                g = a.split_g[sg];
                 tag = -1 - sg;
                 // shares tile the stored values: the last min(K, W) of the
                 // kept run (split.cuh)
-                const long long kt = a.gcnt[g], den = a.split_den[sg];
-                const long long sto = min64(a.gcount[g], a.W), off0 = kt - sto;
+                const long long kt = kt0, den = a.split_den[sg];
+                const long long sto = min64(K, a.W), off0 = kt - sto;
                 r_lo = (int)(off0 + sto * a.share_lo[sh] / den);
                 r_hi = (int)(off0 + sto * a.share_hi[sh] / den);
             }
             int w = 0;
             if (r_hi > r_lo) {
-                const int K = a.gcount[g];                 // batch count
-                const int b = K - a.gcnt[g];               // batch rank of run index 0
+                const int b = K - kt0;                     // batch rank of run index 0
                 const int first = max(r_lo, K - W - b);    // first stored run index
                 if (first < r_hi) {
-                    const int f0 = a.fill[g];
                     const int jb = b + first;              // batch rank of the first stored value
                     w = r_hi - first;
-                    m_start[i] = a.gstart[g] + first;
+                    m_start[i] = gs + first;
                     // 32-bit unsigned remainders (f0, next_pos < W <= 2^30
                     // and jb < 2^31 - 2^30 keep the sums in range; a 64-bit
                     // % is a ~70-instruction sequence)
                     const uint32_t uw = (uint32_t)W;
                     const uint32_t q0 = (uint32_t)f0 + (uint32_t)jb;
                     m_q0[i] = (int)(q0 % uw);
-                    m_s0[i] = (int)(((uint32_t)a.next_pos[g] + q0) % uw);
+                    m_s0[i] = (int)(((uint32_t)np + q0) % uw);
                     m_f0[i] = (K >= W) ? 0 : f0;           // k >= W: nothing old survives
-                    m_off[i] = a.off[g];
+                    m_off[i] = offg;
                     m_dlo[i] = 0;
                     m_dhi[i] = 0;
                     m_min[i] = 0x7fffffff;
