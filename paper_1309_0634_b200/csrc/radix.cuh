@@ -507,7 +507,10 @@ k_os_pass2(OsArgs a) { SS_PDL_ENTRY();
         uint16_t* my = wh + w * BINS;
         uint32_t key[kOs2Items];
         int32_t val[kOs2Items];
-        uint16_t rk[kOs2Items];
+        // ranks packed two per register (16 separate u16 ranks spilled)
+        uint32_t rkp[kOs2Items / 2];
+#pragma unroll
+        for (int r = 0; r < kOs2Items / 2; ++r) rkp[r] = 0u;
         uint32_t ok = 0;
         const unsigned lt = lanemask_lt();
 #pragma unroll
@@ -525,7 +528,8 @@ k_os_pass2(OsArgs a) { SS_PDL_ENTRY();
             __syncwarp();
             if (valid) {
                 ok |= 1u << r;
-                rk[r] = (uint16_t)(before + __popc(peers & lt));
+                const uint32_t rank = (uint32_t)(uint16_t)(before + __popc(peers & lt));
+                rkp[r >> 1] |= (r & 1) ? (rank << 16) : rank;
                 if (lane == 31u - __clz(peers)) my[d] = (uint16_t)(before + __popc(peers));
             }
             __syncwarp();
@@ -575,7 +579,7 @@ k_os_pass2(OsArgs a) { SS_PDL_ENTRY();
         for (int r = 0; r < kOs2Items; ++r) {
             if ((ok >> r) & 1u) {
                 const uint32_t d = (key[r] >> a.shift) & a.mask;
-                const uint32_t p = lst[d] + my[d] + rk[r];
+                const uint32_t p = lst[d] + my[d] + ((r & 1) ? (rkp[r >> 1] >> 16) : (rkp[r >> 1] & 0xffffu));
                 sk[p] = key[r];
                 sv[p] = val[r];
             }
