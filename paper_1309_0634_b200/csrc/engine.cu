@@ -1297,7 +1297,7 @@ static int launch_place_all(ss_engine* e, const uint32_t* dk, const int32_t* dv,
 
 template <int BITS>
 static void launch_os_pass_t(ss_engine* e, const OsArgs& a, unsigned tiles, unsigned blks) {
-    ss_note_launch(), ss_launch(k_os_up<BITS>, tiles, kOsThreads, 0, e->st, a);
+    ss_note_launch(), ss_launch(k_os_up<BITS>, (tiles + kOsUpTiles - 1) / kOsUpTiles, kOsThreads, 0, e->st, a);
     ss_note_launch(), ss_launch(k_os_red<BITS>, blks, 1024, 0, e->st, a);
     ss_note_launch(), ss_launch(k_os_top<BITS>, (1 << BITS) / 32, 1024, 0, e->st, a);
     ss_note_launch(), ss_launch(k_os_down<BITS>, blks, 1024, 0, e->st, a);

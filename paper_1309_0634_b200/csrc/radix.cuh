@@ -41,7 +41,7 @@ constexpr int kOsTile = 8192;
 constexpr int kOsThreads = 1024;
 constexpr int kOsItems = kOsTile / kOsThreads;          // 8 per thread
 constexpr int kOsWarps = kOsThreads / 32;
-constexpr int kOsBlkTiles = 16;                         // tiles per block of the column scan (C4: 128 blocks)
+constexpr int kOsBlkTiles = 8;                          // tiles per block of the column scan (C4: 256 blocks: 16-tile blocks left k_os_red / k_os_down on 128 CTAs, under one wave)
 constexpr int kOsMaxPass = 4;
 
 template <int BITS>
@@ -83,40 +83,60 @@ __device__ __forceinline__ bool os_live(const OsArgs& a, bool drop, int64_t i, u
     return !drop || a.live[(i >> a.chunk_shift) * (int64_t)a.G + g] > 0;
 }
 
+// kOsUpTiles tiles per CTA: every load of the CTA's tiles is issued before
+// the histograms are zeroed, so their latency overlaps the zeroing barrier
+// (one tile per CTA left the load pipe idle through zero / barrier / flush)
+constexpr int kOsUpTiles = 2;
+
 template <int BITS>
 __global__ void __launch_bounds__(kOsThreads)
 k_os_up(OsArgs a) { SS_PDL_ENTRY();
     constexpr int BINS = 1 << BITS;
     constexpr int NH = BINS <= 128 ? kOsWarps : 4;      // sub-histograms (one per warp for narrow digits)
-    __shared__ uint32_t wh[NH][BINS];
+    constexpr int TPC = kOsUpTiles;
+    __shared__ uint32_t wh[TPC][NH][BINS];
     if (*a.bad != (unsigned long long)kNoBad) return;
     const int64_t n = os_count(a);
-    const int64_t t0 = (int64_t)blockIdx.x * kOsTile;
-    if (t0 >= n) return;
-    const int tn = (int)min64(kOsTile, n - t0);
+    const int64_t tile0 = (int64_t)blockIdx.x * TPC;
+    if (tile0 * kOsTile >= n) return;
     const bool drop = a.live && *a.any_dead;
     const unsigned h = warp_id() % NH;
-    for (int i = threadIdx.x; i < NH * BINS; i += blockDim.x) (&wh[0][0])[i] = 0;
-    __syncthreads();
-    // 8 consecutive tuples per thread: two 128-bit loads
+    // 8 consecutive tuples per thread and tile: two 128-bit loads each
     const int i0 = threadIdx.x * kOsItems;
-    uint32_t k[kOsItems];
-    if (i0 + kOsItems <= tn && ((uintptr_t)(a.kin + t0) % 16) == 0) {
-        const uint4 x = ld_stream_v4(a.kin + t0 + i0), y = ld_stream_v4(a.kin + t0 + i0 + 4);
-        k[0] = x.x; k[1] = x.y; k[2] = x.z; k[3] = x.w; k[4] = y.x; k[5] = y.y; k[6] = y.z; k[7] = y.w;
-    } else {
+    uint32_t k[TPC][kOsItems];
+    int tn[TPC];
 #pragma unroll
-        for (int q = 0; q < kOsItems; ++q) k[q] = (i0 + q < tn) ? a.kin[t0 + i0 + q] : 0u;
+    for (int t = 0; t < TPC; ++t) {
+        const int64_t t0 = (tile0 + t) * kOsTile;
+        tn[t] = t0 < n ? (int)min64(kOsTile, n - t0) : 0;
+        if (i0 + kOsItems <= tn[t] && ((uintptr_t)(a.kin + t0) % 16) == 0) {
+            const uint4 x = ld_stream_v4(a.kin + t0 + i0), y = ld_stream_v4(a.kin + t0 + i0 + 4);
+            k[t][0] = x.x; k[t][1] = x.y; k[t][2] = x.z; k[t][3] = x.w;
+            k[t][4] = y.x; k[t][5] = y.y; k[t][6] = y.z; k[t][7] = y.w;
+        } else {
+#pragma unroll
+            for (int q = 0; q < kOsItems; ++q) k[t][q] = (i0 + q < tn[t]) ? a.kin[t0 + i0 + q] : 0u;
+        }
     }
-#pragma unroll
-    for (int q = 0; q < kOsItems; ++q)
-        if (i0 + q < tn && os_live(a, drop, t0 + i0 + q, k[q])) atomicAdd(&wh[h][(k[q] >> a.shift) & a.mask], 1u);
+    for (int i = threadIdx.x; i < TPC * NH * BINS; i += blockDim.x) (&wh[0][0][0])[i] = 0;
     __syncthreads();
-    for (int d = threadIdx.x; d < BINS; d += blockDim.x) {
-        uint32_t s = 0;
+#pragma unroll
+    for (int t = 0; t < TPC; ++t) {
+        const int64_t t0 = (tile0 + t) * kOsTile;
+#pragma unroll
+        for (int q = 0; q < kOsItems; ++q)
+            if (i0 + q < tn[t] && os_live(a, drop, t0 + i0 + q, k[t][q])) atomicAdd(&wh[t][h][(k[t][q] >> a.shift) & a.mask], 1u);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < TPC; ++t) {
+        if (tn[t] == 0) continue;
+        for (int d = threadIdx.x; d < BINS; d += blockDim.x) {
+            uint32_t s = 0;
 #pragma unroll 4
-        for (int q = 0; q < NH; ++q) s += wh[q][d];
-        a.hist[(int64_t)blockIdx.x * BINS + d] = s;
+            for (int q = 0; q < NH; ++q) s += wh[t][q][d];
+            a.hist[(tile0 + t) * BINS + d] = s;
+        }
     }
 }
 

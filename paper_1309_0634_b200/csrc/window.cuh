@@ -330,6 +330,19 @@ k_ingest(IngestArgs a) { SS_PDL_ENTRY();
             }
             return UnitRef{mi, (u - m_uscan[mi]) * kUnit};
         };
+        // a warp's next unit is at or after its current member: gallop from
+        // there (a hot member's next unit costs one shared load, a tail
+        // member a few) instead of the full 11-step search
+        auto next_unit = [&](int u, int mi) -> UnitRef {
+            int step = 1;
+            while (mi + step < m && m_uscan[mi + step] <= u) {
+                mi += step;
+                step <<= 1;
+            }
+            for (step >>= 1; step >= 1; step >>= 1)
+                if (mi + step < m && m_uscan[mi + step] <= u) mi += step;
+            return UnitRef{mi, (u - m_uscan[mi]) * kUnit};
+        };
         const int ustride = cstride * nw;
         int u = csub * nw + warp_id();
         UnitRef cur = u < u_total ? find_unit(u) : UnitRef{0, 0};
@@ -358,7 +371,7 @@ k_ingest(IngestArgs a) { SS_PDL_ENTRY();
                 if (sl >= W) sl -= W;
                 old[k] = (r < w && qq < f0) ? rg[sl] : 0;
             }
-            if (u + ustride < u_total) cur = find_unit(u + ustride);
+            if (u + ustride < u_total) cur = next_unit(u + ustride, mi);
             long long d = 0;
             int32_t mnv = 0x7fffffff, mxv = (int32_t)0x80000000;
 #pragma unroll
