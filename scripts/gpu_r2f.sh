@@ -12,6 +12,7 @@ bench)
   nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/smi.txt
   nproc > $O/nproc.txt
   timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1
+  timeout 900 python -m pytest tests -q -m gpu > $O/gpu_tests.log 2>&1
   timeout 900 python bench.py --steps 10 --warmup 3 > $O/bench_c4.log 2>&1
   for c in c1 c2 c3 c4u c5; do
     timeout 400 python bench.py --config $c --steps 10 --warmup 3 --no-cpu > $O/bench_$c.log 2>&1
