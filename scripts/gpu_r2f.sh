@@ -30,6 +30,9 @@ ncu)
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_count_rows|k_rank_place|k_ingest|k_batch_stats|k_finalize|k_sub' -s 120 -c 6 -o $O/full_c1 $B --config c1 > $O/ncu_c1.log 2>&1
   ;;
 extra)
+  for c in c1 c2 c3 c4 c5; do
+    timeout 300 python scripts/partition_times.py $c 12 > $O/parttimes_$c.log 2>&1
+  done
   timeout 1200 compute-sanitizer --tool memcheck --print-limit 20 python scripts/sanitize_cases.py > $O/memcheck.log 2>&1
   timeout 1200 compute-sanitizer --tool racecheck --racecheck-report hazard --print-limit 20 python scripts/sanitize_cases.py > $O/racecheck.log 2>&1
   timeout 1500 python scripts/compare_policies.py --config c4 --steps 6 --warmup 12 > $O/compare_c4.log 2>&1
